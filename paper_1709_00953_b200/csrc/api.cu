@@ -1,0 +1,1082 @@
+// api.cu -- the C ABI of libblockct_cuda.so (include/blockct.h).
+//
+// Owns the device store, the state vectors and the per-epoch plan staging.
+// Every entry point validates its arguments on the host before touching the
+// device, so an invalid plan leaves the state untouched (executor.py:158-169:
+// "a failed batch leaves no trace").
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cuda_runtime.h>
+#include <string>
+#include <vector>
+
+#include "../../include/blockct.h"
+#include "internal.h"
+
+namespace bct {
+cudaError_t pb_trace_counts(int64_t, int64_t, int64_t, const double *, const double *, int64_t,
+                            int64_t, int32_t *, cudaStream_t);
+cudaError_t pb_compact(const int32_t *, int64_t, int32_t *, int32_t *, void *, size_t, int32_t *,
+                       int32_t *, int64_t *, cudaStream_t);
+size_t scan_temp_bytes(int64_t);
+size_t sort_temp_bytes(int64_t);
+cudaError_t exclusive_scan_i32(const int32_t *, int32_t *, int64_t, void *, size_t, cudaStream_t);
+cudaError_t pb_fill(int64_t, int64_t, int64_t, const double *, const double *, int64_t, int64_t,
+                    const int32_t *, const int32_t *, int64_t, double *, int32_t *, cudaStream_t);
+cudaError_t pb_rbp(const int32_t *, int64_t, const int64_t *, int, int32_t *, cudaStream_t);
+cudaError_t build_csc(int, const double *, const int32_t *, const int32_t *, const int32_t *,
+                      const int32_t *, int, int32_t, int32_t, int64_t, void *, int32_t *,
+                      int32_t *, int32_t *, int32_t *, int32_t *, int32_t *, void *, size_t,
+                      cudaStream_t);
+cudaError_t convert_values(int, const double *, void *, int64_t, cudaStream_t);
+cudaError_t inv_count(const int32_t *, int32_t, int32_t *, cudaStream_t);
+cudaError_t inv_fill(const int32_t *, int32_t, int64_t, const int32_t *, int32_t *, int32_t *,
+                     cudaStream_t);
+cudaError_t fill_z(int, const void *, const int32_t *, const int32_t *, const PanelDev *, int,
+                   int64_t, const double *, double *, cudaStream_t);
+cudaError_t forward(int, const void *, const int32_t *, const int32_t *, const PanelDev *, int,
+                    const int32_t *, const int32_t *, int64_t, const double *, double *,
+                    cudaStream_t);
+cudaError_t zsum(const int32_t *, const int32_t *, int64_t, const double *, double *,
+                 cudaStream_t);
+cudaError_t sub(const double *, const double *, int64_t, double *, cudaStream_t);
+cudaError_t audit(const double *, const double *, const double *, int64_t, unsigned long long *,
+                  cudaStream_t);
+cudaError_t commit(const PanelDev *, int, int32_t *, double *, double *, cudaStream_t);
+cudaError_t sharded_finish(const double *, const double *, int64_t, const int32_t *,
+                           const uint64_t *, double *, double *, int, cudaStream_t);
+}  // namespace bct
+
+namespace {
+
+constexpr int RING = 4;
+
+struct Slot {
+    cudaEvent_t done = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    EpochOut *h_out = nullptr;      // pinned
+    double *h_mus = nullptr;        // pinned [task_cap]
+    int32_t *h_status = nullptr;    // pinned [task_cap]
+    int64_t n_tasks = 0, n_visits = 0;
+    bool pending = false;
+    bool timed = false;
+};
+
+}  // namespace
+
+struct bct_ctx {
+    std::string err;
+    int device = 0, dtype = 0, m = 0, n_panels = 0, pb = 0, pe = 0, np = 0;
+    int64_t n_meas = 0, n_vox = 0, nnz = 0, z_len = 0, x_len = 0, max_rows = 0, max_cols = 0;
+    cudaStream_t stream = nullptr;
+    // host mirrors
+    std::vector<PanelDev> h_panels;
+    std::vector<int64_t> col_ptr, col_vox, rb_ptr, rb_rows;
+    std::vector<double> table_values, table_totals;
+    std::vector<int32_t> h_rbp;
+    // device store
+    void *vals = nullptr, *tvals = nullptr;
+    int32_t *cols = nullptr, *indptr = nullptr, *trows = nullptr, *cptr = nullptr;
+    int32_t *rbp = nullptr, *l2g = nullptr;
+    PanelDev *d_panels = nullptr;
+    int32_t *inv_ptr = nullptr, *inv_z = nullptr, *d_rb_ptr = nullptr, *d_rb_rows = nullptr;
+    int32_t *rb_of_row = nullptr;
+    // device state
+    double *y = nullptr, *r = nullptr, *z = nullptr, *x = nullptr, *xhat = nullptr;
+    double *x_true = nullptr;
+    int32_t *counts = nullptr;
+    // scratch
+    double *gx = nullptr, *t_ax = nullptr, *part = nullptr, *mus = nullptr, *exchange = nullptr;
+    double *vec = nullptr;            // n_meas scratch
+    int32_t *statuses = nullptr;
+    EpochOut *out = nullptr;
+    unsigned int *bar = nullptr, *ticket = nullptr;
+    unsigned long long *audit2 = nullptr;
+    EpochHeader *d_hdr = nullptr;
+    TaskDev *d_tasks = nullptr;
+    int64_t task_cap = 0;
+    // staging
+    EpochHeader *h_hdr = nullptr;
+    TaskDev *h_tasks = nullptr;
+    cudaEvent_t staged = nullptr;
+    Slot slots[RING];
+    int head = 0, tail = 0;           // ring: tail = oldest pending
+    int grid = 0, block = 0;
+    bool has_x_true = false;
+    uint64_t last_epoch_mask[BCT_MASKW] = {0, 0, 0, 0};
+    std::vector<void *> allocs;
+};
+
+static std::string g_create_err;
+
+namespace {
+
+int fail(bct_ctx *c, int code, const char *fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf; else g_create_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                         \
+    do {                                                                                 \
+        cudaError_t _e = (call);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            return fail(c, BCT_ECUDA, "%s failed: %s", #call, cudaGetErrorString(_e)); \
+    } while (0)
+
+template <typename T>
+int dalloc(bct_ctx *c, T **p, int64_t n)
+{
+    size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc((void **)p, bytes);
+    if (e != cudaSuccess)
+        return fail(c, BCT_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+    c->allocs.push_back(*p);
+    return 0;
+}
+
+#define DALLOC(p, n)                          \
+    do {                                      \
+        int _r = dalloc(c, &(p), (int64_t)(n)); \
+        if (_r) return _r;                    \
+    } while (0)
+
+int vsize(const bct_ctx *c) { return c->dtype == BCT_F64 ? 8 : 4; }
+
+int set_mask(uint64_t *mask, int i) { mask[i >> 6] |= 1ull << (i & 63); return 0; }
+
+// Common tail of context creation: state buffers, row-block tables, inverse map.
+int finalize(bct_ctx *c)
+{
+    // row blocks
+    std::vector<int32_t> rbp32(c->rb_ptr.begin(), c->rb_ptr.end());
+    std::vector<int32_t> rows32(c->rb_rows.begin(), c->rb_rows.end());
+    std::vector<int32_t> of_row(c->n_meas, -1);
+    for (int i = 0; i < c->m; ++i)
+        for (int64_t q = c->rb_ptr[i]; q < c->rb_ptr[i + 1]; ++q) of_row[c->rb_rows[q]] = i;
+    DALLOC(c->d_rb_ptr, c->m + 1);
+    DALLOC(c->d_rb_rows, rows32.size());
+    DALLOC(c->rb_of_row, c->n_meas);
+    CK(cudaMemcpy(c->d_rb_ptr, rbp32.data(), 4 * rbp32.size(), cudaMemcpyHostToDevice));
+    if (!rows32.empty())
+        CK(cudaMemcpy(c->d_rb_rows, rows32.data(), 4 * rows32.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->rb_of_row, of_row.data(), 4 * of_row.size(), cudaMemcpyHostToDevice));
+
+    // panel table
+    DALLOC(c->d_panels, c->np);
+    CK(cudaMemcpy(c->d_panels, c->h_panels.data(), sizeof(PanelDev) * c->np,
+                  cudaMemcpyHostToDevice));
+
+    // inverse row map over owned panels, panel-ascending
+    DALLOC(c->inv_ptr, c->n_meas + 1);
+    DALLOC(c->inv_z, c->z_len);
+    int32_t *cnt = nullptr, *fill = nullptr;
+    DALLOC(cnt, c->n_meas + 1);
+    DALLOC(fill, c->n_meas);
+    CK(cudaMemsetAsync(cnt, 0, 4 * (c->n_meas + 1), c->stream));
+    CK(cudaMemsetAsync(fill, 0, 4 * c->n_meas, c->stream));
+    for (int lp = 0; lp < c->np; ++lp) {
+        const PanelDev &P = c->h_panels[lp];
+        CK(bct::inv_count(c->l2g + P.row_off, P.n_rows, cnt, c->stream));
+    }
+    size_t sb = bct::scan_temp_bytes(c->n_meas + 1);
+    char *cub = nullptr;
+    DALLOC(cub, (int64_t)sb);
+    CK(bct::exclusive_scan_i32(cnt, c->inv_ptr, c->n_meas + 1, cub, sb, c->stream));
+    for (int lp = 0; lp < c->np; ++lp) {
+        const PanelDev &P = c->h_panels[lp];
+        CK(bct::inv_fill(c->l2g + P.row_off, P.n_rows, P.row_off, c->inv_ptr, fill, c->inv_z,
+                         c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+
+    // state and scratch
+    DALLOC(c->y, c->n_meas);
+    DALLOC(c->r, c->n_meas);
+    DALLOC(c->vec, c->n_meas + 2);
+    DALLOC(c->exchange, c->n_meas + 2);
+    DALLOC(c->z, c->z_len);
+    DALLOC(c->x, c->x_len);
+    DALLOC(c->xhat, c->x_len);
+    DALLOC(c->x_true, c->x_len);
+    DALLOC(c->counts, c->np);
+    DALLOC(c->gx, 4 * c->max_cols);
+    DALLOC(c->t_ax, 2 * c->max_rows);
+    c->grid = bct::epoch_grid_size(c->dtype, c->device, &c->block);
+    DALLOC(c->part, 8 * (int64_t)c->grid + 8);
+    DALLOC(c->out, 1);
+    DALLOC(c->bar, 1);
+    DALLOC(c->ticket, 1);
+    DALLOC(c->audit2, 2);
+    DALLOC(c->d_hdr, 1);
+    CK(cudaMemsetAsync(c->y, 0, 8 * c->n_meas, c->stream));
+    CK(cudaMemsetAsync(c->r, 0, 8 * c->n_meas, c->stream));
+    CK(cudaMemsetAsync(c->z, 0, 8 * std::max<int64_t>(c->z_len, 1), c->stream));
+    CK(cudaMemsetAsync(c->x, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
+    CK(cudaMemsetAsync(c->xhat, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
+    CK(cudaMemsetAsync(c->counts, 0, 4 * std::max(c->np, 1), c->stream));
+    CK(cudaMemsetAsync(c->bar, 0, 4, c->stream));
+    CK(cudaMemsetAsync(c->ticket, 0, 4, c->stream));
+    CK(cudaHostAlloc((void **)&c->h_hdr, sizeof(EpochHeader), cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming));
+    for (int s = 0; s < RING; ++s) {
+        CK(cudaEventCreateWithFlags(&c->slots[s].done, cudaEventDisableTiming));
+        CK(cudaEventCreate(&c->slots[s].t0));
+        CK(cudaEventCreate(&c->slots[s].t1));
+        CK(cudaHostAlloc((void **)&c->slots[s].h_out, sizeof(EpochOut), cudaHostAllocDefault));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int ensure_task_cap(bct_ctx *c, int64_t n)
+{
+    if (n <= c->task_cap) return 0;
+    int64_t cap = std::max<int64_t>(n, 2 * c->task_cap);
+    // drain pending epochs before reallocating buffers they use
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->d_tasks) cudaFree(c->d_tasks);
+    if (c->mus) cudaFree(c->mus);
+    if (c->statuses) cudaFree(c->statuses);
+    if (c->h_tasks) cudaFreeHost(c->h_tasks);
+    CK(cudaMalloc((void **)&c->d_tasks, sizeof(TaskDev) * cap));
+    CK(cudaMalloc((void **)&c->mus, 8 * cap));
+    CK(cudaMalloc((void **)&c->statuses, 4 * cap));
+    CK(cudaHostAlloc((void **)&c->h_tasks, sizeof(TaskDev) * cap, cudaHostAllocDefault));
+    for (int s = 0; s < RING; ++s) {
+        if (c->slots[s].h_mus) cudaFreeHost(c->slots[s].h_mus);
+        if (c->slots[s].h_status) cudaFreeHost(c->slots[s].h_status);
+        CK(cudaHostAlloc((void **)&c->slots[s].h_mus, 8 * cap, cudaHostAllocDefault));
+        CK(cudaHostAlloc((void **)&c->slots[s].h_status, 4 * cap, cudaHostAllocDefault));
+    }
+    c->task_cap = cap;
+    return 0;
+}
+
+int check_common_desc(bct_ctx *c, int m, int n_panels, int pb, int pe, int dtype)
+{
+    if (m < 1 || m > BCT_MAX_M) return fail(c, BCT_EINVAL, "m=%d outside [1, %d]", m, BCT_MAX_M);
+    if (n_panels < 1) return fail(c, BCT_EINVAL, "n_panels must be >= 1");
+    if (pb < 0 || pe > n_panels || pb >= pe)
+        return fail(c, BCT_EINVAL, "owned panel range [%d, %d) invalid", pb, pe);
+    if (dtype != BCT_F64 && dtype != BCT_F32) return fail(c, BCT_EINVAL, "dtype %d", dtype);
+    return 0;
+}
+
+// Allocates the store once panel sizes are known.
+int alloc_store(bct_ctx *c, const std::vector<int64_t> &rows, const std::vector<int64_t> &nnzs,
+                const std::vector<int64_t> &ncols)
+{
+    c->h_panels.resize(c->np);
+    int64_t vo = 0, ro = 0, xo = 0, co = 0;
+    for (int lp = 0; lp < c->np; ++lp) {
+        if (nnzs[lp] >= (1ll << 31) || rows[lp] >= (1ll << 31))
+            return fail(c, BCT_EINVAL, "panel %d too large for 32-bit local indices", c->pb + lp);
+        PanelDev &P = c->h_panels[lp];
+        P.val_off = vo;
+        P.row_off = ro;
+        P.x_off = xo;
+        P.cptr_off = co;
+        P.n_rows = (int32_t)rows[lp];
+        P.n_cols = (int32_t)ncols[lp];
+        P.nnz = (int32_t)nnzs[lp];
+        P.j = c->pb + lp;
+        vo += nnzs[lp];
+        ro += rows[lp];
+        xo += ncols[lp];
+        co += ncols[lp] * (c->m + 1);
+        c->max_rows = std::max(c->max_rows, rows[lp]);
+        c->max_cols = std::max(c->max_cols, ncols[lp]);
+    }
+    if (ro >= (1ll << 31)) return fail(c, BCT_EINVAL, "z store exceeds 2^31 rows");
+    c->nnz = vo;
+    c->z_len = ro;
+    c->x_len = xo;
+    size_t vs = vsize(c);
+    {
+        void *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, std::max<size_t>(vs * vo, 8));
+        if (e != cudaSuccess) return fail(c, BCT_ENOMEM, "store values: %s", cudaGetErrorString(e));
+        c->allocs.push_back(p);
+        c->vals = p;
+        e = cudaMalloc(&p, std::max<size_t>(vs * vo, 8));
+        if (e != cudaSuccess) return fail(c, BCT_ENOMEM, "store values: %s", cudaGetErrorString(e));
+        c->allocs.push_back(p);
+        c->tvals = p;
+    }
+    DALLOC(c->cols, vo);
+    DALLOC(c->trows, vo);
+    DALLOC(c->indptr, ro + c->np);
+    DALLOC(c->l2g, ro);
+    DALLOC(c->cptr, co);
+    DALLOC(c->rbp, (int64_t)c->np * (c->m + 1));
+    return 0;
+}
+
+struct BuildTmp {
+    double *vals64 = nullptr;
+    int32_t *a = nullptr, *b = nullptr, *cc = nullptr, *d = nullptr;
+    char *cub = nullptr;
+    size_t cub_bytes = 0;
+};
+
+int alloc_build_tmp(bct_ctx *c, BuildTmp &t, int64_t max_nnz, int64_t scan_n)
+{
+    DALLOC(t.vals64, max_nnz);
+    DALLOC(t.a, max_nnz);
+    DALLOC(t.b, max_nnz);
+    DALLOC(t.cc, max_nnz);
+    DALLOC(t.d, max_nnz);
+    t.cub_bytes = std::max(bct::sort_temp_bytes(max_nnz), bct::scan_temp_bytes(scan_n));
+    DALLOC(t.cub, (int64_t)t.cub_bytes);
+    return 0;
+}
+
+void free_tmp(bct_ctx *c, void *p)
+{
+    if (!p) return;
+    cudaFree(p);
+    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+}
+
+// CSC + storage conversion of panel lp whose forward CSR (f64) sits in tmp.vals64.
+int finish_panel(bct_ctx *c, int lp, BuildTmp &t)
+{
+    const PanelDev &P = c->h_panels[lp];
+    size_t vs = vsize(c);
+    char *tv = (char *)c->tvals + vs * P.val_off;
+    CK(bct::build_csc(c->dtype, t.vals64, c->cols + P.val_off, c->indptr + P.row_off + lp,
+                      c->l2g + P.row_off, c->rbp + (int64_t)lp * (c->m + 1), c->m, P.n_rows,
+                      P.n_cols, P.nnz, tv, c->trows + P.val_off, c->cptr + P.cptr_off, t.a, t.b,
+                      t.cc, t.d, t.cub, t.cub_bytes, c->stream));
+    CK(bct::convert_values(c->dtype, t.vals64, (char *)c->vals + vs * P.val_off, P.nnz,
+                           c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+void destroy(bct_ctx *c)
+{
+    if (!c) return;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (void *p : c->allocs) cudaFree(p);
+    if (c->d_tasks) cudaFree(c->d_tasks);
+    if (c->mus) cudaFree(c->mus);
+    if (c->statuses) cudaFree(c->statuses);
+    if (c->h_tasks) cudaFreeHost(c->h_tasks);
+    if (c->h_hdr) cudaFreeHost(c->h_hdr);
+    for (int s = 0; s < RING; ++s) {
+        Slot &S = c->slots[s];
+        if (S.done) cudaEventDestroy(S.done);
+        if (S.t0) cudaEventDestroy(S.t0);
+        if (S.t1) cudaEventDestroy(S.t1);
+        if (S.h_out) cudaFreeHost(S.h_out);
+        if (S.h_mus) cudaFreeHost(S.h_mus);
+        if (S.h_status) cudaFreeHost(S.h_status);
+    }
+    if (c->staged) cudaEventDestroy(c->staged);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int init_ctx(bct_ctx *c, int device)
+{
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    int coop = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+    if (!coop) return fail(c, BCT_ECUDA, "device %d lacks cooperative launch", device);
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *bct_last_error(const bct_ctx *ctx)
+{
+    return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+int bct_version(void) { return 1; }
+
+int bct_create(const bct_system_desc *d, const bct_panel *panels, bct_ctx **out)
+{
+    if (!d || !panels || !out) return fail(nullptr, BCT_EINVAL, "null argument");
+    *out = nullptr;
+    int r = check_common_desc(nullptr, d->m, d->n_panels, d->panel_begin, d->panel_end, d->dtype);
+    if (r) return r;
+    bct_ctx *c = new bct_ctx();
+    auto bail = [&](int code) {
+        g_create_err = c->err;
+        destroy(c);
+        return code;
+    };
+    if ((r = init_ctx(c, d->device))) return bail(r);
+    c->dtype = d->dtype;
+    c->m = d->m;
+    c->n_panels = d->n_panels;
+    c->pb = d->panel_begin;
+    c->pe = d->panel_end;
+    c->np = c->pe - c->pb;
+    c->n_meas = d->n_meas;
+    c->n_vox = d->n_vox;
+    if (c->n_meas >= (1ll << 31) || c->n_meas < 1 || c->n_vox < 1)
+        return bail(fail(c, BCT_EINVAL, "bad sizes n_meas=%lld n_vox=%lld",
+                         (long long)c->n_meas, (long long)c->n_vox));
+    c->rb_ptr.assign(d->row_block_ptr, d->row_block_ptr + c->m + 1);
+    c->rb_rows.assign(d->row_block_rows, d->row_block_rows + c->rb_ptr[c->m]);
+    c->col_ptr.assign(d->col_block_ptr, d->col_block_ptr + c->n_panels + 1);
+    c->col_vox.assign(d->col_block_vox, d->col_block_vox + c->col_ptr[c->n_panels]);
+    c->table_values.assign(d->table_values, d->table_values + (int64_t)c->m * c->n_panels);
+    c->table_totals.assign(d->table_totals, d->table_totals + c->n_panels);
+    for (int64_t g : c->rb_rows)
+        if (g < 0 || g >= c->n_meas) return bail(fail(c, BCT_EINVAL, "row block id out of range"));
+    for (int64_t v : c->col_vox)
+        if (v < 0 || v >= c->n_vox) return bail(fail(c, BCT_EINVAL, "voxel id out of range"));
+
+    std::vector<int64_t> rows(c->np), nnzs(c->np), ncols(c->np);
+    int64_t max_nnz = 1;
+    for (int lp = 0; lp < c->np; ++lp) {
+        const bct_panel &p = panels[lp];
+        int j = c->pb + lp;
+        rows[lp] = p.n_rows;
+        nnzs[lp] = p.nnz;
+        ncols[lp] = c->col_ptr[j + 1] - c->col_ptr[j];
+        if (p.n_rows < 0 || p.nnz < 0 || p.indptr[p.n_rows] != p.nnz || p.rbp[c->m] != p.n_rows ||
+            p.rbp[0] != 0)
+            return bail(fail(c, BCT_EINVAL, "panel %d: inconsistent indptr/rbp", j));
+        for (int64_t q = 0; q < p.nnz; ++q)
+            if (p.cols[q] < 0 || p.cols[q] >= ncols[lp])
+                return bail(fail(c, BCT_EINVAL, "panel %d: column id out of range", j));
+        for (int64_t q = 0; q < p.n_rows; ++q)
+            if (p.l2g[q] < 0 || p.l2g[q] >= c->n_meas)
+                return bail(fail(c, BCT_EINVAL, "panel %d: l2g out of range", j));
+        max_nnz = std::max(max_nnz, p.nnz);
+    }
+    if ((r = alloc_store(c, rows, nnzs, ncols))) return bail(r);
+    BuildTmp t;
+    if ((r = alloc_build_tmp(c, t, max_nnz, 1))) return bail(r);
+    for (int lp = 0; lp < c->np; ++lp) {
+        const bct_panel &p = panels[lp];
+        const PanelDev &P = c->h_panels[lp];
+        std::vector<int32_t> ip(p.indptr, p.indptr + p.n_rows + 1);
+        std::vector<int32_t> rb(p.rbp, p.rbp + c->m + 1);
+        std::vector<int32_t> lg(p.l2g, p.l2g + p.n_rows);
+        c->h_rbp.insert(c->h_rbp.end(), rb.begin(), rb.end());
+        if (cudaMemcpy(t.vals64, p.data, 8 * p.nnz, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(c->cols + P.val_off, p.cols, 4 * p.nnz, cudaMemcpyHostToDevice) !=
+                cudaSuccess ||
+            cudaMemcpy(c->indptr + P.row_off + lp, ip.data(), 4 * ip.size(),
+                       cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(c->rbp + (int64_t)lp * (c->m + 1), rb.data(), 4 * rb.size(),
+                       cudaMemcpyHostToDevice) != cudaSuccess ||
+            (p.n_rows > 0 && cudaMemcpy(c->l2g + P.row_off, lg.data(), 4 * lg.size(),
+                                        cudaMemcpyHostToDevice) != cudaSuccess))
+            return bail(fail(c, BCT_ECUDA, "panel upload failed"));
+        if ((r = finish_panel(c, lp, t))) return bail(r);
+    }
+    free_tmp(c, t.vals64); free_tmp(c, t.a); free_tmp(c, t.b); free_tmp(c, t.cc);
+    free_tmp(c, t.d); free_tmp(c, t.cub);
+    if ((r = finalize(c))) return bail(r);
+    *out = c;
+    return 0;
+}
+
+int bct_create_parallel_beam(const bct_pb_desc *d, bct_ctx **out)
+{
+    if (!d || !out || !d->cos_views || !d->sin_views)
+        return fail(nullptr, BCT_EINVAL, "null argument");
+    *out = nullptr;
+    int r = check_common_desc(nullptr, d->m, d->nc, d->panel_begin, d->panel_end, d->dtype);
+    if (r) return r;
+    if (d->n < 1 || d->views < d->m || d->bins < 1 || d->nc > d->n)
+        return fail(nullptr, BCT_EINVAL, "bad parallel-beam sizes");
+    bct_ctx *c = new bct_ctx();
+    auto bail = [&](int code) {
+        g_create_err = c->err;
+        destroy(c);
+        return code;
+    };
+    if ((r = init_ctx(c, d->device))) return bail(r);
+    const int64_t n = d->n, views = d->views, bins = d->bins;
+    c->dtype = d->dtype;
+    c->m = d->m;
+    c->n_panels = d->nc;
+    c->pb = d->panel_begin;
+    c->pe = d->panel_end;
+    c->np = c->pe - c->pb;
+    c->n_meas = views * bins;
+    c->n_vox = n * n;
+    if (c->n_meas >= (1ll << 31)) return bail(fail(c, BCT_EINVAL, "too many measurements"));
+    // partition
+    std::vector<int64_t> aedge(c->m + 1), xedge(c->n_panels + 1);
+    {
+        // numpy: round(linspace(0, views, m+1)); linspace computes i*step
+        double step = (double)views / c->m;
+        for (int i = 0; i <= c->m; ++i) {
+            double v = (i == c->m) ? (double)views : i * step;
+            aedge[i] = (int64_t)std::nearbyint(v);
+        }
+    }
+    int64_t base = (n + c->n_panels - 1) / c->n_panels;
+    for (int j = 0; j < c->n_panels; ++j) xedge[j] = std::min<int64_t>(j * base, n);
+    xedge[c->n_panels] = n;
+    for (int j = 0; j < c->n_panels; ++j)
+        if (xedge[j] >= xedge[j + 1]) return bail(fail(c, BCT_EINVAL, "empty strip %d", j));
+    c->rb_ptr.resize(c->m + 1);
+    for (int i = 0; i <= c->m; ++i) c->rb_ptr[i] = aedge[i] * bins;
+    c->rb_rows.resize(c->n_meas);
+    for (int64_t g = 0; g < c->n_meas; ++g) c->rb_rows[g] = g;
+    c->col_ptr.resize(c->n_panels + 1);
+    for (int j = 0; j <= c->n_panels; ++j) c->col_ptr[j] = xedge[j] * n;
+    c->col_vox.resize(c->n_vox);
+    for (int64_t v = 0; v < c->n_vox; ++v) c->col_vox[v] = v;
+
+    double *d_cos = nullptr, *d_sin = nullptr;
+    int64_t *d_edges = nullptr;
+    int32_t *d_counts = nullptr, *d_flags = nullptr, *d_pos = nullptr;
+    DALLOC(d_cos, views);
+    DALLOC(d_sin, views);
+    DALLOC(d_edges, c->m + 1);
+    DALLOC(d_counts, c->n_meas);
+    DALLOC(d_flags, c->n_meas);
+    DALLOC(d_pos, c->n_meas + 1);
+    CK(cudaMemcpy(d_cos, d->cos_views, 8 * views, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_sin, d->sin_views, 8 * views, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_edges, c->rb_ptr.data(), 8 * (c->m + 1), cudaMemcpyHostToDevice));
+    size_t sb = bct::scan_temp_bytes(c->n_meas + 1);
+    char *cub = nullptr;
+    DALLOC(cub, (int64_t)sb);
+
+    // pass 1: every panel (the density table needs all of them), per-ray counts
+    std::vector<int32_t> h_counts(c->n_meas);
+    c->table_values.assign((int64_t)c->m * c->n_panels, 0.0);
+    std::vector<int64_t> rows(c->np), nnzs(c->np), ncols(c->np);
+    std::vector<int32_t *> p_l2g(c->np, nullptr), p_ip(c->np, nullptr);
+    int64_t max_nnz = 1;
+    for (int j = 0; j < c->n_panels; ++j) {
+        CK(bct::pb_trace_counts(n, views, bins, d_cos, d_sin, xedge[j], xedge[j + 1], d_counts,
+                                c->stream));
+        CK(cudaMemcpyAsync(h_counts.data(), d_counts, 4 * c->n_meas, cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        int64_t vox_j = (xedge[j + 1] - xedge[j]) * n;
+        int64_t tot = 0;
+        for (int i = 0; i < c->m; ++i) {
+            int64_t s = 0;
+            for (int64_t g = c->rb_ptr[i]; g < c->rb_ptr[i + 1]; ++g) s += h_counts[g];
+            tot += s;
+            c->table_values[(int64_t)i * c->n_panels + j] =
+                (double)s / ((double)(c->rb_ptr[i + 1] - c->rb_ptr[i]) * (double)vox_j);
+        }
+        if (j < c->pb || j >= c->pe) continue;
+        int lp = j - c->pb;
+        int64_t n_hit = 0;
+        int32_t *rowlen = nullptr;
+        DALLOC(p_l2g[lp], c->n_meas);
+        DALLOC(rowlen, c->n_meas + 1);
+        CK(bct::pb_compact(d_counts, c->n_meas, d_flags, d_pos, cub, sb, p_l2g[lp], rowlen, &n_hit,
+                           c->stream));
+        DALLOC(p_ip[lp], n_hit + 1);
+        CK(cudaMemsetAsync(rowlen + n_hit, 0, 4, c->stream));
+        CK(bct::exclusive_scan_i32(rowlen, p_ip[lp], n_hit + 1, cub, sb, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        free_tmp(c, rowlen);
+        rows[lp] = n_hit;
+        nnzs[lp] = tot;
+        ncols[lp] = vox_j;
+        max_nnz = std::max(max_nnz, tot);
+    }
+    c->table_totals.assign(c->n_panels, 0.0);
+    // totals = values.sum(axis=0): numpy reduces axis 0 row by row
+    for (int i = 0; i < c->m; ++i)
+        for (int j = 0; j < c->n_panels; ++j)
+            c->table_totals[j] += c->table_values[(int64_t)i * c->n_panels + j];
+    if ((r = alloc_store(c, rows, nnzs, ncols))) return bail(r);
+    BuildTmp t;
+    if ((r = alloc_build_tmp(c, t, max_nnz, 1))) return bail(r);
+    c->h_rbp.resize((size_t)c->np * (c->m + 1));
+    for (int lp = 0; lp < c->np; ++lp) {
+        const PanelDev &P = c->h_panels[lp];
+        int j = c->pb + lp;
+        CK(cudaMemcpyAsync(c->l2g + P.row_off, p_l2g[lp], 4 * P.n_rows, cudaMemcpyDeviceToDevice,
+                           c->stream));
+        CK(cudaMemcpyAsync(c->indptr + P.row_off + lp, p_ip[lp], 4 * (P.n_rows + 1),
+                           cudaMemcpyDeviceToDevice, c->stream));
+        CK(bct::pb_fill(n, views, bins, d_cos, d_sin, xedge[j], xedge[j + 1], p_l2g[lp], p_ip[lp],
+                        P.n_rows, t.vals64, c->cols + P.val_off, c->stream));
+        CK(bct::pb_rbp(p_l2g[lp], P.n_rows, d_edges, c->m, c->rbp + (int64_t)lp * (c->m + 1),
+                       c->stream));
+        CK(cudaMemcpyAsync(c->h_rbp.data() + (size_t)lp * (c->m + 1),
+                           c->rbp + (int64_t)lp * (c->m + 1), 4 * (c->m + 1),
+                           cudaMemcpyDeviceToHost, c->stream));
+        if ((r = finish_panel(c, lp, t))) return bail(r);
+        free_tmp(c, p_l2g[lp]);
+        free_tmp(c, p_ip[lp]);
+    }
+    free_tmp(c, t.vals64); free_tmp(c, t.a); free_tmp(c, t.b); free_tmp(c, t.cc);
+    free_tmp(c, t.d); free_tmp(c, t.cub);
+    free_tmp(c, d_counts); free_tmp(c, d_flags); free_tmp(c, d_pos); free_tmp(c, cub);
+    if ((r = finalize(c))) return bail(r);
+    *out = c;
+    return 0;
+}
+
+int bct_destroy(bct_ctx *c)
+{
+    destroy(c);
+    return 0;
+}
+
+int bct_info(const bct_ctx *c, int64_t *o)
+{
+    if (!c || !o) return BCT_EINVAL;
+    o[0] = c->n_meas; o[1] = c->n_vox; o[2] = c->m; o[3] = c->n_panels;
+    o[4] = c->pb; o[5] = c->pe; o[6] = c->nnz; o[7] = c->z_len;
+    return 0;
+}
+
+int bct_panel_info(const bct_ctx *c, int32_t j, int64_t *n_rows, int64_t *nnz, int64_t *n_cols)
+{
+    if (!c) return BCT_EINVAL;
+    if (j < c->pb || j >= c->pe) return BCT_EINVAL;
+    const PanelDev &P = c->h_panels[j - c->pb];
+    if (n_rows) *n_rows = P.n_rows;
+    if (nnz) *nnz = P.nnz;
+    if (n_cols) *n_cols = P.n_cols;
+    return 0;
+}
+
+int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *indptr,
+                  int64_t *rbp, int64_t *l2g)
+{
+    if (!c) return BCT_EINVAL;
+    if (j < c->pb || j >= c->pe) return fail(c, BCT_EINVAL, "panel %d not owned", j);
+    int lp = j - c->pb;
+    const PanelDev &P = c->h_panels[lp];
+    CK(cudaStreamSynchronize(c->stream));
+    if (data) {
+        if (c->dtype == BCT_F64) {
+            CK(cudaMemcpy(data, (double *)c->vals + P.val_off, 8 * P.nnz, cudaMemcpyDeviceToHost));
+        } else {
+            std::vector<float> f(P.nnz);
+            CK(cudaMemcpy(f.data(), (float *)c->vals + P.val_off, 4 * P.nnz,
+                          cudaMemcpyDeviceToHost));
+            for (int64_t q = 0; q < P.nnz; ++q) data[q] = f[q];
+        }
+    }
+    if (cols) CK(cudaMemcpy(cols, c->cols + P.val_off, 4 * P.nnz, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> tmp(std::max<int64_t>(P.n_rows + 1, c->m + 1));
+    if (indptr) {
+        CK(cudaMemcpy(tmp.data(), c->indptr + P.row_off + lp, 4 * (P.n_rows + 1),
+                      cudaMemcpyDeviceToHost));
+        for (int64_t q = 0; q <= P.n_rows; ++q) indptr[q] = tmp[q];
+    }
+    if (rbp)
+        for (int i = 0; i <= c->m; ++i) rbp[i] = c->h_rbp[(size_t)lp * (c->m + 1) + i];
+    if (l2g) {
+        CK(cudaMemcpy(tmp.data(), c->l2g + P.row_off, 4 * P.n_rows, cudaMemcpyDeviceToHost));
+        for (int64_t q = 0; q < P.n_rows; ++q) l2g[q] = tmp[q];
+    }
+    return 0;
+}
+
+int bct_get_table(bct_ctx *c, double *values, double *totals)
+{
+    if (!c) return BCT_EINVAL;
+    if (values) std::copy(c->table_values.begin(), c->table_values.end(), values);
+    if (totals) std::copy(c->table_totals.begin(), c->table_totals.end(), totals);
+    return 0;
+}
+
+int bct_get_stream(bct_ctx *c, void **s)
+{
+    if (!c || !s) return BCT_EINVAL;
+    *s = (void *)c->stream;
+    return 0;
+}
+
+// ---- state I/O (global order <-> panel-major) ----------------------------
+
+static int xvec_to_dev(bct_ctx *c, const double *xg, double *dst)
+{
+    std::vector<double> buf(std::max<int64_t>(c->x_len, 1));
+    for (int lp = 0; lp < c->np; ++lp) {
+        const PanelDev &P = c->h_panels[lp];
+        int j = c->pb + lp;
+        for (int64_t q = 0; q < P.n_cols; ++q) buf[P.x_off + q] = xg[c->col_vox[c->col_ptr[j] + q]];
+    }
+    CK(cudaMemcpyAsync(dst, buf.data(), 8 * c->x_len, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+static int xvec_from_dev(bct_ctx *c, const double *src, double *xg)
+{
+    std::vector<double> buf(std::max<int64_t>(c->x_len, 1));
+    CK(cudaMemcpyAsync(buf.data(), src, 8 * c->x_len, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int lp = 0; lp < c->np; ++lp) {
+        const PanelDev &P = c->h_panels[lp];
+        int j = c->pb + lp;
+        for (int64_t q = 0; q < P.n_cols; ++q) xg[c->col_vox[c->col_ptr[j] + q]] = buf[P.x_off + q];
+    }
+    return 0;
+}
+
+int bct_set_y(bct_ctx *c, const double *y)
+{
+    if (!c || !y) return BCT_EINVAL;
+    CK(cudaMemcpyAsync(c->y, y, 8 * c->n_meas, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int bct_set_x(bct_ctx *c, const double *x) { return (!c || !x) ? BCT_EINVAL : xvec_to_dev(c, x, c->x); }
+int bct_get_x(bct_ctx *c, double *x) { return (!c || !x) ? BCT_EINVAL : xvec_from_dev(c, c->x, x); }
+int bct_get_xhat(bct_ctx *c, double *x)
+{
+    return (!c || !x) ? BCT_EINVAL : xvec_from_dev(c, c->xhat, x);
+}
+
+int bct_set_x_true(bct_ctx *c, const double *xt)
+{
+    if (!c) return BCT_EINVAL;
+    if (!xt) {
+        c->has_x_true = false;
+        return 0;
+    }
+    int r = xvec_to_dev(c, xt, c->x_true);
+    if (!r) c->has_x_true = true;
+    return r;
+}
+
+int bct_set_r(bct_ctx *c, const double *r)
+{
+    if (!c || !r) return BCT_EINVAL;
+    CK(cudaMemcpyAsync(c->r, r, 8 * c->n_meas, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int bct_get_r(bct_ctx *c, double *r)
+{
+    if (!c || !r) return BCT_EINVAL;
+    CK(cudaMemcpyAsync(r, c->r, 8 * c->n_meas, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int bct_set_z(bct_ctx *c, int32_t j, const double *zj)
+{
+    if (!c || !zj) return BCT_EINVAL;
+    if (j < c->pb || j >= c->pe) return fail(c, BCT_EINVAL, "panel %d not owned", j);
+    const PanelDev &P = c->h_panels[j - c->pb];
+    CK(cudaMemcpyAsync(c->z + P.row_off, zj, 8 * P.n_rows, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int bct_get_z(bct_ctx *c, int32_t j, double *zj)
+{
+    if (!c || !zj) return BCT_EINVAL;
+    if (j < c->pb || j >= c->pe) return fail(c, BCT_EINVAL, "panel %d not owned", j);
+    const PanelDev &P = c->h_panels[j - c->pb];
+    CK(cudaMemcpyAsync(zj, c->z + P.row_off, 8 * P.n_rows, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int bct_reset_accumulators(bct_ctx *c)
+{
+    if (!c) return BCT_EINVAL;
+    CK(cudaMemsetAsync(c->xhat, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
+    CK(cudaMemsetAsync(c->counts, 0, 4 * std::max(c->np, 1), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int bct_get_counts(bct_ctx *c, int64_t *counts)
+{
+    if (!c || !counts) return BCT_EINVAL;
+    std::vector<int32_t> h(std::max(c->np, 1));
+    CK(cudaMemcpyAsync(h.data(), c->counts, 4 * c->np, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int j = 0; j < c->n_panels; ++j)
+        counts[j] = (j >= c->pb && j < c->pe) ? h[j - c->pb] : 0;
+    return 0;
+}
+
+int bct_commit_epoch(bct_ctx *c)
+{
+    if (!c) return BCT_EINVAL;
+    CK(bct::commit(c->d_panels, c->np, c->counts, c->x, c->xhat, c->stream));
+    CK(cudaMemsetAsync(c->counts, 0, 4 * std::max(c->np, 1), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int bct_fill_z_from_image(bct_ctx *c)
+{
+    if (!c) return BCT_EINVAL;
+    CK(bct::fill_z(c->dtype, c->vals, c->cols, c->indptr, c->d_panels, c->np, c->z_len, c->x, c->z,
+                   c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int bct_projection_sum(bct_ctx *c, double *out)
+{
+    if (!c || !out) return BCT_EINVAL;
+    CK(bct::zsum(c->inv_ptr, c->inv_z, c->n_meas, c->z, c->vec, c->stream));
+    CK(cudaMemcpyAsync(out, c->vec, 8 * c->n_meas, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+// r = y - sum_j z^j over every measurement (SolverState.initialize warm start)
+int bct_reset_residual(bct_ctx *c)
+{
+    if (!c) return BCT_EINVAL;
+    CK(bct::zsum(c->inv_ptr, c->inv_z, c->n_meas, c->z, c->vec, c->stream));
+    CK(bct::sub(c->y, c->vec, c->n_meas, c->r, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int bct_forward(bct_ctx *c, const double *x, double *y_out)
+{
+    if (!c || !x || !y_out) return BCT_EINVAL;
+    double *dx = nullptr;
+    CK(cudaMalloc((void **)&dx, 8 * std::max<int64_t>(c->x_len, 1)));
+    int r = xvec_to_dev(c, x, dx);
+    if (!r) {
+        cudaError_t e = bct::forward(c->dtype, c->vals, c->cols, c->indptr, c->d_panels, c->np,
+                                     c->inv_ptr, c->inv_z, c->n_meas, dx, c->vec, c->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(y_out, c->vec, 8 * c->n_meas, cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) r = fail(c, BCT_ECUDA, "forward: %s", cudaGetErrorString(e));
+    }
+    cudaFree(dx);
+    return r;
+}
+
+int bct_audit(bct_ctx *c, double *drift)
+{
+    if (!c || !drift) return BCT_EINVAL;
+    CK(bct::zsum(c->inv_ptr, c->inv_z, c->n_meas, c->z, c->vec, c->stream));
+    CK(cudaMemsetAsync(c->audit2, 0, 16, c->stream));
+    CK(bct::audit(c->y, c->r, c->vec, c->n_meas, c->audit2, c->stream));
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, c->audit2, 16, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    double d, a;
+    memcpy(&d, &h[0], 8);
+    memcpy(&a, &h[1], 8);
+    if (a == 0.0) a = 1.0;
+    *drift = d / a;
+    return 0;
+}
+
+// ---- epochs ---------------------------------------------------------------
+
+static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, int32_t flags)
+{
+    int s = c->head;
+    Slot &S = c->slots[s];
+    if (S.pending) {
+        // ring full: retire the oldest result implicitly
+        CK(cudaEventSynchronize(S.done));
+        S.pending = false;
+        c->tail = (c->tail + 1) % RING;
+    }
+    CK(cudaMemcpyAsync(c->d_hdr, c->h_hdr, sizeof(EpochHeader), cudaMemcpyHostToDevice, c->stream));
+    if (n_tasks > 0)
+        CK(cudaMemcpyAsync(c->d_tasks, c->h_tasks, sizeof(TaskDev) * n_tasks,
+                           cudaMemcpyHostToDevice, c->stream));
+    CK(cudaEventRecord(c->staged, c->stream));
+    EpochParams p;
+    memset(&p, 0, sizeof p);
+    p.vals = c->vals; p.cols = c->cols; p.indptr = c->indptr; p.tvals = c->tvals;
+    p.trows = c->trows; p.cptr = c->cptr; p.rbp = c->rbp; p.panels = c->d_panels;
+    p.n_panels_owned = c->np; p.m = c->m; p.n_meas = c->n_meas; p.z_len = c->z_len;
+    p.x_len = c->x_len; p.inv_ptr = c->inv_ptr; p.inv_z = c->inv_z; p.rb_ptr = c->d_rb_ptr;
+    p.rb_rows = c->d_rb_rows; p.rb_of_row = c->rb_of_row; p.y = c->y; p.r = c->r; p.z = c->z;
+    p.x = c->x; p.xhat = c->xhat; p.counts = c->counts;
+    p.x_true = c->has_x_true ? c->x_true : nullptr;
+    p.hdr = c->d_hdr; p.tasks = c->d_tasks; p.gx = c->gx; p.gx_stride = 2 * c->max_cols;
+    p.t_ax = c->t_ax; p.part = c->part; p.mus = c->mus; p.statuses = c->statuses; p.out = c->out;
+    p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
+    CK(cudaEventRecord(S.t0, c->stream));
+    cudaError_t e;
+    bct::launch_epoch(p, c->dtype, c->grid, c->block, c->stream, &e);
+    if (e != cudaSuccess) return fail(c, BCT_ECUDA, "epoch launch: %s", cudaGetErrorString(e));
+    CK(cudaEventRecord(S.t1, c->stream));
+    CK(cudaMemcpyAsync(S.h_out, c->out, sizeof(EpochOut), cudaMemcpyDeviceToHost, c->stream));
+    if (n_tasks > 0) {
+        CK(cudaMemcpyAsync(S.h_mus, c->mus, 8 * n_tasks, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(S.h_status, c->statuses, 4 * n_tasks, cudaMemcpyDeviceToHost,
+                           c->stream));
+    }
+    CK(cudaEventRecord(S.done, c->stream));
+    S.n_tasks = n_tasks;
+    S.n_visits = n_visits;
+    S.pending = true;
+    c->head = (c->head + 1) % RING;
+    (void)flags;
+    return 0;
+}
+
+int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task_j,
+                  const int32_t *task_visit, const int64_t *task_gptr, const int64_t *sel,
+                  const double *betas, int32_t flags)
+{
+    if (!c) return BCT_EINVAL;
+    if (mode != BCT_SERIAL_FAITHFUL && mode != BCT_PARALLEL)
+        return fail(c, BCT_EINVAL, "mode %d", mode);
+    if (n_tasks < 0 || (n_tasks > 0 && (!task_j || !task_visit || !task_gptr || !sel || !betas)))
+        return fail(c, BCT_EINVAL, "null plan arrays");
+    const bool sharded = (flags & BCT_SHARDED) != 0;
+    if (sharded && mode != BCT_PARALLEL)
+        return fail(c, BCT_EINVAL, "sharded execution requires parallel mode");
+    // validate and pack before touching the device (a failed batch leaves no trace)
+    std::vector<TaskDev> tasks;
+    tasks.reserve(n_tasks);
+    std::vector<int64_t> src_index;
+    uint64_t emask[BCT_MASKW] = {0, 0, 0, 0};
+    for (int64_t k = 0; k < n_tasks; ++k) {
+        int j = task_j[k];
+        if (j < 0 || j >= c->n_panels)
+            return fail(c, BCT_ESCHEDULE, "task %lld: volume block %d out of range",
+                        (long long)k, j);
+        if (task_gptr[k + 1] < task_gptr[k])
+            return fail(c, BCT_ESCHEDULE, "task %lld: negative group size", (long long)k);
+        TaskDev T;
+        memset(&T, 0, sizeof T);
+        for (int64_t q = task_gptr[k]; q < task_gptr[k + 1]; ++q) {
+            int64_t i = sel[q];
+            if (i < 0 || i >= c->m)
+                return fail(c, BCT_ESCHEDULE, "task %lld: measurement block %lld out of range",
+                            (long long)k, (long long)i);
+            if ((T.mask[i >> 6] >> (i & 63)) & 1ull)
+                return fail(c, BCT_ESCHEDULE, "task %lld: repeated measurement block %lld",
+                            (long long)k, (long long)i);
+            set_mask(T.mask, (int)i);
+        }
+        for (int w = 0; w < BCT_MASKW; ++w) emask[w] |= T.mask[w];
+        if (j < c->pb || j >= c->pe) {
+            if (!sharded)
+                return fail(c, BCT_ESCHEDULE, "task %lld: volume block %d not owned", (long long)k,
+                            j);
+            continue;  // another rank's column block
+        }
+        if (!std::isfinite(betas[k]))
+            return fail(c, BCT_ESCHEDULE, "task %lld: non-finite beta", (long long)k);
+        T.lp = j - c->pb;
+        T.j = j;
+        T.visit = task_visit[k];
+        T.beta = betas[k];
+        tasks.push_back(T);
+        src_index.push_back(k);
+    }
+    // visit boundaries and masks
+    int64_t n_visits = 0;
+    const int64_t nt = (int64_t)tasks.size();
+    for (int64_t a = 0; a < nt;) {
+        int64_t b = a;
+        while (b < nt && tasks[b].visit == tasks[a].visit && tasks[b].j == tasks[a].j) ++b;
+        uint64_t vm[BCT_MASKW] = {0, 0, 0, 0};
+        for (int64_t q = a; q < b; ++q)
+            for (int w = 0; w < BCT_MASKW; ++w) vm[w] |= tasks[q].mask[w];
+        for (int64_t q = a; q < b; ++q) {
+            memcpy(tasks[q].visit_mask, vm, sizeof vm);
+            tasks[q].flags = (q == a ? TASK_FIRST_OF_VISIT : 0) | (q == b - 1 ? TASK_LAST_OF_VISIT : 0);
+        }
+        ++n_visits;
+        a = b;
+    }
+    int r = ensure_task_cap(c, std::max<int64_t>(nt, 1));
+    if (r) return r;
+    // the staging buffers of the previous epoch must have been consumed
+    CK(cudaEventSynchronize(c->staged));
+    memset(c->h_hdr, 0, sizeof(EpochHeader));
+    c->h_hdr->n_tasks = (int32_t)nt;
+    c->h_hdr->mode = mode;
+    c->h_hdr->flags = flags;
+    memcpy(c->h_hdr->epoch_mask, emask, sizeof emask);
+    memcpy(c->last_epoch_mask, emask, sizeof emask);
+    if (nt) memcpy(c->h_tasks, tasks.data(), sizeof(TaskDev) * nt);
+    return launch_staged(c, nt, n_visits, flags);
+}
+
+int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *statuses)
+{
+    if (!c || !o) return BCT_EINVAL;
+    Slot &S = c->slots[c->tail];
+    if (!S.pending) return fail(c, BCT_EINVAL, "no pending epoch");
+    CK(cudaEventSynchronize(S.done));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, BCT_ECUDA, "epoch: %s", cudaGetErrorString(e));
+    o->n_tasks = S.n_tasks;
+    o->n_visits = S.n_visits;
+    o->n_degenerate = S.h_out->n_degenerate;
+    o->resid_sq = S.h_out->resid_sq;
+    o->x_sq = S.h_out->x_sq;
+    o->err_sq = S.h_out->err_sq;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, S.t0, S.t1);
+    o->kernel_ms = ms;
+    if (mus) memcpy(mus, S.h_mus, 8 * S.n_tasks);
+    if (statuses) memcpy(statuses, S.h_status, 4 * S.n_tasks);
+    S.pending = false;
+    c->tail = (c->tail + 1) % RING;
+    return 0;
+}
+
+int bct_exchange_buffer(bct_ctx *c, double **dev_ptr, int64_t *len)
+{
+    if (!c || !dev_ptr || !len) return BCT_EINVAL;
+    *dev_ptr = c->exchange;
+    *len = c->n_meas + 2;
+    return 0;
+}
+
+int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
+{
+    if (!c) return BCT_EINVAL;
+    (void)flags;
+    uint64_t *dmask = nullptr;
+    CK(cudaMalloc((void **)&dmask, sizeof(uint64_t) * BCT_MASKW));
+    CK(cudaMemcpyAsync(dmask, c->last_epoch_mask, sizeof(uint64_t) * BCT_MASKW,
+                       cudaMemcpyHostToDevice, c->stream));
+    const int nb = 296;
+    CK(bct::sharded_finish(c->y, c->exchange, c->n_meas, c->rb_of_row, dmask, c->r, c->part, nb,
+                           c->stream));
+    std::vector<double> part(nb);
+    CK(cudaMemcpyAsync(part.data(), c->part, 8 * nb, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(dmask);
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[b];
+    if (resid_sq) *resid_sq = s;
+    return 0;
+}
+
+int bct_sample_epoch(bct_ctx *c, int32_t, int32_t, const int32_t *, const double *, int64_t,
+                     const int32_t *, int32_t, double, int32_t, double, int32_t, int64_t *)
+{
+    return c ? fail(c, BCT_EINVAL, "bct_sample_epoch not implemented yet") : BCT_EINVAL;
+}
+
+}  // extern "C"

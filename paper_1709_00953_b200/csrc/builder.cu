@@ -1,0 +1,628 @@
+// builder.cu -- device construction of the blocked store (compiled with
+// -fmad=false: the tracer must round exactly like the reference).
+//
+//   pb_count_kernel / pb_fill_kernel
+//       the Siddon/Amanatides-Woo traversal of projector.py:51-198 on one
+//       (ray, strip) pair, with the same half-open boundary rule, probe
+//       offset, step order and segment arithmetic.  The reference finishes
+//       with an insertion sort by local index; local ids (ix-x0)*n + iy are
+//       distinct and the traversal is monotone in ix and, within one ix
+//       column, monotone in iy, so pb_fill_kernel writes every entry straight
+//       to its sorted slot instead (same result, O(len) instead of O(len^2)).
+//   panel CSC (per (column, row block) segment table), storage conversion,
+//   inverse row map and the bitwise forward / z-fill / projection-sum
+//   kernels used for state set-up (projector.py:220-244, 756-777).
+#include <cstdint>
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace {
+
+constexpr double REL_EPS = 1e-12;
+constexpr int MAX_STRIP = 128;   // strip height (ix extent) supported by the fill kernel
+
+struct RayTrace {
+    double length, t0, t1, t;
+    double tmax[3], tdel[3];
+    int64_t iv[3], step[3];
+    int64_t lo[3], hi[3];
+    int64_t max_steps;
+    bool hit;
+};
+
+__device__ __forceinline__ void pb_endpoints(int64_t n, int64_t bins, double c, double s,
+                                             int64_t k, double *src, double *dst)
+{
+    double u = (double)k - (double)(bins - 1) / 2.0;
+    double L = 4.0 * (double)n;
+    double cx = u * (-s), cy = u * c;
+    double lc = L * c, ls = L * s;
+    src[0] = cx - lc; src[1] = cy - ls; src[2] = 0.0;
+    dst[0] = cx + lc; dst[1] = cy + ls; dst[2] = 0.0;
+}
+
+// Set-up half of the traversal (projector.py:59-145).  Returns false on a miss.
+__device__ bool trace_init(const double *src, const double *dst, const double *origin,
+                           const int64_t *lo, const int64_t *hi, RayTrace &T, double *dv)
+{
+    dv[0] = dst[0] - src[0];
+    dv[1] = dst[1] - src[1];
+    dv[2] = dst[2] - src[2];
+    T.length = sqrt(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
+    if (T.length == 0.0) return false;
+    double scale = fabs(dv[0]);
+    if (fabs(dv[1]) > scale) scale = fabs(dv[1]);
+    if (fabs(dv[2]) > scale) scale = fabs(dv[2]);
+    double eps_d = REL_EPS * scale;
+    double t0 = 0.0, t1 = 1.0;
+    for (int a = 0; a < 3; ++a) {
+        double d = dv[a], s = src[a];
+        double blo = origin[a] + (double)lo[a] * 1.0;
+        double bhi = origin[a] + (double)hi[a] * 1.0;
+        if (fabs(d) > eps_d) {
+            double ta = (blo - s) / d, tb = (bhi - s) / d;
+            if (ta > tb) { double t = ta; ta = tb; tb = t; }
+            if (ta > t0) t0 = ta;
+            if (tb < t1) t1 = tb;
+        } else if (!(blo <= s && s < bhi)) {
+            return false;
+        }
+    }
+    if (t1 - t0 <= REL_EPS) return false;
+    double probe = t0 + 1e-9 * (t1 - t0);
+    for (int a = 0; a < 3; ++a) {
+        int64_t c = (int64_t)floor((src[a] + probe * dv[a] - origin[a]) / 1.0);
+        if (c < lo[a]) c = lo[a];
+        if (c > hi[a] - 1) c = hi[a] - 1;
+        T.iv[a] = c;
+        T.lo[a] = lo[a];
+        T.hi[a] = hi[a];
+    }
+    for (int a = 0; a < 3; ++a) {
+        T.step[a] = 0;
+        T.tmax[a] = INFINITY;
+        T.tdel[a] = INFINITY;
+        if (fabs(dv[a]) > eps_d) {
+            bool pos = dv[a] > 0.0;
+            T.step[a] = pos ? 1 : -1;
+            int64_t plane = pos ? T.iv[a] + 1 : T.iv[a];
+            T.tmax[a] = (origin[a] + (double)plane * 1.0 - src[a]) / dv[a];
+            T.tdel[a] = 1.0 / fabs(dv[a]);
+        }
+    }
+    T.t0 = t0;
+    T.t1 = t1;
+    T.t = t0;
+    T.max_steps = (hi[0] - lo[0]) + (hi[1] - lo[1]) + (hi[2] - lo[2]) + 3;
+    return true;
+}
+
+// One traversal; calls emit(ix, iy, seg) for every positive segment.
+template <typename F>
+__device__ void trace_walk(RayTrace &T, F emit)
+{
+    for (int64_t it = 0; it < T.max_steps; ++it) {
+        int a = 0;
+        double tm = T.tmax[0];
+        if (T.tmax[1] < tm) { a = 1; tm = T.tmax[1]; }
+        if (T.tmax[2] < tm) { a = 2; tm = T.tmax[2]; }
+        double tn = tm < T.t1 ? tm : T.t1;
+        double seg = (tn - T.t) * T.length;
+        if (seg > 0.0) emit(T.iv[0], T.iv[1], seg);
+        if (tm >= T.t1) break;
+        T.iv[a] += T.step[a];
+        if (T.iv[a] < T.lo[a] || T.iv[a] >= T.hi[a]) break;
+        T.tmax[a] += T.tdel[a];
+        T.t = tn;
+    }
+}
+
+__global__ void pb_count_kernel(int64_t n, int64_t views, int64_t bins, const double *cosv,
+                                const double *sinv, int64_t x0, int64_t x1, int32_t *counts)
+{
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= views * bins) return;
+    double src[3], dst[3], dv[3];
+    int64_t a = r / bins, k = r % bins;
+    pb_endpoints(n, bins, cosv[a], sinv[a], k, src, dst);
+    double origin[3] = {-0.5 * (double)n, -0.5 * (double)n, -0.5};
+    int64_t lo[3] = {x0, 0, 0}, hi[3] = {x1, n, 1};
+    RayTrace T;
+    int cnt = 0;
+    if (trace_init(src, dst, origin, lo, hi, T, dv))
+        trace_walk(T, [&](int64_t, int64_t, double) { ++cnt; });
+    counts[r] = cnt;
+}
+
+// Writes the sorted row of every hit ray: entries ordered by ix, then iy.
+__global__ void pb_fill_kernel(int64_t n, int64_t views, int64_t bins, const double *cosv,
+                               const double *sinv, int64_t x0, int64_t x1, const int32_t *l2g,
+                               const int32_t *indptr, int64_t n_hit, double *data,
+                               int32_t *cols)
+{
+    int64_t lr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (lr >= n_hit) return;
+    double src[3], dst[3], dv[3];
+    int64_t r = l2g[lr], a = r / bins, k = r % bins;
+    pb_endpoints(n, bins, cosv[a], sinv[a], k, src, dst);
+    double origin[3] = {-0.5 * (double)n, -0.5 * (double)n, -0.5};
+    int64_t lo[3] = {x0, 0, 0}, hi[3] = {x1, n, 1};
+    int colcnt[MAX_STRIP];
+    const int w = (int)(x1 - x0);
+    for (int q = 0; q < w; ++q) colcnt[q] = 0;
+    RayTrace T;
+    if (!trace_init(src, dst, origin, lo, hi, T, dv)) return;
+    RayTrace T2 = T;
+    trace_walk(T, [&](int64_t ix, int64_t, double) { ++colcnt[ix - x0]; });
+    // exclusive prefix -> first slot of every ix column
+    int acc = 0;
+    for (int q = 0; q < w; ++q) {
+        int c = colcnt[q];
+        colcnt[q] = acc;
+        acc += c;
+    }
+    const bool ydown = T2.step[1] < 0;
+    const int base = indptr[lr];
+    int64_t cur_ix = -1;
+    int run_pos = 0, run_len = 0;
+    // within an ix column the traversal is monotone in iy: place ascending
+    trace_walk(T2, [&](int64_t ix, int64_t iy, double seg) {
+        if (ix != cur_ix) {
+            cur_ix = ix;
+            run_pos = 0;
+            int q = (int)(ix - x0);
+            int next = (q + 1 < w) ? colcnt[q + 1] : acc;
+            run_len = next - colcnt[q];
+        }
+        int q = (int)(ix - x0);
+        int slot = colcnt[q] + (ydown ? (run_len - 1 - run_pos) : run_pos);
+        data[base + slot] = seg;
+        cols[base + slot] = (int32_t)((ix - x0) * n + iy);
+        ++run_pos;
+    });
+}
+
+__global__ void flag_hits_kernel(const int32_t *counts, int64_t n, int32_t *flags)
+{
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < n) flags[r] = counts[r] > 0;
+}
+
+__global__ void compact_hits_kernel(const int32_t *counts, const int32_t *pos, int64_t n,
+                                    int32_t *l2g, int32_t *rowlen)
+{
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < n && counts[r] > 0) {
+        l2g[pos[r]] = (int32_t)r;
+        rowlen[pos[r]] = counts[r];
+    }
+}
+
+__global__ void rbp_kernel(const int32_t *l2g, int64_t n_hit, const int64_t *edges, int m,
+                           int32_t *rbp)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > m) return;
+    int64_t key = edges[i];
+    int64_t lo = 0, hi = n_hit;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (l2g[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    rbp[i] = (int32_t)lo;
+}
+
+// ---- panel CSC -----------------------------------------------------------
+
+__global__ void row_of_entry_kernel(const int32_t *indptr, int32_t n_rows, int32_t *rowid)
+{
+    int lr = blockIdx.x * blockDim.x + threadIdx.x;
+    if (lr >= n_rows) return;
+    for (int p = indptr[lr]; p < indptr[lr + 1]; ++p) rowid[p] = lr;
+}
+
+__global__ void iota_kernel(int32_t *v, int64_t n)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) v[i] = (int32_t)i;
+}
+
+template <typename V>
+__global__ void csc_gather_kernel(const int32_t *perm, const double *vals, const int32_t *rowid,
+                                  const int32_t *l2g, int64_t nnz, V *tvals, int32_t *tlocal,
+                                  int32_t *trows)
+{
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= nnz) return;
+    int32_t p = perm[q];
+    int32_t lr = rowid[p];
+    tvals[q] = (V)vals[p];
+    tlocal[q] = lr;
+    trows[q] = l2g[lr];
+}
+
+// cptr[c*(m+1)+i] = first CSC entry of column c whose local row >= rbp[i].
+__global__ void cptr_kernel(const int32_t *sorted_cols, int64_t nnz, const int32_t *tlocal,
+                            const int32_t *rbp, int m, int32_t n_cols, int32_t *cptr)
+{
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n_cols * (m + 1)) return;
+    int c = (int)(t / (m + 1)), i = (int)(t % (m + 1));
+    // column range by binary search on the sorted column keys
+    int64_t lo = 0, hi = nnz;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (sorted_cols[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    int64_t cs = lo;
+    hi = nnz;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (sorted_cols[mid] < c + 1) lo = mid + 1; else hi = mid;
+    }
+    int64_t ce = lo;
+    int32_t key = rbp[i];
+    lo = cs;
+    hi = ce;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (tlocal[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    cptr[t] = (int32_t)lo;
+}
+
+template <typename V>
+__global__ void convert_kernel(const double *src, V *dst, int64_t n)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = (V)src[i];
+}
+
+// ---- inverse row map -----------------------------------------------------
+
+__global__ void inv_count_kernel(const int32_t *l2g, int32_t n_rows, int32_t *cnt)
+{
+    int lr = blockIdx.x * blockDim.x + threadIdx.x;
+    if (lr < n_rows) atomicAdd(&cnt[l2g[lr]], 1);
+}
+
+__global__ void inv_fill_kernel(const int32_t *l2g, int32_t n_rows, int64_t row_off,
+                                const int32_t *inv_ptr, int32_t *fill, int32_t *inv_z)
+{
+    int lr = blockIdx.x * blockDim.x + threadIdx.x;
+    if (lr >= n_rows) return;
+    int g = l2g[lr];  // unique within one panel
+    inv_z[inv_ptr[g] + fill[g]] = (int32_t)(row_off + lr);
+    fill[g] += 1;
+}
+
+// ---- bitwise state kernels (reference operation order, no contraction) --
+
+__device__ __forceinline__ int panel_of_off(const PanelDev *panels, int np, int64_t off)
+{
+    int lo = 0, hi = np - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) / 2;
+        if (panels[mid].row_off <= off) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <typename V>
+__device__ double row_dot(const V *vals, const int32_t *cols, const int32_t *indptr,
+                          const PanelDev &P, int lp, int64_t lr, const double *xj)
+{
+    const int32_t *ip = indptr + P.row_off + lp;
+    double acc = 0.0;
+    for (int q = ip[lr]; q < ip[lr + 1]; ++q)
+        acc = __dadd_rn(acc, __dmul_rn((double)vals[P.val_off + q], xj[cols[P.val_off + q]]));
+    return acc;
+}
+
+// z^j = A_:j x_J (projector.py:220-226 via fill_z_from_image)
+template <typename V>
+__global__ void fill_z_kernel(const V *vals, const int32_t *cols, const int32_t *indptr,
+                              const PanelDev *panels, int np, int64_t z_len, const double *x,
+                              double *z)
+{
+    int64_t off = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (off >= z_len) return;
+    int lp = panel_of_off(panels, np, off);
+    const PanelDev P = panels[lp];
+    z[off] = row_dot(vals, cols, indptr, P, lp, off - P.row_off, x + P.x_off);
+}
+
+// y = A x with per-panel row dots accumulated in ascending j (projector.py:237-244)
+template <typename V>
+__global__ void forward_kernel(const V *vals, const int32_t *cols, const int32_t *indptr,
+                               const PanelDev *panels, int np, const int32_t *inv_ptr,
+                               const int32_t *inv_z, int64_t n_meas, const double *x,
+                               double *out)
+{
+    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= n_meas) return;
+    double acc = 0.0;
+    for (int e = inv_ptr[g]; e < inv_ptr[g + 1]; ++e) {
+        int64_t off = inv_z[e];
+        int lp = panel_of_off(panels, np, off);
+        const PanelDev P = panels[lp];
+        acc = __dadd_rn(acc, row_dot(vals, cols, indptr, P, lp, off - P.row_off, x + P.x_off));
+    }
+    out[g] = acc;
+}
+
+// sum_j z^j per measurement, ascending j (projector.py:767-777)
+__global__ void zsum_kernel(const int32_t *inv_ptr, const int32_t *inv_z, int64_t n_meas,
+                            const double *z, double *out)
+{
+    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= n_meas) return;
+    double acc = 0.0;
+    for (int e = inv_ptr[g]; e < inv_ptr[g + 1]; ++e) acc = __dadd_rn(acc, z[inv_z[e]]);
+    out[g] = acc;
+}
+
+__global__ void sub_kernel(const double *y, const double *s, int64_t n, double *r)
+{
+    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g < n) r[g] = __dsub_rn(y[g], s[g]);
+}
+
+// audit: max |r - (y - S)| and max |y| (solvers.py:154-166); results as
+// ordered bit patterns of non-negative doubles.
+__global__ void audit_kernel(const double *y, const double *r, const double *s, int64_t n,
+                             unsigned long long *out2)
+{
+    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double d = 0.0, a = 0.0;
+    if (g < n) {
+        d = fabs(r[g] - (y[g] - s[g]));
+        a = fabs(y[g]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+        a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&out2[0], (unsigned long long)__double_as_longlong(d));
+        atomicMax(&out2[1], (unsigned long long)__double_as_longlong(a));
+    }
+}
+
+// _commit_epoch (solvers.py:180-185) for owned panels.
+__global__ void commit_kernel(const PanelDev *panels, int np, int32_t *counts, double *x,
+                              double *xhat)
+{
+    for (int lp = 0; lp < np; ++lp) {
+        const PanelDev P = panels[lp];
+        int cnt = counts[lp];
+        if (cnt <= 0) continue;
+        for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < P.n_cols;
+             c += (int64_t)gridDim.x * blockDim.x) {
+            x[P.x_off + c] = xhat[P.x_off + c] / (double)cnt;
+            xhat[P.x_off + c] = 0.0;
+        }
+    }
+}
+
+// Sharded tail: r = y - S for rows of drawn blocks; residual norm partials.
+__global__ void sharded_finish_kernel(const double *y, const double *S, int64_t n,
+                                      const int32_t *rb_of_row, const uint64_t *mask, double *r,
+                                      double *part)
+{
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        double d = y[g] - S[g];
+        int rb = rb_of_row[g];
+        if (rb >= 0 && ((mask[rb >> 6] >> (rb & 63)) & 1ull)) r[g] = d;
+        acc = fma(d, d, acc);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+        part[blockIdx.x] = s;
+    }
+}
+
+inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host-side entry points used by api.cu
+// ---------------------------------------------------------------------------
+namespace bct {
+
+cudaError_t pb_trace_counts(int64_t n, int64_t views, int64_t bins, const double *d_cos,
+                            const double *d_sin, int64_t x0, int64_t x1, int32_t *d_counts,
+                            cudaStream_t s)
+{
+    int64_t nm = views * bins;
+    pb_count_kernel<<<nblk(nm, 128), 128, 0, s>>>(n, views, bins, d_cos, d_sin, x0, x1,
+                                                  d_counts);
+    return cudaGetLastError();
+}
+
+// Compacts hit rays; returns n_hit through a host pointer (synchronizes).
+cudaError_t pb_compact(const int32_t *d_counts, int64_t nm, int32_t *d_tmp_flags,
+                       int32_t *d_tmp_pos, void *d_cub, size_t cub_bytes, int32_t *d_l2g,
+                       int32_t *d_rowlen, int64_t *n_hit, cudaStream_t s)
+{
+    flag_hits_kernel<<<nblk(nm, 256), 256, 0, s>>>(d_counts, nm, d_tmp_flags);
+    size_t need = cub_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(d_cub, need, d_tmp_flags, d_tmp_pos, (int)nm, s);
+    if (e != cudaSuccess) return e;
+    compact_hits_kernel<<<nblk(nm, 256), 256, 0, s>>>(d_counts, d_tmp_pos, nm, d_l2g, d_rowlen);
+    int32_t last_pos = 0, last_flag = 0;
+    cudaMemcpyAsync(&last_pos, d_tmp_pos + nm - 1, 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&last_flag, d_tmp_flags + nm - 1, 4, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    *n_hit = (int64_t)last_pos + last_flag;
+    return e;
+}
+
+size_t scan_temp_bytes(int64_t n)
+{
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (int32_t *)nullptr, (int32_t *)nullptr, (int)n);
+    return b;
+}
+
+size_t sort_temp_bytes(int64_t n)
+{
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, (int32_t *)nullptr, (int32_t *)nullptr,
+                                    (int32_t *)nullptr, (int32_t *)nullptr, (int)n);
+    return b;
+}
+
+cudaError_t exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t n, void *d_cub,
+                               size_t cub_bytes, cudaStream_t s)
+{
+    size_t need = cub_bytes;
+    return cub::DeviceScan::ExclusiveSum(d_cub, need, in, out, (int)n, s);
+}
+
+cudaError_t pb_fill(int64_t n, int64_t views, int64_t bins, const double *d_cos,
+                    const double *d_sin, int64_t x0, int64_t x1, const int32_t *d_l2g,
+                    const int32_t *d_indptr, int64_t n_hit, double *d_data, int32_t *d_cols,
+                    cudaStream_t s)
+{
+    if (x1 - x0 > MAX_STRIP) return cudaErrorInvalidValue;
+    if (n_hit == 0) return cudaSuccess;
+    pb_fill_kernel<<<nblk(n_hit, 64), 64, 0, s>>>(n, views, bins, d_cos, d_sin, x0, x1, d_l2g,
+                                                  d_indptr, n_hit, d_data, d_cols);
+    return cudaGetLastError();
+}
+
+cudaError_t pb_rbp(const int32_t *d_l2g, int64_t n_hit, const int64_t *d_edges, int m,
+                   int32_t *d_rbp, cudaStream_t s)
+{
+    rbp_kernel<<<nblk(m + 1, 128), 128, 0, s>>>(d_l2g, n_hit, d_edges, m, d_rbp);
+    return cudaGetLastError();
+}
+
+// Builds the CSC of one panel from its forward CSR (f64 values).
+cudaError_t build_csc(int dtype, const double *d_vals64, const int32_t *d_cols,
+                      const int32_t *d_indptr, const int32_t *d_l2g, const int32_t *d_rbp,
+                      int m, int32_t n_rows, int32_t n_cols, int64_t nnz, void *d_tvals,
+                      int32_t *d_trows, int32_t *d_cptr, int32_t *tmp_a, int32_t *tmp_b,
+                      int32_t *tmp_c, int32_t *tmp_d, void *d_cub, size_t cub_bytes,
+                      cudaStream_t s)
+{
+    if (nnz > 0) {
+        // tmp_a = row of entry, tmp_b = iota, tmp_c = sorted cols, tmp_d = perm
+        row_of_entry_kernel<<<nblk(n_rows, 128), 128, 0, s>>>(d_indptr, n_rows, tmp_a);
+        iota_kernel<<<nblk(nnz, 256), 256, 0, s>>>(tmp_b, nnz);
+        int bits = 1;
+        while ((1ll << bits) < (int64_t)n_cols + 1) ++bits;
+        size_t need = cub_bytes;
+        cudaError_t e = cub::DeviceRadixSort::SortPairs(d_cub, need, d_cols, tmp_c, tmp_b, tmp_d,
+                                                        (int)nnz, 0, bits, s);
+        if (e != cudaSuccess) return e;
+        // tlocal reuses tmp_b
+        if (dtype == 0)
+            csc_gather_kernel<double><<<nblk(nnz, 256), 256, 0, s>>>(
+                tmp_d, d_vals64, tmp_a, d_l2g, nnz, (double *)d_tvals, tmp_b, d_trows);
+        else
+            csc_gather_kernel<float><<<nblk(nnz, 256), 256, 0, s>>>(
+                tmp_d, d_vals64, tmp_a, d_l2g, nnz, (float *)d_tvals, tmp_b, d_trows);
+    }
+    int64_t nc = (int64_t)n_cols * (m + 1);
+    cptr_kernel<<<nblk(nc, 256), 256, 0, s>>>(tmp_c, nnz, tmp_b, d_rbp, m, n_cols, d_cptr);
+    return cudaGetLastError();
+}
+
+cudaError_t convert_values(int dtype, const double *src, void *dst, int64_t n, cudaStream_t s)
+{
+    if (n == 0) return cudaSuccess;
+    if (dtype == 0) return cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, s);
+    convert_kernel<float><<<nblk(n, 256), 256, 0, s>>>(src, (float *)dst, n);
+    return cudaGetLastError();
+}
+
+cudaError_t inv_count(const int32_t *d_l2g, int32_t n_rows, int32_t *d_cnt, cudaStream_t s)
+{
+    if (n_rows == 0) return cudaSuccess;
+    inv_count_kernel<<<nblk(n_rows, 256), 256, 0, s>>>(d_l2g, n_rows, d_cnt);
+    return cudaGetLastError();
+}
+
+cudaError_t inv_fill(const int32_t *d_l2g, int32_t n_rows, int64_t row_off,
+                     const int32_t *d_inv_ptr, int32_t *d_fill, int32_t *d_inv_z, cudaStream_t s)
+{
+    if (n_rows == 0) return cudaSuccess;
+    inv_fill_kernel<<<nblk(n_rows, 256), 256, 0, s>>>(d_l2g, n_rows, row_off, d_inv_ptr, d_fill,
+                                                      d_inv_z);
+    return cudaGetLastError();
+}
+
+cudaError_t fill_z(int dtype, const void *vals, const int32_t *cols, const int32_t *indptr,
+                   const PanelDev *panels, int np, int64_t z_len, const double *x, double *z,
+                   cudaStream_t s)
+{
+    if (z_len == 0) return cudaSuccess;
+    if (dtype == 0)
+        fill_z_kernel<double><<<nblk(z_len, 128), 128, 0, s>>>((const double *)vals, cols, indptr,
+                                                               panels, np, z_len, x, z);
+    else
+        fill_z_kernel<float><<<nblk(z_len, 128), 128, 0, s>>>((const float *)vals, cols, indptr,
+                                                              panels, np, z_len, x, z);
+    return cudaGetLastError();
+}
+
+cudaError_t forward(int dtype, const void *vals, const int32_t *cols, const int32_t *indptr,
+                    const PanelDev *panels, int np, const int32_t *inv_ptr, const int32_t *inv_z,
+                    int64_t n_meas, const double *x, double *out, cudaStream_t s)
+{
+    if (dtype == 0)
+        forward_kernel<double><<<nblk(n_meas, 128), 128, 0, s>>>(
+            (const double *)vals, cols, indptr, panels, np, inv_ptr, inv_z, n_meas, x, out);
+    else
+        forward_kernel<float><<<nblk(n_meas, 128), 128, 0, s>>>(
+            (const float *)vals, cols, indptr, panels, np, inv_ptr, inv_z, n_meas, x, out);
+    return cudaGetLastError();
+}
+
+cudaError_t zsum(const int32_t *inv_ptr, const int32_t *inv_z, int64_t n_meas, const double *z,
+                 double *out, cudaStream_t s)
+{
+    zsum_kernel<<<nblk(n_meas, 256), 256, 0, s>>>(inv_ptr, inv_z, n_meas, z, out);
+    return cudaGetLastError();
+}
+
+cudaError_t sub(const double *y, const double *sv, int64_t n, double *r, cudaStream_t s)
+{
+    sub_kernel<<<nblk(n, 256), 256, 0, s>>>(y, sv, n, r);
+    return cudaGetLastError();
+}
+
+cudaError_t audit(const double *y, const double *r, const double *sv, int64_t n,
+                  unsigned long long *out2, cudaStream_t s)
+{
+    audit_kernel<<<nblk(n, 256), 256, 0, s>>>(y, r, sv, n, out2);
+    return cudaGetLastError();
+}
+
+cudaError_t commit(const PanelDev *panels, int np, int32_t *counts, double *x, double *xhat,
+                   cudaStream_t s)
+{
+    commit_kernel<<<148, 256, 0, s>>>(panels, np, counts, x, xhat);
+    return cudaGetLastError();
+}
+
+cudaError_t sharded_finish(const double *y, const double *S, int64_t n, const int32_t *rb_of_row,
+                           const uint64_t *mask, double *r, double *part, int nb, cudaStream_t s)
+{
+    sharded_finish_kernel<<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, r, part);
+    return cudaGetLastError();
+}
+
+}  // namespace bct

@@ -1,0 +1,438 @@
+// epoch.cu -- the persistent epoch kernel and the small state kernels.
+//
+// One cooperative launch runs a whole epoch of the plan (executor.py:225-253):
+// for every task k (a basic iteration of _run_tasks, executor.py:42-102)
+//
+//   phase 1  g = (A_I^J)^T r_I       warp per voxel column over the panel CSC,
+//                                    segments of the task's row blocks only;
+//                                    writes (g, x_J) interleaved; gg partials
+//   -- grid barrier --               gg = fixed-order sum of block partials
+//   phase 2  t = A_I g, ax = A_I x_J warp per local row (dual SpMV, one pass
+//                                    over the forward CSR); denom partials
+//   -- grid barrier --               denom, mu = beta*gg/denom, status 0/1/2
+//   phase 3  xhat_J += x_J + mu g    (x_new rounded exactly like the reference)
+//            z_I    = ax + mu t      written straight into the z store
+//                                    (commit_task, projector.py:723-740)
+//            serial_faithful: refresh of the visit's drawn rows
+//            r = y - sum_j z^j in ascending j (executor.py:215-223)
+//   -- grid barrier only between serial visits --
+//
+// then an epoch tail: parallel-mode refresh over the union of drawn rows,
+// projection-sum metrics, optional _commit_epoch (solvers.py:180-185) and a
+// last-block reduction of the norms.  All reductions are fixed-order, so the
+// results are deterministic for a given grid size.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace {
+
+constexpr int BLOCK = 512;
+constexpr int WARPS = BLOCK / 32;
+constexpr int MAX_RUNS = BCT_MAX_M / 2 + 1;
+
+__device__ __forceinline__ void grid_sync(unsigned int *bar)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int nb = gridDim.x;
+        unsigned int inc = (blockIdx.x == 0) ? (0x80000000u - (nb - 1)) : 1u;
+        __threadfence();
+        unsigned int old = atomicAdd(bar, inc);
+        volatile unsigned int *vb = bar;
+        while (((old ^ *vb) & 0x80000000u) == 0) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ bool mask_has(const uint64_t *mask, int i)
+{
+    return (mask[i >> 6] >> (i & 63)) & 1ull;
+}
+
+// Sum of part[0..n) in a fixed order, identical in every block.
+__device__ double fixed_sum(const double *part, int n, double *sh)
+{
+    double v = 0.0;
+    for (int k = threadIdx.x; k < n; k += BLOCK) v += part[k];
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) s += sh[w];
+    __syncthreads();
+    return s;
+}
+
+// Per-block sum of one value held by every warp's lane 0, in warp order.
+__device__ double block_sum_lane0(double v, double *sh)
+{
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < WARPS; ++w) s += sh[w];
+    }
+    __syncthreads();
+    return s;
+}
+
+// Per-block sum of a per-thread value, fixed order.
+__device__ double block_sum_all(double v, double *sh)
+{
+    v = warp_sum(v);
+    return block_sum_lane0(v, sh);
+}
+
+struct Runs {
+    int n;
+    int i0[MAX_RUNS];
+    int i1[MAX_RUNS];
+    int rows0[MAX_RUNS];     // first local row of the run
+    int pre[MAX_RUNS + 1];   // prefix of run row counts
+};
+
+// Contiguous runs of set bits of a row-block mask, with their local row ranges.
+__device__ void build_runs(const uint64_t *mask, int m, const int32_t *rbp, Runs &R)
+{
+    __syncthreads();  // R of the previous task may still be in use
+    if (threadIdx.x == 0) {
+        int n = 0, acc = 0;
+        int i = 0;
+        while (i < m) {
+            if (!mask_has(mask, i)) { ++i; continue; }
+            int s = i;
+            while (i < m && mask_has(mask, i)) ++i;
+            R.i0[n] = s;
+            R.i1[n] = i;
+            R.rows0[n] = rbp[s];
+            R.pre[n] = acc;
+            acc += rbp[i] - rbp[s];
+            ++n;
+        }
+        R.pre[n] = acc;
+        R.n = n;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ int run_row(const Runs &R, int f)
+{
+    int k = 0;
+    while (f >= R.pre[k + 1]) ++k;
+    return R.rows0[k] + (f - R.pre[k]);
+}
+
+template <typename V>
+__device__ __forceinline__ double ldv(const V *p) { return (double)__ldg(p); }
+
+__device__ __forceinline__ double z_value(double t, double ax, double mu, int status)
+{
+    return status == 0 ? fma(mu, t, ax) : ax;
+}
+
+template <typename V>
+__global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
+{
+    __shared__ Runs R;
+    __shared__ double sh[WARPS];
+    __shared__ double s_gg;
+
+    const V *vals = static_cast<const V *>(p.vals);
+    const V *tvals = static_cast<const V *>(p.tvals);
+    const int lane = threadIdx.x & 31;
+    const int gwarp = blockIdx.x * WARPS + (threadIdx.x >> 5);
+    const int nwarps = gridDim.x * WARPS;
+    const int gtid = blockIdx.x * BLOCK + threadIdx.x;
+    const int nthreads = gridDim.x * BLOCK;
+    const int m = p.m;
+    const EpochHeader hdr = *p.hdr;
+    const int n_tasks = hdr.n_tasks;
+    const bool serial = hdr.mode == 0;
+    const bool sharded = (hdr.flags & 4) != 0;
+    double *part_gg = p.part;
+    double *part_den = p.part + gridDim.x;
+    double *part_m = p.part + 2 * gridDim.x;
+
+    for (int k = 0; k < n_tasks; ++k) {
+        const TaskDev T = p.tasks[k];
+        const PanelDev P = p.panels[T.lp];
+        const int32_t *rbp = p.rbp + (int64_t)T.lp * (m + 1);
+        build_runs(T.mask, m, rbp, R);
+        double2 *gx = reinterpret_cast<double2 *>(p.gx + (k & 1) * p.gx_stride);
+        const double *xj = p.x + P.x_off;
+
+        // ---- phase 1: g = A_I^T r_I over the panel CSC -------------------
+        double wsum = 0.0;
+        {
+            const V *tv = tvals + P.val_off;
+            const int32_t *tr = p.trows + P.val_off;
+            for (int c = gwarp; c < P.n_cols; c += nwarps) {
+                const int32_t *cp = p.cptr + P.cptr_off + (int64_t)c * (m + 1);
+                double acc = 0.0;
+                for (int q = 0; q < R.n; ++q) {
+                    int s = __ldg(cp + R.i0[q]), e = __ldg(cp + R.i1[q]);
+                    int i = s + lane;
+                    for (; i + 96 < e; i += 128) {
+                        int r0 = __ldg(tr + i), r1 = __ldg(tr + i + 32);
+                        int r2 = __ldg(tr + i + 64), r3 = __ldg(tr + i + 96);
+                        double v0 = ldv(tv + i), v1 = ldv(tv + i + 32);
+                        double v2 = ldv(tv + i + 64), v3 = ldv(tv + i + 96);
+                        acc = fma(v0, p.r[r0], acc);
+                        acc = fma(v1, p.r[r1], acc);
+                        acc = fma(v2, p.r[r2], acc);
+                        acc = fma(v3, p.r[r3], acc);
+                    }
+                    for (; i < e; i += 32) acc = fma(ldv(tv + i), p.r[__ldg(tr + i)], acc);
+                }
+                acc = warp_sum(acc);
+                if (lane == 0) {
+                    gx[c] = make_double2(acc, xj[c]);
+                    wsum = fma(acc, acc, wsum);
+                }
+            }
+        }
+        double bsum = block_sum_lane0(wsum, sh);
+        if (threadIdx.x == 0) part_gg[blockIdx.x] = bsum;
+        grid_sync(p.bar);
+        double gg = fixed_sum(part_gg, gridDim.x, sh);
+
+        // ---- phase 2: dual SpMV t = A_I g, ax = A_I x_J -----------------
+        wsum = 0.0;
+        const int n_task_rows = R.pre[R.n];
+        if (gg != 0.0) {
+            const V *fv = vals + P.val_off;
+            const int32_t *fc = p.cols + P.val_off;
+            const int32_t *ip = p.indptr + P.row_off + T.lp;
+            for (int f = gwarp; f < n_task_rows; f += nwarps) {
+                int lr = run_row(R, f);
+                int s = __ldg(ip + lr), e = __ldg(ip + lr + 1);
+                double t = 0.0, ax = 0.0;
+                int i = s + lane;
+                for (; i + 32 < e; i += 64) {
+                    int c0 = __ldg(fc + i), c1 = __ldg(fc + i + 32);
+                    double v0 = ldv(fv + i), v1 = ldv(fv + i + 32);
+                    double2 a0 = gx[c0], a1 = gx[c1];
+                    t = fma(v0, a0.x, t);
+                    ax = fma(v0, a0.y, ax);
+                    t = fma(v1, a1.x, t);
+                    ax = fma(v1, a1.y, ax);
+                }
+                if (i < e) {
+                    int c0 = __ldg(fc + i);
+                    double v0 = ldv(fv + i);
+                    double2 a0 = gx[c0];
+                    t = fma(v0, a0.x, t);
+                    ax = fma(v0, a0.y, ax);
+                }
+                t = warp_sum(t);
+                ax = warp_sum(ax);
+                if (lane == 0) {
+                    reinterpret_cast<double2 *>(p.t_ax)[lr] = make_double2(t, ax);
+                    wsum = fma(t, t, wsum);
+                }
+            }
+        } else {
+            // zero gradient: only A_I x_J is needed (z = A x_j, status 1)
+            const V *fv = vals + P.val_off;
+            const int32_t *fc = p.cols + P.val_off;
+            const int32_t *ip = p.indptr + P.row_off + T.lp;
+            for (int f = gwarp; f < n_task_rows; f += nwarps) {
+                int lr = run_row(R, f);
+                int s = __ldg(ip + lr), e = __ldg(ip + lr + 1);
+                double ax = 0.0;
+                for (int i = s + lane; i < e; i += 32) ax = fma(ldv(fv + i), xj[__ldg(fc + i)], ax);
+                ax = warp_sum(ax);
+                if (lane == 0) reinterpret_cast<double2 *>(p.t_ax)[lr] = make_double2(0.0, ax);
+            }
+        }
+        bsum = block_sum_lane0(wsum, sh);
+        if (threadIdx.x == 0) part_den[blockIdx.x] = bsum;
+        grid_sync(p.bar);
+        double denom = fixed_sum(part_den, gridDim.x, sh);
+
+        // ---- phase 3: step, x accumulation, z store, serial refresh -----
+        double mu = 0.0;
+        int status = 0;
+        if (gg == 0.0) {
+            status = 1;
+        } else if (denom < 1e-30) {
+            status = 2;
+        } else {
+            mu = T.beta * gg / denom;
+        }
+        if (gtid == 0) {
+            p.mus[k] = mu;
+            p.statuses[k] = status;
+            p.counts[T.lp] += 1;
+        }
+        {
+            double *xh = p.xhat + P.x_off;
+            for (int c = gtid; c < P.n_cols; c += nthreads) {
+                double2 a = gx[c];
+                double xn = status == 0 ? __dadd_rn(a.y, __dmul_rn(mu, a.x)) : a.y;
+                xh[c] += xn;
+            }
+        }
+        {
+            const double2 *tax = reinterpret_cast<const double2 *>(p.t_ax);
+            double *zj = p.z + P.row_off;
+            for (int f = gtid; f < n_task_rows; f += nthreads) {
+                int lr = run_row(R, f);
+                double2 q = tax[lr];
+                zj[lr] = z_value(q.x, q.y, mu, status);
+            }
+        }
+        const bool last_of_visit = (T.flags & TASK_LAST_OF_VISIT) != 0;
+        if (serial && last_of_visit) {
+            // refresh every row of the visit's drawn blocks (executor.py:215-223)
+            const double2 *tax = reinterpret_cast<const double2 *>(p.t_ax);
+            const int64_t zlo = P.row_off, zhi = P.row_off + P.n_rows;
+            for (int i = 0; i < m; ++i) {
+                if (!mask_has(T.visit_mask, i)) continue;
+                const bool cur = mask_has(T.mask, i);
+                int b0 = p.rb_ptr[i], b1 = p.rb_ptr[i + 1];
+                for (int q = b0 + gtid; q < b1; q += nthreads) {
+                    int g = p.rb_rows[q];
+                    double acc = 0.0;
+                    for (int e = p.inv_ptr[g]; e < p.inv_ptr[g + 1]; ++e) {
+                        int off = p.inv_z[e];
+                        double v;
+                        if (cur && off >= zlo && off < zhi) {
+                            double2 qq = tax[off - zlo];
+                            v = z_value(qq.x, qq.y, mu, status);
+                        } else {
+                            v = p.z[off];
+                        }
+                        acc += v;
+                    }
+                    p.r[g] = p.y[g] - acc;
+                }
+            }
+            if (k + 1 < n_tasks) grid_sync(p.bar);
+        }
+    }
+
+    // ---- epoch tail ------------------------------------------------------
+    grid_sync(p.bar);
+    const bool do_metrics = (hdr.flags & 2) != 0;
+    const bool do_commit = (hdr.flags & 1) != 0;
+    double rsq = 0.0, xsq = 0.0, esq = 0.0;
+    if (!serial || do_metrics || sharded) {
+        for (int g = gtid; g < p.n_meas; g += nthreads) {
+            double acc = 0.0;
+            for (int e = p.inv_ptr[g]; e < p.inv_ptr[g + 1]; ++e) acc += p.z[p.inv_z[e]];
+            if (sharded) {
+                p.exchange[g] = acc;
+            } else {
+                double d = p.y[g] - acc;
+                int rb = p.rb_of_row[g];
+                if (!serial && rb >= 0 && mask_has(hdr.epoch_mask, rb)) p.r[g] = d;
+                rsq = fma(d, d, rsq);
+            }
+        }
+    }
+    for (int lp = 0; lp < p.n_panels_owned; ++lp) {
+        const PanelDev P = p.panels[lp];
+        const int cnt = p.counts[lp];
+        double *xs = p.x + P.x_off;
+        double *xh = p.xhat + P.x_off;
+        const double *xt = p.x_true ? p.x_true + P.x_off : nullptr;
+        for (int c = gtid; c < P.n_cols; c += nthreads) {
+            double xv = xs[c];
+            if (do_commit && cnt > 0) {
+                xv = xh[c] / (double)cnt;
+                xs[c] = xv;
+                xh[c] = 0.0;
+            }
+            xsq = fma(xv, xv, xsq);
+            if (xt) {
+                double d = xt[c] - xv;
+                esq = fma(d, d, esq);
+            }
+        }
+    }
+    double b0 = block_sum_all(rsq, sh);
+    double b1 = block_sum_all(xsq, sh);
+    double b2 = block_sum_all(esq, sh);
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+        part_m[3 * blockIdx.x + 0] = b0;
+        part_m[3 * blockIdx.x + 1] = b1;
+        part_m[3 * blockIdx.x + 2] = b2;
+        __threadfence();
+        unsigned int t = atomicAdd(p.ticket, 1u);
+        is_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (is_last) {
+        __threadfence();
+        if (threadIdx.x == 0) {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+            for (unsigned int b = 0; b < gridDim.x; ++b) {
+                a0 += ((volatile double *)part_m)[3 * b + 0];
+                a1 += ((volatile double *)part_m)[3 * b + 1];
+                a2 += ((volatile double *)part_m)[3 * b + 2];
+            }
+            int ndeg = 0;
+            for (int k = 0; k < n_tasks; ++k) ndeg += p.statuses[k] != 0;
+            p.out->resid_sq = a0;
+            p.out->x_sq = a1;
+            p.out->err_sq = p.x_true ? a2 : __longlong_as_double(0x7ff8000000000000ll);
+            p.out->n_degenerate = ndeg;
+            if (sharded) {
+                p.exchange[p.n_meas] = a1;
+                p.exchange[p.n_meas + 1] = a2;
+            }
+            if (do_commit)
+                for (int lp = 0; lp < p.n_panels_owned; ++lp) p.counts[lp] = 0;
+            *p.ticket = 0;
+        }
+    }
+}
+
+}  // namespace
+
+namespace bct {
+
+std::string cuda_err(cudaError_t e) { return std::string(cudaGetErrorString(e)); }
+
+int epoch_grid_size(int dtype, int device, int *block)
+{
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (dtype == 0)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<double>, BLOCK, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<float>, BLOCK, 0);
+    if (per < 1) per = 1;
+    if (per > 2) per = 2;
+    *block = BLOCK;
+    return sms * per;
+}
+
+void launch_epoch(const EpochParams &p, int dtype, int grid, int block, cudaStream_t s,
+                  cudaError_t *err)
+{
+    EpochParams local = p;
+    void *args[] = {&local};
+    if (dtype == 0)
+        *err = cudaLaunchCooperativeKernel((const void *)epoch_kernel<double>, grid, block,
+                                           args, 0, s);
+    else
+        *err = cudaLaunchCooperativeKernel((const void *)epoch_kernel<float>, grid, block,
+                                           args, 0, s);
+}
+
+}  // namespace bct

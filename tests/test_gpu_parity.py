@@ -1,0 +1,243 @@
+"""Parity of the CUDA path against the reference's own outputs (golden
+fixtures made by tests/golden/make_golden.py) and against the CPU oracle.
+
+Tolerances: bit-exact for the traced matrix, the table, the selection plans
+and the bitwise set-up kernels; FP64 epochs within 1e-10 relative free-running
+(north_star) and 1e-12 teacher-forced; FP32 storage within
+1e-4 relative on the residual curve (north_star).
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, fixture_system_arrays, golden, unflatten_plans
+
+pytestmark = pytest.mark.gpu
+
+bct = pytest.importorskip("paper_1709_00953_b200")
+from paper_1709_00953_b200 import (CONFIGS, DeviceBlockSystem, EpochExecutor,  # noqa: E402
+                                   ExecutorError, SamplingConfig, SolverParams, SolverState,
+                                   run_gcsgd)
+from paper_1709_00953_b200.geometry import ParallelBeamSpec  # noqa: E402
+
+VARIANTS = {
+    "p1": dict(epochs=500, b=0.5, group_size=1, seed=1234, execution_mode="serial_faithful",
+               sampling=SamplingConfig(alpha=0.25)),
+    "ser_g2": dict(epochs=20, b=0.5, group_size=2, seed=11, execution_mode="serial_faithful",
+                   sampling=SamplingConfig(alpha=1.0)),
+    "par_full": dict(epochs=20, b=0.25, group_size=4, seed=12, execution_mode="parallel",
+                     sampling=SamplingConfig(alpha=1.0)),
+    "par_mixed": dict(epochs=20, b=0.3, group_size=1, seed=13, execution_mode="parallel",
+                      sampling=SamplingConfig(strategy="mixed", alpha=0.5, gamma=0.5, theta0=0.2,
+                                              theta_step=0.1)),
+    "ser_random": dict(epochs=20, b=0.5, group_size=3, seed=14, execution_mode="serial_faithful",
+                       sampling=SamplingConfig(strategy="random", alpha=0.75)),
+}
+
+
+def _hash(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def cfg1_system():
+    return DeviceBlockSystem.parallel_beam(CONFIGS[1].spec, dtype="f64")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+# ---------------------------------------------------------------------------
+# the device-built operator is the reference's, bit for bit
+# ---------------------------------------------------------------------------
+
+def test_builder_small_matches_reference_panels():
+    g = golden("pb_small.npz")
+    spec = ParallelBeamSpec(16, 20, 24, 4, 4)
+    sysm = DeviceBlockSystem.parallel_beam(spec, dtype="f64")
+    for j in range(4):
+        p = sysm.panel(j)
+        np.testing.assert_array_equal(p.data, g[f"data{j}"])
+        np.testing.assert_array_equal(p.cols, g[f"cols{j}"])
+        np.testing.assert_array_equal(p.indptr, g[f"indptr{j}"])
+        np.testing.assert_array_equal(p.rbp, g[f"rbp{j}"])
+        np.testing.assert_array_equal(p.l2g, g[f"l2g{j}"])
+    np.testing.assert_array_equal(sysm.table.values, g["table"])
+    # bitwise forward projection (projector.py:692-702 order)
+    np.testing.assert_array_equal(sysm.forward(g["x_true"]), g["y_clean"])
+
+
+@pytest.mark.parametrize("key", [1, 2])
+def test_builder_matches_reference_hashes(key):
+    hashes = json.load(open(os.path.join(GOLDEN, "pb_hashes.json")))
+    sysm = DeviceBlockSystem.parallel_beam(CONFIGS[key].spec, dtype="f64")
+    for j, h in enumerate(hashes[f"cfg{key}"]):
+        p = sysm.panel(j)
+        assert p.data.size == h["nnz"] and p.l2g.size == h["rows"]
+        assert _hash(p.data) == h["data"], f"panel {j} values"
+        assert _hash(p.cols) == h["cols"], f"panel {j} cols"
+        assert _hash(p.indptr) == h["indptr"]
+        assert _hash(p.rbp) == h["rbp"]
+        assert _hash(p.l2g) == h["l2g"]
+    assert _hash(sysm.table.values) == hashes[f"cfg{key}_table_sha"]
+
+
+# ---------------------------------------------------------------------------
+# free-running runs against the reference (config 1)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", list(VARIANTS))
+def test_free_running_matches_reference(cfg1_system, cfg1_runs, name):
+    g = cfg1_runs
+    np.testing.assert_array_equal(cfg1_system.forward(g["x_true"]), g["y_clean"])
+    rec = {}
+    x, tr = run_gcsgd(cfg1_system, g["y"], SolverParams(**VARIANTS[name]), x_true=g["x_true"],
+                      plan_record=rec)
+    # the selection stream is replayed exactly
+    want = unflatten_plans(g[f"{name}_plans"])
+    assert sorted(rec) == sorted(want)
+    for ep, visits in want.items():
+        got = [(j, np.concatenate(gr) if gr else np.empty(0, np.int64)) for j, gr in rec[ep]]
+        assert [j for j, _ in got] == [j for j, _ in visits]
+        for (_, a), (_, b) in zip(got, visits):
+            np.testing.assert_array_equal(a, b)
+    xr = g[f"{name}_x"]
+    assert rel(x, xr) <= 1e-10
+    A_res = np.linalg.norm(g["y"] - cfg1_system.forward(x))
+    A_ref = np.linalg.norm(g["y"] - cfg1_system.forward(xr))
+    assert abs(A_res - A_ref) / A_ref <= 1e-10
+    gaps = np.array([r.obs_gap_db for r in tr.rows])
+    np.testing.assert_allclose(gaps, g[f"{name}_gap"], rtol=1e-9)
+    snrs = np.array([r.snr_db for r in tr.rows])
+    np.testing.assert_allclose(snrs, g[f"{name}_snr"], rtol=1e-9)
+    assert [r.n_tasks for r in tr.rows] == list(g[f"{name}_n_tasks"])
+    assert [r.bytes_moved for r in tr.rows] == list(g[f"{name}_bytes_moved"])
+
+
+@pytest.mark.parametrize("name", ["ser_g2", "par_full", "par_mixed", "ser_random"])
+def test_teacher_forced_epoch(cfg1_system, cfg1_runs, name):
+    g = cfg1_runs
+    p = SolverParams(**VARIANTS[name])
+    plans = unflatten_plans(g[f"{name}_plans"])
+    state = SolverState.initialize(cfg1_system, g["y"])
+    z = g[f"{name}_snap10_z"]
+    zs, off = [], 0
+    for j in range(cfg1_system.n_col_blocks):
+        n = cfg1_system.n_local_rows(j)
+        zs.append(z[off:off + n])
+        off += n
+    state.load(g[f"{name}_snap10_x"], g[f"{name}_snap10_r"], zs)
+    from paper_1709_00953_b200.sampling import group_beta
+    loops = [(j, [(ids[a:a + p.group_size], group_beta(cfg1_system.table, p.b, j,
+                                                         ids[a:a + p.group_size]))
+                  for a in range(0, ids.size, p.group_size)]) for j, ids in plans[11]]
+    EpochExecutor(p.execution_mode).run_epoch(11, loops, state, cfg1_system)
+    cfg1_system.commit_epoch()
+    assert rel(state.x, g[f"{name}_snap11_x"]) <= 1e-12
+    assert rel(state.r, g[f"{name}_snap11_r"]) <= 1e-12
+    assert rel(np.concatenate(state.z), g[f"{name}_snap11_z"]) <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# the reference tests' own systems (fan beam)
+# ---------------------------------------------------------------------------
+
+def test_known_answer_final_snr():
+    """tests/test_solvers.py:196-202: final SNR 6.416697928678968 +- 1e-9."""
+    f = golden("fan12.npz")
+    panels, rows, vidx, table, nm, nv = fixture_system_arrays(f)
+    sysm = DeviceBlockSystem.from_panels(panels, rows, vidx, table, nm, nv, dtype="f64")
+    np.testing.assert_array_equal(sysm.forward(f["x_true"]), f["y"])
+    x, tr = run_gcsgd(sysm, f["y"], SolverParams(epochs=30, b=6.0, seed=3), x_true=f["x_true"])
+    assert tr.rows[-1].snr_db == pytest.approx(6.416697928678968, abs=1e-9)
+    assert rel(x, f["final_x"]) <= 1e-12
+
+
+@pytest.mark.parametrize("gs", [1, 3])
+@pytest.mark.parametrize("mode", ["serial_faithful", "parallel"])
+def test_literal_epochs(gs, mode):
+    """tests/test_solvers.py:125-145 (LiteralSequential at 1e-12)."""
+    f = golden("fan10.npz")
+    panels, rows, vidx, table, nm, nv = fixture_system_arrays(f)
+    sysm = DeviceBlockSystem.from_panels(panels, rows, vidx, table, nm, nv, dtype="f64")
+    rec = {}
+    x, _ = run_gcsgd(sysm, f["y"], SolverParams(epochs=4, b=6.0, group_size=gs, seed=17,
+                                               execution_mode=mode,
+                                               sampling=SamplingConfig(alpha=0.5)),
+                     x_true=f["x_true"], plan_record=rec)
+    want = f[f"x_{gs}_{mode}"]
+    assert np.abs(x - want).max() <= 1e-12 * max(np.abs(want).max(), 1.0)
+
+
+@pytest.fixture(scope="module")
+def exec_system():
+    f = golden("exec10.npz")
+    panels, rows, vidx, table, nm, nv = fixture_system_arrays(f)
+    return f, DeviceBlockSystem.from_panels(panels, rows, vidx, table, nm, nv, dtype="f64")
+
+
+EXEC_PLANS = {
+    "barrier": [(0, [(np.array([2, 3]), 0.7)]), (1, [(np.array([2, 3]), 0.7)])],
+    "workers": [(0, [(np.array([0, 5]), 0.8), (np.array([2, 7]), 0.6)]),
+                (1, [(np.array([1, 4, 6]), 0.5)]), (3, [(np.array([3]), 0.9)])],
+    "mutate": [(0, [(np.array([0, 5]), 0.8)]), (2, [(np.array([3]), 0.5)])],
+}
+
+
+@pytest.mark.parametrize("name", list(EXEC_PLANS))
+@pytest.mark.parametrize("mode", ["serial_faithful", "parallel"])
+def test_executor_matches_reference(exec_system, name, mode):
+    f, sysm = exec_system
+    state = SolverState.initialize(sysm, f["y"], x0=f["x0"])
+    stats = EpochExecutor(mode, 1).run_epoch(1, EXEC_PLANS[name], state, sysm)
+    tol = 1e-12
+    np.testing.assert_allclose(state.xhat, f[f"{name}_{mode}_xhat"], atol=tol, rtol=0)
+    np.testing.assert_allclose(state.r, f[f"{name}_{mode}_r"], atol=tol, rtol=0)
+    np.testing.assert_allclose(np.concatenate(state.z), f[f"{name}_{mode}_z"], atol=tol, rtol=0)
+    np.testing.assert_array_equal(state.counts, f[f"{name}_{mode}_counts"])
+    st = f[f"{name}_{mode}_stats"]
+    assert (stats.n_tasks, stats.n_loops, stats.bytes_moved, stats.n_degenerate) == tuple(st)
+    sysm.commit_epoch()
+    np.testing.assert_allclose(state.x, f[f"{name}_{mode}_x"], atol=tol, rtol=0)
+
+
+def test_degenerate_tasks_accumulate_unchanged_image(exec_system):
+    """tests/test_executor.py:131-140."""
+    f, sysm = exec_system
+    state = SolverState.initialize(sysm, f["y"], x0=f["x0"])
+    sysm.set_r(np.zeros(sysm.n_measurements))
+    ex = EpochExecutor("serial_faithful", 1)
+    stats = ex.run_epoch(1, [(0, [(np.array([0]), 0.8), (np.array([5]), 0.8)])], state, sysm)
+    assert stats.n_degenerate == 2
+    assert list(ex.last_statuses) == [1, 1]
+    v = sysm.voxel_indices(0)
+    np.testing.assert_array_equal(state.xhat[v], 2.0 * f["x0"][v])
+
+
+def test_failed_batch_leaves_no_trace(exec_system):
+    """tests/test_executor.py:143-153."""
+    f, sysm = exec_system
+    state = SolverState.initialize(sysm, f["y"])
+    r0 = state.r.copy()
+    with pytest.raises(ExecutorError) as info:
+        EpochExecutor("serial_faithful", 1).run_epoch(1, [(0, [(np.array([999]), 0.8)])],
+                                                      state, sysm)
+    assert info.value.task is not None
+    assert not np.any(state.xhat) and not np.any(state.counts)
+    np.testing.assert_array_equal(state.r, r0)
+    assert not np.any(sysm.projection_sum())
+
+
+def test_warm_start_and_audit(exec_system):
+    f, sysm = exec_system
+    state = SolverState.initialize(sysm, f["y"], x0=f["x0"])
+    assert sysm.audit_drift() == 0.0
+    r = state.r
+    r[3] += 1e-3
+    sysm.set_r(r)
+    assert abs(sysm.audit_drift() - 1e-3 / np.abs(f["y"]).max()) < 1e-15
