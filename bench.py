@@ -1,0 +1,400 @@
+"""Throughput of the GCSGD hot path on B200 (BASELINE.json metric: block
+updates/s and A-nonzeros/s, GB/s against the HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+Workload: BASELINE config 4 by default (1024^2 parallel beam, 720 views x 1449
+bins, 32x32 blocks, grouped variant with 64 blocks per step capped at the 32
+row blocks, FP32 values + int32 indices, parallel execution, b = 1/32) -- the
+configuration the north star's single-GPU roofline and 8-GPU scaling targets
+are quoted on.  One step = one epoch of run_gcsgd: 32 full-panel tasks
+(= 1024 block updates), the union refresh, the x commit and the metrics.
+Inputs are synthetic (seeded random ellipses + Gaussian noise).  A is 15 GB
+in HBM (forward + CSC copies), far larger than L2, so no L2 flush is needed
+between steps.  N > 1 shards the column blocks across ranks (one NCCL
+all-reduce of the partial projection sums per epoch, strong scaling).
+
+--impl reference times the reference algorithm on the host cores: the CPU
+oracle (a bit-exact C restatement of the reference's numba kernels; the
+reference itself is pure Python + numba and cannot be installed here) on a
+bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout
+                self.samples.append([s.strip() for s in out.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace('.', '').isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace('.', '').isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples if len(s) >= 6
+                          for k in range(4) if s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def task_bytes(system, dtype_bytes):
+    """Algorithmic bytes of one full-panel task:
+    2 nnz (s_val + 4) + 8 (2 rows + 3 |J|) with FP64 vectors."""
+    tot = {}
+    for j in range(system.panel_begin, system.panel_end):
+        nr = system.n_local_rows(j)
+        p_nnz = system._panel_nnz(j)
+        tot[j] = 2 * p_nnz * (dtype_bytes + 4) + 8 * (2 * nr + 3 * int(system.col_sizes[j]))
+    return tot
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+
+    from paper_1709_00953_b200 import (CONFIGS, DeviceBlockSystem, SamplingConfig, SolverParams,
+                                       add_noise, random_ellipses, run_gcsgd)
+    from paper_1709_00953_b200 import distributed as D
+    from paper_1709_00953_b200.executor import pack_loops, submit, wait
+    from paper_1709_00953_b200 import _native as N
+    from paper_1709_00953_b200.sampling import BlockScheduler
+    from paper_1709_00953_b200.solvers import SolverState, _loops
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl")
+    device = local if world > 1 else 0
+    torch.cuda.set_device(device)
+    cfg = CONFIGS[args.config]
+    spec = cfg.spec
+    nc = spec.nc
+    pr = (rank * nc // world, (rank + 1) * nc // world)
+    t_build = time.perf_counter()
+    system = DeviceBlockSystem.parallel_beam(spec, dtype=cfg.dtype, device=device, panel_range=pr)
+    build_s = time.perf_counter() - t_build
+    x_true = random_ellipses(spec.n, cfg.n_ellipses, cfg.phantom_seed)
+    if world > 1:
+        y_clean = D.sharded_forward(system, x_true)
+    else:
+        y_clean = system.forward(x_true)
+    y, _ = add_noise(y_clean, cfg.noise_frac, cfg.noise_seed)
+    params = SolverParams(epochs=args.steps + args.warmup, b=cfg.b, group_size=cfg.group_size,
+                          execution_mode=cfg.mode, seed=cfg.solver_seed,
+                          sampling=SamplingConfig(alpha=cfg.alpha, gamma=cfg.gamma))
+    stream = torch.cuda.ExternalStream(system.stream(), device=device)
+    vb = 4 if cfg.dtype == "f32" else 8
+
+    # -- device-resident loop: plans pre-drawn, state resident ------------------
+    state = SolverState.initialize(system, y)
+    system.set_x_true(x_true)
+    sched = BlockScheduler(system.table, params.sampling, group_size=params.group_size)
+    rng = np.random.default_rng(params.seed)
+    plans = []
+    for e in range(args.warmup + args.steps):
+        plan = sched.epoch_plan(e + 1, rng)
+        plans.append(pack_loops(_loops(plan, system.table, params.b), system))
+        sched.advance_epoch()
+    flags = N.BCT_COMMIT | N.BCT_METRICS
+    mode = cfg.mode
+    runner = D.ShardedRunner(system) if world > 1 else None
+
+    def step(packed):
+        if runner is not None:
+            return runner.epoch(packed, flags)
+        submit(system, mode, packed, flags)
+        return wait(system, packed.task_j.size)[0]
+
+    for e in range(args.warmup):
+        step(plans[e])
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(device)
+    kernel_ms = []
+    with ClockSampler(device) as clk:
+        ev0.record(stream)
+        for e in range(args.warmup, args.warmup + args.steps):
+            res = step(plans[e])
+            kernel_ms.append(res.kernel_ms)
+        ev1.record(stream)
+        torch.cuda.synchronize(device)
+    if world > 1:
+        torch.distributed.barrier()
+    ms = ev0.elapsed_time(ev1)
+    ms_all = ms
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{device}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_all = float(t.item())
+    ms_step = ms_all / args.steps
+    # units: every rank runs its own panels' tasks; the plan is global
+    tasks_per_step = sum(p.task_j.size for p in plans[args.warmup:]) / args.steps
+    blocks_per_step = sum(int(p.task_gptr[-1]) for p in plans[args.warmup:]) / args.steps
+    nnz_total = system.nnz
+    if world > 1:
+        t = torch.tensor([float(nnz_total)], device=f"cuda:{device}")
+        torch.distributed.all_reduce(t)
+        nnz_total = int(t.item())
+    # every task is a full panel when alpha=1, gamma=1: nnz per epoch = nnz(A)
+    nnz_per_step = nnz_total * (blocks_per_step / (spec.m * nc))
+
+    # roofline of the dominant kernel (the epoch kernel), algorithmic bytes
+    tb = task_bytes(system, vb)
+    owned_tasks_bytes = []
+    for p in plans[args.warmup:]:
+        s = 0
+        for k in range(p.task_j.size):
+            j = int(p.task_j[k])
+            if system.owns(j):
+                frac = (p.task_gptr[k + 1] - p.task_gptr[k]) / spec.m
+                s += tb[j] * frac
+        owned_tasks_bytes.append(s)
+    tail_bytes = 8 * (spec.n_measurements * 3 + 2 * system.z_len) + 8 * 4 * system.x_len_owned()
+    alg_bytes = float(np.mean(owned_tasks_bytes)) + tail_bytes
+    k_ms = float(np.mean(kernel_ms))
+    peak, peak_kind = _peaks()
+    achieved = alg_bytes / (k_ms * 1e-3) / 1e9
+
+    # -- end to end through the public API (host y in, host x out) ------------
+    torch.cuda.synchronize(device)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e2e_params = SolverParams(epochs=args.steps, b=cfg.b, group_size=cfg.group_size,
+                              execution_mode=cfg.mode, seed=cfg.solver_seed + 1,
+                              sampling=SamplingConfig(alpha=cfg.alpha, gamma=cfg.gamma))
+    if world > 1:
+        torch.distributed.barrier()
+    e0.record(stream)
+    if world > 1:
+        x_out, tr = D.run_gcsgd_sharded(system, y, e2e_params, x_true=x_true)
+    else:
+        x_out, tr = run_gcsgd(system, y, e2e_params, x_true=x_true)
+    e1.record(stream)
+    torch.cuda.synchronize(device)
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=f"cuda:{device}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    plan_bytes = 64 + 128 * tasks_per_step
+    h2d = (8 * spec.n_measurements + 8 * spec.n_voxels * 2) / args.steps + plan_bytes
+    d2h = 64 + 12 * tasks_per_step + 8 * spec.n_voxels / args.steps
+
+    out = None
+    if rank == 0:
+        value = blocks_per_step / (ms_step * 1e-3)
+        out = {
+            "metric": "block updates/s",
+            "value": value,
+            "unit": "block-updates/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "strong",
+            "vs_baseline": None,
+            "dtype": "f32-values/i32-index/f64-math" if cfg.dtype == "f32" else "f64",
+            "data": "synthetic (seeded random ellipses + 0.5% Gaussian noise; A traced on device)",
+            "config": {"workload": f"{cfg.name}: {spec.n}^2 parallel beam, {spec.views} views "
+                                   f"x {spec.bins} bins, {spec.m}x{nc} blocks, group "
+                                   f"{cfg.group_size} (capped at {spec.m}), {cfg.mode}, "
+                                   f"b={cfg.b:g}",
+                       "step": "one epoch of run_gcsgd (all column-block visits, refresh, "
+                               "commit, metrics)",
+                       "blocks_per_step": blocks_per_step, "tasks_per_step": tasks_per_step,
+                       "nnz_A": nnz_total,
+                       "l2": "inputs larger than L2 (A = %.1f GB in HBM)" % (
+                           nnz_total * (vb + 4) * 2 / 1e9),
+                       "parallelism": f"column-block shards x{world}" if world > 1 else "1 GPU",
+                       "build_s": build_s},
+            "nnz_per_s": nnz_per_step / (ms_step * 1e-3),
+            "gbs_alg": achieved if world == 1 else None,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "epoch_kernel (persistent cooperative; one launch per epoch)",
+                         "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
+                         "peak_kind": peak_kind},
+            "e2e": {"value": blocks_per_step * args.steps / (e2e_ms * 1e-3),
+                    "unit": "block-updates/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "api": "run_gcsgd(system, y_host, params, x_true=host) -> x_host",
+                    "final_snr_db": tr.rows[-1].snr_db if tr.rows else None},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+        }
+    return out, system, cfg, plans
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference algorithm on host cores)
+# ---------------------------------------------------------------------------
+
+def cpu_sample(cfg_key, threads, budget_s=20.0, plans=None):
+    """Reference algorithm on the host: full-panel tasks of epoch 1's plan,
+    one task per thread (the reference's parallel thread fan-out,
+    executor.py:182-198), f64 values as the reference stores them."""
+    from oracle.oracle import OracleSystem, _run_visit
+    from paper_1709_00953_b200 import CONFIGS
+    from paper_1709_00953_b200.sampling import BlockScheduler, SamplingConfig, group_beta
+
+    cfg = CONFIGS[cfg_key]
+    spec = cfg.spec
+    n_tasks = max(1, min(threads, spec.nc))
+    t0 = time.perf_counter()
+    # plan of epoch 1 with the solver seed; trace only the panels it visits first
+    tab_sys = None
+    rng = np.random.default_rng(cfg.solver_seed)
+    order = rng.choice(spec.nc, size=spec.nc, replace=False)[:n_tasks]
+    ora = OracleSystem.parallel_beam(spec.n, spec.views, spec.bins, spec.m, spec.nc,
+                                     panels=set(int(j) for j in order))
+    trace_s = time.perf_counter() - t0
+    r = np.ones(spec.n_measurements)
+    ids = np.arange(spec.m, dtype=np.int64)
+    import concurrent.futures as cf
+
+    def one(j):
+        x_j = np.zeros(ora.vidx[j].size)
+        return _run_visit(ora, int(j), [(ids, 1.0 / spec.nc)], r, x_j, workers=1)
+
+    def run_once():
+        with cf.ThreadPoolExecutor(max_workers=n_tasks) as ex:
+            list(ex.map(one, order))
+
+    # ctypes releases the GIL, so the threads run concurrently
+    t = time.perf_counter()
+    run_once()
+    dt = time.perf_counter() - t
+    nnz = sum(ora.data[int(j)].size for j in order)
+    return {"tasks": n_tasks, "seconds": dt, "block_updates": n_tasks * spec.m, "nnz": nnz,
+            "trace_s": trace_s, "run_once": run_once}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if world > 1 and rank != 0:
+        return None
+    from paper_1709_00953_b200 import CONFIGS
+    cfg = CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    s = cpu_sample(args.config, cores)
+    times = []
+    for _ in range(max(args.warmup, 0)):
+        s["run_once"]()
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        s["run_once"]()
+        times.append(time.perf_counter() - t)
+    sec = float(np.mean(times)) if times else s["seconds"]
+    val = s["block_updates"] / sec
+    sample = (f"{s['tasks']} full-panel tasks of {cfg.name} epoch 1 (one per thread), "
+              f"f64 values, C restatement of _run_tasks")
+    return {"metric": "block updates/s", "value": val, "unit": "block-updates/s",
+            "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "sample": sample},
+            "nnz_per_s": s["nnz"] / sec,
+            "cpu_baseline": {"value": val, "unit": "block-updates/s", "cores": s["tasks"],
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": val, "unit": "block-updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        out = run_reference(args)
+        if out is not None:
+            print(json.dumps(out))
+        return
+    out, system, cfg, plans = run_ours(args)
+    world, rank, _ = dist_env()
+    if rank == 0 and out is not None:
+        if world == 1 and not args.no_cpu:
+            cores = os.cpu_count() or 1
+            s = cpu_sample(args.config, cores)
+            out["cpu_baseline"] = {
+                "value": s["block_updates"] / s["seconds"], "unit": "block-updates/s",
+                "cores": s["tasks"], "kind": "port",
+                "sample": f"{s['tasks']} full-panel {cfg.name} tasks, one per thread, f64 "
+                          f"(C restatement of _run_tasks), {s['seconds']:.2f} s"}
+        print(json.dumps(out))
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,178 @@
+"""Column-block sharding over ranks: one process per GPU.
+
+Rank p owns the contiguous column blocks ``owned_range(n, world, p)``: their
+forward panels, panel CSCs, z^j, x_J and xhat_J.  y and r are replicated and
+every rank draws the same plan from the same seed, so the plan needs no
+broadcast.  Per epoch (parallel execution only -- serial_faithful visits are
+ordered through the residual and do not shard):
+
+1. each rank runs the plan's tasks on its own column blocks against the
+   epoch-start r (the device skips other ranks' tasks; BCT_SHARDED);
+2. the epoch kernel writes the rank's partial projection sums
+   S_p[g] = sum_{j owned} z^j[g] for every measurement, plus the partial
+   squared norms of x and x_true - x, into the context's exchange buffer;
+3. one all-reduce (NCCL over NVLink on the device path) sums the buffer in
+   place;
+4. ``bct_finish_sharded`` sets r = y - S on the rows of the drawn blocks
+   (executor.py:249-252) and reduces |y - S|^2 for the trace.
+
+The runner is written against a small backend interface so the same host
+logic runs on the device (``DeviceShard``) and, in the multi-process CPU tests,
+on a test-side oracle backend over the gloo backend.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+
+import numpy as np
+
+from . import _native as N
+from .errors import ConfigurationError, DivergenceError
+from .executor import pack_loops, submit, wait
+from .metrics import ConvergenceTrace, TraceRow, snr_from_sq
+from .sampling import BlockScheduler, ScriptedScheduler
+from .solvers import SolverState, _loops
+from .validation import as_vector
+
+
+def owned_range(n_panels, world, rank):
+    """Contiguous column-block range of ``rank`` (balanced to within one block)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ConfigurationError(f"bad rank {rank} of {world}")
+    if n_panels < world:
+        raise ConfigurationError(f"{n_panels} column blocks cannot shard over {world} ranks")
+    return rank * n_panels // world, (rank + 1) * n_panels // world
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ wrapper of a device pointer."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+class DeviceShard:
+    """Backend of ShardedRunner on a DeviceBlockSystem (the product path)."""
+
+    def __init__(self, system):
+        import torch
+        self.system = system
+        p = ctypes.c_void_p()
+        n = ctypes.c_int64()
+        N.check(N.load().bct_exchange_buffer(system.ctx, ctypes.byref(p), ctypes.byref(n)),
+                system.ctx)
+        self.n_meas = system.n_measurements
+        self.buf = torch.as_tensor(_CudaArray(p.value, n.value), device=f"cuda:{system.device}")
+        self.stream = torch.cuda.ExternalStream(system.stream(), device=system.device)
+
+    def run_partial(self, packed, flags):
+        submit(self.system, "parallel", packed, flags | N.BCT_SHARDED)
+        return wait(self.system, packed.task_j.size)[0]
+
+    def exchange(self):
+        return self.buf
+
+    def finish(self, flags):
+        import torch
+        torch.cuda.current_stream(self.system.device).synchronize()  # the all-reduce
+        rs = ctypes.c_double()
+        N.check(N.load().bct_finish_sharded(self.system.ctx, flags, ctypes.byref(rs)),
+                self.system.ctx)
+        tail = self.buf[self.n_meas:self.n_meas + 2].cpu().numpy()
+        return rs.value, float(tail[0]), float(tail[1])
+
+
+class ShardedRunner:
+    """One sharded epoch = partial epoch, all-reduce of the exchange buffer,
+    finish.  ``allreduce`` defaults to torch.distributed.all_reduce."""
+
+    def __init__(self, system, backend=None, allreduce=None):
+        self.system = system
+        self.backend = backend if backend is not None else DeviceShard(system)
+        if allreduce is None:
+            import torch.distributed as dist
+            allreduce = dist.all_reduce
+        self.allreduce = allreduce
+
+    def epoch(self, packed, flags):
+        res = self.backend.run_partial(packed, flags)
+        self.allreduce(self.backend.exchange())
+        resid_sq, x_sq, err_sq = self.backend.finish(flags)
+        res.resid_sq = resid_sq
+        res.x_sq = x_sq
+        res.err_sq = err_sq
+        res.n_tasks = packed.task_j.size
+        return res
+
+
+def sharded_forward(system, x, allreduce=None):
+    """y = A x with every rank contributing its panels (one all-reduce)."""
+    import torch
+    import torch.distributed as dist
+    part = system.forward(x)  # owned panels only
+    t = torch.as_tensor(part, device=f"cuda:{system.device}")
+    (allreduce or dist.all_reduce)(t)
+    return t.cpu().numpy()
+
+
+def run_gcsgd_sharded(system, y, params, x_true=None, schedule=None, plan_record=None,
+                      runner=None):
+    """run_gcsgd with the column blocks sharded over the process group
+    (parallel execution).  Returns the full x on every rank and the trace."""
+    import torch
+    import torch.distributed as dist
+    if params.execution_mode != "parallel":
+        raise ConfigurationError("sharded execution requires execution_mode='parallel'")
+    runner = runner or ShardedRunner(system)
+    if schedule is not None:
+        scheduler = ScriptedScheduler(schedule, group_size=params.group_size)
+    else:
+        scheduler = BlockScheduler(system.table, params.sampling, group_size=params.group_size)
+    state = SolverState.initialize(system, y)
+    rng = np.random.default_rng(params.seed)
+    y_norm = float(np.linalg.norm(state.y))
+    xt_norm = None
+    if x_true is not None:
+        x_true = as_vector("x_true", x_true, length=system.n_voxels)
+        xt_norm = float(np.linalg.norm(x_true))
+        system.set_x_true(x_true)
+    else:
+        system.set_x_true(None)
+    flags = N.BCT_COMMIT | N.BCT_METRICS
+    trace = ConvergenceTrace()
+    started = time.perf_counter()
+    ref_norm = None
+    for epoch in range(1, params.epochs + 1):
+        theta_now = scheduler.theta
+        plan = scheduler.epoch_plan(epoch, rng)
+        if plan_record is not None:
+            plan_record[epoch] = plan
+        packed = pack_loops(_loops(plan, system.table, params.b), system)
+        res = runner.epoch(packed, flags)
+        scheduler.advance_epoch()
+        snr = snr_from_sq(xt_norm, res.err_sq) if x_true is not None else math.nan
+        gap = snr_from_sq(y_norm, res.resid_sq) if y_norm > 0 else math.nan
+        row = TraceRow(epoch, epoch * params.sampling.alpha, snr, gap,
+                       time.perf_counter() - started, params.execution_mode, theta_now,
+                       packed.bytes_moved, packed.task_j.size, res.kernel_ms)
+        trace.append(row)
+        norm_x = math.sqrt(res.x_sq) if res.x_sq >= 0 else math.nan
+        if ref_norm is None:
+            ref_norm = max(norm_x, 1e-12)
+        if not math.isfinite(norm_x) or norm_x > params.divergence_factor * ref_norm:
+            raise DivergenceError(f"image norm {norm_x:.3e} left the stable region at epoch "
+                                  f"{epoch}", last_good_epoch=epoch - 1, trace=trace)
+    # assemble the full image: owned entries from every rank
+    x_local = system.get_x()
+    mine = np.zeros(system.n_voxels)
+    for j in range(system.panel_begin, system.panel_end):
+        v = system.voxel_indices(j)
+        mine[v] = x_local[v]
+    t = torch.as_tensor(mine, device=f"cuda:{system.device}")
+    dist.all_reduce(t)
+    return t.cpu().numpy(), trace

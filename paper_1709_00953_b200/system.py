@@ -67,11 +67,14 @@ class DeviceBlockSystem:
         self.nnz = int(info[6])
         self.z_len = int(info[7])
         self._n_rows = {}
+        self._nnz = {}
         for j in range(self.panel_begin, self.panel_end):
             nr = ctypes.c_int64()
-            N.check(N.load().bct_panel_info(self._ctx, j, ctypes.byref(nr), None, None),
-                    self._ctx, "bct_panel_info")
+            nz = ctypes.c_int64()
+            N.check(N.load().bct_panel_info(self._ctx, j, ctypes.byref(nr), ctypes.byref(nz),
+                                            None), self._ctx, "bct_panel_info")
             self._n_rows[j] = nr.value
+            self._nnz[j] = nz.value
         self._y_norm = None
 
     # -- construction -------------------------------------------------------
@@ -175,6 +178,12 @@ class DeviceBlockSystem:
 
     def n_local_rows(self, j):
         return self._n_rows[j]
+
+    def _panel_nnz(self, j):
+        return self._nnz[j]
+
+    def x_len_owned(self):
+        return int(sum(self.col_sizes[j] for j in range(self.panel_begin, self.panel_end)))
 
     def owns(self, j):
         return self.panel_begin <= j < self.panel_end
