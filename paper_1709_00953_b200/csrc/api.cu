@@ -27,19 +27,18 @@ cudaError_t exclusive_scan_i32(const int32_t *, int32_t *, int64_t, void *, size
 cudaError_t pb_fill(int64_t, int64_t, int64_t, const double *, const double *, int64_t, int64_t,
                     const int32_t *, const int32_t *, int64_t, double *, int32_t *, cudaStream_t);
 cudaError_t pb_rbp(const int32_t *, int64_t, const int64_t *, int, int32_t *, cudaStream_t);
-cudaError_t build_csc(int, const double *, const int32_t *, const int32_t *, const int32_t *,
-                      const int32_t *, int, int32_t, int32_t, int64_t, void *, int32_t *,
-                      int32_t *, int32_t *, int32_t *, int32_t *, int32_t *, void *, size_t,
-                      cudaStream_t);
-cudaError_t convert_values(int, const double *, void *, int64_t, cudaStream_t);
+cudaError_t layout_panel(int, const double *, const int32_t *, const int32_t *, const int32_t *,
+                         const int32_t *, int, int32_t, int32_t, int64_t, void *, int32_t *,
+                         int32_t *, int32_t *, void *, int32_t *, int32_t *, int32_t *, int32_t *,
+                         int32_t *, int32_t *, int32_t *, int32_t *, void *, size_t, cudaStream_t);
 cudaError_t inv_count(const int32_t *, int32_t, int32_t *, cudaStream_t);
 cudaError_t inv_fill(const int32_t *, int32_t, int64_t, const int32_t *, int32_t *, int32_t *,
                      cudaStream_t);
-cudaError_t fill_z(int, const void *, const int32_t *, const int32_t *, const PanelDev *, int,
-                   int64_t, const double *, double *, cudaStream_t);
-cudaError_t forward(int, const void *, const int32_t *, const int32_t *, const PanelDev *, int,
-                    const int32_t *, const int32_t *, int64_t, const double *, double *,
-                    cudaStream_t);
+cudaError_t fill_z(int, const void *, const int32_t *, const int32_t *, const int32_t *,
+                   const PanelDev *, int, int64_t, const double *, double *, cudaStream_t);
+cudaError_t forward(int, const void *, const int32_t *, const int32_t *, const int32_t *,
+                    const PanelDev *, int, const int32_t *, const int32_t *, int64_t,
+                    const double *, double *, cudaStream_t);
 cudaError_t zsum(const int32_t *, const int32_t *, int64_t, const double *, double *,
                  cudaStream_t);
 cudaError_t sub(const double *, const double *, int64_t, double *, cudaStream_t);
@@ -79,8 +78,8 @@ struct bct_ctx {
     std::vector<int32_t> h_rbp;
     // device store
     void *vals = nullptr, *tvals = nullptr;
-    int32_t *cols = nullptr, *indptr = nullptr, *trows = nullptr, *cptr = nullptr;
-    int32_t *rbp = nullptr, *l2g = nullptr;
+    int32_t *cols = nullptr, *rptr = nullptr, *rlen = nullptr, *trows = nullptr;
+    int32_t *cptr = nullptr, *corder = nullptr, *rbp = nullptr, *l2g = nullptr;
     PanelDev *d_panels = nullptr;
     int32_t *inv_ptr = nullptr, *inv_z = nullptr, *d_rb_ptr = nullptr, *d_rb_rows = nullptr;
     int32_t *rb_of_row = nullptr;
@@ -276,12 +275,13 @@ int alloc_store(bct_ctx *c, const std::vector<int64_t> &rows, const std::vector<
                 const std::vector<int64_t> &ncols)
 {
     c->h_panels.resize(c->np);
-    int64_t vo = 0, ro = 0, xo = 0, co = 0;
+    int64_t vo = 0, to = 0, ro = 0, xo = 0, co = 0;
     for (int lp = 0; lp < c->np; ++lp) {
-        if (nnzs[lp] >= (1ll << 31) || rows[lp] >= (1ll << 31))
+        if (nnzs[lp] + 3 * (rows[lp] + ncols[lp]) >= (1ll << 31))
             return fail(c, BCT_EINVAL, "panel %d too large for 32-bit local indices", c->pb + lp);
         PanelDev &P = c->h_panels[lp];
-        P.val_off = vo;
+        P.fwd_off = vo;
+        P.csc_off = to;
         P.row_off = ro;
         P.x_off = xo;
         P.cptr_off = co;
@@ -289,7 +289,9 @@ int alloc_store(bct_ctx *c, const std::vector<int64_t> &rows, const std::vector<
         P.n_cols = (int32_t)ncols[lp];
         P.nnz = (int32_t)nnzs[lp];
         P.j = c->pb + lp;
-        vo += nnzs[lp];
+        // rows / columns padded to 4 entries; panel bases stay 4-entry aligned
+        vo += (nnzs[lp] + 3 * rows[lp] + 3) & ~3ll;
+        to += (nnzs[lp] + 3 * ncols[lp] + 3) & ~3ll;
         ro += rows[lp];
         xo += ncols[lp];
         co += ncols[lp] * (c->m + 1);
@@ -297,7 +299,8 @@ int alloc_store(bct_ctx *c, const std::vector<int64_t> &rows, const std::vector<
         c->max_cols = std::max(c->max_cols, ncols[lp]);
     }
     if (ro >= (1ll << 31)) return fail(c, BCT_EINVAL, "z store exceeds 2^31 rows");
-    c->nnz = vo;
+    c->nnz = 0;
+    for (int lp = 0; lp < c->np; ++lp) c->nnz += nnzs[lp];
     c->z_len = ro;
     c->x_len = xo;
     size_t vs = vsize(c);
@@ -307,38 +310,47 @@ int alloc_store(bct_ctx *c, const std::vector<int64_t> &rows, const std::vector<
         if (e != cudaSuccess) return fail(c, BCT_ENOMEM, "store values: %s", cudaGetErrorString(e));
         c->allocs.push_back(p);
         c->vals = p;
-        e = cudaMalloc(&p, std::max<size_t>(vs * vo, 8));
+        e = cudaMalloc(&p, std::max<size_t>(vs * to, 8));
         if (e != cudaSuccess) return fail(c, BCT_ENOMEM, "store values: %s", cudaGetErrorString(e));
         c->allocs.push_back(p);
         c->tvals = p;
     }
     DALLOC(c->cols, vo);
-    DALLOC(c->trows, vo);
-    DALLOC(c->indptr, ro + c->np);
+    DALLOC(c->trows, to);
+    DALLOC(c->rptr, ro + c->np);
+    DALLOC(c->rlen, ro);
     DALLOC(c->l2g, ro);
     DALLOC(c->cptr, co);
+    DALLOC(c->corder, xo);
     DALLOC(c->rbp, (int64_t)c->np * (c->m + 1));
     return 0;
 }
 
 struct BuildTmp {
     double *vals64 = nullptr;
-    int32_t *a = nullptr, *b = nullptr, *cc = nullptr, *d = nullptr;
+    int32_t *cols_c = nullptr, *indptr_c = nullptr;
+    int32_t *a = nullptr, *b = nullptr, *cc = nullptr, *d = nullptr, *e = nullptr, *f = nullptr;
     char *cub = nullptr;
     size_t cub_bytes = 0;
 };
 
-int alloc_build_tmp(bct_ctx *c, BuildTmp &t, int64_t max_nnz, int64_t scan_n)
+int alloc_build_tmp(bct_ctx *c, BuildTmp &t, int64_t max_nnz, int64_t max_dim)
 {
     DALLOC(t.vals64, max_nnz);
+    DALLOC(t.cols_c, max_nnz);
+    DALLOC(t.indptr_c, max_dim + 2);
     DALLOC(t.a, max_nnz);
     DALLOC(t.b, max_nnz);
     DALLOC(t.cc, max_nnz);
     DALLOC(t.d, max_nnz);
-    t.cub_bytes = std::max(bct::sort_temp_bytes(max_nnz), bct::scan_temp_bytes(scan_n));
+    DALLOC(t.e, max_dim + 2);
+    DALLOC(t.f, max_dim + 2);
+    t.cub_bytes = std::max(bct::sort_temp_bytes(max_nnz), bct::scan_temp_bytes(max_dim + 2));
     DALLOC(t.cub, (int64_t)t.cub_bytes);
     return 0;
 }
+
+void free_build_tmp(bct_ctx *c, BuildTmp &t);
 
 void free_tmp(bct_ctx *c, void *p)
 {
@@ -347,20 +359,49 @@ void free_tmp(bct_ctx *c, void *p)
     c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
 }
 
-// CSC + storage conversion of panel lp whose forward CSR (f64) sits in tmp.vals64.
-int finish_panel(bct_ctx *c, int lp, BuildTmp &t)
+void free_build_tmp(bct_ctx *c, BuildTmp &t)
+{
+    free_tmp(c, t.vals64); free_tmp(c, t.cols_c); free_tmp(c, t.indptr_c);
+    free_tmp(c, t.a); free_tmp(c, t.b); free_tmp(c, t.cc); free_tmp(c, t.d);
+    free_tmp(c, t.e); free_tmp(c, t.f); free_tmp(c, t.cub);
+}
+
+// Padded forward rows + padded CSC of panel lp from the compact forward CSR
+// in (vals64, cols_c, indptr_c); corder = processing order of its columns.
+int finish_panel(bct_ctx *c, int lp, BuildTmp &t, const int32_t *indptr_c,
+                 const std::vector<int32_t> &corder)
 {
     const PanelDev &P = c->h_panels[lp];
     size_t vs = vsize(c);
-    char *tv = (char *)c->tvals + vs * P.val_off;
-    CK(bct::build_csc(c->dtype, t.vals64, c->cols + P.val_off, c->indptr + P.row_off + lp,
-                      c->l2g + P.row_off, c->rbp + (int64_t)lp * (c->m + 1), c->m, P.n_rows,
-                      P.n_cols, P.nnz, tv, c->trows + P.val_off, c->cptr + P.cptr_off, t.a, t.b,
-                      t.cc, t.d, t.cub, t.cub_bytes, c->stream));
-    CK(bct::convert_values(c->dtype, t.vals64, (char *)c->vals + vs * P.val_off, P.nnz,
-                           c->stream));
+    CK(bct::layout_panel(c->dtype, t.vals64, t.cols_c, indptr_c, c->l2g + P.row_off,
+                         c->rbp + (int64_t)lp * (c->m + 1), c->m, P.n_rows, P.n_cols, P.nnz,
+                         (char *)c->vals + vs * P.fwd_off, c->cols + P.fwd_off,
+                         c->rptr + P.row_off + lp, c->rlen + P.row_off,
+                         (char *)c->tvals + vs * P.csc_off, c->trows + P.csc_off,
+                         c->cptr + P.cptr_off, t.a, t.b, t.cc, t.d, t.e, t.f, t.cub, t.cub_bytes,
+                         c->stream));
+    CK(cudaMemcpyAsync(c->corder + P.x_off, corder.data(), 4 * corder.size(),
+                       cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return 0;
+}
+
+// Column processing order: 4x4 voxel tiles of a (h x w) grid of local
+// columns c = ix*w + iy, so one CTA's 16 warps gather overlapping residual
+// rows (L1 reuse); identity when the block has no grid shape.
+std::vector<int32_t> tile_order(int64_t n_cols, int64_t h, int64_t w)
+{
+    std::vector<int32_t> o;
+    o.reserve(n_cols);
+    if (h <= 0 || w <= 0 || h * w != n_cols) {
+        for (int64_t q = 0; q < n_cols; ++q) o.push_back((int32_t)q);
+        return o;
+    }
+    for (int64_t tx = 0; tx < h; tx += 4)
+        for (int64_t ty = 0; ty < w; ty += 4)
+            for (int64_t a = tx; a < std::min(h, tx + 4); ++a)
+                for (int64_t b = ty; b < std::min(w, ty + 4); ++b) o.push_back((int32_t)(a * w + b));
+    return o;
 }
 
 void destroy(bct_ctx *c)
@@ -465,7 +506,8 @@ int bct_create(const bct_system_desc *d, const bct_panel *panels, bct_ctx **out)
     }
     if ((r = alloc_store(c, rows, nnzs, ncols))) return bail(r);
     BuildTmp t;
-    if ((r = alloc_build_tmp(c, t, max_nnz, 1))) return bail(r);
+    int64_t max_dim = std::max(c->max_rows, c->max_cols);
+    if ((r = alloc_build_tmp(c, t, max_nnz, max_dim))) return bail(r);
     for (int lp = 0; lp < c->np; ++lp) {
         const bct_panel &p = panels[lp];
         const PanelDev &P = c->h_panels[lp];
@@ -474,19 +516,17 @@ int bct_create(const bct_system_desc *d, const bct_panel *panels, bct_ctx **out)
         std::vector<int32_t> lg(p.l2g, p.l2g + p.n_rows);
         c->h_rbp.insert(c->h_rbp.end(), rb.begin(), rb.end());
         if (cudaMemcpy(t.vals64, p.data, 8 * p.nnz, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(c->cols + P.val_off, p.cols, 4 * p.nnz, cudaMemcpyHostToDevice) !=
+            cudaMemcpy(t.cols_c, p.cols, 4 * p.nnz, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(t.indptr_c, ip.data(), 4 * ip.size(), cudaMemcpyHostToDevice) !=
                 cudaSuccess ||
-            cudaMemcpy(c->indptr + P.row_off + lp, ip.data(), 4 * ip.size(),
-                       cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(c->rbp + (int64_t)lp * (c->m + 1), rb.data(), 4 * rb.size(),
                        cudaMemcpyHostToDevice) != cudaSuccess ||
             (p.n_rows > 0 && cudaMemcpy(c->l2g + P.row_off, lg.data(), 4 * lg.size(),
                                         cudaMemcpyHostToDevice) != cudaSuccess))
             return bail(fail(c, BCT_ECUDA, "panel upload failed"));
-        if ((r = finish_panel(c, lp, t))) return bail(r);
+        if ((r = finish_panel(c, lp, t, t.indptr_c, tile_order(P.n_cols, 0, 0)))) return bail(r);
     }
-    free_tmp(c, t.vals64); free_tmp(c, t.a); free_tmp(c, t.b); free_tmp(c, t.cc);
-    free_tmp(c, t.d); free_tmp(c, t.cub);
+    free_build_tmp(c, t);
     if ((r = finalize(c))) return bail(r);
     *out = c;
     return 0;
@@ -604,28 +644,26 @@ int bct_create_parallel_beam(const bct_pb_desc *d, bct_ctx **out)
             c->table_totals[j] += c->table_values[(int64_t)i * c->n_panels + j];
     if ((r = alloc_store(c, rows, nnzs, ncols))) return bail(r);
     BuildTmp t;
-    if ((r = alloc_build_tmp(c, t, max_nnz, 1))) return bail(r);
+    if ((r = alloc_build_tmp(c, t, max_nnz, std::max(c->max_rows, c->max_cols)))) return bail(r);
     c->h_rbp.resize((size_t)c->np * (c->m + 1));
     for (int lp = 0; lp < c->np; ++lp) {
         const PanelDev &P = c->h_panels[lp];
         int j = c->pb + lp;
         CK(cudaMemcpyAsync(c->l2g + P.row_off, p_l2g[lp], 4 * P.n_rows, cudaMemcpyDeviceToDevice,
                            c->stream));
-        CK(cudaMemcpyAsync(c->indptr + P.row_off + lp, p_ip[lp], 4 * (P.n_rows + 1),
-                           cudaMemcpyDeviceToDevice, c->stream));
         CK(bct::pb_fill(n, views, bins, d_cos, d_sin, xedge[j], xedge[j + 1], p_l2g[lp], p_ip[lp],
-                        P.n_rows, t.vals64, c->cols + P.val_off, c->stream));
+                        P.n_rows, t.vals64, t.cols_c, c->stream));
         CK(bct::pb_rbp(p_l2g[lp], P.n_rows, d_edges, c->m, c->rbp + (int64_t)lp * (c->m + 1),
                        c->stream));
         CK(cudaMemcpyAsync(c->h_rbp.data() + (size_t)lp * (c->m + 1),
                            c->rbp + (int64_t)lp * (c->m + 1), 4 * (c->m + 1),
                            cudaMemcpyDeviceToHost, c->stream));
-        if ((r = finish_panel(c, lp, t))) return bail(r);
+        if ((r = finish_panel(c, lp, t, p_ip[lp], tile_order(P.n_cols, xedge[j + 1] - xedge[j], n))))
+            return bail(r);
         free_tmp(c, p_l2g[lp]);
         free_tmp(c, p_ip[lp]);
     }
-    free_tmp(c, t.vals64); free_tmp(c, t.a); free_tmp(c, t.b); free_tmp(c, t.cc);
-    free_tmp(c, t.d); free_tmp(c, t.cub);
+    free_build_tmp(c, t);
     free_tmp(c, d_counts); free_tmp(c, d_flags); free_tmp(c, d_pos); free_tmp(c, cub);
     if ((r = finalize(c))) return bail(r);
     *out = c;
@@ -665,23 +703,32 @@ int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *i
     int lp = j - c->pb;
     const PanelDev &P = c->h_panels[lp];
     CK(cudaStreamSynchronize(c->stream));
-    if (data) {
-        if (c->dtype == BCT_F64) {
-            CK(cudaMemcpy(data, (double *)c->vals + P.val_off, 8 * P.nnz, cudaMemcpyDeviceToHost));
-        } else {
-            std::vector<float> f(P.nnz);
-            CK(cudaMemcpy(f.data(), (float *)c->vals + P.val_off, 4 * P.nnz,
-                          cudaMemcpyDeviceToHost));
-            for (int64_t q = 0; q < P.nnz; ++q) data[q] = f[q];
+    // compact the padded rows back to the reference layout
+    int64_t cap = (int64_t)P.nnz + 3 * (int64_t)P.n_rows;
+    std::vector<int32_t> rp(P.n_rows + 1), rl(std::max<int32_t>(P.n_rows, 1));
+    CK(cudaMemcpy(rp.data(), c->rptr + P.row_off + lp, 4 * (P.n_rows + 1), cudaMemcpyDeviceToHost));
+    if (P.n_rows > 0)
+        CK(cudaMemcpy(rl.data(), c->rlen + P.row_off, 4 * P.n_rows, cudaMemcpyDeviceToHost));
+    std::vector<double> dv(std::max<int64_t>(cap, 1));
+    std::vector<int32_t> cv(std::max<int64_t>(cap, 1));
+    if (c->dtype == BCT_F64) {
+        CK(cudaMemcpy(dv.data(), (double *)c->vals + P.fwd_off, 8 * cap, cudaMemcpyDeviceToHost));
+    } else {
+        std::vector<float> f(std::max<int64_t>(cap, 1));
+        CK(cudaMemcpy(f.data(), (float *)c->vals + P.fwd_off, 4 * cap, cudaMemcpyDeviceToHost));
+        for (int64_t q = 0; q < cap; ++q) dv[q] = f[q];
+    }
+    CK(cudaMemcpy(cv.data(), c->cols + P.fwd_off, 4 * cap, cudaMemcpyDeviceToHost));
+    int64_t o = 0;
+    for (int64_t lr = 0; lr < P.n_rows; ++lr) {
+        if (indptr) indptr[lr] = o;
+        for (int q = 0; q < rl[lr]; ++q, ++o) {
+            if (data) data[o] = dv[rp[lr] + q];
+            if (cols) cols[o] = cv[rp[lr] + q];
         }
     }
-    if (cols) CK(cudaMemcpy(cols, c->cols + P.val_off, 4 * P.nnz, cudaMemcpyDeviceToHost));
+    if (indptr) indptr[P.n_rows] = o;
     std::vector<int32_t> tmp(std::max<int64_t>(P.n_rows + 1, c->m + 1));
-    if (indptr) {
-        CK(cudaMemcpy(tmp.data(), c->indptr + P.row_off + lp, 4 * (P.n_rows + 1),
-                      cudaMemcpyDeviceToHost));
-        for (int64_t q = 0; q <= P.n_rows; ++q) indptr[q] = tmp[q];
-    }
     if (rbp)
         for (int i = 0; i <= c->m; ++i) rbp[i] = c->h_rbp[(size_t)lp * (c->m + 1) + i];
     if (l2g) {
@@ -829,8 +876,8 @@ int bct_commit_epoch(bct_ctx *c)
 int bct_fill_z_from_image(bct_ctx *c)
 {
     if (!c) return BCT_EINVAL;
-    CK(bct::fill_z(c->dtype, c->vals, c->cols, c->indptr, c->d_panels, c->np, c->z_len, c->x, c->z,
-                   c->stream));
+    CK(bct::fill_z(c->dtype, c->vals, c->cols, c->rptr, c->rlen, c->d_panels, c->np, c->z_len,
+                   c->x, c->z, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return 0;
 }
@@ -861,8 +908,9 @@ int bct_forward(bct_ctx *c, const double *x, double *y_out)
     CK(cudaMalloc((void **)&dx, 8 * std::max<int64_t>(c->x_len, 1)));
     int r = xvec_to_dev(c, x, dx);
     if (!r) {
-        cudaError_t e = bct::forward(c->dtype, c->vals, c->cols, c->indptr, c->d_panels, c->np,
-                                     c->inv_ptr, c->inv_z, c->n_meas, dx, c->vec, c->stream);
+        cudaError_t e = bct::forward(c->dtype, c->vals, c->cols, c->rptr, c->rlen, c->d_panels,
+                                     c->np, c->inv_ptr, c->inv_z, c->n_meas, dx, c->vec,
+                                     c->stream);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(y_out, c->vec, 8 * c->n_meas, cudaMemcpyDeviceToHost, c->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -908,8 +956,9 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, int32_t 
     CK(cudaEventRecord(c->staged, c->stream));
     EpochParams p;
     memset(&p, 0, sizeof p);
-    p.vals = c->vals; p.cols = c->cols; p.indptr = c->indptr; p.tvals = c->tvals;
-    p.trows = c->trows; p.cptr = c->cptr; p.rbp = c->rbp; p.panels = c->d_panels;
+    p.vals = c->vals; p.cols = c->cols; p.rptr = c->rptr; p.rlen = c->rlen; p.tvals = c->tvals;
+    p.trows = c->trows; p.cptr = c->cptr; p.corder = c->corder; p.rbp = c->rbp;
+    p.panels = c->d_panels;
     p.n_panels_owned = c->np; p.m = c->m; p.n_meas = c->n_meas; p.z_len = c->z_len;
     p.x_len = c->x_len; p.inv_ptr = c->inv_ptr; p.inv_z = c->inv_z; p.rb_ptr = c->d_rb_ptr;
     p.rb_rows = c->d_rb_rows; p.rb_of_row = c->rb_of_row; p.y = c->y; p.r = c->r; p.z = c->z;

@@ -137,6 +137,24 @@ __device__ __forceinline__ int run_row(const Runs &R, int f)
 template <typename V>
 __device__ __forceinline__ double ldv(const V *p) { return (double)__ldg(p); }
 
+// 4 consecutive values / indices from a 16-byte aligned position
+__device__ __forceinline__ void ld4v(const float *p, double v[4])
+{
+    float4 a = __ldg(reinterpret_cast<const float4 *>(p));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
+__device__ __forceinline__ void ld4v(const double *p, double v[4])
+{
+    double2 a = __ldg(reinterpret_cast<const double2 *>(p));
+    double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+__device__ __forceinline__ void ld4i(const int32_t *p, int k[4])
+{
+    int4 a = __ldg(reinterpret_cast<const int4 *>(p));
+    k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w;
+}
+
 __device__ __forceinline__ double z_value(double t, double ax, double mu, int status)
 {
     return status == 0 ? fma(mu, t, ax) : ax;
@@ -147,7 +165,8 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
 {
     __shared__ Runs R;
     __shared__ double sh[WARPS];
-    __shared__ double s_gg;
+    __shared__ TaskDev sT;
+    __shared__ PanelDev sP;
 
     const V *vals = static_cast<const V *>(p.vals);
     const V *tvals = static_cast<const V *>(p.tvals);
@@ -166,35 +185,44 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
     double *part_m = p.part + 2 * gridDim.x;
 
     for (int k = 0; k < n_tasks; ++k) {
-        const TaskDev T = p.tasks[k];
-        const PanelDev P = p.panels[T.lp];
+        __syncthreads();  // sT/sP/R of the previous task may still be in use
+        if (threadIdx.x == 0) {
+            sT = p.tasks[k];
+            sP = p.panels[sT.lp];
+        }
+        __syncthreads();
+        const TaskDev &T = sT;
+        const PanelDev &P = sP;
         const int32_t *rbp = p.rbp + (int64_t)T.lp * (m + 1);
         build_runs(T.mask, m, rbp, R);
         double2 *gx = reinterpret_cast<double2 *>(p.gx + (k & 1) * p.gx_stride);
         const double *xj = p.x + P.x_off;
 
         // ---- phase 1: g = A_I^T r_I over the panel CSC -------------------
+        // warp per voxel column, columns taken in 4x4-tile order (corder) so
+        // a CTA's warps gather overlapping r rows; 128-bit loads of 4 entries
         double wsum = 0.0;
         {
-            const V *tv = tvals + P.val_off;
-            const int32_t *tr = p.trows + P.val_off;
-            for (int c = gwarp; c < P.n_cols; c += nwarps) {
+            const V *tv = tvals + P.csc_off;
+            const int32_t *tr = p.trows + P.csc_off;
+            const int32_t *co = p.corder + P.x_off;
+            const double *rr = p.r;
+            for (int q = gwarp; q < P.n_cols; q += nwarps) {
+                const int c = __ldg(co + q);
                 const int32_t *cp = p.cptr + P.cptr_off + (int64_t)c * (m + 1);
                 double acc = 0.0;
-                for (int q = 0; q < R.n; ++q) {
-                    int s = __ldg(cp + R.i0[q]), e = __ldg(cp + R.i1[q]);
-                    int i = s + lane;
-                    for (; i + 96 < e; i += 128) {
-                        int r0 = __ldg(tr + i), r1 = __ldg(tr + i + 32);
-                        int r2 = __ldg(tr + i + 64), r3 = __ldg(tr + i + 96);
-                        double v0 = ldv(tv + i), v1 = ldv(tv + i + 32);
-                        double v2 = ldv(tv + i + 64), v3 = ldv(tv + i + 96);
-                        acc = fma(v0, p.r[r0], acc);
-                        acc = fma(v1, p.r[r1], acc);
-                        acc = fma(v2, p.r[r2], acc);
-                        acc = fma(v3, p.r[r3], acc);
+                for (int k2 = 0; k2 < R.n; ++k2) {
+                    const int s = __ldg(cp + R.i0[k2]), e = __ldg(cp + R.i1[k2]);
+#pragma unroll 2
+                    for (int i = (s & ~3) + 4 * lane; i < e; i += 128) {
+                        int rows[4];
+                        double v[4];
+                        ld4i(tr + i, rows);
+                        ld4v(tv + i, v);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (i + u >= s && i + u < e) acc = fma(v[u], rr[rows[u]], acc);
                     }
-                    for (; i < e; i += 32) acc = fma(ldv(tv + i), p.r[__ldg(tr + i)], acc);
                 }
                 acc = warp_sum(acc);
                 if (lane == 0) {
@@ -209,55 +237,55 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
         double gg = fixed_sum(part_gg, gridDim.x, sh);
 
         // ---- phase 2: dual SpMV t = A_I g, ax = A_I x_J -----------------
+        // 8 lanes per local row (4 rows per warp in flight), 4 entries per
+        // lane per step from 16-byte aligned rows, (g, x) gathered as one double2
         wsum = 0.0;
         const int n_task_rows = R.pre[R.n];
-        if (gg != 0.0) {
-            const V *fv = vals + P.val_off;
-            const int32_t *fc = p.cols + P.val_off;
-            const int32_t *ip = p.indptr + P.row_off + T.lp;
-            for (int f = gwarp; f < n_task_rows; f += nwarps) {
-                int lr = run_row(R, f);
-                int s = __ldg(ip + lr), e = __ldg(ip + lr + 1);
+        {
+            const V *fv = vals + P.fwd_off;
+            const int32_t *fc = p.cols + P.fwd_off;
+            const int32_t *rp = p.rptr + P.row_off + T.lp;
+            const int32_t *rl = p.rlen + P.row_off;
+            const int sub = lane >> 3, sl = lane & 7;
+            const unsigned smask = 0xffu << (sub * 8);
+            const bool grad = gg != 0.0;
+            for (int f = gwarp * 4 + sub; f < n_task_rows; f += nwarps * 4) {
+                const int lr = run_row(R, f);
+                const int s = __ldg(rp + lr), e = s + __ldg(rl + lr);
                 double t = 0.0, ax = 0.0;
-                int i = s + lane;
-                for (; i + 32 < e; i += 64) {
-                    int c0 = __ldg(fc + i), c1 = __ldg(fc + i + 32);
-                    double v0 = ldv(fv + i), v1 = ldv(fv + i + 32);
-                    double2 a0 = gx[c0], a1 = gx[c1];
-                    t = fma(v0, a0.x, t);
-                    ax = fma(v0, a0.y, ax);
-                    t = fma(v1, a1.x, t);
-                    ax = fma(v1, a1.y, ax);
+#pragma unroll 2
+                for (int i = s + 4 * sl; i < e; i += 32) {
+                    int cc[4];
+                    double v[4];
+                    ld4i(fc + i, cc);
+                    ld4v(fv + i, v);
+                    if (grad) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (i + u < e) {
+                                double2 a = gx[cc[u]];
+                                t = fma(v[u], a.x, t);
+                                ax = fma(v[u], a.y, ax);
+                            }
+                    } else {
+                        // zero gradient: only A_I x_J is needed (status 1)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (i + u < e) ax = fma(v[u], xj[cc[u]], ax);
+                    }
                 }
-                if (i < e) {
-                    int c0 = __ldg(fc + i);
-                    double v0 = ldv(fv + i);
-                    double2 a0 = gx[c0];
-                    t = fma(v0, a0.x, t);
-                    ax = fma(v0, a0.y, ax);
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) {
+                    t += __shfl_xor_sync(smask, t, o);
+                    ax += __shfl_xor_sync(smask, ax, o);
                 }
-                t = warp_sum(t);
-                ax = warp_sum(ax);
-                if (lane == 0) {
+                if (sl == 0) {
                     reinterpret_cast<double2 *>(p.t_ax)[lr] = make_double2(t, ax);
                     wsum = fma(t, t, wsum);
                 }
             }
-        } else {
-            // zero gradient: only A_I x_J is needed (z = A x_j, status 1)
-            const V *fv = vals + P.val_off;
-            const int32_t *fc = p.cols + P.val_off;
-            const int32_t *ip = p.indptr + P.row_off + T.lp;
-            for (int f = gwarp; f < n_task_rows; f += nwarps) {
-                int lr = run_row(R, f);
-                int s = __ldg(ip + lr), e = __ldg(ip + lr + 1);
-                double ax = 0.0;
-                for (int i = s + lane; i < e; i += 32) ax = fma(ldv(fv + i), xj[__ldg(fc + i)], ax);
-                ax = warp_sum(ax);
-                if (lane == 0) reinterpret_cast<double2 *>(p.t_ax)[lr] = make_double2(0.0, ax);
-            }
         }
-        bsum = block_sum_lane0(wsum, sh);
+        bsum = block_sum_all(wsum, sh);
         if (threadIdx.x == 0) part_den[blockIdx.x] = bsum;
         grid_sync(p.bar);
         double denom = fixed_sum(part_den, gridDim.x, sh);

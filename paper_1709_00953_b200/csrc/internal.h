@@ -19,10 +19,14 @@
 #define BCT_MASKW 4                 // up to 256 row blocks
 #define BCT_MAX_M (64 * BCT_MASKW)
 
+// Rows of the forward CSR and columns of the CSC start on 4-entry (16-byte
+// for int32/f32) boundaries so the kernels can use 128-bit loads; the
+// padding entries are never read as data (lengths mask them).
 struct PanelDev {
-    int64_t val_off;   // first entry of the panel in vals/cols/tvals/trows
-    int64_t row_off;   // first local row of the panel in z/l2g/scratch; indptr at row_off+lp
-    int64_t x_off;     // first voxel of the panel in x/xhat
+    int64_t fwd_off;   // first (padded) entry of the panel in vals/cols
+    int64_t csc_off;   // first (padded) entry of the panel in tvals/trows
+    int64_t row_off;   // first local row of the panel in z/l2g/rlen/scratch; rptr at row_off+lp
+    int64_t x_off;     // first voxel of the panel in x/xhat/corder
     int64_t cptr_off;  // start of the (|J|)*(m+1) segment table
     int32_t n_rows;
     int32_t n_cols;
@@ -61,10 +65,12 @@ struct EpochParams {
     // store
     const void *vals;          // double* or float*
     const int32_t *cols;
-    const int32_t *indptr;
+    const int32_t *rptr;       // padded row starts (panel-relative), n_rows+1 per panel
+    const int32_t *rlen;       // true row lengths
     const void *tvals;
     const int32_t *trows;
-    const int32_t *cptr;
+    const int32_t *cptr;       // absolute (panel-relative) CSC positions per (column, block)
+    const int32_t *corder;     // column processing order (2D voxel tiles)
     const int32_t *rbp;
     const PanelDev *panels;
     int32_t n_panels_owned;
