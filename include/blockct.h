@@ -185,6 +185,9 @@ int bct_wait_epoch(bct_ctx *ctx, bct_epoch_result *out, double *mus, int32_t *st
 /* Sharded parallel mode: the device exchange buffer holds
  * n_meas partial projection sums followed by x_sq and err_sq. */
 int bct_exchange_buffer(bct_ctx *ctx, double **dev_ptr, int64_t *len);
+/* Profiling only: per-block phase timestamps of the last epoch when the
+ * environment sets BCT_TIMELINE=1 ([task][6][grid] globaltimer ns). */
+int bct_debug_timeline(bct_ctx *ctx, long long *out, int64_t n_tasks, int32_t *grid);
 int bct_finish_sharded(bct_ctx *ctx, int32_t flags, double *resid_sq);
 
 #ifdef __cplusplus

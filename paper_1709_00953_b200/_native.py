@@ -13,7 +13,8 @@ import numpy as np
 
 from .errors import ConfigurationError, ExecutorError, NativeLibraryError, ScheduleError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libblockct_cuda.so")
+LIB_PATH = os.environ.get("BCT_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libblockct_cuda.so")
 
 BCT_OK, BCT_EINVAL, BCT_ECUDA, BCT_ENOMEM, BCT_ESCHEDULE = 0, -1, -2, -3, -4
 BCT_F64, BCT_F32 = 0, 1
@@ -83,6 +84,7 @@ _SIGS = {
     "bct_wait_epoch": [_p, ctypes.POINTER(EpochResult), _p, _p],
     "bct_exchange_buffer": [_p, _pp, ctypes.POINTER(_i64)],
     "bct_finish_sharded": [_p, _i32, _p],
+    "bct_debug_timeline": [_p, _p, _i64, _p],
 }
 
 EXPORTED = tuple(_SIGS) + ("bct_last_error", "bct_version")

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cuda_runtime.h>
 #include <string>
@@ -29,7 +30,8 @@ cudaError_t pb_fill(int64_t, int64_t, int64_t, const double *, const double *, i
 cudaError_t pb_rbp(const int32_t *, int64_t, const int64_t *, int, int32_t *, cudaStream_t);
 cudaError_t layout_panel(int, const double *, const int32_t *, const int32_t *, const int32_t *,
                          const int32_t *, int, int32_t, int32_t, int64_t, void *, int32_t *,
-                         int32_t *, int32_t *, void *, int32_t *, int32_t *, int32_t *, int32_t *,
+                         int32_t *, int32_t *, uint32_t *, void *, int32_t *, int32_t *, int32_t *,
+                         int32_t *,
                          int32_t *, int32_t *, int32_t *, int32_t *, void *, size_t, cudaStream_t);
 cudaError_t inv_count(const int32_t *, int32_t, int32_t *, cudaStream_t);
 cudaError_t inv_fill(const int32_t *, int32_t, int64_t, const int32_t *, int32_t *, int32_t *,
@@ -52,6 +54,7 @@ cudaError_t sharded_finish(const double *, const double *, int64_t, const int32_
 namespace {
 
 constexpr int RING = 4;
+constexpr int32_t UNIT_ENTRIES = 512;   // padded forward entries per row unit (phase 2)
 
 struct Slot {
     cudaEvent_t done = nullptr;
@@ -80,6 +83,9 @@ struct bct_ctx {
     void *vals = nullptr, *tvals = nullptr;
     int32_t *cols = nullptr, *rptr = nullptr, *rlen = nullptr, *trows = nullptr;
     int32_t *cptr = nullptr, *corder = nullptr, *rbp = nullptr, *l2g = nullptr;
+    uint32_t *vbits = nullptr;
+    int32_t *urow = nullptr, *uend = nullptr, *ubp = nullptr;
+    std::vector<int32_t> h_urow, h_uend, h_ubp;   // row units, built panel by panel
     PanelDev *d_panels = nullptr;
     int32_t *inv_ptr = nullptr, *inv_z = nullptr, *d_rb_ptr = nullptr, *d_rb_rows = nullptr;
     int32_t *rb_of_row = nullptr;
@@ -107,6 +113,8 @@ struct bct_ctx {
     bool has_x_true = false;
     uint64_t last_epoch_mask[BCT_MASKW] = {0, 0, 0, 0};
     std::vector<void *> allocs;
+    long long *timeline = nullptr;   // BCT_TIMELINE=1: [task][4][grid] globaltimer stamps
+    int64_t timeline_tasks = 0;
 };
 
 static std::string g_create_err;
@@ -289,8 +297,9 @@ int alloc_store(bct_ctx *c, const std::vector<int64_t> &rows, const std::vector<
         P.n_cols = (int32_t)ncols[lp];
         P.nnz = (int32_t)nnzs[lp];
         P.j = c->pb + lp;
-        // rows / columns padded to 4 entries; panel bases stay 4-entry aligned
-        vo += (nnzs[lp] + 3 * rows[lp] + 3) & ~3ll;
+        // rows / columns padded to 4 entries; forward panel bases 128-entry aligned
+        // (one row-start bitmap word per 128 entries), CSC bases 4-entry aligned
+        vo += (nnzs[lp] + 3 * rows[lp] + 127) & ~127ll;
         to += (nnzs[lp] + 3 * ncols[lp] + 3) & ~3ll;
         ro += rows[lp];
         xo += ncols[lp];
@@ -322,6 +331,9 @@ int alloc_store(bct_ctx *c, const std::vector<int64_t> &rows, const std::vector<
     DALLOC(c->l2g, ro);
     DALLOC(c->cptr, co);
     DALLOC(c->corder, xo);
+    DALLOC(c->vbits, vo / 128 + 1);
+    CK(cudaMemset(c->vbits, 0, 4 * (vo / 128 + 1)));
+    DALLOC(c->ubp, (int64_t)c->np * (c->m + 1));
     DALLOC(c->rbp, (int64_t)c->np * (c->m + 1));
     return 0;
 }
@@ -377,12 +389,47 @@ int finish_panel(bct_ctx *c, int lp, BuildTmp &t, const int32_t *indptr_c,
                          c->rbp + (int64_t)lp * (c->m + 1), c->m, P.n_rows, P.n_cols, P.nnz,
                          (char *)c->vals + vs * P.fwd_off, c->cols + P.fwd_off,
                          c->rptr + P.row_off + lp, c->rlen + P.row_off,
-                         (char *)c->tvals + vs * P.csc_off, c->trows + P.csc_off,
+                         c->vbits + P.fwd_off / 128, (char *)c->tvals + vs * P.csc_off,
+                         c->trows + P.csc_off,
                          c->cptr + P.cptr_off, t.a, t.b, t.cc, t.d, t.e, t.f, t.cub, t.cub_bytes,
                          c->stream));
     CK(cudaMemcpyAsync(c->corder + P.x_off, corder.data(), 4 * corder.size(),
                        cudaMemcpyHostToDevice, c->stream));
+    // row units: whole rows of one row block, ~UNIT_ENTRIES padded entries each
+    std::vector<int32_t> rp(P.n_rows + 1);
+    CK(cudaMemcpyAsync(rp.data(), c->rptr + P.row_off + lp, 4 * (P.n_rows + 1),
+                       cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    const int32_t *rb = c->h_rbp.data() + (size_t)lp * (c->m + 1);
+    c->h_panels[lp].unit_off = (int64_t)c->h_urow.size();
+    const int64_t base = (int64_t)c->h_urow.size();
+    std::vector<int32_t> ubp(c->m + 1);
+    for (int i = 0; i < c->m; ++i) {
+        ubp[i] = (int32_t)((int64_t)c->h_urow.size() - base);
+        int32_t r = rb[i];
+        while (r < rb[i + 1]) {
+            int32_t r1 = r + 1;
+            while (r1 < rb[i + 1] && rp[r1 + 1] - rp[r] <= UNIT_ENTRIES) ++r1;
+            c->h_urow.push_back(r);
+            c->h_uend.push_back(r1);
+            r = r1;
+        }
+    }
+    ubp[c->m] = (int32_t)((int64_t)c->h_urow.size() - base);
+    CK(cudaMemcpy(c->ubp + (int64_t)lp * (c->m + 1), ubp.data(), 4 * (c->m + 1),
+                  cudaMemcpyHostToDevice));
+    return 0;
+}
+
+// after every panel: upload the unit tables
+int upload_units(bct_ctx *c)
+{
+    DALLOC(c->urow, c->h_urow.size());
+    DALLOC(c->uend, c->h_uend.size());
+    if (!c->h_urow.empty()) {
+        CK(cudaMemcpy(c->urow, c->h_urow.data(), 4 * c->h_urow.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->uend, c->h_uend.data(), 4 * c->h_uend.size(), cudaMemcpyHostToDevice));
+    }
     return 0;
 }
 
@@ -527,6 +574,7 @@ int bct_create(const bct_system_desc *d, const bct_panel *panels, bct_ctx **out)
         if ((r = finish_panel(c, lp, t, t.indptr_c, tile_order(P.n_cols, 0, 0)))) return bail(r);
     }
     free_build_tmp(c, t);
+    if ((r = upload_units(c))) return bail(r);
     if ((r = finalize(c))) return bail(r);
     *out = c;
     return 0;
@@ -664,6 +712,7 @@ int bct_create_parallel_beam(const bct_pb_desc *d, bct_ctx **out)
         free_tmp(c, p_ip[lp]);
     }
     free_build_tmp(c, t);
+    if ((r = upload_units(c))) return bail(r);
     free_tmp(c, d_counts); free_tmp(c, d_flags); free_tmp(c, d_pos); free_tmp(c, cub);
     if ((r = finalize(c))) return bail(r);
     *out = c;
@@ -958,6 +1007,7 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, int32_t 
     memset(&p, 0, sizeof p);
     p.vals = c->vals; p.cols = c->cols; p.rptr = c->rptr; p.rlen = c->rlen; p.tvals = c->tvals;
     p.trows = c->trows; p.cptr = c->cptr; p.corder = c->corder; p.rbp = c->rbp;
+    p.vbits = c->vbits; p.urow = c->urow; p.uend = c->uend; p.ubp = c->ubp;
     p.panels = c->d_panels;
     p.n_panels_owned = c->np; p.m = c->m; p.n_meas = c->n_meas; p.z_len = c->z_len;
     p.x_len = c->x_len; p.inv_ptr = c->inv_ptr; p.inv_z = c->inv_z; p.rb_ptr = c->d_rb_ptr;
@@ -967,6 +1017,15 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, int32_t 
     p.hdr = c->d_hdr; p.tasks = c->d_tasks; p.gx = c->gx; p.gx_stride = 2 * c->max_cols;
     p.t_ax = c->t_ax; p.part = c->part; p.mus = c->mus; p.statuses = c->statuses; p.out = c->out;
     p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
+    p.timeline = nullptr;
+    if (getenv("BCT_TIMELINE") && n_tasks > 0) {
+        if (c->timeline_tasks < n_tasks) {
+            if (c->timeline) cudaFree(c->timeline);
+            CK(cudaMalloc((void **)&c->timeline, 8 * 6 * (size_t)n_tasks * c->grid));
+            c->timeline_tasks = n_tasks;
+        }
+        p.timeline = c->timeline;
+    }
     CK(cudaEventRecord(S.t0, c->stream));
     cudaError_t e;
     bct::launch_epoch(p, c->dtype, c->grid, c->block, c->stream, &e);
@@ -1090,6 +1149,18 @@ int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *status
     if (statuses) memcpy(statuses, S.h_status, 4 * S.n_tasks);
     S.pending = false;
     c->tail = (c->tail + 1) % RING;
+    return 0;
+}
+
+// Profiling: phase timestamps of the last epoch (BCT_TIMELINE=1), [task][6][grid].
+int bct_debug_timeline(bct_ctx *c, long long *out, int64_t n_tasks, int32_t *grid)
+{
+    if (!c || !grid) return BCT_EINVAL;
+    *grid = c->grid;
+    if (!c->timeline || !out) return 0;
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(out, c->timeline, 8 * 6 * (size_t)std::min(n_tasks, c->timeline_tasks) * c->grid,
+                  cudaMemcpyDeviceToHost));
     return 0;
 }
 

@@ -239,10 +239,21 @@ __global__ void pad_rows_kernel(const double *vals64, const int32_t *cols_c, con
         vals[d + (q - s)] = (V)vals64[q];
         cols[d + (q - s)] = cols_c[q];
     }
+    // padding: zero value on the row's last column (a gather it makes anyway)
+    const int32_t pc = e > s ? cols_c[e - 1] : 0;
     for (int q = d + (e - s); q < de; ++q) {
         vals[q] = (V)0;
-        cols[q] = 0;
+        cols[q] = pc;
     }
+}
+
+// one bit per 4-entry vector that starts a row (panel-relative words)
+__global__ void vbits_kernel(const int32_t *rptr, int32_t n_rows, uint32_t *vbits)
+{
+    int lr = blockIdx.x * blockDim.x + threadIdx.x;
+    if (lr >= n_rows) return;
+    uint32_t v = (uint32_t)rptr[lr] >> 2;
+    atomicOr(&vbits[v >> 5], 1u << (v & 31));
 }
 
 __global__ void row_of_entry_kernel(const int32_t *indptr, int32_t n_rows, int32_t *rowid)
@@ -309,9 +320,10 @@ __global__ void csc_pad_kernel(const int32_t *colstart, const int32_t *cpad, int
     int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= n_cols) return;
     int64_t d = cpad[c] + (colstart[c + 1] - colstart[c]);
+    const int32_t pr = d > cpad[c] ? trows[d - 1] : 0;  // zero value on the last row
     for (int64_t q = d; q < cpad[c + 1]; ++q) {
         tvals[q] = (V)0;
-        trows[q] = 0;
+        trows[q] = pr;
     }
 }
 
@@ -564,8 +576,8 @@ cudaError_t pb_rbp(const int32_t *d_l2g, int64_t n_hit, const int64_t *d_edges, 
 cudaError_t layout_panel(int dtype, const double *vals64, const int32_t *cols_c,
                          const int32_t *indptr_c, const int32_t *l2g, const int32_t *rbp, int m,
                          int32_t n_rows, int32_t n_cols, int64_t nnz, void *vals, int32_t *cols,
-                         int32_t *rptr, int32_t *rlen, void *tvals, int32_t *trows,
-                         int32_t *cptr, int32_t *tmp_a, int32_t *tmp_b, int32_t *tmp_c,
+                         int32_t *rptr, int32_t *rlen, uint32_t *vbits, void *tvals,
+                         int32_t *trows, int32_t *cptr, int32_t *tmp_a, int32_t *tmp_b, int32_t *tmp_c,
                          int32_t *tmp_d, int32_t *tmp_e, int32_t *tmp_f, void *d_cub,
                          size_t cub_bytes, cudaStream_t s)
 {
@@ -582,6 +594,7 @@ cudaError_t layout_panel(int dtype, const double *vals64, const int32_t *cols_c,
         else
             pad_rows_kernel<float><<<nblk(n_rows, 128), 128, 0, s>>>(
                 vals64, cols_c, indptr_c, rptr, n_rows, (float *)vals, cols);
+        vbits_kernel<<<nblk(n_rows, 256), 256, 0, s>>>(rptr, n_rows, vbits);
     }
     // CSC: stable radix sort of (column, entry): a column's entries stay in row order.
     // tmp_a = row of entry, tmp_b = iota, tmp_c = sorted cols, tmp_d = perm

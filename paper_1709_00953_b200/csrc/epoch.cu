@@ -28,8 +28,23 @@
 
 namespace {
 
-constexpr int BLOCK = 512;
+#ifndef BCT_BLOCK
+#define BCT_BLOCK 512
+#endif
+#ifndef BCT_MINB
+#define BCT_MINB 2
+#endif
+#ifndef BCT_UNROLL
+#define BCT_UNROLL 2
+#endif
+#ifndef BCT_P2_LANES
+#define BCT_P2_LANES 8
+#endif
+constexpr int BLOCK = BCT_BLOCK;
 constexpr int WARPS = BLOCK / 32;
+constexpr int P2L = BCT_P2_LANES;          // lanes per row in phase 2
+constexpr int P2R = 32 / P2L;              // rows per warp in flight
+constexpr int UNR = BCT_UNROLL;
 constexpr int MAX_RUNS = BCT_MAX_M / 2 + 1;
 
 __device__ __forceinline__ void grid_sync(unsigned int *bar)
@@ -47,6 +62,20 @@ __device__ __forceinline__ void grid_sync(unsigned int *bar)
     }
     __syncthreads();
 }
+
+__device__ __forceinline__ long long gtimer()
+{
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// optional per-block phase timestamps: [task][6][block] (profiling only)
+#define TL_MARK(k, ph)                                                               \
+    do {                                                                             \
+        if (p.timeline && threadIdx.x == 0)                                          \
+            p.timeline[((int64_t)(k) * 6 + (ph)) * gridDim.x + blockIdx.x] = gtimer(); \
+    } while (0)
 
 __device__ __forceinline__ double warp_sum(double v)
 {
@@ -101,14 +130,17 @@ struct Runs {
     int i1[MAX_RUNS];
     int rows0[MAX_RUNS];     // first local row of the run
     int pre[MAX_RUNS + 1];   // prefix of run row counts
+    int u0[MAX_RUNS];        // first row unit of the run
+    int upre[MAX_RUNS + 1];  // prefix of run unit counts
 };
 
 // Contiguous runs of set bits of a row-block mask, with their local row ranges.
-__device__ void build_runs(const uint64_t *mask, int m, const int32_t *rbp, Runs &R)
+__device__ void build_runs(const uint64_t *mask, int m, const int32_t *rbp, const int32_t *ubp,
+                           Runs &R)
 {
     __syncthreads();  // R of the previous task may still be in use
     if (threadIdx.x == 0) {
-        int n = 0, acc = 0;
+        int n = 0, acc = 0, uacc = 0;
         int i = 0;
         while (i < m) {
             if (!mask_has(mask, i)) { ++i; continue; }
@@ -119,12 +151,23 @@ __device__ void build_runs(const uint64_t *mask, int m, const int32_t *rbp, Runs
             R.rows0[n] = rbp[s];
             R.pre[n] = acc;
             acc += rbp[i] - rbp[s];
+            R.u0[n] = ubp[s];
+            R.upre[n] = uacc;
+            uacc += ubp[i] - ubp[s];
             ++n;
         }
         R.pre[n] = acc;
+        R.upre[n] = uacc;
         R.n = n;
     }
     __syncthreads();
+}
+
+__device__ __forceinline__ int run_unit(const Runs &R, int f)
+{
+    int k = 0;
+    while (f >= R.upre[k + 1]) ++k;
+    return R.u0[k] + (f - R.upre[k]);
 }
 
 __device__ __forceinline__ int run_row(const Runs &R, int f)
@@ -161,7 +204,7 @@ __device__ __forceinline__ double z_value(double t, double ax, double mu, int st
 }
 
 template <typename V>
-__global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
+__global__ void __launch_bounds__(BLOCK, BCT_MINB) epoch_kernel(EpochParams p)
 {
     __shared__ Runs R;
     __shared__ double sh[WARPS];
@@ -194,7 +237,8 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
         const TaskDev &T = sT;
         const PanelDev &P = sP;
         const int32_t *rbp = p.rbp + (int64_t)T.lp * (m + 1);
-        build_runs(T.mask, m, rbp, R);
+        build_runs(T.mask, m, rbp, p.ubp + (int64_t)T.lp * (m + 1), R);
+        TL_MARK(k, 0);
         double2 *gx = reinterpret_cast<double2 *>(p.gx + (k & 1) * p.gx_stride);
         const double *xj = p.x + P.x_off;
 
@@ -213,7 +257,7 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
                 double acc = 0.0;
                 for (int k2 = 0; k2 < R.n; ++k2) {
                     const int s = __ldg(cp + R.i0[k2]), e = __ldg(cp + R.i1[k2]);
-#pragma unroll 2
+#pragma unroll UNR
                     for (int i = (s & ~3) + 4 * lane; i < e; i += 128) {
                         int rows[4];
                         double v[4];
@@ -231,64 +275,115 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
                 }
             }
         }
+        TL_MARK(k, 1);
         double bsum = block_sum_lane0(wsum, sh);
         if (threadIdx.x == 0) part_gg[blockIdx.x] = bsum;
         grid_sync(p.bar);
         double gg = fixed_sum(part_gg, gridDim.x, sh);
+        TL_MARK(k, 2);
 
         // ---- phase 2: dual SpMV t = A_I g, ax = A_I x_J -----------------
-        // 8 lanes per local row (4 rows per warp in flight), 4 entries per
-        // lane per step from 16-byte aligned rows, (g, x) gathered as one double2
+        // The task's rows come in units of whole rows (~512 padded entries);
+        // a warp streams a unit 128 entries per step (one 4-entry vector per
+        // lane, 16-byte loads; rows are 4-aligned so a vector never straddles
+        // two rows).  Row boundaries come from the row-start bitmap; each step
+        // does a segmented warp reduction, the row left open at lane 31 keeps
+        // per-lane partials until it closes.  Fixed unit -> warp assignment
+        // and fixed reduction order: deterministic.
         wsum = 0.0;
         const int n_task_rows = R.pre[R.n];
         {
             const V *fv = vals + P.fwd_off;
             const int32_t *fc = p.cols + P.fwd_off;
             const int32_t *rp = p.rptr + P.row_off + T.lp;
-            const int32_t *rl = p.rlen + P.row_off;
-            const int sub = lane >> 3, sl = lane & 7;
-            const unsigned smask = 0xffu << (sub * 8);
-            const bool grad = gg != 0.0;
-            for (int f = gwarp * 4 + sub; f < n_task_rows; f += nwarps * 4) {
-                const int lr = run_row(R, f);
-                const int s = __ldg(rp + lr), e = s + __ldg(rl + lr);
-                double t = 0.0, ax = 0.0;
-#pragma unroll 2
-                for (int i = s + 4 * sl; i < e; i += 32) {
-                    int cc[4];
-                    double v[4];
-                    ld4i(fc + i, cc);
-                    ld4v(fv + i, v);
-                    if (grad) {
+            const uint32_t *vb = p.vbits + P.fwd_off / 128;
+            const int32_t *ur = p.urow + P.unit_off;
+            const int32_t *ue = p.uend + P.unit_off;
+            double2 *tax = reinterpret_cast<double2 *>(p.t_ax);
+            const int n_units = R.upre[R.n];
+            const unsigned le_mask = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+            for (int fu = gwarp; fu < n_units; fu += nwarps) {
+                const int u = run_unit(R, fu);
+                const int r0 = __ldg(ur + u), r1 = __ldg(ue + u);
+                const int E0 = __ldg(rp + r0), E1 = __ldg(rp + r1);
+                int open = r0 - 1;                 // row left open by the previous step
+                double pt = 0.0, pax = 0.0;        // per-lane partials of the open row
+                for (int b = E0 & ~127; b < E1; b += 128) {
+                    const int i = b + 4 * lane;
+                    double t = 0.0, ax = 0.0;
+                    if (i >= E0 && i < E1) {
+                        int cc[4];
+                        double v[4];
+                        ld4i(fc + i, cc);
+                        ld4v(fv + i, v);
 #pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (i + u < e) {
-                                double2 a = gx[cc[u]];
-                                t = fma(v[u], a.x, t);
-                                ax = fma(v[u], a.y, ax);
-                            }
-                    } else {
-                        // zero gradient: only A_I x_J is needed (status 1)
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (i + u < e) ax = fma(v[u], xj[cc[u]], ax);
+                        for (int q = 0; q < 4; ++q) {
+                            const double2 a = gx[cc[q]];
+                            t = fma(v[q], a.x, t);
+                            ax = fma(v[q], a.y, ax);
+                        }
                     }
-                }
+                    // bit l: vector (b/4 + l) starts a row; keep the unit's vectors
+                    uint32_t word = __ldg(vb + (b >> 7));
+                    const int nv = (E1 - b) >> 2;
+                    if (nv < 32) word &= (1u << nv) - 1u;
+                    if (b < E0) word &= ~((1u << ((E0 - b) >> 2)) - 1u);
+                    if (word == 0u) {              // the whole step continues the open row
+                        pt += t;
+                        pax += ax;
+                        continue;
+                    }
+                    const int rel = __popc(word & le_mask);   // 0: continues the open row
+                    if (rel == 0) {
+                        pt += t;
+                        pax += ax;
+                        t = 0.0;
+                        ax = 0.0;
+                    }
+                    // the open row closes in this step
+                    const double ot = warp_sum(pt), oax = warp_sum(pax);
+                    if (lane == 0 && open >= r0) {
+                        tax[open] = make_double2(ot, oax);
+                        wsum = fma(ot, ot, wsum);
+                    }
+                    // segmented inclusive scan over lanes keyed by rel
+                    const double t0 = t, ax0 = ax;
 #pragma unroll
-                for (int o = 4; o > 0; o >>= 1) {
-                    t += __shfl_xor_sync(smask, t, o);
-                    ax += __shfl_xor_sync(smask, ax, o);
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const double tt = __shfl_up_sync(0xffffffffu, t, o);
+                        const double aa = __shfl_up_sync(0xffffffffu, ax, o);
+                        const int rr = __shfl_up_sync(0xffffffffu, rel, o);
+                        if (lane >= o && rr == rel) {
+                            t += tt;
+                            ax += aa;
+                        }
+                    }
+                    const int rel31 = __popc(word);
+                    // rows fully inside the step end where the next vector starts a row
+                    if (rel > 0 && rel < rel31 && lane < 31 && ((word >> (lane + 1)) & 1u)) {
+                        tax[open + rel] = make_double2(t, ax);
+                        wsum = fma(t, t, wsum);
+                    }
+                    // the last segment stays open: keep its raw per-lane values
+                    const bool last = rel == rel31;
+                    pt = last ? t0 : 0.0;
+                    pax = last ? ax0 : 0.0;
+                    open += rel31;
                 }
-                if (sl == 0) {
-                    reinterpret_cast<double2 *>(p.t_ax)[lr] = make_double2(t, ax);
-                    wsum = fma(t, t, wsum);
+                // flush the row still open at the unit end
+                const double ot = warp_sum(pt), oax = warp_sum(pax);
+                if (lane == 0) {
+                    tax[open] = make_double2(ot, oax);
+                    wsum = fma(ot, ot, wsum);
                 }
             }
         }
+        TL_MARK(k, 3);
         bsum = block_sum_all(wsum, sh);
         if (threadIdx.x == 0) part_den[blockIdx.x] = bsum;
         grid_sync(p.bar);
         double denom = fixed_sum(part_den, gridDim.x, sh);
+        TL_MARK(k, 4);
 
         // ---- phase 3: step, x accumulation, z store, serial refresh -----
         double mu = 0.0;
@@ -349,6 +444,9 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
                 }
             }
             if (k + 1 < n_tasks) grid_sync(p.bar);
+        }
+        TL_MARK(k, 5);
+        {
         }
     }
 
@@ -445,7 +543,7 @@ int epoch_grid_size(int dtype, int device, int *block)
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<float>, BLOCK, 0);
     if (per < 1) per = 1;
-    if (per > 2) per = 2;
+    if (per > BCT_MINB) per = BCT_MINB;
     *block = BLOCK;
     return sms * per;
 }

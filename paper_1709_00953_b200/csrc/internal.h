@@ -28,6 +28,7 @@ struct PanelDev {
     int64_t row_off;   // first local row of the panel in z/l2g/rlen/scratch; rptr at row_off+lp
     int64_t x_off;     // first voxel of the panel in x/xhat/corder
     int64_t cptr_off;  // start of the (|J|)*(m+1) segment table
+    int64_t unit_off;  // first row unit of the panel in urow/uend
     int32_t n_rows;
     int32_t n_cols;
     int32_t nnz;
@@ -71,6 +72,10 @@ struct EpochParams {
     const int32_t *trows;
     const int32_t *cptr;       // absolute (panel-relative) CSC positions per (column, block)
     const int32_t *corder;     // column processing order (2D voxel tiles)
+    const uint32_t *vbits;     // row-start bit per 4-entry forward vector (word = fwd_off/128)
+    const int32_t *urow;       // row units: [urow[u], uend[u]) whole rows of one row block
+    const int32_t *uend;
+    const int32_t *ubp;        // (m+1) per panel: units of row block i = [ubp[i], ubp[i+1])
     const int32_t *rbp;
     const PanelDev *panels;
     int32_t n_panels_owned;
@@ -106,6 +111,7 @@ struct EpochParams {
     double *exchange;          // sharded: n_meas partial sums + 2
     unsigned int *bar;         // grid barrier word
     unsigned int *ticket;      // last-block counter
+    long long *timeline;       // optional phase timestamps (BCT_TIMELINE=1)
 };
 
 struct bct_ctx_s;

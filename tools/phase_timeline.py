@@ -1,0 +1,69 @@
+"""Profiling helper: per-phase timeline of the epoch kernel (BCT_TIMELINE=1).
+
+    BCT_TIMELINE=1 python tools/phase_timeline.py [--config 4] [--epochs 3]
+
+Prints, per task, the span of phase 1 (CSC SpMV^T), barrier 1, phase 2 (dual
+SpMV), barrier 2 and phase 3, in microseconds, plus the spread of the blocks'
+finish times (load imbalance)."""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("BCT_TIMELINE", "1")
+
+from paper_1709_00953_b200 import CONFIGS, DeviceBlockSystem, SamplingConfig, SolverParams  # noqa
+from paper_1709_00953_b200 import _native as N  # noqa
+from paper_1709_00953_b200.executor import pack_loops, submit, wait  # noqa
+from paper_1709_00953_b200.sampling import BlockScheduler  # noqa
+from paper_1709_00953_b200.solvers import SolverState, _loops  # noqa
+from paper_1709_00953_b200.geometry import random_ellipses, add_noise  # noqa
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--epochs", type=int, default=3)
+    a = ap.parse_args()
+    cfg = CONFIGS[a.config]
+    s = DeviceBlockSystem.parallel_beam(cfg.spec, dtype=cfg.dtype)
+    xt = random_ellipses(cfg.spec.n, cfg.n_ellipses, 0)
+    y, _ = add_noise(s.forward(xt), cfg.noise_frac, 1)
+    SolverState.initialize(s, y)
+    sch = BlockScheduler(s.table, SamplingConfig(alpha=cfg.alpha), cfg.group_size)
+    rng = np.random.default_rng(5)
+    for e in range(a.epochs):
+        packed = pack_loops(_loops(sch.epoch_plan(e + 1, rng), s.table, cfg.b), s)
+        submit(s, cfg.mode, packed, N.BCT_COMMIT | N.BCT_METRICS)
+        res = wait(s, packed.task_j.size)[0]
+    nt = packed.task_j.size
+    grid = ctypes.c_int32()
+    buf = np.zeros(6 * nt * 4096, dtype=np.int64)
+    N.check(N.load().bct_debug_timeline(s.ctx, N.ptr(buf), nt, ctypes.byref(grid)), s.ctx)
+    G = grid.value
+    tl = buf[:nt * 6 * G].reshape(nt, 6, G).astype(np.float64) / 1e3  # us
+    print(f"config {a.config}: kernel {res.kernel_ms:.3f} ms, {nt} tasks, grid {G}")
+    print("task  p1_span  p1_spread  bar1  p2_span  p2_spread  bar2  p3_span   total")
+    tot = np.zeros(7)
+    for k in range(nt):
+        t = tl[k]
+        start = t[0].min()
+        p1 = t[1].max() - start
+        sp1 = t[1].max() - t[1].min()
+        b1 = t[2].max() - t[1].max()
+        p2 = t[3].max() - t[2].min()
+        sp2 = t[3].max() - t[3].min()
+        b2 = t[4].max() - t[3].max()
+        p3 = t[5].max() - t[4].min()
+        row = np.array([p1, sp1, b1, p2, sp2, b2, p3])
+        tot += row
+        if k < 4 or k == nt - 1:
+            print(f"{k:4d} " + " ".join(f"{v:8.1f}" for v in row) + f" {t[5].max() - start:8.1f}")
+    print("mean " + " ".join(f"{v / nt:8.1f}" for v in tot))
+
+
+if __name__ == "__main__":
+    main()
