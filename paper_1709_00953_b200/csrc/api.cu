@@ -1,9 +1,10 @@
 // api.cu -- the C ABI of libblockct_cuda.so (include/blockct.h).
 //
-// Owns the device store, the state vectors and the per-epoch plan staging.
-// Every entry point validates its arguments on the host before touching the
-// device, so an invalid plan leaves the state untouched (executor.py:158-169:
-// "a failed batch leaves no trace").
+// Owns the device store (one layout per owned column panel, layout.cu), the
+// state vectors and the per-epoch plan staging.  Every entry point validates
+// its arguments on the host before touching the device, so an invalid plan
+// leaves the state untouched (executor.py:158-169: "a failed batch leaves no
+// trace").
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -23,23 +24,15 @@ cudaError_t pb_trace_counts(int64_t, int64_t, int64_t, const double *, const dou
 cudaError_t pb_compact(const int32_t *, int64_t, int32_t *, int32_t *, void *, size_t, int32_t *,
                        int32_t *, int64_t *, cudaStream_t);
 size_t scan_temp_bytes(int64_t);
-size_t sort_temp_bytes(int64_t);
 cudaError_t exclusive_scan_i32(const int32_t *, int32_t *, int64_t, void *, size_t, cudaStream_t);
 cudaError_t pb_fill(int64_t, int64_t, int64_t, const double *, const double *, int64_t, int64_t,
                     const int32_t *, const int32_t *, int64_t, double *, int32_t *, cudaStream_t);
 cudaError_t pb_rbp(const int32_t *, int64_t, const int64_t *, int, int32_t *, cudaStream_t);
-cudaError_t layout_panel(int, const double *, const int32_t *, const int32_t *, const int32_t *,
-                         const int32_t *, int, int32_t, int32_t, int64_t, void *, int32_t *,
-                         int32_t *, int32_t *, uint32_t *, void *, int32_t *, int32_t *, int32_t *,
-                         int32_t *,
-                         int32_t *, int32_t *, int32_t *, int32_t *, void *, size_t, cudaStream_t);
 cudaError_t inv_count(const int32_t *, int32_t, int32_t *, cudaStream_t);
 cudaError_t inv_fill(const int32_t *, int32_t, int64_t, const int32_t *, int32_t *, int32_t *,
                      cudaStream_t);
-cudaError_t fill_z(int, const void *, const int32_t *, const int32_t *, const int32_t *,
-                   const PanelDev *, int, int64_t, const double *, double *, cudaStream_t);
-cudaError_t forward(int, const void *, const int32_t *, const int32_t *, const int32_t *,
-                    const PanelDev *, int, const int32_t *, const int32_t *, int64_t,
+cudaError_t fill_z(int, const PanelDev *, int, int64_t, const double *, double *, cudaStream_t);
+cudaError_t forward(int, const PanelDev *, int, const int32_t *, const int32_t *, int64_t,
                     const double *, double *, cudaStream_t);
 cudaError_t zsum(const int32_t *, const int32_t *, int64_t, const double *, double *,
                  cudaStream_t);
@@ -54,7 +47,8 @@ cudaError_t sharded_finish(const double *, const double *, int64_t, const int32_
 namespace {
 
 constexpr int RING = 4;
-constexpr int32_t UNIT_ENTRIES = 512;   // padded forward entries per row unit (phase 2)
+constexpr int UNIT_ENTRIES = 512;   // padded forward entries per row unit (phase 2a)
+constexpr int ST_VOXELS = 4096;     // voxels per super tile (64 KB of (g, x) pairs)
 
 struct Slot {
     cudaEvent_t done = nullptr;
@@ -64,7 +58,6 @@ struct Slot {
     int32_t *h_status = nullptr;    // pinned [task_cap]
     int64_t n_tasks = 0, n_visits = 0;
     bool pending = false;
-    bool timed = false;
 };
 
 }  // namespace
@@ -72,30 +65,25 @@ struct Slot {
 struct bct_ctx {
     std::string err;
     int device = 0, dtype = 0, m = 0, n_panels = 0, pb = 0, pe = 0, np = 0;
-    int64_t n_meas = 0, n_vox = 0, nnz = 0, z_len = 0, x_len = 0, max_rows = 0, max_cols = 0;
+    int64_t n_meas = 0, n_vox = 0, nnz = 0, z_len = 0, x_len = 0;
+    int64_t max_rows = 0, max_cols = 0, max_seg = 0;
+    size_t smem = 0;
     cudaStream_t stream = nullptr;
     // host mirrors
     std::vector<PanelDev> h_panels;
+    std::vector<std::vector<int32_t>> h_d2c;   // per panel: device position -> local column
+    std::vector<std::vector<int32_t>> h_rbp;   // per panel
     std::vector<int64_t> col_ptr, col_vox, rb_ptr, rb_rows;
     std::vector<double> table_values, table_totals;
-    std::vector<int32_t> h_rbp;
-    // device store
-    void *vals = nullptr, *tvals = nullptr;
-    int32_t *cols = nullptr, *rptr = nullptr, *rlen = nullptr, *trows = nullptr;
-    int32_t *cptr = nullptr, *corder = nullptr, *rbp = nullptr, *l2g = nullptr;
-    uint32_t *vbits = nullptr;
-    int32_t *urow = nullptr, *uend = nullptr, *ubp = nullptr;
-    std::vector<int32_t> h_urow, h_uend, h_ubp;   // row units, built panel by panel
+    // device
     PanelDev *d_panels = nullptr;
     int32_t *inv_ptr = nullptr, *inv_z = nullptr, *d_rb_ptr = nullptr, *d_rb_rows = nullptr;
     int32_t *rb_of_row = nullptr;
-    // device state
     double *y = nullptr, *r = nullptr, *z = nullptr, *x = nullptr, *xhat = nullptr;
     double *x_true = nullptr;
     int32_t *counts = nullptr;
-    // scratch
-    double *gx = nullptr, *t_ax = nullptr, *part = nullptr, *mus = nullptr, *exchange = nullptr;
-    double *vec = nullptr;            // n_meas scratch
+    double *gx = nullptr, *t_ax = nullptr, *seg_part = nullptr, *part = nullptr;
+    double *mus = nullptr, *exchange = nullptr, *vec = nullptr;
     int32_t *statuses = nullptr;
     EpochOut *out = nullptr;
     unsigned int *bar = nullptr, *ticket = nullptr;
@@ -113,7 +101,7 @@ struct bct_ctx {
     bool has_x_true = false;
     uint64_t last_epoch_mask[BCT_MASKW] = {0, 0, 0, 0};
     std::vector<void *> allocs;
-    long long *timeline = nullptr;   // BCT_TIMELINE=1: [task][4][grid] globaltimer stamps
+    long long *timeline = nullptr;    // BCT_TIMELINE=1: [task][8][grid] globaltimer stamps
     int64_t timeline_tasks = 0;
 };
 
@@ -150,19 +138,122 @@ int dalloc(bct_ctx *c, T **p, int64_t n)
     return 0;
 }
 
-#define DALLOC(p, n)                          \
-    do {                                      \
+#define DALLOC(p, n)                            \
+    do {                                        \
         int _r = dalloc(c, &(p), (int64_t)(n)); \
-        if (_r) return _r;                    \
+        if (_r) return _r;                      \
     } while (0)
 
-int vsize(const bct_ctx *c) { return c->dtype == BCT_F64 ? 8 : 4; }
+void free_tmp(bct_ctx *c, void *p)
+{
+    if (!p) return;
+    cudaFree(p);
+    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+}
 
 int set_mask(uint64_t *mask, int i) { mask[i >> 6] |= 1ull << (i & 63); return 0; }
 
-// Common tail of context creation: state buffers, row-block tables, inverse map.
+// Voxel placement of a panel: device positions grouped into super tiles of
+// <= ST_VOXELS voxels and the phase-1 tile order (16 per tile).  A strip of
+// h x w voxels (local column c = ix*w + iy) is cut into iy ranges; inside a
+// super tile positions run over (ix, iy).  mdiv = w makes the reference
+// order (c ascending) = (ix, tile, iy).  Any other column block keeps its
+// order in chunks (mdiv = n_cols).
+struct Placement {
+    std::vector<int32_t> c2d, d2c, st_ptr, corder;
+    int32_t mdiv = 1;
+};
+
+Placement place_voxels(int64_t n_cols, int64_t h, int64_t w)
+{
+    Placement pl;
+    pl.c2d.resize(n_cols);
+    pl.d2c.resize(n_cols);
+    if (h > 0 && w > 0 && h * w == n_cols && h <= ST_VOXELS / 4) {
+        int64_t sw = std::max<int64_t>(4, (ST_VOXELS / h) & ~3ll);
+        int32_t d = 0;
+        for (int64_t y0 = 0; y0 < w; y0 += sw) {
+            pl.st_ptr.push_back(d);
+            int64_t y1 = std::min(w, y0 + sw);
+            for (int64_t ix = 0; ix < h; ++ix)
+                for (int64_t iy = y0; iy < y1; ++iy) {
+                    int32_t c = (int32_t)(ix * w + iy);
+                    pl.c2d[c] = d;
+                    pl.d2c[d] = c;
+                    ++d;
+                }
+        }
+        pl.st_ptr.push_back(d);
+        // 4x4 voxel tiles for phase 1
+        for (int64_t tx = 0; tx < h; tx += 4)
+            for (int64_t ty = 0; ty < w; ty += 4)
+                for (int64_t a = tx; a < std::min(h, tx + 4); ++a)
+                    for (int64_t b = ty; b < std::min(w, ty + 4); ++b)
+                        pl.corder.push_back(pl.c2d[a * w + b]);
+        pl.mdiv = (int32_t)w;
+    } else {
+        for (int64_t c = 0; c < n_cols; ++c) {
+            pl.c2d[c] = pl.d2c[c] = (int32_t)c;
+            pl.corder.push_back((int32_t)c);
+        }
+        for (int64_t d = 0; d < n_cols; d += ST_VOXELS) pl.st_ptr.push_back((int32_t)d);
+        pl.st_ptr.push_back((int32_t)n_cols);
+        pl.mdiv = (int32_t)std::max<int64_t>(n_cols, 1);
+    }
+    return pl;
+}
+
+// Lays out panel lp from its compact forward CSR on the device
+// (vals64/cols/indptr temporaries; l2g persistent), rbp on the host.
+int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *vals64,
+                const int32_t *cols, const int32_t *indptr, int32_t *l2g,
+                const std::vector<int32_t> &rbp, int64_t h, int64_t w)
+{
+    PanelDev &P = c->h_panels[lp];
+    const int j = c->pb + lp;
+    const int32_t n_cols = (int32_t)(c->col_ptr[j + 1] - c->col_ptr[j]);
+    Placement pl = place_voxels(n_cols, h, w);
+    int32_t *d_rbp = nullptr, *d_d2c = nullptr;
+    DALLOC(d_rbp, c->m + 1);
+    DALLOC(d_d2c, n_cols);
+    CK(cudaMemcpy(d_rbp, rbp.data(), 4 * (c->m + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_d2c, pl.d2c.data(), 4 * n_cols, cudaMemcpyHostToDevice));
+    std::string err;
+    if (bct::layout_panel_v2(c->dtype, c->m, n_rows, n_cols, nnz, vals64, cols, indptr, l2g, d_rbp,
+                             pl.c2d, pl.st_ptr, pl.corder, UNIT_ENTRIES, P, c->allocs, err,
+                             c->stream))
+        return fail(c, BCT_ENOMEM, "panel %d layout: %s", j, err.c_str());
+    P.rbp = d_rbp;
+    P.l2g = l2g;
+    P.d2c = d_d2c;
+    P.n_rows = n_rows;
+    P.n_cols = n_cols;
+    P.nnz = (int32_t)nnz;
+    P.j = j;
+    P.mdiv = pl.mdiv;
+    c->h_d2c[lp] = pl.d2c;
+    c->h_rbp[lp] = rbp;
+    c->nnz += nnz;
+    c->max_rows = std::max<int64_t>(c->max_rows, n_rows);
+    c->max_cols = std::max<int64_t>(c->max_cols, n_cols);
+    c->max_seg = std::max<int64_t>(c->max_seg, P.n_seg);
+    c->smem = std::max(c->smem, std::max<size_t>((size_t)P.band_max * 8, (size_t)P.st_max * 16));
+    return 0;
+}
+
+// Common tail of context creation: offsets, row-block tables, inverse map, state.
 int finalize(bct_ctx *c)
 {
+    int64_t ro = 0, xo = 0;
+    for (int lp = 0; lp < c->np; ++lp) {
+        c->h_panels[lp].row_off = ro;
+        c->h_panels[lp].x_off = xo;
+        ro += c->h_panels[lp].n_rows;
+        xo += c->h_panels[lp].n_cols;
+    }
+    if (ro >= (1ll << 31)) return fail(c, BCT_EINVAL, "z store exceeds 2^31 rows");
+    c->z_len = ro;
+    c->x_len = xo;
     // row blocks
     std::vector<int32_t> rbp32(c->rb_ptr.begin(), c->rb_ptr.end());
     std::vector<int32_t> rows32(c->rb_rows.begin(), c->rb_rows.end());
@@ -176,8 +267,6 @@ int finalize(bct_ctx *c)
     if (!rows32.empty())
         CK(cudaMemcpy(c->d_rb_rows, rows32.data(), 4 * rows32.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->rb_of_row, of_row.data(), 4 * of_row.size(), cudaMemcpyHostToDevice));
-
-    // panel table
     DALLOC(c->d_panels, c->np);
     CK(cudaMemcpy(c->d_panels, c->h_panels.data(), sizeof(PanelDev) * c->np,
                   cudaMemcpyHostToDevice));
@@ -190,20 +279,20 @@ int finalize(bct_ctx *c)
     DALLOC(fill, c->n_meas);
     CK(cudaMemsetAsync(cnt, 0, 4 * (c->n_meas + 1), c->stream));
     CK(cudaMemsetAsync(fill, 0, 4 * c->n_meas, c->stream));
-    for (int lp = 0; lp < c->np; ++lp) {
-        const PanelDev &P = c->h_panels[lp];
-        CK(bct::inv_count(c->l2g + P.row_off, P.n_rows, cnt, c->stream));
-    }
+    for (int lp = 0; lp < c->np; ++lp)
+        CK(bct::inv_count(c->h_panels[lp].l2g, c->h_panels[lp].n_rows, cnt, c->stream));
     size_t sb = bct::scan_temp_bytes(c->n_meas + 1);
     char *cub = nullptr;
     DALLOC(cub, (int64_t)sb);
     CK(bct::exclusive_scan_i32(cnt, c->inv_ptr, c->n_meas + 1, cub, sb, c->stream));
     for (int lp = 0; lp < c->np; ++lp) {
         const PanelDev &P = c->h_panels[lp];
-        CK(bct::inv_fill(c->l2g + P.row_off, P.n_rows, P.row_off, c->inv_ptr, fill, c->inv_z,
-                         c->stream));
+        CK(bct::inv_fill(P.l2g, P.n_rows, P.row_off, c->inv_ptr, fill, c->inv_z, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
+    free_tmp(c, cnt);
+    free_tmp(c, fill);
+    free_tmp(c, cub);
 
     // state and scratch
     DALLOC(c->y, c->n_meas);
@@ -217,7 +306,9 @@ int finalize(bct_ctx *c)
     DALLOC(c->counts, c->np);
     DALLOC(c->gx, 4 * c->max_cols);
     DALLOC(c->t_ax, 2 * c->max_rows);
-    c->grid = bct::epoch_grid_size(c->dtype, c->device, &c->block);
+    DALLOC(c->seg_part, 2 * c->max_seg + 2);
+    c->smem = std::max<size_t>(c->smem, 16);
+    c->grid = bct::epoch_grid_size(c->dtype, c->device, c->smem, &c->block);
     DALLOC(c->part, 8 * (int64_t)c->grid + 8);
     DALLOC(c->out, 1);
     DALLOC(c->bar, 1);
@@ -278,179 +369,6 @@ int check_common_desc(bct_ctx *c, int m, int n_panels, int pb, int pe, int dtype
     return 0;
 }
 
-// Allocates the store once panel sizes are known.
-int alloc_store(bct_ctx *c, const std::vector<int64_t> &rows, const std::vector<int64_t> &nnzs,
-                const std::vector<int64_t> &ncols)
-{
-    c->h_panels.resize(c->np);
-    int64_t vo = 0, to = 0, ro = 0, xo = 0, co = 0;
-    for (int lp = 0; lp < c->np; ++lp) {
-        if (nnzs[lp] + 3 * (rows[lp] + ncols[lp]) >= (1ll << 31))
-            return fail(c, BCT_EINVAL, "panel %d too large for 32-bit local indices", c->pb + lp);
-        PanelDev &P = c->h_panels[lp];
-        P.fwd_off = vo;
-        P.csc_off = to;
-        P.row_off = ro;
-        P.x_off = xo;
-        P.cptr_off = co;
-        P.n_rows = (int32_t)rows[lp];
-        P.n_cols = (int32_t)ncols[lp];
-        P.nnz = (int32_t)nnzs[lp];
-        P.j = c->pb + lp;
-        // rows / columns padded to 4 entries; forward panel bases 128-entry aligned
-        // (one row-start bitmap word per 128 entries), CSC bases 4-entry aligned
-        vo += (nnzs[lp] + 3 * rows[lp] + 127) & ~127ll;
-        to += (nnzs[lp] + 3 * ncols[lp] + 3) & ~3ll;
-        ro += rows[lp];
-        xo += ncols[lp];
-        co += ncols[lp] * (c->m + 1);
-        c->max_rows = std::max(c->max_rows, rows[lp]);
-        c->max_cols = std::max(c->max_cols, ncols[lp]);
-    }
-    if (ro >= (1ll << 31)) return fail(c, BCT_EINVAL, "z store exceeds 2^31 rows");
-    c->nnz = 0;
-    for (int lp = 0; lp < c->np; ++lp) c->nnz += nnzs[lp];
-    c->z_len = ro;
-    c->x_len = xo;
-    size_t vs = vsize(c);
-    {
-        void *p = nullptr;
-        cudaError_t e = cudaMalloc(&p, std::max<size_t>(vs * vo, 8));
-        if (e != cudaSuccess) return fail(c, BCT_ENOMEM, "store values: %s", cudaGetErrorString(e));
-        c->allocs.push_back(p);
-        c->vals = p;
-        e = cudaMalloc(&p, std::max<size_t>(vs * to, 8));
-        if (e != cudaSuccess) return fail(c, BCT_ENOMEM, "store values: %s", cudaGetErrorString(e));
-        c->allocs.push_back(p);
-        c->tvals = p;
-    }
-    DALLOC(c->cols, vo);
-    DALLOC(c->trows, to);
-    DALLOC(c->rptr, ro + c->np);
-    DALLOC(c->rlen, ro);
-    DALLOC(c->l2g, ro);
-    DALLOC(c->cptr, co);
-    DALLOC(c->corder, xo);
-    DALLOC(c->vbits, vo / 128 + 1);
-    CK(cudaMemset(c->vbits, 0, 4 * (vo / 128 + 1)));
-    DALLOC(c->ubp, (int64_t)c->np * (c->m + 1));
-    DALLOC(c->rbp, (int64_t)c->np * (c->m + 1));
-    return 0;
-}
-
-struct BuildTmp {
-    double *vals64 = nullptr;
-    int32_t *cols_c = nullptr, *indptr_c = nullptr;
-    int32_t *a = nullptr, *b = nullptr, *cc = nullptr, *d = nullptr, *e = nullptr, *f = nullptr;
-    char *cub = nullptr;
-    size_t cub_bytes = 0;
-};
-
-int alloc_build_tmp(bct_ctx *c, BuildTmp &t, int64_t max_nnz, int64_t max_dim)
-{
-    DALLOC(t.vals64, max_nnz);
-    DALLOC(t.cols_c, max_nnz);
-    DALLOC(t.indptr_c, max_dim + 2);
-    DALLOC(t.a, max_nnz);
-    DALLOC(t.b, max_nnz);
-    DALLOC(t.cc, max_nnz);
-    DALLOC(t.d, max_nnz);
-    DALLOC(t.e, max_dim + 2);
-    DALLOC(t.f, max_dim + 2);
-    t.cub_bytes = std::max(bct::sort_temp_bytes(max_nnz), bct::scan_temp_bytes(max_dim + 2));
-    DALLOC(t.cub, (int64_t)t.cub_bytes);
-    return 0;
-}
-
-void free_build_tmp(bct_ctx *c, BuildTmp &t);
-
-void free_tmp(bct_ctx *c, void *p)
-{
-    if (!p) return;
-    cudaFree(p);
-    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
-}
-
-void free_build_tmp(bct_ctx *c, BuildTmp &t)
-{
-    free_tmp(c, t.vals64); free_tmp(c, t.cols_c); free_tmp(c, t.indptr_c);
-    free_tmp(c, t.a); free_tmp(c, t.b); free_tmp(c, t.cc); free_tmp(c, t.d);
-    free_tmp(c, t.e); free_tmp(c, t.f); free_tmp(c, t.cub);
-}
-
-// Padded forward rows + padded CSC of panel lp from the compact forward CSR
-// in (vals64, cols_c, indptr_c); corder = processing order of its columns.
-int finish_panel(bct_ctx *c, int lp, BuildTmp &t, const int32_t *indptr_c,
-                 const std::vector<int32_t> &corder)
-{
-    const PanelDev &P = c->h_panels[lp];
-    size_t vs = vsize(c);
-    CK(bct::layout_panel(c->dtype, t.vals64, t.cols_c, indptr_c, c->l2g + P.row_off,
-                         c->rbp + (int64_t)lp * (c->m + 1), c->m, P.n_rows, P.n_cols, P.nnz,
-                         (char *)c->vals + vs * P.fwd_off, c->cols + P.fwd_off,
-                         c->rptr + P.row_off + lp, c->rlen + P.row_off,
-                         c->vbits + P.fwd_off / 128, (char *)c->tvals + vs * P.csc_off,
-                         c->trows + P.csc_off,
-                         c->cptr + P.cptr_off, t.a, t.b, t.cc, t.d, t.e, t.f, t.cub, t.cub_bytes,
-                         c->stream));
-    CK(cudaMemcpyAsync(c->corder + P.x_off, corder.data(), 4 * corder.size(),
-                       cudaMemcpyHostToDevice, c->stream));
-    // row units: whole rows of one row block, ~UNIT_ENTRIES padded entries each
-    std::vector<int32_t> rp(P.n_rows + 1);
-    CK(cudaMemcpyAsync(rp.data(), c->rptr + P.row_off + lp, 4 * (P.n_rows + 1),
-                       cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    const int32_t *rb = c->h_rbp.data() + (size_t)lp * (c->m + 1);
-    c->h_panels[lp].unit_off = (int64_t)c->h_urow.size();
-    const int64_t base = (int64_t)c->h_urow.size();
-    std::vector<int32_t> ubp(c->m + 1);
-    for (int i = 0; i < c->m; ++i) {
-        ubp[i] = (int32_t)((int64_t)c->h_urow.size() - base);
-        int32_t r = rb[i];
-        while (r < rb[i + 1]) {
-            int32_t r1 = r + 1;
-            while (r1 < rb[i + 1] && rp[r1 + 1] - rp[r] <= UNIT_ENTRIES) ++r1;
-            c->h_urow.push_back(r);
-            c->h_uend.push_back(r1);
-            r = r1;
-        }
-    }
-    ubp[c->m] = (int32_t)((int64_t)c->h_urow.size() - base);
-    CK(cudaMemcpy(c->ubp + (int64_t)lp * (c->m + 1), ubp.data(), 4 * (c->m + 1),
-                  cudaMemcpyHostToDevice));
-    return 0;
-}
-
-// after every panel: upload the unit tables
-int upload_units(bct_ctx *c)
-{
-    DALLOC(c->urow, c->h_urow.size());
-    DALLOC(c->uend, c->h_uend.size());
-    if (!c->h_urow.empty()) {
-        CK(cudaMemcpy(c->urow, c->h_urow.data(), 4 * c->h_urow.size(), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(c->uend, c->h_uend.data(), 4 * c->h_uend.size(), cudaMemcpyHostToDevice));
-    }
-    return 0;
-}
-
-// Column processing order: 4x4 voxel tiles of a (h x w) grid of local
-// columns c = ix*w + iy, so one CTA's 16 warps gather overlapping residual
-// rows (L1 reuse); identity when the block has no grid shape.
-std::vector<int32_t> tile_order(int64_t n_cols, int64_t h, int64_t w)
-{
-    std::vector<int32_t> o;
-    o.reserve(n_cols);
-    if (h <= 0 || w <= 0 || h * w != n_cols) {
-        for (int64_t q = 0; q < n_cols; ++q) o.push_back((int32_t)q);
-        return o;
-    }
-    for (int64_t tx = 0; tx < h; tx += 4)
-        for (int64_t ty = 0; ty < w; ty += 4)
-            for (int64_t a = tx; a < std::min(h, tx + 4); ++a)
-                for (int64_t b = ty; b < std::min(w, ty + 4); ++b) o.push_back((int32_t)(a * w + b));
-    return o;
-}
-
 void destroy(bct_ctx *c)
 {
     if (!c) return;
@@ -459,6 +377,7 @@ void destroy(bct_ctx *c)
     if (c->d_tasks) cudaFree(c->d_tasks);
     if (c->mus) cudaFree(c->mus);
     if (c->statuses) cudaFree(c->statuses);
+    if (c->timeline) cudaFree(c->timeline);
     if (c->h_tasks) cudaFreeHost(c->h_tasks);
     if (c->h_hdr) cudaFreeHost(c->h_hdr);
     for (int s = 0; s < RING; ++s) {
@@ -475,7 +394,7 @@ void destroy(bct_ctx *c)
     delete c;
 }
 
-int init_ctx(bct_ctx *c, int device)
+int init_ctx(bct_ctx *c, int device, int np)
 {
     c->device = device;
     CK(cudaSetDevice(device));
@@ -483,6 +402,9 @@ int init_ctx(bct_ctx *c, int device)
     int coop = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
     if (!coop) return fail(c, BCT_ECUDA, "device %d lacks cooperative launch", device);
+    c->h_panels.assign(np, PanelDev{});
+    c->h_d2c.resize(np);
+    c->h_rbp.resize(np);
     return 0;
 }
 
@@ -495,7 +417,7 @@ const char *bct_last_error(const bct_ctx *ctx)
     return ctx ? ctx->err.c_str() : g_create_err.c_str();
 }
 
-int bct_version(void) { return 1; }
+int bct_version(void) { return 2; }
 
 int bct_create(const bct_system_desc *d, const bct_panel *panels, bct_ctx **out)
 {
@@ -509,7 +431,7 @@ int bct_create(const bct_system_desc *d, const bct_panel *panels, bct_ctx **out)
         destroy(c);
         return code;
     };
-    if ((r = init_ctx(c, d->device))) return bail(r);
+    if ((r = init_ctx(c, d->device, d->panel_end - d->panel_begin))) return bail(r);
     c->dtype = d->dtype;
     c->m = d->m;
     c->n_panels = d->n_panels;
@@ -531,50 +453,52 @@ int bct_create(const bct_system_desc *d, const bct_panel *panels, bct_ctx **out)
         if (g < 0 || g >= c->n_meas) return bail(fail(c, BCT_EINVAL, "row block id out of range"));
     for (int64_t v : c->col_vox)
         if (v < 0 || v >= c->n_vox) return bail(fail(c, BCT_EINVAL, "voxel id out of range"));
-
-    std::vector<int64_t> rows(c->np), nnzs(c->np), ncols(c->np);
-    int64_t max_nnz = 1;
+    int64_t max_nnz = 1, max_rows = 1;
     for (int lp = 0; lp < c->np; ++lp) {
         const bct_panel &p = panels[lp];
         int j = c->pb + lp;
-        rows[lp] = p.n_rows;
-        nnzs[lp] = p.nnz;
-        ncols[lp] = c->col_ptr[j + 1] - c->col_ptr[j];
+        int64_t ncols = c->col_ptr[j + 1] - c->col_ptr[j];
         if (p.n_rows < 0 || p.nnz < 0 || p.indptr[p.n_rows] != p.nnz || p.rbp[c->m] != p.n_rows ||
             p.rbp[0] != 0)
             return bail(fail(c, BCT_EINVAL, "panel %d: inconsistent indptr/rbp", j));
+        if (p.nnz >= (1ll << 30) || ncols >= (1ll << 24))
+            return bail(fail(c, BCT_EINVAL, "panel %d too large", j));
         for (int64_t q = 0; q < p.nnz; ++q)
-            if (p.cols[q] < 0 || p.cols[q] >= ncols[lp])
+            if (p.cols[q] < 0 || p.cols[q] >= ncols)
                 return bail(fail(c, BCT_EINVAL, "panel %d: column id out of range", j));
         for (int64_t q = 0; q < p.n_rows; ++q)
             if (p.l2g[q] < 0 || p.l2g[q] >= c->n_meas)
                 return bail(fail(c, BCT_EINVAL, "panel %d: l2g out of range", j));
         max_nnz = std::max(max_nnz, p.nnz);
+        max_rows = std::max(max_rows, p.n_rows);
     }
-    if ((r = alloc_store(c, rows, nnzs, ncols))) return bail(r);
-    BuildTmp t;
-    int64_t max_dim = std::max(c->max_rows, c->max_cols);
-    if ((r = alloc_build_tmp(c, t, max_nnz, max_dim))) return bail(r);
+    double *vals64 = nullptr;
+    int32_t *cols = nullptr, *indptr = nullptr;
+    {
+        bct_ctx *cc = c;
+        if (dalloc(cc, &vals64, max_nnz) || dalloc(cc, &cols, max_nnz) ||
+            dalloc(cc, &indptr, max_rows + 1))
+            return bail(BCT_ENOMEM);
+    }
     for (int lp = 0; lp < c->np; ++lp) {
         const bct_panel &p = panels[lp];
-        const PanelDev &P = c->h_panels[lp];
         std::vector<int32_t> ip(p.indptr, p.indptr + p.n_rows + 1);
         std::vector<int32_t> rb(p.rbp, p.rbp + c->m + 1);
         std::vector<int32_t> lg(p.l2g, p.l2g + p.n_rows);
-        c->h_rbp.insert(c->h_rbp.end(), rb.begin(), rb.end());
-        if (cudaMemcpy(t.vals64, p.data, 8 * p.nnz, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(t.cols_c, p.cols, 4 * p.nnz, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(t.indptr_c, ip.data(), 4 * ip.size(), cudaMemcpyHostToDevice) !=
-                cudaSuccess ||
-            cudaMemcpy(c->rbp + (int64_t)lp * (c->m + 1), rb.data(), 4 * rb.size(),
-                       cudaMemcpyHostToDevice) != cudaSuccess ||
-            (p.n_rows > 0 && cudaMemcpy(c->l2g + P.row_off, lg.data(), 4 * lg.size(),
-                                        cudaMemcpyHostToDevice) != cudaSuccess))
+        int32_t *l2g = nullptr;
+        if (dalloc(c, &l2g, p.n_rows)) return bail(BCT_ENOMEM);
+        if (cudaMemcpy(vals64, p.data, 8 * p.nnz, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(cols, p.cols, 4 * p.nnz, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(indptr, ip.data(), 4 * ip.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            (p.n_rows > 0 &&
+             cudaMemcpy(l2g, lg.data(), 4 * lg.size(), cudaMemcpyHostToDevice) != cudaSuccess))
             return bail(fail(c, BCT_ECUDA, "panel upload failed"));
-        if ((r = finish_panel(c, lp, t, t.indptr_c, tile_order(P.n_cols, 0, 0)))) return bail(r);
+        if ((r = build_panel(c, lp, (int32_t)p.n_rows, p.nnz, vals64, cols, indptr, l2g, rb, 0, 0)))
+            return bail(r);
     }
-    free_build_tmp(c, t);
-    if ((r = upload_units(c))) return bail(r);
+    free_tmp(c, vals64);
+    free_tmp(c, cols);
+    free_tmp(c, indptr);
     if ((r = finalize(c))) return bail(r);
     *out = c;
     return 0;
@@ -595,7 +519,7 @@ int bct_create_parallel_beam(const bct_pb_desc *d, bct_ctx **out)
         destroy(c);
         return code;
     };
-    if ((r = init_ctx(c, d->device))) return bail(r);
+    if ((r = init_ctx(c, d->device, d->panel_end - d->panel_begin))) return bail(r);
     const int64_t n = d->n, views = d->views, bins = d->bins;
     c->dtype = d->dtype;
     c->m = d->m;
@@ -606,10 +530,9 @@ int bct_create_parallel_beam(const bct_pb_desc *d, bct_ctx **out)
     c->n_meas = views * bins;
     c->n_vox = n * n;
     if (c->n_meas >= (1ll << 31)) return bail(fail(c, BCT_EINVAL, "too many measurements"));
-    // partition
+    // partition: numpy round(linspace(0, views, m+1)), half-even
     std::vector<int64_t> aedge(c->m + 1), xedge(c->n_panels + 1);
     {
-        // numpy: round(linspace(0, views, m+1)); linspace computes i*step
         double step = (double)views / c->m;
         for (int i = 0; i <= c->m; ++i) {
             double v = (i == c->m) ? (double)views : i * step;
@@ -649,7 +572,7 @@ int bct_create_parallel_beam(const bct_pb_desc *d, bct_ctx **out)
     // pass 1: every panel (the density table needs all of them), per-ray counts
     std::vector<int32_t> h_counts(c->n_meas);
     c->table_values.assign((int64_t)c->m * c->n_panels, 0.0);
-    std::vector<int64_t> rows(c->np), nnzs(c->np), ncols(c->np);
+    std::vector<int64_t> rows(c->np), nnzs(c->np);
     std::vector<int32_t *> p_l2g(c->np, nullptr), p_ip(c->np, nullptr);
     int64_t max_nnz = 1;
     for (int j = 0; j < c->n_panels; ++j) {
@@ -682,38 +605,39 @@ int bct_create_parallel_beam(const bct_pb_desc *d, bct_ctx **out)
         free_tmp(c, rowlen);
         rows[lp] = n_hit;
         nnzs[lp] = tot;
-        ncols[lp] = vox_j;
         max_nnz = std::max(max_nnz, tot);
+        if (tot >= (1ll << 30)) return bail(fail(c, BCT_EINVAL, "panel %d too large", j));
     }
     c->table_totals.assign(c->n_panels, 0.0);
     // totals = values.sum(axis=0): numpy reduces axis 0 row by row
     for (int i = 0; i < c->m; ++i)
         for (int j = 0; j < c->n_panels; ++j)
             c->table_totals[j] += c->table_values[(int64_t)i * c->n_panels + j];
-    if ((r = alloc_store(c, rows, nnzs, ncols))) return bail(r);
-    BuildTmp t;
-    if ((r = alloc_build_tmp(c, t, max_nnz, std::max(c->max_rows, c->max_cols)))) return bail(r);
-    c->h_rbp.resize((size_t)c->np * (c->m + 1));
+    free_tmp(c, d_counts);
+    free_tmp(c, d_flags);
+    free_tmp(c, d_pos);
+    double *vals64 = nullptr;
+    int32_t *cols = nullptr, *rbp_tmp = nullptr;
+    DALLOC(vals64, max_nnz);
+    DALLOC(cols, max_nnz);
+    DALLOC(rbp_tmp, c->m + 1);
     for (int lp = 0; lp < c->np; ++lp) {
-        const PanelDev &P = c->h_panels[lp];
         int j = c->pb + lp;
-        CK(cudaMemcpyAsync(c->l2g + P.row_off, p_l2g[lp], 4 * P.n_rows, cudaMemcpyDeviceToDevice,
-                           c->stream));
         CK(bct::pb_fill(n, views, bins, d_cos, d_sin, xedge[j], xedge[j + 1], p_l2g[lp], p_ip[lp],
-                        P.n_rows, t.vals64, t.cols_c, c->stream));
-        CK(bct::pb_rbp(p_l2g[lp], P.n_rows, d_edges, c->m, c->rbp + (int64_t)lp * (c->m + 1),
-                       c->stream));
-        CK(cudaMemcpyAsync(c->h_rbp.data() + (size_t)lp * (c->m + 1),
-                           c->rbp + (int64_t)lp * (c->m + 1), 4 * (c->m + 1),
-                           cudaMemcpyDeviceToHost, c->stream));
-        if ((r = finish_panel(c, lp, t, p_ip[lp], tile_order(P.n_cols, xedge[j + 1] - xedge[j], n))))
+                        rows[lp], vals64, cols, c->stream));
+        CK(bct::pb_rbp(p_l2g[lp], rows[lp], d_edges, c->m, rbp_tmp, c->stream));
+        std::vector<int32_t> rb(c->m + 1);
+        CK(cudaMemcpyAsync(rb.data(), rbp_tmp, 4 * (c->m + 1), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if ((r = build_panel(c, lp, (int32_t)rows[lp], nnzs[lp], vals64, cols, p_ip[lp], p_l2g[lp],
+                             rb, xedge[j + 1] - xedge[j], n)))
             return bail(r);
-        free_tmp(c, p_l2g[lp]);
         free_tmp(c, p_ip[lp]);
     }
-    free_build_tmp(c, t);
-    if ((r = upload_units(c))) return bail(r);
-    free_tmp(c, d_counts); free_tmp(c, d_flags); free_tmp(c, d_pos); free_tmp(c, cub);
+    free_tmp(c, vals64);
+    free_tmp(c, cols);
+    free_tmp(c, rbp_tmp);
+    free_tmp(c, cub);
     if ((r = finalize(c))) return bail(r);
     *out = c;
     return 0;
@@ -744,6 +668,8 @@ int bct_panel_info(const bct_ctx *c, int32_t j, int64_t *n_rows, int64_t *nnz, i
     return 0;
 }
 
+// The panel back in the reference's cached layout (projector.py:474-488):
+// rows in local order, entries in ascending local column.
 int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *indptr,
                   int64_t *rbp, int64_t *l2g)
 {
@@ -752,38 +678,54 @@ int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *i
     int lp = j - c->pb;
     const PanelDev &P = c->h_panels[lp];
     CK(cudaStreamSynchronize(c->stream));
-    // compact the padded rows back to the reference layout
-    int64_t cap = (int64_t)P.nnz + 3 * (int64_t)P.n_rows;
-    std::vector<int32_t> rp(P.n_rows + 1), rl(std::max<int32_t>(P.n_rows, 1));
-    CK(cudaMemcpy(rp.data(), c->rptr + P.row_off + lp, 4 * (P.n_rows + 1), cudaMemcpyDeviceToHost));
-    if (P.n_rows > 0)
-        CK(cudaMemcpy(rl.data(), c->rlen + P.row_off, 4 * P.n_rows, cudaMemcpyDeviceToHost));
-    std::vector<double> dv(std::max<int64_t>(cap, 1));
-    std::vector<int32_t> cv(std::max<int64_t>(cap, 1));
+    const int64_t cap = std::max<int64_t>(P.fwd_cap, 1);
+    std::vector<double> fv(cap);
+    std::vector<uint16_t> fi(cap);
+    std::vector<int32_t> ss(P.n_seg + 1), sk(P.n_seg + 1), rp(P.n_rows + 1), rs(P.n_seg + 1),
+        stp(P.n_st + 1), lg(std::max(P.n_rows, 1));
     if (c->dtype == BCT_F64) {
-        CK(cudaMemcpy(dv.data(), (double *)c->vals + P.fwd_off, 8 * cap, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(fv.data(), P.fvals, 8 * P.fwd_cap, cudaMemcpyDeviceToHost));
     } else {
-        std::vector<float> f(std::max<int64_t>(cap, 1));
-        CK(cudaMemcpy(f.data(), (float *)c->vals + P.fwd_off, 4 * cap, cudaMemcpyDeviceToHost));
-        for (int64_t q = 0; q < cap; ++q) dv[q] = f[q];
+        std::vector<float> f(cap);
+        CK(cudaMemcpy(f.data(), P.fvals, 4 * P.fwd_cap, cudaMemcpyDeviceToHost));
+        for (int64_t q = 0; q < P.fwd_cap; ++q) fv[q] = f[q];
     }
-    CK(cudaMemcpy(cv.data(), c->cols + P.fwd_off, 4 * cap, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(fi.data(), P.fidx, 2 * P.fwd_cap, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ss.data(), P.seg_start, 4 * (P.n_seg + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sk.data(), P.seg_key, 4 * (P.n_seg + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rp.data(), P.rseg_ptr, 4 * (P.n_rows + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rs.data(), P.rseg, 4 * (P.n_seg + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(stp.data(), P.st_ptr, 4 * (P.n_st + 1), cudaMemcpyDeviceToHost));
+    if (P.n_rows > 0) CK(cudaMemcpy(lg.data(), P.l2g, 4 * P.n_rows, cudaMemcpyDeviceToHost));
+    const std::vector<int32_t> &d2c = c->h_d2c[lp];
     int64_t o = 0;
-    for (int64_t lr = 0; lr < P.n_rows; ++lr) {
+    std::vector<std::pair<int32_t, double>> row;
+    for (int32_t lr = 0; lr < P.n_rows; ++lr) {
+        row.clear();
+        for (int q = rp[lr]; q < rp[lr + 1]; ++q) {
+            int s = rs[q];
+            int basev = stp[sk[s] / P.n_rows];
+            for (int e = ss[s]; e < ss[s + 1]; ++e) {
+                if (e > ss[s] && fi[e] == fi[e - 1]) break;  // padding
+                row.push_back({d2c[basev + fi[e]], fv[e]});
+            }
+        }
+        std::sort(row.begin(), row.end(),
+                  [](const std::pair<int32_t, double> &a, const std::pair<int32_t, double> &b) {
+                      return a.first < b.first;
+                  });
         if (indptr) indptr[lr] = o;
-        for (int q = 0; q < rl[lr]; ++q, ++o) {
-            if (data) data[o] = dv[rp[lr] + q];
-            if (cols) cols[o] = cv[rp[lr] + q];
+        for (auto &e : row) {
+            if (data) data[o] = e.second;
+            if (cols) cols[o] = e.first;
+            ++o;
         }
     }
     if (indptr) indptr[P.n_rows] = o;
-    std::vector<int32_t> tmp(std::max<int64_t>(P.n_rows + 1, c->m + 1));
     if (rbp)
-        for (int i = 0; i <= c->m; ++i) rbp[i] = c->h_rbp[(size_t)lp * (c->m + 1) + i];
-    if (l2g) {
-        CK(cudaMemcpy(tmp.data(), c->l2g + P.row_off, 4 * P.n_rows, cudaMemcpyDeviceToHost));
-        for (int64_t q = 0; q < P.n_rows; ++q) l2g[q] = tmp[q];
-    }
+        for (int i = 0; i <= c->m; ++i) rbp[i] = c->h_rbp[lp][i];
+    if (l2g)
+        for (int32_t q = 0; q < P.n_rows; ++q) l2g[q] = lg[q];
     return 0;
 }
 
@@ -802,15 +744,16 @@ int bct_get_stream(bct_ctx *c, void **s)
     return 0;
 }
 
-// ---- state I/O (global order <-> panel-major) ----------------------------
+// ---- state I/O (global order <-> panel-major device order) -----------------
 
 static int xvec_to_dev(bct_ctx *c, const double *xg, double *dst)
 {
     std::vector<double> buf(std::max<int64_t>(c->x_len, 1));
     for (int lp = 0; lp < c->np; ++lp) {
         const PanelDev &P = c->h_panels[lp];
-        int j = c->pb + lp;
-        for (int64_t q = 0; q < P.n_cols; ++q) buf[P.x_off + q] = xg[c->col_vox[c->col_ptr[j] + q]];
+        const int64_t cb = c->col_ptr[c->pb + lp];
+        const std::vector<int32_t> &d2c = c->h_d2c[lp];
+        for (int64_t d = 0; d < P.n_cols; ++d) buf[P.x_off + d] = xg[c->col_vox[cb + d2c[d]]];
     }
     CK(cudaMemcpyAsync(dst, buf.data(), 8 * c->x_len, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -824,8 +767,9 @@ static int xvec_from_dev(bct_ctx *c, const double *src, double *xg)
     CK(cudaStreamSynchronize(c->stream));
     for (int lp = 0; lp < c->np; ++lp) {
         const PanelDev &P = c->h_panels[lp];
-        int j = c->pb + lp;
-        for (int64_t q = 0; q < P.n_cols; ++q) xg[c->col_vox[c->col_ptr[j] + q]] = buf[P.x_off + q];
+        const int64_t cb = c->col_ptr[c->pb + lp];
+        const std::vector<int32_t> &d2c = c->h_d2c[lp];
+        for (int64_t d = 0; d < P.n_cols; ++d) xg[c->col_vox[cb + d2c[d]]] = buf[P.x_off + d];
     }
     return 0;
 }
@@ -925,8 +869,7 @@ int bct_commit_epoch(bct_ctx *c)
 int bct_fill_z_from_image(bct_ctx *c)
 {
     if (!c) return BCT_EINVAL;
-    CK(bct::fill_z(c->dtype, c->vals, c->cols, c->rptr, c->rlen, c->d_panels, c->np, c->z_len,
-                   c->x, c->z, c->stream));
+    CK(bct::fill_z(c->dtype, c->d_panels, c->np, c->z_len, c->x, c->z, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return 0;
 }
@@ -957,9 +900,8 @@ int bct_forward(bct_ctx *c, const double *x, double *y_out)
     CK(cudaMalloc((void **)&dx, 8 * std::max<int64_t>(c->x_len, 1)));
     int r = xvec_to_dev(c, x, dx);
     if (!r) {
-        cudaError_t e = bct::forward(c->dtype, c->vals, c->cols, c->rptr, c->rlen, c->d_panels,
-                                     c->np, c->inv_ptr, c->inv_z, c->n_meas, dx, c->vec,
-                                     c->stream);
+        cudaError_t e = bct::forward(c->dtype, c->d_panels, c->np, c->inv_ptr, c->inv_z, c->n_meas,
+                                     dx, c->vec, c->stream);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(y_out, c->vec, 8 * c->n_meas, cudaMemcpyDeviceToHost, c->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -988,7 +930,7 @@ int bct_audit(bct_ctx *c, double *drift)
 
 // ---- epochs ---------------------------------------------------------------
 
-static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, int32_t flags)
+static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits)
 {
     int s = c->head;
     Slot &S = c->slots[s];
@@ -1005,9 +947,6 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, int32_t 
     CK(cudaEventRecord(c->staged, c->stream));
     EpochParams p;
     memset(&p, 0, sizeof p);
-    p.vals = c->vals; p.cols = c->cols; p.rptr = c->rptr; p.rlen = c->rlen; p.tvals = c->tvals;
-    p.trows = c->trows; p.cptr = c->cptr; p.corder = c->corder; p.rbp = c->rbp;
-    p.vbits = c->vbits; p.urow = c->urow; p.uend = c->uend; p.ubp = c->ubp;
     p.panels = c->d_panels;
     p.n_panels_owned = c->np; p.m = c->m; p.n_meas = c->n_meas; p.z_len = c->z_len;
     p.x_len = c->x_len; p.inv_ptr = c->inv_ptr; p.inv_z = c->inv_z; p.rb_ptr = c->d_rb_ptr;
@@ -1015,20 +954,21 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, int32_t 
     p.x = c->x; p.xhat = c->xhat; p.counts = c->counts;
     p.x_true = c->has_x_true ? c->x_true : nullptr;
     p.hdr = c->d_hdr; p.tasks = c->d_tasks; p.gx = c->gx; p.gx_stride = 2 * c->max_cols;
-    p.t_ax = c->t_ax; p.part = c->part; p.mus = c->mus; p.statuses = c->statuses; p.out = c->out;
+    p.t_ax = c->t_ax; p.seg_part = c->seg_part; p.part = c->part; p.mus = c->mus;
+    p.statuses = c->statuses; p.out = c->out;
     p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
     p.timeline = nullptr;
     if (getenv("BCT_TIMELINE") && n_tasks > 0) {
         if (c->timeline_tasks < n_tasks) {
             if (c->timeline) cudaFree(c->timeline);
-            CK(cudaMalloc((void **)&c->timeline, 8 * 6 * (size_t)n_tasks * c->grid));
+            CK(cudaMalloc((void **)&c->timeline, 8 * 8 * (size_t)n_tasks * c->grid));
             c->timeline_tasks = n_tasks;
         }
         p.timeline = c->timeline;
     }
     CK(cudaEventRecord(S.t0, c->stream));
     cudaError_t e;
-    bct::launch_epoch(p, c->dtype, c->grid, c->block, c->stream, &e);
+    bct::launch_epoch(p, c->dtype, c->grid, c->block, c->smem, c->stream, &e);
     if (e != cudaSuccess) return fail(c, BCT_ECUDA, "epoch launch: %s", cudaGetErrorString(e));
     CK(cudaEventRecord(S.t1, c->stream));
     CK(cudaMemcpyAsync(S.h_out, c->out, sizeof(EpochOut), cudaMemcpyDeviceToHost, c->stream));
@@ -1042,7 +982,6 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, int32_t 
     S.n_visits = n_visits;
     S.pending = true;
     c->head = (c->head + 1) % RING;
-    (void)flags;
     return 0;
 }
 
@@ -1061,7 +1000,6 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
     // validate and pack before touching the device (a failed batch leaves no trace)
     std::vector<TaskDev> tasks;
     tasks.reserve(n_tasks);
-    std::vector<int64_t> src_index;
     uint64_t emask[BCT_MASKW] = {0, 0, 0, 0};
     for (int64_t k = 0; k < n_tasks; ++k) {
         int j = task_j[k];
@@ -1096,7 +1034,6 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
         T.visit = task_visit[k];
         T.beta = betas[k];
         tasks.push_back(T);
-        src_index.push_back(k);
     }
     // visit boundaries and masks
     int64_t n_visits = 0;
@@ -1125,7 +1062,7 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
     memcpy(c->h_hdr->epoch_mask, emask, sizeof emask);
     memcpy(c->last_epoch_mask, emask, sizeof emask);
     if (nt) memcpy(c->h_tasks, tasks.data(), sizeof(TaskDev) * nt);
-    return launch_staged(c, nt, n_visits, flags);
+    return launch_staged(c, nt, n_visits);
 }
 
 int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *statuses)
@@ -1152,14 +1089,14 @@ int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *status
     return 0;
 }
 
-// Profiling: phase timestamps of the last epoch (BCT_TIMELINE=1), [task][6][grid].
+// Profiling: phase timestamps of the last epoch (BCT_TIMELINE=1), [task][8][grid].
 int bct_debug_timeline(bct_ctx *c, long long *out, int64_t n_tasks, int32_t *grid)
 {
     if (!c || !grid) return BCT_EINVAL;
     *grid = c->grid;
     if (!c->timeline || !out) return 0;
     CK(cudaStreamSynchronize(c->stream));
-    CK(cudaMemcpy(out, c->timeline, 8 * 6 * (size_t)std::min(n_tasks, c->timeline_tasks) * c->grid,
+    CK(cudaMemcpy(out, c->timeline, 8 * 8 * (size_t)std::min(n_tasks, c->timeline_tasks) * c->grid,
                   cudaMemcpyDeviceToHost));
     return 0;
 }

@@ -9,9 +9,10 @@
 //       distinct and the traversal is monotone in ix and, within one ix
 //       column, monotone in iy, so pb_fill_kernel writes every entry straight
 //       to its sorted slot instead (same result, O(len) instead of O(len^2)).
-//   panel CSC (per (column, row block) segment table), storage conversion,
 //   inverse row map and the bitwise forward / z-fill / projection-sum
-//   kernels used for state set-up (projector.py:220-244, 756-777).
+//   kernels used for state set-up (projector.py:220-244, 756-777); the panel
+//   layout itself is built in layout.cu.
+#include <climits>
 #include <cstdint>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
@@ -214,131 +215,6 @@ __global__ void rbp_kernel(const int32_t *l2g, int64_t n_hit, const int64_t *edg
     rbp[i] = (int32_t)lo;
 }
 
-// ---- padded panel layout ----------------------------------------------------
-
-__global__ void rowlen_kernel(const int32_t *indptr, int32_t n_rows, int32_t *rlen,
-                              int32_t *rlen4)
-{
-    int lr = blockIdx.x * blockDim.x + threadIdx.x;
-    if (lr > n_rows) return;
-    if (lr == n_rows) { rlen4[lr] = 0; return; }
-    int l = indptr[lr + 1] - indptr[lr];
-    rlen[lr] = l;
-    rlen4[lr] = (l + 3) & ~3;
-}
-
-// forward rows copied to their 4-aligned slots; padding zeroed
-template <typename V>
-__global__ void pad_rows_kernel(const double *vals64, const int32_t *cols_c, const int32_t *indptr,
-                                const int32_t *rptr, int32_t n_rows, V *vals, int32_t *cols)
-{
-    int lr = blockIdx.x * blockDim.x + threadIdx.x;
-    if (lr >= n_rows) return;
-    int s = indptr[lr], e = indptr[lr + 1], d = rptr[lr], de = rptr[lr + 1];
-    for (int q = s; q < e; ++q) {
-        vals[d + (q - s)] = (V)vals64[q];
-        cols[d + (q - s)] = cols_c[q];
-    }
-    // padding: zero value on the row's last column (a gather it makes anyway)
-    const int32_t pc = e > s ? cols_c[e - 1] : 0;
-    for (int q = d + (e - s); q < de; ++q) {
-        vals[q] = (V)0;
-        cols[q] = pc;
-    }
-}
-
-// one bit per 4-entry vector that starts a row (panel-relative words)
-__global__ void vbits_kernel(const int32_t *rptr, int32_t n_rows, uint32_t *vbits)
-{
-    int lr = blockIdx.x * blockDim.x + threadIdx.x;
-    if (lr >= n_rows) return;
-    uint32_t v = (uint32_t)rptr[lr] >> 2;
-    atomicOr(&vbits[v >> 5], 1u << (v & 31));
-}
-
-__global__ void row_of_entry_kernel(const int32_t *indptr, int32_t n_rows, int32_t *rowid)
-{
-    int lr = blockIdx.x * blockDim.x + threadIdx.x;
-    if (lr >= n_rows) return;
-    for (int p = indptr[lr]; p < indptr[lr + 1]; ++p) rowid[p] = lr;
-}
-
-__global__ void iota_kernel(int32_t *v, int64_t n)
-{
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) v[i] = (int32_t)i;
-}
-
-__device__ __forceinline__ int64_t lower_bound_i32(const int32_t *a, int64_t lo, int64_t hi,
-                                                   int32_t key)
-{
-    while (lo < hi) {
-        int64_t mid = (lo + hi) / 2;
-        if (a[mid] < key) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
-// colstart[c] (compact sorted order) and padded column sizes
-__global__ void colcount_kernel(const int32_t *sorted_cols, int64_t nnz, int32_t n_cols,
-                                int32_t *colstart, int32_t *colnnz4)
-{
-    int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c > n_cols) return;
-    int64_t s = lower_bound_i32(sorted_cols, 0, nnz, c);
-    colstart[c] = (int32_t)s;
-    if (c < n_cols) {
-        int64_t e = lower_bound_i32(sorted_cols, s, nnz, c + 1);
-        colnnz4[c] = (int32_t)(((e - s) + 3) & ~3);
-    } else {
-        colnnz4[c] = 0;
-    }
-}
-
-// sorted position q -> padded CSC slot cpad[c] + (q - colstart[c])
-template <typename V>
-__global__ void csc_scatter_kernel(const int32_t *perm, const double *vals64, const int32_t *rowid,
-                                   const int32_t *l2g, const int32_t *sorted_cols,
-                                   const int32_t *colstart, const int32_t *cpad, int64_t nnz,
-                                   V *tvals, int32_t *trows, int32_t *tlocal)
-{
-    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (q >= nnz) return;
-    int32_t p = perm[q];
-    int32_t lr = rowid[p];
-    int c = sorted_cols[q];
-    int64_t d = cpad[c] + (q - colstart[c]);
-    tvals[d] = (V)vals64[p];
-    trows[d] = l2g[lr];
-    tlocal[q] = lr;
-}
-
-template <typename V>
-__global__ void csc_pad_kernel(const int32_t *colstart, const int32_t *cpad, int32_t n_cols,
-                               V *tvals, int32_t *trows)
-{
-    int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= n_cols) return;
-    int64_t d = cpad[c] + (colstart[c + 1] - colstart[c]);
-    const int32_t pr = d > cpad[c] ? trows[d - 1] : 0;  // zero value on the last row
-    for (int64_t q = d; q < cpad[c + 1]; ++q) {
-        tvals[q] = (V)0;
-        trows[q] = pr;
-    }
-}
-
-// cptr[c*(m+1)+i] = padded position of the first entry of column c whose
-// local row >= rbp[i] (entries of a column are in ascending local row).
-__global__ void cptr_kernel(const int32_t *colstart, const int32_t *cpad, const int32_t *tlocal,
-                            const int32_t *rbp, int m, int32_t n_cols, int32_t *cptr)
-{
-    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= (int64_t)n_cols * (m + 1)) return;
-    int c = (int)(t / (m + 1)), i = (int)(t % (m + 1));
-    int64_t lb = lower_bound_i32(tlocal, colstart[c], colstart[c + 1], rbp[i]);
-    cptr[t] = (int32_t)(cpad[c] + (lb - colstart[c]));
-}
-
 // ---- inverse row map -----------------------------------------------------
 
 __global__ void inv_count_kernel(const int32_t *l2g, int32_t n_rows, int32_t *cnt)
@@ -369,37 +245,58 @@ __device__ __forceinline__ int panel_of_off(const PanelDev *panels, int np, int6
     return lo;
 }
 
+constexpr int MAX_ROW_SEGS = 64;
+
+// Row dot in the reference's order (ascending local column, projector.py:220-244)
+// over the row's super-tile segments: merge them by (c / mdiv, tile, c).
 template <typename V>
-__device__ double row_dot(const V *vals, const int32_t *cols, const int32_t *rptr,
-                          const int32_t *rlen, const PanelDev &P, int lp, int64_t lr,
-                          const double *xj)
+__device__ double row_dot(const PanelDev &P, int64_t lr, const double *xj)
 {
-    const int32_t s = rptr[P.row_off + lp + lr], e = s + rlen[P.row_off + lr];
+    const V *fv = static_cast<const V *>(P.fvals);
+    const int q0 = P.rseg_ptr[lr], ns = min(P.rseg_ptr[lr + 1] - q0, MAX_ROW_SEGS);
+    int cur[MAX_ROW_SEGS], beg[MAX_ROW_SEGS], fin[MAX_ROW_SEGS], base[MAX_ROW_SEGS];
+    for (int k = 0; k < ns; ++k) {
+        const int sg = P.rseg[q0 + k];
+        beg[k] = cur[k] = P.seg_start[sg];
+        fin[k] = P.seg_start[sg + 1];
+        base[k] = P.st_ptr[P.seg_key[sg] / P.n_rows];
+    }
+    // a segment ends at its padding (a repeated tile index)
+    auto alive = [&](int k) {
+        return cur[k] < fin[k] && (cur[k] == beg[k] || P.fidx[cur[k]] != P.fidx[cur[k] - 1]);
+    };
     double acc = 0.0;
-    for (int q = s; q < e; ++q)
-        acc = __dadd_rn(acc, __dmul_rn((double)vals[P.fwd_off + q], xj[cols[P.fwd_off + q]]));
+    for (;;) {
+        int gmin = INT_MAX;
+        for (int k = 0; k < ns; ++k)
+            if (alive(k)) gmin = min(gmin, P.d2c[base[k] + P.fidx[cur[k]]] / P.mdiv);
+        if (gmin == INT_MAX) break;
+        for (int k = 0; k < ns; ++k)
+            while (alive(k) && P.d2c[base[k] + P.fidx[cur[k]]] / P.mdiv == gmin) {
+                const int dpos = base[k] + P.fidx[cur[k]];
+                acc = __dadd_rn(acc, __dmul_rn((double)fv[cur[k]], xj[dpos]));
+                ++cur[k];
+            }
+    }
     return acc;
 }
 
 // z^j = A_:j x_J (projector.py:220-226 via fill_z_from_image)
 template <typename V>
-__global__ void fill_z_kernel(const V *vals, const int32_t *cols, const int32_t *rptr,
-                              const int32_t *rlen, const PanelDev *panels, int np, int64_t z_len,
-                              const double *x, double *z)
+__global__ void fill_z_kernel(const PanelDev *panels, int np, int64_t z_len, const double *x,
+                              double *z)
 {
     int64_t off = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (off >= z_len) return;
     int lp = panel_of_off(panels, np, off);
-    const PanelDev P = panels[lp];
-    z[off] = row_dot(vals, cols, rptr, rlen, P, lp, off - P.row_off, x + P.x_off);
+    const PanelDev &P = panels[lp];
+    z[off] = row_dot<V>(P, off - P.row_off, x + P.x_off);
 }
 
 // y = A x with per-panel row dots accumulated in ascending j (projector.py:237-244)
 template <typename V>
-__global__ void forward_kernel(const V *vals, const int32_t *cols, const int32_t *rptr,
-                               const int32_t *rlen, const PanelDev *panels, int np,
-                               const int32_t *inv_ptr, const int32_t *inv_z, int64_t n_meas,
-                               const double *x, double *out)
+__global__ void forward_kernel(const PanelDev *panels, int np, const int32_t *inv_ptr,
+                               const int32_t *inv_z, int64_t n_meas, const double *x, double *out)
 {
     int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (g >= n_meas) return;
@@ -407,9 +304,8 @@ __global__ void forward_kernel(const V *vals, const int32_t *cols, const int32_t
     for (int e = inv_ptr[g]; e < inv_ptr[g + 1]; ++e) {
         int64_t off = inv_z[e];
         int lp = panel_of_off(panels, np, off);
-        const PanelDev P = panels[lp];
-        acc = __dadd_rn(acc, row_dot(vals, cols, rptr, rlen, P, lp, off - P.row_off,
-                                     x + P.x_off));
+        const PanelDev &P = panels[lp];
+        acc = __dadd_rn(acc, row_dot<V>(P, off - P.row_off, x + P.x_off));
     }
     out[g] = acc;
 }
@@ -570,69 +466,6 @@ cudaError_t pb_rbp(const int32_t *d_l2g, int64_t n_hit, const int64_t *d_edges, 
     return cudaGetLastError();
 }
 
-// Lays out one panel from its compact forward CSR (f64 values): the padded
-// forward rows and the padded CSC with its per-(column, block) pointers.
-// tmp_a..tmp_d hold >= nnz int32, tmp_e/tmp_f >= max(rows, cols) + 2 int32.
-cudaError_t layout_panel(int dtype, const double *vals64, const int32_t *cols_c,
-                         const int32_t *indptr_c, const int32_t *l2g, const int32_t *rbp, int m,
-                         int32_t n_rows, int32_t n_cols, int64_t nnz, void *vals, int32_t *cols,
-                         int32_t *rptr, int32_t *rlen, uint32_t *vbits, void *tvals,
-                         int32_t *trows, int32_t *cptr, int32_t *tmp_a, int32_t *tmp_b, int32_t *tmp_c,
-                         int32_t *tmp_d, int32_t *tmp_e, int32_t *tmp_f, void *d_cub,
-                         size_t cub_bytes, cudaStream_t s)
-{
-    size_t need = cub_bytes;
-    cudaError_t e;
-    // forward rows
-    rowlen_kernel<<<nblk(n_rows + 1, 256), 256, 0, s>>>(indptr_c, n_rows, rlen, tmp_e);
-    e = cub::DeviceScan::ExclusiveSum(d_cub, need, tmp_e, rptr, n_rows + 1, s);
-    if (e != cudaSuccess) return e;
-    if (n_rows > 0) {
-        if (dtype == 0)
-            pad_rows_kernel<double><<<nblk(n_rows, 128), 128, 0, s>>>(
-                vals64, cols_c, indptr_c, rptr, n_rows, (double *)vals, cols);
-        else
-            pad_rows_kernel<float><<<nblk(n_rows, 128), 128, 0, s>>>(
-                vals64, cols_c, indptr_c, rptr, n_rows, (float *)vals, cols);
-        vbits_kernel<<<nblk(n_rows, 256), 256, 0, s>>>(rptr, n_rows, vbits);
-    }
-    // CSC: stable radix sort of (column, entry): a column's entries stay in row order.
-    // tmp_a = row of entry, tmp_b = iota, tmp_c = sorted cols, tmp_d = perm
-    if (nnz > 0) {
-        row_of_entry_kernel<<<nblk(n_rows, 128), 128, 0, s>>>(indptr_c, n_rows, tmp_a);
-        iota_kernel<<<nblk(nnz, 256), 256, 0, s>>>(tmp_b, nnz);
-        int bits = 1;
-        while ((1ll << bits) < (int64_t)n_cols + 1) ++bits;
-        need = cub_bytes;
-        e = cub::DeviceRadixSort::SortPairs(d_cub, need, cols_c, tmp_c, tmp_b, tmp_d, (int)nnz, 0,
-                                            bits, s);
-        if (e != cudaSuccess) return e;
-    }
-    // tmp_e = colstart (n_cols+1), tmp_f = padded column sizes, scanned in place -> cpad
-    colcount_kernel<<<nblk(n_cols + 1, 256), 256, 0, s>>>(tmp_c, nnz, n_cols, tmp_e, tmp_f);
-    need = cub_bytes;
-    e = cub::DeviceScan::ExclusiveSum(d_cub, need, tmp_f, tmp_f, n_cols + 1, s);
-    if (e != cudaSuccess) return e;
-    if (nnz > 0) {
-        // tlocal (local row in sorted order) reuses tmp_b
-        if (dtype == 0)
-            csc_scatter_kernel<double><<<nblk(nnz, 256), 256, 0, s>>>(
-                tmp_d, vals64, tmp_a, l2g, tmp_c, tmp_e, tmp_f, nnz, (double *)tvals, trows, tmp_b);
-        else
-            csc_scatter_kernel<float><<<nblk(nnz, 256), 256, 0, s>>>(
-                tmp_d, vals64, tmp_a, l2g, tmp_c, tmp_e, tmp_f, nnz, (float *)tvals, trows, tmp_b);
-    }
-    if (dtype == 0)
-        csc_pad_kernel<double><<<nblk(n_cols, 256), 256, 0, s>>>(tmp_e, tmp_f, n_cols,
-                                                                (double *)tvals, trows);
-    else
-        csc_pad_kernel<float><<<nblk(n_cols, 256), 256, 0, s>>>(tmp_e, tmp_f, n_cols,
-                                                               (float *)tvals, trows);
-    int64_t nc = (int64_t)n_cols * (m + 1);
-    cptr_kernel<<<nblk(nc, 256), 256, 0, s>>>(tmp_e, tmp_f, tmp_b, rbp, m, n_cols, cptr);
-    return cudaGetLastError();
-}
-
 cudaError_t inv_count(const int32_t *d_l2g, int32_t n_rows, int32_t *d_cnt, cudaStream_t s)
 {
     if (n_rows == 0) return cudaSuccess;
@@ -649,31 +482,27 @@ cudaError_t inv_fill(const int32_t *d_l2g, int32_t n_rows, int64_t row_off,
     return cudaGetLastError();
 }
 
-cudaError_t fill_z(int dtype, const void *vals, const int32_t *cols, const int32_t *rptr,
-                   const int32_t *rlen, const PanelDev *panels, int np, int64_t z_len,
-                   const double *x, double *z, cudaStream_t s)
+cudaError_t fill_z(int dtype, const PanelDev *panels, int np, int64_t z_len, const double *x,
+                   double *z, cudaStream_t s)
 {
     if (z_len == 0) return cudaSuccess;
     if (dtype == 0)
-        fill_z_kernel<double><<<nblk(z_len, 128), 128, 0, s>>>((const double *)vals, cols, rptr,
-                                                               rlen, panels, np, z_len, x, z);
+        fill_z_kernel<double><<<nblk(z_len, 128), 128, 0, s>>>(panels, np, z_len, x, z);
     else
-        fill_z_kernel<float><<<nblk(z_len, 128), 128, 0, s>>>((const float *)vals, cols, rptr,
-                                                              rlen, panels, np, z_len, x, z);
+        fill_z_kernel<float><<<nblk(z_len, 128), 128, 0, s>>>(panels, np, z_len, x, z);
     return cudaGetLastError();
 }
 
-cudaError_t forward(int dtype, const void *vals, const int32_t *cols, const int32_t *rptr,
-                    const int32_t *rlen, const PanelDev *panels, int np, const int32_t *inv_ptr,
+cudaError_t forward(int dtype, const PanelDev *panels, int np, const int32_t *inv_ptr,
                     const int32_t *inv_z, int64_t n_meas, const double *x, double *out,
                     cudaStream_t s)
 {
     if (dtype == 0)
-        forward_kernel<double><<<nblk(n_meas, 128), 128, 0, s>>>(
-            (const double *)vals, cols, rptr, rlen, panels, np, inv_ptr, inv_z, n_meas, x, out);
+        forward_kernel<double><<<nblk(n_meas, 128), 128, 0, s>>>(panels, np, inv_ptr, inv_z,
+                                                                 n_meas, x, out);
     else
-        forward_kernel<float><<<nblk(n_meas, 128), 128, 0, s>>>(
-            (const float *)vals, cols, rptr, rlen, panels, np, inv_ptr, inv_z, n_meas, x, out);
+        forward_kernel<float><<<nblk(n_meas, 128), 128, 0, s>>>(panels, np, inv_ptr, inv_z,
+                                                                n_meas, x, out);
     return cudaGetLastError();
 }
 

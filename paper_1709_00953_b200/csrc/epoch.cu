@@ -1,26 +1,32 @@
-// epoch.cu -- the persistent epoch kernel and the small state kernels.
+// epoch.cu -- the persistent epoch kernel.
 //
-// One cooperative launch runs a whole epoch of the plan (executor.py:225-253):
-// for every task k (a basic iteration of _run_tasks, executor.py:42-102)
+// One cooperative launch runs a whole epoch of the plan (executor.py:225-253).
+// For every task k (one basic iteration of _run_tasks, executor.py:42-102):
 //
-//   phase 1  g = (A_I^J)^T r_I       warp per voxel column over the panel CSC,
-//                                    segments of the task's row blocks only;
-//                                    writes (g, x_J) interleaved; gg partials
-//   -- grid barrier --               gg = fixed-order sum of block partials
-//   phase 2  t = A_I g, ax = A_I x_J warp per local row (dual SpMV, one pass
-//                                    over the forward CSR); denom partials
-//   -- grid barrier --               denom, mu = beta*gg/denom, status 0/1/2
-//   phase 3  xhat_J += x_J + mu g    (x_new rounded exactly like the reference)
-//            z_I    = ax + mu t      written straight into the z store
-//                                    (commit_task, projector.py:723-740)
-//            serial_faithful: refresh of the visit's drawn rows
-//            r = y - sum_j z^j in ascending j (executor.py:215-223)
+//   phase 1   g = (A_I^J)^T r_I     per 16-column voxel tile: stage the tile's
+//                                   sinogram band of r in shared memory, one
+//                                   warp per column streams the CSC (16-byte
+//                                   loads of 8 entries) over the task's row
+//                                   blocks and gathers r from shared memory;
+//                                   writes (g, x_J) pairs; gg partials
+//   -- grid barrier --              gg = fixed-order sum of block partials
+//   phase 2a  per super tile: stage its (g, x) pairs in shared memory, stream
+//             the task's row units (one 4-entry vector per lane per step),
+//             segmented warp reduction on the segment-start bitmap ->
+//             (t, ax) partial per (row, super tile) segment
+//   -- grid barrier --
+//   phase 2b  per row: t, ax = sum of its segments in tile order; denom partials
+//   -- grid barrier --              denom, mu = beta*gg/denom, status 0/1/2
+//   phase 3   xhat_J += x_J + mu g  (x_new rounded like the reference)
+//             z_I = ax + mu t       straight into the z store (commit_task)
+//             serial_faithful: refresh of the visit's drawn rows,
+//             r = y - sum_j z^j in ascending j (executor.py:215-223)
 //   -- grid barrier only between serial visits --
 //
-// then an epoch tail: parallel-mode refresh over the union of drawn rows,
-// projection-sum metrics, optional _commit_epoch (solvers.py:180-185) and a
-// last-block reduction of the norms.  All reductions are fixed-order, so the
-// results are deterministic for a given grid size.
+// Epoch tail: parallel-mode refresh over the union of drawn rows, projection
+// sum metrics, optional _commit_epoch (solvers.py:180-185), last-block norm
+// reduction.  All reductions have a fixed order: deterministic for a given
+// grid.
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -28,24 +34,26 @@
 
 namespace {
 
-#ifndef BCT_BLOCK
-#define BCT_BLOCK 512
-#endif
-#ifndef BCT_MINB
-#define BCT_MINB 2
-#endif
-#ifndef BCT_UNROLL
-#define BCT_UNROLL 2
-#endif
-#ifndef BCT_P2_LANES
-#define BCT_P2_LANES 8
-#endif
-constexpr int BLOCK = BCT_BLOCK;
+constexpr int BLOCK = 512;
 constexpr int WARPS = BLOCK / 32;
-constexpr int P2L = BCT_P2_LANES;          // lanes per row in phase 2
-constexpr int P2R = 32 / P2L;              // rows per warp in flight
-constexpr int UNR = BCT_UNROLL;
+static_assert(WARPS == 16, "a CSC tile holds one column per warp");
+constexpr int TILE_COLS = 16;
 constexpr int MAX_RUNS = BCT_MAX_M / 2 + 1;
+constexpr int MAX_ST = 64;
+
+__device__ __forceinline__ long long gtimer()
+{
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// optional per-block phase timestamps: [task][8][block] (profiling only)
+#define TL_MARK(k, ph)                                                                \
+    do {                                                                              \
+        if (p.timeline && threadIdx.x == 0)                                           \
+            p.timeline[((int64_t)(k) * 8 + (ph)) * gridDim.x + blockIdx.x] = gtimer(); \
+    } while (0)
 
 __device__ __forceinline__ void grid_sync(unsigned int *bar)
 {
@@ -62,20 +70,6 @@ __device__ __forceinline__ void grid_sync(unsigned int *bar)
     }
     __syncthreads();
 }
-
-__device__ __forceinline__ long long gtimer()
-{
-    long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-// optional per-block phase timestamps: [task][6][block] (profiling only)
-#define TL_MARK(k, ph)                                                               \
-    do {                                                                             \
-        if (p.timeline && threadIdx.x == 0)                                          \
-            p.timeline[((int64_t)(k) * 6 + (ph)) * gridDim.x + blockIdx.x] = gtimer(); \
-    } while (0)
 
 __device__ __forceinline__ double warp_sum(double v)
 {
@@ -104,43 +98,35 @@ __device__ double fixed_sum(const double *part, int n, double *sh)
     return s;
 }
 
-// Per-block sum of one value held by every warp's lane 0, in warp order.
-__device__ double block_sum_lane0(double v, double *sh)
-{
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-    __syncthreads();
-    double s = 0.0;
-    if (threadIdx.x == 0) {
-        for (int w = 0; w < WARPS; ++w) s += sh[w];
-    }
-    __syncthreads();
-    return s;
-}
-
 // Per-block sum of a per-thread value, fixed order.
 __device__ double block_sum_all(double v, double *sh)
 {
     v = warp_sum(v);
-    return block_sum_lane0(v, sh);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < WARPS; ++w) s += sh[w];
+    __syncthreads();
+    return s;
 }
 
 struct Runs {
     int n;
     int i0[MAX_RUNS];
     int i1[MAX_RUNS];
-    int rows0[MAX_RUNS];     // first local row of the run
-    int pre[MAX_RUNS + 1];   // prefix of run row counts
-    int u0[MAX_RUNS];        // first row unit of the run
-    int upre[MAX_RUNS + 1];  // prefix of run unit counts
+    int rows0[MAX_RUNS];       // first local row of the run
+    int pre[MAX_RUNS + 1];     // prefix of run row counts
+    int nst;
+    int st_pre[MAX_ST + 1];    // prefix over super tiles of the task's unit counts
 };
 
-// Contiguous runs of set bits of a row-block mask, with their local row ranges.
-__device__ void build_runs(const uint64_t *mask, int m, const int32_t *rbp, const int32_t *ubp,
-                           Runs &R)
+// Contiguous runs of set bits of a row-block mask, with their local row ranges
+// and the task's units per super tile.
+__device__ void build_runs(const uint64_t *mask, int m, const PanelDev &P, Runs &R)
 {
-    __syncthreads();  // R of the previous task may still be in use
     if (threadIdx.x == 0) {
-        int n = 0, acc = 0, uacc = 0;
+        int n = 0, acc = 0;
         int i = 0;
         while (i < m) {
             if (!mask_has(mask, i)) { ++i; continue; }
@@ -148,26 +134,23 @@ __device__ void build_runs(const uint64_t *mask, int m, const int32_t *rbp, cons
             while (i < m && mask_has(mask, i)) ++i;
             R.i0[n] = s;
             R.i1[n] = i;
-            R.rows0[n] = rbp[s];
+            R.rows0[n] = P.rbp[s];
             R.pre[n] = acc;
-            acc += rbp[i] - rbp[s];
-            R.u0[n] = ubp[s];
-            R.upre[n] = uacc;
-            uacc += ubp[i] - ubp[s];
+            acc += P.rbp[i] - P.rbp[s];
             ++n;
         }
         R.pre[n] = acc;
-        R.upre[n] = uacc;
         R.n = n;
+        int uacc = 0;
+        for (int st = 0; st < P.n_st; ++st) {
+            R.st_pre[st] = uacc;
+            const int32_t *sb = P.stbu + st * (m + 1);
+            for (int q = 0; q < n; ++q) uacc += sb[R.i1[q]] - sb[R.i0[q]];
+        }
+        R.st_pre[P.n_st] = uacc;
+        R.nst = P.n_st;
     }
     __syncthreads();
-}
-
-__device__ __forceinline__ int run_unit(const Runs &R, int f)
-{
-    int k = 0;
-    while (f >= R.upre[k + 1]) ++k;
-    return R.u0[k] + (f - R.upre[k]);
 }
 
 __device__ __forceinline__ int run_row(const Runs &R, int f)
@@ -177,10 +160,40 @@ __device__ __forceinline__ int run_row(const Runs &R, int f)
     return R.rows0[k] + (f - R.pre[k]);
 }
 
-template <typename V>
-__device__ __forceinline__ double ldv(const V *p) { return (double)__ldg(p); }
+// flattened task unit f of super tile st -> unit id
+__device__ __forceinline__ int task_unit(const Runs &R, const PanelDev &P, int m, int f, int st)
+{
+    int off = f - R.st_pre[st];
+    const int32_t *sb = P.stbu + st * (m + 1);
+    for (int k = 0;; ++k) {
+        int c = sb[R.i1[k]] - sb[R.i0[k]];
+        if (off < c) return sb[R.i0[k]] + off;
+        off -= c;
+    }
+}
 
-// 4 consecutive values / indices from a 16-byte aligned position
+__device__ __forceinline__ void ld8v(const float *p, double v[8])
+{
+    float4 a = __ldg(reinterpret_cast<const float4 *>(p));
+    float4 b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void ld8v(const double *p, double v[8])
+{
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        double2 a = __ldg(reinterpret_cast<const double2 *>(p) + q);
+        v[2 * q] = a.x;
+        v[2 * q + 1] = a.y;
+    }
+}
+__device__ __forceinline__ void ld8u16(const uint16_t *p, int k[8])
+{
+    uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
+    k[0] = a.x & 0xffff; k[1] = a.x >> 16; k[2] = a.y & 0xffff; k[3] = a.y >> 16;
+    k[4] = a.z & 0xffff; k[5] = a.z >> 16; k[6] = a.w & 0xffff; k[7] = a.w >> 16;
+}
 __device__ __forceinline__ void ld4v(const float *p, double v[4])
 {
     float4 a = __ldg(reinterpret_cast<const float4 *>(p));
@@ -192,10 +205,10 @@ __device__ __forceinline__ void ld4v(const double *p, double v[4])
     double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
-__device__ __forceinline__ void ld4i(const int32_t *p, int k[4])
+__device__ __forceinline__ void ld4u16(const uint16_t *p, int k[4])
 {
-    int4 a = __ldg(reinterpret_cast<const int4 *>(p));
-    k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w;
+    uint2 a = __ldg(reinterpret_cast<const uint2 *>(p));
+    k[0] = a.x & 0xffff; k[1] = a.x >> 16; k[2] = a.y & 0xffff; k[3] = a.y >> 16;
 }
 
 __device__ __forceinline__ double z_value(double t, double ax, double mu, int status)
@@ -204,18 +217,16 @@ __device__ __forceinline__ double z_value(double t, double ax, double mu, int st
 }
 
 template <typename V>
-__global__ void __launch_bounds__(BLOCK, BCT_MINB) epoch_kernel(EpochParams p)
+__global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
 {
+    extern __shared__ double4 dyn_smem[];
     __shared__ Runs R;
     __shared__ double sh[WARPS];
     __shared__ TaskDev sT;
     __shared__ PanelDev sP;
 
-    const V *vals = static_cast<const V *>(p.vals);
-    const V *tvals = static_cast<const V *>(p.tvals);
     const int lane = threadIdx.x & 31;
-    const int gwarp = blockIdx.x * WARPS + (threadIdx.x >> 5);
-    const int nwarps = gridDim.x * WARPS;
+    const int warp = threadIdx.x >> 5;
     const int gtid = blockIdx.x * BLOCK + threadIdx.x;
     const int nthreads = gridDim.x * BLOCK;
     const int m = p.m;
@@ -226,6 +237,8 @@ __global__ void __launch_bounds__(BLOCK, BCT_MINB) epoch_kernel(EpochParams p)
     double *part_gg = p.part;
     double *part_den = p.part + gridDim.x;
     double *part_m = p.part + 2 * gridDim.x;
+    double *rs = reinterpret_cast<double *>(dyn_smem);   // phase 1 band
+    double2 *gs = reinterpret_cast<double2 *>(dyn_smem); // phase 2 super tile
 
     for (int k = 0; k < n_tasks; ++k) {
         __syncthreads();  // sT/sP/R of the previous task may still be in use
@@ -236,154 +249,167 @@ __global__ void __launch_bounds__(BLOCK, BCT_MINB) epoch_kernel(EpochParams p)
         __syncthreads();
         const TaskDev &T = sT;
         const PanelDev &P = sP;
-        const int32_t *rbp = p.rbp + (int64_t)T.lp * (m + 1);
-        build_runs(T.mask, m, rbp, p.ubp + (int64_t)T.lp * (m + 1), R);
+        build_runs(T.mask, m, P, R);
         TL_MARK(k, 0);
         double2 *gx = reinterpret_cast<double2 *>(p.gx + (k & 1) * p.gx_stride);
         const double *xj = p.x + P.x_off;
 
-        // ---- phase 1: g = A_I^T r_I over the panel CSC -------------------
-        // warp per voxel column, columns taken in 4x4-tile order (corder) so
-        // a CTA's warps gather overlapping r rows; 128-bit loads of 4 entries
+        // ---- phase 1: g = A_I^T r_I, tile bands in shared memory ----------
         double wsum = 0.0;
         {
-            const V *tv = tvals + P.csc_off;
-            const int32_t *tr = p.trows + P.csc_off;
-            const int32_t *co = p.corder + P.x_off;
-            const double *rr = p.r;
-            for (int q = gwarp; q < P.n_cols; q += nwarps) {
-                const int c = __ldg(co + q);
-                const int32_t *cp = p.cptr + P.cptr_off + (int64_t)c * (m + 1);
-                double acc = 0.0;
-                for (int k2 = 0; k2 < R.n; ++k2) {
-                    const int s = __ldg(cp + R.i0[k2]), e = __ldg(cp + R.i1[k2]);
-#pragma unroll UNR
-                    for (int i = (s & ~3) + 4 * lane; i < e; i += 128) {
-                        int rows[4];
-                        double v[4];
-                        ld4i(tr + i, rows);
-                        ld4v(tv + i, v);
+            const V *tv = static_cast<const V *>(P.tvals);
+            const int sub = lane >> 3, sl = lane & 7;
+            for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+                const int k0 = __ldg(P.band_ptr + t), k1 = __ldg(P.band_ptr + t + 1);
+                for (int q = k0 + warp * 4 + sub; q < k1; q += WARPS * 4) {
+                    const int g0 = __ldg(P.band_start + q), pre = __ldg(P.band_pre + q);
+                    const int len = __ldg(P.band_len + q);
+                    for (int e = sl; e < len; e += 8) rs[pre + e] = p.r[g0 + e];
+                }
+                __syncthreads();
+                const int qc = t * TILE_COLS + warp;
+                if (qc < P.n_cols) {
+                    const int d = __ldg(P.corder + qc);
+                    const int32_t *cp = P.cptr + (int64_t)d * (m + 1);
+                    double acc = 0.0;
+                    for (int kr = 0; kr < R.n; ++kr) {
+                        const int s = __ldg(cp + R.i0[kr]), e = __ldg(cp + R.i1[kr]);
+#pragma unroll 2
+                        for (int i = (s & ~7) + 8 * lane; i < e; i += 256) {
+                            int loc[8];
+                            double v[8];
+                            ld8u16(P.tloc + i, loc);
+                            ld8v(tv + i, v);
 #pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (i + u >= s && i + u < e) acc = fma(v[u], rr[rows[u]], acc);
+                            for (int u = 0; u < 8; ++u)
+                                if (i + u >= s && i + u < e) acc = fma(v[u], rs[loc[u]], acc);
+                        }
+                    }
+                    acc = warp_sum(acc);
+                    if (lane == 0) {
+                        gx[d] = make_double2(acc, xj[d]);
+                        wsum = fma(acc, acc, wsum);
                     }
                 }
-                acc = warp_sum(acc);
-                if (lane == 0) {
-                    gx[c] = make_double2(acc, xj[c]);
-                    wsum = fma(acc, acc, wsum);
-                }
+                __syncthreads();
             }
         }
         TL_MARK(k, 1);
-        double bsum = block_sum_lane0(wsum, sh);
+        double bsum = block_sum_all(wsum, sh);
         if (threadIdx.x == 0) part_gg[blockIdx.x] = bsum;
         grid_sync(p.bar);
-        double gg = fixed_sum(part_gg, gridDim.x, sh);
+        const double gg = fixed_sum(part_gg, gridDim.x, sh);
         TL_MARK(k, 2);
 
-        // ---- phase 2: dual SpMV t = A_I g, ax = A_I x_J -----------------
-        // The task's rows come in units of whole rows (~512 padded entries);
-        // a warp streams a unit 128 entries per step (one 4-entry vector per
-        // lane, 16-byte loads; rows are 4-aligned so a vector never straddles
-        // two rows).  Row boundaries come from the row-start bitmap; each step
-        // does a segmented warp reduction, the row left open at lane 31 keeps
-        // per-lane partials until it closes.  Fixed unit -> warp assignment
-        // and fixed reduction order: deterministic.
-        wsum = 0.0;
-        const int n_task_rows = R.pre[R.n];
+        // ---- phase 2a: segment partials of t = A_I g, ax = A_I x_J -------
         {
-            const V *fv = vals + P.fwd_off;
-            const int32_t *fc = p.cols + P.fwd_off;
-            const int32_t *rp = p.rptr + P.row_off + T.lp;
-            const uint32_t *vb = p.vbits + P.fwd_off / 128;
-            const int32_t *ur = p.urow + P.unit_off;
-            const int32_t *ue = p.uend + P.unit_off;
-            double2 *tax = reinterpret_cast<double2 *>(p.t_ax);
-            const int n_units = R.upre[R.n];
+            const V *fv = static_cast<const V *>(P.fvals);
+            double2 *spart = reinterpret_cast<double2 *>(p.seg_part);
+            const int nu = R.st_pre[R.nst];
+            const int ub = (int)((int64_t)nu * blockIdx.x / gridDim.x);
+            const int ue = (int)((int64_t)nu * (blockIdx.x + 1) / gridDim.x);
             const unsigned le_mask = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
-            for (int fu = gwarp; fu < n_units; fu += nwarps) {
-                const int u = run_unit(R, fu);
-                const int r0 = __ldg(ur + u), r1 = __ldg(ue + u);
-                const int E0 = __ldg(rp + r0), E1 = __ldg(rp + r1);
-                int open = r0 - 1;                 // row left open by the previous step
-                double pt = 0.0, pax = 0.0;        // per-lane partials of the open row
-                for (int b = E0 & ~127; b < E1; b += 128) {
-                    const int i = b + 4 * lane;
-                    double t = 0.0, ax = 0.0;
-                    if (i >= E0 && i < E1) {
-                        int cc[4];
-                        double v[4];
-                        ld4i(fc + i, cc);
-                        ld4v(fv + i, v);
+            int fu = ub;
+            while (fu < ue) {
+                int st = 0;
+                while (fu >= R.st_pre[st + 1]) ++st;
+                const int ge = min(ue, R.st_pre[st + 1]);
+                const int v0 = __ldg(P.st_ptr + st), v1 = __ldg(P.st_ptr + st + 1);
+                for (int q = threadIdx.x; q < v1 - v0; q += BLOCK) gs[q] = gx[v0 + q];
+                __syncthreads();
+                for (int f = fu + warp; f < ge; f += WARPS) {
+                    const int u = task_unit(R, P, m, f, st);
+                    const int s0 = __ldg(P.u_seg + u), s1 = __ldg(P.u_seg + u + 1);
+                    const int E0 = __ldg(P.seg_start + s0), E1 = __ldg(P.seg_start + s1);
+                    int open = s0 - 1;             // segment left open by the previous step
+                    double pt = 0.0, pax = 0.0;    // per-lane partials of the open segment
+                    for (int b = E0 & ~127; b < E1; b += 128) {
+                        const int i = b + 4 * lane;
+                        double t = 0.0, ax = 0.0;
+                        if (i >= E0 && i < E1) {
+                            int cc[4];
+                            double v[4];
+                            ld4u16(P.fidx + i, cc);
+                            ld4v(fv + i, v);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const double2 a = gx[cc[q]];
-                            t = fma(v[q], a.x, t);
-                            ax = fma(v[q], a.y, ax);
+                            for (int q = 0; q < 4; ++q) {
+                                const double2 a = gs[cc[q]];
+                                t = fma(v[q], a.x, t);
+                                ax = fma(v[q], a.y, ax);
+                            }
                         }
+                        uint32_t word = __ldg(P.fbits + (b >> 7));
+                        const int nv = (E1 - b) >> 2;
+                        if (nv < 32) word &= (1u << nv) - 1u;
+                        if (b < E0) word &= ~((1u << ((E0 - b) >> 2)) - 1u);
+                        if (word == 0u) {
+                            pt += t;
+                            pax += ax;
+                            continue;
+                        }
+                        const int rel = __popc(word & le_mask);   // 0: continues the open segment
+                        if (rel == 0) {
+                            pt += t;
+                            pax += ax;
+                            t = 0.0;
+                            ax = 0.0;
+                        }
+                        const double ot = warp_sum(pt), oax = warp_sum(pax);
+                        if (lane == 0 && open >= s0) spart[open] = make_double2(ot, oax);
+                        const double t0 = t, ax0 = ax;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const double tt = __shfl_up_sync(0xffffffffu, t, o);
+                            const double aa = __shfl_up_sync(0xffffffffu, ax, o);
+                            const int rr = __shfl_up_sync(0xffffffffu, rel, o);
+                            if (lane >= o && rr == rel) {
+                                t += tt;
+                                ax += aa;
+                            }
+                        }
+                        const int rel31 = __popc(word);
+                        if (rel > 0 && rel < rel31 && lane < 31 && ((word >> (lane + 1)) & 1u))
+                            spart[open + rel] = make_double2(t, ax);
+                        const bool last = rel == rel31;
+                        pt = last ? t0 : 0.0;
+                        pax = last ? ax0 : 0.0;
+                        open += rel31;
                     }
-                    // bit l: vector (b/4 + l) starts a row; keep the unit's vectors
-                    uint32_t word = __ldg(vb + (b >> 7));
-                    const int nv = (E1 - b) >> 2;
-                    if (nv < 32) word &= (1u << nv) - 1u;
-                    if (b < E0) word &= ~((1u << ((E0 - b) >> 2)) - 1u);
-                    if (word == 0u) {              // the whole step continues the open row
-                        pt += t;
-                        pax += ax;
-                        continue;
-                    }
-                    const int rel = __popc(word & le_mask);   // 0: continues the open row
-                    if (rel == 0) {
-                        pt += t;
-                        pax += ax;
-                        t = 0.0;
-                        ax = 0.0;
-                    }
-                    // the open row closes in this step
                     const double ot = warp_sum(pt), oax = warp_sum(pax);
-                    if (lane == 0 && open >= r0) {
-                        tax[open] = make_double2(ot, oax);
-                        wsum = fma(ot, ot, wsum);
-                    }
-                    // segmented inclusive scan over lanes keyed by rel
-                    const double t0 = t, ax0 = ax;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const double tt = __shfl_up_sync(0xffffffffu, t, o);
-                        const double aa = __shfl_up_sync(0xffffffffu, ax, o);
-                        const int rr = __shfl_up_sync(0xffffffffu, rel, o);
-                        if (lane >= o && rr == rel) {
-                            t += tt;
-                            ax += aa;
-                        }
-                    }
-                    const int rel31 = __popc(word);
-                    // rows fully inside the step end where the next vector starts a row
-                    if (rel > 0 && rel < rel31 && lane < 31 && ((word >> (lane + 1)) & 1u)) {
-                        tax[open + rel] = make_double2(t, ax);
-                        wsum = fma(t, t, wsum);
-                    }
-                    // the last segment stays open: keep its raw per-lane values
-                    const bool last = rel == rel31;
-                    pt = last ? t0 : 0.0;
-                    pax = last ? ax0 : 0.0;
-                    open += rel31;
+                    if (lane == 0) spart[open] = make_double2(ot, oax);
                 }
-                // flush the row still open at the unit end
-                const double ot = warp_sum(pt), oax = warp_sum(pax);
-                if (lane == 0) {
-                    tax[open] = make_double2(ot, oax);
-                    wsum = fma(ot, ot, wsum);
-                }
+                __syncthreads();
+                fu = ge;
             }
         }
         TL_MARK(k, 3);
+        grid_sync(p.bar);
+
+        // ---- phase 2b: rows = sum of their segments in tile order ----------
+        const int n_task_rows = R.pre[R.n];
+        wsum = 0.0;
+        {
+            const double2 *spart = reinterpret_cast<const double2 *>(p.seg_part);
+            double2 *tax = reinterpret_cast<double2 *>(p.t_ax);
+            for (int f = gtid; f < n_task_rows; f += nthreads) {
+                const int lr = run_row(R, f);
+                double t = 0.0, ax = 0.0;
+                const int q1 = __ldg(P.rseg_ptr + lr + 1);
+                for (int q = __ldg(P.rseg_ptr + lr); q < q1; ++q) {
+                    const double2 a = spart[__ldg(P.rseg + q)];
+                    t += a.x;
+                    ax += a.y;
+                }
+                tax[lr] = make_double2(t, ax);
+                wsum = fma(t, t, wsum);
+            }
+        }
+        TL_MARK(k, 4);
         bsum = block_sum_all(wsum, sh);
         if (threadIdx.x == 0) part_den[blockIdx.x] = bsum;
         grid_sync(p.bar);
-        double denom = fixed_sum(part_den, gridDim.x, sh);
-        TL_MARK(k, 4);
+        const double denom = fixed_sum(part_den, gridDim.x, sh);
+        TL_MARK(k, 5);
 
         // ---- phase 3: step, x accumulation, z store, serial refresh -----
         double mu = 0.0;
@@ -402,10 +428,10 @@ __global__ void __launch_bounds__(BLOCK, BCT_MINB) epoch_kernel(EpochParams p)
         }
         {
             double *xh = p.xhat + P.x_off;
-            for (int c = gtid; c < P.n_cols; c += nthreads) {
-                double2 a = gx[c];
+            for (int d = gtid; d < P.n_cols; d += nthreads) {
+                double2 a = gx[d];
                 double xn = status == 0 ? __dadd_rn(a.y, __dmul_rn(mu, a.x)) : a.y;
-                xh[c] += xn;
+                xh[d] += xn;
             }
         }
         {
@@ -445,9 +471,7 @@ __global__ void __launch_bounds__(BLOCK, BCT_MINB) epoch_kernel(EpochParams p)
             }
             if (k + 1 < n_tasks) grid_sync(p.bar);
         }
-        TL_MARK(k, 5);
-        {
-        }
+        TL_MARK(k, 6);
     }
 
     // ---- epoch tail ------------------------------------------------------
@@ -470,12 +494,13 @@ __global__ void __launch_bounds__(BLOCK, BCT_MINB) epoch_kernel(EpochParams p)
         }
     }
     for (int lp = 0; lp < p.n_panels_owned; ++lp) {
-        const PanelDev P = p.panels[lp];
+        const int64_t xo = p.panels[lp].x_off;
+        const int nc = p.panels[lp].n_cols;
         const int cnt = p.counts[lp];
-        double *xs = p.x + P.x_off;
-        double *xh = p.xhat + P.x_off;
-        const double *xt = p.x_true ? p.x_true + P.x_off : nullptr;
-        for (int c = gtid; c < P.n_cols; c += nthreads) {
+        double *xs = p.x + xo;
+        double *xh = p.xhat + xo;
+        const double *xt = p.x_true ? p.x_true + xo : nullptr;
+        for (int c = gtid; c < nc; c += nthreads) {
             double xv = xs[c];
             if (do_commit && cnt > 0) {
                 xv = xh[c] / (double)cnt;
@@ -534,31 +559,33 @@ namespace bct {
 
 std::string cuda_err(cudaError_t e) { return std::string(cudaGetErrorString(e)); }
 
-int epoch_grid_size(int dtype, int device, int *block)
+int epoch_grid_size(int dtype, int device, size_t smem, int *block)
 {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const void *fn = dtype == 0 ? (const void *)epoch_kernel<double> : (const void *)epoch_kernel<float>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (dtype == 0)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<double>, BLOCK, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<double>, BLOCK, smem);
     else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<float>, BLOCK, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<float>, BLOCK, smem);
     if (per < 1) per = 1;
-    if (per > BCT_MINB) per = BCT_MINB;
+    if (per > 2) per = 2;
     *block = BLOCK;
     return sms * per;
 }
 
-void launch_epoch(const EpochParams &p, int dtype, int grid, int block, cudaStream_t s,
-                  cudaError_t *err)
+void launch_epoch(const EpochParams &p, int dtype, int grid, int block, size_t smem,
+                  cudaStream_t s, cudaError_t *err)
 {
     EpochParams local = p;
     void *args[] = {&local};
     if (dtype == 0)
-        *err = cudaLaunchCooperativeKernel((const void *)epoch_kernel<double>, grid, block,
-                                           args, 0, s);
+        *err = cudaLaunchCooperativeKernel((const void *)epoch_kernel<double>, grid, block, args,
+                                           smem, s);
     else
-        *err = cudaLaunchCooperativeKernel((const void *)epoch_kernel<float>, grid, block,
-                                           args, 0, s);
+        *err = cudaLaunchCooperativeKernel((const void *)epoch_kernel<float>, grid, block, args,
+                                           smem, s);
 }
 
 }  // namespace bct

@@ -19,20 +19,42 @@
 #define BCT_MASKW 4                 // up to 256 row blocks
 #define BCT_MAX_M (64 * BCT_MASKW)
 
-// Rows of the forward CSR and columns of the CSC start on 4-entry (16-byte
-// for int32/f32) boundaries so the kernels can use 128-bit loads; the
-// padding entries are never read as data (lengths mask them).
+// One owned column panel in HBM (see layout.cu for the design).
 struct PanelDev {
-    int64_t fwd_off;   // first (padded) entry of the panel in vals/cols
-    int64_t csc_off;   // first (padded) entry of the panel in tvals/trows
-    int64_t row_off;   // first local row of the panel in z/l2g/rlen/scratch; rptr at row_off+lp
-    int64_t x_off;     // first voxel of the panel in x/xhat/corder
-    int64_t cptr_off;  // start of the (|J|)*(m+1) segment table
-    int64_t unit_off;  // first row unit of the panel in urow/uend
-    int32_t n_rows;
-    int32_t n_cols;
-    int32_t nnz;
-    int32_t j;         // global column block id
+    // forward store, super-tile-major segments (phase 2)
+    const void *fvals;         // T, segments padded to 4 entries
+    const uint16_t *fidx;      // voxel index inside the segment's super tile
+    const uint32_t *fbits;     // bit per 4-entry vector that starts a segment
+    const int32_t *seg_start;  // [n_seg+1] padded start of each segment
+    const int32_t *seg_key;    // tile * n_rows + local row
+    const int32_t *seg_row;    // local row of each segment
+    const int32_t *u_seg;      // [n_units+1] first segment of each unit
+    const int32_t *u_st;       // super tile of each unit
+    const int32_t *stbu;       // [n_st*(m+1)] first unit of (tile, row block)
+    const int32_t *st_ptr;     // [n_st+1] device voxel range of each super tile
+    const int32_t *rseg_ptr;   // [n_rows+1] row -> its segments (tile order) in rseg
+    const int32_t *rseg;
+    // panel CSC with tile bands (phase 1)
+    const void *tvals;         // T, columns (device order) padded to 8 entries
+    const uint16_t *tloc;      // slot of the entry's row in its tile's band
+    const int32_t *cptr;       // [n_cols*(m+1)] column segment starts per row block
+    const int32_t *corder;     // tile order of device columns, 16 per tile
+    const int32_t *band_ptr;   // [n_tiles+1] ranges of each tile
+    const int32_t *band_start; // first measurement id of a range
+    const int32_t *band_pre;   // band slot of the range's first row
+    const int32_t *band_len;
+    // rows / voxels
+    const int32_t *rbp;        // [m+1]
+    const int32_t *l2g;        // [n_rows] global measurement ids
+    const int32_t *d2c;        // device voxel position -> reference local column
+    int64_t row_off;           // rows of the panel in z / t_ax
+    int64_t x_off;             // voxels of the panel in x / xhat / x_true / gx order
+    int64_t fwd_cap, csc_cap;
+    int32_t n_rows, n_cols, nnz, j;
+    int32_t n_seg, n_units, n_st, n_tiles;
+    int32_t band_max, st_max;
+    int32_t mdiv;              // reference order = (c / mdiv, tile, c) for bitwise merges
+    int32_t pad_;
 };
 
 struct TaskDev {
@@ -63,20 +85,6 @@ struct EpochOut {
 };
 
 struct EpochParams {
-    // store
-    const void *vals;          // double* or float*
-    const int32_t *cols;
-    const int32_t *rptr;       // padded row starts (panel-relative), n_rows+1 per panel
-    const int32_t *rlen;       // true row lengths
-    const void *tvals;
-    const int32_t *trows;
-    const int32_t *cptr;       // absolute (panel-relative) CSC positions per (column, block)
-    const int32_t *corder;     // column processing order (2D voxel tiles)
-    const uint32_t *vbits;     // row-start bit per 4-entry forward vector (word = fwd_off/128)
-    const int32_t *urow;       // row units: [urow[u], uend[u]) whole rows of one row block
-    const int32_t *uend;
-    const int32_t *ubp;        // (m+1) per panel: units of row block i = [ubp[i], ubp[i+1])
-    const int32_t *rbp;
     const PanelDev *panels;
     int32_t n_panels_owned;
     int32_t m;
@@ -101,9 +109,10 @@ struct EpochParams {
     const EpochHeader *hdr;
     const TaskDev *tasks;
     // scratch
-    double *gx;                // 2 buffers x (2*max_cols) : (g, x_J) interleaved
+    double *gx;                // 2 buffers x (2*max_cols) : (g, x_J) interleaved, device order
     int64_t gx_stride;
     double *t_ax;              // (t, ax) interleaved per local row of the widest panel
+    double *seg_part;          // (t, ax) partial per segment of the widest panel
     double *part;              // per-block partials: [4][grid]
     double *mus;
     int32_t *statuses;
@@ -119,7 +128,13 @@ struct bct_ctx_s;
 // builder / launch helpers implemented in the .cu files
 namespace bct {
 std::string cuda_err(cudaError_t e);
-void launch_epoch(const EpochParams &p, int dtype, int grid, int block, cudaStream_t s,
-                  cudaError_t *err);
-int epoch_grid_size(int dtype, int device, int *block);
+void launch_epoch(const EpochParams &p, int dtype, int grid, int block, size_t smem,
+                  cudaStream_t s, cudaError_t *err);
+int epoch_grid_size(int dtype, int device, size_t smem, int *block);
+int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nnz,
+                    const double *vals64, const int32_t *cols_c, const int32_t *indptr_c,
+                    const int32_t *l2g, const int32_t *rbp, const std::vector<int32_t> &c2d_h,
+                    const std::vector<int32_t> &st_ptr_h, const std::vector<int32_t> &corder_h,
+                    int unit_entries, PanelDev &P, std::vector<void *> &keep, std::string &err,
+                    cudaStream_t s);
 }

@@ -212,7 +212,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(L, name), name
     assert declared == set(N.EXPORTED)
-    assert L.bct_version() == 1
+    assert L.bct_version() == 2
 
 
 def test_oracle_is_not_imported_by_the_product():

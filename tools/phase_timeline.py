@@ -41,28 +41,22 @@ def main():
         res = wait(s, packed.task_j.size)[0]
     nt = packed.task_j.size
     grid = ctypes.c_int32()
-    buf = np.zeros(6 * nt * 4096, dtype=np.int64)
+    buf = np.zeros(8 * nt * 4096, dtype=np.int64)
     N.check(N.load().bct_debug_timeline(s.ctx, N.ptr(buf), nt, ctypes.byref(grid)), s.ctx)
     G = grid.value
-    tl = buf[:nt * 6 * G].reshape(nt, 6, G).astype(np.float64) / 1e3  # us
+    tl = buf[:nt * 8 * G].reshape(nt, 8, G).astype(np.float64) / 1e3  # us
     print(f"config {a.config}: kernel {res.kernel_ms:.3f} ms, {nt} tasks, grid {G}")
-    print("task  p1_span  p1_spread  bar1  p2_span  p2_spread  bar2  p3_span   total")
-    tot = np.zeros(7)
+    print("task     p1   bar1    p2a  bar2+p2b  bar3     p3   total   (us, to the last block)")
+    tot = np.zeros(6)
     for k in range(nt):
         t = tl[k]
         start = t[0].min()
-        p1 = t[1].max() - start
-        sp1 = t[1].max() - t[1].min()
-        b1 = t[2].max() - t[1].max()
-        p2 = t[3].max() - t[2].min()
-        sp2 = t[3].max() - t[3].min()
-        b2 = t[4].max() - t[3].max()
-        p3 = t[5].max() - t[4].min()
-        row = np.array([p1, sp1, b1, p2, sp2, b2, p3])
+        row = np.array([t[1].max() - start, t[2].max() - t[1].max(), t[3].max() - t[2].min(),
+                        t[4].max() - t[3].max(), t[5].max() - t[4].max(), t[6].max() - t[5].min()])
         tot += row
-        if k < 4 or k == nt - 1:
-            print(f"{k:4d} " + " ".join(f"{v:8.1f}" for v in row) + f" {t[5].max() - start:8.1f}")
-    print("mean " + " ".join(f"{v / nt:8.1f}" for v in tot))
+        if k < 3 or k == nt - 1:
+            print(f"{k:4d} " + " ".join(f"{v:6.1f}" for v in row) + f" {t[6].max() - start:7.1f}")
+    print("mean " + " ".join(f"{v / nt:6.1f}" for v in tot))
 
 
 if __name__ == "__main__":
