@@ -47,8 +47,8 @@ cudaError_t sharded_finish(const double *, const double *, int64_t, const int32_
 namespace {
 
 constexpr int RING = 4;
-constexpr int UNIT_ENTRIES = 512;   // padded forward entries per row unit (phase 2a)
 constexpr int ST_VOXELS = 4096;     // voxels per super tile (64 KB of (g, x) pairs)
+constexpr size_t SMEM_BUDGET = 220 * 1024;  // dynamic shared memory per CTA (one CTA per SM)
 
 struct Slot {
     cudaEvent_t done = nullptr;
@@ -68,6 +68,7 @@ struct bct_ctx {
     int64_t n_meas = 0, n_vox = 0, nnz = 0, z_len = 0, x_len = 0;
     int64_t max_rows = 0, max_cols = 0, max_seg = 0;
     size_t smem = 0;
+    int32_t band_cap = 0, band_dbuf = 1;
     cudaStream_t stream = nullptr;
     // host mirrors
     std::vector<PanelDev> h_panels;
@@ -164,7 +165,7 @@ struct Placement {
     int32_t mdiv = 1;
 };
 
-Placement place_voxels(int64_t n_cols, int64_t h, int64_t w)
+Placement place_voxels(int64_t n_cols, int64_t h, int64_t w, int th, int tw)
 {
     Placement pl;
     pl.c2d.resize(n_cols);
@@ -184,11 +185,11 @@ Placement place_voxels(int64_t n_cols, int64_t h, int64_t w)
                 }
         }
         pl.st_ptr.push_back(d);
-        // 4x4 voxel tiles for phase 1
-        for (int64_t tx = 0; tx < h; tx += 4)
-            for (int64_t ty = 0; ty < w; ty += 4)
-                for (int64_t a = tx; a < std::min(h, tx + 4); ++a)
-                    for (int64_t b = ty; b < std::min(w, ty + 4); ++b)
+        // th x tw voxel tiles for phase 1 (consecutive groups of th*tw in corder)
+        for (int64_t tx = 0; tx < h; tx += th)
+            for (int64_t ty = 0; ty < w; ty += tw)
+                for (int64_t a = tx; a < std::min(h, tx + th); ++a)
+                    for (int64_t b = ty; b < std::min(w, ty + tw); ++b)
                         pl.corder.push_back(pl.c2d[a * w + b]);
         pl.mdiv = (int32_t)w;
     } else {
@@ -212,17 +213,31 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     PanelDev &P = c->h_panels[lp];
     const int j = c->pb + lp;
     const int32_t n_cols = (int32_t)(c->col_ptr[j + 1] - c->col_ptr[j]);
-    Placement pl = place_voxels(n_cols, h, w);
     int32_t *d_rbp = nullptr, *d_d2c = nullptr;
     DALLOC(d_rbp, c->m + 1);
     DALLOC(d_d2c, n_cols);
     CK(cudaMemcpy(d_rbp, rbp.data(), 4 * (c->m + 1), cudaMemcpyHostToDevice));
+    // phase-1 tiles: the largest whose double-buffered band fits shared memory
+    static const int shapes[3][2] = {{8, 8}, {4, 8}, {4, 4}};
+    Placement pl;
+    for (int si = 0; si < 3; ++si) {
+        const int th = shapes[si][0], tw = shapes[si][1];
+        pl = place_voxels(n_cols, h, w, th, tw);
+        std::string err;
+        std::vector<void *> kept;
+        PanelDev Q = P;
+        if (bct::layout_panel_v2(c->dtype, c->m, n_rows, n_cols, nnz, vals64, cols, indptr, l2g,
+                                 d_rbp, pl.c2d, pl.st_ptr, pl.corder, th * tw, Q, kept, err,
+                                 c->stream))
+            return fail(c, BCT_ENOMEM, "panel %d layout: %s", j, err.c_str());
+        if (2 * (size_t)Q.band_max * 8 <= SMEM_BUDGET || si == 2) {
+            P = Q;
+            c->allocs.insert(c->allocs.end(), kept.begin(), kept.end());
+            break;
+        }
+        for (void *q : kept) cudaFree(q);
+    }
     CK(cudaMemcpy(d_d2c, pl.d2c.data(), 4 * n_cols, cudaMemcpyHostToDevice));
-    std::string err;
-    if (bct::layout_panel_v2(c->dtype, c->m, n_rows, n_cols, nnz, vals64, cols, indptr, l2g, d_rbp,
-                             pl.c2d, pl.st_ptr, pl.corder, UNIT_ENTRIES, P, c->allocs, err,
-                             c->stream))
-        return fail(c, BCT_ENOMEM, "panel %d layout: %s", j, err.c_str());
     P.rbp = d_rbp;
     P.l2g = l2g;
     P.d2c = d_d2c;
@@ -237,7 +252,8 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     c->max_rows = std::max<int64_t>(c->max_rows, n_rows);
     c->max_cols = std::max<int64_t>(c->max_cols, n_cols);
     c->max_seg = std::max<int64_t>(c->max_seg, P.n_seg);
-    c->smem = std::max(c->smem, std::max<size_t>((size_t)P.band_max * 8, (size_t)P.st_max * 16));
+    c->band_cap = std::max(c->band_cap, (P.band_max + 1) & ~1);
+    c->smem = std::max<size_t>(c->smem, (size_t)P.st_max * 16);
     return 0;
 }
 
@@ -307,7 +323,13 @@ int finalize(bct_ctx *c)
     DALLOC(c->gx, 4 * c->max_cols);
     DALLOC(c->t_ax, 2 * c->max_rows);
     DALLOC(c->seg_part, 2 * c->max_seg + 2);
+    // two band buffers when they fit, else one (staging then serializes)
+    c->band_dbuf = 2 * (size_t)c->band_cap * 8 <= SMEM_BUDGET ? 1 : 0;
+    c->smem = std::max<size_t>(c->smem, (size_t)c->band_cap * 8 * (c->band_dbuf ? 2 : 1));
     c->smem = std::max<size_t>(c->smem, 16);
+    if (c->smem > 227 * 1024)
+        return fail(c, BCT_EINVAL, "shared-memory need %zu B exceeds the SM (band %d slots)",
+                    c->smem, c->band_cap);
     c->grid = bct::epoch_grid_size(c->dtype, c->device, c->smem, &c->block);
     DALLOC(c->part, 8 * (int64_t)c->grid + 8);
     DALLOC(c->out, 1);
@@ -681,8 +703,9 @@ int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *i
     const int64_t cap = std::max<int64_t>(P.fwd_cap, 1);
     std::vector<double> fv(cap);
     std::vector<uint16_t> fi(cap);
-    std::vector<int32_t> ss(P.n_seg + 1), sk(P.n_seg + 1), rp(P.n_rows + 1), rs(P.n_seg + 1),
-        stp(P.n_st + 1), lg(std::max(P.n_rows, 1));
+    std::vector<int32_t> sk(P.n_seg + 1), sln(P.n_seg + 1), ssl(P.n_seg + 1), sla(P.n_seg + 1),
+        rp(P.n_rows + 1), rs(P.n_seg + 1), stp(P.n_st + 1), sst(P.n_slices + 1),
+        lg(std::max(P.n_rows, 1));
     if (c->dtype == BCT_F64) {
         CK(cudaMemcpy(fv.data(), P.fvals, 8 * P.fwd_cap, cudaMemcpyDeviceToHost));
     } else {
@@ -691,11 +714,14 @@ int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *i
         for (int64_t q = 0; q < P.fwd_cap; ++q) fv[q] = f[q];
     }
     CK(cudaMemcpy(fi.data(), P.fidx, 2 * P.fwd_cap, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(ss.data(), P.seg_start, 4 * (P.n_seg + 1), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(sk.data(), P.seg_key, 4 * (P.n_seg + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sln.data(), P.seg_len, 4 * (P.n_seg + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ssl.data(), P.seg_slice, 4 * (P.n_seg + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sla.data(), P.seg_lane, 4 * (P.n_seg + 1), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(rp.data(), P.rseg_ptr, 4 * (P.n_rows + 1), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(rs.data(), P.rseg, 4 * (P.n_seg + 1), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(stp.data(), P.st_ptr, 4 * (P.n_st + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sst.data(), P.slice_start, 4 * (P.n_slices + 1), cudaMemcpyDeviceToHost));
     if (P.n_rows > 0) CK(cudaMemcpy(lg.data(), P.l2g, 4 * P.n_rows, cudaMemcpyDeviceToHost));
     const std::vector<int32_t> &d2c = c->h_d2c[lp];
     int64_t o = 0;
@@ -705,9 +731,9 @@ int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *i
         for (int q = rp[lr]; q < rp[lr + 1]; ++q) {
             int s = rs[q];
             int basev = stp[sk[s] / P.n_rows];
-            for (int e = ss[s]; e < ss[s + 1]; ++e) {
-                if (e > ss[s] && fi[e] == fi[e - 1]) break;  // padding
-                row.push_back({d2c[basev + fi[e]], fv[e]});
+            for (int e = 0; e < sln[s]; ++e) {
+                int64_t pos = sst[ssl[s]] + ((int64_t)(e >> 2) * 32 + sla[s]) * 4 + (e & 3);
+                row.push_back({d2c[basev + fi[pos]], fv[pos]});
             }
         }
         std::sort(row.begin(), row.end(),
@@ -955,6 +981,7 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits)
     p.x_true = c->has_x_true ? c->x_true : nullptr;
     p.hdr = c->d_hdr; p.tasks = c->d_tasks; p.gx = c->gx; p.gx_stride = 2 * c->max_cols;
     p.t_ax = c->t_ax; p.seg_part = c->seg_part; p.part = c->part; p.mus = c->mus;
+    p.band_cap = c->band_cap; p.band_dbuf = c->band_dbuf;
     p.statuses = c->statuses; p.out = c->out;
     p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
     p.timeline = nullptr;

@@ -254,27 +254,27 @@ __device__ double row_dot(const PanelDev &P, int64_t lr, const double *xj)
 {
     const V *fv = static_cast<const V *>(P.fvals);
     const int q0 = P.rseg_ptr[lr], ns = min(P.rseg_ptr[lr + 1] - q0, MAX_ROW_SEGS);
-    int cur[MAX_ROW_SEGS], beg[MAX_ROW_SEGS], fin[MAX_ROW_SEGS], base[MAX_ROW_SEGS];
+    int cur[MAX_ROW_SEGS], len[MAX_ROW_SEGS], base[MAX_ROW_SEGS], lane[MAX_ROW_SEGS];
+    int64_t sb[MAX_ROW_SEGS];
     for (int k = 0; k < ns; ++k) {
         const int sg = P.rseg[q0 + k];
-        beg[k] = cur[k] = P.seg_start[sg];
-        fin[k] = P.seg_start[sg + 1];
+        cur[k] = 0;
+        len[k] = P.seg_len[sg];
         base[k] = P.st_ptr[P.seg_key[sg] / P.n_rows];
+        sb[k] = P.slice_start[P.seg_slice[sg]];
+        lane[k] = P.seg_lane[sg];
     }
-    // a segment ends at its padding (a repeated tile index)
-    auto alive = [&](int k) {
-        return cur[k] < fin[k] && (cur[k] == beg[k] || P.fidx[cur[k]] != P.fidx[cur[k] - 1]);
-    };
+    auto pos = [&](int k) { return sb[k] + ((int64_t)(cur[k] >> 2) * 32 + lane[k]) * 4 + (cur[k] & 3); };
     double acc = 0.0;
     for (;;) {
         int gmin = INT_MAX;
         for (int k = 0; k < ns; ++k)
-            if (alive(k)) gmin = min(gmin, P.d2c[base[k] + P.fidx[cur[k]]] / P.mdiv);
+            if (cur[k] < len[k]) gmin = min(gmin, P.d2c[base[k] + P.fidx[pos(k)]] / P.mdiv);
         if (gmin == INT_MAX) break;
         for (int k = 0; k < ns; ++k)
-            while (alive(k) && P.d2c[base[k] + P.fidx[cur[k]]] / P.mdiv == gmin) {
-                const int dpos = base[k] + P.fidx[cur[k]];
-                acc = __dadd_rn(acc, __dmul_rn((double)fv[cur[k]], xj[dpos]));
+            while (cur[k] < len[k] && P.d2c[base[k] + P.fidx[pos(k)]] / P.mdiv == gmin) {
+                const int64_t ps = pos(k);
+                acc = __dadd_rn(acc, __dmul_rn((double)fv[ps], xj[base[k] + P.fidx[ps]]));
                 ++cur[k];
             }
     }

@@ -34,10 +34,8 @@
 
 namespace {
 
-constexpr int BLOCK = 512;
+constexpr int BLOCK = 1024;         // one CTA per SM
 constexpr int WARPS = BLOCK / 32;
-static_assert(WARPS == 16, "a CSC tile holds one column per warp");
-constexpr int TILE_COLS = 16;
 constexpr int MAX_RUNS = BCT_MAX_M / 2 + 1;
 constexpr int MAX_ST = 64;
 
@@ -118,7 +116,8 @@ struct Runs {
     int rows0[MAX_RUNS];       // first local row of the run
     int pre[MAX_RUNS + 1];     // prefix of run row counts
     int nst;
-    int st_pre[MAX_ST + 1];    // prefix over super tiles of the task's unit counts
+    int st_pre[MAX_ST + 1];    // prefix over super tiles of the task's slice counts
+    bool full;                 // the task covers every row block
 };
 
 // Contiguous runs of set bits of a row-block mask, with their local row ranges
@@ -144,11 +143,12 @@ __device__ void build_runs(const uint64_t *mask, int m, const PanelDev &P, Runs 
         int uacc = 0;
         for (int st = 0; st < P.n_st; ++st) {
             R.st_pre[st] = uacc;
-            const int32_t *sb = P.stbu + st * (m + 1);
+            const int32_t *sb = P.stbs + st * (m + 1);
             for (int q = 0; q < n; ++q) uacc += sb[R.i1[q]] - sb[R.i0[q]];
         }
         R.st_pre[P.n_st] = uacc;
         R.nst = P.n_st;
+        R.full = (n == 1 && R.i0[0] == 0 && R.i1[0] == m);
     }
     __syncthreads();
 }
@@ -160,11 +160,11 @@ __device__ __forceinline__ int run_row(const Runs &R, int f)
     return R.rows0[k] + (f - R.pre[k]);
 }
 
-// flattened task unit f of super tile st -> unit id
-__device__ __forceinline__ int task_unit(const Runs &R, const PanelDev &P, int m, int f, int st)
+// flattened task slice f of super tile st -> slice id
+__device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int m, int f, int st)
 {
     int off = f - R.st_pre[st];
-    const int32_t *sb = P.stbu + st * (m + 1);
+    const int32_t *sb = P.stbs + st * (m + 1);
     for (int k = 0;; ++k) {
         int c = sb[R.i1[k]] - sb[R.i0[k]];
         if (off < c) return sb[R.i0[k]] + off;
@@ -211,13 +211,67 @@ __device__ __forceinline__ void ld4u16(const uint16_t *p, int k[4])
     k[0] = a.x & 0xffff; k[1] = a.x >> 16; k[2] = a.y & 0xffff; k[3] = a.y >> 16;
 }
 
+__device__ __forceinline__ uint32_t smem_addr(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr(sdst)), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
+
+// Band staging of one tile: this lane holds the metadata of ranges
+// k0 + warp*32 + lane + it*BLOCK (it < 2); the warp issues the copies range by
+// range (range broadcast by shuffle, element e by lane e: 8-byte cp.async).
+struct BandMeta {
+    int2 m[2];
+};
+
+__device__ __forceinline__ void band_meta_load(const PanelDev &P, int t, BandMeta &bm)
+{
+    const int k0 = __ldg(P.band_ptr + t), k1 = __ldg(P.band_ptr + t + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+        const int q = k0 + warp * 32 + lane + it * BLOCK;
+        bm.m[it] = q < k1 ? __ldg(P.band_meta + q) : make_int2(0, 0);
+    }
+}
+
+__device__ __forceinline__ void band_issue(const PanelDev &P, int t, const BandMeta &bm,
+                                           const double *r, double *buf)
+{
+    const int k0 = __ldg(P.band_ptr + t), k1 = __ldg(P.band_ptr + t + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+        const int q0 = k0 + warp * 32 + it * BLOCK;
+        const int nr = min(32, k1 - q0);
+        for (int jj = 0; jj < nr; ++jj) {
+            const int g0 = __shfl_sync(0xffffffffu, bm.m[it].x, jj);
+            const int pk = __shfl_sync(0xffffffffu, bm.m[it].y, jj);
+            const int pre = (int)((unsigned)pk >> 16), len = pk & 0xffff;
+            for (int e = lane; e < len; e += 32) cp_async8(buf + pre + e, r + g0 + e);
+        }
+    }
+    // ranges beyond 2*BLOCK per tile (not expected): plain loads
+    for (int q = k0 + 2 * BLOCK + threadIdx.x; q < k1; q += BLOCK) {
+        const int2 mm = __ldg(P.band_meta + q);
+        const int pre = (int)((unsigned)mm.y >> 16), len = mm.y & 0xffff;
+        for (int e = 0; e < len; ++e) buf[pre + e] = r[mm.x + e];
+    }
+}
+
 __device__ __forceinline__ double z_value(double t, double ax, double mu, int status)
 {
     return status == 0 ? fma(mu, t, ax) : ax;
 }
 
 template <typename V>
-__global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
+__global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
 {
     extern __shared__ double4 dyn_smem[];
     __shared__ Runs R;
@@ -255,20 +309,34 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
         const double *xj = p.x + P.x_off;
 
         // ---- phase 1: g = A_I^T r_I, tile bands in shared memory ----------
+        // tiles round-robin over CTAs; the band of the next tile is copied
+        // (cp.async) into the second buffer while this tile is computed
         double wsum = 0.0;
         {
             const V *tv = static_cast<const V *>(P.tvals);
-            const int sub = lane >> 3, sl = lane & 7;
-            for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
-                const int k0 = __ldg(P.band_ptr + t), k1 = __ldg(P.band_ptr + t + 1);
-                for (int q = k0 + warp * 4 + sub; q < k1; q += WARPS * 4) {
-                    const int g0 = __ldg(P.band_start + q), pre = __ldg(P.band_pre + q);
-                    const int len = __ldg(P.band_len + q);
-                    for (int e = sl; e < len; e += 8) rs[pre + e] = p.r[g0 + e];
-                }
+            const int TC = P.tile_cols;
+            const bool dbuf = p.band_dbuf != 0;
+            double *buf0 = rs, *buf1 = rs + (dbuf ? p.band_cap : 0);
+            int t = blockIdx.x;
+            BandMeta bm;
+            if (t < P.n_tiles) {
+                band_meta_load(P, t, bm);
+                band_issue(P, t, bm, p.r, buf0);
+                cp_async_commit();
+                if (t + (int)gridDim.x < P.n_tiles) band_meta_load(P, t + gridDim.x, bm);
+            }
+            int cur = 0;
+            for (; t < P.n_tiles; t += gridDim.x) {
+                cp_async_wait_all();
                 __syncthreads();
-                const int qc = t * TILE_COLS + warp;
-                if (qc < P.n_cols) {
+                const int tn = t + gridDim.x;
+                double *bt = cur ? buf1 : buf0;
+                if (dbuf && tn < P.n_tiles) {
+                    band_issue(P, tn, bm, p.r, cur ? buf0 : buf1);
+                    cp_async_commit();
+                    if (tn + (int)gridDim.x < P.n_tiles) band_meta_load(P, tn + gridDim.x, bm);
+                }
+                for (int qc = t * TC + warp; qc < min((t + 1) * TC, P.n_cols); qc += WARPS) {
                     const int d = __ldg(P.corder + qc);
                     const int32_t *cp = P.cptr + (int64_t)d * (m + 1);
                     double acc = 0.0;
@@ -282,7 +350,7 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
                             ld8v(tv + i, v);
 #pragma unroll
                             for (int u = 0; u < 8; ++u)
-                                if (i + u >= s && i + u < e) acc = fma(v[u], rs[loc[u]], acc);
+                                if (i + u >= s && i + u < e) acc = fma(v[u], bt[loc[u]], acc);
                         }
                     }
                     acc = warp_sum(acc);
@@ -292,6 +360,13 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
                     }
                 }
                 __syncthreads();
+                if (dbuf) {
+                    cur ^= 1;
+                } else if (tn < P.n_tiles) {
+                    band_issue(P, tn, bm, p.r, buf0);
+                    cp_async_commit();
+                    if (tn + (int)gridDim.x < P.n_tiles) band_meta_load(P, tn + gridDim.x, bm);
+                }
             }
         }
         TL_MARK(k, 1);
@@ -302,13 +377,33 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
         TL_MARK(k, 2);
 
         // ---- phase 2a: segment partials of t = A_I g, ax = A_I x_J -------
+        // SELL-32 slices, one segment per lane; (g, x) of the slice's super
+        // tile staged in shared memory.  A full-panel task splits the slices
+        // among CTAs by stored entries, any other task by slice count.
         {
             const V *fv = static_cast<const V *>(P.fvals);
             double2 *spart = reinterpret_cast<double2 *>(p.seg_part);
-            const int nu = R.st_pre[R.nst];
-            const int ub = (int)((int64_t)nu * blockIdx.x / gridDim.x);
-            const int ue = (int)((int64_t)nu * (blockIdx.x + 1) / gridDim.x);
-            const unsigned le_mask = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+            const int ns = R.st_pre[R.nst];
+            int ub, ue;
+            if (R.full) {
+                __shared__ int s_lim[2];
+                if (threadIdx.x < 2) {
+                    const int64_t F = __ldg(P.slice_start + P.n_slices);
+                    const int32_t key = (int32_t)(F * (blockIdx.x + threadIdx.x) / gridDim.x);
+                    int lo = 0, hi = P.n_slices;
+                    while (lo < hi) {
+                        int mid = (lo + hi) / 2;
+                        if (__ldg(P.slice_start + mid) < key) lo = mid + 1; else hi = mid;
+                    }
+                    s_lim[threadIdx.x] = (blockIdx.x + threadIdx.x == gridDim.x) ? P.n_slices : lo;
+                }
+                __syncthreads();
+                ub = s_lim[0];
+                ue = s_lim[1];
+            } else {
+                ub = (int)((int64_t)ns * blockIdx.x / gridDim.x);
+                ue = (int)((int64_t)ns * (blockIdx.x + 1) / gridDim.x);
+            }
             int fu = ub;
             while (fu < ue) {
                 int st = 0;
@@ -318,65 +413,26 @@ __global__ void __launch_bounds__(BLOCK, 2) epoch_kernel(EpochParams p)
                 for (int q = threadIdx.x; q < v1 - v0; q += BLOCK) gs[q] = gx[v0 + q];
                 __syncthreads();
                 for (int f = fu + warp; f < ge; f += WARPS) {
-                    const int u = task_unit(R, P, m, f, st);
-                    const int s0 = __ldg(P.u_seg + u), s1 = __ldg(P.u_seg + u + 1);
-                    const int E0 = __ldg(P.seg_start + s0), E1 = __ldg(P.seg_start + s1);
-                    int open = s0 - 1;             // segment left open by the previous step
-                    double pt = 0.0, pax = 0.0;    // per-lane partials of the open segment
-                    for (int b = E0 & ~127; b < E1; b += 128) {
-                        const int i = b + 4 * lane;
-                        double t = 0.0, ax = 0.0;
-                        if (i >= E0 && i < E1) {
-                            int cc[4];
-                            double v[4];
-                            ld4u16(P.fidx + i, cc);
-                            ld4v(fv + i, v);
+                    const int sl = R.full ? f : task_slice(R, P, m, f, st);
+                    const int base = __ldg(P.slice_start + sl);
+                    const int nvec = (__ldg(P.slice_start + sl + 1) - base) >> 7;
+                    double t = 0.0, ax = 0.0;
+#pragma unroll 4
+                    for (int kv = 0; kv < nvec; ++kv) {
+                        const int i = base + ((kv * 32 + lane) << 2);
+                        int cc[4];
+                        double v[4];
+                        ld4u16(P.fidx + i, cc);
+                        ld4v(fv + i, v);
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const double2 a = gs[cc[q]];
-                                t = fma(v[q], a.x, t);
-                                ax = fma(v[q], a.y, ax);
-                            }
+                        for (int q = 0; q < 4; ++q) {
+                            const double2 a = gs[cc[q]];
+                            t = fma(v[q], a.x, t);
+                            ax = fma(v[q], a.y, ax);
                         }
-                        uint32_t word = __ldg(P.fbits + (b >> 7));
-                        const int nv = (E1 - b) >> 2;
-                        if (nv < 32) word &= (1u << nv) - 1u;
-                        if (b < E0) word &= ~((1u << ((E0 - b) >> 2)) - 1u);
-                        if (word == 0u) {
-                            pt += t;
-                            pax += ax;
-                            continue;
-                        }
-                        const int rel = __popc(word & le_mask);   // 0: continues the open segment
-                        if (rel == 0) {
-                            pt += t;
-                            pax += ax;
-                            t = 0.0;
-                            ax = 0.0;
-                        }
-                        const double ot = warp_sum(pt), oax = warp_sum(pax);
-                        if (lane == 0 && open >= s0) spart[open] = make_double2(ot, oax);
-                        const double t0 = t, ax0 = ax;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const double tt = __shfl_up_sync(0xffffffffu, t, o);
-                            const double aa = __shfl_up_sync(0xffffffffu, ax, o);
-                            const int rr = __shfl_up_sync(0xffffffffu, rel, o);
-                            if (lane >= o && rr == rel) {
-                                t += tt;
-                                ax += aa;
-                            }
-                        }
-                        const int rel31 = __popc(word);
-                        if (rel > 0 && rel < rel31 && lane < 31 && ((word >> (lane + 1)) & 1u))
-                            spart[open + rel] = make_double2(t, ax);
-                        const bool last = rel == rel31;
-                        pt = last ? t0 : 0.0;
-                        pax = last ? ax0 : 0.0;
-                        open += rel31;
                     }
-                    const double ot = warp_sum(pt), oax = warp_sum(pax);
-                    if (lane == 0) spart[open] = make_double2(ot, oax);
+                    const int seg = __ldg(P.sl_seg + (int64_t)sl * 32 + lane);
+                    if (seg >= 0) spart[seg] = make_double2(t, ax);
                 }
                 __syncthreads();
                 fu = ge;
@@ -570,7 +626,7 @@ int epoch_grid_size(int dtype, int device, size_t smem, int *block)
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<float>, BLOCK, smem);
     if (per < 1) per = 1;
-    if (per > 2) per = 2;
+    if (per > 1) per = 1;
     *block = BLOCK;
     return sms * per;
 }

@@ -21,17 +21,17 @@
 
 // One owned column panel in HBM (see layout.cu for the design).
 struct PanelDev {
-    // forward store, super-tile-major segments (phase 2)
-    const void *fvals;         // T, segments padded to 4 entries
-    const uint16_t *fidx;      // voxel index inside the segment's super tile
-    const uint32_t *fbits;     // bit per 4-entry vector that starts a segment
-    const int32_t *seg_start;  // [n_seg+1] padded start of each segment
-    const int32_t *seg_key;    // tile * n_rows + local row
-    const int32_t *seg_row;    // local row of each segment
-    const int32_t *u_seg;      // [n_units+1] first segment of each unit
-    const int32_t *u_st;       // super tile of each unit
-    const int32_t *stbu;       // [n_st*(m+1)] first unit of (tile, row block)
+    // forward store: SELL-32 slices of (row, super tile) segments (phase 2)
+    const void *fvals;         // T; vector k of lane l of slice s at slice_start[s] + (k*32+l)*4
+    const uint16_t *fidx;      // voxel index inside the slice's super tile
+    const int32_t *slice_start;// [n_slices+1] entry offset of each slice
+    const int32_t *sl_seg;     // [n_slices*32] segment of each lane (-1: empty)
+    const int32_t *stbs;       // [n_st*(m+1)] first slice of (tile, row block >= i)
     const int32_t *st_ptr;     // [n_st+1] device voxel range of each super tile
+    const int32_t *seg_key;    // tile * n_rows + local row
+    const int32_t *seg_len;    // entries of each segment
+    const int32_t *seg_slice;  // slice / lane holding each segment
+    const int32_t *seg_lane;
     const int32_t *rseg_ptr;   // [n_rows+1] row -> its segments (tile order) in rseg
     const int32_t *rseg;
     // panel CSC with tile bands (phase 1)
@@ -40,9 +40,7 @@ struct PanelDev {
     const int32_t *cptr;       // [n_cols*(m+1)] column segment starts per row block
     const int32_t *corder;     // tile order of device columns, 16 per tile
     const int32_t *band_ptr;   // [n_tiles+1] ranges of each tile
-    const int32_t *band_start; // first measurement id of a range
-    const int32_t *band_pre;   // band slot of the range's first row
-    const int32_t *band_len;
+    const int2 *band_meta;     // per range: (first measurement id, slot << 16 | length)
     // rows / voxels
     const int32_t *rbp;        // [m+1]
     const int32_t *l2g;        // [n_rows] global measurement ids
@@ -51,10 +49,10 @@ struct PanelDev {
     int64_t x_off;             // voxels of the panel in x / xhat / x_true / gx order
     int64_t fwd_cap, csc_cap;
     int32_t n_rows, n_cols, nnz, j;
-    int32_t n_seg, n_units, n_st, n_tiles;
+    int32_t n_seg, n_slices, n_st, n_tiles;
     int32_t band_max, st_max;
     int32_t mdiv;              // reference order = (c / mdiv, tile, c) for bitwise merges
-    int32_t pad_;
+    int32_t tile_cols;         // columns per phase-1 tile
 };
 
 struct TaskDev {
@@ -113,6 +111,8 @@ struct EpochParams {
     int64_t gx_stride;
     double *t_ax;              // (t, ax) interleaved per local row of the widest panel
     double *seg_part;          // (t, ax) partial per segment of the widest panel
+    int32_t band_cap;          // shared-memory slots per band buffer
+    int32_t band_dbuf;         // 1: two band buffers (copy next tile while computing)
     double *part;              // per-block partials: [4][grid]
     double *mus;
     int32_t *statuses;
@@ -135,6 +135,6 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
                     const double *vals64, const int32_t *cols_c, const int32_t *indptr_c,
                     const int32_t *l2g, const int32_t *rbp, const std::vector<int32_t> &c2d_h,
                     const std::vector<int32_t> &st_ptr_h, const std::vector<int32_t> &corder_h,
-                    int unit_entries, PanelDev &P, std::vector<void *> &keep, std::string &err,
+                    int tile_cols, PanelDev &P, std::vector<void *> &keep, std::string &err,
                     cudaStream_t s);
 }

@@ -6,20 +6,21 @@
 // 32 lines).  The layout therefore makes every gather a shared-memory access:
 //
 // Phase 1 (g = A_I^T r_I) reads the panel CSC.  Columns (voxels) are grouped
-// into tiles of 16 (4x4 voxels for strips); the rows crossing a tile form a
+// into tiles (8x8 voxels for strips); the rows crossing a tile form a
 // narrow "sinogram band" (a few bins per view).  Per tile the band is stored
 // as ranges of consecutive measurement ids; the kernel stages r over the band
 // in shared memory and every CSC entry carries its 16-bit band slot (tloc).
 //
 // Phase 2 (t = A_I g, ax = A_I x_J) reads the forward store.  The panel's
 // voxels are cut into super tiles of <= 4096 (iy ranges of a strip); each
-// row's entries are grouped per super tile into segments (row, tile) padded
-// to 4 entries, stored super-tile-major, and carry 16-bit tile-local voxel
-// indices (fidx).  The kernel stages one super tile's (g, x) pairs in shared
-// memory and streams its segments; per-segment partial sums are combined per
-// row in super-tile order (deterministic).  Segments are grouped into units
-// of whole segments (<= ~512 entries) that never cross a (tile, row block)
-// boundary, so any subset of row blocks maps to whole units.
+// row's entries are grouped per super tile into segments (row, tile) that
+// carry 16-bit tile-local voxel indices (fidx).  The segments of one (super
+// tile, row block) group are sorted by length and stored as SELL-32 slices
+// (32 segments interleaved 4 entries at a time), so a warp streams a slice
+// with coalesced 16-byte loads, one segment per lane, gathering (g, x) pairs
+// from the super tile staged in shared memory.  Per-segment partial sums are
+// combined per row in super-tile order (deterministic).  A task over any
+// subset of row blocks maps to whole slices.
 //
 // Entries inside a segment stay in the reference's column order, and a row's
 // segments in tile order, so the bitwise set-up kernels (builder.cu) recover
@@ -104,118 +105,122 @@ __global__ void seg_first_k(const int32_t *flag, const int32_t *incl, const int3
     seg_key[s] = skey[q];
 }
 
-__global__ void seg_len4_k(const int32_t *seg_first, int32_t n_seg, int64_t nnz, int32_t *len4)
+
+// ---- forward store, SELL-32 slices of segments (phase 2) ------------------------
+//
+// segments (row, super tile) of one (super tile, row block) group are sorted
+// by length (longest first) and cut into slices of 32; a slice stores its 32
+// segments interleaved 4 entries at a time -- vector k of lane l sits at
+// slice_start + (k*32 + l)*4 -- so a warp streams a slice with coalesced
+// 16-byte loads, one segment per lane and no cross-lane reduction.
+
+__global__ void seg_len_k(const int32_t *seg_first, int32_t n_seg, int64_t nnz, int32_t *len,
+                          int32_t *nvec)
 {
     int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s > n_seg) return;
-    if (s == n_seg) { len4[s] = 0; return; }
+    if (s >= n_seg) return;
     int64_t e = (s + 1 < n_seg) ? seg_first[s + 1] : nnz;
-    len4[s] = (int32_t)(((e - seg_first[s]) + 3) & ~3);
+    len[s] = (int32_t)(e - seg_first[s]);
+    nvec[s] = (int32_t)((e - seg_first[s] + 3) / 4);
 }
 
-// scatter sorted entries into padded segment slots
+// key: (tile, row block) group ascending, vector count descending
+__global__ void sell_key_k(const int32_t *seg_key, const int32_t *nvec, int32_t n_seg,
+                           int32_t n_rows, const int32_t *rbp, int m, uint64_t *key)
+{
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_seg) return;
+    int st = seg_key[s] / n_rows, lr = seg_key[s] % n_rows;
+    int blk = (int)lb_i32(rbp, 0, m + 1, lr + 1) - 1;
+    uint32_t gid = (uint32_t)(st * (m + 1) + blk);
+    key[s] = ((uint64_t)gid << 32) | (uint32_t)(0x7fffffff - nvec[s]);
+}
+
+__global__ void slice_flag_k(const uint64_t *skey, int32_t n_seg, int32_t *flag)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_seg) return;
+    uint32_t g = (uint32_t)(skey[q] >> 32);
+    int64_t lo = 0, hi = q;   // first position of this group
+    while (lo < hi) {
+        int64_t mid = (lo + hi) / 2;
+        if ((uint32_t)(skey[mid] >> 32) < g) lo = mid + 1; else hi = mid;
+    }
+    flag[q] = ((q - lo) % 32 == 0) ? 1 : 0;
+}
+
+__global__ void slice_info_k(const uint64_t *skey, const int32_t *sseg, const int32_t *flag_incl,
+                             const int32_t *nvec, int32_t n_seg, int32_t *seg_slice,
+                             int32_t *seg_lane, int32_t *sl_seg, int32_t *slice_len4,
+                             int32_t *slice_gid)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_seg) return;
+    uint32_t g = (uint32_t)(skey[q] >> 32);
+    int64_t lo = 0, hi = q;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) / 2;
+        if ((uint32_t)(skey[mid] >> 32) < g) lo = mid + 1; else hi = mid;
+    }
+    int lane = (int)((q - lo) % 32);
+    int sl = flag_incl[q] - 1;
+    int s = sseg[q];
+    seg_slice[s] = sl;
+    seg_lane[s] = lane;
+    sl_seg[(int64_t)sl * 32 + lane] = s;
+    if (lane == 0) {
+        slice_len4[sl] = nvec[s] * 128;  // entries of the slice (longest segment first)
+        slice_gid[sl] = (int32_t)g;
+    }
+}
+
 template <typename V>
-__global__ void fwd_scatter_k(const int32_t *perm, const int32_t *incl, const int32_t *seg_first,
-                              const int32_t *seg_start, const int32_t *seg_key,
-                              const double *vals64, const int32_t *cols_c, const int32_t *c2d,
-                              const int32_t *st_ptr, int32_t n_rows, int64_t nnz, V *fvals,
-                              uint16_t *fidx)
+__global__ void sell_scatter_k(const int32_t *perm, const int32_t *incl, const int32_t *seg_first,
+                               const int32_t *seg_key, const int32_t *seg_slice,
+                               const int32_t *seg_lane, const int32_t *slice_start,
+                               const double *vals64, const int32_t *cols_c, const int32_t *c2d,
+                               const int32_t *st_ptr, int32_t n_rows, int64_t nnz, V *fvals,
+                               uint16_t *fidx)
 {
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= nnz) return;
     int s = incl[q] - 1;
     int p = perm[q];
     int st = seg_key[s] / n_rows;
-    int64_t dst = seg_start[s] + (q - seg_first[s]);
-    fvals[dst] = (V)vals64[p];
-    fidx[dst] = (uint16_t)(c2d[cols_c[p]] - st_ptr[st]);
+    int64_t e = q - seg_first[s];
+    int64_t pos = slice_start[seg_slice[s]] + ((e >> 2) * 32 + seg_lane[s]) * 4 + (e & 3);
+    fvals[pos] = (V)vals64[p];
+    fidx[pos] = (uint16_t)(c2d[cols_c[p]] - st_ptr[st]);
 }
 
-// padding: zero value on the segment's last voxel; row-start bitmap; seg_row
+// padding of every (slice, lane): zero values on the lane's last voxel
 template <typename V>
-__global__ void fwd_pad_k(const int32_t *seg_first, const int32_t *seg_start, const int32_t *seg_key,
-                          int32_t n_seg, int64_t nnz, int32_t n_rows, V *fvals, uint16_t *fidx,
-                          uint32_t *bits, int32_t *seg_row)
+__global__ void sell_pad_k(const int32_t *sl_seg, const int32_t *seg_len, const int32_t *slice_start,
+                           int32_t n_slices, V *fvals, uint16_t *fidx)
 {
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n_seg) return;
-    int64_t len = ((s + 1 < n_seg) ? seg_first[s + 1] : nnz) - seg_first[s];
-    int64_t a = seg_start[s] + len, e = seg_start[s + 1];
-    uint16_t last = fidx[a - 1];
-    for (int64_t q = a; q < e; ++q) {
-        fvals[q] = (V)0;
-        fidx[q] = last;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n_slices * 32) return;
+    int sl = (int)(t / 32), lane = (int)(t % 32);
+    int s = sl_seg[t];
+    int len = s >= 0 ? seg_len[s] : 0;
+    int64_t base = slice_start[sl];
+    int64_t nent = ((int64_t)slice_start[sl + 1] - base) / 32;  // entries per lane
+    uint16_t last = 0;
+    if (len > 0) last = fidx[base + (((int64_t)(len - 1) >> 2) * 32 + lane) * 4 + ((len - 1) & 3)];
+    for (int64_t e = len; e < nent; ++e) {
+        int64_t pos = base + ((e >> 2) * 32 + lane) * 4 + (e & 3);
+        fvals[pos] = (V)0;
+        fidx[pos] = last;
     }
-    uint32_t v = (uint32_t)seg_start[s] >> 2;
-    atomicOr(&bits[v >> 5], 1u << (v & 31));
-    seg_row[s] = seg_key[s] % n_rows;
 }
 
-// units: segment s opens a unit when it is the first of its (tile, row
-// block) group or its start enters a new 512-entry window of the group
-__global__ void unit_flag_k(const int32_t *seg_key, const int32_t *seg_start, int32_t n_seg,
-                            int32_t n_rows, const int32_t *rbp, int m, int unit_entries,
-                            int32_t *grp, int32_t *flag)
-{
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n_seg) return;
-    int st = seg_key[s] / n_rows, lr = seg_key[s] % n_rows;
-    int i = (int)lb_i32(rbp, 0, m + 1, lr + 1) - 1;  // block of lr
-    grp[s] = st * (m + 1) + i;
-    __syncwarp();
-}
-
-__global__ void unit_flag2_k(const int32_t *grp, const int32_t *seg_start, int32_t n_seg,
-                             int unit_entries, const int32_t *grp_first_pos, int32_t *flag)
-{
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n_seg) return;
-    if (s == 0 || grp[s] != grp[s - 1]) { flag[s] = 1; return; }
-    int g0 = grp_first_pos[s];
-    flag[s] = ((seg_start[s] - g0) / unit_entries != (seg_start[s - 1] - g0) / unit_entries) ? 1 : 0;
-}
-
-// first segment start of every segment's group (segments of a group are contiguous)
-__global__ void grp_first_k(const int32_t *grp, const int32_t *seg_start, int32_t n_seg,
-                            int32_t *grp_first_pos)
-{
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n_seg) return;
-    // binary search the first segment with the same group
-    int lo = 0, hi = s;
-    while (lo < hi) {
-        int mid = (lo + hi) / 2;
-        if (grp[mid] < grp[s]) lo = mid + 1; else hi = mid;
-    }
-    grp_first_pos[s] = seg_start[lo];
-}
-
-__global__ void unit_collect_k(const int32_t *flag, const int32_t *incl, int32_t n_seg,
-                               int32_t *u_seg)
-{
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n_seg || !flag[s]) return;
-    u_seg[incl[s] - 1] = s;
-}
-
-__global__ void unit_st_k(const int32_t *u_seg, const int32_t *seg_key, int32_t n_units,
-                          int32_t n_rows, int32_t *u_st)
-{
-    int u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= n_units) return;
-    u_st[u] = seg_key[u_seg[u]] / n_rows;
-}
-
-// stbu[st*(m+1)+i] = first unit of (tile st, block >= i)
-__global__ void stbu_k(const int32_t *seg_key, int32_t n_seg, const int32_t *u_seg, int32_t n_units,
-                       const int32_t *rbp, int m, int32_t n_st, int32_t n_rows, int32_t *stbu)
+// stbs[st*(m+1)+i] = first slice of (tile st, row block >= i)
+__global__ void stbs_k(const int32_t *slice_gid, int32_t n_slices, int m, int32_t n_st,
+                       int32_t *stbs)
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_st * (m + 1)) return;
-    int st = t / (m + 1), i = t % (m + 1);
-    int32_t key = st * n_rows + rbp[i];
-    int64_t s = lb_i32(seg_key, 0, n_seg, key);
-    stbu[t] = (int32_t)lb_i32(u_seg, 0, n_units, (int32_t)s);
+    stbs[t] = (int32_t)lb_i32(slice_gid, 0, n_slices, t);
 }
 
 // rows -> segments in tile order: sort segment ids by row*n_st + tile
@@ -304,19 +309,18 @@ __global__ void tile_bounds_k(const uint64_t *u, int64_t nu, const int32_t *rfla
 }
 
 __global__ void ranges_k(const uint64_t *u, int64_t nu, const int32_t *rflag, const int32_t *rincl,
-                         const int32_t *tile_u0, int32_t *band_start, int32_t *band_pre,
-                         int32_t *band_len)
+                         const int32_t *tile_u0, int2 *band_meta)
 {
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= nu || !rflag[q]) return;
     int k = rincl[q] - 1;
     int t = (int)(u[q] >> 32);
-    band_start[k] = (int32_t)(uint32_t)u[q];
-    band_pre[k] = (int32_t)(q - tile_u0[t]);
+    const int32_t g0 = (int32_t)(uint32_t)u[q];
+    const int32_t pre = (int32_t)(q - tile_u0[t]);
     // length: up to the next range start
     int64_t e = q + 1;
     while (e < nu && !rflag[e]) ++e;
-    band_len[k] = (int32_t)(e - q);
+    band_meta[k] = make_int2(g0, (int32_t)(((uint32_t)pre << 16) | (uint32_t)(e - q)));
 }
 
 template <typename V>
@@ -469,20 +473,20 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
                     const double *vals64, const int32_t *cols_c, const int32_t *indptr_c,
                     const int32_t *l2g, const int32_t *rbp, const std::vector<int32_t> &c2d_h,
                     const std::vector<int32_t> &st_ptr_h, const std::vector<int32_t> &corder_h,
-                    int unit_entries, PanelDev &P, std::vector<void *> &keep, std::string &err,
+                    int tile_cols, PanelDev &P, std::vector<void *> &keep, std::string &err,
                     cudaStream_t s)
 {
     std::vector<void *> tmp;
     Alloc K{&keep, &err}, T{&tmp, &err};
     const int vs = dtype == 0 ? 8 : 4;
     const int32_t n_st = (int32_t)st_ptr_h.size() - 1;
-    const int32_t n_tiles = (int32_t)((corder_h.size() + 15) / 16);
+    const int32_t n_tiles = (int32_t)((corder_h.size() + tile_cols - 1) / tile_cols);
 
     // host tables -> device
     std::vector<int32_t> d2st_h(n_cols), tile_of_d_h(n_cols);
     for (int st = 0; st < n_st; ++st)
         for (int d = st_ptr_h[st]; d < st_ptr_h[st + 1]; ++d) d2st_h[d] = st;
-    for (size_t q = 0; q < corder_h.size(); ++q) tile_of_d_h[corder_h[q]] = (int32_t)(q / 16);
+    for (size_t q = 0; q < corder_h.size(); ++q) tile_of_d_h[corder_h[q]] = (int32_t)(q / tile_cols);
     int32_t *c2d = T.get<int32_t>(n_cols), *d2st = T.get<int32_t>(n_cols);
     int32_t *tile_of_d = T.get<int32_t>(n_cols);
     int32_t *st_ptr = K.get<int32_t>(n_st + 1), *corder = K.get<int32_t>(n_cols);
@@ -512,62 +516,70 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
         n_seg = read1(incl + nnz - 1, s);
     }
     int32_t *seg_first = T.get<int32_t>(n_seg + 1), *seg_key = K.get<int32_t>(n_seg + 1);
-    int32_t *len4 = T.get<int32_t>(n_seg + 1), *seg_start = K.get<int32_t>(n_seg + 1);
-    LNN(seg_first); LNN(seg_key); LNN(len4); LNN(seg_start);
-    int64_t fwd_cap = 0;
+    int32_t *seg_len = K.get<int32_t>(n_seg + 1), *nvec = T.get<int32_t>(n_seg + 1);
+    int32_t *seg_slice = K.get<int32_t>(n_seg + 1), *seg_lane = K.get<int32_t>(n_seg + 1);
+    uint64_t *skey0 = T.get<uint64_t>(n_seg + 1), *skey1 = T.get<uint64_t>(n_seg + 1);
+    int32_t *sid0 = T.get<int32_t>(n_seg + 1), *sseg = T.get<int32_t>(n_seg + 1);
+    int32_t *sflag = T.get<int32_t>(n_seg + 1), *sincl = T.get<int32_t>(n_seg + 1);
+    LNN(seg_first); LNN(seg_key); LNN(seg_len); LNN(nvec); LNN(seg_slice); LNN(seg_lane);
+    LNN(skey0); LNN(skey1); LNN(sid0); LNN(sseg); LNN(sflag); LNN(sincl);
+    int32_t n_slices = 0;
     if (n_seg > 0) {
         seg_first_k<<<nb(nnz, 256), 256, 0, s>>>(flag, incl, skey, nnz, seg_first, seg_key);
-        seg_len4_k<<<nb(n_seg + 1, 256), 256, 0, s>>>(seg_first, n_seg, nnz, len4);
-        LCK(scan_i32(len4, seg_start, n_seg + 1, false, tmp, s));
-        fwd_cap = read1(seg_start + n_seg, s);
+        seg_len_k<<<nb(n_seg, 256), 256, 0, s>>>(seg_first, n_seg, nnz, seg_len, nvec);
+        sell_key_k<<<nb(n_seg, 256), 256, 0, s>>>(seg_key, nvec, n_seg, n_rows, rbp, m, skey0);
+        iota_k<<<nb(n_seg, 256), 256, 0, s>>>(sid0, n_seg);
+        {
+            size_t b = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, b, skey0, skey1, sid0, sseg, (int)n_seg, 0, 64, s);
+            void *tt = T.get<char>((int64_t)b + 16);
+            LNN(tt);
+            LCK(cub::DeviceRadixSort::SortPairs(tt, b, skey0, skey1, sid0, sseg, (int)n_seg, 0, 64, s));
+        }
+        slice_flag_k<<<nb(n_seg, 256), 256, 0, s>>>(skey1, n_seg, sflag);
+        LCK(scan_i32(sflag, sincl, n_seg, true, tmp, s));
+        n_slices = read1(sincl + n_seg - 1, s);
+    }
+    int32_t *sl_seg = K.get<int32_t>((int64_t)n_slices * 32 + 1);
+    int32_t *slice_len = T.get<int32_t>(n_slices + 1), *slice_start = K.get<int32_t>(n_slices + 1);
+    int32_t *slice_gid = K.get<int32_t>(n_slices + 1);
+    int32_t *stbs = K.get<int32_t>((int64_t)n_st * (m + 1) + 1);
+    LNN(sl_seg); LNN(slice_len); LNN(slice_start); LNN(slice_gid); LNN(stbs);
+    LCK(cudaMemsetAsync(sl_seg, 0xff, 4 * ((int64_t)n_slices * 32 + 1), s));
+    int64_t fwd_cap = 0;
+    if (n_slices > 0) {
+        slice_info_k<<<nb(n_seg, 256), 256, 0, s>>>(skey1, sseg, sincl, nvec, n_seg, seg_slice,
+                                                    seg_lane, sl_seg, slice_len, slice_gid);
+        LCK(cudaMemsetAsync(slice_len + n_slices, 0, 4, s));
+        LCK(scan_i32(slice_len, slice_start, n_slices + 1, false, tmp, s));
+        fwd_cap = read1(slice_start + n_slices, s);
     } else {
-        LCK(cudaMemsetAsync(seg_start, 0, 4, s));
+        LCK(cudaMemsetAsync(slice_start, 0, 4, s));
+    }
+    if (fwd_cap >= (1ll << 31)) {
+        err = "panel forward store exceeds 2^31 entries";
+        release(tmp);
+        return -1;
     }
     void *fvals = K.get<char>(std::max<int64_t>(fwd_cap, 1) * vs);
     uint16_t *fidx = K.get<uint16_t>(fwd_cap);
-    int64_t nwords = fwd_cap / 128 + 1;
-    uint32_t *fbits = K.get<uint32_t>(nwords);
-    int32_t *seg_row = K.get<int32_t>(n_seg + 1);
-    LNN(fvals); LNN(fidx); LNN(fbits); LNN(seg_row);
-    LCK(cudaMemsetAsync(fbits, 0, 4 * nwords, s));
-    if (n_seg > 0) {
+    LNN(fvals); LNN(fidx);
+    if (n_slices > 0) {
         if (dtype == 0) {
-            fwd_scatter_k<double><<<nb(nnz, 256), 256, 0, s>>>(perm, incl, seg_first, seg_start,
-                seg_key, vals64, cols_c, c2d, st_ptr, n_rows, nnz, (double *)fvals, fidx);
-            fwd_pad_k<double><<<nb(n_seg, 256), 256, 0, s>>>(seg_first, seg_start, seg_key, n_seg,
-                nnz, n_rows, (double *)fvals, fidx, fbits, seg_row);
+            sell_scatter_k<double><<<nb(nnz, 256), 256, 0, s>>>(perm, incl, seg_first, seg_key,
+                seg_slice, seg_lane, slice_start, vals64, cols_c, c2d, st_ptr, n_rows, nnz,
+                (double *)fvals, fidx);
+            sell_pad_k<double><<<nb((int64_t)n_slices * 32, 256), 256, 0, s>>>(sl_seg, seg_len,
+                slice_start, n_slices, (double *)fvals, fidx);
         } else {
-            fwd_scatter_k<float><<<nb(nnz, 256), 256, 0, s>>>(perm, incl, seg_first, seg_start,
-                seg_key, vals64, cols_c, c2d, st_ptr, n_rows, nnz, (float *)fvals, fidx);
-            fwd_pad_k<float><<<nb(n_seg, 256), 256, 0, s>>>(seg_first, seg_start, seg_key, n_seg,
-                nnz, n_rows, (float *)fvals, fidx, fbits, seg_row);
+            sell_scatter_k<float><<<nb(nnz, 256), 256, 0, s>>>(perm, incl, seg_first, seg_key,
+                seg_slice, seg_lane, slice_start, vals64, cols_c, c2d, st_ptr, n_rows, nnz,
+                (float *)fvals, fidx);
+            sell_pad_k<float><<<nb((int64_t)n_slices * 32, 256), 256, 0, s>>>(sl_seg, seg_len,
+                slice_start, n_slices, (float *)fvals, fidx);
         }
     }
-    // units
-    int32_t *grp = T.get<int32_t>(n_seg + 1), *gfirst = T.get<int32_t>(n_seg + 1);
-    int32_t *uflag = T.get<int32_t>(n_seg + 1), *uincl = T.get<int32_t>(n_seg + 1);
-    LNN(grp); LNN(gfirst); LNN(uflag); LNN(uincl);
-    int32_t n_units = 0;
-    if (n_seg > 0) {
-        unit_flag_k<<<nb(n_seg, 256), 256, 0, s>>>(seg_key, seg_start, n_seg, n_rows, rbp, m,
-                                                   unit_entries, grp, uflag);
-        grp_first_k<<<nb(n_seg, 256), 256, 0, s>>>(grp, seg_start, n_seg, gfirst);
-        unit_flag2_k<<<nb(n_seg, 256), 256, 0, s>>>(grp, seg_start, n_seg, unit_entries, gfirst,
-                                                    uflag);
-        LCK(scan_i32(uflag, uincl, n_seg, true, tmp, s));
-        n_units = read1(uincl + n_seg - 1, s);
-    }
-    int32_t *u_seg = K.get<int32_t>(n_units + 1), *u_st = K.get<int32_t>(n_units + 1);
-    int32_t *stbu = K.get<int32_t>((int64_t)n_st * (m + 1) + 1);
-    LNN(u_seg); LNN(u_st); LNN(stbu);
-    if (n_units > 0) {
-        unit_collect_k<<<nb(n_seg, 256), 256, 0, s>>>(uflag, uincl, n_seg, u_seg);
-        unit_st_k<<<nb(n_units, 256), 256, 0, s>>>(u_seg, seg_key, n_units, n_rows, u_st);
-    }
-    LCK(cudaMemcpyAsync(u_seg + n_units, &n_seg, 4, cudaMemcpyHostToDevice, s));
-    LCK(cudaStreamSynchronize(s));  // &n_seg is a host stack value
-    stbu_k<<<nb((int64_t)n_st * (m + 1), 128), 128, 0, s>>>(seg_key, n_seg, u_seg, n_units, rbp, m,
-                                                           n_st, n_rows, stbu);
+    stbs_k<<<nb((int64_t)n_st * (m + 1), 128), 128, 0, s>>>(slice_gid, n_slices, m, n_st, stbs);
     // rows -> segments (tile order)
     int32_t *rkey = T.get<int32_t>(n_seg + 1), *srkey = T.get<int32_t>(n_seg + 1);
     int32_t *sid = T.get<int32_t>(n_seg + 1), *rseg = K.get<int32_t>(n_seg + 1);
@@ -617,13 +629,12 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
         LCK(scan_i32(rflag, rincl, nu, true, tmp, s));
         n_ranges = read1(rincl + nu - 1, s);
     }
-    int32_t *band_ptr = K.get<int32_t>(n_tiles + 1), *band_start = K.get<int32_t>(n_ranges + 1);
-    int32_t *band_pre = K.get<int32_t>(n_ranges + 1), *band_len = K.get<int32_t>(n_ranges + 1);
-    LNN(band_ptr); LNN(band_start); LNN(band_pre); LNN(band_len);
+    int32_t *band_ptr = K.get<int32_t>(n_tiles + 1);
+    int2 *band_meta = K.get<int2>(n_ranges + 1);
+    LNN(band_ptr); LNN(band_meta);
     tile_bounds_k<<<nb(n_tiles + 1, 128), 128, 0, s>>>(uk, nu, rincl, n_tiles, tile_u0, band_ptr);
     if (n_ranges > 0)
-        ranges_k<<<nb(nu, 256), 256, 0, s>>>(uk, nu, rflag, rincl, tile_u0, band_start, band_pre,
-                                             band_len);
+        ranges_k<<<nb(nu, 256), 256, 0, s>>>(uk, nu, rflag, rincl, tile_u0, band_meta);
     // the widest band sets the shared-memory size
     std::vector<int32_t> tu(n_tiles + 1);
     LCK(cudaMemcpyAsync(tu.data(), tile_u0, 4 * (n_tiles + 1), cudaMemcpyDeviceToHost, s));
@@ -661,26 +672,24 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
 
     P.fvals = fvals;
     P.fidx = fidx;
-    P.fbits = fbits;
-    P.seg_start = seg_start;
+    P.slice_start = slice_start;
+    P.sl_seg = sl_seg;
+    P.stbs = stbs;
     P.seg_key = seg_key;
-    P.u_seg = u_seg;
-    P.u_st = u_st;
-    P.stbu = stbu;
+    P.seg_len = seg_len;
+    P.seg_slice = seg_slice;
+    P.seg_lane = seg_lane;
     P.st_ptr = st_ptr;
     P.rseg_ptr = rseg_ptr;
     P.rseg = rseg;
-    P.seg_row = seg_row;
     P.tvals = tvals;
     P.tloc = tloc;
     P.cptr = cptr;
     P.corder = corder;
     P.band_ptr = band_ptr;
-    P.band_start = band_start;
-    P.band_pre = band_pre;
-    P.band_len = band_len;
+    P.band_meta = band_meta;
     P.n_seg = n_seg;
-    P.n_units = n_units;
+    P.n_slices = n_slices;
     P.n_st = n_st;
     P.n_tiles = n_tiles;
     P.band_max = band_max;
@@ -689,6 +698,7 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     P.st_max = st_max;
     P.fwd_cap = fwd_cap;
     P.csc_cap = csc_cap;
+    P.tile_cols = tile_cols;
     return 0;
 }
 
