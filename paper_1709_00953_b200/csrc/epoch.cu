@@ -228,11 +228,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // range (range broadcast by shuffle, element e by lane e: 8-byte cp.async).
 struct BandMeta {
     int2 m[2];
+    int k0, k1;
 };
 
 __device__ __forceinline__ void band_meta_load(const PanelDev &P, int t, BandMeta &bm)
 {
     const int k0 = __ldg(P.band_ptr + t), k1 = __ldg(P.band_ptr + t + 1);
+    bm.k0 = k0;
+    bm.k1 = k1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int it = 0; it < 2; ++it) {
@@ -241,10 +244,10 @@ __device__ __forceinline__ void band_meta_load(const PanelDev &P, int t, BandMet
     }
 }
 
-__device__ __forceinline__ void band_issue(const PanelDev &P, int t, const BandMeta &bm,
-                                           const double *r, double *buf)
+__device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm, const double *r,
+                                           double *buf)
 {
-    const int k0 = __ldg(P.band_ptr + t), k1 = __ldg(P.band_ptr + t + 1);
+    const int k0 = bm.k0, k1 = bm.k1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int it = 0; it < 2; ++it) {
@@ -309,34 +312,49 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         const double *xj = p.x + P.x_off;
 
         // ---- phase 1: g = A_I^T r_I, tile bands in shared memory ----------
-        // tiles round-robin over CTAs; the band of the next tile is copied
-        // (cp.async) into the second buffer while this tile is computed
+        // Work items are whole tiles in rounds of gridDim.x; the tiles left for
+        // the last round are split into column parts so every CTA gets the
+        // same share.  The band of the next item is copied (cp.async) into the
+        // second buffer while the current item is computed.
         double wsum = 0.0;
         {
             const V *tv = static_cast<const V *>(P.tvals);
             const int TC = P.tile_cols;
+            const int G = gridDim.x;
+            const int full = P.n_tiles / G, rem = P.n_tiles - full * G;
+            const int S = rem > 0 ? max(1, G / rem) : 1;
+            const int n_items = full + ((int)blockIdx.x < rem * S ? 1 : 0);
+            auto item_tile = [&](int it) {
+                return it < full ? (int)blockIdx.x + it * G : full * G + (int)blockIdx.x / S;
+            };
             const bool dbuf = p.band_dbuf != 0;
             double *buf0 = rs, *buf1 = rs + (dbuf ? p.band_cap : 0);
-            int t = blockIdx.x;
             BandMeta bm;
-            if (t < P.n_tiles) {
-                band_meta_load(P, t, bm);
-                band_issue(P, t, bm, p.r, buf0);
+            if (n_items > 0) {
+                band_meta_load(P, item_tile(0), bm);
+                band_issue(P, bm, p.r, buf0);
                 cp_async_commit();
-                if (t + (int)gridDim.x < P.n_tiles) band_meta_load(P, t + gridDim.x, bm);
+                if (n_items > 1) band_meta_load(P, item_tile(1), bm);
             }
             int cur = 0;
-            for (; t < P.n_tiles; t += gridDim.x) {
+            for (int it = 0; it < n_items; ++it) {
                 cp_async_wait_all();
                 __syncthreads();
-                const int tn = t + gridDim.x;
-                double *bt = cur ? buf1 : buf0;
-                if (dbuf && tn < P.n_tiles) {
-                    band_issue(P, tn, bm, p.r, cur ? buf0 : buf1);
-                    cp_async_commit();
-                    if (tn + (int)gridDim.x < P.n_tiles) band_meta_load(P, tn + gridDim.x, bm);
+                const int t = item_tile(it);
+                int c0 = 0, c1 = TC;
+                if (it >= full) {
+                    const int part = (int)blockIdx.x % S;
+                    c0 = part * TC / S;
+                    c1 = (part + 1) * TC / S;
                 }
-                for (int qc = t * TC + warp; qc < min((t + 1) * TC, P.n_cols); qc += WARPS) {
+                double *bt = cur ? buf1 : buf0;
+                if (dbuf && it + 1 < n_items) {
+                    band_issue(P, bm, p.r, cur ? buf0 : buf1);
+                    cp_async_commit();
+                    if (it + 2 < n_items) band_meta_load(P, item_tile(it + 2), bm);
+                }
+                const int q_end = min(t * TC + c1, P.n_cols);
+                for (int qc = t * TC + c0 + warp; qc < q_end; qc += WARPS) {
                     const int d = __ldg(P.corder + qc);
                     const int32_t *cp = P.cptr + (int64_t)d * (m + 1);
                     double acc = 0.0;
@@ -362,10 +380,10 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 __syncthreads();
                 if (dbuf) {
                     cur ^= 1;
-                } else if (tn < P.n_tiles) {
-                    band_issue(P, tn, bm, p.r, buf0);
+                } else if (it + 1 < n_items) {
+                    band_issue(P, bm, p.r, buf0);
                     cp_async_commit();
-                    if (tn + (int)gridDim.x < P.n_tiles) band_meta_load(P, tn + gridDim.x, bm);
+                    if (it + 2 < n_items) band_meta_load(P, item_tile(it + 2), bm);
                 }
             }
         }

@@ -37,6 +37,8 @@ namespace {
 
 inline unsigned nb(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
+constexpr int SEG_CAP = 64;   // max entries of one forward segment
+
 int bits_for(int64_t v)
 {
     int b = 1;
@@ -87,11 +89,18 @@ __global__ void fwd_key_k(const int32_t *cols_c, const int32_t *rowid, const int
 }
 
 // 1 where a new segment starts in sorted order
-__global__ void seg_flag_k(const int32_t *skey, int64_t nnz, int32_t *flag)
+// (a (row, super tile) group longer than cap entries is cut into several
+// segments so that no SELL slice is much longer than its neighbours)
+__global__ void seg_flag_k(const int32_t *skey, int64_t nnz, int cap, int32_t *flag)
 {
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= nnz) return;
-    flag[q] = (q == 0 || skey[q] != skey[q - 1]) ? 1 : 0;
+    if (q == 0 || skey[q] != skey[q - 1]) {
+        flag[q] = 1;
+        return;
+    }
+    int64_t lo = lb_i32(skey, 0, q, skey[q]);
+    flag[q] = ((q - lo) % cap == 0) ? 1 : 0;
 }
 
 // segment s: first sorted position, key; (seg id = inclusive scan - 1)
@@ -511,7 +520,7 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     if (nnz > 0) {
         fwd_key_k<<<nb(nnz, 256), 256, 0, s>>>(cols_c, rowid, c2d, d2st, n_rows, nnz, key);
         LCK(sort_pairs<int32_t>(key, skey, iota, perm, nnz, bits_for((int64_t)n_st * n_rows), tmp, s));
-        seg_flag_k<<<nb(nnz, 256), 256, 0, s>>>(skey, nnz, flag);
+        seg_flag_k<<<nb(nnz, 256), 256, 0, s>>>(skey, nnz, SEG_CAP, flag);
         LCK(scan_i32(flag, incl, nnz, true, tmp, s));
         n_seg = read1(incl + nnz - 1, s);
     }

@@ -57,6 +57,14 @@ def main():
         if k < 3 or k == nt - 1:
             print(f"{k:4d} " + " ".join(f"{v:6.1f}" for v in row) + f" {t[6].max() - start:7.1f}")
     print("mean " + " ".join(f"{v / nt:6.1f}" for v in tot))
+    d1 = (tl[:, 1, :] - tl[:, 0, :]).ravel()
+    d2 = (tl[:, 3, :] - tl[:, 2, :]).ravel()
+    for name, d in (("p1 per block", d1), ("p2a per block", d2)):
+        q = np.percentile(d, [0, 10, 50, 90, 100])
+        print(f"{name:14s} min {q[0]:6.1f} p10 {q[1]:6.1f} med {q[2]:6.1f} p90 {q[3]:6.1f} max {q[4]:6.1f}")
+    k = 0
+    d2k = tl[k, 3, :] - tl[k, 2, :]
+    print("task 0 p2a by block (every 8th):", " ".join(f"{v:.0f}" for v in d2k[::8]))
 
 
 if __name__ == "__main__":
