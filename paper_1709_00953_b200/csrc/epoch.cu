@@ -29,11 +29,26 @@
 // grid.
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 #include "internal.h"
 
 namespace {
 
+#ifndef BCT_EXP
+#define BCT_EXP 0
+#endif
+#ifndef BCT_PLAIN_STAGE
+#define BCT_PLAIN_STAGE 0
+#endif
+#ifndef BCT_P1_UNROLL
+#define BCT_P1_UNROLL 2
+#endif
+#ifndef BCT_P2_UNROLL
+#define BCT_P2_UNROLL 4
+#endif
+constexpr int P1U = BCT_P1_UNROLL;
+constexpr int P2U = BCT_P2_UNROLL;
 constexpr int BLOCK = 1024;         // one CTA per SM
 constexpr int WARPS = BLOCK / 32;
 constexpr int MAX_RUNS = BCT_MAX_M / 2 + 1;
@@ -172,10 +187,66 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
     }
 }
 
+// streamed panel data is read once per task: keep it from evicting the
+// residual / gradient vectors that must stay in L2
+#ifndef BCT_STREAM_HINT
+#define BCT_STREAM_HINT 1
+#endif
+__device__ __forceinline__ uint64_t evict_first_policy()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ float4 ld_stream(const float4 *p)
+{
+#if BCT_STREAM_HINT
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(evict_first_policy()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double2 ld_stream(const double2 *p)
+{
+#if BCT_STREAM_HINT
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(evict_first_policy()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p)
+{
+#if BCT_STREAM_HINT
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(evict_first_policy()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ uint2 ld_stream(const uint2 *p)
+{
+#if BCT_STREAM_HINT
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(evict_first_policy()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 __device__ __forceinline__ void ld8v(const float *p, double v[8])
 {
-    float4 a = __ldg(reinterpret_cast<const float4 *>(p));
-    float4 b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+    float4 a = ld_stream(reinterpret_cast<const float4 *>(p));
+    float4 b = ld_stream(reinterpret_cast<const float4 *>(p) + 1);
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
     v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
@@ -183,31 +254,31 @@ __device__ __forceinline__ void ld8v(const double *p, double v[8])
 {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        double2 a = __ldg(reinterpret_cast<const double2 *>(p) + q);
+        double2 a = ld_stream(reinterpret_cast<const double2 *>(p) + q);
         v[2 * q] = a.x;
         v[2 * q + 1] = a.y;
     }
 }
 __device__ __forceinline__ void ld8u16(const uint16_t *p, int k[8])
 {
-    uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
+    uint4 a = ld_stream(reinterpret_cast<const uint4 *>(p));
     k[0] = a.x & 0xffff; k[1] = a.x >> 16; k[2] = a.y & 0xffff; k[3] = a.y >> 16;
     k[4] = a.z & 0xffff; k[5] = a.z >> 16; k[6] = a.w & 0xffff; k[7] = a.w >> 16;
 }
 __device__ __forceinline__ void ld4v(const float *p, double v[4])
 {
-    float4 a = __ldg(reinterpret_cast<const float4 *>(p));
+    float4 a = ld_stream(reinterpret_cast<const float4 *>(p));
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
 }
 __device__ __forceinline__ void ld4v(const double *p, double v[4])
 {
-    double2 a = __ldg(reinterpret_cast<const double2 *>(p));
-    double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+    double2 a = ld_stream(reinterpret_cast<const double2 *>(p));
+    double2 b = ld_stream(reinterpret_cast<const double2 *>(p) + 1);
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 __device__ __forceinline__ void ld4u16(const uint16_t *p, int k[4])
 {
-    uint2 a = __ldg(reinterpret_cast<const uint2 *>(p));
+    uint2 a = ld_stream(reinterpret_cast<const uint2 *>(p));
     k[0] = a.x & 0xffff; k[1] = a.x >> 16; k[2] = a.y & 0xffff; k[3] = a.y >> 16;
 }
 
@@ -247,6 +318,9 @@ __device__ __forceinline__ void band_meta_load(const PanelDev &P, int t, BandMet
 __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm, const double *r,
                                            double *buf)
 {
+#if BCT_EXP == 3
+    return;
+#endif
     const int k0 = bm.k0, k1 = bm.k1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
@@ -257,7 +331,11 @@ __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm
             const int g0 = __shfl_sync(0xffffffffu, bm.m[it].x, jj);
             const int pk = __shfl_sync(0xffffffffu, bm.m[it].y, jj);
             const int pre = (int)((unsigned)pk >> 16), len = pk & 0xffff;
+#if BCT_PLAIN_STAGE
+            for (int e = lane; e < len; e += 32) buf[pre + e] = r[g0 + e];
+#else
             for (int e = lane; e < len; e += 32) cp_async8(buf + pre + e, r + g0 + e);
+#endif
         }
     }
     // ranges beyond 2*BLOCK per tile (not expected): plain loads
@@ -295,7 +373,9 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     double *part_den = p.part + gridDim.x;
     double *part_m = p.part + 2 * gridDim.x;
     double *rs = reinterpret_cast<double *>(dyn_smem);   // phase 1 band
-    double2 *gs = reinterpret_cast<double2 *>(dyn_smem); // phase 2 super tile
+    // phase 2 super tile: (g, x) pairs, float2 when values are float (FP32 mode)
+    using GS = typename std::conditional<sizeof(V) == 4, float2, double2>::type;
+    GS *gs = reinterpret_cast<GS *>(dyn_smem);
 
     for (int k = 0; k < n_tasks; ++k) {
         __syncthreads();  // sT/sP/R of the previous task may still be in use
@@ -354,13 +434,14 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                     if (it + 2 < n_items) band_meta_load(P, item_tile(it + 2), bm);
                 }
                 const int q_end = min(t * TC + c1, P.n_cols);
+#if BCT_EXP != 4
                 for (int qc = t * TC + c0 + warp; qc < q_end; qc += WARPS) {
                     const int d = __ldg(P.corder + qc);
                     const int32_t *cp = P.cptr + (int64_t)d * (m + 1);
                     double acc = 0.0;
                     for (int kr = 0; kr < R.n; ++kr) {
                         const int s = __ldg(cp + R.i0[kr]), e = __ldg(cp + R.i1[kr]);
-#pragma unroll 2
+#pragma unroll P1U
                         for (int i = (s & ~7) + 8 * lane; i < e; i += 256) {
                             int loc[8];
                             double v[8];
@@ -377,6 +458,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                         wsum = fma(acc, acc, wsum);
                     }
                 }
+#endif
                 __syncthreads();
                 if (dbuf) {
                     cur ^= 1;
@@ -428,25 +510,37 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 while (fu >= R.st_pre[st + 1]) ++st;
                 const int ge = min(ue, R.st_pre[st + 1]);
                 const int v0 = __ldg(P.st_ptr + st), v1 = __ldg(P.st_ptr + st + 1);
-                for (int q = threadIdx.x; q < v1 - v0; q += BLOCK) gs[q] = gx[v0 + q];
+                for (int q = threadIdx.x; q < v1 - v0; q += BLOCK) {
+                    const double2 a = gx[v0 + q];
+                    gs[q] = GS{(decltype(GS::x))a.x, (decltype(GS::x))a.y};
+                }
                 __syncthreads();
                 for (int f = fu + warp; f < ge; f += WARPS) {
                     const int sl = R.full ? f : task_slice(R, P, m, f, st);
                     const int base = __ldg(P.slice_start + sl);
                     const int nvec = (__ldg(P.slice_start + sl + 1) - base) >> 7;
                     double t = 0.0, ax = 0.0;
-#pragma unroll 4
+#pragma unroll P2U
                     for (int kv = 0; kv < nvec; ++kv) {
                         const int i = base + ((kv * 32 + lane) << 2);
                         int cc[4];
                         double v[4];
+#if BCT_EXP == 2
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) { cc[q] = (i * 13 + q * 7) & 4095; v[q] = 1.0; }
+#else
                         ld4u16(P.fidx + i, cc);
                         ld4v(fv + i, v);
+#endif
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const double2 a = gs[cc[q]];
-                            t = fma(v[q], a.x, t);
-                            ax = fma(v[q], a.y, ax);
+#if BCT_EXP == 1
+                            const double2 a = make_double2((double)cc[q], 1.0);
+#else
+                            const GS a = gs[cc[q]];
+#endif
+                            t = fma(v[q], (double)a.x, t);
+                            ax = fma(v[q], (double)a.y, ax);
                         }
                     }
                     const int seg = __ldg(P.sl_seg + (int64_t)sl * 32 + lane);
