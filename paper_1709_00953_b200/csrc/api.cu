@@ -84,6 +84,10 @@ struct bct_ctx {
     double *x_true = nullptr;
     int32_t *counts = nullptr;
     double *gx = nullptr, *t_ax = nullptr, *seg_part = nullptr, *part = nullptr;
+    // epoch-batched parallel path scratch (grow-only)
+    double *gx_batch = nullptr, *seg_batch = nullptr, *tax_batch = nullptr, *part_task = nullptr;
+    int64_t gx_batch_n = 0, seg_batch_n = 0, tax_batch_n = 0, part_task_n = 0;
+    std::vector<std::vector<int32_t>> h_stbs;  // per panel (n_st*(m+1)) first slice table
     double *mus = nullptr, *exchange = nullptr, *vec = nullptr;
     int32_t *statuses = nullptr;
     EpochOut *out = nullptr;
@@ -326,7 +330,7 @@ int finalize(bct_ctx *c)
     // two band buffers when they fit, else one (staging then serializes)
     c->band_dbuf = 2 * (size_t)c->band_cap * 8 <= SMEM_BUDGET ? 1 : 0;
     c->smem = std::max<size_t>(c->smem, (size_t)c->band_cap * 8 * (c->band_dbuf ? 2 : 1));
-    c->smem = std::max<size_t>(c->smem, 16);
+    c->smem = std::max<size_t>(c->smem, 1024 * 12 + 64);
     if (c->smem > 227 * 1024)
         return fail(c, BCT_EINVAL, "shared-memory need %zu B exceeds the SM (band %d slots)",
                     c->smem, c->band_cap);
@@ -400,6 +404,8 @@ void destroy(bct_ctx *c)
     if (c->mus) cudaFree(c->mus);
     if (c->statuses) cudaFree(c->statuses);
     if (c->timeline) cudaFree(c->timeline);
+    for (double *q : {c->gx_batch, c->seg_batch, c->tax_batch, c->part_task})
+        if (q) cudaFree(q);
     if (c->h_tasks) cudaFreeHost(c->h_tasks);
     if (c->h_hdr) cudaFreeHost(c->h_hdr);
     for (int s = 0; s < RING; ++s) {
@@ -982,6 +988,8 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits)
     p.hdr = c->d_hdr; p.tasks = c->d_tasks; p.gx = c->gx; p.gx_stride = 2 * c->max_cols;
     p.t_ax = c->t_ax; p.seg_part = c->seg_part; p.part = c->part; p.mus = c->mus;
     p.band_cap = c->band_cap; p.band_dbuf = c->band_dbuf;
+    p.gx_batch = c->gx_batch; p.seg_batch = c->seg_batch; p.tax_batch = c->tax_batch;
+    p.part_task = c->part_task;
     p.statuses = c->statuses; p.out = c->out;
     p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
     p.timeline = nullptr;
@@ -1080,12 +1088,60 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
     }
     int r = ensure_task_cap(c, std::max<int64_t>(nt, 1));
     if (r) return r;
+    // epoch-batched path: parallel epoch whose tasks are all full panels
+    bool batched = mode == BCT_PARALLEL && nt > 0 && nt <= 1024 && !getenv("BCT_NO_BATCH");
+    uint64_t full[BCT_MASKW] = {0, 0, 0, 0};
+    for (int i = 0; i < c->m; ++i) set_mask(full, i);
+    for (int64_t k = 0; batched && k < nt; ++k)
+        if (memcmp(tasks[k].mask, full, sizeof full) != 0) batched = false;
+    int64_t tot_tiles = 0, tot_slices = 0, tot_rows = 0, tot_vox = 0, gxo = 0, sgo = 0, txo = 0;
+    if (batched) {
+        for (int64_t k = 0; k < nt; ++k) {
+            TaskDev &T = tasks[k];
+            const PanelDev &P = c->h_panels[T.lp];
+            T.tile_pre = (int32_t)tot_tiles;
+            T.slice_pre = (int32_t)tot_slices;
+            T.row_pre = (int32_t)tot_rows;
+            T.vox_pre = (int32_t)tot_vox;
+            T.gx_off = gxo;
+            T.seg_off = sgo;
+            T.tax_off = txo;
+            tot_tiles += P.n_tiles;
+            tot_slices += P.n_slices;
+            tot_rows += P.n_rows;
+            if (T.flags & TASK_FIRST_OF_VISIT) tot_vox += P.n_cols;
+            gxo += P.n_cols;
+            sgo += P.n_seg;
+            txo += P.n_rows;
+        }
+        if (tot_slices >= (1ll << 31) || tot_rows >= (1ll << 31)) batched = false;
+    }
+    if (batched) {
+        // the device may still read the old scratch: drain before growing it
+        auto grow = [&](double **ptr, int64_t *have, int64_t need) -> int {
+            if (need <= *have) return 0;
+            CK(cudaStreamSynchronize(c->stream));
+            if (*ptr) cudaFree(*ptr);
+            CK(cudaMalloc((void **)ptr, 8 * std::max<int64_t>(need, 1)));
+            *have = need;
+            return 0;
+        };
+        if ((r = grow(&c->gx_batch, &c->gx_batch_n, 2 * gxo))) return r;
+        if ((r = grow(&c->seg_batch, &c->seg_batch_n, 2 * sgo))) return r;
+        if ((r = grow(&c->tax_batch, &c->tax_batch_n, 2 * txo))) return r;
+        if ((r = grow(&c->part_task, &c->part_task_n, 2 * nt * (int64_t)c->grid))) return r;
+    }
     // the staging buffers of the previous epoch must have been consumed
     CK(cudaEventSynchronize(c->staged));
     memset(c->h_hdr, 0, sizeof(EpochHeader));
     c->h_hdr->n_tasks = (int32_t)nt;
     c->h_hdr->mode = mode;
     c->h_hdr->flags = flags;
+    c->h_hdr->batched = batched ? 1 : 0;
+    c->h_hdr->n_tiles_total = (int32_t)tot_tiles;
+    c->h_hdr->n_slices_total = (int32_t)tot_slices;
+    c->h_hdr->n_rows_total = (int32_t)tot_rows;
+    c->h_hdr->n_vox_total = (int32_t)tot_vox;
     memcpy(c->h_hdr->epoch_mask, emask, sizeof emask);
     memcpy(c->last_epoch_mask, emask, sizeof emask);
     if (nt) memcpy(c->h_tasks, tasks.data(), sizeof(TaskDev) * nt);

@@ -62,6 +62,9 @@ __device__ __forceinline__ long long gtimer()
 }
 
 // optional per-block phase timestamps: [task][8][block] (profiling only)
+#ifndef BCT_NO_TL_BATCH
+#define BCT_NO_TL_BATCH 0
+#endif
 #define TL_MARK(k, ph)                                                                \
     do {                                                                              \
         if (p.timeline && threadIdx.x == 0)                                           \
@@ -351,6 +354,278 @@ __device__ __forceinline__ double z_value(double t, double ax, double mu, int st
     return status == 0 ? fma(mu, t, ax) : ax;
 }
 
+
+// ======================================================================
+// Epoch-batched path (parallel mode, every task a full panel): all tasks
+// read the epoch-start residual and image, so each phase runs over the
+// tasks of the whole epoch at once -- one continuous, pipelined stream per
+// phase and four grid barriers per epoch instead of three per task.
+// ======================================================================
+
+__device__ __forceinline__ int task_of(const TaskDev *tasks, int n_tasks, int which, int f)
+{
+    // last task whose prefix (field `which`) is <= f
+    int lo = 0, hi = n_tasks - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) / 2;
+        const TaskDev &T = tasks[mid];
+        const int v = which == 0 ? T.tile_pre : which == 1 ? T.slice_pre : which == 2 ? T.row_pre
+                                                                               : T.vox_pre;
+        if (v <= f) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <typename V>
+__device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, double *rs, double *sh,
+                              PanelDev *ring, int *ring_task)
+{
+    if (!BCT_NO_TL_BATCH) TL_MARK(0, 0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int G = gridDim.x, b = blockIdx.x;
+    const int n_tasks = hdr.n_tasks;
+    const int m = p.m;
+    double2 *gxb = reinterpret_cast<double2 *>(p.gx_batch);
+    double2 *segb = reinterpret_cast<double2 *>(p.seg_batch);
+    double2 *taxb = reinterpret_cast<double2 *>(p.tax_batch);
+    double *pgg = p.part_task;                       // [k][G]
+    double *pden = p.part_task + (int64_t)n_tasks * G;
+
+    // ---- phase A: g = A^T r for every task, tiles round-robin over CTAs ----
+    for (int k = threadIdx.x; k < n_tasks; k += BLOCK) pgg[(int64_t)k * G + b] = 0.0;
+    {
+        const int n_items = (hdr.n_tiles_total - b + G - 1) / G;
+        const bool dbuf = p.band_dbuf != 0;
+        double *buf0 = rs, *buf1 = rs + (dbuf ? p.band_cap : 0);
+        auto load_ring = [&](int it) {   // thread 0: panel of item it into ring[it % 3]
+            const int item = b + it * G;
+            const int k = task_of(p.tasks, n_tasks, 0, item);
+            ring_task[it % 3] = k;
+            ring[it % 3] = p.panels[p.tasks[k].lp];
+        };
+        auto item_tile = [&](int it) { return b + it * G - p.tasks[ring_task[it % 3]].tile_pre; };
+        BandMeta bm;
+        if (threadIdx.x == 0) {
+            if (n_items > 0) load_ring(0);
+            if (n_items > 1) load_ring(1);
+        }
+        __syncthreads();
+        if (n_items > 0) {
+            band_meta_load(ring[0], item_tile(0), bm);
+            band_issue(ring[0], bm, p.r, buf0);
+            cp_async_commit();
+            if (n_items > 1) band_meta_load(ring[1], item_tile(1), bm);
+        }
+        int cur = 0;
+        for (int it = 0; it < n_items; ++it) {
+            cp_async_wait_all();
+            __syncthreads();
+            const PanelDev &P = ring[it % 3];
+            const int k = ring_task[it % 3];
+            const int t = item_tile(it);
+            double *bt = cur ? buf1 : buf0;
+            if (dbuf && it + 1 < n_items) {
+                band_issue(ring[(it + 1) % 3], bm, p.r, cur ? buf0 : buf1);
+                cp_async_commit();
+            }
+            if (threadIdx.x == 0 && it + 2 < n_items) load_ring(it + 2);
+            const V *tv = static_cast<const V *>(P.tvals);
+            const int TC = P.tile_cols;
+            const int q_end = min((t + 1) * TC, P.n_cols);
+            const double *xj = p.x + P.x_off;
+            double2 *gx = gxb + p.tasks[k].gx_off;
+            double wsum = 0.0;
+            for (int qc = t * TC + warp; qc < q_end; qc += WARPS) {
+                const int d = __ldg(P.corder + qc);
+                const int32_t *cp = P.cptr + (int64_t)d * (m + 1);
+                const int s = __ldg(cp), e = __ldg(cp + m);
+                double acc = 0.0;
+#pragma unroll P1U
+                for (int i = s + 8 * lane; i < e; i += 256) {
+                    int loc[8];
+                    double v[8];
+                    ld8u16(P.tloc + i, loc);
+                    ld8v(tv + i, v);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (i + u < e) acc = fma(v[u], bt[loc[u]], acc);
+                }
+                acc = warp_sum(acc);
+                if (lane == 0) {
+                    gx[d] = make_double2(acc, xj[d]);
+                    wsum = fma(acc, acc, wsum);
+                }
+            }
+            if (lane == 0) sh[warp] = wsum;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double s2 = 0.0;
+                for (int w = 0; w < WARPS; ++w) s2 += sh[w];
+                pgg[(int64_t)k * G + b] += s2;
+            }
+            if (!dbuf && it + 1 < n_items) {
+                band_issue(ring[(it + 1) % 3], bm, p.r, buf0);
+                cp_async_commit();
+            }
+            if (it + 2 < n_items) band_meta_load(ring[(it + 2) % 3], item_tile(it + 2), bm);
+            if (dbuf) cur ^= 1;
+        }
+    }
+    if (!BCT_NO_TL_BATCH) TL_MARK(0, 1);
+    grid_sync(p.bar);
+    if (!BCT_NO_TL_BATCH) TL_MARK(0, 2);
+
+    // ---- phase B: segment partials of every task (contiguous slice ranges) --
+    {
+        using GS = typename std::conditional<sizeof(V) == 4, float2, double2>::type;
+        GS *gs = reinterpret_cast<GS *>(rs);
+        const int ns = hdr.n_slices_total;
+        const int ub = (int)((int64_t)ns * b / G), ue = (int)((int64_t)ns * (b + 1) / G);
+        int fu = ub;
+        while (fu < ue) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const int k = task_of(p.tasks, n_tasks, 1, fu);
+                ring_task[0] = k;
+                ring[0] = p.panels[p.tasks[k].lp];
+            }
+            __syncthreads();
+            const PanelDev &P = ring[0];
+            const int k = ring_task[0];
+            const TaskDev &T = p.tasks[k];
+            const int sl0 = fu - T.slice_pre;          // full panel: flattened = slice id
+            // super tile of slice sl0 and the end of its slices
+            int st = 0;
+            while (__ldg(P.stbs + (st + 1) * (m + 1)) <= sl0 && st + 1 < P.n_st) ++st;
+            const int st_end = (st + 1 < P.n_st) ? __ldg(P.stbs + (st + 1) * (m + 1)) : P.n_slices;
+            const int ge = min(ue, T.slice_pre + st_end);
+            const int v0 = __ldg(P.st_ptr + st), v1 = __ldg(P.st_ptr + st + 1);
+            const double2 *gx = gxb + T.gx_off;
+            for (int q = threadIdx.x; q < v1 - v0; q += BLOCK) {
+                const double2 a = gx[v0 + q];
+                gs[q] = GS{(decltype(GS::x))a.x, (decltype(GS::x))a.y};
+            }
+            __syncthreads();
+            const V *fv = static_cast<const V *>(P.fvals);
+            double2 *spart = segb + T.seg_off;
+            for (int f = fu + warp; f < ge; f += WARPS) {
+                const int sl = f - T.slice_pre;
+                const int base = __ldg(P.slice_start + sl);
+                const int nvec = (__ldg(P.slice_start + sl + 1) - base) >> 7;
+                double t = 0.0, ax = 0.0;
+#pragma unroll P2U
+                for (int kv = 0; kv < nvec; ++kv) {
+                    const int i = base + ((kv * 32 + lane) << 2);
+                    int cc[4];
+                    double v[4];
+                    ld4u16(P.fidx + i, cc);
+                    ld4v(fv + i, v);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const GS a = gs[cc[q]];
+                        t = fma(v[q], (double)a.x, t);
+                        ax = fma(v[q], (double)a.y, ax);
+                    }
+                }
+                const int seg = __ldg(P.sl_seg + (int64_t)sl * 32 + lane);
+                if (seg >= 0) spart[seg] = make_double2(t, ax);
+            }
+            fu = ge;
+        }
+    }
+    if (!BCT_NO_TL_BATCH) TL_MARK(0, 3);
+    grid_sync(p.bar);
+    if (!BCT_NO_TL_BATCH) TL_MARK(0, 4);
+
+    // ---- phase C: rows of every task (contiguous ranges), denom partials ----
+    for (int k = threadIdx.x; k < n_tasks; k += BLOCK) pden[(int64_t)k * G + b] = 0.0;
+    __syncthreads();
+    {
+        const int nr = hdr.n_rows_total;
+        const int rb0 = (int)((int64_t)nr * b / G), rb1 = (int)((int64_t)nr * (b + 1) / G);
+        int f0 = rb0;
+        while (f0 < rb1) {
+            const int k = task_of(p.tasks, n_tasks, 2, f0);
+            const TaskDev &T = p.tasks[k];
+            const PanelDev &P = p.panels[T.lp];
+            const int f1 = min(rb1, T.row_pre + P.n_rows);
+            const double2 *spart = segb + T.seg_off;
+            double2 *tax = taxb + T.tax_off;
+            double wsum = 0.0;
+            for (int f = f0 + (int)threadIdx.x; f < f1; f += BLOCK) {
+                const int lr = f - T.row_pre;
+                double t = 0.0, ax = 0.0;
+                const int q1 = __ldg(P.rseg_ptr + lr + 1);
+                for (int q = __ldg(P.rseg_ptr + lr); q < q1; ++q) {
+                    const double2 a = spart[__ldg(P.rseg + q)];
+                    t += a.x;
+                    ax += a.y;
+                }
+                tax[lr] = make_double2(t, ax);
+                wsum = fma(t, t, wsum);
+            }
+            const double bs = block_sum_all(wsum, sh);
+            if (threadIdx.x == 0) pden[(int64_t)k * G + b] += bs;
+            f0 = f1;
+        }
+    }
+    if (!BCT_NO_TL_BATCH) TL_MARK(0, 5);
+    grid_sync(p.bar);
+
+    // ---- phase D: mu per task, xhat per visit, z per task -----------------
+    double *mu_s = rs;                                    // [n_tasks]
+    int *st_s = reinterpret_cast<int *>(rs + n_tasks);   // [n_tasks]
+    for (int k = threadIdx.x; k < n_tasks; k += BLOCK) {
+        double gg = 0.0, den = 0.0;
+        for (int q = 0; q < G; ++q) gg += pgg[(int64_t)k * G + q];
+        for (int q = 0; q < G; ++q) den += pden[(int64_t)k * G + q];
+        double mu = 0.0;
+        int status = 0;
+        if (gg == 0.0) status = 1;
+        else if (den < 1e-30) status = 2;
+        else mu = p.tasks[k].beta * gg / den;
+        mu_s[k] = mu;
+        st_s[k] = status;
+        if (b == 0) {
+            p.mus[k] = mu;
+            p.statuses[k] = status;
+        }
+    }
+    __syncthreads();
+    if (b == 0 && threadIdx.x == 0)
+        for (int k = 0; k < n_tasks; ++k) p.counts[p.tasks[k].lp] += 1;
+    {
+        const int gtid = b * BLOCK + threadIdx.x, nth = G * BLOCK;
+        // xhat: voxels of every visit (its first task), its tasks summed in order
+        for (int v = gtid; v < hdr.n_vox_total; v += nth) {
+            int k0 = task_of(p.tasks, n_tasks, 3, v);
+            while (k0 > 0 && !(p.tasks[k0].flags & TASK_FIRST_OF_VISIT)) --k0;
+            const TaskDev &T0 = p.tasks[k0];
+            const PanelDev &P = p.panels[T0.lp];
+            const int d = v - T0.vox_pre;
+            double xs = 0.0;
+            const double xv = p.x[P.x_off + d];
+            for (int k = k0; k < n_tasks; ++k) {
+                const TaskDev &T = p.tasks[k];
+                if (k > k0 && (T.flags & TASK_FIRST_OF_VISIT)) break;
+                const double2 a = gxb[T.gx_off + d];
+                xs += st_s[k] == 0 ? __dadd_rn(xv, __dmul_rn(mu_s[k], a.x)) : xv;
+            }
+            p.xhat[P.x_off + d] += xs;
+        }
+        // z of every task's rows
+        for (int f = gtid; f < hdr.n_rows_total; f += nth) {
+            const int k = task_of(p.tasks, n_tasks, 2, f);
+            const TaskDev &T = p.tasks[k];
+            const PanelDev &P = p.panels[T.lp];
+            const int lr = f - T.row_pre;
+            const double2 q = taxb[T.tax_off + lr];
+            p.z[P.row_off + lr] = z_value(q.x, q.y, mu_s[k], st_s[k]);
+        }
+    }
+    if (!BCT_NO_TL_BATCH) TL_MARK(0, 6);
+}
+
 template <typename V>
 __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
 {
@@ -377,7 +652,10 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     using GS = typename std::conditional<sizeof(V) == 4, float2, double2>::type;
     GS *gs = reinterpret_cast<GS *>(dyn_smem);
 
-    for (int k = 0; k < n_tasks; ++k) {
+    __shared__ PanelDev ring[3];
+    __shared__ int ring_task[3];
+    if (hdr.batched) batched_epoch<V>(p, hdr, rs, sh, ring, ring_task);
+    for (int k = 0; k < (hdr.batched ? 0 : n_tasks); ++k) {
         __syncthreads();  // sT/sP/R of the previous task may still be in use
         if (threadIdx.x == 0) {
             sT = p.tasks[k];

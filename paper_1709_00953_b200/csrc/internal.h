@@ -63,6 +63,12 @@ struct TaskDev {
     double beta;
     uint64_t mask[BCT_MASKW];        // row blocks of the task's group
     uint64_t visit_mask[BCT_MASKW];  // union over the visit (serial refresh set)
+    // epoch-batched parallel path (full-panel tasks): flattened work prefixes
+    // and the task's slices of the batch scratch buffers
+    int32_t tile_pre, slice_pre, row_pre, vox_pre;   // exclusive prefixes over tasks
+    int64_t gx_off;    // (g, x) pairs of the task: gx_batch + gx_off
+    int64_t seg_off;   // segment partials: seg_batch + seg_off
+    int64_t tax_off;   // (t, ax) per local row: tax_batch + tax_off
 };
 
 enum { TASK_LAST_OF_VISIT = 1, TASK_FIRST_OF_VISIT = 2 };
@@ -71,7 +77,8 @@ struct EpochHeader {
     int32_t n_tasks;
     int32_t mode;
     int32_t flags;
-    int32_t pad;
+    int32_t batched;   // 1: parallel epoch of full-panel tasks, phase-by-phase over all tasks
+    int32_t n_tiles_total, n_slices_total, n_rows_total, n_vox_total;
     uint64_t epoch_mask[BCT_MASKW];  // union of all drawn blocks (parallel refresh)
 };
 
@@ -111,6 +118,10 @@ struct EpochParams {
     int64_t gx_stride;
     double *t_ax;              // (t, ax) interleaved per local row of the widest panel
     double *seg_part;          // (t, ax) partial per segment of the widest panel
+    double *gx_batch;          // batched path scratch (see TaskDev offsets)
+    double *seg_batch;
+    double *tax_batch;
+    double *part_task;         // [n_tasks][2][grid] gg / denom partials (batched)
     int32_t band_cap;          // shared-memory slots per band buffer
     int32_t band_dbuf;         // 1: two band buffers (copy next tile while computing)
     double *part;              // per-block partials: [4][grid]

@@ -27,6 +27,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--epochs", type=int, default=3)
+    ap.add_argument("--batched", action="store_true")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     s = DeviceBlockSystem.parallel_beam(cfg.spec, dtype=cfg.dtype)
@@ -46,6 +47,17 @@ def main():
     G = grid.value
     tl = buf[:nt * 8 * G].reshape(nt, 8, G).astype(np.float64) / 1e3  # us
     print(f"config {a.config}: kernel {res.kernel_ms:.3f} ms, {nt} tasks, grid {G}")
+    if a.batched:
+        t = tl[0]
+        st = t[0].min()
+        print("batched epoch (us): A(g) %.1f  barA %.1f  B(seg) %.1f  barB %.1f  C(rows) %.1f  D(step) %.1f"
+              % (t[1].max() - st, t[2].max() - t[1].max(), t[3].max() - t[2].min(),
+                 t[4].max() - t[3].max(), t[5].max() - t[4].min(), t[6].max() - t[5].max()))
+        for name, d in (("A per block", t[1] - t[0]), ("B per block", t[3] - t[2]),
+                        ("C per block", t[5] - t[4])):
+            q = np.percentile(d, [0, 10, 50, 90, 100])
+            print(f"{name:12s} min {q[0]:6.1f} p10 {q[1]:6.1f} med {q[2]:6.1f} p90 {q[3]:6.1f} max {q[4]:6.1f}")
+        return
     print("task     p1   bar1    p2a  bar2+p2b  bar3     p3   total   (us, to the last block)")
     tot = np.zeros(6)
     for k in range(nt):
