@@ -48,7 +48,8 @@ namespace {
 
 constexpr int RING = 4;
 constexpr int ST_VOXELS = 4096;     // voxels per super tile (64 KB of (g, x) pairs)
-constexpr size_t SMEM_BUDGET = 220 * 1024;  // dynamic shared memory per CTA (one CTA per SM)
+constexpr size_t SMEM_BUDGET = 210 * 1024;  // dynamic shared memory per CTA (one CTA per SM;
+                                            // 227 KB less the kernel's static arrays)
 
 struct Slot {
     cudaEvent_t done = nullptr;
@@ -222,9 +223,9 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     DALLOC(d_d2c, n_cols);
     CK(cudaMemcpy(d_rbp, rbp.data(), 4 * (c->m + 1), cudaMemcpyHostToDevice));
     // phase-1 tiles: the largest whose double-buffered band fits shared memory
-    static const int shapes[3][2] = {{8, 8}, {4, 8}, {4, 4}};
+    static const int shapes[2][2] = {{8, 8}, {4, 8}};
     Placement pl;
-    for (int si = 0; si < 3; ++si) {
+    for (int si = 0; si < 2; ++si) {
         const int th = shapes[si][0], tw = shapes[si][1];
         pl = place_voxels(n_cols, h, w, th, tw);
         std::string err;
@@ -234,7 +235,7 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
                                  d_rbp, pl.c2d, pl.st_ptr, pl.corder, th * tw, Q, kept, err,
                                  c->stream))
             return fail(c, BCT_ENOMEM, "panel %d layout: %s", j, err.c_str());
-        if (2 * (size_t)Q.band_max * 8 <= SMEM_BUDGET || si == 2) {
+        if (2 * (size_t)Q.band_max * 8 + bct::PHASE1_RED_BYTES <= SMEM_BUDGET || si == 1) {
             P = Q;
             c->allocs.insert(c->allocs.end(), kept.begin(), kept.end());
             break;
@@ -316,7 +317,7 @@ int finalize(bct_ctx *c)
 
     // state and scratch
     DALLOC(c->y, c->n_meas);
-    DALLOC(c->r, c->n_meas);
+    DALLOC(c->r, c->n_meas + 2);   // + 16-byte bulk-copy overhang (epoch.cu band staging)
     DALLOC(c->vec, c->n_meas + 2);
     DALLOC(c->exchange, c->n_meas + 2);
     DALLOC(c->z, c->z_len);
@@ -328,8 +329,10 @@ int finalize(bct_ctx *c)
     DALLOC(c->t_ax, 2 * c->max_rows);
     DALLOC(c->seg_part, 2 * c->max_seg + 2);
     // two band buffers when they fit, else one (staging then serializes)
-    c->band_dbuf = 2 * (size_t)c->band_cap * 8 <= SMEM_BUDGET ? 1 : 0;
-    c->smem = std::max<size_t>(c->smem, (size_t)c->band_cap * 8 * (c->band_dbuf ? 2 : 1));
+    // phase-1 bands (double-buffered when they fit) + the tile reduction area
+    c->band_dbuf = 2 * (size_t)c->band_cap * 8 + bct::PHASE1_RED_BYTES <= SMEM_BUDGET ? 1 : 0;
+    c->smem = std::max<size_t>(c->smem, (size_t)c->band_cap * 8 * (c->band_dbuf ? 2 : 1) +
+                                            bct::PHASE1_RED_BYTES);
     c->smem = std::max<size_t>(c->smem, 1024 * 12 + 64);
     if (c->smem > 227 * 1024)
         return fail(c, BCT_EINVAL, "shared-memory need %zu B exceeds the SM (band %d slots)",
@@ -342,7 +345,7 @@ int finalize(bct_ctx *c)
     DALLOC(c->audit2, 2);
     DALLOC(c->d_hdr, 1);
     CK(cudaMemsetAsync(c->y, 0, 8 * c->n_meas, c->stream));
-    CK(cudaMemsetAsync(c->r, 0, 8 * c->n_meas, c->stream));
+    CK(cudaMemsetAsync(c->r, 0, 8 * (c->n_meas + 2), c->stream));
     CK(cudaMemsetAsync(c->z, 0, 8 * std::max<int64_t>(c->z_len, 1), c->stream));
     CK(cudaMemsetAsync(c->x, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
     CK(cudaMemsetAsync(c->xhat, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
@@ -1114,7 +1117,7 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
             sgo += P.n_seg;
             txo += P.n_rows;
         }
-        if (tot_slices >= (1ll << 31) || tot_rows >= (1ll << 31)) batched = false;
+        if (tot_slices >= (1ll << 31) || tot_rows >= (1ll << 31) || gxo >= (1ll << 31)) batched = false;
     }
     if (batched) {
         // the device may still read the old scratch: drain before growing it
@@ -1129,7 +1132,7 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
         if ((r = grow(&c->gx_batch, &c->gx_batch_n, 2 * gxo))) return r;
         if ((r = grow(&c->seg_batch, &c->seg_batch_n, 2 * sgo))) return r;
         if ((r = grow(&c->tax_batch, &c->tax_batch_n, 2 * txo))) return r;
-        if ((r = grow(&c->part_task, &c->part_task_n, 2 * nt * (int64_t)c->grid))) return r;
+        if ((r = grow(&c->part_task, &c->part_task_n, 33 * nt * (int64_t)c->grid))) return r;
     }
     // the staging buffers of the previous epoch must have been consumed
     CK(cudaEventSynchronize(c->staged));

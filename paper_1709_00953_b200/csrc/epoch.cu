@@ -38,9 +38,6 @@ namespace {
 #ifndef BCT_EXP
 #define BCT_EXP 0
 #endif
-#ifndef BCT_PLAIN_STAGE
-#define BCT_PLAIN_STAGE 0
-#endif
 #ifndef BCT_P1_UNROLL
 #define BCT_P1_UNROLL 2
 #endif
@@ -297,15 +294,54 @@ __device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
 
-// Band staging of one tile: this lane holds the metadata of ranges
-// k0 + warp*32 + lane + it*BLOCK (it < 2); the warp issues the copies range by
-// range (range broadcast by shuffle, element e by lane e: 8-byte cp.async).
+// ---- mbarrier + bulk-copy (TMA) helpers ----
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// Band staging of one tile.  Range k of the tile is an even-aligned span of
+// the residual copied by ONE bulk copy (16-byte granules, completion counted
+// on the buffer's mbarrier): this lane owns ranges k0 + warp*32 + lane +
+// it*BLOCK (it < 2).  Each warp arrives once with its bytes, so the barrier
+// (count WARPS) completes when every range has landed.  A partial task
+// (mask != nullptr) writes zeros for ranges of row blocks outside its mask.
 struct BandMeta {
     int2 m[2];
+    int keep[2];
     int k0, k1;
 };
 
-__device__ __forceinline__ void band_meta_load(const PanelDev &P, int t, BandMeta &bm)
+__device__ __forceinline__ void band_meta_load(const PanelDev &P, int t, BandMeta &bm,
+                                               const uint64_t *mask)
 {
     const int k0 = __ldg(P.band_ptr + t), k1 = __ldg(P.band_ptr + t + 1);
     bm.k0 = k0;
@@ -315,37 +351,138 @@ __device__ __forceinline__ void band_meta_load(const PanelDev &P, int t, BandMet
     for (int it = 0; it < 2; ++it) {
         const int q = k0 + warp * 32 + lane + it * BLOCK;
         bm.m[it] = q < k1 ? __ldg(P.band_meta + q) : make_int2(0, 0);
+        bm.keep[it] = (mask == nullptr || q >= k1) ? 1 : (int)mask_has(mask, __ldg(P.band_rb + q));
     }
 }
 
+// Caller guarantees every generic read of buf is ordered before this call
+// by a CTA barrier.
 __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm, const double *r,
-                                           double *buf)
+                                           double *buf, const uint64_t *mask, uint64_t *bar)
 {
-#if BCT_EXP == 3
-    return;
-#endif
-    const int k0 = bm.k0, k1 = bm.k1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t bytes = 0;
+    fence_proxy_async();
 #pragma unroll
     for (int it = 0; it < 2; ++it) {
-        const int q0 = k0 + warp * 32 + it * BLOCK;
-        const int nr = min(32, k1 - q0);
-        for (int jj = 0; jj < nr; ++jj) {
-            const int g0 = __shfl_sync(0xffffffffu, bm.m[it].x, jj);
-            const int pk = __shfl_sync(0xffffffffu, bm.m[it].y, jj);
-            const int pre = (int)((unsigned)pk >> 16), len = pk & 0xffff;
-#if BCT_PLAIN_STAGE
-            for (int e = lane; e < len; e += 32) buf[pre + e] = r[g0 + e];
-#else
-            for (int e = lane; e < len; e += 32) cp_async8(buf + pre + e, r + g0 + e);
-#endif
+        const int q = bm.k0 + warp * 32 + lane + it * BLOCK;
+        if (q < bm.k1) {
+            const int g0 = bm.m[it].x;
+            const int pre = (int)((unsigned)bm.m[it].y >> 16), len = bm.m[it].y & 0xffff;
+            const int alen = ((g0 & 1) + len + 1) & ~1;
+            if (bm.keep[it]) {
+                bulk_g2s(buf + pre, r + (g0 & ~1), (uint32_t)alen * 8u, bar);
+                bytes += (uint32_t)alen * 8u;
+            } else {
+                for (int e = 0; e < alen; ++e) buf[pre + e] = 0.0;
+            }
         }
     }
     // ranges beyond 2*BLOCK per tile (not expected): plain loads
-    for (int q = k0 + 2 * BLOCK + threadIdx.x; q < k1; q += BLOCK) {
+    for (int q = bm.k0 + 2 * BLOCK + threadIdx.x; q < bm.k1; q += BLOCK) {
         const int2 mm = __ldg(P.band_meta + q);
         const int pre = (int)((unsigned)mm.y >> 16), len = mm.y & 0xffff;
-        for (int e = 0; e < len; ++e) buf[pre + e] = r[mm.x + e];
+        const bool keep = mask == nullptr || mask_has(mask, __ldg(P.band_rb + q));
+        const int off = mm.x & 1;
+        for (int e = 0; e < len; ++e) buf[pre + off + e] = keep ? r[mm.x + e] : 0.0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+    __syncwarp();
+    if (lane == 0) mbar_arrive_tx(bar, bytes);
+}
+
+// Phase-1 work of one tile: g of its columns in slices [sl0, sl1) of the tile.
+// Each 32-column slice is stored lane-interleaved (lane = column, 8 entries
+// per 16/64-byte vector), so the warps split the tile's vector rows and every
+// load is a fully coalesced 2 KB (FP64) / 1 KB (FP32) warp access.  Per-warp
+// column partials meet in `red` and one warp per column sums them in a fixed
+// order.  vr (partial tasks): per slice, the vector rows that can hold rows
+// of the task (others are skipped; rows outside the mask read zeros).
+// Returns this thread's share of gg (lane 0 of the column-owning warps).
+constexpr int RED_STRIDE = 65;
+constexpr int RED_DOUBLES = WARPS * RED_STRIDE;
+static_assert(2 * RED_DOUBLES * 8 == bct::PHASE1_RED_BYTES, "reduction areas");
+
+template <typename V>
+__device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int sl1,
+                                         const double *bt, const double *xj, double2 *gx,
+                                         double *red, const int2 *vr)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const V *tv = static_cast<const V *>(P.tvals);
+    const int nsl_tile = P.tile_cols >> 5;
+    const int sb = t * nsl_tile + sl0;
+    const int ns = min(sb + (sl1 - sl0), P.n_cslices) - sb;   // 1 or 2
+    const int base0 = __ldg(P.csl_start + sb);
+    const int base1 = ns > 1 ? __ldg(P.csl_start + sb + 1) : 0;
+    const int end1 = __ldg(P.csl_start + sb + ns);
+    int lo0 = 0, n0 = ((ns > 1 ? base1 : end1) - base0) >> 8;
+    int lo1 = 0, n1 = ns > 1 ? (end1 - base1) >> 8 : 0;
+    if (vr != nullptr) {
+        lo0 = vr[0].x;
+        n0 = vr[0].y - lo0;
+        if (ns > 1) {
+            lo1 = vr[1].x;
+            n1 = vr[1].y - lo1;
+        }
+    }
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll P1U
+    for (int u = warp; u < n0 + n1; u += WARPS) {
+        const bool first = u < n0;
+        const int i = (first ? base0 + (lo0 + u) * 256 : base1 + (lo1 + u - n0) * 256) + lane * 8;
+        int loc[8];
+        double v[8];
+        ld8u16(P.tloc + i, loc);
+        ld8v(tv + i, v);
+        double a = first ? acc0 : acc1;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a = fma(v[e], bt[loc[e]], a);
+        if (first) acc0 = a; else acc1 = a;
+    }
+    red[warp * RED_STRIDE + lane] = acc0;
+    if (ns > 1) red[warp * RED_STRIDE + 32 + lane] = acc1;
+    cp_async_wait_all();   // (batched path: ring copies of this thread)
+    __syncthreads();
+    double wsum = 0.0;
+    for (int c = warp; c < ns * 32; c += WARPS) {
+        const double g = warp_sum(red[lane * RED_STRIDE + c]);
+        const int q = sb * 32 + c;
+        if (lane == 0 && q < P.n_cols) {
+            const int d = __ldg(P.corder + q);
+            gx[d] = make_double2(g, xj[d]);
+            wsum = fma(g, g, wsum);
+        }
+    }
+    return wsum;
+}
+
+// vr of a partial task (see tile_g): warp si < ns computes slice si's range
+// over the columns' entries of row blocks [i_first, i_last)
+__device__ __forceinline__ void tile_vr(const PanelDev &P, int m, int t, int sl0, int sl1,
+                                        int i_first, int i_last, int2 *vr)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sb = t * (P.tile_cols >> 5) + sl0;
+    const int ns = min(sb + (sl1 - sl0), P.n_cslices) - sb;
+    if (warp < ns) {
+        const int q = (sb + warp) * 32 + lane;
+        int lo = 1 << 30, hi = 0;
+        if (q < P.n_cols) {
+            const int32_t *cp = P.cptr + (int64_t)__ldg(P.corder + q) * (m + 1);
+            const int s = __ldg(cp + i_first), e = __ldg(cp + i_last);
+            if (e > s) {
+                lo = s >> 3;
+                hi = (e + 7) >> 3;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) vr[warp] = hi > lo ? make_int2(lo, hi) : make_int2(0, 0);
     }
 }
 
@@ -376,9 +513,20 @@ __device__ __forceinline__ int task_of(const TaskDev *tasks, int n_tasks, int wh
     return lo;
 }
 
+// Batched phase-A ring: panel + item of the next tiles, copied by warp 0
+// with cp.async (4 slots: a slot is rewritten two tiles after its last read)
+struct RingSlot {
+    PanelDev P;
+    int64_t gx_off;
+    int k, t;
+};
+constexpr int RING = 4;
+static_assert(sizeof(RingSlot) % 8 == 0, "ring slots are copied in 8-byte words");
+
 template <typename V>
 __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, double *rs, double *sh,
-                              PanelDev *ring, int *ring_task)
+                              RingSlot *ring, int *s_tpre, int *s_lp, uint64_t *band_bar,
+                              uint32_t &bph)
 {
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -388,87 +536,80 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     double2 *gxb = reinterpret_cast<double2 *>(p.gx_batch);
     double2 *segb = reinterpret_cast<double2 *>(p.seg_batch);
     double2 *taxb = reinterpret_cast<double2 *>(p.tax_batch);
-    double *pgg = p.part_task;                       // [k][G]
-    double *pden = p.part_task + (int64_t)n_tasks * G;
+    double *pgg = p.part_task;                       // [k][G][WARPS]
+    double *pden = p.part_task + (int64_t)n_tasks * G * WARPS;   // [k][G]
 
     // ---- phase A: g = A^T r for every task, tiles round-robin over CTAs ----
-    for (int k = threadIdx.x; k < n_tasks; k += BLOCK) pgg[(int64_t)k * G + b] = 0.0;
+    // One CTA barrier per tile: the band of tile it+1 streams in (bulk
+    // copies, mbarrier) while tile it is computed; the reduction area is
+    // double-buffered by tile parity.  gg partials per (task, CTA, warp).
+    for (int k = threadIdx.x; k < n_tasks; k += BLOCK) {
+        s_tpre[k] = p.tasks[k].tile_pre;
+        s_lp[k] = p.tasks[k].lp;
+    }
+    if (threadIdx.x == 0) s_tpre[n_tasks] = hdr.n_tiles_total;
+    for (int q = threadIdx.x; q < n_tasks * WARPS; q += BLOCK)
+        pgg[((int64_t)(q / WARPS) * G + b) * WARPS + q % WARPS] = 0.0;
+    __syncthreads();
     {
         const int n_items = (hdr.n_tiles_total - b + G - 1) / G;
         const bool dbuf = p.band_dbuf != 0;
-        double *buf0 = rs, *buf1 = rs + (dbuf ? p.band_cap : 0);
-        auto load_ring = [&](int it) {   // thread 0: panel of item it into ring[it % 3]
+        double *buf[2] = {rs, rs + (dbuf ? p.band_cap : 0)};
+        double *red = rs + (int64_t)p.band_cap * (dbuf ? 2 : 1);
+        auto ring_issue = [&](int it) {   // warp 0
             const int item = b + it * G;
-            const int k = task_of(p.tasks, n_tasks, 0, item);
-            ring_task[it % 3] = k;
-            ring[it % 3] = p.panels[p.tasks[k].lp];
+            int lo = 0, hi = n_tasks - 1;  // last task with tile_pre <= item
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_tpre[mid] <= item) lo = mid; else hi = mid - 1;
+            }
+            RingSlot &S = ring[it % RING];
+            const uint64_t *src = reinterpret_cast<const uint64_t *>(p.panels + s_lp[lo]);
+            uint64_t *dst = reinterpret_cast<uint64_t *>(&S.P);
+            for (int w = lane; w < (int)(sizeof(PanelDev) / 8); w += 32) cp_async8(dst + w, src + w);
+            if (lane == 0) {
+                cp_async8(&S.gx_off, &p.tasks[lo].gx_off);
+                S.k = lo;
+                S.t = item - s_tpre[lo];
+            }
+            cp_async_commit();
         };
-        auto item_tile = [&](int it) { return b + it * G - p.tasks[ring_task[it % 3]].tile_pre; };
         BandMeta bm;
-        if (threadIdx.x == 0) {
-            if (n_items > 0) load_ring(0);
-            if (n_items > 1) load_ring(1);
+        if (warp == 0) {
+            if (n_items > 0) ring_issue(0);
+            if (n_items > 1) ring_issue(1);
+            cp_async_wait_all();
         }
         __syncthreads();
         if (n_items > 0) {
-            band_meta_load(ring[0], item_tile(0), bm);
-            band_issue(ring[0], bm, p.r, buf0);
-            cp_async_commit();
-            if (n_items > 1) band_meta_load(ring[1], item_tile(1), bm);
+            band_meta_load(ring[0].P, ring[0].t, bm, nullptr);
+            band_issue(ring[0].P, bm, p.r, buf[0], nullptr, &band_bar[0]);
+            if (n_items > 1) band_meta_load(ring[1].P, ring[1].t, bm, nullptr);
         }
-        int cur = 0;
+        double wacc = 0.0;
         for (int it = 0; it < n_items; ++it) {
-            cp_async_wait_all();
-            __syncthreads();
-            const PanelDev &P = ring[it % 3];
-            const int k = ring_task[it % 3];
-            const int t = item_tile(it);
-            double *bt = cur ? buf1 : buf0;
-            if (dbuf && it + 1 < n_items) {
-                band_issue(ring[(it + 1) % 3], bm, p.r, cur ? buf0 : buf1);
-                cp_async_commit();
+            const int cb = dbuf ? (it & 1) : 0;
+            mbar_wait(&band_bar[cb], (bph >> cb) & 1);
+            bph ^= 1u << cb;
+            const RingSlot &S = ring[it % RING];
+            // the other buffer was last read by tile it-1 (before its barrier)
+            if (dbuf && it + 1 < n_items)
+                band_issue(ring[(it + 1) % RING].P, bm, p.r, buf[cb ^ 1], nullptr, &band_bar[cb ^ 1]);
+            if (warp == 0 && it + 2 < n_items) ring_issue(it + 2);
+            const double wsum = tile_g<V>(S.P, S.t, 0, S.P.tile_cols >> 5, buf[cb],
+                                          p.x + S.P.x_off, gxb + S.gx_off,
+                                          red + (it & 1) * RED_DOUBLES, nullptr);
+            wacc += wsum;
+            // flush this warp's gg partial when the next item is another task
+            const int k = S.k;
+            if (it + 1 == n_items || ring[(it + 1) % RING].k != k) {
+                if (lane == 0) pgg[((int64_t)k * G + b) * WARPS + warp] = wacc;
+                wacc = 0.0;
             }
-            if (threadIdx.x == 0 && it + 2 < n_items) load_ring(it + 2);
-            const V *tv = static_cast<const V *>(P.tvals);
-            const int TC = P.tile_cols;
-            const int q_end = min((t + 1) * TC, P.n_cols);
-            const double *xj = p.x + P.x_off;
-            double2 *gx = gxb + p.tasks[k].gx_off;
-            double wsum = 0.0;
-            for (int qc = t * TC + warp; qc < q_end; qc += WARPS) {
-                const int d = __ldg(P.corder + qc);
-                const int32_t *cp = P.cptr + (int64_t)d * (m + 1);
-                const int s = __ldg(cp), e = __ldg(cp + m);
-                double acc = 0.0;
-#pragma unroll P1U
-                for (int i = s + 8 * lane; i < e; i += 256) {
-                    int loc[8];
-                    double v[8];
-                    ld8u16(P.tloc + i, loc);
-                    ld8v(tv + i, v);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        if (i + u < e) acc = fma(v[u], bt[loc[u]], acc);
-                }
-                acc = warp_sum(acc);
-                if (lane == 0) {
-                    gx[d] = make_double2(acc, xj[d]);
-                    wsum = fma(acc, acc, wsum);
-                }
-            }
-            if (lane == 0) sh[warp] = wsum;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                double s2 = 0.0;
-                for (int w = 0; w < WARPS; ++w) s2 += sh[w];
-                pgg[(int64_t)k * G + b] += s2;
-            }
-            if (!dbuf && it + 1 < n_items) {
-                band_issue(ring[(it + 1) % 3], bm, p.r, buf0);
-                cp_async_commit();
-            }
-            if (it + 2 < n_items) band_meta_load(ring[(it + 2) % 3], item_tile(it + 2), bm);
-            if (dbuf) cur ^= 1;
+            if (!dbuf && it + 1 < n_items)
+                band_issue(ring[(it + 1) % RING].P, bm, p.r, buf[0], nullptr, &band_bar[0]);
+            if (it + 2 < n_items)
+                band_meta_load(ring[(it + 2) % RING].P, ring[(it + 2) % RING].t, bm, nullptr);
         }
     }
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 1);
@@ -486,12 +627,12 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             __syncthreads();
             if (threadIdx.x == 0) {
                 const int k = task_of(p.tasks, n_tasks, 1, fu);
-                ring_task[0] = k;
-                ring[0] = p.panels[p.tasks[k].lp];
+                ring[0].k = k;
+                ring[0].P = p.panels[p.tasks[k].lp];
             }
             __syncthreads();
-            const PanelDev &P = ring[0];
-            const int k = ring_task[0];
+            const PanelDev &P = ring[0].P;
+            const int k = ring[0].k;
             const TaskDev &T = p.tasks[k];
             const int sl0 = fu - T.slice_pre;          // full panel: flattened = slice id
             // super tile of slice sl0 and the end of its slices
@@ -575,10 +716,13 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     // ---- phase D: mu per task, xhat per visit, z per task -----------------
     double *mu_s = rs;                                    // [n_tasks]
     int *st_s = reinterpret_cast<int *>(rs + n_tasks);   // [n_tasks]
-    for (int k = threadIdx.x; k < n_tasks; k += BLOCK) {
+    for (int k = warp; k < n_tasks; k += WARPS) {
         double gg = 0.0, den = 0.0;
-        for (int q = 0; q < G; ++q) gg += pgg[(int64_t)k * G + q];
-        for (int q = 0; q < G; ++q) den += pden[(int64_t)k * G + q];
+        for (int q = lane; q < G * WARPS; q += 32) gg += pgg[(int64_t)k * G * WARPS + q];
+        for (int q = lane; q < G; q += 32) den += pden[(int64_t)k * G + q];
+        gg = warp_sum(gg);
+        den = warp_sum(den);
+        if (lane != 0) continue;
         double mu = 0.0;
         int status = 0;
         if (gg == 0.0) status = 1;
@@ -634,6 +778,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     __shared__ double sh[WARPS];
     __shared__ TaskDev sT;
     __shared__ PanelDev sP;
+    __shared__ int2 vr_s[2];
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -652,9 +797,17 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     using GS = typename std::conditional<sizeof(V) == 4, float2, double2>::type;
     GS *gs = reinterpret_cast<GS *>(dyn_smem);
 
-    __shared__ PanelDev ring[3];
-    __shared__ int ring_task[3];
-    if (hdr.batched) batched_epoch<V>(p, hdr, rs, sh, ring, ring_task);
+    __shared__ RingSlot ring[RING];
+    __shared__ int s_tpre[1025], s_lp[1024];
+    __shared__ uint64_t band_bar[2];
+    uint32_t bph = 0;   // phase parity of band_bar[0..1]
+    if (threadIdx.x == 0) {
+        mbar_init(&band_bar[0], WARPS);
+        mbar_init(&band_bar[1], WARPS);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (hdr.batched) batched_epoch<V>(p, hdr, rs, sh, ring, s_tpre, s_lp, band_bar, bph);
     for (int k = 0; k < (hdr.batched ? 0 : n_tasks); ++k) {
         __syncthreads();  // sT/sP/R of the previous task may still be in use
         if (threadIdx.x == 0) {
@@ -672,78 +825,59 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         // ---- phase 1: g = A_I^T r_I, tile bands in shared memory ----------
         // Work items are whole tiles in rounds of gridDim.x; the tiles left for
         // the last round are split into column parts so every CTA gets the
-        // same share.  The band of the next item is copied (cp.async) into the
-        // second buffer while the current item is computed.
+        // same share.  The band of the next item is copied (bulk copies) into
+        // the second buffer while the current item is computed.
         double wsum = 0.0;
         {
-            const V *tv = static_cast<const V *>(P.tvals);
-            const int TC = P.tile_cols;
+            const int NSL = P.tile_cols >> 5;
             const int G = gridDim.x;
             const int full = P.n_tiles / G, rem = P.n_tiles - full * G;
-            const int S = rem > 0 ? max(1, G / rem) : 1;
+            const int S = rem > 0 ? max(1, min(NSL, G / rem)) : 1;
             const int n_items = full + ((int)blockIdx.x < rem * S ? 1 : 0);
             auto item_tile = [&](int it) {
                 return it < full ? (int)blockIdx.x + it * G : full * G + (int)blockIdx.x / S;
             };
             const bool dbuf = p.band_dbuf != 0;
             double *buf0 = rs, *buf1 = rs + (dbuf ? p.band_cap : 0);
+            double *red = rs + (int64_t)p.band_cap * (dbuf ? 2 : 1);
+            const uint64_t *bmask = R.full ? nullptr : T.mask;
             BandMeta bm;
             if (n_items > 0) {
-                band_meta_load(P, item_tile(0), bm);
-                band_issue(P, bm, p.r, buf0);
-                cp_async_commit();
-                if (n_items > 1) band_meta_load(P, item_tile(1), bm);
+                band_meta_load(P, item_tile(0), bm, bmask);
+                band_issue(P, bm, p.r, buf0, bmask, &band_bar[0]);
+                if (n_items > 1) band_meta_load(P, item_tile(1), bm, bmask);
             }
             int cur = 0;
             for (int it = 0; it < n_items; ++it) {
-                cp_async_wait_all();
+                mbar_wait(&band_bar[cur], (bph >> cur) & 1);
+                bph ^= 1u << cur;
                 __syncthreads();
                 const int t = item_tile(it);
-                int c0 = 0, c1 = TC;
+                int c0 = 0, c1 = NSL;
                 if (it >= full) {
                     const int part = (int)blockIdx.x % S;
-                    c0 = part * TC / S;
-                    c1 = (part + 1) * TC / S;
+                    c0 = part * NSL / S;
+                    c1 = (part + 1) * NSL / S;
                 }
                 double *bt = cur ? buf1 : buf0;
                 if (dbuf && it + 1 < n_items) {
-                    band_issue(P, bm, p.r, cur ? buf0 : buf1);
-                    cp_async_commit();
-                    if (it + 2 < n_items) band_meta_load(P, item_tile(it + 2), bm);
+                    band_issue(P, bm, p.r, cur ? buf0 : buf1, bmask, &band_bar[cur ^ 1]);
+                    if (it + 2 < n_items) band_meta_load(P, item_tile(it + 2), bm, bmask);
                 }
-                const int q_end = min(t * TC + c1, P.n_cols);
+                if (bmask != nullptr) {
+                    tile_vr(P, m, t, c0, c1, R.n > 0 ? R.i0[0] : 0, R.n > 0 ? R.i1[R.n - 1] : 0,
+                            vr_s);
+                    __syncthreads();
+                }
 #if BCT_EXP != 4
-                for (int qc = t * TC + c0 + warp; qc < q_end; qc += WARPS) {
-                    const int d = __ldg(P.corder + qc);
-                    const int32_t *cp = P.cptr + (int64_t)d * (m + 1);
-                    double acc = 0.0;
-                    for (int kr = 0; kr < R.n; ++kr) {
-                        const int s = __ldg(cp + R.i0[kr]), e = __ldg(cp + R.i1[kr]);
-#pragma unroll P1U
-                        for (int i = (s & ~7) + 8 * lane; i < e; i += 256) {
-                            int loc[8];
-                            double v[8];
-                            ld8u16(P.tloc + i, loc);
-                            ld8v(tv + i, v);
-#pragma unroll
-                            for (int u = 0; u < 8; ++u)
-                                if (i + u >= s && i + u < e) acc = fma(v[u], bt[loc[u]], acc);
-                        }
-                    }
-                    acc = warp_sum(acc);
-                    if (lane == 0) {
-                        gx[d] = make_double2(acc, xj[d]);
-                        wsum = fma(acc, acc, wsum);
-                    }
-                }
+                wsum += tile_g<V>(P, t, c0, c1, bt, xj, gx, red, bmask != nullptr ? vr_s : nullptr);
 #endif
                 __syncthreads();
                 if (dbuf) {
                     cur ^= 1;
                 } else if (it + 1 < n_items) {
-                    band_issue(P, bm, p.r, buf0);
-                    cp_async_commit();
-                    if (it + 2 < n_items) band_meta_load(P, item_tile(it + 2), bm);
+                    band_issue(P, bm, p.r, buf0, bmask, &band_bar[0]);
+                    if (it + 2 < n_items) band_meta_load(P, item_tile(it + 2), bm, bmask);
                 }
             }
         }

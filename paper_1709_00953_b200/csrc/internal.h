@@ -34,13 +34,16 @@ struct PanelDev {
     const int32_t *seg_lane;
     const int32_t *rseg_ptr;   // [n_rows+1] row -> its segments (tile order) in rseg
     const int32_t *rseg;
-    // panel CSC with tile bands (phase 1)
-    const void *tvals;         // T, columns (device order) padded to 8 entries
+    // panel CSC with tile bands (phase 1): slices of 32 columns of a tile,
+    // entry e of lane l of slice s at csl_start[s] + ((e/8)*32 + l)*8 + e%8
+    const void *tvals;         // T
     const uint16_t *tloc;      // slot of the entry's row in its tile's band
-    const int32_t *cptr;       // [n_cols*(m+1)] column segment starts per row block
-    const int32_t *corder;     // tile order of device columns, 16 per tile
+    const int32_t *csl_start;  // [n_cslices+1]
+    const int32_t *cptr;       // [n_cols*(m+1)] column-local start of each row block
+    const int32_t *corder;     // tile order of device columns, tile_cols per tile
     const int32_t *band_ptr;   // [n_tiles+1] ranges of each tile
     const int2 *band_meta;     // per range: (first measurement id, slot << 16 | length)
+    const uint8_t *band_rb;    // row block of each range
     // rows / voxels
     const int32_t *rbp;        // [m+1]
     const int32_t *l2g;        // [n_rows] global measurement ids
@@ -52,7 +55,9 @@ struct PanelDev {
     int32_t n_seg, n_slices, n_st, n_tiles;
     int32_t band_max, st_max;
     int32_t mdiv;              // reference order = (c / mdiv, tile, c) for bitwise merges
-    int32_t tile_cols;         // columns per phase-1 tile
+    int32_t tile_cols;         // columns per phase-1 tile (multiple of 32)
+    int32_t n_cslices;
+    int32_t pad2_;
 };
 
 struct TaskDev {
@@ -138,6 +143,9 @@ struct bct_ctx_s;
 
 // builder / launch helpers implemented in the .cu files
 namespace bct {
+
+// phase-1 tile reduction areas in dynamic shared memory (2 x epoch.cu RED_DOUBLES)
+constexpr size_t PHASE1_RED_BYTES = 2 * 32 * 65 * 8;
 std::string cuda_err(cudaError_t e);
 void launch_epoch(const EpochParams &p, int dtype, int grid, int block, size_t smem,
                   cudaStream_t s, cudaError_t *err);

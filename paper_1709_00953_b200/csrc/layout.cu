@@ -272,16 +272,19 @@ __global__ void colcount_k(const int32_t *sorted_d, int64_t nnz, int32_t n_cols,
     }
 }
 
-// band keys: (tile of column) << 32 | global row, per CSC entry in sorted order
+// band keys: tile << 40 | row block << 32 | global row, per CSC entry in sorted
+// order (ranges never cross a row block, so a partial task can zero the rest)
 __global__ void band_key_k(const int32_t *perm, const int32_t *rowid, const int32_t *l2g,
-                           const int32_t *sorted_d, const int32_t *tile_of_d, int64_t nnz,
-                           uint64_t *bkey, int32_t *grow)
+                           const int32_t *rbp, int m, const int32_t *sorted_d,
+                           const int32_t *tile_of_d, int64_t nnz, uint64_t *bkey)
 {
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= nnz) return;
-    int32_t g = l2g[rowid[perm[q]]];
-    grow[q] = g;
-    bkey[q] = ((uint64_t)(uint32_t)tile_of_d[sorted_d[q]] << 32) | (uint32_t)g;
+    const int32_t lr = rowid[perm[q]];
+    const int32_t g = l2g[lr];
+    const int blk = (int)lb_i32(rbp, 0, m + 1, lr + 1) - 1;
+    bkey[q] = ((uint64_t)(uint32_t)tile_of_d[sorted_d[q]] << 40) | ((uint64_t)blk << 32) |
+              (uint32_t)g;
 }
 
 __global__ void uniq_flag_k(const uint64_t *k, int64_t n, int32_t *flag)
@@ -303,6 +306,7 @@ __global__ void range_flag_k(const uint64_t *u, int64_t nu, int32_t *flag)
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= nu) return;
     flag[q] = (q == 0 || (u[q] >> 32) != (u[q - 1] >> 32) || u[q] != u[q - 1] + 1) ? 1 : 0;
+    // (the upper 32 bits are tile and row block)
 }
 
 // per tile: first unique index (tile_u0) and first range (band_ptr)
@@ -311,73 +315,124 @@ __global__ void tile_bounds_k(const uint64_t *u, int64_t nu, const int32_t *rfla
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t > n_tiles) return;
-    int64_t q = lb_u64(u, 0, nu, (uint64_t)(uint32_t)t << 32);
+    int64_t q = lb_u64(u, 0, nu, (uint64_t)(uint32_t)t << 40);
     tile_u0[t] = (int32_t)q;
     // ranges before q = number of range starts in [0, q)
     band_ptr[t] = q == 0 ? 0 : rflag_incl[q - 1];
 }
 
+// Ranges are staged with 16-byte bulk copies: range k covers the aligned
+// measurement span [g0 & ~1, g0 + len rounded up to even), alen slots, and
+// starts at an even band slot (apre = exclusive prefix of alen).
 __global__ void ranges_k(const uint64_t *u, int64_t nu, const int32_t *rflag, const int32_t *rincl,
-                         const int32_t *tile_u0, int2 *band_meta)
+                         int32_t *rstart, int32_t *rlen, int32_t *alen, uint8_t *band_rb)
 {
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= nu || !rflag[q]) return;
     int k = rincl[q] - 1;
-    int t = (int)(u[q] >> 32);
+    band_rb[k] = (uint8_t)(u[q] >> 32);
     const int32_t g0 = (int32_t)(uint32_t)u[q];
-    const int32_t pre = (int32_t)(q - tile_u0[t]);
     // length: up to the next range start
     int64_t e = q + 1;
     while (e < nu && !rflag[e]) ++e;
-    band_meta[k] = make_int2(g0, (int32_t)(((uint32_t)pre << 16) | (uint32_t)(e - q)));
+    rstart[k] = (int32_t)q;
+    rlen[k] = (int32_t)(e - q);
+    alen[k] = ((g0 & 1) + (int32_t)(e - q) + 1) & ~1;
 }
 
-template <typename V>
-__global__ void csc_scatter_k(const int32_t *perm, const double *vals64, const int32_t *sorted_d,
-                              const int32_t *grow, const int32_t *tile_of_d, const uint64_t *u,
-                              const int32_t *tile_u0, const int32_t *colstart, const int32_t *cpad,
-                              int64_t nnz, V *tvals, uint16_t *tloc)
+__global__ void range_meta_k(const uint64_t *u, const int32_t *rstart, const int32_t *rlen,
+                             const int32_t *apre, const int32_t *band_ptr, int32_t n_ranges,
+                             int2 *band_meta)
 {
-    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (q >= nnz) return;
-    int d = sorted_d[q];
-    int t = tile_of_d[d];
-    uint64_t key = ((uint64_t)(uint32_t)t << 32) | (uint32_t)grow[q];
-    int64_t pos = lb_u64(u, tile_u0[t], tile_u0[t + 1], key);
-    int64_t dst = cpad[d] + (q - colstart[d]);
-    tvals[dst] = (V)vals64[perm[q]];
-    tloc[dst] = (uint16_t)(pos - tile_u0[t]);
-}
-
-template <typename V>
-__global__ void csc_pad_k(const int32_t *colstart, const int32_t *cpad, int32_t n_cols, V *tvals,
-                          uint16_t *tloc)
-{
-    int d = blockIdx.x * blockDim.x + threadIdx.x;
-    if (d >= n_cols) return;
-    int64_t a = cpad[d] + (colstart[d + 1] - colstart[d]);
-    uint16_t last = a > cpad[d] ? tloc[a - 1] : 0;
-    for (int64_t q = a; q < cpad[d + 1]; ++q) {
-        tvals[q] = (V)0;
-        tloc[q] = last;
-    }
-}
-
-// cptr[d*(m+1)+i] = padded position of column d's first entry with local row >= rbp[i]
-__global__ void cptr_k(const int32_t *colstart, const int32_t *cpad, const int32_t *tlocal_sorted,
-                       const int32_t *rbp, int m, int32_t n_cols, int32_t *cptr)
-{
-    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= (int64_t)n_cols * (m + 1)) return;
-    int d = (int)(t / (m + 1)), i = (int)(t % (m + 1));
-    int64_t lb = lb_i32(tlocal_sorted, colstart[d], colstart[d + 1], rbp[i]);
-    cptr[t] = (int32_t)(cpad[d] + (lb - colstart[d]));
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_ranges) return;
+    const uint64_t key = u[rstart[k]];
+    const int t = (int)(key >> 40);
+    const int32_t pre = apre[k] - apre[band_ptr[t]];
+    band_meta[k] = make_int2((int32_t)(uint32_t)key,
+                             (int32_t)(((uint32_t)pre << 16) | (uint32_t)rlen[k]));
 }
 
 __global__ void gather_rows_k(const int32_t *perm, const int32_t *rowid, int64_t nnz, int32_t *out)
 {
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q < nnz) out[q] = rowid[perm[q]];
+}
+
+// ---- CSC slices: 32 columns (lanes) of a tile interleaved 8 entries at a time
+// -- entry e of the column in lane l of slice s at
+// csl_start[s] + ((e / 8) * 32 + l) * 8 + e % 8
+
+__global__ void cslice_len_k(const int32_t *colstart, const int32_t *corder, int32_t n_cols,
+                             int32_t n_cslices, int32_t *slice_ent)
+{
+    int sl = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sl > n_cslices) return;
+    if (sl == n_cslices) { slice_ent[sl] = 0; return; }
+    int kmax = 0;
+    for (int l = 0; l < 32; ++l) {
+        int q = sl * 32 + l;
+        if (q >= n_cols) break;
+        int d = corder[q];
+        kmax = max(kmax, (colstart[d + 1] - colstart[d] + 7) / 8);
+    }
+    slice_ent[sl] = kmax * 256;
+}
+
+template <typename V>
+__global__ void csc_sell_scatter_k(const int32_t *perm, const double *vals64, const int32_t *sorted_d,
+                                   const uint64_t *bkey, const int32_t *tile_of_d, const uint64_t *u,
+                                   const int32_t *tile_u0, const int32_t *rincl,
+                                   const int32_t *rstart, const int32_t *apre,
+                                   const int32_t *band_ptr, const int32_t *colstart,
+                                   const int32_t *dslot, const int32_t *csl_start, int64_t nnz,
+                                   V *tvals, uint16_t *tloc)
+{
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= nnz) return;
+    int d = sorted_d[q];
+    int t = tile_of_d[d];
+    int64_t bpos = lb_u64(u, tile_u0[t], tile_u0[t + 1], bkey[q]);
+    int64_t e = q - colstart[d];
+    int slot = dslot[d];
+    int64_t dst = csl_start[slot / 32] + ((e >> 3) * 32 + (slot % 32)) * 8 + (e & 7);
+    tvals[dst] = (V)vals64[perm[q]];
+    const int k = rincl[bpos] - 1;   // range of the entry's row
+    const int32_t g0 = (int32_t)(uint32_t)u[rstart[k]];
+    tloc[dst] = (uint16_t)(apre[k] - apre[band_ptr[t]] + (g0 & 1) + (bpos - rstart[k]));
+}
+
+// padding of every (slice, lane): zero values on the column's last band slot
+template <typename V>
+__global__ void csc_sell_pad_k(const int32_t *colstart, const int32_t *corder, int32_t n_cols,
+                               const int32_t *csl_start, int32_t n_cslices, V *tvals,
+                               uint16_t *tloc)
+{
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n_cslices * 32) return;
+    int sl = (int)(t / 32), lane = (int)(t % 32);
+    int q = sl * 32 + lane;
+    int len = q < n_cols ? colstart[corder[q] + 1] - colstart[corder[q]] : 0;
+    int64_t base = csl_start[sl];
+    int64_t nent = ((int64_t)csl_start[sl + 1] - base) / 32;
+    uint16_t last = 0;
+    if (len > 0) last = tloc[base + (((int64_t)(len - 1) >> 3) * 32 + lane) * 8 + ((len - 1) & 7)];
+    for (int64_t e = len; e < nent; ++e) {
+        int64_t pos = base + ((e >> 3) * 32 + lane) * 8 + (e & 7);
+        tvals[pos] = (V)0;
+        tloc[pos] = last;
+    }
+}
+
+// cptr[d*(m+1)+i] = column-local index of column d's first entry with local row >= rbp[i]
+__global__ void cptr_local_k(const int32_t *colstart, const int32_t *tlocal_sorted,
+                             const int32_t *rbp, int m, int32_t n_cols, int32_t *cptr)
+{
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n_cols * (m + 1)) return;
+    int d = (int)(t / (m + 1)), i = (int)(t % (m + 1));
+    int64_t lb = lb_i32(tlocal_sorted, colstart[d], colstart[d + 1], rbp[i]);
+    cptr[t] = (int32_t)(lb - colstart[d]);
 }
 
 }  // namespace
@@ -605,24 +660,42 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
 
     // ================= CSC with tile bands =================
     int32_t *sd = T.get<int32_t>(nnz), *cperm = T.get<int32_t>(nnz);
-    int32_t *colstart = T.get<int32_t>(n_cols + 1), *cpad = T.get<int32_t>(n_cols + 1);
+    int32_t *colstart = T.get<int32_t>(n_cols + 1);
     int32_t *len8 = T.get<int32_t>(n_cols + 1);
-    LNN(sd); LNN(cperm); LNN(colstart); LNN(cpad); LNN(len8);
+    LNN(sd); LNN(cperm); LNN(colstart); LNN(len8);
     if (nnz > 0) {
         csc_key_k<<<nb(nnz, 256), 256, 0, s>>>(cols_c, c2d, nnz, key);
         LCK(sort_pairs<int32_t>(key, sd, iota, cperm, nnz, bits_for(n_cols), tmp, s));
     }
     colcount_k<<<nb(n_cols + 1, 256), 256, 0, s>>>(sd, nnz, n_cols, colstart, len8);
-    LCK(scan_i32(len8, cpad, n_cols + 1, false, tmp, s));
-    int64_t csc_cap = read1(cpad + n_cols, s);
+    // slices of 32 columns in tile order
+    const int32_t n_cslices = (n_cols + 31) / 32;
+    int32_t *slice_ent = T.get<int32_t>(n_cslices + 1), *csl_start = K.get<int32_t>(n_cslices + 1);
+    int32_t *dslot = T.get<int32_t>(n_cols);
+    LNN(slice_ent); LNN(csl_start); LNN(dslot);
+    {
+        std::vector<int32_t> ds(n_cols);
+        for (size_t q = 0; q < corder_h.size(); ++q) ds[corder_h[q]] = (int32_t)q;
+        LCK(cudaMemcpyAsync(dslot, ds.data(), 4 * n_cols, cudaMemcpyHostToDevice, s));
+        LCK(cudaStreamSynchronize(s));
+    }
+    cslice_len_k<<<nb(n_cslices + 1, 128), 128, 0, s>>>(colstart, corder, n_cols, n_cslices,
+                                                       slice_ent);
+    LCK(scan_i32(slice_ent, csl_start, n_cslices + 1, false, tmp, s));
+    int64_t csc_cap = read1(csl_start + n_cslices, s);
+    if (csc_cap >= (1ll << 31)) {
+        err = "panel CSC exceeds 2^31 entries";
+        release(tmp);
+        return -1;
+    }
     // bands
     uint64_t *bkey = T.get<uint64_t>(nnz), *bsorted = T.get<uint64_t>(nnz);
-    int32_t *grow = T.get<int32_t>(nnz);
-    LNN(bkey); LNN(bsorted); LNN(grow);
+    LNN(bkey); LNN(bsorted);
     int64_t nu = 0;
     if (nnz > 0) {
-        band_key_k<<<nb(nnz, 256), 256, 0, s>>>(cperm, rowid, l2g, sd, tile_of_d, nnz, bkey, grow);
-        LCK(sort_keys_u64(bkey, bsorted, nnz, 32 + bits_for(n_tiles), tmp, s));
+        band_key_k<<<nb(nnz, 256), 256, 0, s>>>(cperm, rowid, l2g, rbp, m, sd, tile_of_d, nnz,
+                                                 bkey);
+        LCK(sort_keys_u64(bkey, bsorted, nnz, 40 + bits_for(n_tiles), tmp, s));
         uniq_flag_k<<<nb(nnz, 256), 256, 0, s>>>(bsorted, nnz, flag);
         LCK(scan_i32(flag, incl, nnz, true, tmp, s));
         nu = read1(incl + nnz - 1, s);
@@ -640,16 +713,25 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     }
     int32_t *band_ptr = K.get<int32_t>(n_tiles + 1);
     int2 *band_meta = K.get<int2>(n_ranges + 1);
-    LNN(band_ptr); LNN(band_meta);
+    uint8_t *band_rb = K.get<uint8_t>(n_ranges + 1);
+    int32_t *rstart = T.get<int32_t>(n_ranges + 1), *rlen = T.get<int32_t>(n_ranges + 1);
+    int32_t *alen = T.get<int32_t>(n_ranges + 1), *apre = T.get<int32_t>(n_ranges + 1);
+    LNN(band_ptr); LNN(band_meta); LNN(band_rb); LNN(rstart); LNN(rlen); LNN(alen); LNN(apre);
     tile_bounds_k<<<nb(n_tiles + 1, 128), 128, 0, s>>>(uk, nu, rincl, n_tiles, tile_u0, band_ptr);
+    LCK(cudaMemsetAsync(alen + n_ranges, 0, 4, s));
     if (n_ranges > 0)
-        ranges_k<<<nb(nu, 256), 256, 0, s>>>(uk, nu, rflag, rincl, tile_u0, band_meta);
+        ranges_k<<<nb(nu, 256), 256, 0, s>>>(uk, nu, rflag, rincl, rstart, rlen, alen, band_rb);
+    LCK(scan_i32(alen, apre, n_ranges + 1, false, tmp, s));
+    if (n_ranges > 0)
+        range_meta_k<<<nb(n_ranges, 256), 256, 0, s>>>(uk, rstart, rlen, apre, band_ptr, n_ranges,
+                                                       band_meta);
     // the widest band sets the shared-memory size
-    std::vector<int32_t> tu(n_tiles + 1);
-    LCK(cudaMemcpyAsync(tu.data(), tile_u0, 4 * (n_tiles + 1), cudaMemcpyDeviceToHost, s));
+    std::vector<int32_t> bp(n_tiles + 1), ap(n_ranges + 1);
+    LCK(cudaMemcpyAsync(bp.data(), band_ptr, 4 * (n_tiles + 1), cudaMemcpyDeviceToHost, s));
+    LCK(cudaMemcpyAsync(ap.data(), apre, 4 * (n_ranges + 1), cudaMemcpyDeviceToHost, s));
     LCK(cudaStreamSynchronize(s));
     int32_t band_max = 0;
-    for (int t = 0; t < n_tiles; ++t) band_max = std::max(band_max, tu[t + 1] - tu[t]);
+    for (int t = 0; t < n_tiles; ++t) band_max = std::max(band_max, ap[bp[t + 1]] - ap[bp[t]]);
     if (band_max > 65535) {
         err = "a column tile touches more than 65535 measurement rows";
         release(tmp);
@@ -662,19 +744,23 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     LNN(tvals); LNN(tloc); LNN(cptr); LNN(tls);
     if (nnz > 0) {
         if (dtype == 0)
-            csc_scatter_k<double><<<nb(nnz, 256), 256, 0, s>>>(cperm, vals64, sd, grow, tile_of_d, uk,
-                tile_u0, colstart, cpad, nnz, (double *)tvals, tloc);
+            csc_sell_scatter_k<double><<<nb(nnz, 256), 256, 0, s>>>(cperm, vals64, sd, bkey,
+                tile_of_d, uk, tile_u0, rincl, rstart, apre, band_ptr, colstart, dslot,
+                csl_start, nnz, (double *)tvals, tloc);
         else
-            csc_scatter_k<float><<<nb(nnz, 256), 256, 0, s>>>(cperm, vals64, sd, grow, tile_of_d, uk,
-                tile_u0, colstart, cpad, nnz, (float *)tvals, tloc);
+            csc_sell_scatter_k<float><<<nb(nnz, 256), 256, 0, s>>>(cperm, vals64, sd, bkey,
+                tile_of_d, uk, tile_u0, rincl, rstart, apre, band_ptr, colstart, dslot,
+                csl_start, nnz, (float *)tvals, tloc);
         gather_rows_k<<<nb(nnz, 256), 256, 0, s>>>(cperm, rowid, nnz, tls);
     }
     if (dtype == 0)
-        csc_pad_k<double><<<nb(n_cols, 256), 256, 0, s>>>(colstart, cpad, n_cols, (double *)tvals, tloc);
+        csc_sell_pad_k<double><<<nb((int64_t)n_cslices * 32, 256), 256, 0, s>>>(colstart, corder,
+            n_cols, csl_start, n_cslices, (double *)tvals, tloc);
     else
-        csc_pad_k<float><<<nb(n_cols, 256), 256, 0, s>>>(colstart, cpad, n_cols, (float *)tvals, tloc);
-    cptr_k<<<nb((int64_t)n_cols * (m + 1), 256), 256, 0, s>>>(colstart, cpad, tls, rbp, m, n_cols,
-                                                             cptr);
+        csc_sell_pad_k<float><<<nb((int64_t)n_cslices * 32, 256), 256, 0, s>>>(colstart, corder,
+            n_cols, csl_start, n_cslices, (float *)tvals, tloc);
+    cptr_local_k<<<nb((int64_t)n_cols * (m + 1), 256), 256, 0, s>>>(colstart, tls, rbp, m, n_cols,
+                                                                   cptr);
     LCK(cudaGetLastError());
     LCK(cudaStreamSynchronize(s));
     release(tmp);
@@ -692,11 +778,14 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     P.rseg_ptr = rseg_ptr;
     P.rseg = rseg;
     P.tvals = tvals;
+    P.csl_start = csl_start;
+    P.n_cslices = n_cslices;
     P.tloc = tloc;
     P.cptr = cptr;
     P.corder = corder;
     P.band_ptr = band_ptr;
     P.band_meta = band_meta;
+    P.band_rb = band_rb;
     P.n_seg = n_seg;
     P.n_slices = n_slices;
     P.n_st = n_st;
