@@ -38,6 +38,9 @@ namespace {
 #ifndef BCT_EXP
 #define BCT_EXP 0
 #endif
+#ifndef BCT_TMA_QUARTERS
+#define BCT_TMA_QUARTERS 3   // share of band ranges staged by bulk copy (TMA), in quarters
+#endif
 #ifndef BCT_P1_UNROLL
 #define BCT_P1_UNROLL 2
 #endif
@@ -291,6 +294,11 @@ __device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr(sdst)), "l"(gsrc));
 }
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(sdst)), "l"(gsrc)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
 
@@ -366,13 +374,18 @@ __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm
 #pragma unroll
     for (int it = 0; it < 2; ++it) {
         const int q = bm.k0 + warp * 32 + lane + it * BLOCK;
-        if (q < bm.k1) {
+        if (q < bm.k1 && BCT_EXP != 5) {
             const int g0 = bm.m[it].x;
             const int pre = (int)((unsigned)bm.m[it].y >> 16), len = bm.m[it].y & 0xffff;
             const int alen = ((g0 & 1) + len + 1) & ~1;
-            if (bm.keep[it]) {
+            if (bm.keep[it] && ((q - bm.k0) & 3) < BCT_TMA_QUARTERS) {
                 bulk_g2s(buf + pre, r + (g0 & ~1), (uint32_t)alen * 8u, bar);
                 bytes += (uint32_t)alen * 8u;
+            } else if (bm.keep[it]) {
+                // the rest on the LSU path, so the TMA request rate and the
+                // LSU share the staging (waited with cp.async.wait_group)
+                const double *src = r + (g0 & ~1);
+                for (int e = 0; e < alen; e += 2) cp_async16(buf + pre + e, src + e);
             } else {
                 for (int e = 0; e < alen; ++e) buf[pre + e] = 0.0;
             }
@@ -390,6 +403,7 @@ __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm
     for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
     __syncwarp();
     if (lane == 0) mbar_arrive_tx(bar, bytes);
+    cp_async_commit();
 }
 
 // Phase-1 work of one tile: g of its columns in slices [sl0, sl1) of the tile.
@@ -429,7 +443,7 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
     }
     double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll P1U
-    for (int u = warp; u < n0 + n1; u += WARPS) {
+    for (int u = warp; u < ((BCT_EXP == 6) ? 0 : n0 + n1); u += WARPS) {
         const bool first = u < n0;
         const int i = (first ? base0 + (lo0 + u) * 256 : base1 + (lo1 + u - n0) * 256) + lane * 8;
         int loc[8];
@@ -591,6 +605,10 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const int cb = dbuf ? (it & 1) : 0;
             mbar_wait(&band_bar[cb], (bph >> cb) & 1);
             bph ^= 1u << cb;
+            if (!dbuf) {   // LSU-staged ranges of this band: issued after the last barrier
+                cp_async_wait_all();
+                __syncthreads();
+            }
             const RingSlot &S = ring[it % RING];
             // the other buffer was last read by tile it-1 (before its barrier)
             if (dbuf && it + 1 < n_items)
@@ -851,6 +869,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             for (int it = 0; it < n_items; ++it) {
                 mbar_wait(&band_bar[cur], (bph >> cur) & 1);
                 bph ^= 1u << cur;
+                cp_async_wait_all();
                 __syncthreads();
                 const int t = item_tile(it);
                 int c0 = 0, c1 = NSL;
