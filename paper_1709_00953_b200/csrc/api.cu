@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cuda_runtime.h>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -59,6 +60,9 @@ struct Slot {
     int32_t *h_status = nullptr;    // pinned [task_cap]
     int64_t n_tasks = 0, n_visits = 0;
     bool pending = false;
+    int32_t *h_plan = nullptr;      // pinned: device-sampled ids of the epoch
+    int64_t plan_cap = 0, n_plan = 0;
+    int64_t *plan_user = nullptr;   // caller's buffer, filled by bct_wait_epoch
 };
 
 }  // namespace
@@ -105,7 +109,13 @@ struct bct_ctx {
     int head = 0, tail = 0;           // ring: tail = oldest pending
     int grid = 0, block = 0;
     bool has_x_true = false;
-    uint64_t last_epoch_mask[BCT_MASKW] = {0, 0, 0, 0};
+    // device sampler (bct_sample_epoch)
+    double *d_values = nullptr, *d_totals = nullptr, *d_exp = nullptr;
+    int64_t d_exp_n = 0;
+    bct::SampleVisit *d_visits = nullptr;
+    int64_t d_visits_n = 0;
+    int32_t *d_plan = nullptr;
+    int64_t d_plan_n = 0;
     std::vector<void *> allocs;
     long long *timeline = nullptr;    // BCT_TIMELINE=1: [task][8][grid] globaltimer stamps
     int64_t timeline_tasks = 0;
@@ -965,7 +975,8 @@ int bct_audit(bct_ctx *c, double *drift)
 
 // ---- epochs ---------------------------------------------------------------
 
-static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits)
+static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
+                         const std::function<int(Slot &)> &before_epoch = nullptr)
 {
     int s = c->head;
     Slot &S = c->slots[s];
@@ -980,6 +991,12 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits)
         CK(cudaMemcpyAsync(c->d_tasks, c->h_tasks, sizeof(TaskDev) * n_tasks,
                            cudaMemcpyHostToDevice, c->stream));
     CK(cudaEventRecord(c->staged, c->stream));
+    S.plan_user = nullptr;
+    S.n_plan = 0;
+    if (before_epoch) {
+        int r = before_epoch(S);
+        if (r) return r;
+    }
     EpochParams p;
     memset(&p, 0, sizeof p);
     p.panels = c->d_panels;
@@ -1022,6 +1039,9 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits)
     c->head = (c->head + 1) % RING;
     return 0;
 }
+
+static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<TaskDev> &tasks,
+                           const uint64_t *emask, const std::function<int(Slot &)> &hook);
 
 int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task_j,
                   const int32_t *task_visit, const int64_t *task_gptr, const int64_t *sel,
@@ -1073,6 +1093,15 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
         T.beta = betas[k];
         tasks.push_back(T);
     }
+    return plan_and_launch(c, mode, flags, tasks, emask, nullptr);
+}
+
+// Visit flags/masks, batched-path prefixes and scratch, staging and launch of
+// a validated task list (shared by bct_run_epoch and bct_sample_epoch; the
+// hook runs on the stream between the plan upload and the epoch kernel).
+static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<TaskDev> &tasks,
+                           const uint64_t *emask, const std::function<int(Slot &)> &hook)
+{
     // visit boundaries and masks
     int64_t n_visits = 0;
     const int64_t nt = (int64_t)tasks.size();
@@ -1145,10 +1174,9 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
     c->h_hdr->n_slices_total = (int32_t)tot_slices;
     c->h_hdr->n_rows_total = (int32_t)tot_rows;
     c->h_hdr->n_vox_total = (int32_t)tot_vox;
-    memcpy(c->h_hdr->epoch_mask, emask, sizeof emask);
-    memcpy(c->last_epoch_mask, emask, sizeof emask);
+    memcpy(c->h_hdr->epoch_mask, emask, sizeof(uint64_t) * BCT_MASKW);
     if (nt) memcpy(c->h_tasks, tasks.data(), sizeof(TaskDev) * nt);
-    return launch_staged(c, nt, n_visits);
+    return launch_staged(c, nt, n_visits, hook);
 }
 
 int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *statuses)
@@ -1170,6 +1198,9 @@ int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *status
     o->kernel_ms = ms;
     if (mus) memcpy(mus, S.h_mus, 8 * S.n_tasks);
     if (statuses) memcpy(statuses, S.h_status, 4 * S.n_tasks);
+    if (S.plan_user)
+        for (int64_t q = 0; q < S.n_plan; ++q) S.plan_user[q] = S.h_plan[q];
+    S.plan_user = nullptr;
     S.pending = false;
     c->tail = (c->tail + 1) % RING;
     return 0;
@@ -1199,27 +1230,145 @@ int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
 {
     if (!c) return BCT_EINVAL;
     (void)flags;
-    uint64_t *dmask = nullptr;
-    CK(cudaMalloc((void **)&dmask, sizeof(uint64_t) * BCT_MASKW));
-    CK(cudaMemcpyAsync(dmask, c->last_epoch_mask, sizeof(uint64_t) * BCT_MASKW,
-                       cudaMemcpyHostToDevice, c->stream));
+    // the drawn blocks of the last epoch, as the device saw them (host plan or sampler)
+    const uint64_t *dmask = c->d_hdr->epoch_mask;
     const int nb = 296;
     CK(bct::sharded_finish(c->y, c->exchange, c->n_meas, c->rb_of_row, dmask, c->r, c->part, nb,
                            c->stream));
     std::vector<double> part(nb);
     CK(cudaMemcpyAsync(part.data(), c->part, 8 * nb, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    cudaFree(dmask);
     double s = 0.0;
     for (int b = 0; b < nb; ++b) s += part[b];
     if (resid_sq) *resid_sq = s;
     return 0;
 }
 
-int bct_sample_epoch(bct_ctx *c, int32_t, int32_t, const int32_t *, const double *, int64_t,
-                     const int32_t *, int32_t, double, int32_t, double, int32_t, int64_t *)
+int bct_sample_epoch(bct_ctx *c, int32_t mode, int32_t n_visits, const int32_t *visit_j,
+                     const double *exp_variates, int64_t n_variates, const int32_t *draws,
+                     int32_t group_size, double b, int32_t strategy, double theta,
+                     int32_t flags, int64_t *plan_ids_out)
 {
-    return c ? fail(c, BCT_EINVAL, "bct_sample_epoch not implemented yet") : BCT_EINVAL;
+    if (!c) return BCT_EINVAL;
+    if (mode != BCT_SERIAL_FAITHFUL && mode != BCT_PARALLEL)
+        return fail(c, BCT_EINVAL, "mode %d", mode);
+    if (strategy < BCT_IMPORTANCE || strategy > BCT_MIXED)
+        return fail(c, BCT_EINVAL, "strategy %d", strategy);
+    if (group_size < 1) return fail(c, BCT_EINVAL, "group_size %d", group_size);
+    if (n_visits < 0 || (n_visits > 0 && (!visit_j || !draws)) ||
+        (n_variates > 0 && !exp_variates))
+        return fail(c, BCT_EINVAL, "null sampler arrays");
+    const bool sharded = (flags & BCT_SHARDED) != 0;
+    if (sharded && mode != BCT_PARALLEL)
+        return fail(c, BCT_EINVAL, "sharded execution requires parallel mode");
+    // structure of the plan from the host table (sampling.py:140-152): scope,
+    // variate offsets, task skeletons; the ids/masks/betas come from the device
+    std::vector<bct::SampleVisit> vis(n_visits);
+    std::vector<TaskDev> tasks;
+    uint64_t emask[BCT_MASKW] = {0, 0, 0, 0};   // ORed by the sampler on the device
+    int64_t var_off = 0, id_off = 0;
+    for (int32_t v = 0; v < n_visits; ++v) {
+        const int j = visit_j[v];
+        if (j < 0 || j >= c->n_panels)
+            return fail(c, BCT_ESCHEDULE, "visit %d: volume block %d out of range", v, j);
+        int scope = 0;
+        for (int i = 0; i < c->m; ++i) scope += c->table_values[(int64_t)i * c->n_panels + j] > 0.0;
+        if (draws[v] < 0 || draws[v] > scope)
+            return fail(c, BCT_ESCHEDULE, "cannot draw %d blocks from %d in scope", draws[v], scope);
+        if (draws[v] > 0 && !(c->table_totals[j] > 0.0))
+            return fail(c, BCT_ESCHEDULE, "volume block %d has no selectable measurement blocks",
+                        j);
+        bct::SampleVisit &V = vis[v];
+        V.j = j;
+        V.draws = draws[v];
+        V.var_off = (int32_t)var_off;
+        V.id_off = (int32_t)id_off;
+        V.task_base = -1;
+        var_off += scope;
+        id_off += draws[v];
+        const bool owned = j >= c->pb && j < c->pe;
+        if (!owned && !sharded)
+            return fail(c, BCT_ESCHEDULE, "visit %d: volume block %d not owned", v, j);
+        if (!owned) continue;
+        const int ng = (draws[v] + group_size - 1) / group_size;
+        V.task_base = (int32_t)tasks.size();
+        for (int t = 0; t < ng; ++t) {
+            TaskDev T;
+            memset(&T, 0, sizeof T);
+            T.lp = j - c->pb;
+            T.j = j;
+            T.visit = v;
+            // full group <=> it holds every row block (masks are filled on the device)
+            if (std::min(group_size, draws[v] - t * group_size) == c->m)
+                for (int i = 0; i < c->m; ++i) set_mask(T.mask, i);
+            tasks.push_back(T);
+        }
+    }
+    if (var_off != n_variates)
+        return fail(c, BCT_ESCHEDULE, "%lld variates for %lld in-scope blocks",
+                    (long long)n_variates, (long long)var_off);
+    if (c->m > 256) return fail(c, BCT_EINVAL, "device sampler supports m <= 256");
+    // device inputs (grow-only; drained before reallocation)
+    auto grow = [&](auto **ptr, int64_t *have, int64_t need, size_t elt) -> int {
+        if (need <= *have) return 0;
+        CK(cudaStreamSynchronize(c->stream));
+        if (*ptr) cudaFree(*ptr);
+        CK(cudaMalloc((void **)ptr, elt * std::max<int64_t>(need, 1)));
+        *have = need;
+        return 0;
+    };
+    int r;
+    if (!c->d_values) {
+        CK(cudaMalloc((void **)&c->d_values, 8 * std::max<size_t>(c->table_values.size(), 1)));
+        CK(cudaMalloc((void **)&c->d_totals, 8 * std::max<size_t>(c->table_totals.size(), 1)));
+        CK(cudaMemcpy(c->d_values, c->table_values.data(), 8 * c->table_values.size(),
+                      cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_totals, c->table_totals.data(), 8 * c->table_totals.size(),
+                      cudaMemcpyHostToDevice));
+    }
+    if ((r = grow(&c->d_exp, &c->d_exp_n, n_variates, 8))) return r;
+    if ((r = grow(&c->d_visits, &c->d_visits_n, n_visits, sizeof(bct::SampleVisit)))) return r;
+    if ((r = grow(&c->d_plan, &c->d_plan_n, id_off, 4))) return r;
+    // variates and visits are copied synchronously: the caller's buffers are
+    // free on return, and the previous epoch may still read nothing of these
+    auto hook = [&](Slot &S) -> int {
+        if (n_variates > 0)
+            CK(cudaMemcpyAsync(c->d_exp, exp_variates, 8 * n_variates, cudaMemcpyHostToDevice,
+                               c->stream));
+        if (n_visits > 0)
+            CK(cudaMemcpyAsync(c->d_visits, vis.data(), sizeof(bct::SampleVisit) * n_visits,
+                               cudaMemcpyHostToDevice, c->stream));
+        bct::SamplerParams sp;
+        sp.values = c->d_values;
+        sp.totals = c->d_totals;
+        sp.n_panels = c->n_panels;
+        sp.m = c->m;
+        sp.visits = c->d_visits;
+        sp.exp = c->d_exp;
+        sp.strategy = strategy;
+        sp.theta = theta;
+        sp.group_size = group_size;
+        sp.b = b;
+        sp.tasks = c->d_tasks;
+        sp.hdr = c->d_hdr;
+        sp.plan_ids = c->d_plan;
+        cudaError_t e;
+        bct::launch_sampler(sp, n_visits, c->stream, &e);
+        if (e != cudaSuccess) return fail(c, BCT_ECUDA, "sampler launch: %s", cudaGetErrorString(e));
+        if (plan_ids_out && id_off > 0) {
+            if (S.plan_cap < id_off) {
+                if (S.h_plan) cudaFreeHost(S.h_plan);
+                CK(cudaHostAlloc((void **)&S.h_plan, 4 * id_off, cudaHostAllocDefault));
+                S.plan_cap = id_off;
+            }
+            CK(cudaMemcpyAsync(S.h_plan, c->d_plan, 4 * id_off, cudaMemcpyDeviceToHost,
+                               c->stream));
+            S.plan_user = plan_ids_out;
+            S.n_plan = id_off;
+        }
+        return 0;
+    };
+    return plan_and_launch(c, mode, flags, tasks, emask, hook);
 }
 
 }  // extern "C"

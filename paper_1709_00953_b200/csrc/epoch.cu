@@ -1163,7 +1163,7 @@ int epoch_grid_size(int dtype, int device, size_t smem, int *block)
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const void *fn = dtype == 0 ? (const void *)epoch_kernel<double> : (const void *)epoch_kernel<float>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 16384);
     if (dtype == 0)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<double>, BLOCK, smem);
     else
@@ -1179,6 +1179,15 @@ void launch_epoch(const EpochParams &p, int dtype, int grid, int block, size_t s
 {
     EpochParams local = p;
     void *args[] = {&local};
+    // the dynamic shared-memory limit is per function, shared by every context
+    // of the process: set it to this context's need before each launch
+    static size_t set_for[2] = {0, 0};
+    if (set_for[dtype != 0] != smem) {
+        cudaFuncSetAttribute(dtype == 0 ? (const void *)epoch_kernel<double>
+                                        : (const void *)epoch_kernel<float>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        set_for[dtype != 0] = smem;
+    }
     if (dtype == 0)
         *err = cudaLaunchCooperativeKernel((const void *)epoch_kernel<double>, grid, block, args,
                                            smem, s);

@@ -144,6 +144,28 @@ struct bct_ctx_s;
 // builder / launch helpers implemented in the .cu files
 namespace bct {
 
+// device sampler (sampler.cu)
+struct SampleVisit {
+    int32_t j, draws;
+    int32_t var_off;     // first exponential variate of the visit
+    int32_t id_off;      // first drawn id of the visit in the plan record
+    int32_t task_base;   // first task of the visit, -1 when another rank owns j
+    int32_t pad_;
+};
+struct SamplerParams {
+    const double *values;    // [m * n_panels] table values (row-major, values[i*n+j])
+    const double *totals;    // [n_panels]
+    int32_t n_panels, m;
+    const SampleVisit *visits;
+    const double *exp;       // exponential variates, visit order
+    int32_t strategy, group_size;
+    double theta, b;
+    TaskDev *tasks;          // the epoch's device task array (masks, betas written)
+    EpochHeader *hdr;        // epoch_mask ORed
+    int32_t *plan_ids;       // drawn ids, visit order, draw order
+};
+void launch_sampler(const SamplerParams &p, int n_visits, cudaStream_t s, cudaError_t *err);
+
 // phase-1 tile reduction areas in dynamic shared memory (2 x epoch.cu RED_DOUBLES)
 constexpr size_t PHASE1_RED_BYTES = 2 * 32 * 65 * 8;
 std::string cuda_err(cudaError_t e);

@@ -101,6 +101,54 @@ def submit(system, mode, plan, flags):
                 task=TaskDescriptor(0, j, ids, float(plan.betas[0]) if plan.betas.size else 0.0))
 
 
+class SampledPlan:
+    """An epoch whose plan the device draws (bct_sample_epoch) from the host's
+    variates (sampling.BlockScheduler.epoch_variates).  The task structure is
+    known up front; the drawn ids arrive with the epoch result
+    (``finalize`` after ``wait``), giving the plan and bytes_moved."""
+
+    def __init__(self, system, variates, group_size):
+        self.variates = variates
+        self.group_size = int(group_size)
+        gs = self.group_size
+        owned = [system.owns(int(j)) for j in variates.visit_j]
+        self.task_j = np.array([int(j) for j, d, o in zip(variates.visit_j, variates.draws, owned)
+                                if o for _ in range(-(-int(d) // gs))], dtype=np.int32)
+        self.plan_ids = np.zeros(max(int(variates.draws.sum()), 1), dtype=np.int64)
+        self.plan = None
+        self.bytes_moved = 0
+        self.n_loops = int(variates.visit_j.size)
+        self._system = system
+
+    def finalize(self):
+        """Plan [(j, [ids chunks])] in visit order, and the reference's
+        bytes_moved (executor.py:210-213), from the device-drawn ids."""
+        plan, off, moved = [], 0, 0
+        gs = self.group_size
+        for j, d in zip(self.variates.visit_j, self.variates.draws):
+            ids = self.plan_ids[off:off + int(d)].copy()
+            off += int(d)
+            groups = [ids[p:p + gs] for p in range(0, ids.size, gs)]
+            plan.append((int(j), groups))
+            pix = int(self._system.row_sizes[ids].sum()) if ids.size else 0
+            moved += 16 * (pix + len(groups) * int(self._system.col_sizes[int(j)]))
+        self.plan = plan
+        self.bytes_moved = moved
+        return plan
+
+
+def submit_sampled(system, mode, sampled, b, strategy, flags):
+    """Queue one epoch whose plan the device samples (asynchronous)."""
+    v = sampled.variates
+    rc = N.load().bct_sample_epoch(system.ctx, N.MODES[mode], int(v.visit_j.size),
+                                   N.ptr(N.i32(v.visit_j)), N.ptr(N.f64(v.exp)), int(v.exp.size),
+                                   N.ptr(N.i32(v.draws)), sampled.group_size, float(b),
+                                   N.STRATEGY_CODES[strategy], float(v.theta), flags,
+                                   N.ptr(sampled.plan_ids))
+    if rc != 0:
+        N.check(rc, system.ctx, "sampled epoch rejected")
+
+
 def wait(system, n_tasks, want_status=False):
     """Block on the oldest queued epoch; returns (EpochResult, mus, statuses)."""
     res = N.EpochResult()

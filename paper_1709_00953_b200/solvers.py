@@ -20,7 +20,8 @@ import numpy as np
 
 from . import _native as N
 from .errors import ConfigurationError, DivergenceError
-from .executor import EXECUTION_MODES, EpochExecutor, pack_loops, submit, wait
+from .executor import (EXECUTION_MODES, EpochExecutor, SampledPlan, pack_loops, submit,
+                       submit_sampled, wait)
 from .metrics import ConvergenceTrace, TraceRow, snr_from_sq
 from .sampling import BlockScheduler, SamplingConfig, ScriptedScheduler, group_beta
 from .validation import as_vector, check_choice, check_count, check_positive
@@ -127,12 +128,14 @@ def _loops(plan, table, b):
 
 
 def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=None,
-              plan_record=None):
+              plan_record=None, device_sampling=False):
     """Grouped solver for ``params.epochs`` epochs (solvers.py:188-269).
 
     Returns (x, ConvergenceTrace); raises DivergenceError with
     last_good_epoch and the partial trace when |x| is non-finite or exceeds
-    divergence_factor times its first-epoch value.
+    divergence_factor times its first-epoch value.  ``device_sampling``
+    draws the plan on the device from the same numpy variates
+    (bct_sample_epoch); the trajectory is identical.
     """
     if schedule is not None:
         scheduler = ScriptedScheduler(schedule, group_size=params.group_size)
@@ -156,20 +159,30 @@ def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=N
     ref_norm = None
     pipelined = callback is None and params.audit_interval == 0
 
+    sampled = device_sampling and schedule is None
+
     def prepare(epoch):
         theta_now = scheduler.theta
         try:
-            plan = scheduler.epoch_plan(epoch, rng)
-            packed = pack_loops(_loops(plan, system.table, params.b), system)
+            if sampled:
+                packed = SampledPlan(system, scheduler.epoch_variates(epoch, rng),
+                                     params.group_size)
+            else:
+                plan = scheduler.epoch_plan(epoch, rng)
+                packed = pack_loops(_loops(plan, system.table, params.b), system)
+                if plan_record is not None:
+                    plan_record[epoch] = plan
         except Exception as exc:  # surfaced when the loop reaches this epoch
             return exc, theta_now
-        if plan_record is not None:
-            plan_record[epoch] = plan
         scheduler.advance_epoch()
         return packed, theta_now
 
     def launch(prep):
-        if not isinstance(prep[0], Exception):
+        if isinstance(prep[0], Exception):
+            return
+        if sampled:
+            submit_sampled(system, mode, prep[0], params.b, params.sampling.strategy, flags)
+        else:
             submit(system, mode, prep[0], flags)
 
     pending = None
@@ -185,6 +198,10 @@ def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=N
             nxt = prepare(epoch + 1)
             launch(nxt)
         res, _, _ = wait(system, packed.task_j.size)
+        if sampled:
+            plan = packed.finalize()
+            if plan_record is not None:
+                plan_record[epoch] = plan
         state.epoch = epoch
         snr = snr_from_sq(xt_norm, res.err_sq) if x_true is not None else math.nan
         gap = snr_from_sq(y_norm, res.resid_sq) if y_norm > 0.0 else math.nan

@@ -241,3 +241,48 @@ def test_warm_start_and_audit(exec_system):
     r[3] += 1e-3
     sysm.set_r(r)
     assert abs(sysm.audit_drift() - 1e-3 / np.abs(f["y"]).max()) < 1e-15
+
+
+# ---------------------------------------------------------------------------
+# device sampler (bct_sample_epoch) == host BlockScheduler, bit for bit
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", list(VARIANTS))
+def test_device_sampler_replays_host_plans(cfg1_system, name):
+    """Same variates -> same plans, betas and trajectory (x bitwise)."""
+    kw = dict(VARIANTS[name])
+    kw["epochs"] = min(kw["epochs"], 12)
+    p = SolverParams(**kw)
+    f = golden("pb_cfg1_runs.npz")
+    y, xt = f["y"], f["x_true"]
+    rec_h, rec_d = {}, {}
+    x_h, tr_h = run_gcsgd(cfg1_system, y, p, x_true=xt, plan_record=rec_h)
+    x_d, tr_d = run_gcsgd(cfg1_system, y, p, x_true=xt, plan_record=rec_d, device_sampling=True)
+    for e in rec_h:
+        assert [(j, [g.tolist() for g in gs]) for j, gs in rec_h[e]] == \
+               [(j, [g.tolist() for g in gs]) for j, gs in rec_d[e]]
+    assert np.array_equal(x_h, x_d)
+    assert [r.bytes_moved for r in tr_h.rows] == [r.bytes_moved for r in tr_d.rows]
+    assert [r.snr_db for r in tr_h.rows] == [r.snr_db for r in tr_d.rows]
+
+
+@pytest.mark.parametrize("gs,alpha,strategy", [(150, 1.0, "importance"), (20, 0.5, "importance"),
+                                                (9, 0.3, "mixed"), (150, 1.0, "random")])
+def test_device_sampler_many_row_blocks(gs, alpha, strategy):
+    """m = 150 row blocks: numpy's pairwise sum in all three regimes
+    (<8, 8-accumulator, halved) for the betas, stable ties in the race."""
+    spec = ParallelBeamSpec(32, 180, 46, 150, 2)
+    sysm = DeviceBlockSystem.parallel_beam(spec, dtype="f64")
+    from paper_1709_00953_b200.geometry import add_noise, random_ellipses
+    xt = random_ellipses(32, 5, 3)
+    y, _ = add_noise(sysm.forward(xt), 0.01, 4)
+    p = SolverParams(epochs=4, b=0.2, group_size=gs, seed=21, execution_mode="parallel",
+                     sampling=SamplingConfig(strategy=strategy, alpha=alpha, theta0=0.25,
+                                             theta_step=0.25))
+    rec_h, rec_d = {}, {}
+    x_h, _ = run_gcsgd(sysm, y, p, x_true=xt, plan_record=rec_h)
+    x_d, _ = run_gcsgd(sysm, y, p, x_true=xt, plan_record=rec_d, device_sampling=True)
+    for e in rec_h:
+        assert [(j, [g.tolist() for g in gs_]) for j, gs_ in rec_h[e]] == \
+               [(j, [g.tolist() for g in gs_]) for j, gs_ in rec_d[e]]
+    assert np.array_equal(x_h, x_d)

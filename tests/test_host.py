@@ -223,3 +223,37 @@ def test_oracle_is_not_imported_by_the_product():
                 text = open(os.path.join(root, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", text, re.M), f
                 assert "libblockct_oracle" not in text, f
+
+
+def _np_pairwise(a):
+    """Restatement of numpy's pairwise_sum (loops_utils.h.src), the order the
+    device sampler (csrc/sampler.cu np_pairwise) uses for the betas."""
+    n = len(a)
+    if n < 8:
+        res = 0.0
+        for v in a:
+            res = res + v
+        return res
+    if n <= 128:
+        r = list(a[:8])
+        i = 8
+        while i < n - (n % 8):
+            for k in range(8):
+                r[k] = r[k] + a[i + k]
+            i += 8
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+        while i < n:
+            res = res + a[i]
+            i += 1
+        return res
+    n2 = n // 2
+    n2 -= n2 % 8
+    return _np_pairwise(a[:n2]) + _np_pairwise(a[n2:])
+
+
+def test_numpy_sum_is_the_pairwise_order_of_the_device_sampler():
+    rng = np.random.default_rng(0)
+    for n in list(range(1, 140)) + [200, 255, 256]:
+        for _ in range(5):
+            a = rng.random(n) * 10.0 ** rng.integers(-6, 6, n)
+            assert _np_pairwise(a) == float(np.sum(a))
