@@ -132,6 +132,9 @@ int bct_get_z(bct_ctx *ctx, int32_t j, double *z_j);
 int bct_get_xhat(bct_ctx *ctx, double *xhat);
 int bct_set_x_true(bct_ctx *ctx, const double *x_true);      /* NULL clears */
 int bct_reset_accumulators(bct_ctx *ctx);                    /* xhat=0, counts=0 */
+/* Cold start on the device: x = 0, z = 0, xhat = 0, counts = 0
+ * (SolverState.initialize with x0=None, solvers.py:70-76, without uploads). */
+int bct_clear_state(bct_ctx *ctx);
 int bct_get_counts(bct_ctx *ctx, int64_t *counts);            /* [n_panels] */
 
 /* _commit_epoch (solvers.py:180-185): x_J = xhat_J / counts[j], reset. */

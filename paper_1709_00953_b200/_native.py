@@ -72,6 +72,7 @@ _SIGS = {
     "bct_get_xhat": [_p, _p],
     "bct_set_x_true": [_p, _p],
     "bct_reset_accumulators": [_p],
+    "bct_clear_state": [_p],
     "bct_get_counts": [_p, _p],
     "bct_commit_epoch": [_p],
     "bct_reset_residual": [_p],

@@ -891,6 +891,17 @@ int bct_reset_accumulators(bct_ctx *c)
     return 0;
 }
 
+int bct_clear_state(bct_ctx *c)
+{
+    if (!c) return BCT_EINVAL;
+    CK(cudaMemsetAsync(c->x, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
+    CK(cudaMemsetAsync(c->z, 0, 8 * std::max<int64_t>(c->z_len, 1), c->stream));
+    CK(cudaMemsetAsync(c->xhat, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
+    CK(cudaMemsetAsync(c->counts, 0, 4 * std::max(c->np, 1), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
 int bct_get_counts(bct_ctx *c, int64_t *counts)
 {
     if (!c || !counts) return BCT_EINVAL;

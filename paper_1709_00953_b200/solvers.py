@@ -71,10 +71,8 @@ class SolverState:
         system.set_y(y)
         system.reset_accumulators()
         if x0 is None:
-            system.set_x(np.zeros(system.n_voxels))
-            system.set_z([np.zeros(system.n_local_rows(j)) if system.owns(j) else None
-                          for j in range(system.n_col_blocks)])
-            system.set_r(y)
+            system.clear_state()        # x = 0, z = 0 on the device
+            system.reset_residual()     # r = y - 0 = y, exactly
         else:
             x0 = as_vector("x0", x0, length=system.n_voxels)
             system.set_x(x0)

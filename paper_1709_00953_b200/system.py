@@ -284,6 +284,10 @@ class DeviceBlockSystem:
             xt = N.f64(x_true)
             N.check(L.bct_set_x_true(self._ctx, N.ptr(xt)), self._ctx)
 
+    def clear_state(self):
+        """x = 0, z = 0, xhat = 0, counts = 0 on the device (no uploads)."""
+        N.check(N.load().bct_clear_state(self._ctx), self._ctx)
+
     def reset_accumulators(self):
         N.check(N.load().bct_reset_accumulators(self._ctx), self._ctx)
 
