@@ -232,11 +232,21 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     DALLOC(d_rbp, c->m + 1);
     DALLOC(d_d2c, n_cols);
     CK(cudaMemcpy(d_rbp, rbp.data(), 4 * (c->m + 1), cudaMemcpyHostToDevice));
-    // phase-1 tiles: the largest whose double-buffered band fits shared memory
-    static const int shapes[2][2] = {{8, 8}, {4, 8}};
+    // phase-1 tiles, in order of preference: 16x16 voxels with one band
+    // buffer (long per-warp streams, a quarter of the band staging per column
+    // of 8x8), else 8x8 / 4x8 with double-buffered bands.  BCT_TILE=HxW
+    // forces a shape (profiling).
+    struct Shape { int th, tw, nbuf; };
+    std::vector<Shape> shapes = {{16, 16, 1}, {8, 8, 2}, {4, 8, 2}, {4, 8, 1}};
+    if (const char *e = getenv("BCT_TILE")) {
+        int a = 0, b2 = 0;
+        if (sscanf(e, "%dx%d", &a, &b2) == 2 && a > 0 && b2 > 0 && (a * b2) % 32 == 0 &&
+            a * b2 <= 256)
+            shapes = {{a, b2, 1}, {4, 8, 1}};
+    }
     Placement pl;
-    for (int si = 0; si < 2; ++si) {
-        const int th = shapes[si][0], tw = shapes[si][1];
+    for (size_t si = 0; si < shapes.size(); ++si) {
+        const int th = shapes[si].th, tw = shapes[si].tw;
         pl = place_voxels(n_cols, h, w, th, tw);
         std::string err;
         std::vector<void *> kept;
@@ -245,7 +255,8 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
                                  d_rbp, pl.c2d, pl.st_ptr, pl.corder, th * tw, Q, kept, err,
                                  c->stream))
             return fail(c, BCT_ENOMEM, "panel %d layout: %s", j, err.c_str());
-        if (2 * (size_t)Q.band_max * 8 + bct::PHASE1_RED_BYTES <= SMEM_BUDGET || si == 1) {
+        if ((size_t)shapes[si].nbuf * Q.band_max * 8 + bct::PHASE1_RED_BYTES <= SMEM_BUDGET ||
+            si + 1 == shapes.size()) {
             P = Q;
             c->allocs.insert(c->allocs.end(), kept.begin(), kept.end());
             break;

@@ -38,9 +38,6 @@ namespace {
 #ifndef BCT_EXP
 #define BCT_EXP 0
 #endif
-#ifndef BCT_TMA_QUARTERS
-#define BCT_TMA_QUARTERS 3   // share of band ranges staged by bulk copy (TMA), in quarters
-#endif
 #ifndef BCT_P1_UNROLL
 #define BCT_P1_UNROLL 2
 #endif
@@ -302,46 +299,14 @@ __device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
 
-// ---- mbarrier + bulk-copy (TMA) helpers ----
-__device__ __forceinline__ void mbar_init(uint64_t *bar, int count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
-{
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
-{
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-        ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
-        : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async()
-{
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-
-// Band staging of one tile.  Range k of the tile is an even-aligned span of
-// the residual copied by ONE bulk copy (16-byte granules, completion counted
-// on the buffer's mbarrier): this lane owns ranges k0 + warp*32 + lane +
-// it*BLOCK (it < 2).  Each warp arrives once with its bytes, so the barrier
-// (count WARPS) completes when every range has landed.  A partial task
-// (mask != nullptr) writes zeros for ranges of row blocks outside its mask.
+// Band staging of one tile (whole CTA).  Range k of the tile is an
+// even-aligned span of the residual (layout.cu ranges_k).  Lanes hold the
+// metadata of 32 consecutive ranges; each 8-lane group then copies one range
+// in 16-byte granules (cp.async), so one instruction moves four whole ranges
+// (a handful of cache lines) instead of 32 scattered ones.  (One bulk copy
+// per ~100-byte range is TMA request-rate bound: ~35 cycles per request.)
+// A partial task (mask != nullptr) writes zeros for the ranges of row blocks
+// outside its mask, so phase 1 may stream whole vectors of the tile.
 struct BandMeta {
     int2 m[2];
     int keep[2];
@@ -363,31 +328,34 @@ __device__ __forceinline__ void band_meta_load(const PanelDev &P, int t, BandMet
     }
 }
 
-// Caller guarantees every generic read of buf is ordered before this call
-// by a CTA barrier.
+// Caller guarantees every read of buf is ordered before this call by a CTA
+// barrier; completion: cp.async.wait_group 0 + a CTA barrier.
 __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm, const double *r,
-                                           double *buf, const uint64_t *mask, uint64_t *bar)
+                                           double *buf, const uint64_t *mask)
 {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t bytes = 0;
-    fence_proxy_async();
+    const int sub = lane >> 3, sl = lane & 7;
 #pragma unroll
     for (int it = 0; it < 2; ++it) {
-        const int q = bm.k0 + warp * 32 + lane + it * BLOCK;
-        if (q < bm.k1 && BCT_EXP != 5) {
-            const int g0 = bm.m[it].x;
-            const int pre = (int)((unsigned)bm.m[it].y >> 16), len = bm.m[it].y & 0xffff;
-            const int alen = ((g0 & 1) + len + 1) & ~1;
-            if (bm.keep[it] && ((q - bm.k0) & 3) < BCT_TMA_QUARTERS) {
-                bulk_g2s(buf + pre, r + (g0 & ~1), (uint32_t)alen * 8u, bar);
-                bytes += (uint32_t)alen * 8u;
-            } else if (bm.keep[it]) {
-                // the rest on the LSU path, so the TMA request rate and the
-                // LSU share the staging (waited with cp.async.wait_group)
-                const double *src = r + (g0 & ~1);
-                for (int e = 0; e < alen; e += 2) cp_async16(buf + pre + e, src + e);
-            } else {
-                for (int e = 0; e < alen; ++e) buf[pre + e] = 0.0;
+        const int q0 = bm.k0 + warp * 32 + it * BLOCK;
+        if (q0 >= bm.k1) continue;   // warp-uniform
+#pragma unroll 2
+        for (int jj = 0; jj < 8; ++jj) {
+            const int src = jj * 4 + sub;
+            const int g0 = __shfl_sync(0xffffffffu, bm.m[it].x, src);
+            const int pk = __shfl_sync(0xffffffffu, bm.m[it].y, src);
+            const int keep = __shfl_sync(0xffffffffu, bm.keep[it], src);
+            if (q0 + src < bm.k1 && BCT_EXP != 5) {
+                const int pre = (int)((unsigned)pk >> 16), len = pk & 0xffff;
+                const int ng = ((g0 & 1) + len + 1) >> 1;
+                const double *rs = r + (g0 & ~1);
+                double *dst = buf + pre;
+                if (keep) {
+                    for (int e = sl; e < ng; e += 8) cp_async16(dst + 2 * e, rs + 2 * e);
+                } else {
+                    for (int e = sl; e < ng; e += 8)
+                        *reinterpret_cast<double2 *>(dst + 2 * e) = make_double2(0.0, 0.0);
+                }
             }
         }
     }
@@ -399,23 +367,19 @@ __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm
         const int off = mm.x & 1;
         for (int e = 0; e < len; ++e) buf[pre + off + e] = keep ? r[mm.x + e] : 0.0;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-    __syncwarp();
-    if (lane == 0) mbar_arrive_tx(bar, bytes);
     cp_async_commit();
 }
 
 // Phase-1 work of one tile: g of its columns in slices [sl0, sl1) of the tile.
 // Each 32-column slice is stored lane-interleaved (lane = column, 8 entries
-// per 16/64-byte vector), so the warps split the tile's vector rows and every
-// load is a fully coalesced 2 KB (FP64) / 1 KB (FP32) warp access.  Per-warp
-// column partials meet in `red` and one warp per column sums them in a fixed
-// order.  vr (partial tasks): per slice, the vector rows that can hold rows
-// of the task (others are skipped; rows outside the mask read zeros).
-// Returns this thread's share of gg (lane 0 of the column-owning warps).
-constexpr int RED_STRIDE = 65;
-constexpr int RED_DOUBLES = WARPS * RED_STRIDE;
+// per 16/32-byte lane vector), so a warp-wide vector row is one coalesced
+// 2 KB (FP64) / 1 KB (FP32) access.  The slices of the tile are split over
+// the warps (WARPS/ns warps per slice, vector rows interleaved among them);
+// per-warp column partials meet in `red` and thread c sums column c's
+// partials in a fixed order.  vr (partial tasks): per slice, the vector rows
+// that can hold rows of the task (rows outside the mask read zeros).
+// Returns this thread's share of gg (threads < 32*ns, one column each).
+constexpr int RED_DOUBLES = WARPS * 32;         // partials: (WARPS/ns) x (32*ns)
 static_assert(2 * RED_DOUBLES * 8 == bct::PHASE1_RED_BYTES, "reduction areas");
 
 template <typename V>
@@ -427,47 +391,48 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
     const V *tv = static_cast<const V *>(P.tvals);
     const int nsl_tile = P.tile_cols >> 5;
     const int sb = t * nsl_tile + sl0;
-    const int ns = min(sb + (sl1 - sl0), P.n_cslices) - sb;   // 1 or 2
-    const int base0 = __ldg(P.csl_start + sb);
-    const int base1 = ns > 1 ? __ldg(P.csl_start + sb + 1) : 0;
-    const int end1 = __ldg(P.csl_start + sb + ns);
-    int lo0 = 0, n0 = ((ns > 1 ? base1 : end1) - base0) >> 8;
-    int lo1 = 0, n1 = ns > 1 ? (end1 - base1) >> 8 : 0;
-    if (vr != nullptr) {
-        lo0 = vr[0].x;
-        n0 = vr[0].y - lo0;
-        if (ns > 1) {
-            lo1 = vr[1].x;
-            n1 = vr[1].y - lo1;
+    // slices of this item (0 when a column part lies past the panel's last slice)
+    const int ns = max(0, min(sb + (sl1 - sl0), P.n_cslices) - sb);
+    const int wps = WARPS / max(ns, 1);
+    const int si = warp / wps, sub = warp - si * wps;
+    // the column this thread reduces: prefetch its id and x_J entry
+    const int c = threadIdx.x;
+    const int qc = sb * 32 + c;
+    const bool owner = c < ns * 32 && qc < P.n_cols;
+    int d = 0;
+    double xv = 0.0;
+    if (owner) {
+        d = __ldg(P.corder + qc);
+        xv = xj[d];
+    }
+    if (si < ns) {
+        const int base = __ldg(P.csl_start + sb + si);
+        int lo = 0, hi = (__ldg(P.csl_start + sb + si + 1) - base) >> 8;
+        if (vr != nullptr) {
+            lo = vr[si].x;
+            hi = vr[si].y;
         }
-    }
-    double acc0 = 0.0, acc1 = 0.0;
+        double acc = 0.0;
 #pragma unroll P1U
-    for (int u = warp; u < ((BCT_EXP == 6) ? 0 : n0 + n1); u += WARPS) {
-        const bool first = u < n0;
-        const int i = (first ? base0 + (lo0 + u) * 256 : base1 + (lo1 + u - n0) * 256) + lane * 8;
-        int loc[8];
-        double v[8];
-        ld8u16(P.tloc + i, loc);
-        ld8v(tv + i, v);
-        double a = first ? acc0 : acc1;
+        for (int u = lo + sub; u < hi; u += wps) {
+            const int i = base + u * 256 + lane * 8;
+            int loc[8];
+            double v[8];
+            ld8u16(P.tloc + i, loc);
+            ld8v(tv + i, v);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) a = fma(v[e], bt[loc[e]], a);
-        if (first) acc0 = a; else acc1 = a;
+            for (int e = 0; e < 8; ++e) acc = fma(v[e], bt[loc[e]], acc);
+        }
+        red[sub * (ns * 32) + si * 32 + lane] = acc;
     }
-    red[warp * RED_STRIDE + lane] = acc0;
-    if (ns > 1) red[warp * RED_STRIDE + 32 + lane] = acc1;
-    cp_async_wait_all();   // (batched path: ring copies of this thread)
+    cp_async_wait_all();   // (batched path: ring copies / next band of this thread)
     __syncthreads();
     double wsum = 0.0;
-    for (int c = warp; c < ns * 32; c += WARPS) {
-        const double g = warp_sum(red[lane * RED_STRIDE + c]);
-        const int q = sb * 32 + c;
-        if (lane == 0 && q < P.n_cols) {
-            const int d = __ldg(P.corder + q);
-            gx[d] = make_double2(g, xj[d]);
-            wsum = fma(g, g, wsum);
-        }
+    if (owner) {
+        double g = 0.0;
+        for (int k = 0; k < wps; ++k) g += red[k * (ns * 32) + c];
+        gx[d] = make_double2(g, xv);
+        wsum = g * g;
     }
     return wsum;
 }
@@ -539,8 +504,7 @@ static_assert(sizeof(RingSlot) % 8 == 0, "ring slots are copied in 8-byte words"
 
 template <typename V>
 __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, double *rs, double *sh,
-                              RingSlot *ring, int *s_tpre, int *s_lp, uint64_t *band_bar,
-                              uint32_t &bph)
+                              RingSlot *ring, int *s_tpre, int *s_lp)
 {
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -597,22 +561,20 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
         __syncthreads();
         if (n_items > 0) {
             band_meta_load(ring[0].P, ring[0].t, bm, nullptr);
-            band_issue(ring[0].P, bm, p.r, buf[0], nullptr, &band_bar[0]);
+            band_issue(ring[0].P, bm, p.r, buf[0], nullptr);
             if (n_items > 1) band_meta_load(ring[1].P, ring[1].t, bm, nullptr);
         }
         double wacc = 0.0;
         for (int it = 0; it < n_items; ++it) {
             const int cb = dbuf ? (it & 1) : 0;
-            mbar_wait(&band_bar[cb], (bph >> cb) & 1);
-            bph ^= 1u << cb;
-            if (!dbuf) {   // LSU-staged ranges of this band: issued after the last barrier
+            if (it == 0 || !dbuf) {   // this band was issued after the last barrier
                 cp_async_wait_all();
                 __syncthreads();
             }
             const RingSlot &S = ring[it % RING];
             // the other buffer was last read by tile it-1 (before its barrier)
             if (dbuf && it + 1 < n_items)
-                band_issue(ring[(it + 1) % RING].P, bm, p.r, buf[cb ^ 1], nullptr, &band_bar[cb ^ 1]);
+                band_issue(ring[(it + 1) % RING].P, bm, p.r, buf[cb ^ 1], nullptr);
             if (warp == 0 && it + 2 < n_items) ring_issue(it + 2);
             const double wsum = tile_g<V>(S.P, S.t, 0, S.P.tile_cols >> 5, buf[cb],
                                           p.x + S.P.x_off, gxb + S.gx_off,
@@ -621,11 +583,12 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             // flush this warp's gg partial when the next item is another task
             const int k = S.k;
             if (it + 1 == n_items || ring[(it + 1) % RING].k != k) {
-                if (lane == 0) pgg[((int64_t)k * G + b) * WARPS + warp] = wacc;
+                const double ws = warp_sum(wacc);
+                if (lane == 0) pgg[((int64_t)k * G + b) * WARPS + warp] = ws;
                 wacc = 0.0;
             }
             if (!dbuf && it + 1 < n_items)
-                band_issue(ring[(it + 1) % RING].P, bm, p.r, buf[0], nullptr, &band_bar[0]);
+                band_issue(ring[(it + 1) % RING].P, bm, p.r, buf[0], nullptr);
             if (it + 2 < n_items)
                 band_meta_load(ring[(it + 2) % RING].P, ring[(it + 2) % RING].t, bm, nullptr);
         }
@@ -796,7 +759,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     __shared__ double sh[WARPS];
     __shared__ TaskDev sT;
     __shared__ PanelDev sP;
-    __shared__ int2 vr_s[2];
+    __shared__ int2 vr_s[8];
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -817,15 +780,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
 
     __shared__ RingSlot ring[RING];
     __shared__ int s_tpre[1025], s_lp[1024];
-    __shared__ uint64_t band_bar[2];
-    uint32_t bph = 0;   // phase parity of band_bar[0..1]
-    if (threadIdx.x == 0) {
-        mbar_init(&band_bar[0], WARPS);
-        mbar_init(&band_bar[1], WARPS);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    if (hdr.batched) batched_epoch<V>(p, hdr, rs, sh, ring, s_tpre, s_lp, band_bar, bph);
+    if (hdr.batched) batched_epoch<V>(p, hdr, rs, sh, ring, s_tpre, s_lp);
     for (int k = 0; k < (hdr.batched ? 0 : n_tasks); ++k) {
         __syncthreads();  // sT/sP/R of the previous task may still be in use
         if (threadIdx.x == 0) {
@@ -862,13 +817,11 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             BandMeta bm;
             if (n_items > 0) {
                 band_meta_load(P, item_tile(0), bm, bmask);
-                band_issue(P, bm, p.r, buf0, bmask, &band_bar[0]);
+                band_issue(P, bm, p.r, buf0, bmask);
                 if (n_items > 1) band_meta_load(P, item_tile(1), bm, bmask);
             }
             int cur = 0;
             for (int it = 0; it < n_items; ++it) {
-                mbar_wait(&band_bar[cur], (bph >> cur) & 1);
-                bph ^= 1u << cur;
                 cp_async_wait_all();
                 __syncthreads();
                 const int t = item_tile(it);
@@ -880,7 +833,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 }
                 double *bt = cur ? buf1 : buf0;
                 if (dbuf && it + 1 < n_items) {
-                    band_issue(P, bm, p.r, cur ? buf0 : buf1, bmask, &band_bar[cur ^ 1]);
+                    band_issue(P, bm, p.r, cur ? buf0 : buf1, bmask);
                     if (it + 2 < n_items) band_meta_load(P, item_tile(it + 2), bm, bmask);
                 }
                 if (bmask != nullptr) {
@@ -895,7 +848,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 if (dbuf) {
                     cur ^= 1;
                 } else if (it + 1 < n_items) {
-                    band_issue(P, bm, p.r, buf0, bmask, &band_bar[0]);
+                    band_issue(P, bm, p.r, buf0, bmask);
                     if (it + 2 < n_items) band_meta_load(P, item_tile(it + 2), bm, bmask);
                 }
             }

@@ -167,7 +167,7 @@ struct SamplerParams {
 void launch_sampler(const SamplerParams &p, int n_visits, cudaStream_t s, cudaError_t *err);
 
 // phase-1 tile reduction areas in dynamic shared memory (2 x epoch.cu RED_DOUBLES)
-constexpr size_t PHASE1_RED_BYTES = 2 * 32 * 65 * 8;
+constexpr size_t PHASE1_RED_BYTES = 2 * 32 * 256 / 8 * 8;
 std::string cuda_err(cudaError_t e);
 void launch_epoch(const EpochParams &p, int dtype, int grid, int block, size_t smem,
                   cudaStream_t s, cudaError_t *err);
