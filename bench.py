@@ -47,28 +47,54 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region."""
+    """SM clocks and throttle reasons during the timed region, through NVML
+    (no nvidia-smi subprocesses: forking a process that holds a CUDA context
+    stalls the submitting thread); nvidia-smi only if NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, period=0.01):
         self.index = index
+        self.period = period
         self.samples = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            bits = [pynvml.nvmlClocksEventReasonHwSlowdown,
+                    pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwPowerCap]
+            self._nvml = (pynvml, h, bits)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            nv, h, bits = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            return [float(sm), float(mx)] + [bool(rs & b) for b in bits]
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5).stdout
+        f = [x.strip() for x in out.strip().split(",")]
+        return [float(f[0]), float(f[1])] + [x.lower() == "active" for x in f[2:6]]
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
-                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout
-                self.samples.append([s.strip() for s in out.strip().split(",")])
+                self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period if self._nvml is not None else 0.2)
 
     def __enter__(self):
         self._t.start()
@@ -79,14 +105,12 @@ class ClockSampler:
         self._t.join(timeout=6)
 
     def summary(self):
-        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace('.', '').isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace('.', '').isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples if len(s) >= 6
-                          for k in range(4) if s[2 + k].lower() == "active"})
+        ok = [s for s in self.samples if len(s) == 6]
+        sm = [s[0] for s in ok]
+        reasons = sorted({self.NAMES[k] for s in ok for k in range(4) if s[2 + k]})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "sm_max_mhz": max(s[1] for s in ok) if ok else None, "reasons": reasons,
+                "samples": len(ok), "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def _ncu_traffic(cfg_key):
