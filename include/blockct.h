@@ -191,6 +191,10 @@ int bct_exchange_buffer(bct_ctx *ctx, double **dev_ptr, int64_t *len);
 /* Profiling only: per-block phase timestamps of the last epoch when the
  * environment sets BCT_TIMELINE=1 ([task][6][grid] globaltimer ns). */
 int bct_debug_timeline(bct_ctx *ctx, long long *out, int64_t n_tasks, int32_t *grid);
+/* After the all-reduce of the exchange buffer (enqueued on the context's
+ * stream): r = y - S on the drawn rows; the last epoch's result (bct_wait_epoch)
+ * then holds the global |y - S|^2, |x|^2, |x_t - x|^2.  Asynchronous when
+ * resid_sq is NULL, else it synchronises and returns |y - S|^2. */
 int bct_finish_sharded(bct_ctx *ctx, int32_t flags, double *resid_sq);
 
 #ifdef __cplusplus

@@ -43,6 +43,7 @@ cudaError_t audit(const double *, const double *, const double *, int64_t, unsig
 cudaError_t commit(const PanelDev *, int, int32_t *, double *, double *, cudaStream_t);
 cudaError_t sharded_finish(const double *, const double *, int64_t, const int32_t *,
                            const uint64_t *, double *, double *, int, cudaStream_t);
+cudaError_t sharded_out(const double *, int, const double *, EpochOut *, cudaStream_t);
 }  // namespace bct
 
 namespace {
@@ -1257,12 +1258,20 @@ int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
     const int nb = 296;
     CK(bct::sharded_finish(c->y, c->exchange, c->n_meas, c->rb_of_row, dmask, c->r, c->part, nb,
                            c->stream));
-    std::vector<double> part(nb);
-    CK(cudaMemcpyAsync(part.data(), c->part, 8 * nb, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += part[b];
-    if (resid_sq) *resid_sq = s;
+    // the epoch's result (slot of the last submitted epoch) now carries the
+    // global norms; bct_wait_epoch returns them
+    CK(bct::sharded_out(c->part, nb, c->exchange + c->n_meas, c->out, c->stream));
+    Slot &S = c->slots[(c->head + RING - 1) % RING];
+    if (S.pending) {
+        CK(cudaMemcpyAsync(S.h_out, c->out, sizeof(EpochOut), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaEventRecord(S.done, c->stream));
+    }
+    if (resid_sq) {   // synchronous form
+        double s = 0.0;
+        CK(cudaMemcpyAsync(&s, &c->out->resid_sq, 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        *resid_sq = s;
+    }
     return 0;
 }
 

@@ -388,6 +388,19 @@ __global__ void sharded_finish_kernel(const double *y, const double *S, int64_t 
     }
 }
 
+// Sharded epoch result on the device: |y - S|^2 from the finish partials (block
+// order, like the host sum it replaces), |x|^2 and |x_t - x|^2 from the
+// all-reduced exchange tail.
+__global__ void sharded_out_kernel(const double *part, int nb, const double *tail, EpochOut *out)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[b];
+    out->resid_sq = s;
+    out->x_sq = tail[0];
+    out->err_sq = tail[1];
+}
+
 inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 }  // namespace
@@ -537,6 +550,13 @@ cudaError_t sharded_finish(const double *y, const double *S, int64_t n, const in
                            const uint64_t *mask, double *r, double *part, int nb, cudaStream_t s)
 {
     sharded_finish_kernel<<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, r, part);
+    return cudaGetLastError();
+}
+
+cudaError_t sharded_out(const double *part, int nb, const double *tail, EpochOut *out,
+                        cudaStream_t s)
+{
+    sharded_out_kernel<<<1, 32, 0, s>>>(part, nb, tail, out);
     return cudaGetLastError();
 }
 

@@ -71,20 +71,24 @@ class DeviceShard:
         self.stream = torch.cuda.ExternalStream(system.stream(), device=system.device)
 
     def run_partial(self, packed, flags):
+        # asynchronous: the all-reduce and the finish kernels follow on the
+        # same stream; the host waits only in ``result``
         submit(self.system, "parallel", packed, flags | N.BCT_SHARDED)
-        return wait(self.system, packed.task_j.size)[0]
+        return packed.task_j.size
 
     def exchange(self):
         return self.buf
 
-    def finish(self, flags):
+    def comm_stream(self):
         import torch
-        torch.cuda.current_stream(self.system.device).synchronize()  # the all-reduce
-        rs = ctypes.c_double()
-        N.check(N.load().bct_finish_sharded(self.system.ctx, flags, ctypes.byref(rs)),
-                self.system.ctx)
-        tail = self.buf[self.n_meas:self.n_meas + 2].cpu().numpy()
-        return rs.value, float(tail[0]), float(tail[1])
+        return torch.cuda.stream(self.stream)
+
+    def finish(self, flags):
+        N.check(N.load().bct_finish_sharded(self.system.ctx, flags, None), self.system.ctx)
+        return None
+
+    def result(self, n_tasks):
+        return wait(self.system, n_tasks)[0]
 
 
 class ShardedRunner:
@@ -98,16 +102,32 @@ class ShardedRunner:
             import torch.distributed as dist
             allreduce = dist.all_reduce
         self.allreduce = allreduce
+        self._pending = []
 
-    def epoch(self, packed, flags):
-        res = self.backend.run_partial(packed, flags)
-        self.allreduce(self.backend.exchange())
-        resid_sq, x_sq, err_sq = self.backend.finish(flags)
-        res.resid_sq = resid_sq
-        res.x_sq = x_sq
-        res.err_sq = err_sq
+    def submit(self, packed, flags):
+        """Enqueue one sharded epoch: partial epoch, all-reduce, finish."""
+        token = self.backend.run_partial(packed, flags)
+        ctx = getattr(self.backend, "comm_stream", None)
+        if ctx is not None:
+            with ctx():
+                self.allreduce(self.backend.exchange())
+        else:
+            self.allreduce(self.backend.exchange())
+        norms = self.backend.finish(flags)
+        self._pending.append((packed, token, norms))
+
+    def collect(self):
+        """Result of the oldest submitted epoch (EpochResult with global norms)."""
+        packed, token, norms = self._pending.pop(0)
+        res = self.backend.result(token) if hasattr(self.backend, "result") else token
+        if norms is not None:
+            res.resid_sq, res.x_sq, res.err_sq = norms
         res.n_tasks = packed.task_j.size
         return res
+
+    def epoch(self, packed, flags):
+        self.submit(packed, flags)
+        return self.collect()
 
 
 def sharded_forward(system, x, allreduce=None):

@@ -286,3 +286,35 @@ def test_device_sampler_many_row_blocks(gs, alpha, strategy):
         assert [(j, [g.tolist() for g in gs_]) for j, gs_ in rec_h[e]] == \
                [(j, [g.tolist() for g in gs_]) for j, gs_ in rec_d[e]]
     assert np.array_equal(x_h, x_d)
+
+
+# ---------------------------------------------------------------------------
+# sharded parallel mode on the device (NCCL, world size 1: the pool has one
+# GPU; the 2-rank protocol is covered on CPU by tests/test_sharded_gloo.py)
+# ---------------------------------------------------------------------------
+
+def test_sharded_device_path_single_rank(cfg1_system):
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_00953_b200.distributed import run_gcsgd_sharded
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1)
+    try:
+        f = golden("pb_cfg1_runs.npz")
+        p = SolverParams(epochs=8, b=0.25, group_size=2, seed=19, execution_mode="parallel",
+                         sampling=SamplingConfig(alpha=0.75))
+        x_ref, tr_ref = run_gcsgd(cfg1_system, f["y"], p, x_true=f["x_true"])
+        x_sh, tr_sh = run_gcsgd_sharded(cfg1_system, f["y"], p, x_true=f["x_true"])
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(x_sh, x_ref)
+    assert [r.snr_db for r in tr_sh.rows] == [r.snr_db for r in tr_ref.rows]
+    assert [r.obs_gap_db for r in tr_sh.rows] == pytest.approx(
+        [r.obs_gap_db for r in tr_ref.rows], rel=1e-12)
