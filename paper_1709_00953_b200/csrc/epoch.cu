@@ -412,6 +412,7 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
             lo = vr[si].x;
             hi = vr[si].y;
         }
+        if (BCT_EXP == 6) hi = lo;   // profiling: staging and structure only
         double acc = 0.0;
 #pragma unroll P1U
         for (int u = lo + sub; u < hi; u += wps) {

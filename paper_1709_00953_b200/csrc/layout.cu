@@ -26,6 +26,7 @@
 // segments in tile order, so the bitwise set-up kernels (builder.cu) recover
 // the reference's summation order by merging a row's segments by column.
 #include <cstdint>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <string>
@@ -424,6 +425,94 @@ __global__ void csc_sell_pad_k(const int32_t *colstart, const int32_t *corder, i
     }
 }
 
+// Bank-aware order inside each lane's 8-entry vector.  Phase 1 gathers
+// band[tloc] with one 8-byte shared load per entry position e: a half-warp
+// (16 lanes) is one 128-byte wavefront when its 16 slots fall in distinct
+// bank pairs (slot mod 16) or repeat an address, and one more wavefront per
+// extra distinct slot in a bank pair otherwise.  The order of a lane's 8
+// entries is free (it only reorders that lane's fma chain), so a warp per
+// vector row assigns, position by position and lane by lane, the remaining
+// entry that adds the fewest wavefronts; zero padding entries take the slot
+// another lane already reads (a broadcast).
+template <typename V>
+__global__ void csc_bank_perm_k(V *tvals, uint16_t *tloc, const int32_t *csl_start,
+                                int32_t n_cslices)
+{
+    constexpr int WPB = 4;
+    __shared__ int cnt_s[WPB][2][16];
+    __shared__ int first_s[WPB][2][16];
+    __shared__ int any_s[WPB][2];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int gw = blockIdx.x * WPB + wib, nw = gridDim.x * WPB;
+    int *cnt = &cnt_s[wib][lane >> 4][0];
+    int *first = &first_s[wib][lane >> 4][0];
+    for (int sl = gw; sl < n_cslices; sl += nw) {
+        const int64_t base0 = csl_start[sl];
+        const int nvr = (int)((csl_start[sl + 1] - base0) >> 8);
+        for (int u = 0; u < nvr; ++u) {
+            const int64_t base = base0 + (int64_t)u * 256 + lane * 8;
+            V val[8];
+            int loc[8];
+            for (int e = 0; e < 8; ++e) {
+                val[e] = tvals[base + e];
+                loc[e] = tloc[base + e];
+            }
+            V oval[8];
+            int oloc[8];
+            unsigned left = 0xffu;
+            for (int e = 0; e < 8; ++e) {
+                if (lane < 16) {
+                    cnt_s[wib][0][lane] = 0;
+                    cnt_s[wib][1][lane] = 0;
+                }
+                if (lane < 2) any_s[wib][lane] = -1;
+                __syncwarp();
+                for (int who = 0; who < 32; ++who) {
+                    if (lane == who) {
+                        int best = -1, bcost = 1 << 30, pad = -1;
+                        for (int j = 0; j < 8; ++j) {
+                            if (!((left >> j) & 1u)) continue;
+                            if (val[j] == (V)0) {
+                                if (pad < 0) pad = j;
+                                continue;
+                            }
+                            const int b = loc[j] & 15;
+                            const int c = (cnt[b] == 0 || first[b] == loc[j]) ? 0 : cnt[b];
+                            if (c < bcost) {
+                                bcost = c;
+                                best = j;
+                            }
+                        }
+                        int pick = best;
+                        int a = best >= 0 ? loc[best] : 0;
+                        if (pad >= 0 && (best < 0 || bcost > 0)) {
+                            pick = pad;   // a zero entry: read a slot already read
+                            const int an = any_s[wib][lane >> 4];
+                            a = an >= 0 ? an : (best >= 0 ? loc[best] : loc[pad]);
+                        }
+                        const int b = a & 15;
+                        if (cnt[b] == 0) {
+                            cnt[b] = 1;
+                            first[b] = a;
+                        } else if (first[b] != a) {
+                            ++cnt[b];
+                        }
+                        if (any_s[wib][lane >> 4] < 0) any_s[wib][lane >> 4] = a;
+                        oval[e] = val[pick];
+                        oloc[e] = a;
+                        left &= ~(1u << pick);
+                    }
+                    __syncwarp();
+                }
+            }
+            for (int e = 0; e < 8; ++e) {
+                tvals[base + e] = oval[e];
+                tloc[base + e] = (uint16_t)oloc[e];
+            }
+        }
+    }
+}
+
 // cptr[d*(m+1)+i] = column-local index of column d's first entry with local row >= rbp[i]
 __global__ void cptr_local_k(const int32_t *colstart, const int32_t *tlocal_sorted,
                              const int32_t *rbp, int m, int32_t n_cols, int32_t *cptr)
@@ -761,6 +850,13 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
             n_cols, csl_start, n_cslices, (float *)tvals, tloc);
     cptr_local_k<<<nb((int64_t)n_cols * (m + 1), 256), 256, 0, s>>>(colstart, tls, rbp, m, n_cols,
                                                                    cptr);
+    if (!getenv("BCT_NO_BANK_PERM") && n_cslices > 0) {
+        const unsigned pb = (unsigned)std::min<int64_t>((n_cslices + 3) / 4, 4096);
+        if (dtype == 0)
+            csc_bank_perm_k<double><<<pb, 128, 0, s>>>((double *)tvals, tloc, csl_start, n_cslices);
+        else
+            csc_bank_perm_k<float><<<pb, 128, 0, s>>>((float *)tvals, tloc, csl_start, n_cslices);
+    }
     LCK(cudaGetLastError());
     LCK(cudaStreamSynchronize(s));
     release(tmp);
