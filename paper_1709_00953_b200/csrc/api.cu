@@ -260,6 +260,11 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
             si + 1 == shapes.size()) {
             P = Q;
             c->allocs.insert(c->allocs.end(), kept.begin(), kept.end());
+            if (getenv("BCT_VERBOSE"))
+                fprintf(stderr, "panel %d: tile %dx%d nnz %lld fwd_cap %lld csc_cap %lld band_max %d "
+                        "n_seg %d n_slices %d\n", j, th, tw, (long long)nnz,
+                        (long long)Q.fwd_cap, (long long)Q.csc_cap, Q.band_max,
+                        Q.n_seg, Q.n_slices);
             break;
         }
         for (void *q : kept) cudaFree(q);
@@ -278,7 +283,7 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     c->nnz += nnz;
     c->max_rows = std::max<int64_t>(c->max_rows, n_rows);
     c->max_cols = std::max<int64_t>(c->max_cols, n_cols);
-    c->max_seg = std::max<int64_t>(c->max_seg, P.n_seg);
+    c->max_seg = std::max<int64_t>(c->max_seg, (int64_t)P.n_slices * 32);   // partial slots
     c->band_cap = std::max(c->band_cap, (P.band_max + 1) & ~1);
     c->smem = std::max<size_t>(c->smem, (size_t)P.st_max * 16);
     return 0;
@@ -1166,7 +1171,7 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
             tot_rows += P.n_rows;
             if (T.flags & TASK_FIRST_OF_VISIT) tot_vox += P.n_cols;
             gxo += P.n_cols;
-            sgo += P.n_seg;
+            sgo += (int64_t)P.n_slices * 32;
             txo += P.n_rows;
         }
         if (tot_slices >= (1ll << 31) || tot_rows >= (1ll << 31) || gxo >= (1ll << 31)) batched = false;

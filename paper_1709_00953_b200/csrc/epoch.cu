@@ -422,7 +422,8 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
             ld8u16(P.tloc + i, loc);
             ld8v(tv + i, v);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc = fma(v[e], bt[loc[e]], acc);
+            for (int e = 0; e < 8; ++e)
+                acc = fma(v[e], BCT_EXP == 7 ? (double)loc[e] : bt[loc[e]], acc);
         }
         red[sub * (ns * 32) + si * 32 + lane] = acc;
     }
@@ -650,8 +651,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                         ax = fma(v[q], (double)a.y, ax);
                     }
                 }
-                const int seg = __ldg(P.sl_seg + (int64_t)sl * 32 + lane);
-                if (seg >= 0) spart[seg] = make_double2(t, ax);
+                spart[(int64_t)sl * 32 + lane] = make_double2(t, ax);   // SELL order
             }
             fu = ge;
         }
@@ -680,7 +680,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                 double t = 0.0, ax = 0.0;
                 const int q1 = __ldg(P.rseg_ptr + lr + 1);
                 for (int q = __ldg(P.rseg_ptr + lr); q < q1; ++q) {
-                    const double2 a = spart[__ldg(P.rseg + q)];
+                    const double2 a = spart[__ldg(P.rpos + q)];   // SELL-order partials
                     t += a.x;
                     ax += a.y;
                 }
@@ -928,8 +928,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                             ax = fma(v[q], (double)a.y, ax);
                         }
                     }
-                    const int seg = __ldg(P.sl_seg + (int64_t)sl * 32 + lane);
-                    if (seg >= 0) spart[seg] = make_double2(t, ax);
+                    spart[(int64_t)sl * 32 + lane] = make_double2(t, ax);   // SELL order
                 }
                 __syncthreads();
                 fu = ge;
@@ -949,7 +948,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 double t = 0.0, ax = 0.0;
                 const int q1 = __ldg(P.rseg_ptr + lr + 1);
                 for (int q = __ldg(P.rseg_ptr + lr); q < q1; ++q) {
-                    const double2 a = spart[__ldg(P.rseg + q)];
+                    const double2 a = spart[__ldg(P.rpos + q)];   // SELL-order partials
                     t += a.x;
                     ax += a.y;
                 }

@@ -34,6 +34,8 @@ struct PanelDev {
     const int32_t *seg_lane;
     const int32_t *rseg_ptr;   // [n_rows+1] row -> its segments (tile order) in rseg
     const int32_t *rseg;
+    const int32_t *rpos;       // [n_seg] SELL position (slice*32+lane) of rseg's segments:
+                               // where the epoch kernel stores each segment's partial
     // panel CSC with tile bands (phase 1): slices of 32 columns of a tile,
     // entry e of lane l of slice s at csl_start[s] + ((e/8)*32 + l)*8 + e%8
     const void *tvals;         // T

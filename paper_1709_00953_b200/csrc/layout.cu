@@ -242,6 +242,13 @@ __global__ void rkey_k(const int32_t *seg_key, int32_t n_seg, int32_t n_rows, in
     rkey[s] = (seg_key[s] % n_rows) * n_st + seg_key[s] / n_rows;
 }
 
+__global__ void rpos_k(const int32_t *rseg, const int32_t *seg_slice, const int32_t *seg_lane,
+                       int32_t n_seg, int32_t *rpos)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < n_seg) rpos[q] = seg_slice[rseg[q]] * 32 + seg_lane[rseg[q]];
+}
+
 __global__ void rseg_ptr_k(const int32_t *srkey, int32_t n_seg, int32_t n_rows, int32_t n_st,
                            int32_t *rseg_ptr)
 {
@@ -745,6 +752,12 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
                                 bits_for((int64_t)n_rows * n_st), tmp, s));
     }
     rseg_ptr_k<<<nb(n_rows + 1, 256), 256, 0, s>>>(srkey, n_seg, n_rows, n_st, rseg_ptr);
+    // the epoch kernel stores segment partials in SELL order (slice*32 +
+    // lane: coalesced stores in phase 2); rpos lists each row's partials
+    int32_t *rpos = K.get<int32_t>(n_seg + 1);
+    LNN(rpos);
+    if (n_seg > 0)
+        rpos_k<<<nb(n_seg, 256), 256, 0, s>>>(rseg, seg_slice, seg_lane, n_seg, rpos);
     LCK(cudaGetLastError());
 
     // ================= CSC with tile bands =================
@@ -873,6 +886,7 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     P.st_ptr = st_ptr;
     P.rseg_ptr = rseg_ptr;
     P.rseg = rseg;
+    P.rpos = rpos;
     P.tvals = tvals;
     P.csl_start = csl_start;
     P.n_cslices = n_cslices;
