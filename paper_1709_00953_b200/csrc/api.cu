@@ -179,6 +179,7 @@ int set_mask(uint64_t *mask, int i) { mask[i >> 6] |= 1ull << (i & 63); return 0
 struct Placement {
     std::vector<int32_t> c2d, d2c, st_ptr, corder;
     int32_t mdiv = 1;
+    int32_t swz_shift = 7;   // log2 of the super tiles' row length (swz_idx)
 };
 
 Placement place_voxels(int64_t n_cols, int64_t h, int64_t w, int th, int tw)
@@ -188,6 +189,8 @@ Placement place_voxels(int64_t n_cols, int64_t h, int64_t w, int th, int tw)
     pl.d2c.resize(n_cols);
     if (h > 0 && w > 0 && h * w == n_cols && h <= ST_VOXELS / 4) {
         int64_t sw = std::max<int64_t>(4, (ST_VOXELS / h) & ~3ll);
+        pl.swz_shift = 4;
+        while (pl.swz_shift < 15 && (2ll << pl.swz_shift) <= sw) ++pl.swz_shift;
         int32_t d = 0;
         for (int64_t y0 = 0; y0 < w; y0 += sw) {
             pl.st_ptr.push_back(d);
@@ -252,6 +255,7 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
         std::string err;
         std::vector<void *> kept;
         PanelDev Q = P;
+        Q.swz_shift = pl.swz_shift;
         if (bct::layout_panel_v2(c->dtype, c->m, n_rows, n_cols, nnz, vals64, cols, indptr, l2g,
                                  d_rbp, pl.c2d, pl.st_ptr, pl.corder, th * tw, Q, kept, err,
                                  c->stream))
@@ -285,7 +289,7 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     c->max_cols = std::max<int64_t>(c->max_cols, n_cols);
     c->max_seg = std::max<int64_t>(c->max_seg, (int64_t)P.n_slices * 32);   // partial slots
     c->band_cap = std::max(c->band_cap, (P.band_max + 1) & ~1);
-    c->smem = std::max<size_t>(c->smem, (size_t)P.st_max * 16);
+    c->smem = std::max<size_t>(c->smem, (size_t)((P.st_max + 15) & ~15) * 16);   // swizzled
     return 0;
 }
 
@@ -769,7 +773,7 @@ int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *i
             int basev = stp[sk[s] / P.n_rows];
             for (int e = 0; e < sln[s]; ++e) {
                 int64_t pos = sst[ssl[s]] + ((int64_t)(e >> 2) * 32 + sla[s]) * 4 + (e & 3);
-                row.push_back({d2c[basev + fi[pos]], fv[pos]});
+                row.push_back({d2c[basev + swz_idx(fi[pos], P.swz_shift)], fv[pos]});
             }
         }
         std::sort(row.begin(), row.end(),
@@ -1155,6 +1159,7 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
     for (int64_t k = 0; batched && k < nt; ++k)
         if (memcmp(tasks[k].mask, full, sizeof full) != 0) batched = false;
     int64_t tot_tiles = 0, tot_slices = 0, tot_rows = 0, tot_vox = 0, gxo = 0, sgo = 0, txo = 0;
+    int64_t tot_ent = 0;
     if (batched) {
         for (int64_t k = 0; k < nt; ++k) {
             TaskDev &T = tasks[k];
@@ -1166,6 +1171,8 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
             T.gx_off = gxo;
             T.seg_off = sgo;
             T.tax_off = txo;
+            T.ent_pre = tot_ent;
+            tot_ent += P.fwd_cap;
             tot_tiles += P.n_tiles;
             tot_slices += P.n_slices;
             tot_rows += P.n_rows;
@@ -1202,6 +1209,7 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
     c->h_hdr->n_slices_total = (int32_t)tot_slices;
     c->h_hdr->n_rows_total = (int32_t)tot_rows;
     c->h_hdr->n_vox_total = (int32_t)tot_vox;
+    c->h_hdr->n_ent_total = tot_ent;
     memcpy(c->h_hdr->epoch_mask, emask, sizeof(uint64_t) * BCT_MASKW);
     if (nt) memcpy(c->h_tasks, tasks.data(), sizeof(TaskDev) * nt);
     return launch_staged(c, nt, n_visits, hook);

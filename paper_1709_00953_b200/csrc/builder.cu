@@ -269,12 +269,12 @@ __device__ double row_dot(const PanelDev &P, int64_t lr, const double *xj)
     for (;;) {
         int gmin = INT_MAX;
         for (int k = 0; k < ns; ++k)
-            if (cur[k] < len[k]) gmin = min(gmin, P.d2c[base[k] + P.fidx[pos(k)]] / P.mdiv);
+            if (cur[k] < len[k]) gmin = min(gmin, P.d2c[base[k] + swz_idx(P.fidx[pos(k)], P.swz_shift)] / P.mdiv);
         if (gmin == INT_MAX) break;
         for (int k = 0; k < ns; ++k)
-            while (cur[k] < len[k] && P.d2c[base[k] + P.fidx[pos(k)]] / P.mdiv == gmin) {
+            while (cur[k] < len[k] && P.d2c[base[k] + swz_idx(P.fidx[pos(k)], P.swz_shift)] / P.mdiv == gmin) {
                 const int64_t ps = pos(k);
-                acc = __dadd_rn(acc, __dmul_rn((double)fv[ps], xj[base[k] + P.fidx[ps]]));
+                acc = __dadd_rn(acc, __dmul_rn((double)fv[ps], xj[base[k] + swz_idx(P.fidx[ps], P.swz_shift)]));
                 ++cur[k];
             }
     }

@@ -480,6 +480,32 @@ __device__ __forceinline__ double z_value(double t, double ax, double mu, int st
 // phase and four grid barriers per epoch instead of three per task.
 // ======================================================================
 
+// First i in [0, n] with key <= at(i) (at ascending; at(n) = +inf), found by one
+// full warp with 32-way probes: a few dependent loads instead of log2(n).
+template <typename At, typename K>
+__device__ __forceinline__ int lower_bound_warp(At at, int n, K key)
+{
+    const int lane = threadIdx.x & 31;
+    int lo = 0, hi = n;
+    for (;;) {
+        const int span = hi - lo;
+        const int step = span > 32 ? (span + 31) / 32 : 1;
+        const int idx = lo + lane * step;
+        const bool ge = idx >= hi || !(at(idx) < key);
+        const unsigned m = __ballot_sync(0xffffffffu, ge);
+        if (span <= 32) return m ? min(lo + __ffs(m) - 1, hi) : hi;
+        if (m == 0) {                        // every probe < key: past the last probe
+            lo += 31 * step + 1;
+            continue;
+        }
+        const int f = __ffs(m) - 1;
+        if (f == 0) return lo;
+        const int nlo = lo + (f - 1) * step + 1;
+        hi = min(hi, lo + f * step);
+        lo = nlo;
+    }
+}
+
 __device__ __forceinline__ int task_of(const TaskDev *tasks, int n_tasks, int which, int f)
 {
     // last task whose prefix (field `which`) is <= f
@@ -500,6 +526,8 @@ struct RingSlot {
     PanelDev P;
     int64_t gx_off;
     int k, t;
+    int part, nparts;   // slice part of a split last-round tile (nparts 1: whole tile)
+    int pad_;
 };
 constexpr int RING = 4;
 static_assert(sizeof(RingSlot) % 8 == 0, "ring slots are copied in 8-byte words");
@@ -508,6 +536,7 @@ template <typename V>
 __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, double *rs, double *sh,
                               RingSlot *ring, int *s_tpre, int *s_lp)
 {
+    __shared__ long long s_range_dbg[3];
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int G = gridDim.x, b = blockIdx.x;
@@ -532,12 +561,17 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
         pgg[((int64_t)(q / WARPS) * G + b) * WARPS + q % WARPS] = 0.0;
     __syncthreads();
     {
-        const int n_items = (hdr.n_tiles_total - b + G - 1) / G;
+        // whole tiles in rounds of G; the tiles of the last partial round are
+        // cut into up to 8 slice parts so every CTA gets the same share
+        const int bb = BCT_EXP == 9 ? G - 1 - b : b;   // profiling: reversed item map
+        const int full = hdr.n_tiles_total / G, rem = hdr.n_tiles_total - full * G;
+        const int nsplit = rem > 0 ? max(1, min(8, G / rem)) : 1;
+        const int n_items = full + (bb < rem * nsplit ? 1 : 0);
         const bool dbuf = p.band_dbuf != 0;
         double *buf[2] = {rs, rs + (dbuf ? p.band_cap : 0)};
         double *red = rs + (int64_t)p.band_cap * (dbuf ? 2 : 1);
         auto ring_issue = [&](int it) {   // warp 0
-            const int item = b + it * G;
+            const int item = it < full ? bb + it * G : full * G + bb / nsplit;
             int lo = 0, hi = n_tasks - 1;  // last task with tile_pre <= item
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
@@ -551,6 +585,8 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                 cp_async8(&S.gx_off, &p.tasks[lo].gx_off);
                 S.k = lo;
                 S.t = item - s_tpre[lo];
+                S.part = it < full ? 0 : bb % nsplit;
+                S.nparts = it < full ? 1 : nsplit;
             }
             cp_async_commit();
         };
@@ -578,7 +614,9 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             if (dbuf && it + 1 < n_items)
                 band_issue(ring[(it + 1) % RING].P, bm, p.r, buf[cb ^ 1], nullptr);
             if (warp == 0 && it + 2 < n_items) ring_issue(it + 2);
-            const double wsum = tile_g<V>(S.P, S.t, 0, S.P.tile_cols >> 5, buf[cb],
+            const int nsl = S.P.tile_cols >> 5;
+            const double wsum = tile_g<V>(S.P, S.t, S.part * nsl / S.nparts,
+                                          (S.part + 1) * nsl / S.nparts, buf[cb],
                                           p.x + S.P.x_off, gxb + S.gx_off,
                                           red + (it & 1) * RED_DOUBLES, nullptr);
             wacc += wsum;
@@ -603,15 +641,40 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     {
         using GS = typename std::conditional<sizeof(V) == 4, float2, double2>::type;
         GS *gs = reinterpret_cast<GS *>(rs);
-        const int ns = hdr.n_slices_total;
-        const int ub = (int)((int64_t)ns * b / G), ue = (int)((int64_t)ns * (b + 1) / G);
+        // this CTA: the slices whose first entry lies in an equal share of the
+        // epoch's stored entries (slices differ in length)
+        auto slice_at = [&](int64_t ent) -> int {
+            if (ent >= hdr.n_ent_total) return hdr.n_slices_total;
+            const int k = lower_bound_warp([&](int q) { return p.tasks[q].ent_pre; }, n_tasks,
+                                           ent + 1) - 1;
+            const TaskDev &T = p.tasks[k];
+            const PanelDev &PP = p.panels[T.lp];
+            const int64_t local = ent - T.ent_pre;
+            return T.slice_pre +
+                   lower_bound_warp([&](int q) { return PP.slice_start[q]; }, PP.n_slices,
+                                    (int32_t)local);
+        };
+        __shared__ int s_range[2];
+        __shared__ int s_next;
+        if (warp == 0) {
+            const int u0 = slice_at(hdr.n_ent_total * b / G);
+            const int u1 = slice_at(hdr.n_ent_total * (b + 1) / G);
+            if (lane == 0) {
+                s_range[0] = u0;
+                s_range[1] = u1;
+            }
+        }
+        __syncthreads();
+        const int ub = s_range[0], ue = s_range[1];
         int fu = ub;
+        int dbg_segs = 0;   // profiling (BCT_TIMELINE): super tiles of this CTA
         while (fu < ue) {
             __syncthreads();
             if (threadIdx.x == 0) {
                 const int k = task_of(p.tasks, n_tasks, 1, fu);
                 ring[0].k = k;
                 ring[0].P = p.panels[p.tasks[k].lp];
+                s_next = fu;
             }
             __syncthreads();
             const PanelDev &P = ring[0].P;
@@ -625,14 +688,22 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const int ge = min(ue, T.slice_pre + st_end);
             const int v0 = __ldg(P.st_ptr + st), v1 = __ldg(P.st_ptr + st + 1);
             const double2 *gx = gxb + T.gx_off;
-            for (int q = threadIdx.x; q < v1 - v0; q += BLOCK) {
+            ++dbg_segs;
+            for (int q = threadIdx.x; q < (BCT_EXP == 10 ? 0 : v1 - v0); q += BLOCK) {
                 const double2 a = gx[v0 + q];
-                gs[q] = GS{(decltype(GS::x))a.x, (decltype(GS::x))a.y};
+                gs[swz_idx(q, P.swz_shift)] = GS{(decltype(GS::x))a.x, (decltype(GS::x))a.y};
             }
             __syncthreads();
             const V *fv = static_cast<const V *>(P.fvals);
             double2 *spart = segb + T.seg_off;
-            for (int f = fu + warp; f < ge; f += WARPS) {
+            // slices are taken one at a time from a shared counter: their
+            // lengths vary (up to SEG_CAP/4 vectors), so a static round robin
+            // leaves warps idle at the super tile's barrier
+            for (;;) {
+                int f = 0;
+                if (lane == 0) f = atomicAdd(&s_next, 1);
+                f = __shfl_sync(0xffffffffu, f, 0);
+                if (f >= ge) break;
                 const int sl = f - T.slice_pre;
                 const int base = __ldg(P.slice_start + sl);
                 const int nvec = (__ldg(P.slice_start + sl + 1) - base) >> 7;
@@ -655,8 +726,18 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             }
             fu = ge;
         }
+        if (threadIdx.x == 0) {
+            s_range_dbg[0] = ub;
+            s_range_dbg[1] = ue;
+            s_range_dbg[2] = dbg_segs;
+        }
     }
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 3);
+    if (p.timeline && threadIdx.x == 0 && n_tasks > 1) {   // profiling: phase-B shares
+        p.timeline[((int64_t)1 * 8 + 0) * gridDim.x + blockIdx.x] = s_range_dbg[0];
+        p.timeline[((int64_t)1 * 8 + 1) * gridDim.x + blockIdx.x] = s_range_dbg[1];
+        p.timeline[((int64_t)1 * 8 + 2) * gridDim.x + blockIdx.x] = s_range_dbg[2];
+    }
     grid_sync(p.bar);
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 4);
 
@@ -897,7 +978,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 const int v0 = __ldg(P.st_ptr + st), v1 = __ldg(P.st_ptr + st + 1);
                 for (int q = threadIdx.x; q < v1 - v0; q += BLOCK) {
                     const double2 a = gx[v0 + q];
-                    gs[q] = GS{(decltype(GS::x))a.x, (decltype(GS::x))a.y};
+                    gs[swz_idx(q, P.swz_shift)] = GS{(decltype(GS::x))a.x, (decltype(GS::x))a.y};
                 }
                 __syncthreads();
                 for (int f = fu + warp; f < ge; f += WARPS) {
@@ -1066,6 +1147,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             }
         }
     }
+    if (hdr.batched && !BCT_NO_TL_BATCH) TL_MARK(0, 7);
     double b0 = block_sum_all(rsq, sh);
     double b1 = block_sum_all(xsq, sh);
     double b2 = block_sum_all(esq, sh);

@@ -59,7 +59,7 @@ struct PanelDev {
     int32_t mdiv;              // reference order = (c / mdiv, tile, c) for bitwise merges
     int32_t tile_cols;         // columns per phase-1 tile (multiple of 32)
     int32_t n_cslices;
-    int32_t pad2_;
+    int32_t swz_shift;         // phase-2 super tile swizzle (see swz_idx)
 };
 
 struct TaskDev {
@@ -76,6 +76,7 @@ struct TaskDev {
     int64_t gx_off;    // (g, x) pairs of the task: gx_batch + gx_off
     int64_t seg_off;   // segment partials: seg_batch + seg_off
     int64_t tax_off;   // (t, ax) per local row: tax_batch + tax_off
+    int64_t ent_pre;   // forward-store entries of the tasks before this one
 };
 
 enum { TASK_LAST_OF_VISIT = 1, TASK_FIRST_OF_VISIT = 2 };
@@ -87,6 +88,7 @@ struct EpochHeader {
     int32_t batched;   // 1: parallel epoch of full-panel tasks, phase-by-phase over all tasks
     int32_t n_tiles_total, n_slices_total, n_rows_total, n_vox_total;
     uint64_t epoch_mask[BCT_MASKW];  // union of all drawn blocks (parallel refresh)
+    int64_t n_ent_total;             // forward-store entries of the batched tasks
 };
 
 // Device-side per-epoch outputs.
@@ -144,6 +146,16 @@ struct EpochParams {
 struct bct_ctx_s;
 
 // builder / launch helpers implemented in the .cu files
+// Position of super-tile voxel q in the staged (g, x) array: the low four bits
+// are XORed with the voxel's pseudo-row (q >> shift, shift = log2 of the super
+// tile's row length), so the lanes of a slice that read one voxel column of
+// consecutive image rows (rays along the strip) hit distinct shared-memory
+// bank pairs.  An involution for shift >= 4.
+__host__ __device__ __forceinline__ int swz_idx(int q, int shift)
+{
+    return q ^ ((q >> shift) & 15);
+}
+
 namespace bct {
 
 // device sampler (sampler.cu)

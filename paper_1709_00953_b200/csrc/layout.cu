@@ -190,7 +190,7 @@ __global__ void sell_scatter_k(const int32_t *perm, const int32_t *incl, const i
                                const int32_t *seg_lane, const int32_t *slice_start,
                                const double *vals64, const int32_t *cols_c, const int32_t *c2d,
                                const int32_t *st_ptr, int32_t n_rows, int64_t nnz, V *fvals,
-                               uint16_t *fidx)
+                               uint16_t *fidx, int swz_shift)
 {
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= nnz) return;
@@ -200,7 +200,7 @@ __global__ void sell_scatter_k(const int32_t *perm, const int32_t *incl, const i
     int64_t e = q - seg_first[s];
     int64_t pos = slice_start[seg_slice[s]] + ((e >> 2) * 32 + seg_lane[s]) * 4 + (e & 3);
     fvals[pos] = (V)vals64[p];
-    fidx[pos] = (uint16_t)(c2d[cols_c[p]] - st_ptr[st]);
+    fidx[pos] = (uint16_t)swz_idx(c2d[cols_c[p]] - st_ptr[st], swz_shift);
 }
 
 // padding of every (slice, lane): zero values on the lane's last voxel
@@ -728,13 +728,13 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
         if (dtype == 0) {
             sell_scatter_k<double><<<nb(nnz, 256), 256, 0, s>>>(perm, incl, seg_first, seg_key,
                 seg_slice, seg_lane, slice_start, vals64, cols_c, c2d, st_ptr, n_rows, nnz,
-                (double *)fvals, fidx);
+                (double *)fvals, fidx, P.swz_shift);
             sell_pad_k<double><<<nb((int64_t)n_slices * 32, 256), 256, 0, s>>>(sl_seg, seg_len,
                 slice_start, n_slices, (double *)fvals, fidx);
         } else {
             sell_scatter_k<float><<<nb(nnz, 256), 256, 0, s>>>(perm, incl, seg_first, seg_key,
                 seg_slice, seg_lane, slice_start, vals64, cols_c, c2d, st_ptr, n_rows, nnz,
-                (float *)fvals, fidx);
+                (float *)fvals, fidx, P.swz_shift);
             sell_pad_k<float><<<nb((int64_t)n_slices * 32, 256), 256, 0, s>>>(sl_seg, seg_len,
                 slice_start, n_slices, (float *)fvals, fidx);
         }

@@ -28,9 +28,12 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--epochs", type=int, default=3)
     ap.add_argument("--batched", action="store_true")
+    ap.add_argument("--world", type=int, default=1,
+                    help="build rank 0's share of a W-way sharded system (BCT_SHARDED epochs)")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
-    s = DeviceBlockSystem.parallel_beam(cfg.spec, dtype=cfg.dtype)
+    pr = (0, cfg.spec.nc // a.world)
+    s = DeviceBlockSystem.parallel_beam(cfg.spec, dtype=cfg.dtype, panel_range=pr)
     xt = random_ellipses(cfg.spec.n, cfg.n_ellipses, 0)
     y, _ = add_noise(s.forward(xt), cfg.noise_frac, 1)
     SolverState.initialize(s, y)
@@ -38,7 +41,8 @@ def main():
     rng = np.random.default_rng(5)
     for e in range(a.epochs):
         packed = pack_loops(_loops(sch.epoch_plan(e + 1, rng), s.table, cfg.b), s)
-        submit(s, cfg.mode, packed, N.BCT_COMMIT | N.BCT_METRICS)
+        submit(s, cfg.mode, packed,
+               N.BCT_COMMIT | N.BCT_METRICS | (N.BCT_SHARDED if a.world > 1 else 0))
         res = wait(s, packed.task_j.size)[0]
     nt = packed.task_j.size
     grid = ctypes.c_int32()
@@ -51,12 +55,24 @@ def main():
         t = tl[0]
         st = t[0].min()
         print("batched epoch (us): A(g) %.1f  barA %.1f  B(seg) %.1f  barB %.1f  C(rows) %.1f  D(step) %.1f"
+              "  tail %.1f"
               % (t[1].max() - st, t[2].max() - t[1].max(), t[3].max() - t[2].min(),
-                 t[4].max() - t[3].max(), t[5].max() - t[4].min(), t[6].max() - t[5].max()))
+                 t[4].max() - t[3].max(), t[5].max() - t[4].min(), t[6].max() - t[5].max(),
+                 t[7].max() - t[6].max()))
         for name, d in (("A per block", t[1] - t[0]), ("B per block", t[3] - t[2]),
                         ("C per block", t[5] - t[4])):
             q = np.percentile(d, [0, 10, 50, 90, 100])
             print(f"{name:12s} min {q[0]:6.1f} p10 {q[1]:6.1f} med {q[2]:6.1f} p90 {q[3]:6.1f} max {q[4]:6.1f}")
+        if os.environ.get("DUMP_BLOCKS") and tl.shape[0] > 1:
+            ub, ue, nst = (buf[(1 * 8 + q) * G:(1 * 8 + q + 1) * G] for q in range(3))
+            dB = t[3] - t[2]
+            order = np.argsort(dB)
+            print("B slowest blocks (us, slices, super tiles):",
+                  " ".join(f"{dB[i]:.0f}/{ue[i]-ub[i]}/{nst[i]}" for i in order[-12:]))
+            print("B fastest blocks:", " ".join(f"{dB[i]:.0f}/{ue[i]-ub[i]}/{nst[i]}" for i in order[:12]))
+        if os.environ.get("DUMP_BLOCKS"):
+            for name, d in (("A", t[1] - t[0]), ("B", t[3] - t[2])):
+                print(name, "by block:", " ".join(f"{v:.0f}" for v in d))
         return
     print("task     p1   bar1    p2a  bar2+p2b  bar3     p3   total   (us, to the last block)")
     tot = np.zeros(6)
