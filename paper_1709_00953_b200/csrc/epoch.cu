@@ -802,32 +802,51 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     if (b == 0 && threadIdx.x == 0)
         for (int k = 0; k < n_tasks; ++k) p.counts[p.tasks[k].lp] += 1;
     {
-        const int gtid = b * BLOCK + threadIdx.x, nth = G * BLOCK;
-        // xhat: voxels of every visit (its first task), its tasks summed in order
-        for (int v = gtid; v < hdr.n_vox_total; v += nth) {
-            int k0 = task_of(p.tasks, n_tasks, 3, v);
+        // xhat: voxels of every visit (its first task), its tasks summed in
+        // order; contiguous voxel ranges per CTA, one task lookup per visit
+        const int nv = hdr.n_vox_total;
+        const int vb0 = (int)((int64_t)nv * b / G), vb1 = (int)((int64_t)nv * (b + 1) / G);
+        int v0 = vb0;
+        while (v0 < vb1) {
+            int k0 = task_of(p.tasks, n_tasks, 3, v0);
             while (k0 > 0 && !(p.tasks[k0].flags & TASK_FIRST_OF_VISIT)) --k0;
+            int k1 = k0 + 1;
+            while (k1 < n_tasks && !(p.tasks[k1].flags & TASK_FIRST_OF_VISIT)) ++k1;
             const TaskDev &T0 = p.tasks[k0];
             const PanelDev &P = p.panels[T0.lp];
-            const int d = v - T0.vox_pre;
-            double xs = 0.0;
-            const double xv = p.x[P.x_off + d];
-            for (int k = k0; k < n_tasks; ++k) {
-                const TaskDev &T = p.tasks[k];
-                if (k > k0 && (T.flags & TASK_FIRST_OF_VISIT)) break;
-                const double2 a = gxb[T.gx_off + d];
-                xs += st_s[k] == 0 ? __dadd_rn(xv, __dmul_rn(mu_s[k], a.x)) : xv;
+            const int v1 = min(vb1, T0.vox_pre + P.n_cols);
+            const double *xs_in = p.x + P.x_off;
+            double *xh = p.xhat + P.x_off;
+            for (int v = v0 + (int)threadIdx.x; v < v1; v += BLOCK) {
+                const int d = v - T0.vox_pre;
+                const double xv = xs_in[d];
+                double xs = 0.0;
+                for (int k = k0; k < k1; ++k) {
+                    const double2 a = gxb[p.tasks[k].gx_off + d];
+                    xs += st_s[k] == 0 ? __dadd_rn(xv, __dmul_rn(mu_s[k], a.x)) : xv;
+                }
+                xh[d] += xs;
             }
-            p.xhat[P.x_off + d] += xs;
+            v0 = v1;
         }
-        // z of every task's rows
-        for (int f = gtid; f < hdr.n_rows_total; f += nth) {
-            const int k = task_of(p.tasks, n_tasks, 2, f);
+        // z of every task's rows: contiguous row ranges per CTA (as phase C)
+        const int nr = hdr.n_rows_total;
+        const int rb0 = (int)((int64_t)nr * b / G), rb1 = (int)((int64_t)nr * (b + 1) / G);
+        int f0 = rb0;
+        while (f0 < rb1) {
+            const int k = task_of(p.tasks, n_tasks, 2, f0);
             const TaskDev &T = p.tasks[k];
             const PanelDev &P = p.panels[T.lp];
-            const int lr = f - T.row_pre;
-            const double2 q = taxb[T.tax_off + lr];
-            p.z[P.row_off + lr] = z_value(q.x, q.y, mu_s[k], st_s[k]);
+            const int f1 = min(rb1, T.row_pre + P.n_rows);
+            const double2 *tax = taxb + T.tax_off - T.row_pre;
+            double *zr = p.z + P.row_off - T.row_pre;
+            const double mu = mu_s[k];
+            const int st = st_s[k];
+            for (int f = f0 + (int)threadIdx.x; f < f1; f += BLOCK) {
+                const double2 q = tax[f];
+                zr[f] = z_value(q.x, q.y, mu, st);
+            }
+            f0 = f1;
         }
     }
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 6);
