@@ -38,7 +38,7 @@ namespace {
 
 inline unsigned nb(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
-constexpr int SEG_CAP = 64;   // max entries of one forward segment
+constexpr int SEG_CAP = 64;   // default max entries of one forward segment (PanelDev::seg_cap)
 
 int bits_for(int64_t v)
 {
@@ -240,6 +240,13 @@ __global__ void rkey_k(const int32_t *seg_key, int32_t n_seg, int32_t n_rows, in
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n_seg) return;
     rkey[s] = (seg_key[s] % n_rows) * n_st + seg_key[s] / n_rows;
+}
+
+__global__ void seg_of_entry_k(const int32_t *perm, const int32_t *incl, int64_t nnz,
+                               int32_t *out)
+{
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q < nnz) out[perm[q]] = incl[q] - 1;
 }
 
 __global__ void rpos_k(const int32_t *rseg, const int32_t *seg_slice, const int32_t *seg_lane,
@@ -634,7 +641,7 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
                     const int32_t *l2g, const int32_t *rbp, const std::vector<int32_t> &c2d_h,
                     const std::vector<int32_t> &st_ptr_h, const std::vector<int32_t> &corder_h,
                     int tile_cols, PanelDev &P, std::vector<void *> &keep, std::string &err,
-                    cudaStream_t s)
+                    cudaStream_t s, int32_t *seg_of_entry)
 {
     std::vector<void *> tmp;
     Alloc K{&keep, &err}, T{&tmp, &err};
@@ -671,7 +678,8 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     if (nnz > 0) {
         fwd_key_k<<<nb(nnz, 256), 256, 0, s>>>(cols_c, rowid, c2d, d2st, n_rows, nnz, key);
         LCK(sort_pairs<int32_t>(key, skey, iota, perm, nnz, bits_for((int64_t)n_st * n_rows), tmp, s));
-        seg_flag_k<<<nb(nnz, 256), 256, 0, s>>>(skey, nnz, SEG_CAP, flag);
+        seg_flag_k<<<nb(nnz, 256), 256, 0, s>>>(skey, nnz, P.seg_cap > 0 ? P.seg_cap : SEG_CAP,
+                                                 flag);
         LCK(scan_i32(flag, incl, nnz, true, tmp, s));
         n_seg = read1(incl + nnz - 1, s);
     }
@@ -686,6 +694,8 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     int32_t n_slices = 0;
     if (n_seg > 0) {
         seg_first_k<<<nb(nnz, 256), 256, 0, s>>>(flag, incl, skey, nnz, seg_first, seg_key);
+        if (seg_of_entry)   // CSR entry -> its forward segment (replay records, builder.cu)
+            seg_of_entry_k<<<nb(nnz, 256), 256, 0, s>>>(perm, incl, nnz, seg_of_entry);
         seg_len_k<<<nb(n_seg, 256), 256, 0, s>>>(seg_first, n_seg, nnz, seg_len, nvec);
         sell_key_k<<<nb(n_seg, 256), 256, 0, s>>>(seg_key, nvec, n_seg, n_rows, rbp, m, skey0);
         iota_k<<<nb(n_seg, 256), 256, 0, s>>>(sid0, n_seg);
