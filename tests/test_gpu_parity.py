@@ -386,3 +386,21 @@ def test_full_size_fixed_point(cfg3_system):
     y = cfg3_system.forward(xt)
     x, tr = run_gcsgd(cfg3_system, y, _cfg_params(cfg, 1), x0=xt)
     assert np.array_equal(x, xt)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_matrix_free_phase_b_matches_reference(cfg1_runs, dtype, monkeypatch):
+    """BCT_REPLAY=1: phase B regenerates the forward values by re-walking the
+    rays (bit-identical to the stored ones); same tolerances as the stored
+    path (x at 1e-10 in FP64, the residual curve at 1e-4 in FP32)."""
+    monkeypatch.setenv("BCT_REPLAY", "1")
+    sysm = DeviceBlockSystem.parallel_beam(CONFIGS[1].spec, dtype=dtype)
+    g = cfg1_runs
+    name = "par_full"
+    x, tr = run_gcsgd(sysm, g["y"], SolverParams(**VARIANTS[name]), x_true=g["x_true"])
+    if dtype == "f64":
+        assert rel(x, g[f"{name}_x"]) <= 1e-10
+    ynorm = np.linalg.norm(g["y"])
+    r_dev = ynorm / 10.0 ** (np.array([r.obs_gap_db for r in tr.rows]) / 20.0)
+    r_ref = ynorm / 10.0 ** (g[f"{name}_gap"] / 20.0)
+    assert np.max(np.abs(r_dev - r_ref) / r_ref) <= (1e-9 if dtype == "f64" else 1e-4)
