@@ -78,6 +78,8 @@ struct bct_ctx {
     int device = 0, dtype = 0, m = 0, n_panels = 0, pb = 0, pe = 0, np = 0;
     int64_t n_meas = 0, n_vox = 0, nnz = 0, z_len = 0, x_len = 0;
     int64_t max_rows = 0, max_cols = 0, max_seg = 0;
+    int32_t *d_gvox = nullptr;     // [x_len] global voxel id of each device position
+    double *d_xstage = nullptr;    // [n_vox] global-order staging of image transfers
     size_t smem = 0;
     int32_t band_cap = 0, band_dbuf = 1;
     cudaStream_t stream = nullptr;
@@ -363,6 +365,18 @@ int finalize(bct_ctx *c)
     if (ro >= (1ll << 31)) return fail(c, BCT_EINVAL, "z store exceeds 2^31 rows");
     c->z_len = ro;
     c->x_len = xo;
+    {   // device position -> global voxel id (state transfers permute on the device)
+        std::vector<int32_t> gv(std::max<int64_t>(xo, 1));
+        for (int lp = 0; lp < c->np; ++lp) {
+            const PanelDev &P = c->h_panels[lp];
+            const int64_t cb = c->col_ptr[c->pb + lp];
+            for (int64_t d = 0; d < P.n_cols; ++d)
+                gv[P.x_off + d] = (int32_t)c->col_vox[cb + c->h_d2c[lp][d]];
+        }
+        DALLOC(c->d_gvox, std::max<int64_t>(xo, 1));
+        DALLOC(c->d_xstage, std::max<int64_t>(c->n_vox, 1));
+        CK(cudaMemcpy(c->d_gvox, gv.data(), 4 * std::max<int64_t>(xo, 1), cudaMemcpyHostToDevice));
+    }
     // row blocks
     std::vector<int32_t> rbp32(c->rb_ptr.begin(), c->rb_ptr.end());
     std::vector<int32_t> rows32(c->rb_rows.begin(), c->rb_rows.end());
@@ -870,8 +884,32 @@ int bct_get_stream(bct_ctx *c, void **s)
 
 // ---- state I/O (global order <-> panel-major device order) -----------------
 
+__global__ void vox_gather_k(const double *stage, const int32_t *gvox, int64_t n, double *dst)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = stage[gvox[i]];
+}
+
+__global__ void vox_scatter_k(const double *src, const int32_t *gvox, int64_t n, double *stage)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) stage[gvox[i]] = src[i];
+}
+
+// Image transfers in global voxel order; the permutation runs on the device.
+// A context owning every panel moves the whole image in one copy; a shard
+// moves only its own voxels on the host side (global order untouched elsewhere).
 static int xvec_to_dev(bct_ctx *c, const double *xg, double *dst)
 {
+    const unsigned nb = (unsigned)((c->x_len + 255) / 256);
+    if (c->np == c->n_panels) {
+        CK(cudaMemcpyAsync(c->d_xstage, xg, 8 * c->n_vox, cudaMemcpyHostToDevice, c->stream));
+        if (c->x_len > 0)
+            vox_gather_k<<<nb, 256, 0, c->stream>>>(c->d_xstage, c->d_gvox, c->x_len, dst);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(c->stream));
+        return 0;
+    }
     std::vector<double> buf(std::max<int64_t>(c->x_len, 1));
     for (int lp = 0; lp < c->np; ++lp) {
         const PanelDev &P = c->h_panels[lp];
@@ -886,6 +924,15 @@ static int xvec_to_dev(bct_ctx *c, const double *xg, double *dst)
 
 static int xvec_from_dev(bct_ctx *c, const double *src, double *xg)
 {
+    if (c->np == c->n_panels && c->x_len == c->n_vox) {
+        const unsigned nb = (unsigned)((c->x_len + 255) / 256);
+        if (c->x_len > 0)
+            vox_scatter_k<<<nb, 256, 0, c->stream>>>(src, c->d_gvox, c->x_len, c->d_xstage);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(xg, c->d_xstage, 8 * c->n_vox, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return 0;
+    }
     std::vector<double> buf(std::max<int64_t>(c->x_len, 1));
     CK(cudaMemcpyAsync(buf.data(), src, 8 * c->x_len, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
