@@ -429,7 +429,7 @@ int finalize(bct_ctx *c)
     DALLOC(c->counts, c->np);
     DALLOC(c->gx, 4 * c->max_cols);
     DALLOC(c->t_ax, 2 * c->max_rows);
-    DALLOC(c->seg_part, 2 * c->max_seg + 2);
+    DALLOC(c->seg_part, 2 * 4 * c->max_seg + 2);   // TASK_SPLIT (epoch.cu) partials per lane
     // two band buffers when they fit, else one (staging then serializes)
     // phase-1 bands (double-buffered when they fit) + the tile reduction area
     c->band_dbuf = 2 * (size_t)c->band_cap * 8 + bct::PHASE1_RED_BYTES <= SMEM_BUDGET ? 1 : 0;

@@ -48,6 +48,7 @@ namespace {
 #define BCT_NO_REPLAY_K 0   // 1: phase B streams the stored values even when replay records exist
 #endif
 constexpr int P1U = BCT_P1_UNROLL;
+constexpr int TASK_SPLIT = 4;       // per-task phase 2a: parts per SELL slice
 constexpr int P2U = BCT_P2_UNROLL;
 constexpr int BLOCK = 1024;         // one CTA per SM
 constexpr int WARPS = BLOCK / 32;
@@ -1105,13 +1106,18 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                     gs[swz_idx(q, P.swz_shift)] = GS{(decltype(GS::x))a.x, (decltype(GS::x))a.y};
                 }
                 __syncthreads();
-                for (int f = fu + warp; f < ge; f += WARPS) {
+                // work unit = (slice, part): part q of a slice takes its
+                // vectors kv = q (mod TASK_SPLIT), so a single task (a few
+                // slices per CTA) still keeps every warp streaming; the
+                // TASK_SPLIT partials of a lane are summed in phase 2b
+                for (int u = fu * TASK_SPLIT + warp; u < ge * TASK_SPLIT; u += WARPS) {
+                    const int f = u / TASK_SPLIT, part = u - f * TASK_SPLIT;
                     const int sl = R.full ? f : task_slice(R, P, m, f, st);
                     const int base = __ldg(P.slice_start + sl);
                     const int nvec = (__ldg(P.slice_start + sl + 1) - base) >> 7;
                     double t = 0.0, ax = 0.0;
 #pragma unroll P2U
-                    for (int kv = 0; kv < nvec; ++kv) {
+                    for (int kv = part; kv < nvec; kv += TASK_SPLIT) {
                         const int i = base + ((kv * 32 + lane) << 2);
                         int cc[4];
                         double v[4];
@@ -1133,7 +1139,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                             ax = fma(v[q], (double)a.y, ax);
                         }
                     }
-                    spart[(int64_t)sl * 32 + lane] = make_double2(t, ax);   // SELL order
+                    spart[((int64_t)sl * TASK_SPLIT + part) * 32 + lane] = make_double2(t, ax);
                 }
                 __syncthreads();
                 fu = ge;
@@ -1153,9 +1159,17 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 double t = 0.0, ax = 0.0;
                 const int q1 = __ldg(P.rseg_ptr + lr + 1);
                 for (int q = __ldg(P.rseg_ptr + lr); q < q1; ++q) {
-                    const double2 a = spart[__ldg(P.rpos + q)];   // SELL-order partials
-                    t += a.x;
-                    ax += a.y;
+                    const int rp = __ldg(P.rpos + q);   // SELL position: slice*32 + lane
+                    const double2 *pp = spart + ((int64_t)(rp >> 5) * TASK_SPLIT) * 32 + (rp & 31);
+                    double st_ = 0.0, sa_ = 0.0;
+#pragma unroll
+                    for (int part = 0; part < TASK_SPLIT; ++part) {
+                        const double2 a = pp[part * 32];
+                        st_ += a.x;
+                        sa_ += a.y;
+                    }
+                    t += st_;
+                    ax += sa_;
                 }
                 tax[lr] = make_double2(t, ax);
                 wsum = fma(t, t, wsum);
