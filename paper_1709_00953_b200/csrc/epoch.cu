@@ -1205,7 +1205,9 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 xh[d] += xn;
             }
         }
-        {
+        const bool last_of_visit = (T.flags & TASK_LAST_OF_VISIT) != 0;
+        const bool refresh = serial && last_of_visit;
+        if (!refresh) {   // (the refresh below stores this task's z itself)
             const double2 *tax = reinterpret_cast<const double2 *>(p.t_ax);
             double *zj = p.z + P.row_off;
             for (int f = gtid; f < n_task_rows; f += nthreads) {
@@ -1214,31 +1216,51 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 zj[lr] = z_value(q.x, q.y, mu, status);
             }
         }
-        const bool last_of_visit = (T.flags & TASK_LAST_OF_VISIT) != 0;
-        if (serial && last_of_visit) {
-            // refresh every row of the visit's drawn blocks (executor.py:215-223)
+        if (refresh) {
+            // refresh every row of the visit's drawn blocks (executor.py:215-223),
+            // one flat pass over their rows; the current task's z is computed
+            // here and stored on the way (every one of its rows is refreshed)
+            __shared__ int s_vb[BCT_MAX_M], s_vpre[BCT_MAX_M + 1];
+            __shared__ int s_nvb;
+            if (threadIdx.x == 0) {
+                int nv = 0, acc = 0;
+                for (int i = 0; i < m; ++i) {
+                    if (!mask_has(T.visit_mask, i)) continue;
+                    s_vb[nv] = i;
+                    s_vpre[nv] = acc;
+                    acc += p.rb_ptr[i + 1] - p.rb_ptr[i];
+                    ++nv;
+                }
+                s_vpre[nv] = acc;
+                s_nvb = nv;
+            }
+            __syncthreads();
+            const int nvb = s_nvb, tot = s_vpre[nvb];
             const double2 *tax = reinterpret_cast<const double2 *>(p.t_ax);
             const int64_t zlo = P.row_off, zhi = P.row_off + P.n_rows;
-            for (int i = 0; i < m; ++i) {
-                if (!mask_has(T.visit_mask, i)) continue;
-                const bool cur = mask_has(T.mask, i);
-                int b0 = p.rb_ptr[i], b1 = p.rb_ptr[i + 1];
-                for (int q = b0 + gtid; q < b1; q += nthreads) {
-                    int g = p.rb_rows[q];
-                    double acc = 0.0;
-                    for (int e = p.inv_ptr[g]; e < p.inv_ptr[g + 1]; ++e) {
-                        int off = p.inv_z[e];
-                        double v;
-                        if (cur && off >= zlo && off < zhi) {
-                            double2 qq = tax[off - zlo];
-                            v = z_value(qq.x, qq.y, mu, status);
-                        } else {
-                            v = p.z[off];
-                        }
-                        acc += v;
-                    }
-                    p.r[g] = p.y[g] - acc;
+            for (int f = gtid; f < tot; f += nthreads) {
+                int lo = 0, hi = nvb - 1;   // last drawn block with prefix <= f
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_vpre[mid] <= f) lo = mid; else hi = mid - 1;
                 }
+                const int i = s_vb[lo];
+                const bool cur = mask_has(T.mask, i);
+                const int g = p.rb_rows[p.rb_ptr[i] + (f - s_vpre[lo])];
+                double acc = 0.0;
+                for (int e = p.inv_ptr[g]; e < p.inv_ptr[g + 1]; ++e) {
+                    const int off = p.inv_z[e];
+                    double v;
+                    if (cur && off >= zlo && off < zhi) {
+                        const double2 qq = tax[off - zlo];
+                        v = z_value(qq.x, qq.y, mu, status);
+                        p.z[off] = v;
+                    } else {
+                        v = p.z[off];
+                    }
+                    acc += v;
+                }
+                p.r[g] = p.y[g] - acc;
             }
             if (k + 1 < n_tasks) grid_sync(p.bar);
         }
