@@ -44,6 +44,9 @@ namespace {
 #ifndef BCT_P2_UNROLL
 #define BCT_P2_UNROLL 4
 #endif
+#ifndef BCT_FENCED_BARRIER
+#define BCT_FENCED_BARRIER 0
+#endif
 #ifndef BCT_NO_REPLAY_K
 #define BCT_NO_REPLAY_K 0   // 1: phase B streams the stored values even when replay records exist
 #endif
@@ -78,12 +81,24 @@ __device__ __forceinline__ void grid_sync(unsigned int *bar)
     if (threadIdx.x == 0) {
         unsigned int nb = gridDim.x;
         unsigned int inc = (blockIdx.x == 0) ? (0x80000000u - (nb - 1)) : 1u;
+#if BCT_FENCED_BARRIER
         __threadfence();
         unsigned int old = atomicAdd(bar, inc);
         volatile unsigned int *vb = bar;
         while (((old ^ *vb) & 0x80000000u) == 0) {
         }
         __threadfence();
+#else
+        // release-add / acquire-poll at gpu scope: the CTA's writes (ordered
+        // before this thread by __syncthreads, release is cumulative) are
+        // visible to every CTA that observes the flip, without full fences
+        unsigned int old, cur;
+        asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(bar), "r"(inc)
+                     : "memory");
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];\n" : "=r"(cur) : "l"(bar) : "memory");
+        } while (((old ^ cur) & 0x80000000u) == 0);
+#endif
     }
     __syncthreads();
 }
