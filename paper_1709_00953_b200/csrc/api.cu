@@ -54,7 +54,17 @@ cudaError_t sharded_out(const double *, int, const double *, EpochOut *, cudaStr
 namespace {
 
 constexpr int RING = 4;
-constexpr int ST_VOXELS = 4096;     // voxels per super tile (64 KB of (g, x) pairs)
+// voxels per super tile: its (g, x) pairs are staged in shared memory for
+// phase 2 -- 16384 x 8 B (float2, 128 KB) in FP32 mode: fewer (row, super
+// tile) segments per row for the batched epochs; 4096 x 16 B in FP64 mode,
+// whose serial per-task epochs would stage a large tile per CTA for little work
+// (the matrix-free phase B needs segments that are whole walk runs: <= 255
+// entries, so it keeps 4096-voxel super tiles)
+inline int st_voxels(int dtype)
+{
+    if (getenv("BCT_ST_SMALL") || getenv("BCT_REPLAY")) return 4096;
+    return dtype == 0 ? 4096 : 16384;   // FP64 configs run per-task (small) epochs
+}
 constexpr size_t SMEM_BUDGET = 210 * 1024;  // dynamic shared memory per CTA (one CTA per SM;
                                             // 227 KB less the kernel's static arrays)
 
@@ -190,8 +200,9 @@ struct Placement {
     int32_t st_w = 0;        // strip placement: super tile row length (0: generic)
 };
 
-Placement place_voxels(int64_t n_cols, int64_t h, int64_t w, int th, int tw)
+Placement place_voxels(int64_t n_cols, int64_t h, int64_t w, int th, int tw, int dtype)
 {
+    const int ST_VOXELS = st_voxels(dtype);
     Placement pl;
     pl.c2d.resize(n_cols);
     pl.d2c.resize(n_cols);
@@ -273,7 +284,7 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     if (replay) DALLOC(seg_of, nnz);
     for (size_t si = 0; si < shapes.size(); ++si) {
         const int th = shapes[si].th, tw = shapes[si].tw;
-        pl = place_voxels(n_cols, h, w, th, tw);
+        pl = place_voxels(n_cols, h, w, th, tw, c->dtype);
         std::string err;
         std::vector<void *> kept;
         PanelDev Q = P;
@@ -348,7 +359,8 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     c->max_cols = std::max<int64_t>(c->max_cols, n_cols);
     c->max_seg = std::max<int64_t>(c->max_seg, (int64_t)P.n_slices * 32);   // partial slots
     c->band_cap = std::max(c->band_cap, (P.band_max + 1) & ~1);
-    c->smem = std::max<size_t>(c->smem, (size_t)((P.st_max + 15) & ~15) * 16);   // swizzled
+    // staged super tile: (g, x) as float2 in FP32 mode, double2 in FP64 mode (swizzled)
+    c->smem = std::max<size_t>(c->smem, (size_t)((P.st_max + 15) & ~15) * (c->dtype == 0 ? 16 : 8));
     return 0;
 }
 
