@@ -1313,7 +1313,7 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
         if ((r = grow(&c->gx_batch, &c->gx_batch_n, 2 * gxo))) return r;
         if ((r = grow(&c->seg_batch, &c->seg_batch_n, 2 * sgo))) return r;
         if ((r = grow(&c->tax_batch, &c->tax_batch_n, 2 * txo))) return r;
-        if ((r = grow(&c->part_task, &c->part_task_n, 33 * nt * (int64_t)c->grid))) return r;
+        if ((r = grow(&c->part_task, &c->part_task_n, 33 * nt * (int64_t)c->grid + nt))) return r;
     }
     // the staging buffers of the previous epoch must have been consumed
     CK(cudaEventSynchronize(c->staged));

@@ -660,6 +660,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     double2 *taxb = reinterpret_cast<double2 *>(p.tax_batch);
     double *pgg = p.part_task;                       // [k][G][WARPS]
     double *pden = p.part_task + (int64_t)n_tasks * G * WARPS;   // [k][G]
+    double *ggs = p.part_task + (int64_t)n_tasks * G * (WARPS + 1);   // [k] reduced gg
 
     // ---- phase A: g = A^T r for every task, tiles round-robin over CTAs ----
     // One CTA barrier per tile: the band of tile it+1 streams in (bulk
@@ -864,6 +865,14 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
 
     // ---- phase C: rows of every task (contiguous ranges), denom partials ----
     for (int k = threadIdx.x; k < n_tasks; k += BLOCK) pden[(int64_t)k * G + b] = 0.0;
+    // gg of task k from its G*WARPS phase-A partials, one CTA per task (fixed
+    // order), so phase D reads one value instead of every CTA summing them all
+    for (int k = b; k < n_tasks; k += G) {
+        double v = 0.0;
+        for (int q = threadIdx.x; q < G * WARPS; q += BLOCK) v += pgg[(int64_t)k * G * WARPS + q];
+        v = block_sum_all(v, sh);
+        if (threadIdx.x == 0) ggs[k] = v;
+    }
     __syncthreads();
     {
         const int nr = hdr.n_rows_total;
@@ -902,9 +911,8 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     int *st_s = reinterpret_cast<int *>(rs + n_tasks);   // [n_tasks]
     for (int k = warp; k < n_tasks; k += WARPS) {
         double gg = 0.0, den = 0.0;
-        for (int q = lane; q < G * WARPS; q += 32) gg += pgg[(int64_t)k * G * WARPS + q];
         for (int q = lane; q < G; q += 32) den += pden[(int64_t)k * G + q];
-        gg = warp_sum(gg);
+        gg = ggs[k];
         den = warp_sum(den);
         if (lane != 0) continue;
         double mu = 0.0;
