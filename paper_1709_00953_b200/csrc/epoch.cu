@@ -886,17 +886,44 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const double2 *spart = segb + T.seg_off;
             double2 *tax = taxb + T.tax_off;
             double wsum = 0.0;
-            for (int f = f0 + (int)threadIdx.x; f < f1; f += BLOCK) {
-                const int lr = f - T.row_pre;
-                double t = 0.0, ax = 0.0;
-                const int q1 = __ldg(P.rseg_ptr + lr + 1);
-                for (int q = __ldg(P.rseg_ptr + lr); q < q1; ++q) {
-                    const double2 a = spart[__ldg(P.rpos + q)];   // SELL-order partials
-                    t += a.x;
-                    ax += a.y;
+            // CR rows per thread at a time, their (pointer, position, partial)
+            // loads issued level by level: CR-fold memory parallelism for a
+            // chain of three dependent loads per row
+            constexpr int CR = 4;
+            for (int fb = f0 + (int)threadIdx.x; fb < f1; fb += CR * BLOCK) {
+                int q0[CR], q1[CR];
+                double t[CR], ax[CR];
+                int nmax = 0;
+#pragma unroll
+                for (int j = 0; j < CR; ++j) {
+                    const int f = fb + j * BLOCK;
+                    const int lr = f - T.row_pre;
+                    q0[j] = f < f1 ? __ldg(P.rseg_ptr + lr) : 0;
+                    q1[j] = f < f1 ? __ldg(P.rseg_ptr + lr + 1) : 0;
+                    t[j] = 0.0;
+                    ax[j] = 0.0;
+                    nmax = max(nmax, q1[j] - q0[j]);
                 }
-                tax[lr] = make_double2(t, ax);
-                wsum = fma(t, t, wsum);
+                for (int s = 0; s < nmax; ++s) {
+                    int pos[CR];
+#pragma unroll
+                    for (int j = 0; j < CR; ++j) pos[j] = q0[j] + s < q1[j] ? __ldg(P.rpos + q0[j] + s) : -1;
+#pragma unroll
+                    for (int j = 0; j < CR; ++j)
+                        if (pos[j] >= 0) {
+                            const double2 a = __ldg(spart + pos[j]);   // SELL-order partials
+                            t[j] += a.x;
+                            ax[j] += a.y;
+                        }
+                }
+#pragma unroll
+                for (int j = 0; j < CR; ++j) {
+                    const int f = fb + j * BLOCK;
+                    if (f < f1) {
+                        tax[f - T.row_pre] = make_double2(t[j], ax[j]);
+                        wsum = fma(t[j], t[j], wsum);
+                    }
+                }
             }
             const double bs = block_sum_all(wsum, sh);
             if (threadIdx.x == 0) pden[(int64_t)k * G + b] += bs;
@@ -971,8 +998,11 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             double *zr = p.z + P.row_off - T.row_pre;
             const double mu = mu_s[k];
             const int st = st_s[k];
+            // read-only loads (no aliasing with the z stores): the loop keeps
+            // several rows in flight per thread
+#pragma unroll 4
             for (int f = f0 + (int)threadIdx.x; f < f1; f += BLOCK) {
-                const double2 q = tax[f];
+                const double2 q = __ldg(tax + f);
                 zr[f] = z_value(q.x, q.y, mu, st);
             }
             f0 = f1;
