@@ -911,7 +911,8 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
 #pragma unroll
                     for (int j = 0; j < CR; ++j)
                         if (pos[j] >= 0) {
-                            const double2 a = __ldg(spart + pos[j]);   // SELL-order partials
+                            // written in phase B of this launch: L2-coherent load
+                            const double2 a = __ldcg(spart + pos[j]);   // SELL-order partials
                             t[j] += a.x;
                             ax[j] += a.y;
                         }
@@ -998,12 +999,16 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             double *zr = p.z + P.row_off - T.row_pre;
             const double mu = mu_s[k];
             const int st = st_s[k];
-            // read-only loads (no aliasing with the z stores): the loop keeps
-            // several rows in flight per thread
-#pragma unroll 4
-            for (int f = f0 + (int)threadIdx.x; f < f1; f += BLOCK) {
-                const double2 q = __ldg(tax + f);
-                zr[f] = z_value(q.x, q.y, mu, st);
+            // four rows in flight per thread: loads (L2-coherent: tax was
+            // written in phase C of this launch) before the stores
+            for (int fb = f0 + (int)threadIdx.x; fb < f1; fb += 4 * BLOCK) {
+                double2 q[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    q[j] = fb + j * BLOCK < f1 ? __ldcg(tax + fb + j * BLOCK) : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (fb + j * BLOCK < f1) zr[fb + j * BLOCK] = z_value(q[j].x, q[j].y, mu, st);
             }
             f0 = f1;
         }
@@ -1328,7 +1333,21 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     if (!serial || do_metrics || sharded) {
         for (int g = gtid; g < p.n_meas; g += nthreads) {
             double acc = 0.0;
-            for (int e = p.inv_ptr[g]; e < p.inv_ptr[g + 1]; ++e) acc += p.z[p.inv_z[e]];
+            const int e1 = __ldg(p.inv_ptr + g + 1);
+            // ascending j (the reference's fold); z was written earlier in this
+            // launch: L2-coherent loads, four in flight
+            int e = __ldg(p.inv_ptr + g);
+            for (; e + 4 <= e1; e += 4) {
+                int o[4];
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) o[u] = __ldg(p.inv_z + e + u);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldcg(p.z + o[u]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc += v[u];
+            }
+            for (; e < e1; ++e) acc += __ldcg(p.z + __ldg(p.inv_z + e));
             if (sharded) {
                 p.exchange[g] = acc;
             } else {
