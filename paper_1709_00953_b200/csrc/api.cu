@@ -65,7 +65,7 @@ inline int st_voxels(int dtype)
     if (getenv("BCT_ST_SMALL") || getenv("BCT_REPLAY")) return 4096;
     return dtype == 0 ? 4096 : 16384;   // FP64 configs run per-task (small) epochs
 }
-constexpr size_t SMEM_BUDGET = 210 * 1024;  // dynamic shared memory per CTA (one CTA per SM;
+constexpr size_t SMEM_BUDGET = 218 * 1024;  // dynamic shared memory per CTA (one CTA per SM;
                                             // 227 KB less the kernel's static arrays)
 
 struct Slot {
@@ -274,7 +274,7 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
         int a = 0, b2 = 0;
         if (sscanf(e, "%dx%d", &a, &b2) == 2 && a > 0 && b2 > 0 && (a * b2) % 32 == 0 &&
             a * b2 <= 256)
-            shapes = {{a, b2, 1}, {4, 8, 1}};
+            shapes = {{a, b2, 2}, {a, b2, 1}, {4, 8, 1}};
     }
     Placement pl;
     // matrix-free phase B is opt-in (BCT_REPLAY=1): regenerating the values
@@ -1270,7 +1270,7 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
     int r = ensure_task_cap(c, std::max<int64_t>(nt, 1));
     if (r) return r;
     // epoch-batched path: parallel epoch whose tasks are all full panels
-    bool batched = mode == BCT_PARALLEL && nt > 0 && nt <= 1024 && !getenv("BCT_NO_BATCH");
+    bool batched = mode == BCT_PARALLEL && nt > 0 && nt <= bct::MAX_BATCH_TASKS && !getenv("BCT_NO_BATCH");
     uint64_t full[BCT_MASKW] = {0, 0, 0, 0};
     for (int i = 0; i < c->m; ++i) set_mask(full, i);
     for (int64_t k = 0; batched && k < nt; ++k)

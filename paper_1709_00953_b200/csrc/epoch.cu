@@ -1044,7 +1044,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     GS *gs = reinterpret_cast<GS *>(dyn_smem);
 
     __shared__ RingSlot ring[RING];
-    __shared__ int s_tpre[1025], s_lp[1024];
+    __shared__ int s_tpre[bct::MAX_BATCH_TASKS + 1], s_lp[bct::MAX_BATCH_TASKS];
     if (hdr.batched) batched_epoch<V>(p, hdr, rs, sh, ring, s_tpre, s_lp);
     for (int k = 0; k < (hdr.batched ? 0 : n_tasks); ++k) {
         __syncthreads();  // sT/sP/R of the previous task may still be in use
@@ -1430,7 +1430,7 @@ int epoch_grid_size(int dtype, int device, size_t smem, int *block)
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const void *fn = dtype == 0 ? (const void *)epoch_kernel<double> : (const void *)epoch_kernel<float>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 16384);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 218 * 1024);
     if (dtype == 0)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<double>, BLOCK, smem);
     else

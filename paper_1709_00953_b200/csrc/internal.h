@@ -167,6 +167,9 @@ __host__ __device__ __forceinline__ int swz_idx(int q, int shift)
 
 namespace bct {
 
+// epoch-batched path: at most this many tasks (task tables live in shared memory)
+constexpr int MAX_BATCH_TASKS = 256;
+
 // device sampler (sampler.cu)
 struct SampleVisit {
     int32_t j, draws;
