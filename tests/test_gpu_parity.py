@@ -404,3 +404,72 @@ def test_matrix_free_phase_b_matches_reference(cfg1_runs, dtype, monkeypatch):
     r_dev = ynorm / 10.0 ** (np.array([r.obs_gap_db for r in tr.rows]) / 20.0)
     r_ref = ynorm / 10.0 ** (g[f"{name}_gap"] / 20.0)
     assert np.max(np.abs(r_dev - r_ref) / r_ref) <= (1e-9 if dtype == "f64" else 1e-4)
+
+
+# ---------------------------------------------------------------------------
+# edge cases: empty / excluded column blocks, the largest mask (256 row
+# blocks), zero epochs
+# ---------------------------------------------------------------------------
+
+def _device_from_oracle(ora, dtype="f64"):
+    from paper_1709_00953_b200.system import PanelArrays
+    panels = [PanelArrays(ora.data[j], ora.cols[j], ora.indptr[j], ora.rbp[j], ora.l2g[j])
+              for j in range(ora.n_col_blocks)]
+    return DeviceBlockSystem.from_panels(panels, ora.row_meas, ora.vidx, ora.table.values,
+                                         ora.n_measurements, ora.n_voxels, dtype=dtype)
+
+
+@pytest.mark.parametrize("mode,gs,alpha", [("parallel", 2, 1.0), ("serial_faithful", 1, 0.5)])
+def test_empty_panel_is_excluded_and_untouched(mode, gs, alpha):
+    """A column block with no entries has a zero table column: the scheduler
+    never visits it (sampling.py active_cols), its voxels keep x0, and the rest
+    matches the oracle (empty panels also exercise the zero-size layout)."""
+    from oracle.oracle import OracleTable, oracle_run_gcsgd
+    from paper_1709_00953_b200.geometry import add_noise, random_ellipses
+    ora = __import__("oracle.oracle", fromlist=["OracleSystem"]).OracleSystem.parallel_beam(
+        16, 20, 24, 4, 4)
+    j0 = 2
+    ora.data[j0] = np.empty(0)
+    ora.cols[j0] = np.empty(0, np.int32)
+    ora.indptr[j0] = np.zeros(1, np.int64)
+    ora.rbp[j0] = np.zeros(5, np.int64)
+    ora.l2g[j0] = np.empty(0, np.int64)
+    vals = ora.table.values.copy()
+    vals[:, j0] = 0.0
+    ora.table = OracleTable(vals, vals.sum(axis=0))
+    sysm = _device_from_oracle(ora)
+    xt = random_ellipses(16, 3, 0)
+    y, _ = add_noise(ora.forward(xt), 0.01, 1)
+    rec = {}
+    x, _ = run_gcsgd(sysm, y, SolverParams(epochs=6, b=0.4, group_size=gs, seed=9,
+                                          execution_mode=mode,
+                                          sampling=SamplingConfig(alpha=alpha)),
+                     x_true=xt, plan_record=rec)
+    assert all(j != j0 for plan in rec.values() for j, _ in plan)
+    assert np.all(x[ora.vidx[j0]] == 0.0)
+    x_ref, _ = oracle_run_gcsgd(ora, y, 6, 0.4, alpha=alpha, group_size=gs, mode=mode, seed=9)
+    assert rel(x, x_ref) <= 1e-10
+    assert sysm.audit_drift() <= 1e-12
+
+
+@pytest.mark.parametrize("mode,gs,alpha", [("serial_faithful", 5, 0.1), ("parallel", 256, 1.0),
+                                           ("parallel", 100, 0.7)])
+def test_256_row_blocks(mode, gs, alpha):
+    """m = BCT_MAX_M = 256 (every mask word in use): device vs oracle."""
+    from oracle.oracle import OracleSystem, oracle_run_gcsgd
+    from paper_1709_00953_b200.geometry import add_noise, random_ellipses
+    spec = ParallelBeamSpec(24, 256, 34, 256, 3)
+    ora = OracleSystem.parallel_beam(24, 256, 34, 256, 3)
+    sysm = DeviceBlockSystem.parallel_beam(spec, dtype="f64")
+    xt = random_ellipses(24, 4, 2)
+    y, _ = add_noise(ora.forward(xt), 0.01, 3)
+    x, _ = run_gcsgd(sysm, y, SolverParams(epochs=3, b=0.3, group_size=gs, seed=5,
+                                          execution_mode=mode,
+                                          sampling=SamplingConfig(alpha=alpha)), x_true=xt)
+    x_ref, _ = oracle_run_gcsgd(ora, y, 3, 0.3, alpha=alpha, group_size=gs, mode=mode, seed=5)
+    assert rel(x, x_ref) <= 1e-10
+
+
+def test_zero_epochs_returns_start(cfg1_system, cfg1_runs):
+    x, tr = run_gcsgd(cfg1_system, cfg1_runs["y"], SolverParams(epochs=0, b=0.5, seed=1))
+    assert np.all(x == 0.0) and len(tr.rows) == 0
