@@ -11,7 +11,8 @@ from .metrics import ConvergenceTrace, TraceRow, observation_gap_db, snr_db
 from .sampling import (BlockScheduler, ProbabilityTable, SamplingConfig, ScriptedScheduler,
                        dump_schedule, mixed_weights, parse_schedule, select_column_blocks,
                        select_row_blocks)
-from .solvers import SolverParams, SolverState, audit_state, run_csgd, run_gcsgd
+from .solvers import (SolverParams, SolverState, audit_state, basic_iteration, run_csgd,
+                      run_gcsgd)
 from .system import DeviceBlockSystem, PanelArrays
 
 __version__ = "0.1.0"
@@ -25,6 +26,6 @@ __all__ = [
     "BlockScheduler", "ProbabilityTable", "SamplingConfig", "ScriptedScheduler",
     "dump_schedule", "mixed_weights", "parse_schedule", "select_column_blocks",
     "select_row_blocks",
-    "SolverParams", "SolverState", "audit_state", "run_csgd", "run_gcsgd",
+    "SolverParams", "SolverState", "audit_state", "basic_iteration", "run_csgd", "run_gcsgd",
     "DeviceBlockSystem", "PanelArrays",
 ]

@@ -112,6 +112,41 @@ class SolverState:
         return self.system.get_counts()
 
 
+def basic_iteration(system, i, j, r_i, x_j, beta):
+    """One relaxed steepest-descent step on block pair (I_i, J_j), on the device
+    (the reference's single-step reference, solvers.py:123-147, here on a
+    block of a DeviceBlockSystem instead of a SubmatrixHandle).
+
+    Returns (x_j_new, z_i, mu): z_i = A_I^J x_j_new over the full row block
+    (rows the panel does not hit are 0).  A zero gradient or a gradient in the
+    block null space gives mu = 0 and an unchanged image.  Uses (and
+    overwrites) the system's device state.
+    """
+    check_positive("beta", beta)
+    rows = system.measurement_rows([i])
+    x_j = as_vector("x_j", x_j, length=int(system.col_sizes[j]))
+    r_i = as_vector("r_i", r_i, length=rows.size)
+    x = np.zeros(system.n_voxels)
+    x[system.voxel_indices(j)] = x_j
+    r = np.zeros(system.n_measurements)
+    r[rows] = r_i
+    system.set_x(x)
+    system.set_r(r)
+    system.reset_accumulators()
+    ex = EpochExecutor("parallel")
+    ex.run_epoch(1, [(j, [(np.array([i], dtype=np.int64), float(beta))])], None, system)
+    x_new = system.get_xhat()[system.voxel_indices(j)]
+    # z of the block's rows: panel-local rows rbp[i]..rbp[i+1] -> their measurements
+    pan = system.panel(j)
+    zj = system.get_z()[j]
+    z_i = np.zeros(rows.size)
+    lo, hi = int(pan.rbp[i]), int(pan.rbp[i + 1])
+    order = np.argsort(rows, kind="stable")
+    pos = order[np.searchsorted(rows[order], pan.l2g[lo:hi])]
+    z_i[pos] = zj[lo:hi]
+    return x_new, z_i, float(ex.last_mus[0])
+
+
 def audit_state(state, system):
     """max |r - (y - sum_j z^j)| / max |y| on the device (solvers.py:154-166)."""
     return {"epoch": state.epoch, "r_drift": system.audit_drift()}

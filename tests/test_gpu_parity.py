@@ -473,3 +473,32 @@ def test_256_row_blocks(mode, gs, alpha):
 def test_zero_epochs_returns_start(cfg1_system, cfg1_runs):
     x, tr = run_gcsgd(cfg1_system, cfg1_runs["y"], SolverParams(epochs=0, b=0.5, seed=1))
     assert np.all(x == 0.0) and len(tr.rows) == 0
+
+
+@pytest.mark.parametrize("i,j", [(0, 0), (2, 1), (3, 3)])
+def test_basic_iteration_dense_single_step(cfg1_system, i, j):
+    """tests/test_solvers.py:83-101 analogue: one step on block (i, j) against a
+    dense numpy computation of g, mu, x_new and z_i at 1e-10."""
+    from paper_1709_00953_b200 import basic_iteration
+    rng = np.random.default_rng(40 + i + 10 * j)
+    rows = cfg1_system.measurement_rows([i])
+    vox = cfg1_system.voxel_indices(j)
+    pan = cfg1_system.panel(j)
+    # dense A_ij (rows of block i x columns of panel j)
+    A = np.zeros((rows.size, vox.size))
+    rpos = {int(g): q for q, g in enumerate(rows)}
+    for lr in range(int(pan.rbp[i]), int(pan.rbp[i + 1])):
+        for p_ in range(int(pan.indptr[lr]), int(pan.indptr[lr + 1])):
+            A[rpos[int(pan.l2g[lr])], int(pan.cols[p_])] = pan.data[p_]
+    r_i = rng.normal(size=rows.size)
+    x_j = rng.normal(size=vox.size)
+    x_new, z_i, mu = basic_iteration(cfg1_system, i, j, r_i, x_j, 0.7)
+    g = A.T @ r_i
+    t = A @ g
+    mu_ref = 0.7 * (g @ g) / (t @ t)
+    assert abs(mu - mu_ref) <= 1e-10 * mu_ref
+    assert rel(x_new, x_j + mu_ref * g) <= 1e-10
+    assert rel(z_i, A @ (x_j + mu_ref * g)) <= 1e-10
+    # zero residual: zero gradient, unchanged image, z = A x_j
+    x0, z0, mu0 = basic_iteration(cfg1_system, i, j, np.zeros(rows.size), x_j, 0.7)
+    assert mu0 == 0.0 and np.array_equal(x0, x_j) and rel(z0, A @ x_j) <= 1e-12
