@@ -1,32 +1,26 @@
 // epoch.cu -- the persistent epoch kernel.
 //
-// One cooperative launch runs a whole epoch of the plan (executor.py:225-253).
-// For every task k (one basic iteration of _run_tasks, executor.py:42-102):
+// One cooperative launch (one 1024-thread CTA per SM) runs a whole epoch of
+// the plan (executor.py:225-253): every task is one basic iteration of
+// _run_tasks (executor.py:42-102), then the z commits, the refresh, the
+// optional _commit_epoch (solvers.py:180-185) and the metric norms.  All
+// reductions have a fixed order: a run is bitwise reproducible for a grid.
 //
-//   phase 1   g = (A_I^J)^T r_I     per 16-column voxel tile: stage the tile's
-//                                   sinogram band of r in shared memory, one
-//                                   warp per column streams the CSC (16-byte
-//                                   loads of 8 entries) over the task's row
-//                                   blocks and gathers r from shared memory;
-//                                   writes (g, x_J) pairs; gg partials
-//   -- grid barrier --              gg = fixed-order sum of block partials
-//   phase 2a  per super tile: stage its (g, x) pairs in shared memory, stream
-//             the task's row units (one 4-entry vector per lane per step),
-//             segmented warp reduction on the segment-start bitmap ->
-//             (t, ax) partial per (row, super tile) segment
-//   -- grid barrier --
-//   phase 2b  per row: t, ax = sum of its segments in tile order; denom partials
-//   -- grid barrier --              denom, mu = beta*gg/denom, status 0/1/2
-//   phase 3   xhat_J += x_J + mu g  (x_new rounded like the reference)
-//             z_I = ax + mu t       straight into the z store (commit_task)
-//             serial_faithful: refresh of the visit's drawn rows,
-//             r = y - sum_j z^j in ascending j (executor.py:215-223)
-//   -- grid barrier only between serial visits --
-//
-// Epoch tail: parallel-mode refresh over the union of drawn rows, projection
-// sum metrics, optional _commit_epoch (solvers.py:180-185), last-block norm
-// reduction.  All reductions have a fixed order: deterministic for a given
-// grid.
+// Batched path (parallel epochs whose tasks are all full panels; the BASELINE
+// configs 3-5): every phase runs over the tasks of the whole epoch at once,
+// four grid barriers per epoch.
+//   A  g = A_J^T r per 16x16-voxel tile: the tile's band of r staged in
+//      shared memory (cp.async, 8-lane groups per range), the lane-
+//      interleaved CSC streamed by 4 warps per 32-column slice, column
+//      partials reduced in a fixed order; (g, x) pairs + gg partials
+//   B  per SELL slice of a super tile (its (g, x) staged, swizzled): one
+//      (row, super tile) segment per lane -> (t, ax) partial, SELL order
+//   C  per row: t, ax = its segments' partials in tile order; denom partials
+//   D  mu, status per task; xhat += x_new per visit; z = ax + mu t
+//   tail: r = y - sum_j z^j on the drawn rows (ascending j), commit, norms
+// Per-task path (serial_faithful and partial groups): the same phase-1 and
+// phase-2 code per task, three grid barriers per task, and in serial mode the
+// refresh of the visit's drawn rows after its last task (executor.py:215-223).
 #include <cstdio>
 #include <cuda_runtime.h>
 #include <type_traits>
@@ -36,7 +30,7 @@
 namespace {
 
 #ifndef BCT_EXP
-#define BCT_EXP 0
+#define BCT_EXP 0   // profiling variants (5: no band copies, 6: no phase-1 stream, 7: no gathers)
 #endif
 #ifndef BCT_P1_UNROLL
 #define BCT_P1_UNROLL 2
@@ -677,7 +671,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     {
         // whole tiles in rounds of G; the tiles of the last partial round are
         // cut into up to 8 slice parts so every CTA gets the same share
-        const int bb = BCT_EXP == 9 ? G - 1 - b : b;   // profiling: reversed item map
+        const int bb = b;
         const int full = hdr.n_tiles_total / G, rem = hdr.n_tiles_total - full * G;
         const int nsplit = rem > 0 ? max(1, min(8, G / rem)) : 1;
         const int n_items = full + (bb < rem * nsplit ? 1 : 0);
@@ -803,7 +797,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const int v0 = __ldg(P.st_ptr + st), v1 = __ldg(P.st_ptr + st + 1);
             const double2 *gx = gxb + T.gx_off;
             ++dbg_segs;
-            for (int q = threadIdx.x; q < (BCT_EXP == 10 ? 0 : v1 - v0); q += BLOCK) {
+            for (int q = threadIdx.x; q < v1 - v0; q += BLOCK) {
                 const double2 a = gx[v0 + q];
                 gs[swz_idx(q, P.swz_shift)] = GS{(decltype(GS::x))a.x, (decltype(GS::x))a.y};
             }
@@ -1106,9 +1100,8 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                             vr_s);
                     __syncthreads();
                 }
-#if BCT_EXP != 4
                 wsum += tile_g<V>(P, t, c0, c1, bt, xj, gx, red, bmask != nullptr ? vr_s : nullptr);
-#endif
+
                 __syncthreads();
                 if (dbuf) {
                     cur ^= 1;
@@ -1179,20 +1172,11 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                         const int i = base + ((kv * 32 + lane) << 2);
                         int cc[4];
                         double v[4];
-#if BCT_EXP == 2
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) { cc[q] = (i * 13 + q * 7) & 4095; v[q] = 1.0; }
-#else
                         ld4u16(P.fidx + i, cc);
                         ld4v(fv + i, v);
-#endif
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-#if BCT_EXP == 1
-                            const double2 a = make_double2((double)cc[q], 1.0);
-#else
                             const GS a = gs[cc[q]];
-#endif
                             t = fma(v[q], (double)a.x, t);
                             ax = fma(v[q], (double)a.y, ax);
                         }
