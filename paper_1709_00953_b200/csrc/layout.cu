@@ -1,26 +1,29 @@
 // layout.cu -- the HBM layout of one column panel, built on the device.
 //
-// The epoch kernel is bound by L1 wavefronts, not bytes, when it gathers the
-// dense vectors straight from global memory (one wavefront per distinct
+// The epoch kernel would be bound by L1 wavefronts, not bytes, if it gathered
+// the dense vectors straight from global memory (one wavefront per distinct
 // 128-byte line; a warp-wide gather of residual or image entries touches up to
 // 32 lines).  The layout therefore makes every gather a shared-memory access:
 //
 // Phase 1 (g = A_I^T r_I) reads the panel CSC.  Columns (voxels) are grouped
-// into tiles (8x8 voxels for strips); the rows crossing a tile form a
-// narrow "sinogram band" (a few bins per view).  Per tile the band is stored
-// as ranges of consecutive measurement ids; the kernel stages r over the band
-// in shared memory and every CSC entry carries its 16-bit band slot (tloc).
+// into tiles (16x16 voxels for strips, 8x8 / 4x8 when the band would not fit);
+// the rows crossing a tile form a narrow "sinogram band" (a few bins per
+// view), stored as even-aligned ranges of consecutive measurement ids that
+// never cross a row block.  Each tile's columns are stored in 32-column slices,
+// lane-interleaved 8 entries at a time (csl_start), every entry carrying its
+// 16-bit band slot (tloc); a lane's 8 entries are ordered to spread the
+// shared-memory banks of each gather.
 //
 // Phase 2 (t = A_I g, ax = A_I x_J) reads the forward store.  The panel's
-// voxels are cut into super tiles of <= 4096 (iy ranges of a strip); each
-// row's entries are grouped per super tile into segments (row, tile) that
-// carry 16-bit tile-local voxel indices (fidx).  The segments of one (super
-// tile, row block) group are sorted by length and stored as SELL-32 slices
-// (32 segments interleaved 4 entries at a time), so a warp streams a slice
-// with coalesced 16-byte loads, one segment per lane, gathering (g, x) pairs
-// from the super tile staged in shared memory.  Per-segment partial sums are
-// combined per row in super-tile order (deterministic).  A task over any
-// subset of row blocks maps to whole slices.
+// voxels are cut into super tiles (16384 voxels in FP32 mode, 4096 in FP64;
+// iy ranges of a strip); each row's entries are grouped per super tile into
+// segments (row, super tile) that carry 16-bit, swizzled super-tile voxel
+// indices (fidx).  The segments of one (super tile, row block) group are
+// sorted by length and stored as SELL-32 slices (32 segments interleaved 4
+// entries at a time), so a warp streams a slice with coalesced 16-byte loads,
+// one segment per lane, gathering (g, x) pairs from the staged super tile.
+// Per-segment partials are combined per row in super-tile order
+// (deterministic).  A task over any subset of row blocks maps to whole slices.
 //
 // Entries inside a segment stay in the reference's column order, and a row's
 // segments in tile order, so the bitwise set-up kernels (builder.cu) recover
