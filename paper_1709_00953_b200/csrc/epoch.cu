@@ -33,7 +33,7 @@ namespace {
 #define BCT_EXP 0   // profiling variants (5: no band copies, 6: no phase-1 stream, 7: no gathers)
 #endif
 #ifndef BCT_P1_UNROLL
-#define BCT_P1_UNROLL 2
+#define BCT_P1_UNROLL 1
 #endif
 #ifndef BCT_P2_UNROLL
 #define BCT_P2_UNROLL 4
@@ -203,7 +203,10 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
 // streamed panel data is read once per task: keep it from evicting the
 // residual / gradient vectors that must stay in L2
 #ifndef BCT_STREAM_HINT
-#define BCT_STREAM_HINT 1
+#define BCT_STREAM_HINT 0        // measured: costs phase 1 ~10% on f32 panels
+#endif
+#ifndef BCT_STREAM_HINT_F64
+#define BCT_STREAM_HINT_F64 1    // f64 values (serial configs): the hint helps
 #endif
 __device__ __forceinline__ uint64_t evict_first_policy()
 {
@@ -224,7 +227,7 @@ __device__ __forceinline__ float4 ld_stream(const float4 *p)
 }
 __device__ __forceinline__ double2 ld_stream(const double2 *p)
 {
-#if BCT_STREAM_HINT
+#if BCT_STREAM_HINT || BCT_STREAM_HINT_F64
     double2 v;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
                  : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(evict_first_policy()));
@@ -427,16 +430,36 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
         }
         if (BCT_EXP == 6) hi = lo;   // profiling: staging and structure only
         double acc = 0.0;
+        const uint8_t *toff = P.toff;
+        if (toff != nullptr) {   // delta form: 8-bit offsets on a 16-bit base
+            const uint16_t *tbase = P.tbase;
 #pragma unroll P1U
-        for (int u = lo + sub; u < hi; u += wps) {
-            const int i = base + u * 256 + lane * 8;
-            int loc[8];
-            double v[8];
-            ld8u16(P.tloc + i, loc);
-            ld8v(tv + i, v);
+            for (int u = lo + sub; u < hi; u += wps) {
+                const int i = base + u * 256 + lane * 8;
+                const uint2 o = ld_stream(reinterpret_cast<const uint2 *>(toff + i));
+                const int b0 = __ldg(tbase + (i >> 3));
+                double v[8];
+                ld8v(tv + i, v);
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-                acc = fma(v[e], BCT_EXP == 7 ? (double)loc[e] : bt[loc[e]], acc);
+                for (int e = 0; e < 4; ++e)
+                    acc = fma(v[e], bt[b0 + ((o.x >> (8 * e)) & 0xff)], acc);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    acc = fma(v[4 + e], bt[b0 + ((o.y >> (8 * e)) & 0xff)], acc);
+            }
+        } else {
+            const uint16_t *tloc = P.tloc;
+#pragma unroll P1U
+            for (int u = lo + sub; u < hi; u += wps) {
+                const int i = base + u * 256 + lane * 8;
+                int loc[8];
+                double v[8];
+                ld8u16(tloc + i, loc);
+                ld8v(tv + i, v);
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    acc = fma(v[e], BCT_EXP == 7 ? (double)loc[e] : bt[loc[e]], acc);
+            }
         }
         red[sub * (ns * 32) + si * 32 + lane] = acc;
     }

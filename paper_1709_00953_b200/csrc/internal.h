@@ -39,7 +39,10 @@ struct PanelDev {
     // panel CSC with tile bands (phase 1): slices of 32 columns of a tile,
     // entry e of lane l of slice s at csl_start[s] + ((e/8)*32 + l)*8 + e%8
     const void *tvals;         // T
-    const uint16_t *tloc;      // slot of the entry's row in its tile's band
+    const uint16_t *tloc;      // slot of the entry's row in its tile's band (null when
+                               // the delta form below is used)
+    const uint8_t *toff;       // delta form: slot = tbase[e / 8] + toff[e] (a lane's 8
+    const uint16_t *tbase;     // entries span < 256 slots on strip tiles)
     const int32_t *csl_start;  // [n_cslices+1]
     const int32_t *cptr;       // [n_cols*(m+1)] column-local start of each row block
     const int32_t *corder;     // tile order of device columns, tile_cols per tile

@@ -530,6 +530,30 @@ __global__ void csc_bank_perm_k(V *tvals, uint16_t *tloc, const int32_t *csl_sta
     }
 }
 
+// Delta form of tloc: per lane-vector (8 entries) a 16-bit base (the smallest
+// slot of its nonzero entries) and 8-bit offsets; zero (padding) entries read
+// the base.  Flags a vector whose span does not fit 8 bits.
+template <typename V>
+__global__ void tloc_delta_k(const V *tvals, const uint16_t *tloc, int64_t n_vec, uint8_t *toff,
+                             uint16_t *tbase, int *overflow)
+{
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n_vec) return;
+    int lo = 1 << 30, hi = -1;
+    for (int e = 0; e < 8; ++e)
+        if (tvals[q * 8 + e] != (V)0) {
+            lo = min(lo, (int)tloc[q * 8 + e]);
+            hi = max(hi, (int)tloc[q * 8 + e]);
+        }
+    if (hi < 0) lo = hi = tloc[q * 8];   // all padding
+    if (hi - lo > 255) atomicOr(overflow, 1);
+    tbase[q] = (uint16_t)lo;
+    for (int e = 0; e < 8; ++e) {
+        const int d = tvals[q * 8 + e] != (V)0 ? (int)tloc[q * 8 + e] - lo : 0;
+        toff[q * 8 + e] = (uint8_t)min(d, 255);
+    }
+}
+
 // cptr[d*(m+1)+i] = column-local index of column d's first entry with local row >= rbp[i]
 __global__ void cptr_local_k(const int32_t *colstart, const int32_t *tlocal_sorted,
                              const int32_t *rbp, int m, int32_t n_cols, int32_t *cptr)
@@ -884,9 +908,32 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
             csc_bank_perm_k<float><<<pb, 128, 0, s>>>((float *)tvals, tloc, csl_start, n_cslices);
     }
     LCK(cudaGetLastError());
+    // 8-bit band offsets when every lane-vector spans < 256 slots (strip tiles)
+    uint8_t *toff = nullptr;
+    uint16_t *tbase = nullptr;
+    if (!getenv("BCT_NO_TLOC_DELTA") && csc_cap > 0) {
+        const int64_t n_vec = csc_cap / 8;
+        uint8_t *to = K.get<uint8_t>(csc_cap);
+        uint16_t *tb = K.get<uint16_t>(n_vec);
+        int *ovf = T.get<int>(1);
+        LNN(to); LNN(tb); LNN(ovf);
+        LCK(cudaMemsetAsync(ovf, 0, 4, s));
+        if (dtype == 0)
+            tloc_delta_k<double><<<nb(n_vec, 256), 256, 0, s>>>((const double *)tvals, tloc, n_vec,
+                                                               to, tb, ovf);
+        else
+            tloc_delta_k<float><<<nb(n_vec, 256), 256, 0, s>>>((const float *)tvals, tloc, n_vec,
+                                                              to, tb, ovf);
+        if (read1(ovf, s) == 0) {
+            toff = to;
+            tbase = tb;
+        }
+    }
     LCK(cudaStreamSynchronize(s));
     release(tmp);
 
+    P.toff = toff;
+    P.tbase = tbase;
     P.fvals = fvals;
     P.fidx = fidx;
     P.slice_start = slice_start;
