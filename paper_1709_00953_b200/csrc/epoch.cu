@@ -205,6 +205,9 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
 #ifndef BCT_STREAM_HINT
 #define BCT_STREAM_HINT 0        // measured: costs phase 1 ~10% on f32 panels
 #endif
+#ifndef BCT_B_HINT
+#define BCT_B_HINT 1
+#endif
 #ifndef BCT_STREAM_HINT_F64
 #define BCT_STREAM_HINT_F64 1    // f64 values (serial configs): the hint helps
 #endif
@@ -281,9 +284,17 @@ __device__ __forceinline__ void ld8u16(const uint16_t *p, int k[8])
     k[0] = a.x & 0xffff; k[1] = a.x >> 16; k[2] = a.y & 0xffff; k[3] = a.y >> 16;
     k[4] = a.z & 0xffff; k[5] = a.z >> 16; k[6] = a.w & 0xffff; k[7] = a.w >> 16;
 }
+// phase-2 streams (SELL values / indices): L2 evict-first measured a small
+// gain here (it costs phase 1, whose loads use the plain path)
 __device__ __forceinline__ void ld4v(const float *p, double v[4])
 {
+#if BCT_B_HINT
+    float4 a;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(p), "l"(evict_first_policy()));
+#else
     float4 a = ld_stream(reinterpret_cast<const float4 *>(p));
+#endif
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
 }
 __device__ __forceinline__ void ld4v(const double *p, double v[4])
@@ -294,7 +305,13 @@ __device__ __forceinline__ void ld4v(const double *p, double v[4])
 }
 __device__ __forceinline__ void ld4u16(const uint16_t *p, int k[4])
 {
+#if BCT_B_HINT
+    uint2 a;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(a.x), "=r"(a.y) : "l"(p), "l"(evict_first_policy()));
+#else
     uint2 a = ld_stream(reinterpret_cast<const uint2 *>(p));
+#endif
     k[0] = a.x & 0xffff; k[1] = a.x >> 16; k[2] = a.y & 0xffff; k[3] = a.y >> 16;
 }
 
