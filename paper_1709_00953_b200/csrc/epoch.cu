@@ -288,7 +288,11 @@ __device__ __forceinline__ void ld8u16(const uint16_t *p, int k[8])
 // gain here (it costs phase 1, whose loads use the plain path)
 __device__ __forceinline__ void ld4v(const float *p, double v[4])
 {
-#if BCT_B_HINT
+#if BCT_B_HINT == 2
+    float4 a;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(p), "l"(evict_first_policy()));
+#elif BCT_B_HINT
     float4 a;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(p), "l"(evict_first_policy()));
@@ -305,7 +309,11 @@ __device__ __forceinline__ void ld4v(const double *p, double v[4])
 }
 __device__ __forceinline__ void ld4u16(const uint16_t *p, int k[4])
 {
-#if BCT_B_HINT
+#if BCT_B_HINT == 2
+    uint2 a;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(a.x), "=r"(a.y) : "l"(p), "l"(evict_first_policy()));
+#elif BCT_B_HINT
     uint2 a;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
                  : "=r"(a.x), "=r"(a.y) : "l"(p), "l"(evict_first_policy()));
