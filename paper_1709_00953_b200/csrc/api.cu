@@ -274,7 +274,8 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
         int a = 0, b2 = 0;
         if (sscanf(e, "%dx%d", &a, &b2) == 2 && a > 0 && b2 > 0 && (a * b2) % 32 == 0 &&
             a * b2 <= 256)
-            shapes = {{a, b2, 2}, {a, b2, 1}, {4, 8, 1}};
+            shapes = getenv("BCT_TILE_NBUF1") ? std::vector<Shape>{{a, b2, 1}, {4, 8, 1}}
+                                              : std::vector<Shape>{{a, b2, 2}, {a, b2, 1}, {4, 8, 1}};
     }
     Placement pl;
     // matrix-free phase B is opt-in (BCT_REPLAY=1): regenerating the values
@@ -444,7 +445,8 @@ int finalize(bct_ctx *c)
     DALLOC(c->seg_part, 2 * 4 * c->max_seg + 2);   // TASK_SPLIT (epoch.cu) partials per lane
     // two band buffers when they fit, else one (staging then serializes)
     // phase-1 bands (double-buffered when they fit) + the tile reduction area
-    c->band_dbuf = 2 * (size_t)c->band_cap * 8 + bct::PHASE1_RED_BYTES <= SMEM_BUDGET ? 1 : 0;
+    c->band_dbuf = (2 * (size_t)c->band_cap * 8 + bct::PHASE1_RED_BYTES <= SMEM_BUDGET &&
+                    !getenv("BCT_TILE_NBUF1")) ? 1 : 0;
     c->smem = std::max<size_t>(c->smem, (size_t)c->band_cap * 8 * (c->band_dbuf ? 2 : 1) +
                                             bct::PHASE1_RED_BYTES);
     c->smem = std::max<size_t>(c->smem, 1024 * 12 + 64);
