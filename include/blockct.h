@@ -13,6 +13,10 @@
  *          of SURVEY §8c.  The device additionally builds a per-panel CSC
  *          ("transposed panel") with per-(column,row-block) segment pointers
  *          so A_I^T r needs no atomics.
+ *   bct_create_scan
+ *       <- BlockSystem.build(geometry, partition, table) for any ScanGeometry
+ *          (fan / cone beam), projector.py:541-626 with _trace_ray_kernel
+ *          (projector.py:51-198) run on the device.
  *   bct_run_epoch
  *       <- EpochExecutor.run_epoch, executor.py:225-253, with the numba
  *          kernel _run_tasks (executor.py:42-102), commit_task/_commit_kernel
@@ -94,6 +98,32 @@ typedef struct {
     int32_t device;
 } bct_pb_desc;
 
+/* General scan (fan / cone beam, any pose list) traced on the device:
+ * geometry.py:42-312 (grid, flat detector, poses) and the blocked store of
+ * projector.py:563-626.  The partition and the silhouette probability table
+ * (geometry.py:586-672) come from the host (paper_1709_00953_b200/scan.py). */
+typedef struct {
+    int64_t dims[3];                /* voxel grid; a 2D grid has dims[2]=1  */
+    double voxel_size[3];
+    double origin[3];               /* low corner of voxel (0,0,0)          */
+    int64_t det_nu, det_nv;         /* pixel g = view*nu*nv + iv*nu + iu    */
+    double det_du, det_dv;
+    int64_t n_views;
+    const double *poses;            /* [n_views*12]: source, detector centre,
+                                       det_u, det_v                         */
+    int32_t m;                      /* row blocks, <= 256                   */
+    int32_t n_panels;               /* column blocks (voxel boxes)          */
+    const int64_t *row_block_ptr;   /* [m+1]                                */
+    const int64_t *row_block_rows;  /* measurement ids of each row block    */
+    const int64_t *box_lo;          /* [n_panels*3] voxel index bounds      */
+    const int64_t *box_hi;
+    const double *table_values;     /* [m*n_panels]                         */
+    const double *table_totals;     /* [n_panels]                           */
+    int32_t panel_begin, panel_end;
+    int32_t dtype;
+    int32_t device;
+} bct_scan_desc;
+
 typedef struct {
     int64_t n_tasks;
     int64_t n_visits;
@@ -109,6 +139,9 @@ int bct_version(void);
 
 int bct_create(const bct_system_desc *desc, const bct_panel *panels, bct_ctx **out);
 int bct_create_parallel_beam(const bct_pb_desc *desc, bct_ctx **out);
+/* Errors: BCT_EINVAL for a degenerate ray or a source inside a voxel box
+ * (projector.py:278-284, 591-592: GeometryError in the reference). */
+int bct_create_scan(const bct_scan_desc *desc, bct_ctx **out);
 int bct_destroy(bct_ctx *ctx);
 
 /* Sizes: n_meas, n_vox, m, n_panels, owned range, nnz (owned), z length. */

@@ -207,6 +207,63 @@ class OracleSystem:
         tab = OracleTable(vals, vals.sum(axis=0))
         return cls(data, cols, indptr, rbp, l2g, row_meas, vidx, tab, n_meas, n * n)
 
+    @classmethod
+    def scan(cls, geometry, partition, values):
+        """_assemble (projector.py:563-626) for a general scan: every column
+        block's rays traced per row block in order with the C restatement of
+        _trace_ray_kernel; pixel centres as geometry.py:234-240.  Small cases
+        only (one ctypes call per ray)."""
+        L = lib()
+        g, det = geometry.grid, geometry.detector
+        origin = _c(g.origin, np.float64)
+        vsize = _c(g.voxel_size, np.float64)
+        nu, nv = det.pixel_counts
+        du, dv = det.pixel_spacing
+        u = (np.arange(nu) - (nu - 1) / 2.0) * du
+        v = (np.arange(nv) - (nv - 1) / 2.0) * dv
+        uu, vv = np.meshgrid(u, v)
+        off = np.column_stack([uu.ravel(), vv.ravel()])
+        per = nu * nv
+        m, nc = partition.n_row_blocks, partition.n_col_blocks
+        data, cols, indptr, rbp, l2g = [], [], [], [], []
+        for j in range(nc):
+            lo = _c(partition.vol_lo[j], np.int64)
+            hi = _c(partition.vol_hi[j], np.int64)
+            cap = int((hi - lo).sum() + 3)
+            idx = np.empty(cap, np.int64)
+            lng = np.empty(cap)
+            d_parts, c_parts, counts, rows = [], [], [], []
+            rb = np.zeros(m + 1, np.int64)
+            for i, meas in enumerate(partition.rows):
+                hits = 0
+                for gm in meas:
+                    pose = geometry.poses[int(gm) // per]
+                    o = off[int(gm) % per]
+                    dst = _c(pose.detector_center + o[0] * pose.det_u + o[1] * pose.det_v,
+                             np.float64)
+                    k = L.oracle_trace_ray(_c(pose.source, np.float64), dst, origin, vsize, lo,
+                                           hi, idx, lng)
+                    if k < 0:
+                        raise ValueError("degenerate ray")
+                    if k > 0:
+                        d_parts.append(lng[:k].copy())
+                        c_parts.append(idx[:k].astype(np.int32))
+                        counts.append(k)
+                        rows.append(int(gm))
+                        hits += 1
+                rb[i + 1] = rb[i] + hits
+            ip = np.zeros(len(counts) + 1, np.int64)
+            np.cumsum(counts, out=ip[1:])
+            data.append(np.concatenate(d_parts) if d_parts else np.empty(0))
+            cols.append(np.concatenate(c_parts) if c_parts else np.empty(0, np.int32))
+            indptr.append(ip)
+            rbp.append(rb)
+            l2g.append(np.array(rows, np.int64))
+        vals = np.asarray(values, dtype=np.float64)
+        tab = OracleTable(vals, vals.sum(axis=0))
+        return cls(data, cols, indptr, rbp, l2g, list(partition.rows), list(partition.vidx),
+                   tab, geometry.n_measurements, g.n_voxels)
+
     def voxel_indices(self, j):
         return self.vidx[j]
 

@@ -47,6 +47,15 @@ class PBDesc(ctypes.Structure):
                 ("panel_end", _i32), ("dtype", _i32), ("device", _i32)]
 
 
+class ScanDesc(ctypes.Structure):
+    _fields_ = [("dims", _i64 * 3), ("voxel_size", _dbl * 3), ("origin", _dbl * 3),
+                ("det_nu", _i64), ("det_nv", _i64), ("det_du", _dbl), ("det_dv", _dbl),
+                ("n_views", _i64), ("poses", _p), ("m", _i32), ("n_panels", _i32),
+                ("row_block_ptr", _p), ("row_block_rows", _p), ("box_lo", _p), ("box_hi", _p),
+                ("table_values", _p), ("table_totals", _p), ("panel_begin", _i32),
+                ("panel_end", _i32), ("dtype", _i32), ("device", _i32)]
+
+
 class EpochResult(ctypes.Structure):
     _fields_ = [("n_tasks", _i64), ("n_visits", _i64), ("n_degenerate", _i64),
                 ("resid_sq", _dbl), ("x_sq", _dbl), ("err_sq", _dbl), ("kernel_ms", _dbl)]
@@ -56,6 +65,7 @@ class EpochResult(ctypes.Structure):
 _SIGS = {
     "bct_create": [ctypes.POINTER(SystemDesc), ctypes.POINTER(Panel), _pp],
     "bct_create_parallel_beam": [ctypes.POINTER(PBDesc), _pp],
+    "bct_create_scan": [ctypes.POINTER(ScanDesc), _pp],
     "bct_destroy": [_p],
     "bct_info": [_p, _p],
     "bct_panel_info": [_p, _i32, _p, _p, _p],

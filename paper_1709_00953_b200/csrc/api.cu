@@ -791,6 +791,171 @@ int bct_create_parallel_beam(const bct_pb_desc *d, bct_ctx **out)
     return 0;
 }
 
+int bct_create_scan(const bct_scan_desc *d, bct_ctx **out)
+{
+    if (!d || !out || !d->poses || !d->row_block_ptr || !d->row_block_rows || !d->box_lo ||
+        !d->box_hi || !d->table_values || !d->table_totals)
+        return fail(nullptr, BCT_EINVAL, "null argument");
+    *out = nullptr;
+    int r = check_common_desc(nullptr, d->m, d->n_panels, d->panel_begin, d->panel_end, d->dtype);
+    if (r) return r;
+    for (int a = 0; a < 3; ++a)
+        if (d->dims[a] < 1 || !(d->voxel_size[a] > 0.0) || !std::isfinite(d->origin[a]))
+            return fail(nullptr, BCT_EINVAL, "bad voxel grid");
+    if (d->det_nu < 1 || d->det_nv < 1 || d->n_views < 1 || !(d->det_du > 0.0) ||
+        !(d->det_dv > 0.0))
+        return fail(nullptr, BCT_EINVAL, "bad detector");
+    bct_ctx *c = new bct_ctx();
+    auto bail = [&](int code) {
+        g_create_err = c->err;
+        destroy(c);
+        return code;
+    };
+    if ((r = init_ctx(c, d->device, d->panel_end - d->panel_begin))) return bail(r);
+    c->dtype = d->dtype;
+    c->m = d->m;
+    c->n_panels = d->n_panels;
+    c->pb = d->panel_begin;
+    c->pe = d->panel_end;
+    c->np = c->pe - c->pb;
+    c->n_meas = d->n_views * d->det_nu * d->det_nv;
+    c->n_vox = d->dims[0] * d->dims[1] * d->dims[2];
+    if (c->n_meas >= (1ll << 31) || c->n_vox >= (1ll << 40))
+        return bail(fail(c, BCT_EINVAL, "scan too large"));
+    c->rb_ptr.assign(d->row_block_ptr, d->row_block_ptr + c->m + 1);
+    if (c->rb_ptr[0] != 0) return bail(fail(c, BCT_EINVAL, "row_block_ptr[0] != 0"));
+    for (int i = 0; i < c->m; ++i)
+        if (c->rb_ptr[i + 1] < c->rb_ptr[i]) return bail(fail(c, BCT_EINVAL, "bad row_block_ptr"));
+    c->rb_rows.assign(d->row_block_rows, d->row_block_rows + c->rb_ptr[c->m]);
+    for (int64_t g : c->rb_rows)
+        if (g < 0 || g >= c->n_meas) return bail(fail(c, BCT_EINVAL, "row block id out of range"));
+    const int64_t nL = (int64_t)c->rb_rows.size();
+    // column blocks: voxel boxes, ids in C order inside the box (geometry.py:366-383)
+    std::vector<Box> boxes(c->n_panels);
+    c->col_ptr.assign(1, 0);
+    for (int j = 0; j < c->n_panels; ++j) {
+        Box &B = boxes[j];
+        for (int a = 0; a < 3; ++a) {
+            B.lo[a] = d->box_lo[3 * j + a];
+            B.hi[a] = d->box_hi[3 * j + a];
+            if (B.lo[a] < 0 || B.hi[a] > d->dims[a] || B.lo[a] >= B.hi[a])
+                return bail(fail(c, BCT_EINVAL, "column block %d: bad voxel box", j));
+        }
+        const int64_t bx = B.hi[0] - B.lo[0], by = B.hi[1] - B.lo[1], bz = B.hi[2] - B.lo[2];
+        if (bx * by * bz >= (1ll << 24)) return bail(fail(c, BCT_EINVAL, "panel %d too large", j));
+        for (int64_t ix = B.lo[0]; ix < B.hi[0]; ++ix)
+            for (int64_t iy = B.lo[1]; iy < B.hi[1]; ++iy)
+                for (int64_t iz = B.lo[2]; iz < B.hi[2]; ++iz)
+                    c->col_vox.push_back((ix * d->dims[1] + iy) * d->dims[2] + iz);
+        c->col_ptr.push_back((int64_t)c->col_vox.size());
+    }
+    c->table_values.assign(d->table_values, d->table_values + (int64_t)c->m * c->n_panels);
+    c->table_totals.assign(d->table_totals, d->table_totals + c->n_panels);
+    // a source strictly inside an owned box has no defined projection
+    // (projector.py:278-284)
+    for (int j = c->pb; j < c->pe; ++j)
+        for (int64_t v = 0; v < d->n_views; ++v) {
+            bool inside = true;
+            for (int a = 0; a < 3; ++a) {
+                const double s = d->poses[12 * v + a];
+                const double plo = d->origin[a] + (double)boxes[j].lo[a] * d->voxel_size[a];
+                const double phi = d->origin[a] + (double)boxes[j].hi[a] * d->voxel_size[a];
+                inside = inside && s > plo && s < phi;
+            }
+            if (inside)
+                return bail(fail(c, BCT_EINVAL, "source of view %lld lies inside column block %d",
+                                 (long long)v, j));
+        }
+    ScanDev S;
+    for (int a = 0; a < 3; ++a) {
+        S.origin[a] = d->origin[a];
+        S.vsize[a] = d->voxel_size[a];
+    }
+    S.nu = d->det_nu;
+    S.nv = d->det_nv;
+    S.du = d->det_du;
+    S.dv = d->det_dv;
+    double *d_poses = nullptr;
+    int64_t *d_edges = nullptr;
+    int32_t *d_L = nullptr, *d_counts = nullptr, *d_flags = nullptr, *d_pos = nullptr,
+            *d_bad = nullptr;
+    DALLOC(d_poses, 12 * d->n_views);
+    DALLOC(d_edges, c->m + 1);
+    DALLOC(d_L, std::max<int64_t>(nL, 1));
+    DALLOC(d_counts, std::max<int64_t>(nL, 1));
+    DALLOC(d_flags, std::max<int64_t>(nL, 1));
+    DALLOC(d_pos, nL + 1);
+    DALLOC(d_bad, 1);
+    S.poses = d_poses;
+    {
+        std::vector<int32_t> L(c->rb_rows.begin(), c->rb_rows.end());
+        CK(cudaMemcpy(d_poses, d->poses, 8 * 12 * d->n_views, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_edges, c->rb_ptr.data(), 8 * (c->m + 1), cudaMemcpyHostToDevice));
+        if (nL > 0) CK(cudaMemcpy(d_L, L.data(), 4 * nL, cudaMemcpyHostToDevice));
+        CK(cudaMemset(d_bad, 0, 4));
+    }
+    size_t sb = bct::scan_temp_bytes(nL + 1);
+    char *cub = nullptr;
+    DALLOC(cub, (int64_t)sb);
+    double *vals64 = nullptr;
+    int32_t *cols = nullptr, *rbp_tmp = nullptr;
+    DALLOC(rbp_tmp, c->m + 1);
+    for (int lp = 0; lp < c->np; ++lp) {
+        const int j = c->pb + lp;
+        const Box &B = boxes[j];
+        // 1. per-ray counts in row-block order; 2. compaction of the hit rows
+        CK(bct::scan_trace_counts(S, d_L, nL, B, d_counts, d_bad, c->stream));
+        int32_t bad = 0;
+        CK(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (bad) return bail(fail(c, BCT_EINVAL, "degenerate ray (source on a pixel centre)"));
+        int64_t n_hit = 0;
+        int32_t *l2g = nullptr, *rowlen = nullptr, *ip = nullptr;
+        DALLOC(l2g, std::max<int64_t>(nL, 1));
+        DALLOC(rowlen, nL + 1);
+        if (nL > 0)
+            CK(bct::pb_compact(d_counts, nL, d_flags, d_pos, cub, sb, l2g, rowlen, &n_hit,
+                               c->stream));
+        DALLOC(ip, n_hit + 1);
+        CK(cudaMemsetAsync(rowlen + n_hit, 0, 4, c->stream));
+        CK(bct::exclusive_scan_i32(rowlen, ip, n_hit + 1, cub, sb, c->stream));
+        int32_t nnz32 = 0;
+        CK(cudaMemcpyAsync(&nnz32, ip + n_hit, 4, cudaMemcpyDeviceToHost, c->stream));
+        // 3. rbp over list positions, then positions -> measurement ids
+        CK(bct::pb_rbp(l2g, n_hit, d_edges, c->m, rbp_tmp, c->stream));
+        std::vector<int32_t> rb(c->m + 1);
+        CK(cudaMemcpyAsync(rb.data(), rbp_tmp, 4 * (c->m + 1), cudaMemcpyDeviceToHost, c->stream));
+        CK(bct::gather_i32(d_L, l2g, n_hit, l2g, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        free_tmp(c, rowlen);
+        const int64_t nnz = nnz32;
+        if (nnz >= (1ll << 30)) return bail(fail(c, BCT_EINVAL, "panel %d too large", j));
+        // 4. sorted rows (values + local indices)
+        DALLOC(vals64, std::max<int64_t>(nnz, 1));
+        DALLOC(cols, std::max<int64_t>(nnz, 1));
+        CK(bct::scan_fill(S, l2g, ip, n_hit, B, vals64, cols, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const int64_t bx = B.hi[0] - B.lo[0], byz = (B.hi[1] - B.lo[1]) * (B.hi[2] - B.lo[2]);
+        if ((r = build_panel(c, lp, (int32_t)n_hit, nnz, vals64, cols, ip, l2g, rb, bx, byz)))
+            return bail(r);
+        free_tmp(c, ip);
+        free_tmp(c, vals64);
+        free_tmp(c, cols);
+    }
+    free_tmp(c, rbp_tmp);
+    free_tmp(c, cub);
+    free_tmp(c, d_L);
+    free_tmp(c, d_counts);
+    free_tmp(c, d_flags);
+    free_tmp(c, d_pos);
+    free_tmp(c, d_bad);
+    free_tmp(c, d_poses);
+    free_tmp(c, d_edges);
+    if ((r = finalize(c))) return bail(r);
+    *out = c;
+    return 0;
+}
+
 int bct_destroy(bct_ctx *c)
 {
     destroy(c);

@@ -45,8 +45,11 @@ __device__ __forceinline__ void pb_endpoints(int64_t n, int64_t bins, double c, 
 }
 
 // Set-up half of the traversal (projector.py:59-145).  Returns false on a miss.
-__device__ bool trace_init(const double *src, const double *dst, const double *origin,
-                           const int64_t *lo, const int64_t *hi, RayTrace &T, double *dv)
+// vsize = 1 on the parallel-beam harness; the general scan passes the grid's.
+template <bool UNIT>
+__device__ bool trace_init_t(const double *src, const double *dst, const double *origin,
+                             const double *vsize, const int64_t *lo, const int64_t *hi,
+                             RayTrace &T, double *dv)
 {
     dv[0] = dst[0] - src[0];
     dv[1] = dst[1] - src[1];
@@ -59,9 +62,10 @@ __device__ bool trace_init(const double *src, const double *dst, const double *o
     double eps_d = REL_EPS * scale;
     double t0 = 0.0, t1 = 1.0;
     for (int a = 0; a < 3; ++a) {
+        const double vs = UNIT ? 1.0 : vsize[a];
         double d = dv[a], s = src[a];
-        double blo = origin[a] + (double)lo[a] * 1.0;
-        double bhi = origin[a] + (double)hi[a] * 1.0;
+        double blo = origin[a] + (double)lo[a] * vs;
+        double bhi = origin[a] + (double)hi[a] * vs;
         if (fabs(d) > eps_d) {
             double ta = (blo - s) / d, tb = (bhi - s) / d;
             if (ta > tb) { double t = ta; ta = tb; tb = t; }
@@ -74,7 +78,7 @@ __device__ bool trace_init(const double *src, const double *dst, const double *o
     if (t1 - t0 <= REL_EPS) return false;
     double probe = t0 + 1e-9 * (t1 - t0);
     for (int a = 0; a < 3; ++a) {
-        int64_t c = (int64_t)floor((src[a] + probe * dv[a] - origin[a]) / 1.0);
+        int64_t c = (int64_t)floor((src[a] + probe * dv[a] - origin[a]) / (UNIT ? 1.0 : vsize[a]));
         if (c < lo[a]) c = lo[a];
         if (c > hi[a] - 1) c = hi[a] - 1;
         T.iv[a] = c;
@@ -89,8 +93,9 @@ __device__ bool trace_init(const double *src, const double *dst, const double *o
             bool pos = dv[a] > 0.0;
             T.step[a] = pos ? 1 : -1;
             int64_t plane = pos ? T.iv[a] + 1 : T.iv[a];
-            T.tmax[a] = (origin[a] + (double)plane * 1.0 - src[a]) / dv[a];
-            T.tdel[a] = 1.0 / fabs(dv[a]);
+            const double vs = UNIT ? 1.0 : vsize[a];
+            T.tmax[a] = (origin[a] + (double)plane * vs - src[a]) / dv[a];
+            T.tdel[a] = vs / fabs(dv[a]);
         }
     }
     T.t0 = t0;
@@ -98,6 +103,13 @@ __device__ bool trace_init(const double *src, const double *dst, const double *o
     T.t = t0;
     T.max_steps = (hi[0] - lo[0]) + (hi[1] - lo[1]) + (hi[2] - lo[2]) + 3;
     return true;
+}
+
+__device__ __forceinline__ bool trace_init(const double *src, const double *dst,
+                                           const double *origin, const int64_t *lo,
+                                           const int64_t *hi, RayTrace &T, double *dv)
+{
+    return trace_init_t<true>(src, dst, origin, nullptr, lo, hi, T, dv);
 }
 
 // One traversal; calls emit(ix, iy, seg) for every positive segment.
@@ -183,6 +195,125 @@ __global__ void pb_fill_kernel(int64_t n, int64_t views, int64_t bins, const dou
         cols[base + slot] = (int32_t)((ix - x0) * n + iy);
         ++run_pos;
     });
+}
+
+// ---- general scan geometry (fan / cone beam, geometry.py + projector.py) ----
+//
+// Measurement g = view * nu*nv + iv*nu + iu; its ray runs from the view's
+// source to the pixel centre dc + off_u*det_u + off_v*det_v, offsets
+// (i - (n-1)/2) * spacing (geometry.py:144-153, 234-240).  The column block is
+// a voxel box [lo, hi); local index ((i0-lo0)*bny + (i1-lo1))*bnz + (i2-lo2)
+// (projector.py:164).  Rays are traced in the row-block order of the
+// partition (list L: every row block's measurement ids in turn), which is the
+// reference's panel row order (projector.py:563-626).
+
+__device__ __forceinline__ void scan_endpoints(const ScanDev &S, int64_t g, double *src,
+                                               double *dst)
+{
+    const int64_t ppv = S.nu * S.nv;
+    const int64_t view = g / ppv, pix = g % ppv;
+    const int64_t iv = pix / S.nu, iu = pix % S.nu;
+    const double ou = ((double)iu - (double)(S.nu - 1) / 2.0) * S.du;
+    const double ov = ((double)iv - (double)(S.nv - 1) / 2.0) * S.dv;
+    const double *p = S.poses + 12 * view;
+    for (int a = 0; a < 3; ++a) {
+        src[a] = p[a];
+        dst[a] = (p[3 + a] + ou * p[6 + a]) + ov * p[9 + a];
+    }
+}
+
+template <typename F>
+__device__ void trace_walk3(RayTrace &T, F emit)
+{
+    for (int64_t it = 0; it < T.max_steps; ++it) {
+        int a = 0;
+        double tm = T.tmax[0];
+        if (T.tmax[1] < tm) { a = 1; tm = T.tmax[1]; }
+        if (T.tmax[2] < tm) { a = 2; tm = T.tmax[2]; }
+        double tn = tm < T.t1 ? tm : T.t1;
+        double seg = (tn - T.t) * T.length;
+        if (seg > 0.0) emit(T.iv[0], T.iv[1], T.iv[2], seg);
+        if (tm >= T.t1) break;
+        T.iv[a] += T.step[a];
+        if (T.iv[a] < T.lo[a] || T.iv[a] >= T.hi[a]) break;
+        T.tmax[a] += T.tdel[a];
+        T.t = tn;
+    }
+}
+
+// counts[q] = entries of ray L[q] in the box; a degenerate ray (source on
+// the pixel centre) sets *bad (projector.py:591-592 raises GeometryError).
+__global__ void scan_count_kernel(ScanDev S, const int32_t *L, int64_t n, Box B, int32_t *counts,
+                                  int32_t *bad)
+{
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    double src[3], dst[3], dv[3];
+    scan_endpoints(S, L[q], src, dst);
+    RayTrace T;
+    int cnt = 0;
+    if (trace_init_t<false>(src, dst, S.origin, S.vsize, B.lo, B.hi, T, dv))
+        trace_walk3(T, [&](int64_t, int64_t, int64_t, double) { ++cnt; });
+    else if (T.length == 0.0)
+        atomicExch(bad, 1);
+    counts[q] = cnt;
+}
+
+__device__ __forceinline__ void rev_range(double *d, int32_t *c, int a, int b)
+{
+    for (--b; a < b; ++a, --b) {
+        double td = d[a]; d[a] = d[b]; d[b] = td;
+        int32_t tc = c[a]; c[a] = c[b]; c[b] = tc;
+    }
+}
+
+// Reverses every maximal run of equal key c / div in [a, b).
+__device__ void rev_runs(double *d, int32_t *c, int a, int b, int32_t div)
+{
+    while (a < b) {
+        int e = a + 1;
+        const int32_t k = c[a] / div;
+        while (e < b && c[e] / div == k) ++e;
+        rev_range(d, c, a, e);
+        a = e;
+    }
+}
+
+// Writes the row of every hit ray sorted by local index.  The reference
+// traverses, then insertion-sorts (projector.py:185-197).  The traversal is
+// monotone along every axis, so the sorted order is reached in O(len) by
+// reversing the whole row when it runs backwards in i0, then each equal-i0
+// run backwards in i1, then each equal-(i0, i1) run backwards in i2 (local
+// indices are distinct, so the order is the same).
+__global__ void scan_fill_kernel(ScanDev S, const int32_t *l2g, const int32_t *indptr,
+                                 int64_t n_hit, Box B, double *data, int32_t *cols)
+{
+    int64_t lr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (lr >= n_hit) return;
+    double src[3], dst[3], dv[3];
+    scan_endpoints(S, l2g[lr], src, dst);
+    RayTrace T;
+    if (!trace_init_t<false>(src, dst, S.origin, S.vsize, B.lo, B.hi, T, dv)) return;
+    const int64_t bny = B.hi[1] - B.lo[1], bnz = B.hi[2] - B.lo[2];
+    const int base = indptr[lr];
+    int k = 0;
+    const int64_t s0 = T.step[0], s1 = T.step[1], s2 = T.step[2];
+    trace_walk3(T, [&](int64_t i0, int64_t i1, int64_t i2, double seg) {
+        data[base + k] = seg;
+        cols[base + k] = (int32_t)(((i0 - B.lo[0]) * bny + (i1 - B.lo[1])) * bnz + (i2 - B.lo[2]));
+        ++k;
+    });
+    const int e = base + k;
+    int dir = 1;
+    if (s0 < 0) { rev_range(data, cols, base, e); dir = -dir; }
+    if (s1 * dir < 0) { rev_runs(data, cols, base, e, (int32_t)(bny * bnz)); dir = -dir; }
+    if (s2 * dir < 0) rev_runs(data, cols, base, e, (int32_t)bnz);
+}
+
+__global__ void gather_i32_kernel(const int32_t *src, const int32_t *idx, int64_t n, int32_t *dst)
+{
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q < n) dst[q] = src[idx[q]];
 }
 
 // Replay records of the forward segments (matrix-free phase B, epoch.cu): the
@@ -599,6 +730,30 @@ cudaError_t pb_fill(int64_t n, int64_t views, int64_t bins, const double *d_cos,
     if (n_hit == 0) return cudaSuccess;
     pb_fill_kernel<<<nblk(n_hit, 64), 64, 0, s>>>(n, views, bins, d_cos, d_sin, x0, x1, d_l2g,
                                                   d_indptr, n_hit, d_data, d_cols);
+    return cudaGetLastError();
+}
+
+cudaError_t scan_trace_counts(const ScanDev &S, const int32_t *L, int64_t n, const Box &B,
+                              int32_t *counts, int32_t *bad, cudaStream_t s)
+{
+    if (n == 0) return cudaSuccess;
+    scan_count_kernel<<<nblk(n, 128), 128, 0, s>>>(S, L, n, B, counts, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t scan_fill(const ScanDev &S, const int32_t *l2g, const int32_t *indptr, int64_t n_hit,
+                      const Box &B, double *data, int32_t *cols, cudaStream_t s)
+{
+    if (n_hit == 0) return cudaSuccess;
+    scan_fill_kernel<<<nblk(n_hit, 64), 64, 0, s>>>(S, l2g, indptr, n_hit, B, data, cols);
+    return cudaGetLastError();
+}
+
+cudaError_t gather_i32(const int32_t *src, const int32_t *idx, int64_t n, int32_t *dst,
+                       cudaStream_t s)
+{
+    if (n == 0) return cudaSuccess;
+    gather_i32_kernel<<<nblk(n, 256), 256, 0, s>>>(src, idx, n, dst);
     return cudaGetLastError();
 }
 

@@ -168,7 +168,25 @@ __host__ __device__ __forceinline__ int swz_idx(int q, int shift)
     return q ^ ((q >> shift) & 15);
 }
 
+// general scan geometry for the device tracer (builder.cu)
+struct ScanDev {
+    double origin[3], vsize[3];
+    int64_t nu, nv;
+    double du, dv;
+    const double *poses;     // [views * 12]: source, detector centre, det_u, det_v
+};
+struct Box {
+    int64_t lo[3], hi[3];    // voxel index bounds of a column block
+};
+
 namespace bct {
+
+cudaError_t scan_trace_counts(const ScanDev &S, const int32_t *L, int64_t n, const Box &B,
+                              int32_t *counts, int32_t *bad, cudaStream_t s);
+cudaError_t scan_fill(const ScanDev &S, const int32_t *l2g, const int32_t *indptr, int64_t n_hit,
+                      const Box &B, double *data, int32_t *cols, cudaStream_t s);
+cudaError_t gather_i32(const int32_t *src, const int32_t *idx, int64_t n, int32_t *dst,
+                       cudaStream_t s);
 
 // epoch-batched path: at most this many tasks (task tables live in shared memory)
 constexpr int MAX_BATCH_TASKS = 256;

@@ -14,7 +14,9 @@ Construction:
   plus the partition and table, uploaded through ``bct_create``;
 * ``from_reference`` -- the same, read off a reference ``BlockSystem`` object;
 * ``parallel_beam`` -- traced on the device (``bct_create_parallel_beam``) for
-  the BASELINE geometry.
+  the BASELINE geometry;
+* ``scan`` -- any fan / cone-beam ``ScanGeometry`` (scan.py), traced on the
+  device (``bct_create_scan``).
 """
 
 from __future__ import annotations
@@ -25,7 +27,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .errors import ConfigurationError
+from .errors import ConfigurationError, GeometryError
 from .geometry import ParallelBeamSpec
 from .sampling import ProbabilityTable
 
@@ -142,6 +144,50 @@ class DeviceBlockSystem:
         return cls(out.value, spec.row_meas(), spec.voxel_indices(),
                    ProbabilityTable(vals, totals), spec.n_measurements, spec.n_voxels, dtype,
                    (pb, pe), device)
+
+    @classmethod
+    def scan(cls, geometry, partition=None, volume_splits=None, detector_splits=None,
+             table=None, dtype="f64", device=0, panel_range=None):
+        """BlockSystem.build(geometry, partition, table) for any ScanGeometry
+        (scan.py): the partition and the silhouette table on the host, the
+        blocked store traced on the device (bct_create_scan)."""
+        from . import scan as S
+        L = N.load()
+        if partition is None:
+            if volume_splits is None or detector_splits is None:
+                raise ConfigurationError("need a partition or volume/detector splits")
+            partition = S.make_partition(geometry, volume_splits, detector_splits)
+        if table is None:
+            vals, totals = S.probability_table(geometry, partition)
+        else:
+            vals = N.f64(table.values)
+            totals = N.f64(table.totals)
+        m, nc = partition.n_row_blocks, partition.n_col_blocks
+        vals = N.f64(vals)
+        totals = N.f64(totals)
+        pb, pe = panel_range if panel_range is not None else (0, nc)
+        g, det = geometry.grid, geometry.detector
+        poses = N.f64(np.concatenate([np.concatenate([p.source, p.detector_center, p.det_u,
+                                                      p.det_v]) for p in geometry.poses]))
+        rb_ptr = np.zeros(m + 1, dtype=np.int64)
+        np.cumsum([r.size for r in partition.rows], out=rb_ptr[1:])
+        rb_rows = N.i64(np.concatenate(partition.rows))
+        lo, hi = N.i64(partition.vol_lo), N.i64(partition.vol_hi)
+        desc = N.ScanDesc((ctypes.c_int64 * 3)(*g.dims), (ctypes.c_double * 3)(*g.voxel_size),
+                          (ctypes.c_double * 3)(*g.origin), det.pixel_counts[0],
+                          det.pixel_counts[1], det.pixel_spacing[0], det.pixel_spacing[1],
+                          geometry.n_views, N.ptr(poses), m, nc, N.ptr(rb_ptr), N.ptr(rb_rows),
+                          N.ptr(lo), N.ptr(hi), N.ptr(vals), N.ptr(totals), pb, pe,
+                          _dtype_code(dtype), device)
+        out = ctypes.c_void_p()
+        code = L.bct_create_scan(ctypes.byref(desc), ctypes.byref(out))
+        if code == N.BCT_EINVAL:
+            msg = L.bct_last_error(None).decode(errors="replace")
+            if "inside" in msg or "degenerate" in msg:
+                raise GeometryError(f"bct_create_scan: {msg}")
+        N.check(code, None, "bct_create_scan")
+        return cls(out.value, partition.rows, partition.vidx, ProbabilityTable(vals, totals),
+                   geometry.n_measurements, g.n_voxels, dtype, (pb, pe), device)
 
     def close(self):
         if self._ctx is not None and self._ctx.value:
