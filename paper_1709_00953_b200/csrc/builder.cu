@@ -532,12 +532,24 @@ __device__ double row_dot(const PanelDev &P, int64_t lr, const double *xj)
         for (int k = 0; k < ns; ++k)
             if (cur[k] < len[k]) gmin = min(gmin, P.d2c[base[k] + swz_idx(P.fidx[pos(k)], P.swz_shift)] / P.mdiv);
         if (gmin == INT_MAX) break;
-        for (int k = 0; k < ns; ++k)
-            while (cur[k] < len[k] && P.d2c[base[k] + swz_idx(P.fidx[pos(k)], P.swz_shift)] / P.mdiv == gmin) {
-                const int64_t ps = pos(k);
+        // a segment's run of equal c / mdiv is stored ascending, or descending
+        // when the step-coded layout keeps it in walk order (layout.cu fcode_k)
+        auto col = [&](int k, int e) {
+            const int64_t ps = sb[k] + ((int64_t)(e >> 2) * 32 + lane[k]) * 4 + (e & 3);
+            return P.d2c[base[k] + swz_idx(P.fidx[ps], P.swz_shift)];
+        };
+        for (int k = 0; k < ns; ++k) {
+            int e1 = cur[k];
+            while (e1 < len[k] && col(k, e1) / P.mdiv == gmin) ++e1;
+            const int e0 = cur[k];
+            const bool down = e1 - e0 >= 2 && col(k, e0) > col(k, e0 + 1);
+            for (int u = 0; u < e1 - e0; ++u) {
+                const int e = down ? e1 - 1 - u : e0 + u;
+                const int64_t ps = sb[k] + ((int64_t)(e >> 2) * 32 + lane[k]) * 4 + (e & 3);
                 acc = __dadd_rn(acc, __dmul_rn((double)fv[ps], xj[base[k] + swz_idx(P.fidx[ps], P.swz_shift)]));
-                ++cur[k];
             }
+            cur[k] = e1;
+        }
     }
     return acc;
 }

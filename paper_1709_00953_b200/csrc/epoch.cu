@@ -208,6 +208,9 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
 #ifndef BCT_B_HINT
 #define BCT_B_HINT 1
 #endif
+#ifndef BCT_NO_FCODE_K
+#define BCT_NO_FCODE_K 0         // 1: phase B ignores the step codes (profiling)
+#endif
 #ifndef BCT_STREAM_HINT_F64
 #define BCT_STREAM_HINT_F64 1    // f64 values (serial configs): the hint helps
 #endif
@@ -321,6 +324,79 @@ __device__ __forceinline__ void ld4u16(const uint16_t *p, int k[4])
     uint2 a = ld_stream(reinterpret_cast<const uint2 *>(p));
 #endif
     k[0] = a.x & 0xffff; k[1] = a.x >> 16; k[2] = a.y & 0xffff; k[3] = a.y >> 16;
+}
+
+__device__ __forceinline__ uint32_t ld_code(const uint32_t *p)
+{
+#if BCT_B_HINT
+    uint32_t a;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(a) : "l"(p), "l"(evict_first_policy()));
+    return a;
+#else
+    return __ldg(p);
+#endif
+}
+
+// One SELL lane's (t, ax) partial over a step-coded segment (layout.cu
+// fcode_k): the voxel index of every entry is the previous one moved by
+// code 0 / 1 / 2 / 3 -> 0 / s / w / w + s.  All value loads of a 4-vector
+// group are issued before the gathers (memory-level parallelism).
+__device__ __forceinline__ void coded_decode4(uint32_t byte, int &q, int sy, int wst, int shift,
+                                              int cc[4])
+{
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int code = (byte >> (2 * e)) & 3;
+        q += ((code & 1) ? sy : 0) + (code >> 1) * wst;
+        cc[e] = swz_idx(q, shift);
+    }
+}
+
+template <typename V, typename GS>
+__device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv, int sl, int base,
+                                                 int nvec, int lane, int wst, const GS *gs)
+{
+    const int hdr = __ldg(P.fq0 + (int64_t)sl * 32 + lane);
+    const int sy = (hdr >> 16) & 1 ? -1 : 1;
+    const int shift = P.swz_shift;
+    int q = hdr & 0xffff;
+    const uint32_t *cw = P.fcode + (base >> 4) + 24 * sl + lane;
+    double t = 0.0, ax = 0.0;
+    // the code word of the next 4-vector group is loaded one group ahead
+    uint32_t word = nvec > 0 ? ld_code(cw) : 0u;
+    int kv4 = 0;
+    for (; kv4 + 4 <= nvec; kv4 += 4) {
+        const uint32_t wnext = kv4 + 4 < nvec ? ld_code(cw + ((kv4 >> 2) + 1) * 32) : 0u;
+        double v[4][4];
+        int cc[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ld4v(fv + base + (((kv4 + j) * 32 + lane) << 2), v[j]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) coded_decode4(word >> (8 * j), q, sy, wst, shift, cc[j]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const GS a = gs[cc[j][e]];
+                t = fma(v[j][e], (double)a.x, t);
+                ax = fma(v[j][e], (double)a.y, ax);
+            }
+        word = wnext;
+    }
+    for (int j = 0; kv4 + j < nvec; ++j) {
+        double v[4];
+        int cc[4];
+        ld4v(fv + base + (((kv4 + j) * 32 + lane) << 2), v);
+        coded_decode4(word >> (8 * j), q, sy, wst, shift, cc);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const GS a = gs[cc[e]];
+            t = fma(v[e], (double)a.x, t);
+            ax = fma(v[e], (double)a.y, ax);
+        }
+    }
+    return make_double2(t, ax);
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p)
@@ -855,6 +931,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const bool replay = P.rp_meta != nullptr && !BCT_NO_REPLAY_K;
             const int y0 = st * P.st_w;
             const int wid = P.pb_x1 > P.pb_x0 ? (v1 - v0) / (P.pb_x1 - P.pb_x0) : 1;
+            const int wst = P.st_h > 0 ? (v1 - v0) / P.st_h : 1;   // step-coded row length
             // slices are taken one at a time from a shared counter: their
             // lengths vary (up to seg_cap/4 vectors), so a static round robin
             // leaves warps idle at the super tile's barrier
@@ -871,6 +948,14 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                 }
                 const int base = __ldg(P.slice_start + sl);
                 const int nvec = (__ldg(P.slice_start + sl + 1) - base) >> 7;
+                // step-coded slices; a slice with a lane that keeps its 16-bit
+                // indices (fq0 bit 17, rare) takes the indexed loop below
+                if (P.fcode != nullptr && !BCT_NO_FCODE_K &&
+                    !__any_sync(0xffffffffu, (__ldg(P.fq0 + (int64_t)sl * 32 + lane) >> 17) & 1)) {
+                    spart[(int64_t)sl * 32 + lane] =
+                        coded_segment<V, GS>(P, fv, sl, base, nvec, lane, wst, gs);
+                    continue;
+                }
                 double t = 0.0, ax = 0.0;
 #pragma unroll P2U
                 for (int kv = 0; kv < nvec; ++kv) {

@@ -72,6 +72,14 @@ struct PanelDev {
     int32_t pb_x0, pb_x1;      // strip rows [x0, x1)
     int32_t st_w;              // super tile row length (voxels per strip row)
     int32_t seg_cap;           // set-up input: max entries per forward segment (0: 64)
+    // step-coded voxel indices of the forward store (strip panels; phase B):
+    // a segment's entries are stored in walk order, so each entry is its
+    // predecessor moved by one of {0, s, w, w + s} (s = +-1 the row step, w =
+    // the super tile's row length): 2 bits per entry instead of 16
+    const uint32_t *fcode;     // word (slice_start[sl]/16 + 24*sl) + (k/4)*32 + lane holds
+                               // vectors k..k+3 of the lane, a byte per vector
+    const int32_t *fq0;        // per SELL slot: first voxel (logical) | (s < 0) << 16
+    int32_t st_h;              // set-up input: strip height (0: generic placement)
 };
 
 struct TaskDev {

@@ -29,6 +29,7 @@
 // segments in tile order, so the bitwise set-up kernels (builder.cu) recover
 // the reference's summation order by merging a row's segments by column.
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
@@ -224,6 +225,97 @@ __global__ void sell_pad_k(const int32_t *sl_seg, const int32_t *seg_len, const 
         int64_t pos = base + ((e >> 2) * 32 + lane) * 4 + (e & 3);
         fvals[pos] = (V)0;
         fidx[pos] = last;
+    }
+}
+
+// Step codes of the forward store (strip panels).  A segment is one ray's run
+// through a super tile; its entries arrive sorted by (ix, iy).  The ray walks
+// monotonically, so the runs of equal ix are contiguous, adjacent, and all go
+// the same way in iy.  Reversing every run when the ray goes down in iy puts
+// the entries in walk order (ix ascending), where each entry is its
+// predecessor moved by 0 (first entry / padding), s (row step), w (next strip
+// row) or w + s (through a corner: the zero-length voxel is not stored).
+// Phase B then reads 2 bits per entry instead of a 16-bit index.  A segment
+// that does not fit (a capped run cut inside a descending ix run) is flagged
+// in fq0 (bit 17) and read through its 16-bit indices; *bad counts them.
+template <typename V>
+__global__ void fcode_k(const int32_t *seg_key, const int32_t *seg_len, const int32_t *seg_slice,
+                        const int32_t *seg_lane, const int32_t *slice_start,
+                        const int32_t *st_ptr, int32_t n_seg, int32_t n_rows, int32_t h,
+                        int swz_shift, V *fvals, uint16_t *fidx, uint32_t *fcode, int32_t *fq0,
+                        int *bad)
+{
+    const int sg = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sg >= n_seg) return;
+    const int st = seg_key[sg] / n_rows, K = seg_len[sg];
+    const int w = (st_ptr[st + 1] - st_ptr[st]) / h;
+    const int sl = seg_slice[sg], lane = seg_lane[sg];
+    const int64_t base = slice_start[sl];
+    auto pos = [&](int e) { return base + ((int64_t)(e >> 2) * 32 + lane) * 4 + (e & 3); };
+    auto qat = [&](int e) { return swz_idx(fidx[pos(e)], swz_shift); };
+    // row direction: first pair of adjacent ix runs that tells it apart
+    int s = 1;
+    {
+        int e = 0, prev_lo = -1, prev_hi = -1;
+        while (e < K) {
+            const int ix = qat(e) / w;
+            int f = e;
+            while (f + 1 < K && qat(f + 1) / w == ix) ++f;
+            const int lo = qat(e) % w, hi = qat(f) % w;
+            if (prev_lo >= 0 && !(lo == hi && prev_lo == prev_hi && lo == prev_lo)) {
+                s = lo >= prev_hi ? 1 : -1;
+                break;
+            }
+            prev_lo = lo;
+            prev_hi = hi;
+            e = f + 1;
+        }
+    }
+    if (s < 0) {   // reverse every run of equal ix
+        int e = 0;
+        while (e < K) {
+            const int ix = qat(e) / w;
+            int f = e;
+            while (f + 1 < K && qat(f + 1) / w == ix) ++f;
+            for (int a = e, b = f; a < b; ++a, --b) {
+                const int64_t pa = pos(a), pb = pos(b);
+                const V tv = fvals[pa]; fvals[pa] = fvals[pb]; fvals[pb] = tv;
+                const uint16_t ti = fidx[pa]; fidx[pa] = fidx[pb]; fidx[pb] = ti;
+            }
+            e = f + 1;
+        }
+    }
+    // codes; padding entries (value 0, the lane's last voxel) keep code 0
+    auto code_of = [&](int qp, int qn) {
+        const int d = qn - qp;
+        if (d == s && qn / w == qp / w) return 1;
+        if (d == w) return 2;
+        if (d == w + s && qn / w == qp / w + 1) return 3;
+        return -1;
+    };
+    bool ok = true;
+    for (int e = 1; e < K && ok; ++e) ok = code_of(qat(e - 1), qat(e)) >= 0;
+    const int64_t slot = (int64_t)sl * 32 + lane;
+    if (!ok) {   // e.g. a capped run cut inside a descending ix run: keep the indices
+        fq0[slot] = 1 << 17;
+        atomicAdd(bad, 1);
+        return;
+    }
+    const int64_t wbase = slice_start[sl] / 16 + 24ll * sl;
+    const int nvec = (slice_start[sl + 1] - slice_start[sl]) >> 7;
+    int q = K > 0 ? qat(0) : 0;
+    fq0[slot] = q | (s < 0 ? 1 << 16 : 0);
+    for (int kv4 = 0; kv4 < nvec; kv4 += 4) {
+        uint32_t word = 0;
+        for (int j = 0; j < 4; ++j)
+            for (int e4 = 0; e4 < 4; ++e4) {
+                const int e = (kv4 + j) * 4 + e4;
+                if (e == 0 || e >= K) continue;
+                const int qn = qat(e);
+                word |= (uint32_t)code_of(q, qn) << (8 * j + 2 * e4);
+                q = qn;
+            }
+        fcode[wbase + (int64_t)(kv4 >> 2) * 32 + lane] = word;
     }
 }
 
@@ -776,6 +868,32 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
                 slice_start, n_slices, (float *)fvals, fidx);
         }
     }
+    // step codes of strip panels (phase B); BCT_NO_FCODE keeps the indices
+    uint32_t *fcode = nullptr;
+    int32_t *fq0 = nullptr;
+    if (P.st_h > 0 && n_seg > 0 && !getenv("BCT_NO_FCODE")) {
+        const int64_t n_words = fwd_cap / 16 + 24ll * n_slices + 32;
+        uint32_t *fc = K.get<uint32_t>(n_words);
+        int32_t *fq = K.get<int32_t>((int64_t)n_slices * 32 + 1);
+        int *bad = T.get<int>(1);
+        LNN(fc); LNN(fq); LNN(bad);
+        LCK(cudaMemsetAsync(fc, 0, 4 * n_words, s));
+        LCK(cudaMemsetAsync(fq, 0, 4 * ((int64_t)n_slices * 32 + 1), s));
+        LCK(cudaMemsetAsync(bad, 0, 4, s));
+        if (dtype == 0)
+            fcode_k<double><<<nb(n_seg, 128), 128, 0, s>>>(seg_key, seg_len, seg_slice, seg_lane,
+                slice_start, st_ptr, n_seg, n_rows, P.st_h, P.swz_shift, (double *)fvals, fidx,
+                fc, fq, bad);
+        else
+            fcode_k<float><<<nb(n_seg, 128), 128, 0, s>>>(seg_key, seg_len, seg_slice, seg_lane,
+                slice_start, st_ptr, n_seg, n_rows, P.st_h, P.swz_shift, (float *)fvals, fidx,
+                fc, fq, bad);
+        LCK(cudaGetLastError());
+        fcode = fc;
+        fq0 = fq;
+        if (getenv("BCT_VERBOSE"))
+            fprintf(stderr, "fcode: %d of %d segments keep indices\n", read1(bad, s), n_seg);
+    }
     stbs_k<<<nb((int64_t)n_st * (m + 1), 128), 128, 0, s>>>(slice_gid, n_slices, m, n_st, stbs);
     // rows -> segments (tile order)
     int32_t *rkey = T.get<int32_t>(n_seg + 1), *srkey = T.get<int32_t>(n_seg + 1);
@@ -936,6 +1054,8 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     P.tbase = tbase;
     P.fvals = fvals;
     P.fidx = fidx;
+    P.fcode = fcode;
+    P.fq0 = fq0;
     P.slice_start = slice_start;
     P.sl_seg = sl_seg;
     P.stbs = stbs;
