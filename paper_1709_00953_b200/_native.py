@@ -109,7 +109,7 @@ def load(path=LIB_PATH):
     if _LIB is not None:
         return _LIB
     # profiling: BCT_LIB selects a variant build (tools/build_variant.sh)
-    path = os.environ.get("BCT_LIB", path)
+    path = os.environ.get("BCT_LIB") or path
     if not os.path.exists(path):
         raise NativeLibraryError(
             f"{path} is missing; build it with `python -c 'import __graft_entry__ as g; "

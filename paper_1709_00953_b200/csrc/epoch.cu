@@ -357,6 +357,7 @@ template <typename V, typename GS>
 __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv, int sl, int base,
                                                  int nvec, int lane, int wst, const GS *gs)
 {
+
     const int hdr = __ldg(P.fq0 + (int64_t)sl * 32 + lane);
     const int sy = (hdr >> 16) & 1 ? -1 : 1;
     const int shift = P.swz_shift;
