@@ -104,6 +104,7 @@ struct bct_ctx {
     int32_t *inv_ptr = nullptr, *inv_z = nullptr, *d_rb_ptr = nullptr, *d_rb_rows = nullptr;
     int32_t *rb_of_row = nullptr;
     double *y = nullptr, *r = nullptr, *z = nullptr, *x = nullptr, *xhat = nullptr;
+    float *r32 = nullptr;   // FP32 mode: band staging copy of r (epoch kernel)
     double *x_true = nullptr;
     int32_t *counts = nullptr;
     double *gx = nullptr, *t_ax = nullptr, *seg_part = nullptr, *part = nullptr;
@@ -434,6 +435,10 @@ int finalize(bct_ctx *c)
     // state and scratch
     DALLOC(c->y, c->n_meas);
     DALLOC(c->r, c->n_meas + 2);   // + 16-byte bulk-copy overhang (epoch.cu band staging)
+    if (c->dtype == BCT_F32) {
+        DALLOC(c->r32, c->n_meas + 4);
+        CK(cudaMemsetAsync(c->r32, 0, 4 * (c->n_meas + 4), c->stream));
+    }
     DALLOC(c->vec, c->n_meas + 2);
     DALLOC(c->exchange, c->n_meas + 2);
     DALLOC(c->z, c->z_len);
@@ -1319,7 +1324,7 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
     p.panels = c->d_panels;
     p.n_panels_owned = c->np; p.m = c->m; p.n_meas = c->n_meas; p.z_len = c->z_len;
     p.x_len = c->x_len; p.inv_ptr = c->inv_ptr; p.inv_z = c->inv_z; p.rb_ptr = c->d_rb_ptr;
-    p.rb_rows = c->d_rb_rows; p.rb_of_row = c->rb_of_row; p.y = c->y; p.r = c->r; p.z = c->z;
+    p.rb_rows = c->d_rb_rows; p.rb_of_row = c->rb_of_row; p.y = c->y; p.r = c->r; p.r32 = c->r32; p.z = c->z;
     p.x = c->x; p.xhat = c->xhat; p.counts = c->counts;
     p.x_true = c->has_x_true ? c->x_true : nullptr;
     p.hdr = c->d_hdr; p.tasks = c->d_tasks; p.gx = c->gx; p.gx_stride = 2 * c->max_cols;

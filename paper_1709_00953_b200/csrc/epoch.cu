@@ -208,6 +208,9 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
 #ifndef BCT_B_HINT
 #define BCT_B_HINT 1
 #endif
+#ifndef BCT_B_PREFETCH
+#define BCT_B_PREFETCH 0         // >0: phase B prefetches slice f+N into L2 (profiling)
+#endif
 #ifndef BCT_NO_FCODE_K
 #define BCT_NO_FCODE_K 0         // 1: phase B ignores the step codes (profiling)
 #endif
@@ -326,6 +329,12 @@ __device__ __forceinline__ void ld4u16(const uint16_t *p, int k[4])
     k[0] = a.x & 0xffff; k[1] = a.x >> 16; k[2] = a.y & 0xffff; k[3] = a.y >> 16;
 }
 
+// L2 prefetch of a byte range (one bulk request; 16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ uint32_t ld_code(const uint32_t *p)
 {
 #if BCT_B_HINT
@@ -353,26 +362,43 @@ __device__ __forceinline__ void coded_decode4(uint32_t byte, int &q, int sy, int
     }
 }
 
+// Raw 4-vector of stored values (no conversion): FP32 products in FP32 mode.
+__device__ __forceinline__ void ld4raw(const float *p, float v[4])
+{
+#if BCT_B_HINT
+    float4 a;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(p), "l"(evict_first_policy()));
+#else
+    const float4 a = __ldg(reinterpret_cast<const float4 *>(p));
+#endif
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
+__device__ __forceinline__ void ld4raw(const double *p, double v[4]) { ld4v(p, v); }
+
+// FP32 mode accumulates a lane's segment in FP32 (north_star: FP32 mode
+// matches the reference's residual curve to 1e-4); rows sum the segment
+// partials in FP64 (phase C).  FP64 mode is FP64 throughout.
 template <typename V, typename GS>
 __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv, int sl, int base,
                                                  int nvec, int lane, int wst, const GS *gs)
 {
-
+    using A = V;
     const int hdr = __ldg(P.fq0 + (int64_t)sl * 32 + lane);
     const int sy = (hdr >> 16) & 1 ? -1 : 1;
     const int shift = P.swz_shift;
     int q = hdr & 0xffff;
     const uint32_t *cw = P.fcode + (base >> 4) + 24 * sl + lane;
-    double t = 0.0, ax = 0.0;
+    A t = A(0), ax = A(0);
     // the code word of the next 4-vector group is loaded one group ahead
     uint32_t word = nvec > 0 ? ld_code(cw) : 0u;
     int kv4 = 0;
     for (; kv4 + 4 <= nvec; kv4 += 4) {
         const uint32_t wnext = kv4 + 4 < nvec ? ld_code(cw + ((kv4 >> 2) + 1) * 32) : 0u;
-        double v[4][4];
+        V v[4][4];
         int cc[4][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ld4v(fv + base + (((kv4 + j) * 32 + lane) << 2), v[j]);
+        for (int j = 0; j < 4; ++j) ld4raw(fv + base + (((kv4 + j) * 32 + lane) << 2), v[j]);
 #pragma unroll
         for (int j = 0; j < 4; ++j) coded_decode4(word >> (8 * j), q, sy, wst, shift, cc[j]);
 #pragma unroll
@@ -380,24 +406,24 @@ __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv,
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const GS a = gs[cc[j][e]];
-                t = fma(v[j][e], (double)a.x, t);
-                ax = fma(v[j][e], (double)a.y, ax);
+                t = fma(v[j][e], (A)a.x, t);
+                ax = fma(v[j][e], (A)a.y, ax);
             }
         word = wnext;
     }
     for (int j = 0; kv4 + j < nvec; ++j) {
-        double v[4];
+        V v[4];
         int cc[4];
-        ld4v(fv + base + (((kv4 + j) * 32 + lane) << 2), v);
+        ld4raw(fv + base + (((kv4 + j) * 32 + lane) << 2), v);
         coded_decode4(word >> (8 * j), q, sy, wst, shift, cc);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const GS a = gs[cc[e]];
-            t = fma(v[e], (double)a.x, t);
-            ax = fma(v[e], (double)a.y, ax);
+            t = fma(v[e], (A)a.x, t);
+            ax = fma(v[e], (A)a.y, ax);
         }
     }
-    return make_double2(t, ax);
+    return make_double2((double)t, (double)ax);
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p)
@@ -448,8 +474,9 @@ __device__ __forceinline__ void band_meta_load(const PanelDev &P, int t, BandMet
 
 // Caller guarantees every read of buf is ordered before this call by a CTA
 // barrier; completion: cp.async.wait_group 0 + a CTA barrier.
-__device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm, const double *r,
-                                           double *buf, const uint64_t *mask)
+template <typename TB>
+__device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm, const TB *r,
+                                           TB *buf, const uint64_t *mask)
 {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sub = lane >> 3, sl = lane & 7;
@@ -466,13 +493,18 @@ __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm
             if (q0 + src < bm.k1 && BCT_EXP != 5) {
                 const int pre = (int)((unsigned)pk >> 16), len = pk & 0xffff;
                 const int ng = ((g0 & 1) + len + 1) >> 1;
-                const double *rs = r + (g0 & ~1);
-                double *dst = buf + pre;
+                const TB *rs = r + (g0 & ~1);
+                TB *dst = buf + pre;
                 if (keep) {
-                    for (int e = sl; e < ng; e += 8) cp_async16(dst + 2 * e, rs + 2 * e);
+                    for (int e = sl; e < ng; e += 8) {
+                        if (sizeof(TB) == 8) cp_async16(dst + 2 * e, rs + 2 * e);
+                        else cp_async8(dst + 2 * e, rs + 2 * e);
+                    }
                 } else {
-                    for (int e = sl; e < ng; e += 8)
-                        *reinterpret_cast<double2 *>(dst + 2 * e) = make_double2(0.0, 0.0);
+                    for (int e = sl; e < ng; e += 8) {
+                        dst[2 * e] = TB(0);
+                        dst[2 * e + 1] = TB(0);
+                    }
                 }
             }
         }
@@ -483,7 +515,7 @@ __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm
         const int pre = (int)((unsigned)mm.y >> 16), len = mm.y & 0xffff;
         const bool keep = mask == nullptr || mask_has(mask, __ldg(P.band_rb + q));
         const int off = mm.x & 1;
-        for (int e = 0; e < len; ++e) buf[pre + off + e] = keep ? r[mm.x + e] : 0.0;
+        for (int e = 0; e < len; ++e) buf[pre + off + e] = keep ? r[mm.x + e] : TB(0);
     }
     cp_async_commit();
 }
@@ -500,9 +532,9 @@ __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm
 constexpr int RED_DOUBLES = WARPS * 32;         // partials: (WARPS/ns) x (32*ns)
 static_assert(2 * RED_DOUBLES * 8 == bct::PHASE1_RED_BYTES, "reduction areas");
 
-template <typename V>
+template <typename V, typename TB = double>
 __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int sl1,
-                                         const double *bt, const double *xj, double2 *gx,
+                                         const TB *bt, const double *xj, double2 *gx,
                                          double *red, const int2 *vr)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -533,7 +565,36 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
         if (BCT_EXP == 6) hi = lo;   // profiling: staging and structure only
         double acc = 0.0;
         const uint8_t *toff = P.toff;
-        if (toff != nullptr) {   // delta form: 8-bit offsets on a 16-bit base
+        if (sizeof(TB) == 4 && sizeof(V) == 4) {
+            // FP32 mode, batched path: FP32 products and lane partial sums
+            // (north_star: FP32 mode matches the reference curve to 1e-4);
+            // the partials meet in FP64 below
+            float acc32 = 0.f;
+            const uint16_t *tbase = P.tbase;
+            const uint16_t *tloc = P.tloc;
+#pragma unroll P1U
+            for (int u = lo + sub; u < hi; u += wps) {
+                const int i = base + u * 256 + lane * 8;
+                const float4 a0 = ld_stream(reinterpret_cast<const float4 *>(tv + i));
+                const float4 a1 = ld_stream(reinterpret_cast<const float4 *>(tv + i) + 1);
+                const float vf[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                int loc[8];
+                if (toff != nullptr) {
+                    const uint2 o = ld_stream(reinterpret_cast<const uint2 *>(toff + i));
+                    const int b0 = __ldg(tbase + (i >> 3));
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        loc[e] = b0 + ((o.x >> (8 * e)) & 0xff);
+                        loc[4 + e] = b0 + ((o.y >> (8 * e)) & 0xff);
+                    }
+                } else {
+                    ld8u16(tloc + i, loc);
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc32 = fmaf(vf[e], (float)bt[loc[e]], acc32);
+            }
+            acc = acc32;
+        } else if (toff != nullptr) {   // delta form: 8-bit offsets on a 16-bit base
             const uint16_t *tbase = P.tbase;
 #pragma unroll P1U
             for (int u = lo + sub; u < hi; u += wps) {
@@ -544,10 +605,10 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
                 ld8v(tv + i, v);
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    acc = fma(v[e], bt[b0 + ((o.x >> (8 * e)) & 0xff)], acc);
+                    acc = fma(v[e], (double)bt[b0 + ((o.x >> (8 * e)) & 0xff)], acc);
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    acc = fma(v[4 + e], bt[b0 + ((o.y >> (8 * e)) & 0xff)], acc);
+                    acc = fma(v[4 + e], (double)bt[b0 + ((o.y >> (8 * e)) & 0xff)], acc);
             }
         } else {
             const uint16_t *tloc = P.tloc;
@@ -560,7 +621,7 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
                 ld8v(tv + i, v);
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
-                    acc = fma(v[e], BCT_EXP == 7 ? (double)loc[e] : bt[loc[e]], acc);
+                    acc = fma(v[e], BCT_EXP == 7 ? (double)loc[e] : (double)bt[loc[e]], acc);
             }
         }
         red[sub * (ns * 32) + si * 32 + lane] = acc;
@@ -785,6 +846,18 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     // One CTA barrier per tile: the band of tile it+1 streams in (bulk
     // copies, mbarrier) while tile it is computed; the reduction area is
     // double-buffered by tile parity.  gg partials per (task, CTA, warp).
+    // FP32 mode: the bands are staged from an FP32 copy of the epoch-start r
+    // (half the staging bytes and single-wavefront gathers)
+    using TB = typename std::conditional<sizeof(V) == 4, float, double>::type;
+    const TB *rband;
+    if constexpr (sizeof(V) == 4) {
+        for (int64_t i = (int64_t)b * BLOCK + threadIdx.x; i < p.n_meas; i += (int64_t)G * BLOCK)
+            p.r32[i] = (float)p.r[i];
+        grid_sync(p.bar);
+        rband = p.r32;
+    } else {
+        rband = p.r;
+    }
     for (int k = threadIdx.x; k < n_tasks; k += BLOCK) {
         s_tpre[k] = p.tasks[k].tile_pre;
         s_lp[k] = p.tasks[k].lp;
@@ -800,9 +873,10 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
         const int full = hdr.n_tiles_total / G, rem = hdr.n_tiles_total - full * G;
         const int nsplit = rem > 0 ? max(1, min(8, G / rem)) : 1;
         const int n_items = full + (bb < rem * nsplit ? 1 : 0);
-        const bool dbuf = p.band_dbuf != 0;
-        double *buf[2] = {rs, rs + (dbuf ? p.band_cap : 0)};
-        double *red = rs + (int64_t)p.band_cap * (dbuf ? 2 : 1);
+        // FP32 bands: two buffers fit in one FP64 band's space
+        const bool dbuf = sizeof(TB) == 4 || p.band_dbuf != 0;
+        TB *buf[2] = {reinterpret_cast<TB *>(rs), reinterpret_cast<TB *>(rs) + (dbuf ? p.band_cap : 0)};
+        double *red = rs + (int64_t)p.band_cap * (sizeof(TB) == 4 ? 1 : (dbuf ? 2 : 1));
         auto ring_issue = [&](int it) {   // warp 0
             const int item = it < full ? bb + it * G : full * G + bb / nsplit;
             int lo = 0, hi = n_tasks - 1;  // last task with tile_pre <= item
@@ -832,7 +906,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
         __syncthreads();
         if (n_items > 0) {
             band_meta_load(ring[0].P, ring[0].t, bm, nullptr);
-            band_issue(ring[0].P, bm, p.r, buf[0], nullptr);
+            band_issue(ring[0].P, bm, rband, buf[0], nullptr);
             if (n_items > 1) band_meta_load(ring[1].P, ring[1].t, bm, nullptr);
         }
         double wacc = 0.0;
@@ -845,10 +919,10 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const RingSlot &S = ring[it % RING];
             // the other buffer was last read by tile it-1 (before its barrier)
             if (dbuf && it + 1 < n_items)
-                band_issue(ring[(it + 1) % RING].P, bm, p.r, buf[cb ^ 1], nullptr);
+                band_issue(ring[(it + 1) % RING].P, bm, rband, buf[cb ^ 1], nullptr);
             if (warp == 0 && it + 2 < n_items) ring_issue(it + 2);
             const int nsl = S.P.tile_cols >> 5;
-            const double wsum = tile_g<V>(S.P, S.t, S.part * nsl / S.nparts,
+            const double wsum = tile_g<V, TB>(S.P, S.t, S.part * nsl / S.nparts,
                                           (S.part + 1) * nsl / S.nparts, buf[cb],
                                           p.x + S.P.x_off, gxb + S.gx_off,
                                           red + (it & 1) * RED_DOUBLES, nullptr);
@@ -861,7 +935,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                 wacc = 0.0;
             }
             if (!dbuf && it + 1 < n_items)
-                band_issue(ring[(it + 1) % RING].P, bm, p.r, buf[0], nullptr);
+                band_issue(ring[(it + 1) % RING].P, bm, rband, buf[0], nullptr);
             if (it + 2 < n_items)
                 band_meta_load(ring[(it + 2) % RING].P, ring[(it + 2) % RING].t, bm, nullptr);
         }
@@ -942,6 +1016,12 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                 f = __shfl_sync(0xffffffffu, f, 0);
                 if (f >= ge) break;
                 const int sl = f - T.slice_pre;
+                if (BCT_B_PREFETCH > 0 && lane == 0 && f + BCT_B_PREFETCH < ge) {
+                    // the slice another warp takes next round: into L2 now
+                    const int sp = sl + BCT_B_PREFETCH;
+                    const int e0 = __ldg(P.slice_start + sp), e1 = __ldg(P.slice_start + sp + 1);
+                    prefetch_l2(fv + e0, (uint32_t)(e1 - e0) * (uint32_t)sizeof(V));
+                }
                 if (replay) {
                     spart[(int64_t)sl * 32 + lane] =
                         replay_segment<V, GS>(P, (int64_t)sl * 32 + lane, gs, y0, wid);
@@ -957,22 +1037,22 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                         coded_segment<V, GS>(P, fv, sl, base, nvec, lane, wst, gs);
                     continue;
                 }
-                double t = 0.0, ax = 0.0;
+                V t = V(0), ax = V(0);   // FP32 mode: FP32 lane partials (see coded_segment)
 #pragma unroll P2U
                 for (int kv = 0; kv < nvec; ++kv) {
                     const int i = base + ((kv * 32 + lane) << 2);
                     int cc[4];
-                    double v[4];
+                    V v[4];
                     ld4u16(P.fidx + i, cc);
-                    ld4v(fv + i, v);
+                    ld4raw(fv + i, v);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const GS a = gs[cc[q]];
-                        t = fma(v[q], (double)a.x, t);
-                        ax = fma(v[q], (double)a.y, ax);
+                        t = fma(v[q], (V)a.x, t);
+                        ax = fma(v[q], (V)a.y, ax);
                     }
                 }
-                spart[(int64_t)sl * 32 + lane] = make_double2(t, ax);   // SELL order
+                spart[(int64_t)sl * 32 + lane] = make_double2((double)t, (double)ax);   // SELL order
             }
             fu = ge;
         }

@@ -134,6 +134,7 @@ struct EpochParams {
     // state
     const double *y;
     double *r;
+    float *r32;                // FP32 mode: copy of r for the batched phase-A bands
     double *z;
     double *x;
     double *xhat;

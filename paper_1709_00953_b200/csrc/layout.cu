@@ -543,18 +543,22 @@ __global__ void csc_sell_pad_k(const int32_t *colstart, const int32_t *corder, i
 // vector row assigns, position by position and lane by lane, the remaining
 // entry that adds the fewest wavefronts; zero padding entries take the slot
 // another lane already reads (a broadcast).
+// FP32 mode stages FP32 bands for the batched path: one 4-byte load per
+// entry, one wavefront per warp when the 32 slots fall in distinct banks
+// (slot mod 32) -- the same greedy over the whole warp (nbank = 32).
 template <typename V>
 __global__ void csc_bank_perm_k(V *tvals, uint16_t *tloc, const int32_t *csl_start,
-                                int32_t n_cslices)
+                                int32_t n_cslices, int nbank)
 {
     constexpr int WPB = 4;
-    __shared__ int cnt_s[WPB][2][16];
-    __shared__ int first_s[WPB][2][16];
+    __shared__ int cnt_s[WPB][2][32];
+    __shared__ int first_s[WPB][2][32];
     __shared__ int any_s[WPB][2];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int gw = blockIdx.x * WPB + wib, nw = gridDim.x * WPB;
-    int *cnt = &cnt_s[wib][lane >> 4][0];
-    int *first = &first_s[wib][lane >> 4][0];
+    const int grp = nbank == 32 ? 0 : lane >> 4, bmask = nbank - 1;
+    int *cnt = &cnt_s[wib][grp][0];
+    int *first = &first_s[wib][grp][0];
     for (int sl = gw; sl < n_cslices; sl += nw) {
         const int64_t base0 = csl_start[sl];
         const int nvr = (int)((csl_start[sl + 1] - base0) >> 8);
@@ -570,10 +574,8 @@ __global__ void csc_bank_perm_k(V *tvals, uint16_t *tloc, const int32_t *csl_sta
             int oloc[8];
             unsigned left = 0xffu;
             for (int e = 0; e < 8; ++e) {
-                if (lane < 16) {
-                    cnt_s[wib][0][lane] = 0;
-                    cnt_s[wib][1][lane] = 0;
-                }
+                cnt_s[wib][0][lane] = 0;
+                cnt_s[wib][1][lane] = 0;
                 if (lane < 2) any_s[wib][lane] = -1;
                 __syncwarp();
                 for (int who = 0; who < 32; ++who) {
@@ -585,7 +587,7 @@ __global__ void csc_bank_perm_k(V *tvals, uint16_t *tloc, const int32_t *csl_sta
                                 if (pad < 0) pad = j;
                                 continue;
                             }
-                            const int b = loc[j] & 15;
+                            const int b = loc[j] & bmask;
                             const int c = (cnt[b] == 0 || first[b] == loc[j]) ? 0 : cnt[b];
                             if (c < bcost) {
                                 bcost = c;
@@ -596,17 +598,17 @@ __global__ void csc_bank_perm_k(V *tvals, uint16_t *tloc, const int32_t *csl_sta
                         int a = best >= 0 ? loc[best] : 0;
                         if (pad >= 0 && (best < 0 || bcost > 0)) {
                             pick = pad;   // a zero entry: read a slot already read
-                            const int an = any_s[wib][lane >> 4];
+                            const int an = any_s[wib][grp];
                             a = an >= 0 ? an : (best >= 0 ? loc[best] : loc[pad]);
                         }
-                        const int b = a & 15;
+                        const int b = a & bmask;
                         if (cnt[b] == 0) {
                             cnt[b] = 1;
                             first[b] = a;
                         } else if (first[b] != a) {
                             ++cnt[b];
                         }
-                        if (any_s[wib][lane >> 4] < 0) any_s[wib][lane >> 4] = a;
+                        if (any_s[wib][grp] < 0) any_s[wib][grp] = a;
                         oval[e] = val[pick];
                         oloc[e] = a;
                         left &= ~(1u << pick);
@@ -1021,9 +1023,11 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     if (!getenv("BCT_NO_BANK_PERM") && n_cslices > 0) {
         const unsigned pb = (unsigned)std::min<int64_t>((n_cslices + 3) / 4, 4096);
         if (dtype == 0)
-            csc_bank_perm_k<double><<<pb, 128, 0, s>>>((double *)tvals, tloc, csl_start, n_cslices);
+            csc_bank_perm_k<double><<<pb, 128, 0, s>>>((double *)tvals, tloc, csl_start, n_cslices,
+                                                       16);
         else
-            csc_bank_perm_k<float><<<pb, 128, 0, s>>>((float *)tvals, tloc, csl_start, n_cslices);
+            csc_bank_perm_k<float><<<pb, 128, 0, s>>>((float *)tvals, tloc, csl_start, n_cslices,
+                                                      getenv("BCT_BANK16") ? 16 : 32);
     }
     LCK(cudaGetLastError());
     // 8-bit band offsets when every lane-vector spans < 256 slots (strip tiles)
