@@ -294,7 +294,9 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
         // replayed segments must be contiguous runs of the ray's walk: whole
         // (row, super tile) runs, so no cap inside a strip (a run is at most
         // strip height + super tile width entries; K is stored in 8 bits)
-        Q.seg_cap = pl.st_w > 0 ? 255 : 0;
+        // (step-coded phase B: no cap at all, so no run is cut and every
+        // segment codes; the replay records store K in 8 bits)
+        Q.seg_cap = pl.st_w > 0 ? (replay ? 255 : 1 << 20) : 0;
         Q.st_h = pl.st_w > 0 ? (int32_t)h : 0;   // strip placement: step-coded phase B
         if (bct::layout_panel_v2(c->dtype, c->m, n_rows, n_cols, nnz, vals64, cols, indptr, l2g,
                                  d_rbp, pl.c2d, pl.st_ptr, pl.corder, th * tw, Q, kept, err,
