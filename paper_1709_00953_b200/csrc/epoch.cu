@@ -211,6 +211,9 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
 #ifndef BCT_B_PREFETCH
 #define BCT_B_PREFETCH 0         // >0: phase B prefetches slice f+N into L2 (profiling)
 #endif
+#ifndef BCT_B_SLICE_COST
+#define BCT_B_SLICE_COST 120     // phase-B balance: entries-equivalent cost of one slice
+#endif
 #ifndef BCT_NO_FCODE_K
 #define BCT_NO_FCODE_K 0         // 1: phase B ignores the step codes (profiling)
 #endif
@@ -381,10 +384,10 @@ __device__ __forceinline__ void ld4raw(const double *p, double v[4]) { ld4v(p, v
 // partials in FP64 (phase C).  FP64 mode is FP64 throughout.
 template <typename V, typename GS>
 __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv, int sl, int base,
-                                                 int nvec, int lane, int wst, const GS *gs)
+                                                 int nvec, int lane, int wst, const GS *gs,
+                                                 int hdr)
 {
     using A = V;
-    const int hdr = __ldg(P.fq0 + (int64_t)sl * 32 + lane);
     const int sy = (hdr >> 16) & 1 ? -1 : 1;
     const int shift = P.swz_shift;
     int q = hdr & 0xffff;
@@ -830,6 +833,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                               RingSlot *ring, int *s_tpre, int *s_lp)
 {
     __shared__ long long s_range_dbg[3];
+    __shared__ long long s_stage_dbg;
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int G = gridDim.x, b = blockIdx.x;
@@ -950,22 +954,27 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
         GS *gs = reinterpret_cast<GS *>(rs);
         // this CTA: the slices whose first entry lies in an equal share of the
         // epoch's stored entries (slices differ in length)
-        auto slice_at = [&](int64_t ent) -> int {
-            if (ent >= hdr.n_ent_total) return hdr.n_slices_total;
-            const int k = lower_bound_warp([&](int q) { return p.tasks[q].ent_pre; }, n_tasks,
-                                           ent + 1) - 1;
+        // cost of a slice prefix = its entries + BCT_B_SLICE_COST per slice
+        // (per-slice latency: short slices of rays across the strip cost more
+        // per entry than long ones)
+        constexpr int64_t SC = BCT_B_SLICE_COST;
+        const int64_t cost_total = hdr.n_ent_total + SC * hdr.n_slices_total;
+        auto slice_at = [&](int64_t c) -> int {
+            if (c >= cost_total) return hdr.n_slices_total;
+            const int k = lower_bound_warp([&](int q) {
+                return p.tasks[q].ent_pre + SC * p.tasks[q].slice_pre; }, n_tasks, c + 1) - 1;
             const TaskDev &T = p.tasks[k];
             const PanelDev &PP = p.panels[T.lp];
-            const int64_t local = ent - T.ent_pre;
+            const int64_t local = c - (T.ent_pre + SC * T.slice_pre);
             return T.slice_pre +
-                   lower_bound_warp([&](int q) { return PP.slice_start[q]; }, PP.n_slices,
-                                    (int32_t)local);
+                   lower_bound_warp([&](int q) { return (int64_t)PP.slice_start[q] + SC * q; },
+                                    PP.n_slices, local);
         };
         __shared__ int s_range[2];
         __shared__ int s_next;
         if (warp == 0) {
-            const int u0 = slice_at(hdr.n_ent_total * b / G);
-            const int u1 = slice_at(hdr.n_ent_total * (b + 1) / G);
+            const int u0 = slice_at(cost_total * b / G);
+            const int u1 = slice_at(cost_total * (b + 1) / G);
             if (lane == 0) {
                 s_range[0] = u0;
                 s_range[1] = u1;
@@ -975,6 +984,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
         const int ub = s_range[0], ue = s_range[1];
         int fu = ub;
         int dbg_segs = 0;   // profiling (BCT_TIMELINE): super tiles of this CTA
+        long long dbg_stage = 0;   // and their staging time
         while (fu < ue) {
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -996,11 +1006,13 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const int v0 = __ldg(P.st_ptr + st), v1 = __ldg(P.st_ptr + st + 1);
             const double2 *gx = gxb + T.gx_off;
             ++dbg_segs;
+            const long long tst0 = p.timeline ? gtimer() : 0;
             for (int q = threadIdx.x; q < v1 - v0; q += BLOCK) {
                 const double2 a = gx[v0 + q];
                 gs[swz_idx(q, P.swz_shift)] = GS{(decltype(GS::x))a.x, (decltype(GS::x))a.y};
             }
             __syncthreads();
+            if (p.timeline) dbg_stage += gtimer() - tst0;   // profiling: super-tile staging
             const V *fv = static_cast<const V *>(P.fvals);
             double2 *spart = segb + T.seg_off;
             const bool replay = P.rp_meta != nullptr && !BCT_NO_REPLAY_K;
@@ -1010,49 +1022,71 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             // slices are taken one at a time from a shared counter: their
             // lengths vary (up to seg_cap/4 vectors), so a static round robin
             // leaves warps idle at the super tile's barrier
-            for (;;) {
-                int f = 0;
-                if (lane == 0) f = atomicAdd(&s_next, 1);
-                f = __shfl_sync(0xffffffffu, f, 0);
-                if (f >= ge) break;
+            // The next slice is taken (and its metadata loaded) before the
+            // current one is processed: short slices (rays across the strip)
+            // would otherwise pay the counter, slice_start and fq0 round trips
+            // back to back before their first stream load.
+            auto grab = [&]() {
+                int g = 0;
+                if (lane == 0) g = atomicAdd(&s_next, 1);
+                return __shfl_sync(0xffffffffu, g, 0);
+            };
+            const bool coded = P.fcode != nullptr && !BCT_NO_FCODE_K;
+            int f = grab();
+            int base = 0, bend = 0, hdr = 0;
+            if (f < ge) {
                 const int sl = f - T.slice_pre;
+                base = __ldg(P.slice_start + sl);
+                bend = __ldg(P.slice_start + sl + 1);
+                if (coded) hdr = __ldg(P.fq0 + (int64_t)sl * 32 + lane);
+            }
+            while (f < ge) {
+                const int sl = f - T.slice_pre;
+                const int fn = grab();
+                int nbase = 0, nbend = 0, nhdr = 0;
+                if (fn < ge) {
+                    const int sn = fn - T.slice_pre;
+                    nbase = __ldg(P.slice_start + sn);
+                    nbend = __ldg(P.slice_start + sn + 1);
+                    if (coded) nhdr = __ldg(P.fq0 + (int64_t)sn * 32 + lane);
+                }
                 if (BCT_B_PREFETCH > 0 && lane == 0 && f + BCT_B_PREFETCH < ge) {
                     // the slice another warp takes next round: into L2 now
                     const int sp = sl + BCT_B_PREFETCH;
                     const int e0 = __ldg(P.slice_start + sp), e1 = __ldg(P.slice_start + sp + 1);
                     prefetch_l2(fv + e0, (uint32_t)(e1 - e0) * (uint32_t)sizeof(V));
                 }
+                const int nvec = (bend - base) >> 7;
                 if (replay) {
                     spart[(int64_t)sl * 32 + lane] =
                         replay_segment<V, GS>(P, (int64_t)sl * 32 + lane, gs, y0, wid);
-                    continue;
-                }
-                const int base = __ldg(P.slice_start + sl);
-                const int nvec = (__ldg(P.slice_start + sl + 1) - base) >> 7;
-                // step-coded slices; a slice with a lane that keeps its 16-bit
-                // indices (fq0 bit 17, rare) takes the indexed loop below
-                if (P.fcode != nullptr && !BCT_NO_FCODE_K &&
-                    !__any_sync(0xffffffffu, (__ldg(P.fq0 + (int64_t)sl * 32 + lane) >> 17) & 1)) {
+                } else if (coded && !__any_sync(0xffffffffu, (hdr >> 17) & 1)) {
+                    // step-coded slice (a lane flagged in fq0 bit 17 keeps its
+                    // 16-bit indices: the indexed loop below)
                     spart[(int64_t)sl * 32 + lane] =
-                        coded_segment<V, GS>(P, fv, sl, base, nvec, lane, wst, gs);
-                    continue;
-                }
-                V t = V(0), ax = V(0);   // FP32 mode: FP32 lane partials (see coded_segment)
+                        coded_segment<V, GS>(P, fv, sl, base, nvec, lane, wst, gs, hdr);
+                } else {
+                    V t = V(0), ax = V(0);   // FP32 mode: FP32 lane partials (see coded_segment)
 #pragma unroll P2U
-                for (int kv = 0; kv < nvec; ++kv) {
-                    const int i = base + ((kv * 32 + lane) << 2);
-                    int cc[4];
-                    V v[4];
-                    ld4u16(P.fidx + i, cc);
-                    ld4raw(fv + i, v);
+                    for (int kv = 0; kv < nvec; ++kv) {
+                        const int i = base + ((kv * 32 + lane) << 2);
+                        int cc[4];
+                        V v[4];
+                        ld4u16(P.fidx + i, cc);
+                        ld4raw(fv + i, v);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const GS a = gs[cc[q]];
-                        t = fma(v[q], (V)a.x, t);
-                        ax = fma(v[q], (V)a.y, ax);
+                        for (int q = 0; q < 4; ++q) {
+                            const GS a = gs[cc[q]];
+                            t = fma(v[q], (V)a.x, t);
+                            ax = fma(v[q], (V)a.y, ax);
+                        }
                     }
+                    spart[(int64_t)sl * 32 + lane] = make_double2((double)t, (double)ax);
                 }
-                spart[(int64_t)sl * 32 + lane] = make_double2((double)t, (double)ax);   // SELL order
+                f = fn;
+                base = nbase;
+                bend = nbend;
+                hdr = nhdr;
             }
             fu = ge;
         }
@@ -1060,6 +1094,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             s_range_dbg[0] = ub;
             s_range_dbg[1] = ue;
             s_range_dbg[2] = dbg_segs;
+            s_stage_dbg = dbg_stage;
         }
     }
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 3);
@@ -1067,6 +1102,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
         p.timeline[((int64_t)1 * 8 + 0) * gridDim.x + blockIdx.x] = s_range_dbg[0];
         p.timeline[((int64_t)1 * 8 + 1) * gridDim.x + blockIdx.x] = s_range_dbg[1];
         p.timeline[((int64_t)1 * 8 + 2) * gridDim.x + blockIdx.x] = s_range_dbg[2];
+        p.timeline[((int64_t)1 * 8 + 3) * gridDim.x + blockIdx.x] = s_stage_dbg;
     }
     grid_sync(p.bar);
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 4);

@@ -64,7 +64,9 @@ def main():
             q = np.percentile(d, [0, 10, 50, 90, 100])
             print(f"{name:12s} min {q[0]:6.1f} p10 {q[1]:6.1f} med {q[2]:6.1f} p90 {q[3]:6.1f} max {q[4]:6.1f}")
         if os.environ.get("DUMP_BLOCKS") and tl.shape[0] > 1:
-            ub, ue, nst = (buf[(1 * 8 + q) * G:(1 * 8 + q + 1) * G] for q in range(3))
+            ub, ue, nst, stg = (buf[(1 * 8 + q) * G:(1 * 8 + q + 1) * G] for q in range(4))
+            print("B super-tile staging per block (us):",
+                  " ".join(f"{v / 1e3:.0f}" for v in stg[:40]))
             dB = t[3] - t[2]
             order = np.argsort(dB)
             print("B slowest blocks (us, slices, super tiles):",
