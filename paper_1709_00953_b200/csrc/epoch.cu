@@ -214,6 +214,9 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
 #ifndef BCT_B_SLICE_COST
 #define BCT_B_SLICE_COST 120     // phase-B balance: entries-equivalent cost of one slice
 #endif
+#ifndef BCT_FC_G
+#define BCT_FC_G 8               // phase-B coded loop: vectors per load group (4 or 8)
+#endif
 #ifndef BCT_NO_FCODE_K
 #define BCT_NO_FCODE_K 0         // 1: phase B ignores the step codes (profiling)
 #endif
@@ -393,32 +396,35 @@ __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv,
     int q = hdr & 0xffff;
     const uint32_t *cw = P.fcode + (base >> 4) + 24 * sl + lane;
     A t = A(0), ax = A(0);
-    // the code word of the next 4-vector group is loaded one group ahead
-    uint32_t word = nvec > 0 ? ld_code(cw) : 0u;
+    // groups of FG vectors (FG/4 code words): all value loads of a group are
+    // issued before its gathers; indices are decoded just in time
+    constexpr int FG = BCT_FC_G;
     int kv4 = 0;
-    for (; kv4 + 4 <= nvec; kv4 += 4) {
-        const uint32_t wnext = kv4 + 4 < nvec ? ld_code(cw + ((kv4 >> 2) + 1) * 32) : 0u;
-        V v[4][4];
-        int cc[4][4];
+    for (; kv4 + FG <= nvec; kv4 += FG) {
+        uint32_t word[FG / 4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ld4raw(fv + base + (((kv4 + j) * 32 + lane) << 2), v[j]);
+        for (int w = 0; w < FG / 4; ++w) word[w] = ld_code(cw + ((kv4 >> 2) + w) * 32);
+        V v[FG][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) coded_decode4(word >> (8 * j), q, sy, wst, shift, cc[j]);
+        for (int j = 0; j < FG; ++j) ld4raw(fv + base + (((kv4 + j) * 32 + lane) << 2), v[j]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < FG; ++j)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const GS a = gs[cc[j][e]];
+                const int code = (word[j >> 2] >> (8 * (j & 3) + 2 * e)) & 3;
+                q += ((code & 1) ? sy : 0) + (code >> 1) * wst;
+                const GS a = gs[swz_idx(q, shift)];
                 t = fma(v[j][e], (A)a.x, t);
                 ax = fma(v[j][e], (A)a.y, ax);
             }
-        word = wnext;
     }
     for (int j = 0; kv4 + j < nvec; ++j) {
+        const int kv = kv4 + j;
+        const uint32_t word = ld_code(cw + (kv >> 2) * 32);
         V v[4];
         int cc[4];
-        ld4raw(fv + base + (((kv4 + j) * 32 + lane) << 2), v);
-        coded_decode4(word >> (8 * j), q, sy, wst, shift, cc);
+        ld4raw(fv + base + ((kv * 32 + lane) << 2), v);
+        coded_decode4(word >> (8 * (kv & 3)), q, sy, wst, shift, cc);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const GS a = gs[cc[e]];
