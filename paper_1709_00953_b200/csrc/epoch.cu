@@ -214,6 +214,9 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
 #ifndef BCT_B_SLICE_COST
 #define BCT_B_SLICE_COST 120     // phase-B balance: entries-equivalent cost of one slice
 #endif
+#ifndef BCT_P1_G
+#define BCT_P1_G 4               // phase-A FP32 loop: vector rows per load group
+#endif
 #ifndef BCT_FC_G
 #define BCT_FC_G 8               // phase-B coded loop: vectors per load group (4 or 8)
 #endif
@@ -333,6 +336,30 @@ __device__ __forceinline__ void ld4u16(const uint16_t *p, int k[4])
     uint2 a = ld_stream(reinterpret_cast<const uint2 *>(p));
 #endif
     k[0] = a.x & 0xffff; k[1] = a.x >> 16; k[2] = a.y & 0xffff; k[3] = a.y >> 16;
+}
+
+// Ordered stream load (asm volatile keeps it ahead of the gathers that follow)
+__device__ __forceinline__ float4 ldv4_ordered(const float *p)
+{
+    float4 a;
+    asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(p));
+    return a;
+}
+__device__ __forceinline__ uint2 ldu2_ordered(const void *p)
+{
+    uint2 a;
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(a.x), "=r"(a.y) : "l"(p));
+    return a;
+}
+// Band gather through a 32-bit shared-window address (the band pointer is a
+// generic pointer by the time it reaches tile_g: without this the compiler
+// emits generic 64-bit loads)
+__device__ __forceinline__ float lds_f32(uint32_t a)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
 }
 
 // L2 prefetch of a byte range (one bulk request; 16-byte aligned, size % 16 == 0)
@@ -581,26 +608,57 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
             float acc32 = 0.f;
             const uint16_t *tbase = P.tbase;
             const uint16_t *tloc = P.tloc;
-#pragma unroll P1U
-            for (int u = lo + sub; u < hi; u += wps) {
-                const int i = base + u * 256 + lane * 8;
-                const float4 a0 = ld_stream(reinterpret_cast<const float4 *>(tv + i));
-                const float4 a1 = ld_stream(reinterpret_cast<const float4 *>(tv + i) + 1);
-                const float vf[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                int loc[8];
-                if (toff != nullptr) {
-                    const uint2 o = ld_stream(reinterpret_cast<const uint2 *>(toff + i));
-                    const int b0 = __ldg(tbase + (i >> 3));
+            if (toff != nullptr) {
+                // groups of R vector rows: every stream load of the group is
+                // issued before its gathers
+                constexpr int R = BCT_P1_G;
+                const uint32_t bts = (uint32_t)__cvta_generic_to_shared(bt);
+                int u = lo + sub;
+#pragma unroll 1
+                for (; u < hi; u += R * wps) {
+                    float4 a[R][2];
+                    uint2 o[R];
+                    int b0[R];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        loc[e] = b0 + ((o.x >> (8 * e)) & 0xff);
-                        loc[4 + e] = b0 + ((o.y >> (8 * e)) & 0xff);
+                    for (int r = 0; r < R; ++r) {
+                        const bool ok = u + r * wps < hi;
+                        const int i = base + (u + r * wps) * 256 + lane * 8;
+                        if (ok) {
+                            a[r][0] = ldv4_ordered(reinterpret_cast<const float *>(tv) + i);
+                            a[r][1] = ldv4_ordered(reinterpret_cast<const float *>(tv) + i + 4);
+                            o[r] = ldu2_ordered(toff + i);
+                            b0[r] = __ldg(tbase + (i >> 3));
+                        } else {
+                            a[r][0] = a[r][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            o[r] = make_uint2(0u, 0u);
+                            b0[r] = 0;
+                        }
                     }
-                } else {
-                    ld8u16(tloc + i, loc);
-                }
 #pragma unroll
-                for (int e = 0; e < 8; ++e) acc32 = fmaf(vf[e], (float)bt[loc[e]], acc32);
+                    for (int r = 0; r < R; ++r) {
+                        const float vf[8] = {a[r][0].x, a[r][0].y, a[r][0].z, a[r][0].w,
+                                             a[r][1].x, a[r][1].y, a[r][1].z, a[r][1].w};
+                        const uint32_t bb = bts + 4u * (uint32_t)b0[r];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            acc32 = fmaf(vf[e], lds_f32(bb + 4u * ((o[r].x >> (8 * e)) & 0xff)), acc32);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            acc32 = fmaf(vf[4 + e], lds_f32(bb + 4u * ((o[r].y >> (8 * e)) & 0xff)), acc32);
+                    }
+                }
+            } else {
+#pragma unroll 1
+                for (int u = lo + sub; u < hi; u += wps) {
+                    const int i = base + u * 256 + lane * 8;
+                    const float4 a0 = ld_stream(reinterpret_cast<const float4 *>(tv + i));
+                    const float4 a1 = ld_stream(reinterpret_cast<const float4 *>(tv + i) + 1);
+                    const float vf[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    int loc[8];
+                    ld8u16(tloc + i, loc);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc32 = fmaf(vf[e], (float)bt[loc[e]], acc32);
+                }
             }
             acc = acc32;
         } else if (toff != nullptr) {   // delta form: 8-bit offsets on a 16-bit base
