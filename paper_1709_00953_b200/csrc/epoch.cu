@@ -904,8 +904,11 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     const int n_tasks = hdr.n_tasks;
     const int m = p.m;
     double2 *gxb = reinterpret_cast<double2 *>(p.gx_batch);
-    double2 *segb = reinterpret_cast<double2 *>(p.seg_batch);
-    double2 *taxb = reinterpret_cast<double2 *>(p.tax_batch);
+    // segment partials and row (t, ax) pairs: FP32 in FP32 mode (the lane
+    // partials are FP32 sums already), FP64 in FP64 mode
+    using PT = typename std::conditional<sizeof(V) == 4, float2, double2>::type;
+    PT *segb = reinterpret_cast<PT *>(p.seg_batch);
+    PT *taxb = reinterpret_cast<PT *>(p.tax_batch);
     double *pgg = p.part_task;                       // [k][G][WARPS]
     double *pden = p.part_task + (int64_t)n_tasks * G * WARPS;   // [k][G]
     double *ggs = p.part_task + (int64_t)n_tasks * G * (WARPS + 1);   // [k] reduced gg
@@ -1078,7 +1081,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             __syncthreads();
             if (p.timeline) dbg_stage += gtimer() - tst0;   // profiling: super-tile staging
             const V *fv = static_cast<const V *>(P.fvals);
-            double2 *spart = segb + T.seg_off;
+            PT *spart = segb + T.seg_off;
             const bool replay = P.rp_meta != nullptr && !BCT_NO_REPLAY_K;
             const int y0 = st * P.st_w;
             const int wid = P.pb_x1 > P.pb_x0 ? (v1 - v0) / (P.pb_x1 - P.pb_x0) : 1;
@@ -1122,13 +1125,13 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                 }
                 const int nvec = (bend - base) >> 7;
                 if (replay) {
-                    spart[(int64_t)sl * 32 + lane] =
-                        replay_segment<V, GS>(P, (int64_t)sl * 32 + lane, gs, y0, wid);
+                    const double2 rp = replay_segment<V, GS>(P, (int64_t)sl * 32 + lane, gs, y0, wid);
+                    spart[(int64_t)sl * 32 + lane] = PT{(decltype(PT::x))rp.x, (decltype(PT::x))rp.y};
                 } else if (coded && !__any_sync(0xffffffffu, (hdr >> 17) & 1)) {
                     // step-coded slice (a lane flagged in fq0 bit 17 keeps its
                     // 16-bit indices: the indexed loop below)
-                    spart[(int64_t)sl * 32 + lane] =
-                        coded_segment<V, GS>(P, fv, sl, base, nvec, lane, wst, gs, hdr);
+                    const double2 cp = coded_segment<V, GS>(P, fv, sl, base, nvec, lane, wst, gs, hdr);
+                    spart[(int64_t)sl * 32 + lane] = PT{(decltype(PT::x))cp.x, (decltype(PT::x))cp.y};
                 } else {
                     V t = V(0), ax = V(0);   // FP32 mode: FP32 lane partials (see coded_segment)
 #pragma unroll P2U
@@ -1145,7 +1148,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                             ax = fma(v[q], (V)a.y, ax);
                         }
                     }
-                    spart[(int64_t)sl * 32 + lane] = make_double2((double)t, (double)ax);
+                    spart[(int64_t)sl * 32 + lane] = PT{(decltype(PT::x))t, (decltype(PT::x))ax};
                 }
                 f = fn;
                 base = nbase;
@@ -1191,8 +1194,8 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const TaskDev &T = p.tasks[k];
             const PanelDev &P = p.panels[T.lp];
             const int f1 = min(rb1, T.row_pre + P.n_rows);
-            const double2 *spart = segb + T.seg_off;
-            double2 *tax = taxb + T.tax_off;
+            const PT *spart = segb + T.seg_off;
+            PT *tax = taxb + T.tax_off;
             double wsum = 0.0;
             // CR rows per thread at a time, their (pointer, position, partial)
             // loads issued level by level: CR-fold memory parallelism for a
@@ -1220,17 +1223,19 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                     for (int j = 0; j < CR; ++j)
                         if (pos[j] >= 0) {
                             // written in phase B of this launch: L2-coherent load
-                            const double2 a = __ldcg(spart + pos[j]);   // SELL-order partials
-                            t[j] += a.x;
-                            ax[j] += a.y;
+                            const PT a = __ldcg(spart + pos[j]);   // SELL-order partials
+                            t[j] += (double)a.x;
+                            ax[j] += (double)a.y;
                         }
                 }
 #pragma unroll
                 for (int j = 0; j < CR; ++j) {
                     const int f = fb + j * BLOCK;
                     if (f < f1) {
-                        tax[f - T.row_pre] = make_double2(t[j], ax[j]);
-                        wsum = fma(t[j], t[j], wsum);
+                        const PT tq = PT{(decltype(PT::x))t[j], (decltype(PT::x))ax[j]};
+                        tax[f - T.row_pre] = tq;
+                        // denom from the stored t (phase D's z uses the same t)
+                        wsum = fma((double)tq.x, (double)tq.x, wsum);
                     }
                 }
             }
@@ -1303,20 +1308,21 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const TaskDev &T = p.tasks[k];
             const PanelDev &P = p.panels[T.lp];
             const int f1 = min(rb1, T.row_pre + P.n_rows);
-            const double2 *tax = taxb + T.tax_off - T.row_pre;
+            const PT *tax = taxb + T.tax_off - T.row_pre;
             double *zr = p.z + P.row_off - T.row_pre;
             const double mu = mu_s[k];
             const int st = st_s[k];
             // four rows in flight per thread: loads (L2-coherent: tax was
             // written in phase C of this launch) before the stores
             for (int fb = f0 + (int)threadIdx.x; fb < f1; fb += 4 * BLOCK) {
-                double2 q[4];
+                PT q[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    q[j] = fb + j * BLOCK < f1 ? __ldcg(tax + fb + j * BLOCK) : make_double2(0.0, 0.0);
+                    q[j] = fb + j * BLOCK < f1 ? __ldcg(tax + fb + j * BLOCK) : PT{0, 0};
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    if (fb + j * BLOCK < f1) zr[fb + j * BLOCK] = z_value(q[j].x, q[j].y, mu, st);
+                    if (fb + j * BLOCK < f1)
+                        zr[fb + j * BLOCK] = z_value((double)q[j].x, (double)q[j].y, mu, st);
             }
             f0 = f1;
         }
