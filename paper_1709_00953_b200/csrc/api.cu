@@ -90,6 +90,8 @@ struct bct_ctx {
     int64_t max_rows = 0, max_cols = 0, max_seg = 0;
     int32_t *d_gvox = nullptr;     // [x_len] global voxel id of each device position
     double *d_xstage = nullptr;    // [n_vox] global-order staging of image transfers
+    char *h_pin[2] = {nullptr, nullptr};   // pinned host chunks for state transfers
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     size_t smem = 0;
     int32_t band_cap = 0, band_dbuf = 1;
     cudaStream_t stream = nullptr;
@@ -527,6 +529,10 @@ void destroy(bct_ctx *c)
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void *p : c->allocs) cudaFree(p);
+    for (int i = 0; i < 2; ++i) {
+        if (c->h_pin[i]) cudaFreeHost(c->h_pin[i]);
+        if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
+    }
     if (c->d_tasks) cudaFree(c->d_tasks);
     if (c->mus) cudaFree(c->mus);
     if (c->statuses) cudaFree(c->statuses);
@@ -1086,11 +1092,64 @@ __global__ void vox_scatter_k(const double *src, const int32_t *gvox, int64_t n,
 // Image transfers in global voxel order; the permutation runs on the device.
 // A context owning every panel moves the whole image in one copy; a shard
 // moves only its own voxels on the host side (global order untouched elsewhere).
+// Host <-> device copies of state vectors through two pinned chunks: the
+// host memcpy of chunk i+1 overlaps the DMA of chunk i (pageable copies run
+// at a few GB/s on these hosts).
+constexpr size_t PIN_CHUNK = 2u << 20;
+
+static int pin_init(bct_ctx *c)
+{
+    if (c->h_pin[0]) return 0;
+    for (int i = 0; i < 2; ++i) {
+        if (cudaMallocHost(&c->h_pin[i], PIN_CHUNK) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->pin_ev[i], cudaEventDisableTiming) != cudaSuccess)
+            return fail(c, BCT_ENOMEM, "pinned staging allocation failed");
+    }
+    return 0;
+}
+
+static int h2d_staged(bct_ctx *c, void *dst, const void *src, size_t bytes)
+{
+    if (int r = pin_init(c)) return r;
+    size_t off = 0;
+    for (int i = 0; off < bytes; ++i, off += PIN_CHUNK) {
+        const int k = i & 1;
+        const size_t n = std::min(PIN_CHUNK, bytes - off);
+        CK(cudaEventSynchronize(c->pin_ev[k]));   // the DMA that last used chunk k
+        memcpy(c->h_pin[k], static_cast<const char *>(src) + off, n);
+        CK(cudaMemcpyAsync(static_cast<char *>(dst) + off, c->h_pin[k], n,
+                           cudaMemcpyHostToDevice, c->stream));
+        CK(cudaEventRecord(c->pin_ev[k], c->stream));
+    }
+    return 0;
+}
+
+static int d2h_staged(bct_ctx *c, void *dst, const void *src, size_t bytes)
+{
+    if (int r = pin_init(c)) return r;
+    const size_t nch = (bytes + PIN_CHUNK - 1) / PIN_CHUNK;
+    auto issue = [&](size_t i) -> cudaError_t {
+        const size_t off = i * PIN_CHUNK, n = std::min(PIN_CHUNK, bytes - off);
+        cudaError_t e = cudaMemcpyAsync(c->h_pin[i & 1], static_cast<const char *>(src) + off, n,
+                                        cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaEventRecord(c->pin_ev[i & 1], c->stream);
+        return e;
+    };
+    if (nch > 0) CK(issue(0));
+    for (size_t i = 0; i < nch; ++i) {
+        if (i + 1 < nch) CK(issue(i + 1));
+        CK(cudaEventSynchronize(c->pin_ev[i & 1]));
+        const size_t off = i * PIN_CHUNK, n = std::min(PIN_CHUNK, bytes - off);
+        memcpy(static_cast<char *>(dst) + off, c->h_pin[i & 1], n);
+    }
+    return 0;
+}
+
 static int xvec_to_dev(bct_ctx *c, const double *xg, double *dst)
 {
     const unsigned nb = (unsigned)((c->x_len + 255) / 256);
     if (c->np == c->n_panels) {
-        CK(cudaMemcpyAsync(c->d_xstage, xg, 8 * c->n_vox, cudaMemcpyHostToDevice, c->stream));
+        if (int r = h2d_staged(c, c->d_xstage, xg, 8 * c->n_vox)) return r;
         if (c->x_len > 0)
             vox_gather_k<<<nb, 256, 0, c->stream>>>(c->d_xstage, c->d_gvox, c->x_len, dst);
         CK(cudaGetLastError());
@@ -1116,9 +1175,7 @@ static int xvec_from_dev(bct_ctx *c, const double *src, double *xg)
         if (c->x_len > 0)
             vox_scatter_k<<<nb, 256, 0, c->stream>>>(src, c->d_gvox, c->x_len, c->d_xstage);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(xg, c->d_xstage, 8 * c->n_vox, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        return 0;
+        return d2h_staged(c, xg, c->d_xstage, 8 * c->n_vox);
     }
     std::vector<double> buf(std::max<int64_t>(c->x_len, 1));
     CK(cudaMemcpyAsync(buf.data(), src, 8 * c->x_len, cudaMemcpyDeviceToHost, c->stream));
@@ -1135,7 +1192,7 @@ static int xvec_from_dev(bct_ctx *c, const double *src, double *xg)
 int bct_set_y(bct_ctx *c, const double *y)
 {
     if (!c || !y) return BCT_EINVAL;
-    CK(cudaMemcpyAsync(c->y, y, 8 * c->n_meas, cudaMemcpyHostToDevice, c->stream));
+    if (int r = h2d_staged(c, c->y, y, 8 * c->n_meas)) return r;
     CK(cudaStreamSynchronize(c->stream));
     return 0;
 }
@@ -1162,7 +1219,7 @@ int bct_set_x_true(bct_ctx *c, const double *xt)
 int bct_set_r(bct_ctx *c, const double *r)
 {
     if (!c || !r) return BCT_EINVAL;
-    CK(cudaMemcpyAsync(c->r, r, 8 * c->n_meas, cudaMemcpyHostToDevice, c->stream));
+    if (int e = h2d_staged(c, c->r, r, 8 * c->n_meas)) return e;
     CK(cudaStreamSynchronize(c->stream));
     return 0;
 }
@@ -1170,7 +1227,7 @@ int bct_set_r(bct_ctx *c, const double *r)
 int bct_get_r(bct_ctx *c, double *r)
 {
     if (!c || !r) return BCT_EINVAL;
-    CK(cudaMemcpyAsync(r, c->r, 8 * c->n_meas, cudaMemcpyDeviceToHost, c->stream));
+    if (int e = d2h_staged(c, r, c->r, 8 * c->n_meas)) return e;
     CK(cudaStreamSynchronize(c->stream));
     return 0;
 }
