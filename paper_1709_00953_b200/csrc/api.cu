@@ -35,6 +35,9 @@ cudaError_t pb_replay(int64_t, int64_t, const double *, const double *, int64_t,
                       cudaStream_t);
 unsigned long long pb_replay_check(int, const PanelDev &, int64_t, int64_t, cudaStream_t);
 cudaError_t inv_count(const int32_t *, int32_t, int32_t *, cudaStream_t);
+cudaError_t invt_len(const int32_t *, int64_t, int32_t *, cudaStream_t);
+cudaError_t invt_fill(const int32_t *, const int32_t *, int64_t, const int32_t *, int32_t *,
+                      cudaStream_t);
 cudaError_t inv_fill(const int32_t *, int32_t, int64_t, const int32_t *, int32_t *, int32_t *,
                      cudaStream_t);
 cudaError_t fill_z(int, const PanelDev *, int, int64_t, const double *, double *, cudaStream_t);
@@ -104,6 +107,7 @@ struct bct_ctx {
     // device
     PanelDev *d_panels = nullptr;
     int32_t *inv_ptr = nullptr, *inv_z = nullptr, *d_rb_ptr = nullptr, *d_rb_rows = nullptr;
+    int32_t *invt = nullptr, *invt_off = nullptr;   // interleaved inverse map (epoch tail)
     int32_t *rb_of_row = nullptr;
     double *y = nullptr, *r = nullptr, *z = nullptr, *x = nullptr, *xhat = nullptr;
     float *r32 = nullptr;   // FP32 mode: band staging copy of r (epoch kernel)
@@ -430,6 +434,26 @@ int finalize(bct_ctx *c)
     for (int lp = 0; lp < c->np; ++lp) {
         const PanelDev &P = c->h_panels[lp];
         CK(bct::inv_fill(P.l2g, P.n_rows, P.row_off, c->inv_ptr, fill, c->inv_z, c->stream));
+    }
+    {
+        // interleaved copy for the epoch tail (groups of 32 measurements)
+        const int64_t ng = (c->n_meas + 31) / 32;
+        size_t sb2 = bct::scan_temp_bytes(ng + 1);
+        char *cub2 = nullptr;
+        DALLOC(cub2, (int64_t)sb2);
+        int32_t *glen = nullptr;
+        DALLOC(glen, ng + 1);
+        DALLOC(c->invt_off, ng + 1);
+        CK(cudaMemsetAsync(glen, 0, 4 * (ng + 1), c->stream));
+        CK(bct::invt_len(c->inv_ptr, c->n_meas, glen, c->stream));
+        CK(bct::exclusive_scan_i32(glen, c->invt_off, ng + 1, cub2, sb2, c->stream));
+        int32_t tot = 0;
+        CK(cudaMemcpyAsync(&tot, c->invt_off + ng, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        DALLOC(c->invt, std::max<int32_t>(tot, 1));
+        CK(bct::invt_fill(c->inv_ptr, c->inv_z, c->n_meas, c->invt_off, c->invt, c->stream));
+        free_tmp(c, glen);
+        free_tmp(c, cub2);
     }
     CK(cudaStreamSynchronize(c->stream));
     free_tmp(c, cnt);
@@ -1382,7 +1406,8 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
     memset(&p, 0, sizeof p);
     p.panels = c->d_panels;
     p.n_panels_owned = c->np; p.m = c->m; p.n_meas = c->n_meas; p.z_len = c->z_len;
-    p.x_len = c->x_len; p.inv_ptr = c->inv_ptr; p.inv_z = c->inv_z; p.rb_ptr = c->d_rb_ptr;
+    p.x_len = c->x_len; p.inv_ptr = c->inv_ptr; p.inv_z = c->inv_z;
+    p.invt = c->invt; p.invt_off = c->invt_off; p.rb_ptr = c->d_rb_ptr;
     p.rb_rows = c->d_rb_rows; p.rb_of_row = c->rb_of_row; p.y = c->y; p.r = c->r; p.r32 = c->r32; p.z = c->z;
     p.x = c->x; p.xhat = c->xhat; p.counts = c->counts;
     p.x_true = c->has_x_true ? c->x_true : nullptr;

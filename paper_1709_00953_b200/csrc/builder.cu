@@ -496,6 +496,30 @@ __global__ void inv_fill_kernel(const int32_t *l2g, int32_t n_rows, int64_t row_
 
 // ---- bitwise state kernels (reference operation order, no contraction) --
 
+// Interleaved copy of the inverse row map for the epoch tail: groups of 32
+// consecutive measurements, slot s of lane l at off[G] + s*32 + l (padding -1
+// after a lane's list), so a warp reads its lists with coalesced loads.
+__global__ void invt_len_kernel(const int32_t *inv_ptr, int64_t n_meas, int32_t *glen)
+{
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int len = g < n_meas ? inv_ptr[g + 1] - inv_ptr[g] : 0;
+    int mx = len;
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && g < ((n_meas + 31) & ~31ll)) glen[g >> 5] = mx * 32;
+}
+
+__global__ void invt_fill_kernel(const int32_t *inv_ptr, const int32_t *inv_z, int64_t n_meas,
+                                 const int32_t *goff, int32_t *invt)
+{
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= ((n_meas + 31) & ~31ll)) return;
+    const int64_t G = g >> 5;
+    const int lane = (int)(g & 31);
+    const int nmax = (goff[G + 1] - goff[G]) / 32;
+    const int e0 = g < n_meas ? inv_ptr[g] : 0, len = g < n_meas ? inv_ptr[g + 1] - e0 : 0;
+    for (int s = 0; s < nmax; ++s) invt[goff[G] + s * 32 + lane] = s < len ? inv_z[e0 + s] : -1;
+}
+
 __device__ __forceinline__ int panel_of_off(const PanelDev *panels, int np, int64_t off)
 {
     int lo = 0, hi = np - 1;
@@ -813,6 +837,23 @@ cudaError_t pb_rbp(const int32_t *d_l2g, int64_t n_hit, const int64_t *d_edges, 
                    int32_t *d_rbp, cudaStream_t s)
 {
     rbp_kernel<<<nblk(m + 1, 128), 128, 0, s>>>(d_l2g, n_hit, d_edges, m, d_rbp);
+    return cudaGetLastError();
+}
+
+cudaError_t invt_len(const int32_t *inv_ptr, int64_t n_meas, int32_t *glen, cudaStream_t s)
+{
+    const int64_t n = (n_meas + 31) & ~31ll;
+    if (n == 0) return cudaSuccess;
+    invt_len_kernel<<<nblk(n, 256), 256, 0, s>>>(inv_ptr, n_meas, glen);
+    return cudaGetLastError();
+}
+
+cudaError_t invt_fill(const int32_t *inv_ptr, const int32_t *inv_z, int64_t n_meas,
+                      const int32_t *goff, int32_t *invt, cudaStream_t s)
+{
+    const int64_t n = (n_meas + 31) & ~31ll;
+    if (n == 0) return cudaSuccess;
+    invt_fill_kernel<<<nblk(n, 256), 256, 0, s>>>(inv_ptr, inv_z, n_meas, goff, invt);
     return cudaGetLastError();
 }
 

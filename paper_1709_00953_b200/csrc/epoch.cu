@@ -1635,23 +1635,32 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     const bool do_commit = (hdr.flags & 1) != 0;
     double rsq = 0.0, xsq = 0.0, esq = 0.0;
     if (!serial || do_metrics || sharded) {
-        for (int g = gtid; g < p.n_meas; g += nthreads) {
+        // warps cover 32 consecutive measurements (gtid and nthreads are
+        // multiples of 32): the interleaved inverse map is read coalesced
+        const int64_t n_pad = (p.n_meas + 31) & ~31ll;
+        for (int64_t g = gtid; g < n_pad; g += nthreads) {
             double acc = 0.0;
-            const int e1 = __ldg(p.inv_ptr + g + 1);
+            const int64_t G = g >> 5;
+            const int e0 = __ldg(p.invt_off + G), e1 = __ldg(p.invt_off + G + 1);
             // ascending j (the reference's fold); z was written earlier in this
-            // launch: L2-coherent loads, four in flight
-            int e = __ldg(p.inv_ptr + g);
-            for (; e + 4 <= e1; e += 4) {
+            // launch: L2-coherent loads, four in flight; -1 pads a list
+            int e = e0 + (int)(g & 31);
+            for (; e + 96 < e1; e += 128) {
                 int o[4];
                 double v[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) o[u] = __ldg(p.inv_z + e + u);
+                for (int u = 0; u < 4; ++u) o[u] = __ldg(p.invt + e + 32 * u);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = __ldcg(p.z + o[u]);
+                for (int u = 0; u < 4; ++u) v[u] = o[u] >= 0 ? __ldcg(p.z + o[u]) : 0.0;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) acc += v[u];
+                for (int u = 0; u < 4; ++u)
+                    if (o[u] >= 0) acc += v[u];
             }
-            for (; e < e1; ++e) acc += __ldcg(p.z + __ldg(p.inv_z + e));
+            for (; e < e1; e += 32) {
+                const int o = __ldg(p.invt + e);
+                if (o >= 0) acc += __ldcg(p.z + o);
+            }
+            if (g >= p.n_meas) continue;
             if (sharded) {
                 p.exchange[g] = acc;
             } else {
@@ -1662,23 +1671,26 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             }
         }
     }
-    for (int lp = 0; lp < p.n_panels_owned; ++lp) {
-        const int64_t xo = p.panels[lp].x_off;
-        const int nc = p.panels[lp].n_cols;
-        const int cnt = p.counts[lp];
-        double *xs = p.x + xo;
-        double *xh = p.xhat + xo;
-        const double *xt = p.x_true ? p.x_true + xo : nullptr;
-        for (int c = gtid; c < nc; c += nthreads) {
-            double xv = xs[c];
+    // commit and image norms over all owned voxels at once (panels are
+    // contiguous in x / xhat / x_true); the panel of a voxel by binary search
+    {
+        const int npo = p.n_panels_owned;
+        for (int64_t v = gtid; v < p.x_len; v += nthreads) {
+            int lo = 0, hi = npo - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (p.panels[mid].x_off <= v) lo = mid; else hi = mid - 1;
+            }
+            const int cnt = p.counts[lo];
+            double xv = p.x[v];
             if (do_commit && cnt > 0) {
-                xv = xh[c] / (double)cnt;
-                xs[c] = xv;
-                xh[c] = 0.0;
+                xv = p.xhat[v] / (double)cnt;
+                p.x[v] = xv;
+                p.xhat[v] = 0.0;
             }
             xsq = fma(xv, xv, xsq);
-            if (xt) {
-                double d = xt[c] - xv;
+            if (p.x_true) {
+                const double d = p.x_true[v] - xv;
                 esq = fma(d, d, esq);
             }
         }

@@ -128,6 +128,8 @@ struct EpochParams {
     // refresh / metrics
     const int32_t *inv_ptr;
     const int32_t *inv_z;
+    const int32_t *invt;       // interleaved inverse map: groups of 32 measurements,
+    const int32_t *invt_off;   //   slot s of lane l at invt_off[G] + s*32 + l (-1: none)
     const int32_t *rb_ptr;
     const int32_t *rb_rows;
     const int32_t *rb_of_row;
