@@ -310,7 +310,8 @@ def run_ours(args):
             "higher_is_better": True,
             "scaling": "strong" if world > 1 else "strong",
             "vs_baseline": None,
-            "dtype": "f32-values/i32-index/f64-math" if cfg.dtype == "f32" else "f64",
+            "dtype": ("f32 (FP32 values and inner products, FP64 reductions and state)"
+                      if cfg.dtype == "f32" else "f64"),
             "data": "synthetic (seeded random ellipses + 0.5% Gaussian noise; A traced on device)",
             "config": {"workload": f"{cfg.name}: {spec.n}^2 parallel beam, {spec.views} views "
                                    f"x {spec.bins} bins, {spec.m}x{nc} blocks, group "
@@ -332,7 +333,7 @@ def run_ours(args):
                          "kernel": "epoch_kernel (persistent cooperative; one launch per epoch)",
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
                          "note": "algorithmic bytes count 4-byte indices (SURVEY 8d); the "
-                                 "store keeps 2-byte indices, so DRAM traffic (ncu) is lower "
+                                 "store keeps 8-bit band offsets / 2-bit step codes, so DRAM traffic (ncu) is lower "
                                  "and frac can approach or pass 1",
                          "peak_kind": peak_kind},
             "e2e": {"value": blocks_per_step * args.steps / (e2e_ms * 1e-3),
