@@ -369,7 +369,7 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     c->max_rows = std::max<int64_t>(c->max_rows, n_rows);
     c->max_cols = std::max<int64_t>(c->max_cols, n_cols);
     c->max_seg = std::max<int64_t>(c->max_seg, (int64_t)P.n_slices * 32);   // partial slots
-    c->band_cap = std::max(c->band_cap, (P.band_max + 1) & ~1);
+    c->band_cap = std::max(c->band_cap, (P.band_max + 3) & ~3);   // 16-byte aligned FP32 buffers
     // staged super tile: (g, x) as float2 in FP32 mode, double2 in FP64 mode (swizzled)
     c->smem = std::max<size_t>(c->smem, (size_t)((P.st_max + 15) & ~15) * (c->dtype == 0 ? 16 : 8));
     return 0;

@@ -528,19 +528,18 @@ __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm
             const int keep = __shfl_sync(0xffffffffu, bm.keep[it], src);
             if (q0 + src < bm.k1 && BCT_EXP != 5) {
                 const int pre = (int)((unsigned)pk >> 16), len = pk & 0xffff;
-                const int ng = ((g0 & 1) + len + 1) >> 1;
-                const TB *rs = r + (g0 & ~1);
+                // 16-byte granules of GE elements from the aligned range start
+                constexpr int GE = 16 / sizeof(TB);
+                constexpr int AM = bct::BAND_ALIGN - 1;
+                const int ng = ((g0 & AM) + len + GE - 1) / GE;
+                const TB *rs = r + (g0 & ~AM);
                 TB *dst = buf + pre;
                 if (keep) {
-                    for (int e = sl; e < ng; e += 8) {
-                        if (sizeof(TB) == 8) cp_async16(dst + 2 * e, rs + 2 * e);
-                        else cp_async8(dst + 2 * e, rs + 2 * e);
-                    }
+                    for (int e = sl; e < ng; e += 8) cp_async16(dst + GE * e, rs + GE * e);
                 } else {
-                    for (int e = sl; e < ng; e += 8) {
-                        dst[2 * e] = TB(0);
-                        dst[2 * e + 1] = TB(0);
-                    }
+                    for (int e = sl; e < ng; e += 8)
+#pragma unroll
+                        for (int u = 0; u < GE; ++u) dst[GE * e + u] = TB(0);
                 }
             }
         }
@@ -550,7 +549,7 @@ __device__ __forceinline__ void band_issue(const PanelDev &P, const BandMeta &bm
         const int2 mm = __ldg(P.band_meta + q);
         const int pre = (int)((unsigned)mm.y >> 16), len = mm.y & 0xffff;
         const bool keep = mask == nullptr || mask_has(mask, __ldg(P.band_rb + q));
-        const int off = mm.x & 1;
+        const int off = mm.x & (bct::BAND_ALIGN - 1);
         for (int e = 0; e < len; ++e) buf[pre + off + e] = keep ? r[mm.x + e] : TB(0);
     }
     cp_async_commit();

@@ -199,6 +199,10 @@ cudaError_t scan_fill(const ScanDev &S, const int32_t *l2g, const int32_t *indpt
 cudaError_t gather_i32(const int32_t *src, const int32_t *idx, int64_t n, int32_t *dst,
                        cudaStream_t s);
 
+// band ranges start at multiples of this many slots / measurement ids, so a
+// range is staged in 16-byte granules of 4 FP32 or 2 FP64 residuals
+constexpr int BAND_ALIGN = 4;
+
 // epoch-batched path: at most this many tasks (task tables live in shared memory)
 constexpr int MAX_BATCH_TASKS = 256;
 

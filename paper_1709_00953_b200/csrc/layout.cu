@@ -431,9 +431,10 @@ __global__ void tile_bounds_k(const uint64_t *u, int64_t nu, const int32_t *rfla
     band_ptr[t] = q == 0 ? 0 : rflag_incl[q - 1];
 }
 
-// Ranges are staged with 16-byte bulk copies: range k covers the aligned
-// measurement span [g0 & ~1, g0 + len rounded up to even), alen slots, and
-// starts at an even band slot (apre = exclusive prefix of alen).
+// Ranges are staged in 16-byte granules: range k covers the aligned
+// measurement span [g0 & ~3, g0 + len rounded up to 4), alen slots, and
+// starts at a band slot that is a multiple of 4 (apre = exclusive prefix of
+// alen): 4 FP32 or 2 FP64 residuals per granule (bct::BAND_ALIGN).
 __global__ void ranges_k(const uint64_t *u, int64_t nu, const int32_t *rflag, const int32_t *rincl,
                          int32_t *rstart, int32_t *rlen, int32_t *alen, uint8_t *band_rb)
 {
@@ -447,7 +448,8 @@ __global__ void ranges_k(const uint64_t *u, int64_t nu, const int32_t *rflag, co
     while (e < nu && !rflag[e]) ++e;
     rstart[k] = (int32_t)q;
     rlen[k] = (int32_t)(e - q);
-    alen[k] = ((g0 & 1) + (int32_t)(e - q) + 1) & ~1;
+    constexpr int A = bct::BAND_ALIGN;
+    alen[k] = ((g0 & (A - 1)) + (int32_t)(e - q) + A - 1) & ~(A - 1);
 }
 
 __global__ void range_meta_k(const uint64_t *u, const int32_t *rstart, const int32_t *rlen,
@@ -509,7 +511,8 @@ __global__ void csc_sell_scatter_k(const int32_t *perm, const double *vals64, co
     tvals[dst] = (V)vals64[perm[q]];
     const int k = rincl[bpos] - 1;   // range of the entry's row
     const int32_t g0 = (int32_t)(uint32_t)u[rstart[k]];
-    tloc[dst] = (uint16_t)(apre[k] - apre[band_ptr[t]] + (g0 & 1) + (bpos - rstart[k]));
+    tloc[dst] = (uint16_t)(apre[k] - apre[band_ptr[t]] + (g0 & (bct::BAND_ALIGN - 1)) +
+                           (bpos - rstart[k]));
 }
 
 // padding of every (slice, lane): zero values on the column's last band slot
