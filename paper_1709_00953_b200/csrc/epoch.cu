@@ -362,6 +362,20 @@ __device__ __forceinline__ float lds_f32(uint32_t a)
     return v;
 }
 
+__device__ __forceinline__ double lds_f64(uint32_t a)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+// element idx of a shared band of TB (32-bit shared-window base address)
+template <typename TB>
+__device__ __forceinline__ double lds_band(uint32_t base, int idx)
+{
+    if constexpr (sizeof(TB) == 8) return lds_f64(base + 8u * (uint32_t)idx);
+    else return (double)lds_f32(base + 4u * (uint32_t)idx);
+}
+
 // L2 prefetch of a byte range (one bulk request; 16-byte aligned, size % 16 == 0)
 __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes)
 {
@@ -662,6 +676,7 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
             acc = acc32;
         } else if (toff != nullptr) {   // delta form: 8-bit offsets on a 16-bit base
             const uint16_t *tbase = P.tbase;
+            const uint32_t bts = (uint32_t)__cvta_generic_to_shared(bt);
 #pragma unroll P1U
             for (int u = lo + sub; u < hi; u += wps) {
                 const int i = base + u * 256 + lane * 8;
@@ -671,13 +686,14 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
                 ld8v(tv + i, v);
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    acc = fma(v[e], (double)bt[b0 + ((o.x >> (8 * e)) & 0xff)], acc);
+                    acc = fma(v[e], lds_band<TB>(bts, b0 + ((o.x >> (8 * e)) & 0xff)), acc);
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    acc = fma(v[4 + e], (double)bt[b0 + ((o.y >> (8 * e)) & 0xff)], acc);
+                    acc = fma(v[4 + e], lds_band<TB>(bts, b0 + ((o.y >> (8 * e)) & 0xff)), acc);
             }
         } else {
             const uint16_t *tloc = P.tloc;
+            const uint32_t bts = (uint32_t)__cvta_generic_to_shared(bt);
 #pragma unroll P1U
             for (int u = lo + sub; u < hi; u += wps) {
                 const int i = base + u * 256 + lane * 8;
@@ -687,7 +703,7 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
                 ld8v(tv + i, v);
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
-                    acc = fma(v[e], BCT_EXP == 7 ? (double)loc[e] : (double)bt[loc[e]], acc);
+                    acc = fma(v[e], BCT_EXP == 7 ? (double)loc[e] : lds_band<TB>(bts, loc[e]), acc);
             }
         }
         red[sub * (ns * 32) + si * 32 + lane] = acc;
