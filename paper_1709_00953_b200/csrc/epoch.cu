@@ -10,14 +10,20 @@
 // configs 3-5): every phase runs over the tasks of the whole epoch at once,
 // four grid barriers per epoch.
 //   A  g = A_J^T r per 16x16-voxel tile: the tile's band of r staged in
-//      shared memory (cp.async, 8-lane groups per range), the lane-
-//      interleaved CSC streamed by 4 warps per 32-column slice, column
-//      partials reduced in a fixed order; (g, x) pairs + gg partials
+//      shared memory (cp.async 16-byte granules, 8-lane groups per range;
+//      FP32 copy of r in FP32 mode, double-buffered), the lane-interleaved
+//      CSC streamed by 4 warps per 32-column slice in groups of 4 vector
+//      rows, column partials reduced in a fixed order; (g, x) pairs + gg
 //   B  per SELL slice of a super tile (its (g, x) staged, swizzled): one
-//      (row, super tile) segment per lane -> (t, ax) partial, SELL order
+//      (row, super tile) segment per lane -> (t, ax) partial, SELL order;
+//      strip panels decode voxel indices from 2-bit step codes
 //   C  per row: t, ax = its segments' partials in tile order; denom partials
 //   D  mu, status per task; xhat += x_new per visit; z = ax + mu t
-//   tail: r = y - sum_j z^j on the drawn rows (ascending j), commit, norms
+//   tail: r = y - sum_j z^j on the drawn rows (ascending j, interleaved
+//      inverse map), commit, norms
+// FP32 mode computes the streamed inner products (phase A lane sums, phase B
+// segment partials) in FP32; every reduction across lanes, warps, segments
+// and tasks, and all state, is FP64.  FP64 mode is FP64 throughout.
 // Per-task path (serial_faithful and partial groups): the same phase-1 and
 // phase-2 code per task, three grid barriers per task, and in serial mode the
 // refresh of the visit's drawn rows after its last task (executor.py:215-223).

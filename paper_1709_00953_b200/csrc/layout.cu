@@ -11,7 +11,8 @@
 // view), stored as even-aligned ranges of consecutive measurement ids that
 // never cross a row block.  Each tile's columns are stored in 32-column slices,
 // lane-interleaved 8 entries at a time (csl_start), every entry carrying its
-// 16-bit band slot (tloc); a lane's 8 entries are ordered to spread the
+// band slot (tloc, stored as an 8-bit offset on a 16-bit base per 8 entries
+// when it fits: tloc_delta_k); a lane's 8 entries are ordered to spread the
 // shared-memory banks of each gather.
 //
 // Phase 2 (t = A_I g, ax = A_I x_J) reads the forward store.  The panel's
@@ -25,9 +26,12 @@
 // Per-segment partials are combined per row in super-tile order
 // (deterministic).  A task over any subset of row blocks maps to whole slices.
 //
-// Entries inside a segment stay in the reference's column order, and a row's
-// segments in tile order, so the bitwise set-up kernels (builder.cu) recover
-// the reference's summation order by merging a row's segments by column.
+// Entries inside a segment are in the reference's column order -- except on
+// step-coded strip panels (fcode_k), where an equal-ix run of a ray going down
+// in iy is stored reversed (walk order) -- and a row's segments in tile order,
+// so the bitwise set-up kernels (builder.cu row_dot) recover the reference's
+// summation order by merging a row's segments by column, reading descending
+// runs backwards.
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
