@@ -122,6 +122,8 @@ struct bct_ctx {
     int32_t *statuses = nullptr;
     EpochOut *out = nullptr;
     unsigned int *bar = nullptr, *ticket = nullptr;
+    TaskPrep *d_prep = nullptr;      // [task_cap] per-task set-up (host_prep)
+    TaskPrep *h_prep = nullptr;      // pinned
     unsigned long long *audit2 = nullptr;
     EpochHeader *d_hdr = nullptr;
     TaskDev *d_tasks = nullptr;
@@ -365,6 +367,8 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     P.mdiv = pl.mdiv;
     c->h_d2c[lp] = pl.d2c;
     c->h_rbp[lp] = rbp;
+    c->h_stbs[lp].resize((size_t)P.n_st * (c->m + 1));
+    CK(cudaMemcpy(c->h_stbs[lp].data(), P.stbs, 4 * c->h_stbs[lp].size(), cudaMemcpyDeviceToHost));
     c->nnz += nnz;
     c->max_rows = std::max<int64_t>(c->max_rows, n_rows);
     c->max_cols = std::max<int64_t>(c->max_cols, n_cols);
@@ -524,7 +528,11 @@ int ensure_task_cap(bct_ctx *c, int64_t n)
     if (c->mus) cudaFree(c->mus);
     if (c->statuses) cudaFree(c->statuses);
     if (c->h_tasks) cudaFreeHost(c->h_tasks);
+    if (c->d_prep) cudaFree(c->d_prep);
+    if (c->h_prep) cudaFreeHost(c->h_prep);
     CK(cudaMalloc((void **)&c->d_tasks, sizeof(TaskDev) * cap));
+    CK(cudaMalloc((void **)&c->d_prep, sizeof(TaskPrep) * cap));
+    CK(cudaHostAlloc((void **)&c->h_prep, sizeof(TaskPrep) * cap, cudaHostAllocDefault));
     CK(cudaMalloc((void **)&c->mus, 8 * cap));
     CK(cudaMalloc((void **)&c->statuses, 4 * cap));
     CK(cudaHostAlloc((void **)&c->h_tasks, sizeof(TaskDev) * cap, cudaHostAllocDefault));
@@ -564,6 +572,8 @@ void destroy(bct_ctx *c)
     for (double *q : {c->gx_batch, c->seg_batch, c->tax_batch, c->part_task})
         if (q) cudaFree(q);
     if (c->h_tasks) cudaFreeHost(c->h_tasks);
+    if (c->d_prep) cudaFree(c->d_prep);
+    if (c->h_prep) cudaFreeHost(c->h_prep);
     if (c->h_hdr) cudaFreeHost(c->h_hdr);
     for (int s = 0; s < RING; ++s) {
         Slot &S = c->slots[s];
@@ -590,6 +600,7 @@ int init_ctx(bct_ctx *c, int device, int np)
     c->h_panels.assign(np, PanelDev{});
     c->h_d2c.resize(np);
     c->h_rbp.resize(np);
+    c->h_stbs.resize(np);
     return 0;
 }
 
@@ -1395,6 +1406,9 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
     if (n_tasks > 0)
         CK(cudaMemcpyAsync(c->d_tasks, c->h_tasks, sizeof(TaskDev) * n_tasks,
                            cudaMemcpyHostToDevice, c->stream));
+    if (n_tasks > 0 && c->h_hdr->host_prep)
+        CK(cudaMemcpyAsync(c->d_prep, c->h_prep, sizeof(TaskPrep) * n_tasks,
+                           cudaMemcpyHostToDevice, c->stream));
     CK(cudaEventRecord(c->staged, c->stream));
     S.plan_user = nullptr;
     S.n_plan = 0;
@@ -1418,6 +1432,7 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
     p.part_task = c->part_task;
     p.statuses = c->statuses; p.out = c->out;
     p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
+    p.prep = c->d_prep;
     p.timeline = nullptr;
     if (getenv("BCT_TIMELINE") && n_tasks > 0) {
         if (c->timeline_tasks < n_tasks) {
@@ -1447,7 +1462,8 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
 }
 
 static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<TaskDev> &tasks,
-                           const uint64_t *emask, const std::function<int(Slot &)> &hook);
+                           const uint64_t *emask, const std::function<int(Slot &)> &hook,
+                           bool host_masks);
 
 int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task_j,
                   const int32_t *task_visit, const int64_t *task_gptr, const int64_t *sel,
@@ -1499,14 +1515,65 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
         T.beta = betas[k];
         tasks.push_back(T);
     }
-    return plan_and_launch(c, mode, flags, tasks, emask, nullptr);
+    return plan_and_launch(c, mode, flags, tasks, emask, nullptr, true);
+}
+
+// Host restatement of epoch.cu build_runs / prep_task: the per-task path's
+// set-up of one task (its TaskDev, panel, mask runs and the visit's drawn
+// rows), built with the plan so the kernel copies it instead of walking a
+// chain of dependent device loads per task.
+static void host_prep(const bct_ctx *c, const TaskDev &T, TaskPrep &o)
+{
+    o.T = T;
+    o.P = c->h_panels[T.lp];
+    const std::vector<int32_t> &rbp = c->h_rbp[T.lp];
+    const std::vector<int32_t> &stbs = c->h_stbs[T.lp];
+    const int m = c->m;
+    auto has = [](const uint64_t *mk, int i) { return ((mk[i >> 6] >> (i & 63)) & 1ull) != 0; };
+    Runs &R = o.R;
+    int n = 0, acc = 0;
+    for (int i = 0; i < m;) {
+        if (!has(T.mask, i)) { ++i; continue; }
+        const int s = i;
+        while (i < m && has(T.mask, i)) ++i;
+        R.i0[n] = s;
+        R.i1[n] = i;
+        R.rows0[n] = rbp[s];
+        R.pre[n] = acc;
+        acc += rbp[i] - rbp[s];
+        ++n;
+    }
+    R.pre[n] = acc;
+    R.n = n;
+    int uacc = 0;
+    for (int st = 0; st < o.P.n_st; ++st) {
+        R.st_pre[st] = uacc;
+        const int32_t *sb = stbs.data() + (size_t)st * (m + 1);
+        for (int q = 0; q < n; ++q) uacc += sb[R.i1[q]] - sb[R.i0[q]];
+    }
+    R.st_pre[o.P.n_st] = uacc;
+    R.nst = o.P.n_st;
+    R.full = (n == 1 && R.i0[0] == 0 && R.i1[0] == m);
+    VisitRows &V = o.V;
+    int nv = 0;
+    acc = 0;
+    for (int i = 0; i < m; ++i) {
+        if (!has(T.visit_mask, i)) continue;
+        V.vb[nv] = i;
+        V.vpre[nv] = acc;
+        acc += (int)(c->rb_ptr[i + 1] - c->rb_ptr[i]);
+        ++nv;
+    }
+    V.vpre[nv] = acc;
+    V.nvb = nv;
 }
 
 // Visit flags/masks, batched-path prefixes and scratch, staging and launch of
 // a validated task list (shared by bct_run_epoch and bct_sample_epoch; the
 // hook runs on the stream between the plan upload and the epoch kernel).
 static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<TaskDev> &tasks,
-                           const uint64_t *emask, const std::function<int(Slot &)> &hook)
+                           const uint64_t *emask, const std::function<int(Slot &)> &hook,
+                           bool host_masks)
 {
     // visit boundaries and masks
     int64_t n_visits = 0;
@@ -1586,6 +1653,10 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
     c->h_hdr->n_ent_total = tot_ent;
     memcpy(c->h_hdr->epoch_mask, emask, sizeof(uint64_t) * BCT_MASKW);
     if (nt) memcpy(c->h_tasks, tasks.data(), sizeof(TaskDev) * nt);
+    // per-task path with host-known masks: every task's set-up built here
+    c->h_hdr->host_prep = (!batched && host_masks && nt > 0) ? 1 : 0;
+    if (c->h_hdr->host_prep)
+        for (int64_t k = 0; k < nt; ++k) host_prep(c, tasks[k], c->h_prep[k]);
     return launch_staged(c, nt, n_visits, hook);
 }
 
@@ -1786,7 +1857,7 @@ int bct_sample_epoch(bct_ctx *c, int32_t mode, int32_t n_visits, const int32_t *
         }
         return 0;
     };
-    return plan_and_launch(c, mode, flags, tasks, emask, hook);
+    return plan_and_launch(c, mode, flags, tasks, emask, hook, false);
 }
 
 }  // extern "C"

@@ -55,8 +55,6 @@ constexpr int TASK_SPLIT = 4;       // per-task phase 2a: parts per SELL slice
 constexpr int P2U = BCT_P2_UNROLL;
 constexpr int BLOCK = 1024;         // one CTA per SM
 constexpr int WARPS = BLOCK / 32;
-constexpr int MAX_RUNS = BCT_MAX_M / 2 + 1;
-constexpr int MAX_ST = 64;
 
 __device__ __forceinline__ long long gtimer()
 {
@@ -143,22 +141,11 @@ __device__ double block_sum_all(double v, double *sh)
     return s;
 }
 
-struct Runs {
-    int n;
-    int i0[MAX_RUNS];
-    int i1[MAX_RUNS];
-    int rows0[MAX_RUNS];       // first local row of the run
-    int pre[MAX_RUNS + 1];     // prefix of run row counts
-    int nst;
-    int st_pre[MAX_ST + 1];    // prefix over super tiles of the task's slice counts
-    bool full;                 // the task covers every row block
-};
-
 // Contiguous runs of set bits of a row-block mask, with their local row ranges
 // and the task's units per super tile.
 __device__ void build_runs(const uint64_t *mask, int m, const PanelDev &P, Runs &R)
 {
-    if (threadIdx.x == 0) {
+    {   // (restated on the host: api.cu host_prep)
         int n = 0, acc = 0;
         int i = 0;
         while (i < m) {
@@ -184,8 +171,27 @@ __device__ void build_runs(const uint64_t *mask, int m, const PanelDev &P, Runs 
         R.nst = P.n_st;
         R.full = (n == 1 && R.i0[0] == 0 && R.i1[0] == m);
     }
-    __syncthreads();
 }
+
+__device__ void prep_task(const EpochParams &p, int k, TaskPrep &out)
+{
+    const TaskDev &T = p.tasks[k];
+    const PanelDev &P = p.panels[T.lp];
+    out.T = T;
+    out.P = P;
+    build_runs(T.mask, p.m, P, out.R);
+    int nv = 0, acc = 0;
+    for (int i = 0; i < p.m; ++i) {
+        if (!mask_has(T.visit_mask, i)) continue;
+        out.V.vb[nv] = i;
+        out.V.vpre[nv] = acc;
+        acc += p.rb_ptr[i + 1] - p.rb_ptr[i];
+        ++nv;
+    }
+    out.V.vpre[nv] = acc;
+    out.V.nvb = nv;
+}
+
 
 __device__ __forceinline__ int run_row(const Runs &R, int f)
 {
@@ -1355,10 +1361,9 @@ template <typename V>
 __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
 {
     extern __shared__ double4 dyn_smem[];
-    __shared__ Runs R;
     __shared__ double sh[WARPS];
-    __shared__ TaskDev sT;
-    __shared__ PanelDev sP;
+    __shared__ TaskPrep sPrep;
+    Runs &R = sPrep.R;
     __shared__ int2 vr_s[8];
 
     const int lane = threadIdx.x & 31;
@@ -1382,15 +1387,19 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     __shared__ int s_tpre[bct::MAX_BATCH_TASKS + 1], s_lp[bct::MAX_BATCH_TASKS];
     if (hdr.batched) batched_epoch<V>(p, hdr, rs, sh, ring, s_tpre, s_lp);
     for (int k = 0; k < (hdr.batched ? 0 : n_tasks); ++k) {
-        __syncthreads();  // sT/sP/R of the previous task may still be in use
-        if (threadIdx.x == 0) {
-            sT = p.tasks[k];
-            sP = p.panels[sT.lp];
+        __syncthreads();  // sPrep of the previous task may still be in use
+        if (!hdr.host_prep) {
+            if (threadIdx.x == 0) prep_task(p, k, sPrep);
+        } else {
+            // built on the host with the plan (api.cu host_prep): one copy
+            const float4 *src = reinterpret_cast<const float4 *>(p.prep + k);
+            float4 *dst = reinterpret_cast<float4 *>(&sPrep);
+            for (int q = threadIdx.x; q < (int)(sizeof(TaskPrep) / sizeof(float4)); q += BLOCK)
+                dst[q] = __ldcg(src + q);
         }
         __syncthreads();
-        const TaskDev &T = sT;
-        const PanelDev &P = sP;
-        build_runs(T.mask, m, P, R);
+        const TaskDev &T = sPrep.T;
+        const PanelDev &P = sPrep.P;
         TL_MARK(k, 0);
         double2 *gx = reinterpret_cast<double2 *>(p.gx + (k & 1) * p.gx_stride);
         const double *xj = p.x + P.x_off;
@@ -1603,22 +1612,8 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             // refresh every row of the visit's drawn blocks (executor.py:215-223),
             // one flat pass over their rows; the current task's z is computed
             // here and stored on the way (every one of its rows is refreshed)
-            __shared__ int s_vb[BCT_MAX_M], s_vpre[BCT_MAX_M + 1];
-            __shared__ int s_nvb;
-            if (threadIdx.x == 0) {
-                int nv = 0, acc = 0;
-                for (int i = 0; i < m; ++i) {
-                    if (!mask_has(T.visit_mask, i)) continue;
-                    s_vb[nv] = i;
-                    s_vpre[nv] = acc;
-                    acc += p.rb_ptr[i + 1] - p.rb_ptr[i];
-                    ++nv;
-                }
-                s_vpre[nv] = acc;
-                s_nvb = nv;
-            }
-            __syncthreads();
-            const int nvb = s_nvb, tot = s_vpre[nvb];
+            const int *s_vb = sPrep.V.vb, *s_vpre = sPrep.V.vpre;
+            const int nvb = sPrep.V.nvb, tot = s_vpre[nvb];
             const double2 *tax = reinterpret_cast<const double2 *>(p.t_ax);
             const int64_t zlo = P.row_off, zhi = P.row_off + P.n_rows;
             for (int f = gtid; f < tot; f += nthreads) {

@@ -109,6 +109,8 @@ struct EpochHeader {
     int32_t n_tiles_total, n_slices_total, n_rows_total, n_vox_total;
     uint64_t epoch_mask[BCT_MASKW];  // union of all drawn blocks (parallel refresh)
     int64_t n_ent_total;             // forward-store entries of the batched tasks
+    int32_t host_prep;               // 1: EpochParams::prep holds every task's TaskPrep
+    int32_t pad_;
 };
 
 // Device-side per-epoch outputs.
@@ -116,6 +118,43 @@ struct EpochOut {
     double resid_sq, x_sq, err_sq, pad;
     int32_t n_degenerate;
     int32_t pad2[7];
+};
+
+// ---- per-task path set-up (epoch.cu per-task loop; built by api.cu when the
+// masks are host-known) ----
+constexpr int MAX_RUNS = BCT_MAX_M / 2 + 1;
+constexpr int MAX_ST = 64;
+
+// Contiguous runs of set bits of a task's row-block mask, with their local row
+// ranges and the task's SELL slices per super tile.
+struct Runs {
+    int n;
+    int i0[MAX_RUNS];
+    int i1[MAX_RUNS];
+    int rows0[MAX_RUNS];       // first local row of the run
+    int pre[MAX_RUNS + 1];     // prefix of run row counts
+    int nst;
+    int st_pre[MAX_ST + 1];    // prefix over super tiles of the task's slice counts
+    bool full;                 // the task covers every row block
+};
+
+// The drawn row blocks of a visit with their row prefixes (serial refresh).
+struct VisitRows {
+    int nvb;
+    int vb[BCT_MAX_M];
+    int vpre[BCT_MAX_M + 1];
+};
+
+// Everything a task of the per-task path needs before phase 1: its TaskDev,
+// its panel, the runs of its row-block mask and its visit's drawn rows.  On
+// the device one thread builds it, a chain of dependent loads (~6 us); when
+// the host knows the masks (bct_run_epoch) it builds every task's with the
+// plan and each CTA copies it into shared memory in one pass.
+struct alignas(16) TaskPrep {
+    TaskDev T;
+    PanelDev P;
+    Runs R;
+    VisitRows V;
 };
 
 struct EpochParams {
@@ -164,6 +203,7 @@ struct EpochParams {
     unsigned int *bar;         // grid barrier word
     unsigned int *ticket;      // last-block counter
     long long *timeline;       // optional phase timestamps (BCT_TIMELINE=1)
+    const struct TaskPrep *prep;  // per-task path: host-built set-up of every task (hdr.host_prep)
 };
 
 struct bct_ctx_s;
