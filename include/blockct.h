@@ -55,6 +55,9 @@ typedef struct bct_ctx bct_ctx;
 enum { BCT_OK = 0, BCT_EINVAL = -1, BCT_ECUDA = -2, BCT_ENOMEM = -3, BCT_ESCHEDULE = -4 };
 enum { BCT_F64 = 0, BCT_F32 = 1 };                          /* value storage */
 enum { BCT_SERIAL_FAITHFUL = 0, BCT_PARALLEL = 1 };         /* executor.py:37 */
+/* whole-system baselines (solvers.py:283-379): sweep kind and scaling rule */
+enum { BCT_ROW_ACTION = 0, BCT_COLUMN_ACTION = 1 };
+enum { BCT_M_IDENTITY = 0, BCT_M_SUM_INVERSE = 1, BCT_M_NORM_INVERSE = 2 };   /* M_RULES */
 enum { BCT_COMMIT = 1, BCT_METRICS = 2, BCT_SHARDED = 4 };  /* bct_run_epoch flags */
 enum { BCT_IMPORTANCE = 0, BCT_RANDOM = 1, BCT_MIXED = 2 }; /* sampling.py:25 */
 
@@ -229,6 +232,24 @@ int bct_debug_timeline(bct_ctx *ctx, long long *out, int64_t n_tasks, int32_t *g
  * then holds the global |y - S|^2, |x|^2, |x_t - x|^2.  Asynchronous when
  * resid_sq is NULL, else it synchronises and returns |y - S|^2. */
 int bct_finish_sharded(bct_ctx *ctx, int32_t flags, double *resid_sq);
+
+/*
+ * Whole-system cyclic baselines, replacing run_row_action /
+ * run_column_action (solvers.py:317-379) on the context's own A (every panel
+ * must be owned).  bct_baseline_init assembles A as a device CSR + CSC in
+ * BlockSystem.to_scipy's order (projector.py:779-793) on first use, computes
+ * the scaling (rows for BCT_ROW_ACTION, columns for BCT_COLUMN_ACTION; m_rule
+ * as BaselineParams.m_rule) and resets the baseline state: x = 0 and, for the
+ * column action, r = y (bct_set_y first).  bct_baseline_epoch runs one sweep
+ * over every block in partition order and returns |y|^2, |y - y_est|^2,
+ * |x_t|^2, |x_t - x|^2 (y_est = A x for the row action, y - r for the column
+ * action; the x_t terms are NaN without bct_set_x_true).  bct_baseline_get_x
+ * copies x out in global voxel order.  Results are bitwise equal to the
+ * reference's scipy sweeps.  The GCSGD state (x, r, z) is not touched.
+ */
+int bct_baseline_init(bct_ctx *ctx, int32_t kind, int32_t m_rule);
+int bct_baseline_epoch(bct_ctx *ctx, double omega, double *norms4);
+int bct_baseline_get_x(bct_ctx *ctx, double *x);
 
 #ifdef __cplusplus
 }

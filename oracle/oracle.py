@@ -14,6 +14,9 @@ restatement of its numba kernels (blockct_oracle.c):
 * ``oracle_run_epoch``      <- executor.py:128-253 (EpochExecutor.run_epoch)
 * ``oracle_commit_epoch``   <- solvers.py:180-185
 * ``oracle_run_gcsgd``      <- solvers.py:188-269
+* ``oracle_row_action`` / ``oracle_column_action`` <- solvers.py:303-379 (the
+                               whole-system baselines, on ``OracleSystem.to_scipy``
+                               <- projector.py:779-793)
 * ``pb_trig`` / ``OracleSystem.parallel_beam`` <- the parallel-beam harness of
                                SURVEY §8c (reference tracer on strip panels).
 
@@ -302,6 +305,18 @@ class OracleSystem:
         for j in range(self.n_col_blocks):
             lib().oracle_zsum(z[j], self.l2g[j], self.rbp[j], ids, ids.size, out)
 
+    def to_scipy(self):
+        """projector.py:779-793: COO of every panel -> CSR."""
+        import scipy.sparse as sp
+        rows, cols, vals = [], [], []
+        for j in range(self.n_col_blocks):
+            rows.append(np.repeat(self.l2g[j], np.diff(self.indptr[j])))
+            cols.append(self.vidx[j][self.cols[j]])
+            vals.append(self.data[j])
+        mat = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                            shape=(self.n_measurements, self.n_voxels))
+        return mat.tocsr()
+
     def dense(self):
         A = np.zeros((self.n_measurements, self.n_voxels))
         for j in range(self.n_col_blocks):
@@ -535,3 +550,60 @@ def oracle_run_gcsgd(system, y, epochs, b, alpha=1.0, gamma=1.0, group_size=1,
         if callback is not None:
             callback(epoch, state, row)
     return state.x.copy(), rows
+
+
+# ---------------------------------------------------------------------------
+# whole-system baselines (solvers.py:303-379)
+# ---------------------------------------------------------------------------
+
+def _safe_inverse(v):
+    """solvers.py:303-308."""
+    v = np.asarray(v, dtype=np.float64).ravel()
+    out = np.zeros_like(v)
+    nz = v > 0.0
+    out[nz] = 1.0 / v[nz]
+    return out
+
+
+def _scaling(sub, rule, axis):
+    if rule == "identity":
+        return np.ones(sub.shape[1 - axis])
+    if rule == "sum_inverse":
+        return _safe_inverse(np.asarray(sub.sum(axis=axis)))
+    return _safe_inverse(np.asarray(sub.multiply(sub).sum(axis=axis)))
+
+
+def oracle_row_action(system, y, epochs, omega, m_rule="norm_inverse"):
+    """solvers.py:317-346: per row block in partition order,
+    x += omega * A_I^T (M (y_I - A_I x)).  Returns x and the per-epoch A x."""
+    A = system.to_scipy()
+    blocks = []
+    for meas in system.row_meas:
+        A_i = A[meas]
+        blocks.append((A_i, meas, _scaling(A_i, m_rule, 1)))
+    x = np.zeros(system.n_voxels)
+    est = []
+    for _ in range(epochs):
+        for A_i, meas, m_diag in blocks:
+            res = y[meas] - A_i @ x
+            x += omega * (A_i.T @ (m_diag * res))
+        est.append(A @ x)
+    return x, est
+
+
+def oracle_column_action(system, y, epochs, omega, m_rule="norm_inverse"):
+    """solvers.py:349-379: per column block in partition order,
+    dx = omega * (D (A_J^T r)); x_J += dx; r -= A_J dx.  Returns x and r."""
+    A = system.to_scipy().tocsc()
+    blocks = []
+    for vox in system.vidx:
+        A_j = A[:, vox]
+        blocks.append((A_j, vox, _scaling(A_j, m_rule, 0)))
+    x = np.zeros(system.n_voxels)
+    r = np.asarray(y, dtype=np.float64).copy()
+    for _ in range(epochs):
+        for A_j, vox, d_diag in blocks:
+            dx = omega * (d_diag * (A_j.T @ r))
+            x[vox] += dx
+            r -= A_j @ dx
+    return x, r

@@ -3,6 +3,7 @@ arXiv 1709.00953), a drop-in for the reference package ``blockct``'s solver
 path: hand-written sm_100a kernels behind a C ABI (include/blockct.h), with
 the reference's Python solver API on the host.  No CPU fallback."""
 
+from .baselines import BaselineParams, run_column_action, run_row_action
 from .errors import (BlockCTError, BudgetExceededError, ConfigurationError, DivergenceError,
                      ExecutorError, GeometryError, NativeLibraryError, ScheduleError)
 from .executor import EpochExecutor, EpochStats, TaskDescriptor
@@ -28,4 +29,5 @@ __all__ = [
     "select_row_blocks",
     "SolverParams", "SolverState", "audit_state", "basic_iteration", "run_csgd", "run_gcsgd",
     "DeviceBlockSystem", "PanelArrays",
+    "BaselineParams", "run_row_action", "run_column_action",
 ]

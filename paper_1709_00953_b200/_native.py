@@ -21,6 +21,8 @@ BCT_F64, BCT_F32 = 0, 1
 MODES = {"serial_faithful": 0, "parallel": 1}
 BCT_COMMIT, BCT_METRICS, BCT_SHARDED = 1, 2, 4
 STRATEGY_CODES = {"importance": 0, "random": 1, "mixed": 2}
+BCT_ROW_ACTION, BCT_COLUMN_ACTION = 0, 1
+M_RULE_CODES = {"identity": 0, "sum_inverse": 1, "norm_inverse": 2}
 
 _i32 = ctypes.c_int32
 _i64 = ctypes.c_int64
@@ -96,6 +98,9 @@ _SIGS = {
     "bct_exchange_buffer": [_p, _pp, ctypes.POINTER(_i64)],
     "bct_finish_sharded": [_p, _i32, _p],
     "bct_debug_timeline": [_p, _p, _i64, _p],
+    "bct_baseline_init": [_p, _i32, _i32],
+    "bct_baseline_epoch": [_p, _dbl, _p],
+    "bct_baseline_get_x": [_p, _p],
 }
 
 EXPORTED = tuple(_SIGS) + ("bct_last_error", "bct_version")

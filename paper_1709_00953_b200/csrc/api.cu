@@ -136,6 +136,14 @@ struct bct_ctx {
     int head = 0, tail = 0;           // ring: tail = oldest pending
     int grid = 0, block = 0;
     bool has_x_true = false;
+    // whole-system baselines (baseline.cu)
+    bct::BaselineMat bm;
+    bool bm_built = false;
+    int32_t bl_kind = -1;
+    double *bl_diag = nullptr, *bl_x = nullptr, *bl_r = nullptr, *bl_tmp = nullptr;
+    double *bl_part = nullptr, *bl_out = nullptr;
+    int32_t *bl_cb_of_vox = nullptr;
+    int64_t *bl_col_vox = nullptr;
     // device sampler (bct_sample_epoch)
     double *d_values = nullptr, *d_totals = nullptr, *d_exp = nullptr;
     int64_t d_exp_n = 0;
@@ -560,6 +568,7 @@ void destroy(bct_ctx *c)
 {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
+    bct::baseline_free(c->bm);
     for (void *p : c->allocs) cudaFree(p);
     for (int i = 0; i < 2; ++i) {
         if (c->h_pin[i]) cudaFreeHost(c->h_pin[i]);
@@ -1861,3 +1870,82 @@ int bct_sample_epoch(bct_ctx *c, int32_t mode, int32_t n_visits, const int32_t *
 }
 
 }  // extern "C"
+
+// ---- whole-system baselines (solvers.py:283-379; baseline.cu) -------------
+
+int bct_baseline_init(bct_ctx *c, int32_t kind, int32_t m_rule)
+{
+    if (!c) return BCT_EINVAL;
+    if (kind != BCT_ROW_ACTION && kind != BCT_COLUMN_ACTION)
+        return fail(c, BCT_EINVAL, "baseline kind %d", kind);
+    if (m_rule < BCT_M_IDENTITY || m_rule > BCT_M_NORM_INVERSE)
+        return fail(c, BCT_EINVAL, "m_rule %d", m_rule);
+    if (c->pb != 0 || c->pe != c->n_panels)
+        return fail(c, BCT_EINVAL, "baselines need every volume block on this context");
+    CK(cudaStreamSynchronize(c->stream));
+    if (!c->bm_built) {
+        CK(bct::baseline_build(c->dtype, c->h_panels.data(), c->np, c->d_gvox, c->n_meas, c->n_vox,
+                               c->bm, c->stream));
+        DALLOC(c->bl_diag, std::max(c->n_meas, c->n_vox));
+        DALLOC(c->bl_x, c->n_vox);
+        DALLOC(c->bl_r, c->n_meas);
+        DALLOC(c->bl_tmp, std::max(c->n_meas, c->n_vox));
+        DALLOC(c->bl_part, 4 * 148);
+        DALLOC(c->bl_out, 4);
+        std::vector<int32_t> cb(c->n_vox, -1);
+        for (int j = 0; j < c->n_panels; ++j)
+            for (int64_t q = c->col_ptr[j]; q < c->col_ptr[j + 1]; ++q) cb[c->col_vox[q]] = j;
+        DALLOC(c->bl_cb_of_vox, c->n_vox);
+        DALLOC(c->bl_col_vox, std::max<int64_t>((int64_t)c->col_vox.size(), 1));
+        CK(cudaMemcpy(c->bl_cb_of_vox, cb.data(), 4 * c->n_vox, cudaMemcpyHostToDevice));
+        if (!c->col_vox.empty())
+            CK(cudaMemcpy(c->bl_col_vox, c->col_vox.data(), 8 * c->col_vox.size(),
+                          cudaMemcpyHostToDevice));
+        c->bm_built = true;
+    }
+    CK(bct::baseline_scale(c->bm, kind, m_rule, c->bl_diag, c->stream));
+    CK(cudaMemsetAsync(c->bl_x, 0, 8 * c->n_vox, c->stream));
+    CK(cudaMemcpyAsync(c->bl_r, c->y, 8 * c->n_meas, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemsetAsync(c->bl_tmp, 0, 8 * std::max(c->n_meas, c->n_vox), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->bl_kind = kind;
+    return 0;
+}
+
+int bct_baseline_epoch(bct_ctx *c, double omega, double *norms4)
+{
+    if (!c) return BCT_EINVAL;
+    if (c->bl_kind < 0) return fail(c, BCT_EINVAL, "bct_baseline_init first");
+    if (!(omega > 0.0) || !std::isfinite(omega)) return fail(c, BCT_EINVAL, "omega %g", omega);
+    if (c->bl_kind == BCT_ROW_ACTION) {
+        for (int i = 0; i < c->m; ++i)   // row blocks in partition order
+            CK(bct::baseline_row_block(c->bm, c->d_rb_rows + c->rb_ptr[i],
+                                       c->rb_ptr[i + 1] - c->rb_ptr[i], i, c->rb_of_row, omega,
+                                       c->y, c->bl_diag, c->bl_tmp, c->bl_x, c->stream));
+    } else {
+        for (int j = 0; j < c->n_panels; ++j)   // volume blocks in partition order
+            CK(bct::baseline_col_block(c->bm, c->bl_col_vox + c->col_ptr[j],
+                                       c->col_ptr[j + 1] - c->col_ptr[j], j, c->bl_cb_of_vox,
+                                       omega, c->bl_diag, c->bl_tmp, c->bl_x, c->bl_r,
+                                       c->stream));
+    }
+    CK(bct::baseline_norms(c->bm, c->y, c->bl_r, c->bl_x, c->has_x_true ? c->x_true : nullptr,
+                           c->d_gvox, c->x_len, c->bl_kind == BCT_COLUMN_ACTION, c->bl_part,
+                           c->bl_out, c->stream));
+    double o[4];
+    CK(cudaMemcpyAsync(o, c->bl_out, sizeof o, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (!c->has_x_true) o[2] = o[3] = NAN;
+    if (norms4) memcpy(norms4, o, sizeof o);
+    return 0;
+}
+
+int bct_baseline_get_x(bct_ctx *c, double *x)
+{
+    if (!c || !x) return BCT_EINVAL;
+    if (c->bl_kind < 0) return fail(c, BCT_EINVAL, "bct_baseline_init first");
+    CK(cudaStreamSynchronize(c->stream));
+    if (int e = d2h_staged(c, x, c->bl_x, 8 * c->n_vox)) return e;
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}

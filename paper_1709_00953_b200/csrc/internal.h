@@ -232,6 +232,29 @@ struct Box {
 
 namespace bct {
 
+// whole-system baselines (baseline.cu): A as a device CSR and CSC, global
+// measurement rows x global voxel columns, in BlockSystem.to_scipy's order
+struct BaselineMat {
+    int64_t nnz = 0, n_meas = 0, n_vox = 0;
+    int64_t *row_ptr = nullptr, *col_ptr = nullptr;
+    int32_t *csr_col = nullptr, *csc_row = nullptr;
+    double *csr_val = nullptr, *csc_val = nullptr;
+};
+cudaError_t baseline_build(int dtype, const PanelDev *h_panels, int np, const int32_t *d_gvox,
+                           int64_t n_meas, int64_t n_vox, BaselineMat &M, cudaStream_t s);
+void baseline_free(BaselineMat &M);
+cudaError_t baseline_scale(const BaselineMat &M, int kind, int rule, double *diag, cudaStream_t s);
+cudaError_t baseline_row_block(const BaselineMat &M, const int32_t *rows, int64_t n_rows, int blk,
+                               const int32_t *rb_of_row, double omega, const double *y,
+                               const double *mdiag, double *res, double *x, cudaStream_t s);
+cudaError_t baseline_col_block(const BaselineMat &M, const int64_t *vox, int64_t n_vox_blk,
+                               int blk, const int32_t *cb_of_vox, double omega,
+                               const double *ddiag, double *dx, double *x, double *r,
+                               cudaStream_t s);
+cudaError_t baseline_norms(const BaselineMat &M, const double *y, const double *r, const double *x,
+                           const double *x_true, const int32_t *gvox, int64_t x_len, int use_r,
+                           double *part, double *out4, cudaStream_t s);
+
 cudaError_t scan_trace_counts(const ScanDev &S, const int32_t *L, int64_t n, const Box &B,
                               int32_t *counts, int32_t *bad, cudaStream_t s);
 cudaError_t scan_fill(const ScanDev &S, const int32_t *l2g, const int32_t *indptr, int64_t n_hit,

@@ -11,5 +11,5 @@ NVCC=/usr/local/cuda/bin/nvcc
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 $NVCC $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC "$@" -c epoch.cu -o /tmp/epoch_$NAME.o
 $NVCC $ARCH -shared -o ../_lib/libblockct_cuda_$NAME.so /tmp/epoch_$NAME.o ../_lib/builder.o \
-    ../_lib/layout.o ../_lib/sampler.o ../_lib/api.o
+    ../_lib/layout.o ../_lib/sampler.o ../_lib/baseline.o ../_lib/api.o
 echo ../_lib/libblockct_cuda_$NAME.so
