@@ -221,10 +221,19 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
 #define BCT_B_HINT 1
 #endif
 #ifndef BCT_B_PREFETCH
-#define BCT_B_PREFETCH 0         // >0: phase B prefetches slice f+N into L2 (profiling)
+#define BCT_B_PREFETCH 8         // phase B prefetches the values of slice f+8 into L2 (0: off)
 #endif
 #ifndef BCT_B_SLICE_COST
 #define BCT_B_SLICE_COST 120     // phase-B balance: entries-equivalent cost of one slice
+#endif
+#ifndef BCT_A_PF_VALUES_ONLY
+#define BCT_A_PF_VALUES_ONLY 0
+#endif
+#ifndef BCT_A_PF_LEN
+#define BCT_A_PF_LEN 16          // vector rows per phase-A prefetch request set
+#endif
+#ifndef BCT_A_PREFETCH
+#define BCT_A_PREFETCH 8         // phase A prefetches its slice 8 vector rows ahead into L2 (0: off)
 #endif
 #ifndef BCT_P1_G
 #define BCT_P1_G 4               // phase-A FP32 loop: vector rows per load group
@@ -641,6 +650,26 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
                 int u = lo + sub;
 #pragma unroll 1
                 for (; u < hi; u += R * wps) {
+#if BCT_A_PREFETCH
+                    // the slice's vector rows BCT_A_PREFETCH ahead (one group's
+                    // worth) into L2: bulk requests hold bytes in flight
+                    // without registers
+                    // (BCT_A_PF_LEN: a multiple of the R * wps rows one
+                    // iteration consumes; longer requests every few iterations)
+                    if (sub == 0 && lane == 0 &&
+                        ((u - lo) / (R * wps)) % max(1, BCT_A_PF_LEN / (R * wps)) == 0) {
+                        const int v0 = u + BCT_A_PREFETCH;
+                        const int v1 = min(hi, v0 + BCT_A_PF_LEN);
+                        if (v0 < v1) {
+                            const int64_t e0 = base + (int64_t)v0 * 256, n = (int64_t)(v1 - v0) * 256;
+                            prefetch_l2(reinterpret_cast<const float *>(tv) + e0, (uint32_t)(4 * n));
+#if !BCT_A_PF_VALUES_ONLY
+                            prefetch_l2(toff + e0, (uint32_t)n);
+                            prefetch_l2(tbase + (e0 >> 3), (uint32_t)(n >> 2));
+#endif
+                        }
+                    }
+#endif
                     float4 a[R][2];
                     uint2 o[R];
                     int b0[R];
