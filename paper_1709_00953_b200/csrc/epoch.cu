@@ -223,6 +223,9 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
 #ifndef BCT_B_PREFETCH
 #define BCT_B_PREFETCH 8         // phase B prefetches the values of slice f+8 into L2 (0: off)
 #endif
+#ifndef BCT_B_PF_CODES
+#define BCT_B_PF_CODES 0         // 1: the phase-B prefetch also covers the slice's step codes
+#endif
 #ifndef BCT_B_SLICE_COST
 #define BCT_B_SLICE_COST 120     // phase-B balance: entries-equivalent cost of one slice
 #endif
@@ -237,6 +240,9 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
 #endif
 #ifndef BCT_P1_G
 #define BCT_P1_G 4               // phase-A FP32 loop: vector rows per load group
+#endif
+#ifndef BCT_FC_TAIL_GROUP
+#define BCT_FC_TAIL_GROUP 0      // 1: phase-B coded tail (< BCT_FC_G vectors) as one predicated group
 #endif
 #ifndef BCT_FC_G
 #define BCT_FC_G 8               // phase-B coded loop: vectors per load group (4 or 8)
@@ -480,6 +486,40 @@ __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv,
                 ax = fma(v[j][e], (A)a.y, ax);
             }
     }
+#if BCT_FC_TAIL_GROUP
+    // the last < FG vectors as one predicated group: every load issued
+    // before the first gather (one vector at a time exposed the load
+    // latency per vector)
+    if (kv4 < nvec) {
+        const int nr = nvec - kv4;
+        uint32_t word[FG / 4];
+#pragma unroll
+        for (int w = 0; w < FG / 4; ++w)
+            word[w] = 4 * w < nr ? ld_code(cw + ((kv4 >> 2) + w) * 32) : 0u;
+        V v[FG][4];
+#pragma unroll
+        for (int j = 0; j < FG; ++j) {
+            if (j < nr) {
+                ld4raw(fv + base + (((kv4 + j) * 32 + lane) << 2), v[j]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) v[j][e] = V(0);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < FG; ++j) {
+            if (j >= nr) break;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int code = (word[j >> 2] >> (8 * (j & 3) + 2 * e)) & 3;
+                q += ((code & 1) ? sy : 0) + (code >> 1) * wst;
+                const GS a = gs[swz_idx(q, shift)];
+                t = fma(v[j][e], (A)a.x, t);
+                ax = fma(v[j][e], (A)a.y, ax);
+            }
+        }
+    }
+#else
     for (int j = 0; kv4 + j < nvec; ++j) {
         const int kv = kv4 + j;
         const uint32_t word = ld_code(cw + (kv >> 2) * 32);
@@ -494,6 +534,7 @@ __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv,
             ax = fma(v[e], (A)a.y, ax);
         }
     }
+#endif
     return make_double2((double)t, (double)ax);
 }
 
@@ -1178,6 +1219,13 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                     const int sp = sl + BCT_B_PREFETCH;
                     const int e0 = __ldg(P.slice_start + sp), e1 = __ldg(P.slice_start + sp + 1);
                     prefetch_l2(fv + e0, (uint32_t)(e1 - e0) * (uint32_t)sizeof(V));
+#if BCT_B_PF_CODES
+                    // and its step-code words: (k/4)*32 + lane past
+                    // slice_start/16 + 24*slice (128 B per 4 vectors)
+                    if (coded && e1 > e0)
+                        prefetch_l2(P.fcode + (e0 >> 4) + 24 * sp,
+                                    (uint32_t)((((e1 - e0) >> 7) + 3) >> 2) * 128u);
+#endif
                 }
                 const int nvec = (bend - base) >> 7;
                 if (replay) {
