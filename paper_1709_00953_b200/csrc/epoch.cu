@@ -229,6 +229,9 @@ __device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int 
 #ifndef BCT_B_SLICE_COST
 #define BCT_B_SLICE_COST 120     // phase-B balance: entries-equivalent cost of one slice
 #endif
+#ifndef BCT_ROW_ORDER
+#define BCT_ROW_ORDER 1          // batched phase B stores segment partials in row order (P.rq)
+#endif
 #ifndef BCT_A_PF_VALUES_ONLY
 #define BCT_A_PF_VALUES_ONLY 0
 #endif
@@ -1197,22 +1200,29 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             };
             const bool coded = P.fcode != nullptr && !BCT_NO_FCODE_K;
             int f = grab();
-            int base = 0, bend = 0, hdr = 0;
+            int base = 0, bend = 0, hdr = 0, dst = 0;
+            // a lane's partial goes to its segment's row-order position
+            // (P.rq): phase C then reads each row's partials contiguously
+            auto dst_of = [&](int slc) {
+                return BCT_ROW_ORDER ? __ldg(P.rq + (int64_t)slc * 32 + lane) : slc * 32 + lane;
+            };
             if (f < ge) {
                 const int sl = f - T.slice_pre;
                 base = __ldg(P.slice_start + sl);
                 bend = __ldg(P.slice_start + sl + 1);
                 if (coded) hdr = __ldg(P.fq0 + (int64_t)sl * 32 + lane);
+                dst = dst_of(sl);
             }
             while (f < ge) {
                 const int sl = f - T.slice_pre;
                 const int fn = grab();
-                int nbase = 0, nbend = 0, nhdr = 0;
+                int nbase = 0, nbend = 0, nhdr = 0, ndst = 0;
                 if (fn < ge) {
                     const int sn = fn - T.slice_pre;
                     nbase = __ldg(P.slice_start + sn);
                     nbend = __ldg(P.slice_start + sn + 1);
                     if (coded) nhdr = __ldg(P.fq0 + (int64_t)sn * 32 + lane);
+                    ndst = dst_of(sn);
                 }
                 if (BCT_B_PREFETCH > 0 && lane == 0 && f + BCT_B_PREFETCH < ge) {
                     // the slice another warp takes next round: into L2 now
@@ -1230,12 +1240,12 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                 const int nvec = (bend - base) >> 7;
                 if (replay) {
                     const double2 rp = replay_segment<V, GS>(P, (int64_t)sl * 32 + lane, gs, y0, wid);
-                    spart[(int64_t)sl * 32 + lane] = PT{(decltype(PT::x))rp.x, (decltype(PT::x))rp.y};
+                    if (dst >= 0) spart[dst] = PT{(decltype(PT::x))rp.x, (decltype(PT::x))rp.y};
                 } else if (coded && !__any_sync(0xffffffffu, (hdr >> 17) & 1)) {
                     // step-coded slice (a lane flagged in fq0 bit 17 keeps its
                     // 16-bit indices: the indexed loop below)
                     const double2 cp = coded_segment<V, GS>(P, fv, sl, base, nvec, lane, wst, gs, hdr);
-                    spart[(int64_t)sl * 32 + lane] = PT{(decltype(PT::x))cp.x, (decltype(PT::x))cp.y};
+                    if (dst >= 0) spart[dst] = PT{(decltype(PT::x))cp.x, (decltype(PT::x))cp.y};
                 } else {
                     V t = V(0), ax = V(0);   // FP32 mode: FP32 lane partials (see coded_segment)
 #pragma unroll P2U
@@ -1252,12 +1262,13 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                             ax = fma(v[q], (V)a.y, ax);
                         }
                     }
-                    spart[(int64_t)sl * 32 + lane] = PT{(decltype(PT::x))t, (decltype(PT::x))ax};
+                    if (dst >= 0) spart[dst] = PT{(decltype(PT::x))t, (decltype(PT::x))ax};
                 }
                 f = fn;
                 base = nbase;
                 bend = nbend;
                 hdr = nhdr;
+                dst = ndst;
             }
             fu = ge;
         }
@@ -1322,12 +1333,14 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                 for (int s = 0; s < nmax; ++s) {
                     int pos[CR];
 #pragma unroll
-                    for (int j = 0; j < CR; ++j) pos[j] = q0[j] + s < q1[j] ? __ldg(P.rpos + q0[j] + s) : -1;
+                    for (int j = 0; j < CR; ++j)
+                        pos[j] = q0[j] + s < q1[j] ? (BCT_ROW_ORDER ? q0[j] + s : __ldg(P.rpos + q0[j] + s))
+                                                   : -1;
 #pragma unroll
                     for (int j = 0; j < CR; ++j)
                         if (pos[j] >= 0) {
                             // written in phase B of this launch: L2-coherent load
-                            const PT a = __ldcg(spart + pos[j]);   // SELL-order partials
+                            const PT a = __ldcg(spart + pos[j]);   // row-order partials
                             t[j] += (double)a.x;
                             ax[j] += (double)a.y;
                         }

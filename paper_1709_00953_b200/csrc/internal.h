@@ -79,6 +79,8 @@ struct PanelDev {
     const uint32_t *fcode;     // word (slice_start[sl]/16 + 24*sl) + (k/4)*32 + lane holds
                                // vectors k..k+3 of the lane, a byte per vector
     const int32_t *fq0;        // per SELL slot: first voxel (logical) | (s < 0) << 16
+    const int32_t *rq;         // per SELL slot: its segment's position in rseg (-1: empty
+                               // lane): the batched phase B stores partials in row order
     int32_t st_h;              // set-up input: strip height (0: generic placement)
 };
 

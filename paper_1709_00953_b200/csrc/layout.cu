@@ -348,6 +348,12 @@ __global__ void seg_of_entry_k(const int32_t *perm, const int32_t *incl, int64_t
     if (q < nnz) out[perm[q]] = incl[q] - 1;
 }
 
+__global__ void rq_k(const int32_t *rpos, int32_t n_seg, int32_t *rq)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < n_seg) rq[rpos[q]] = q;
+}
+
 __global__ void rpos_k(const int32_t *rseg, const int32_t *seg_slice, const int32_t *seg_lane,
                        int32_t n_seg, int32_t *rpos)
 {
@@ -922,6 +928,13 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     LNN(rpos);
     if (n_seg > 0)
         rpos_k<<<nb(n_seg, 256), 256, 0, s>>>(rseg, seg_slice, seg_lane, n_seg, rpos);
+    // and its inverse per SELL slot: the batched phase B stores each partial
+    // at its row-order position, so phase C reads every row's partials
+    // contiguously
+    int32_t *rq = K.get<int32_t>((int64_t)n_slices * 32 + 1);
+    LNN(rq);
+    LCK(cudaMemsetAsync(rq, 0xff, 4 * ((int64_t)n_slices * 32 + 1), s));
+    if (n_seg > 0) rq_k<<<nb(n_seg, 256), 256, 0, s>>>(rpos, n_seg, rq);
     LCK(cudaGetLastError());
 
     // ================= CSC with tile bands =================
@@ -1078,6 +1091,7 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     P.rseg_ptr = rseg_ptr;
     P.rseg = rseg;
     P.rpos = rpos;
+    P.rq = rq;
     P.tvals = tvals;
     P.csl_start = csl_start;
     P.n_cslices = n_cslices;
