@@ -145,32 +145,31 @@ __device__ double block_sum_all(double v, double *sh)
 // and the task's units per super tile.
 __device__ void build_runs(const uint64_t *mask, int m, const PanelDev &P, Runs &R)
 {
-    {   // (restated on the host: api.cu host_prep)
-        int n = 0, acc = 0;
-        int i = 0;
-        while (i < m) {
-            if (!mask_has(mask, i)) { ++i; continue; }
-            int s = i;
-            while (i < m && mask_has(mask, i)) ++i;
-            R.i0[n] = s;
-            R.i1[n] = i;
-            R.rows0[n] = P.rbp[s];
-            R.pre[n] = acc;
-            acc += P.rbp[i] - P.rbp[s];
-            ++n;
-        }
+    // one thread; restated on the host (api.cu host_prep) when the masks are known
+    int n = 0, acc = 0;
+    int i = 0;
+    while (i < m) {
+        if (!mask_has(mask, i)) { ++i; continue; }
+        int s = i;
+        while (i < m && mask_has(mask, i)) ++i;
+        R.i0[n] = s;
+        R.i1[n] = i;
+        R.rows0[n] = P.rbp[s];
         R.pre[n] = acc;
-        R.n = n;
-        int uacc = 0;
-        for (int st = 0; st < P.n_st; ++st) {
-            R.st_pre[st] = uacc;
-            const int32_t *sb = P.stbs + st * (m + 1);
-            for (int q = 0; q < n; ++q) uacc += sb[R.i1[q]] - sb[R.i0[q]];
-        }
-        R.st_pre[P.n_st] = uacc;
-        R.nst = P.n_st;
-        R.full = (n == 1 && R.i0[0] == 0 && R.i1[0] == m);
+        acc += P.rbp[i] - P.rbp[s];
+        ++n;
     }
+    R.pre[n] = acc;
+    R.n = n;
+    int uacc = 0;
+    for (int st = 0; st < P.n_st; ++st) {
+        R.st_pre[st] = uacc;
+        const int32_t *sb = P.stbs + st * (m + 1);
+        for (int q = 0; q < n; ++q) uacc += sb[R.i1[q]] - sb[R.i0[q]];
+    }
+    R.st_pre[P.n_st] = uacc;
+    R.nst = P.n_st;
+    R.full = (n == 1 && R.i0[0] == 0 && R.i1[0] == m);
 }
 
 __device__ void prep_task(const EpochParams &p, int k, TaskPrep &out)
