@@ -485,7 +485,18 @@ def oracle_run_epoch(system, state, loops, mode="serial_faithful", workers=1):
             _commit_visit(system, state, run, stats)
             _refresh(system, state, run["sel"])
     else:
-        runs = [_run_visit(system, j, groups, state.r, snaps[j], workers) for j, groups in loops]
+        # parallel mode: every visit reads the epoch-start r and its own x_J
+        # snapshot, so the visits fan out over threads (executor.py:194-198
+        # fans the runs over worker_count threads the same way; the C kernel
+        # runs without the GIL).  Commits stay in plan order below.
+        if workers > 1 and len(loops) > 1:
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(workers) as pool:
+                runs = list(pool.map(lambda jg: _run_visit(system, jg[0], jg[1], state.r,
+                                                           snaps[jg[0]], 1), loops))
+        else:
+            runs = [_run_visit(system, j, groups, state.r, snaps[j], workers)
+                    for j, groups in loops]
         for run in runs:
             _commit_visit(system, state, run, stats)
         if runs:

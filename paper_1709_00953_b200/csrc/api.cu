@@ -95,7 +95,8 @@ struct bct_ctx {
     double *d_xstage = nullptr;    // [n_vox] global-order staging of image transfers
     char *h_pin[2] = {nullptr, nullptr};   // pinned host chunks for state transfers
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
-    size_t smem = 0;
+    size_t smem = 0;                 // dynamic shared memory of the phase buffers
+    size_t smem_total = 0;           // + the per-task record
     int32_t band_cap = 0, band_dbuf = 1;
     cudaStream_t stream = nullptr;
     // host mirrors
@@ -122,8 +123,14 @@ struct bct_ctx {
     int32_t *statuses = nullptr;
     EpochOut *out = nullptr;
     unsigned int *bar = nullptr, *ticket = nullptr;
-    TaskPrep *d_prep = nullptr;      // [task_cap] per-task set-up (host_prep)
-    TaskPrep *h_prep = nullptr;      // pinned
+    char *d_prep = nullptr;          // [task_cap] per-task records (host_prep), pd.bytes() apart
+    char *h_prep = nullptr;          // pinned
+    PrepDims pd{};                   // record dimensions (finalize)
+    int32_t prep_off = 0;            // byte offset of the record in dynamic shared memory
+    int32_t sc_bound = 1;            // bound on super tiles per panel (record size at layout)
+    int mw = 1;                      // 64-bit words per row-block set
+    uint64_t *d_masks = nullptr;     // [(1 + 2 task_cap) mw] epoch mask, task / visit masks
+    uint64_t *h_masks = nullptr;     // pinned
     unsigned long long *audit2 = nullptr;
     EpochHeader *d_hdr = nullptr;
     TaskDev *d_tasks = nullptr;
@@ -157,6 +164,26 @@ struct bct_ctx {
 };
 
 static std::string g_create_err;
+
+// Every entry point runs on its context's device and leaves the calling
+// thread's current device as it found it (one process may hold contexts on
+// several GPUs, and the caller -- e.g. torch -- keeps its own current device).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess)
+            prev = cur;
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard &) = delete;
+    DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
+#define DEVICE_GUARD(c) DeviceGuard device_guard_((c)->device)
 
 namespace {
 
@@ -203,6 +230,21 @@ void free_tmp(bct_ctx *c, void *p)
 }
 
 int set_mask(uint64_t *mask, int i) { mask[i >> 6] |= 1ull << (i & 63); return 0; }
+bool has_bit(const uint64_t *mask, int i) { return ((mask[i >> 6] >> (i & 63)) & 1ull) != 0; }
+
+// Dynamic shared memory the epoch kernel's phase buffers may use: the SM's
+// per-CTA opt-in limit less the kernel's static arrays and the per-task
+// record (PrepDims for this context's m and a bound on super tiles), and at
+// most SMEM_BUDGET (the shapes were tuned under it).
+size_t smem_budget(const bct_ctx *c, int sc)
+{
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    const size_t stat = bct::epoch_static_smem(c->dtype);
+    PrepDims d{c->m / 2 + 1, sc, c->m, 0};
+    const int64_t room = (int64_t)optin - (int64_t)stat - d.bytes() - 16;
+    return (size_t)std::max<int64_t>(0, std::min<int64_t>(room, (int64_t)SMEM_BUDGET));
+}
 
 // Voxel placement of a panel: device positions grouped into super tiles of
 // <= ST_VOXELS voxels and the phase-1 tile order (16 per tile).  A strip of
@@ -277,6 +319,9 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     PanelDev &P = c->h_panels[lp];
     const int j = c->pb + lp;
     const int32_t n_cols = (int32_t)(c->col_ptr[j + 1] - c->col_ptr[j]);
+    if (nnz >= (1ll << 31) || n_cols >= (1ll << 30))
+        return fail(c, BCT_EINVAL, "panel %d: %lld entries / %d voxels exceed 32-bit panel offsets",
+                    j, (long long)nnz, n_cols);
     int32_t *d_rbp = nullptr, *d_d2c = nullptr;
     DALLOC(d_rbp, c->m + 1);
     DALLOC(d_d2c, n_cols);
@@ -294,6 +339,9 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
             shapes = getenv("BCT_TILE_NBUF1") ? std::vector<Shape>{{a, b2, 1}, {4, 8, 1}}
                                               : std::vector<Shape>{{a, b2, 2}, {a, b2, 1}, {4, 8, 1}};
     }
+    // record bound: super tiles of any placement hold >= ST_VOXELS/4 voxels
+    c->sc_bound = std::max<int32_t>(c->sc_bound, (int32_t)((4ll * n_cols) / st_voxels(c->dtype) + 2));
+    const size_t budget = smem_budget(c, c->sc_bound);
     Placement pl;
     // matrix-free phase B is opt-in (BCT_REPLAY=1): regenerating the values
     // costs more FP64 issue than streaming them saves
@@ -318,7 +366,7 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
                                  d_rbp, pl.c2d, pl.st_ptr, pl.corder, th * tw, Q, kept, err,
                                  c->stream, seg_of))
             return fail(c, BCT_ENOMEM, "panel %d layout: %s", j, err.c_str());
-        if ((size_t)shapes[si].nbuf * Q.band_max * 8 + bct::PHASE1_RED_BYTES <= SMEM_BUDGET ||
+        if ((size_t)shapes[si].nbuf * Q.band_max * 8 + bct::PHASE1_RED_BYTES <= budget ||
             si + 1 == shapes.size()) {
             P = Q;
             c->allocs.insert(c->allocs.end(), kept.begin(), kept.end());
@@ -331,6 +379,9 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
         }
         for (void *q : kept) cudaFree(q);
     }
+    if (P.n_st > c->sc_bound)
+        return fail(c, BCT_EINVAL, "panel %d: %d super tiles exceed the record bound %d", j,
+                    P.n_st, c->sc_bound);
     CK(cudaMemcpy(d_d2c, pl.d2c.data(), 4 * n_cols, cudaMemcpyHostToDevice));
     if (replay && pl.st_w > 0) {
         // walk states of the forward segments: phase B regenerates the values
@@ -491,15 +542,27 @@ int finalize(bct_ctx *c)
     DALLOC(c->seg_part, 2 * 4 * c->max_seg + 2);   // TASK_SPLIT (epoch.cu) partials per lane
     // two band buffers when they fit, else one (staging then serializes)
     // phase-1 bands (double-buffered when they fit) + the tile reduction area
-    c->band_dbuf = (2 * (size_t)c->band_cap * 8 + bct::PHASE1_RED_BYTES <= SMEM_BUDGET &&
+    // per-task records: runs of a mask, super tiles, the visit's row blocks
+    int sc = 1;
+    for (int lp = 0; lp < c->np; ++lp) sc = std::max(sc, c->h_panels[lp].n_st);
+    c->pd = PrepDims{c->m / 2 + 1, sc, c->m, 0};
+    c->mw = mask_words(c->m);
+    const size_t budget = smem_budget(c, sc);
+    c->band_dbuf = (2 * (size_t)c->band_cap * 8 + bct::PHASE1_RED_BYTES <= budget &&
                     !getenv("BCT_TILE_NBUF1")) ? 1 : 0;
     c->smem = std::max<size_t>(c->smem, (size_t)c->band_cap * 8 * (c->band_dbuf ? 2 : 1) +
                                             bct::PHASE1_RED_BYTES);
     c->smem = std::max<size_t>(c->smem, 1024 * 12 + 64);
-    if (c->smem > 227 * 1024)
-        return fail(c, BCT_EINVAL, "shared-memory need %zu B exceeds the SM (band %d slots)",
-                    c->smem, c->band_cap);
-    c->grid = bct::epoch_grid_size(c->dtype, c->device, c->smem, &c->block);
+    c->prep_off = (int32_t)((c->smem + 15) & ~(size_t)15);
+    c->smem_total = (size_t)c->prep_off + (size_t)c->pd.bytes();
+    {
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+        if (c->smem_total + bct::epoch_static_smem(c->dtype) > (size_t)optin)
+            return fail(c, BCT_EINVAL, "shared-memory need %zu B exceeds the SM (band %d slots, "
+                        "m %d)", c->smem_total, c->band_cap, c->m);
+    }
+    c->grid = bct::epoch_grid_size(c->dtype, c->device, c->smem_total, &c->block);
     DALLOC(c->part, 8 * (int64_t)c->grid + 8);
     DALLOC(c->out, 1);
     DALLOC(c->bar, 1);
@@ -538,9 +601,14 @@ int ensure_task_cap(bct_ctx *c, int64_t n)
     if (c->h_tasks) cudaFreeHost(c->h_tasks);
     if (c->d_prep) cudaFree(c->d_prep);
     if (c->h_prep) cudaFreeHost(c->h_prep);
+    if (c->d_masks) cudaFree(c->d_masks);
+    if (c->h_masks) cudaFreeHost(c->h_masks);
     CK(cudaMalloc((void **)&c->d_tasks, sizeof(TaskDev) * cap));
-    CK(cudaMalloc((void **)&c->d_prep, sizeof(TaskPrep) * cap));
-    CK(cudaHostAlloc((void **)&c->h_prep, sizeof(TaskPrep) * cap, cudaHostAllocDefault));
+    CK(cudaMalloc((void **)&c->d_prep, c->pd.bytes() * cap));
+    CK(cudaHostAlloc((void **)&c->h_prep, c->pd.bytes() * cap, cudaHostAllocDefault));
+    CK(cudaMalloc((void **)&c->d_masks, 8 * (size_t)c->mw * (1 + 2 * cap)));
+    CK(cudaHostAlloc((void **)&c->h_masks, 8 * (size_t)c->mw * (1 + 2 * cap),
+                     cudaHostAllocDefault));
     CK(cudaMalloc((void **)&c->mus, 8 * cap));
     CK(cudaMalloc((void **)&c->statuses, 4 * cap));
     CK(cudaHostAlloc((void **)&c->h_tasks, sizeof(TaskDev) * cap, cudaHostAllocDefault));
@@ -583,6 +651,8 @@ void destroy(bct_ctx *c)
     if (c->h_tasks) cudaFreeHost(c->h_tasks);
     if (c->d_prep) cudaFree(c->d_prep);
     if (c->h_prep) cudaFreeHost(c->h_prep);
+    if (c->d_masks) cudaFree(c->d_masks);
+    if (c->h_masks) cudaFreeHost(c->h_masks);
     if (c->h_hdr) cudaFreeHost(c->h_hdr);
     for (int s = 0; s < RING; ++s) {
         Slot &S = c->slots[s];
@@ -627,6 +697,7 @@ int bct_version(void) { return 2; }
 int bct_create(const bct_system_desc *d, const bct_panel *panels, bct_ctx **out)
 {
     if (!d || !panels || !out) return fail(nullptr, BCT_EINVAL, "null argument");
+    DeviceGuard device_guard_(d->device);
     *out = nullptr;
     int r = check_common_desc(nullptr, d->m, d->n_panels, d->panel_begin, d->panel_end, d->dtype);
     if (r) return r;
@@ -713,6 +784,7 @@ int bct_create_parallel_beam(const bct_pb_desc *d, bct_ctx **out)
 {
     if (!d || !out || !d->cos_views || !d->sin_views)
         return fail(nullptr, BCT_EINVAL, "null argument");
+    DeviceGuard device_guard_(d->device);
     *out = nullptr;
     int r = check_common_desc(nullptr, d->m, d->nc, d->panel_begin, d->panel_end, d->dtype);
     if (r) return r;
@@ -854,6 +926,7 @@ int bct_create_scan(const bct_scan_desc *d, bct_ctx **out)
     if (!d || !out || !d->poses || !d->row_block_ptr || !d->row_block_rows || !d->box_lo ||
         !d->box_hi || !d->table_values || !d->table_totals)
         return fail(nullptr, BCT_EINVAL, "null argument");
+    DeviceGuard device_guard_(d->device);
     *out = nullptr;
     int r = check_common_desc(nullptr, d->m, d->n_panels, d->panel_begin, d->panel_end, d->dtype);
     if (r) return r;
@@ -1016,6 +1089,8 @@ int bct_create_scan(const bct_scan_desc *d, bct_ctx **out)
 
 int bct_destroy(bct_ctx *c)
 {
+    if (!c) return 0;
+    DEVICE_GUARD(c);
     destroy(c);
     return 0;
 }
@@ -1023,6 +1098,7 @@ int bct_destroy(bct_ctx *c)
 int bct_info(const bct_ctx *c, int64_t *o)
 {
     if (!c || !o) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     o[0] = c->n_meas; o[1] = c->n_vox; o[2] = c->m; o[3] = c->n_panels;
     o[4] = c->pb; o[5] = c->pe; o[6] = c->nnz; o[7] = c->z_len;
     return 0;
@@ -1031,6 +1107,7 @@ int bct_info(const bct_ctx *c, int64_t *o)
 int bct_panel_info(const bct_ctx *c, int32_t j, int64_t *n_rows, int64_t *nnz, int64_t *n_cols)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (j < c->pb || j >= c->pe) return BCT_EINVAL;
     const PanelDev &P = c->h_panels[j - c->pb];
     if (n_rows) *n_rows = P.n_rows;
@@ -1045,6 +1122,7 @@ int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *i
                   int64_t *rbp, int64_t *l2g)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (j < c->pb || j >= c->pe) return fail(c, BCT_EINVAL, "panel %d not owned", j);
     int lp = j - c->pb;
     const PanelDev &P = c->h_panels[lp];
@@ -1107,6 +1185,7 @@ int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *i
 int bct_get_table(bct_ctx *c, double *values, double *totals)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (values) std::copy(c->table_values.begin(), c->table_values.end(), values);
     if (totals) std::copy(c->table_totals.begin(), c->table_totals.end(), totals);
     return 0;
@@ -1115,6 +1194,7 @@ int bct_get_table(bct_ctx *c, double *values, double *totals)
 int bct_get_stream(bct_ctx *c, void **s)
 {
     if (!c || !s) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     *s = (void *)c->stream;
     return 0;
 }
@@ -1236,21 +1316,35 @@ static int xvec_from_dev(bct_ctx *c, const double *src, double *xg)
 int bct_set_y(bct_ctx *c, const double *y)
 {
     if (!c || !y) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (int r = h2d_staged(c, c->y, y, 8 * c->n_meas)) return r;
     CK(cudaStreamSynchronize(c->stream));
     return 0;
 }
 
-int bct_set_x(bct_ctx *c, const double *x) { return (!c || !x) ? BCT_EINVAL : xvec_to_dev(c, x, c->x); }
-int bct_get_x(bct_ctx *c, double *x) { return (!c || !x) ? BCT_EINVAL : xvec_from_dev(c, c->x, x); }
+int bct_set_x(bct_ctx *c, const double *x)
+{
+    if (!c || !x) return BCT_EINVAL;
+    DEVICE_GUARD(c);
+    return xvec_to_dev(c, x, c->x);
+}
+int bct_get_x(bct_ctx *c, double *x)
+{
+    if (!c || !x) return BCT_EINVAL;
+    DEVICE_GUARD(c);
+    return xvec_from_dev(c, c->x, x);
+}
 int bct_get_xhat(bct_ctx *c, double *x)
 {
-    return (!c || !x) ? BCT_EINVAL : xvec_from_dev(c, c->xhat, x);
+    if (!c || !x) return BCT_EINVAL;
+    DEVICE_GUARD(c);
+    return xvec_from_dev(c, c->xhat, x);
 }
 
 int bct_set_x_true(bct_ctx *c, const double *xt)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (!xt) {
         c->has_x_true = false;
         return 0;
@@ -1263,6 +1357,7 @@ int bct_set_x_true(bct_ctx *c, const double *xt)
 int bct_set_r(bct_ctx *c, const double *r)
 {
     if (!c || !r) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (int e = h2d_staged(c, c->r, r, 8 * c->n_meas)) return e;
     CK(cudaStreamSynchronize(c->stream));
     return 0;
@@ -1271,6 +1366,7 @@ int bct_set_r(bct_ctx *c, const double *r)
 int bct_get_r(bct_ctx *c, double *r)
 {
     if (!c || !r) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (int e = d2h_staged(c, r, c->r, 8 * c->n_meas)) return e;
     CK(cudaStreamSynchronize(c->stream));
     return 0;
@@ -1279,6 +1375,7 @@ int bct_get_r(bct_ctx *c, double *r)
 int bct_set_z(bct_ctx *c, int32_t j, const double *zj)
 {
     if (!c || !zj) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (j < c->pb || j >= c->pe) return fail(c, BCT_EINVAL, "panel %d not owned", j);
     const PanelDev &P = c->h_panels[j - c->pb];
     CK(cudaMemcpyAsync(c->z + P.row_off, zj, 8 * P.n_rows, cudaMemcpyHostToDevice, c->stream));
@@ -1289,6 +1386,7 @@ int bct_set_z(bct_ctx *c, int32_t j, const double *zj)
 int bct_get_z(bct_ctx *c, int32_t j, double *zj)
 {
     if (!c || !zj) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (j < c->pb || j >= c->pe) return fail(c, BCT_EINVAL, "panel %d not owned", j);
     const PanelDev &P = c->h_panels[j - c->pb];
     CK(cudaMemcpyAsync(zj, c->z + P.row_off, 8 * P.n_rows, cudaMemcpyDeviceToHost, c->stream));
@@ -1299,6 +1397,7 @@ int bct_get_z(bct_ctx *c, int32_t j, double *zj)
 int bct_reset_accumulators(bct_ctx *c)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     CK(cudaMemsetAsync(c->xhat, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
     CK(cudaMemsetAsync(c->counts, 0, 4 * std::max(c->np, 1), c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1308,6 +1407,7 @@ int bct_reset_accumulators(bct_ctx *c)
 int bct_clear_state(bct_ctx *c)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     CK(cudaMemsetAsync(c->x, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
     CK(cudaMemsetAsync(c->z, 0, 8 * std::max<int64_t>(c->z_len, 1), c->stream));
     CK(cudaMemsetAsync(c->xhat, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
@@ -1319,6 +1419,7 @@ int bct_clear_state(bct_ctx *c)
 int bct_get_counts(bct_ctx *c, int64_t *counts)
 {
     if (!c || !counts) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     std::vector<int32_t> h(std::max(c->np, 1));
     CK(cudaMemcpyAsync(h.data(), c->counts, 4 * c->np, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1330,6 +1431,7 @@ int bct_get_counts(bct_ctx *c, int64_t *counts)
 int bct_commit_epoch(bct_ctx *c)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     CK(bct::commit(c->d_panels, c->np, c->counts, c->x, c->xhat, c->stream));
     CK(cudaMemsetAsync(c->counts, 0, 4 * std::max(c->np, 1), c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1339,6 +1441,7 @@ int bct_commit_epoch(bct_ctx *c)
 int bct_fill_z_from_image(bct_ctx *c)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     CK(bct::fill_z(c->dtype, c->d_panels, c->np, c->z_len, c->x, c->z, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return 0;
@@ -1347,6 +1450,7 @@ int bct_fill_z_from_image(bct_ctx *c)
 int bct_projection_sum(bct_ctx *c, double *out)
 {
     if (!c || !out) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     CK(bct::zsum(c->inv_ptr, c->inv_z, c->n_meas, c->z, c->vec, c->stream));
     CK(cudaMemcpyAsync(out, c->vec, 8 * c->n_meas, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1357,6 +1461,7 @@ int bct_projection_sum(bct_ctx *c, double *out)
 int bct_reset_residual(bct_ctx *c)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     CK(bct::zsum(c->inv_ptr, c->inv_z, c->n_meas, c->z, c->vec, c->stream));
     CK(bct::sub(c->y, c->vec, c->n_meas, c->r, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1366,6 +1471,7 @@ int bct_reset_residual(bct_ctx *c)
 int bct_forward(bct_ctx *c, const double *x, double *y_out)
 {
     if (!c || !x || !y_out) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     double *dx = nullptr;
     CK(cudaMalloc((void **)&dx, 8 * std::max<int64_t>(c->x_len, 1)));
     int r = xvec_to_dev(c, x, dx);
@@ -1384,6 +1490,7 @@ int bct_forward(bct_ctx *c, const double *x, double *y_out)
 int bct_audit(bct_ctx *c, double *drift)
 {
     if (!c || !drift) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     CK(bct::zsum(c->inv_ptr, c->inv_z, c->n_meas, c->z, c->vec, c->stream));
     CK(cudaMemsetAsync(c->audit2, 0, 16, c->stream));
     CK(bct::audit(c->y, c->r, c->vec, c->n_meas, c->audit2, c->stream));
@@ -1415,8 +1522,10 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
     if (n_tasks > 0)
         CK(cudaMemcpyAsync(c->d_tasks, c->h_tasks, sizeof(TaskDev) * n_tasks,
                            cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_masks, c->h_masks, 8 * (size_t)c->mw * (1 + 2 * n_tasks),
+                       cudaMemcpyHostToDevice, c->stream));
     if (n_tasks > 0 && c->h_hdr->host_prep)
-        CK(cudaMemcpyAsync(c->d_prep, c->h_prep, sizeof(TaskPrep) * n_tasks,
+        CK(cudaMemcpyAsync(c->d_prep, c->h_prep, c->pd.bytes() * n_tasks,
                            cudaMemcpyHostToDevice, c->stream));
     CK(cudaEventRecord(c->staged, c->stream));
     S.plan_user = nullptr;
@@ -1442,6 +1551,10 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
     p.statuses = c->statuses; p.out = c->out;
     p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
     p.prep = c->d_prep;
+    p.masks = c->d_masks;
+    p.mw = c->mw;
+    p.prep_smem_off = c->prep_off;
+    p.prep_dims = c->pd;
     p.timeline = nullptr;
     if (getenv("BCT_TIMELINE") && n_tasks > 0) {
         if (c->timeline_tasks < n_tasks) {
@@ -1453,7 +1566,7 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
     }
     CK(cudaEventRecord(S.t0, c->stream));
     cudaError_t e;
-    bct::launch_epoch(p, c->dtype, c->grid, c->block, c->smem, c->stream, &e);
+    bct::launch_epoch(p, c->dtype, c->grid, c->block, c->smem_total, c->stream, &e);
     if (e != cudaSuccess) return fail(c, BCT_ECUDA, "epoch launch: %s", cudaGetErrorString(e));
     CK(cudaEventRecord(S.t1, c->stream));
     CK(cudaMemcpyAsync(S.h_out, c->out, sizeof(EpochOut), cudaMemcpyDeviceToHost, c->stream));
@@ -1471,14 +1584,15 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
 }
 
 static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<TaskDev> &tasks,
-                           const uint64_t *emask, const std::function<int(Slot &)> &hook,
-                           bool host_masks);
+                           std::vector<uint64_t> &tmasks, const std::vector<uint64_t> &emask,
+                           const std::function<int(Slot &)> &hook, bool host_masks);
 
 int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task_j,
                   const int32_t *task_visit, const int64_t *task_gptr, const int64_t *sel,
                   const double *betas, int32_t flags)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (mode != BCT_SERIAL_FAITHFUL && mode != BCT_PARALLEL)
         return fail(c, BCT_EINVAL, "mode %d", mode);
     if (n_tasks < 0 || (n_tasks > 0 && (!task_j || !task_visit || !task_gptr || !sel || !betas)))
@@ -1487,9 +1601,12 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
     if (sharded && mode != BCT_PARALLEL)
         return fail(c, BCT_EINVAL, "sharded execution requires parallel mode");
     // validate and pack before touching the device (a failed batch leaves no trace)
+    const int mw = c->mw;
     std::vector<TaskDev> tasks;
+    std::vector<uint64_t> tmasks;        // mw words per kept task
+    std::vector<uint64_t> emask(mw, 0);  // union of every drawn block (all ranks' tasks)
+    std::vector<uint64_t> mk(mw);
     tasks.reserve(n_tasks);
-    uint64_t emask[BCT_MASKW] = {0, 0, 0, 0};
     for (int64_t k = 0; k < n_tasks; ++k) {
         int j = task_j[k];
         if (j < 0 || j >= c->n_panels)
@@ -1497,19 +1614,18 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
                         (long long)k, j);
         if (task_gptr[k + 1] < task_gptr[k])
             return fail(c, BCT_ESCHEDULE, "task %lld: negative group size", (long long)k);
-        TaskDev T;
-        memset(&T, 0, sizeof T);
+        std::fill(mk.begin(), mk.end(), 0ull);
         for (int64_t q = task_gptr[k]; q < task_gptr[k + 1]; ++q) {
             int64_t i = sel[q];
             if (i < 0 || i >= c->m)
                 return fail(c, BCT_ESCHEDULE, "task %lld: measurement block %lld out of range",
                             (long long)k, (long long)i);
-            if ((T.mask[i >> 6] >> (i & 63)) & 1ull)
+            if (has_bit(mk.data(), (int)i))
                 return fail(c, BCT_ESCHEDULE, "task %lld: repeated measurement block %lld",
                             (long long)k, (long long)i);
-            set_mask(T.mask, (int)i);
+            set_mask(mk.data(), (int)i);
         }
-        for (int w = 0; w < BCT_MASKW; ++w) emask[w] |= T.mask[w];
+        for (int w = 0; w < mw; ++w) emask[w] |= mk[w];
         if (j < c->pb || j >= c->pe) {
             if (!sharded)
                 return fail(c, BCT_ESCHEDULE, "task %lld: volume block %d not owned", (long long)k,
@@ -1518,33 +1634,38 @@ int bct_run_epoch(bct_ctx *c, int32_t mode, int64_t n_tasks, const int32_t *task
         }
         if (!std::isfinite(betas[k]))
             return fail(c, BCT_ESCHEDULE, "task %lld: non-finite beta", (long long)k);
+        TaskDev T;
+        memset(&T, 0, sizeof T);
         T.lp = j - c->pb;
         T.j = j;
         T.visit = task_visit[k];
         T.beta = betas[k];
+        if (task_gptr[k + 1] - task_gptr[k] == c->m) T.flags |= TASK_FULL;
         tasks.push_back(T);
+        tmasks.insert(tmasks.end(), mk.begin(), mk.end());
     }
-    return plan_and_launch(c, mode, flags, tasks, emask, nullptr, true);
+    return plan_and_launch(c, mode, flags, tasks, tmasks, emask, nullptr, true);
 }
 
 // Host restatement of epoch.cu build_runs / prep_task: the per-task path's
 // set-up of one task (its TaskDev, panel, mask runs and the visit's drawn
 // rows), built with the plan so the kernel copies it instead of walking a
 // chain of dependent device loads per task.
-static void host_prep(const bct_ctx *c, const TaskDev &T, TaskPrep &o)
+static void host_prep(const bct_ctx *c, const TaskDev &T, const uint64_t *mask,
+                      const uint64_t *vmask, char *rec)
 {
-    o.T = T;
-    o.P = c->h_panels[T.lp];
+    PrepView R(rec, c->pd);
+    PrepHdr &H = *R.h;
+    H.T = T;
+    H.P = c->h_panels[T.lp];
     const std::vector<int32_t> &rbp = c->h_rbp[T.lp];
     const std::vector<int32_t> &stbs = c->h_stbs[T.lp];
     const int m = c->m;
-    auto has = [](const uint64_t *mk, int i) { return ((mk[i >> 6] >> (i & 63)) & 1ull) != 0; };
-    Runs &R = o.R;
     int n = 0, acc = 0;
     for (int i = 0; i < m;) {
-        if (!has(T.mask, i)) { ++i; continue; }
+        if (!has_bit(mask, i)) { ++i; continue; }
         const int s = i;
-        while (i < m && has(T.mask, i)) ++i;
+        while (i < m && has_bit(mask, i)) ++i;
         R.i0[n] = s;
         R.i1[n] = i;
         R.rows0[n] = rbp[s];
@@ -1553,49 +1674,53 @@ static void host_prep(const bct_ctx *c, const TaskDev &T, TaskPrep &o)
         ++n;
     }
     R.pre[n] = acc;
-    R.n = n;
+    H.n_runs = n;
     int uacc = 0;
-    for (int st = 0; st < o.P.n_st; ++st) {
+    for (int st = 0; st < H.P.n_st; ++st) {
         R.st_pre[st] = uacc;
         const int32_t *sb = stbs.data() + (size_t)st * (m + 1);
         for (int q = 0; q < n; ++q) uacc += sb[R.i1[q]] - sb[R.i0[q]];
     }
-    R.st_pre[o.P.n_st] = uacc;
-    R.nst = o.P.n_st;
-    R.full = (n == 1 && R.i0[0] == 0 && R.i1[0] == m);
-    VisitRows &V = o.V;
+    R.st_pre[H.P.n_st] = uacc;
+    H.nst = H.P.n_st;
+    H.full = (n == 1 && R.i0[0] == 0 && R.i1[0] == m);
     int nv = 0;
     acc = 0;
     for (int i = 0; i < m; ++i) {
-        if (!has(T.visit_mask, i)) continue;
-        V.vb[nv] = i;
-        V.vpre[nv] = acc;
+        if (!has_bit(vmask, i)) continue;
+        R.vb[nv] = i;
+        R.vpre[nv] = acc;
         acc += (int)(c->rb_ptr[i + 1] - c->rb_ptr[i]);
         ++nv;
     }
-    V.vpre[nv] = acc;
-    V.nvb = nv;
+    R.vpre[nv] = acc;
+    H.nvb = nv;
 }
 
 // Visit flags/masks, batched-path prefixes and scratch, staging and launch of
 // a validated task list (shared by bct_run_epoch and bct_sample_epoch; the
 // hook runs on the stream between the plan upload and the epoch kernel).
+// tmasks: each task's row-block set (mw words; zeros when the device sampler
+// fills them), emask: the epoch's drawn blocks (zeros: the sampler ORs them).
 static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<TaskDev> &tasks,
-                           const uint64_t *emask, const std::function<int(Slot &)> &hook,
-                           bool host_masks)
+                           std::vector<uint64_t> &tmasks, const std::vector<uint64_t> &emask,
+                           const std::function<int(Slot &)> &hook, bool host_masks)
 {
-    // visit boundaries and masks
-    int64_t n_visits = 0;
+    const int mw = c->mw;
     const int64_t nt = (int64_t)tasks.size();
+    // visit boundaries and masks
+    std::vector<uint64_t> vmasks((size_t)nt * mw, 0ull);
+    int64_t n_visits = 0;
     for (int64_t a = 0; a < nt;) {
         int64_t b = a;
         while (b < nt && tasks[b].visit == tasks[a].visit && tasks[b].j == tasks[a].j) ++b;
-        uint64_t vm[BCT_MASKW] = {0, 0, 0, 0};
         for (int64_t q = a; q < b; ++q)
-            for (int w = 0; w < BCT_MASKW; ++w) vm[w] |= tasks[q].mask[w];
+            for (int w = 0; w < mw; ++w) vmasks[(size_t)a * mw + w] |= tmasks[(size_t)q * mw + w];
         for (int64_t q = a; q < b; ++q) {
-            memcpy(tasks[q].visit_mask, vm, sizeof vm);
-            tasks[q].flags = (q == a ? TASK_FIRST_OF_VISIT : 0) | (q == b - 1 ? TASK_LAST_OF_VISIT : 0);
+            if (q > a)
+                std::copy(vmasks.begin() + (size_t)a * mw, vmasks.begin() + (size_t)(a + 1) * mw,
+                          vmasks.begin() + (size_t)q * mw);
+            tasks[q].flags |= (q == a ? TASK_FIRST_OF_VISIT : 0) | (q == b - 1 ? TASK_LAST_OF_VISIT : 0);
         }
         ++n_visits;
         a = b;
@@ -1604,10 +1729,20 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
     if (r) return r;
     // epoch-batched path: parallel epoch whose tasks are all full panels
     bool batched = mode == BCT_PARALLEL && nt > 0 && nt <= bct::MAX_BATCH_TASKS && !getenv("BCT_NO_BATCH");
-    uint64_t full[BCT_MASKW] = {0, 0, 0, 0};
-    for (int i = 0; i < c->m; ++i) set_mask(full, i);
     for (int64_t k = 0; batched && k < nt; ++k)
-        if (memcmp(tasks[k].mask, full, sizeof full) != 0) batched = false;
+        if (!(tasks[k].flags & TASK_FULL)) batched = false;
+    // phase D writes each task's z and each panel's x_hat without ordering
+    // between tasks: two full-panel tasks of one column block in an epoch (a
+    // scripted plan: a repeated visit, or a visit with two full groups) would
+    // race where the reference keeps plan order (executor.py:200-213,
+    // 247-248), so such plans run on the per-task path
+    if (batched) {
+        std::vector<char> seen(c->np, 0);
+        for (int64_t k = 0; k < nt && batched; ++k) {
+            if (seen[tasks[k].lp]) batched = false;
+            seen[tasks[k].lp] = 1;
+        }
+    }
     int64_t tot_tiles = 0, tot_slices = 0, tot_rows = 0, tot_vox = 0, gxo = 0, sgo = 0, txo = 0;
     int64_t tot_ent = 0;
     if (batched) {
@@ -1631,7 +1766,9 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
             sgo += (int64_t)P.n_slices * 32;
             txo += P.n_rows;
         }
-        if (tot_slices >= (1ll << 31) || tot_rows >= (1ll << 31) || gxo >= (1ll << 31)) batched = false;
+        if (tot_slices >= (1ll << 31) || tot_rows >= (1ll << 31) || gxo >= (1ll << 31) ||
+            tot_tiles >= (1ll << 31) || tot_vox >= (1ll << 31))
+            batched = false;
     }
     if (batched) {
         // the device may still read the old scratch: drain before growing it
@@ -1660,18 +1797,28 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
     c->h_hdr->n_rows_total = (int32_t)tot_rows;
     c->h_hdr->n_vox_total = (int32_t)tot_vox;
     c->h_hdr->n_ent_total = tot_ent;
-    memcpy(c->h_hdr->epoch_mask, emask, sizeof(uint64_t) * BCT_MASKW);
     if (nt) memcpy(c->h_tasks, tasks.data(), sizeof(TaskDev) * nt);
+    // masks: the epoch's, then per task its group and its visit's union
+    std::copy(emask.begin(), emask.end(), c->h_masks);
+    for (int64_t k = 0; k < nt; ++k) {
+        std::copy(tmasks.begin() + (size_t)k * mw, tmasks.begin() + (size_t)(k + 1) * mw,
+                  c->h_masks + task_mask_off(k, mw));
+        std::copy(vmasks.begin() + (size_t)k * mw, vmasks.begin() + (size_t)(k + 1) * mw,
+                  c->h_masks + visit_mask_off(k, mw));
+    }
     // per-task path with host-known masks: every task's set-up built here
     c->h_hdr->host_prep = (!batched && host_masks && nt > 0) ? 1 : 0;
     if (c->h_hdr->host_prep)
-        for (int64_t k = 0; k < nt; ++k) host_prep(c, tasks[k], c->h_prep[k]);
+        for (int64_t k = 0; k < nt; ++k)
+            host_prep(c, tasks[k], tmasks.data() + (size_t)k * mw, vmasks.data() + (size_t)k * mw,
+                      c->h_prep + c->pd.bytes() * k);
     return launch_staged(c, nt, n_visits, hook);
 }
 
 int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *statuses)
 {
     if (!c || !o) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     Slot &S = c->slots[c->tail];
     if (!S.pending) return fail(c, BCT_EINVAL, "no pending epoch");
     CK(cudaEventSynchronize(S.done));
@@ -1700,6 +1847,7 @@ int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *status
 int bct_debug_timeline(bct_ctx *c, long long *out, int64_t n_tasks, int32_t *grid)
 {
     if (!c || !grid) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     *grid = c->grid;
     if (!c->timeline || !out) return 0;
     CK(cudaStreamSynchronize(c->stream));
@@ -1711,6 +1859,7 @@ int bct_debug_timeline(bct_ctx *c, long long *out, int64_t n_tasks, int32_t *gri
 int bct_exchange_buffer(bct_ctx *c, double **dev_ptr, int64_t *len)
 {
     if (!c || !dev_ptr || !len) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     *dev_ptr = c->exchange;
     *len = c->n_meas + 2;
     return 0;
@@ -1719,9 +1868,10 @@ int bct_exchange_buffer(bct_ctx *c, double **dev_ptr, int64_t *len)
 int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     (void)flags;
     // the drawn blocks of the last epoch, as the device saw them (host plan or sampler)
-    const uint64_t *dmask = c->d_hdr->epoch_mask;
+    const uint64_t *dmask = c->d_masks;   // epoch mask first (EpochParams::masks)
     const int nb = 296;
     CK(bct::sharded_finish(c->y, c->exchange, c->n_meas, c->rb_of_row, dmask, c->r, c->part, nb,
                            c->stream));
@@ -1748,6 +1898,7 @@ int bct_sample_epoch(bct_ctx *c, int32_t mode, int32_t n_visits, const int32_t *
                      int32_t flags, int64_t *plan_ids_out)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (mode != BCT_SERIAL_FAITHFUL && mode != BCT_PARALLEL)
         return fail(c, BCT_EINVAL, "mode %d", mode);
     if (strategy < BCT_IMPORTANCE || strategy > BCT_MIXED)
@@ -1763,7 +1914,8 @@ int bct_sample_epoch(bct_ctx *c, int32_t mode, int32_t n_visits, const int32_t *
     // variate offsets, task skeletons; the ids/masks/betas come from the device
     std::vector<bct::SampleVisit> vis(n_visits);
     std::vector<TaskDev> tasks;
-    uint64_t emask[BCT_MASKW] = {0, 0, 0, 0};   // ORed by the sampler on the device
+    std::vector<uint64_t> emask(c->mw, 0ull);    // ORed by the sampler on the device
+    std::vector<uint64_t> tmasks;                // written by the sampler
     int64_t var_off = 0, id_off = 0;
     for (int32_t v = 0; v < n_visits; ++v) {
         const int j = visit_j[v];
@@ -1797,15 +1949,14 @@ int bct_sample_epoch(bct_ctx *c, int32_t mode, int32_t n_visits, const int32_t *
             T.j = j;
             T.visit = v;
             // full group <=> it holds every row block (masks are filled on the device)
-            if (std::min(group_size, draws[v] - t * group_size) == c->m)
-                for (int i = 0; i < c->m; ++i) set_mask(T.mask, i);
+            if (std::min(group_size, draws[v] - t * group_size) == c->m) T.flags |= TASK_FULL;
             tasks.push_back(T);
+            tmasks.resize(tmasks.size() + c->mw, 0ull);
         }
     }
     if (var_off != n_variates)
         return fail(c, BCT_ESCHEDULE, "%lld variates for %lld in-scope blocks",
                     (long long)n_variates, (long long)var_off);
-    if (c->m > 256) return fail(c, BCT_EINVAL, "device sampler supports m <= 256");
     // device inputs (grow-only; drained before reallocation)
     auto grow = [&](auto **ptr, int64_t *have, int64_t need, size_t elt) -> int {
         if (need <= *have) return 0;
@@ -1848,7 +1999,8 @@ int bct_sample_epoch(bct_ctx *c, int32_t mode, int32_t n_visits, const int32_t *
         sp.group_size = group_size;
         sp.b = b;
         sp.tasks = c->d_tasks;
-        sp.hdr = c->d_hdr;
+        sp.masks = c->d_masks;
+        sp.mw = c->mw;
         sp.plan_ids = c->d_plan;
         cudaError_t e;
         bct::launch_sampler(sp, n_visits, c->stream, &e);
@@ -1866,7 +2018,7 @@ int bct_sample_epoch(bct_ctx *c, int32_t mode, int32_t n_visits, const int32_t *
         }
         return 0;
     };
-    return plan_and_launch(c, mode, flags, tasks, emask, hook, false);
+    return plan_and_launch(c, mode, flags, tasks, tmasks, emask, hook, false);
 }
 
 }  // extern "C"
@@ -1876,6 +2028,7 @@ int bct_sample_epoch(bct_ctx *c, int32_t mode, int32_t n_visits, const int32_t *
 int bct_baseline_init(bct_ctx *c, int32_t kind, int32_t m_rule)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (kind != BCT_ROW_ACTION && kind != BCT_COLUMN_ACTION)
         return fail(c, BCT_EINVAL, "baseline kind %d", kind);
     if (m_rule < BCT_M_IDENTITY || m_rule > BCT_M_NORM_INVERSE)
@@ -1915,6 +2068,7 @@ int bct_baseline_init(bct_ctx *c, int32_t kind, int32_t m_rule)
 int bct_baseline_epoch(bct_ctx *c, double omega, double *norms4)
 {
     if (!c) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (c->bl_kind < 0) return fail(c, BCT_EINVAL, "bct_baseline_init first");
     if (!(omega > 0.0) || !std::isfinite(omega)) return fail(c, BCT_EINVAL, "omega %g", omega);
     if (c->bl_kind == BCT_ROW_ACTION) {
@@ -1943,6 +2097,7 @@ int bct_baseline_epoch(bct_ctx *c, double omega, double *norms4)
 int bct_baseline_get_x(bct_ctx *c, double *x)
 {
     if (!c || !x) return BCT_EINVAL;
+    DEVICE_GUARD(c);
     if (c->bl_kind < 0) return fail(c, BCT_EINVAL, "bct_baseline_init first");
     CK(cudaStreamSynchronize(c->stream));
     if (int e = d2h_staged(c, x, c->bl_x, 8 * c->n_vox)) return e;

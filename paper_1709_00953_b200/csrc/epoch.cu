@@ -142,10 +142,10 @@ __device__ double block_sum_all(double v, double *sh)
 }
 
 // Contiguous runs of set bits of a row-block mask, with their local row ranges
-// and the task's units per super tile.
-__device__ void build_runs(const uint64_t *mask, int m, const PanelDev &P, Runs &R)
+// and the task's units per super tile (one thread; restated on the host,
+// api.cu host_prep, when the masks are known)
+__device__ void build_runs(const uint64_t *mask, int m, const PanelDev &P, PrepView &R)
 {
-    // one thread; restated on the host (api.cu host_prep) when the masks are known
     int n = 0, acc = 0;
     int i = 0;
     while (i < m) {
@@ -160,7 +160,7 @@ __device__ void build_runs(const uint64_t *mask, int m, const PanelDev &P, Runs 
         ++n;
     }
     R.pre[n] = acc;
-    R.n = n;
+    R.h->n_runs = n;
     int uacc = 0;
     for (int st = 0; st < P.n_st; ++st) {
         R.st_pre[st] = uacc;
@@ -168,31 +168,32 @@ __device__ void build_runs(const uint64_t *mask, int m, const PanelDev &P, Runs 
         for (int q = 0; q < n; ++q) uacc += sb[R.i1[q]] - sb[R.i0[q]];
     }
     R.st_pre[P.n_st] = uacc;
-    R.nst = P.n_st;
-    R.full = (n == 1 && R.i0[0] == 0 && R.i1[0] == m);
+    R.h->nst = P.n_st;
+    R.h->full = (n == 1 && R.i0[0] == 0 && R.i1[0] == m);
 }
 
-__device__ void prep_task(const EpochParams &p, int k, TaskPrep &out)
+__device__ void prep_task(const EpochParams &p, int k, PrepView &out)
 {
     const TaskDev &T = p.tasks[k];
     const PanelDev &P = p.panels[T.lp];
-    out.T = T;
-    out.P = P;
-    build_runs(T.mask, p.m, P, out.R);
+    out.h->T = T;
+    out.h->P = P;
+    build_runs(p.masks + task_mask_off(k, p.mw), p.m, P, out);
+    const uint64_t *vm = p.masks + visit_mask_off(k, p.mw);
     int nv = 0, acc = 0;
     for (int i = 0; i < p.m; ++i) {
-        if (!mask_has(T.visit_mask, i)) continue;
-        out.V.vb[nv] = i;
-        out.V.vpre[nv] = acc;
+        if (!mask_has(vm, i)) continue;
+        out.vb[nv] = i;
+        out.vpre[nv] = acc;
         acc += p.rb_ptr[i + 1] - p.rb_ptr[i];
         ++nv;
     }
-    out.V.vpre[nv] = acc;
-    out.V.nvb = nv;
+    out.vpre[nv] = acc;
+    out.h->nvb = nv;
 }
 
 
-__device__ __forceinline__ int run_row(const Runs &R, int f)
+__device__ __forceinline__ int run_row(const PrepView &R, int f)
 {
     int k = 0;
     while (f >= R.pre[k + 1]) ++k;
@@ -200,7 +201,7 @@ __device__ __forceinline__ int run_row(const Runs &R, int f)
 }
 
 // flattened task slice f of super tile st -> slice id
-__device__ __forceinline__ int task_slice(const Runs &R, const PanelDev &P, int m, int f, int st)
+__device__ __forceinline__ int task_slice(const PrepView &R, const PanelDev &P, int m, int f, int st)
 {
     int off = f - R.st_pre[st];
     const int32_t *sb = P.stbs + st * (m + 1);
@@ -1451,8 +1452,8 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
 {
     extern __shared__ double4 dyn_smem[];
     __shared__ double sh[WARPS];
-    __shared__ TaskPrep sPrep;
-    Runs &R = sPrep.R;
+    // the current task's record (PrepHdr + arrays) after the phase buffers
+    PrepView R(reinterpret_cast<char *>(dyn_smem) + p.prep_smem_off, p.prep_dims);
     __shared__ int2 vr_s[8];
 
     const int lane = threadIdx.x & 31;
@@ -1476,19 +1477,20 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     __shared__ int s_tpre[bct::MAX_BATCH_TASKS + 1], s_lp[bct::MAX_BATCH_TASKS];
     if (hdr.batched) batched_epoch<V>(p, hdr, rs, sh, ring, s_tpre, s_lp);
     for (int k = 0; k < (hdr.batched ? 0 : n_tasks); ++k) {
-        __syncthreads();  // sPrep of the previous task may still be in use
+        __syncthreads();  // the previous task's record may still be in use
         if (!hdr.host_prep) {
-            if (threadIdx.x == 0) prep_task(p, k, sPrep);
+            if (threadIdx.x == 0) prep_task(p, k, R);
         } else {
             // built on the host with the plan (api.cu host_prep): one copy
-            const float4 *src = reinterpret_cast<const float4 *>(p.prep + k);
-            float4 *dst = reinterpret_cast<float4 *>(&sPrep);
-            for (int q = threadIdx.x; q < (int)(sizeof(TaskPrep) / sizeof(float4)); q += BLOCK)
-                dst[q] = __ldcg(src + q);
+            const int64_t rb = p.prep_dims.bytes();
+            const float4 *src = reinterpret_cast<const float4 *>(p.prep + rb * k);
+            float4 *dst = reinterpret_cast<float4 *>(R.h);
+            for (int q = threadIdx.x; q < (int)(rb / 16); q += BLOCK) dst[q] = __ldcg(src + q);
         }
         __syncthreads();
-        const TaskDev &T = sPrep.T;
-        const PanelDev &P = sPrep.P;
+        const TaskDev &T = R.h->T;
+        const PanelDev &P = R.h->P;
+        const uint64_t *tmask = p.masks + task_mask_off(k, p.mw);
         TL_MARK(k, 0);
         double2 *gx = reinterpret_cast<double2 *>(p.gx + (k & 1) * p.gx_stride);
         const double *xj = p.x + P.x_off;
@@ -1511,7 +1513,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             const bool dbuf = p.band_dbuf != 0;
             double *buf0 = rs, *buf1 = rs + (dbuf ? p.band_cap : 0);
             double *red = rs + (int64_t)p.band_cap * (dbuf ? 2 : 1);
-            const uint64_t *bmask = R.full ? nullptr : T.mask;
+            const uint64_t *bmask = R.h->full ? nullptr : tmask;
             BandMeta bm;
             if (n_items > 0) {
                 band_meta_load(P, item_tile(0), bm, bmask);
@@ -1535,7 +1537,8 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                     if (it + 2 < n_items) band_meta_load(P, item_tile(it + 2), bm, bmask);
                 }
                 if (bmask != nullptr) {
-                    tile_vr(P, m, t, c0, c1, R.n > 0 ? R.i0[0] : 0, R.n > 0 ? R.i1[R.n - 1] : 0,
+                    const int nr = R.h->n_runs;
+                    tile_vr(P, m, t, c0, c1, nr > 0 ? R.i0[0] : 0, nr > 0 ? R.i1[nr - 1] : 0,
                             vr_s);
                     __syncthreads();
                 }
@@ -1564,9 +1567,10 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         {
             const V *fv = static_cast<const V *>(P.fvals);
             double2 *spart = reinterpret_cast<double2 *>(p.seg_part);
-            const int ns = R.st_pre[R.nst];
+            const int ns = R.st_pre[R.h->nst];
+            const bool rfull = R.h->full != 0;
             int ub, ue;
-            if (R.full) {
+            if (rfull) {
                 __shared__ int s_lim[2];
                 if (threadIdx.x < 2) {
                     const int64_t F = __ldg(P.slice_start + P.n_slices);
@@ -1602,7 +1606,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 // TASK_SPLIT partials of a lane are summed in phase 2b
                 for (int u = fu * TASK_SPLIT + warp; u < ge * TASK_SPLIT; u += WARPS) {
                     const int f = u / TASK_SPLIT, part = u - f * TASK_SPLIT;
-                    const int sl = R.full ? f : task_slice(R, P, m, f, st);
+                    const int sl = rfull ? f : task_slice(R, P, m, f, st);
                     const int base = __ldg(P.slice_start + sl);
                     const int nvec = (__ldg(P.slice_start + sl + 1) - base) >> 7;
                     double t = 0.0, ax = 0.0;
@@ -1630,7 +1634,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         grid_sync(p.bar);
 
         // ---- phase 2b: rows = sum of their segments in tile order ----------
-        const int n_task_rows = R.pre[R.n];
+        const int n_task_rows = R.pre[R.h->n_runs];
         wsum = 0.0;
         {
             const double2 *spart = reinterpret_cast<const double2 *>(p.seg_part);
@@ -1701,8 +1705,8 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             // refresh every row of the visit's drawn blocks (executor.py:215-223),
             // one flat pass over their rows; the current task's z is computed
             // here and stored on the way (every one of its rows is refreshed)
-            const int *s_vb = sPrep.V.vb, *s_vpre = sPrep.V.vpre;
-            const int nvb = sPrep.V.nvb, tot = s_vpre[nvb];
+            const int *s_vb = R.vb, *s_vpre = R.vpre;
+            const int nvb = R.h->nvb, tot = s_vpre[nvb];
             const double2 *tax = reinterpret_cast<const double2 *>(p.t_ax);
             const int64_t zlo = P.row_off, zhi = P.row_off + P.n_rows;
             for (int f = gtid; f < tot; f += nthreads) {
@@ -1712,7 +1716,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                     if (s_vpre[mid] <= f) lo = mid; else hi = mid - 1;
                 }
                 const int i = s_vb[lo];
-                const bool cur = mask_has(T.mask, i);
+                const bool cur = mask_has(tmask, i);
                 const int g = p.rb_rows[p.rb_ptr[i] + (f - s_vpre[lo])];
                 double acc = 0.0;
                 for (int e = p.inv_ptr[g]; e < p.inv_ptr[g + 1]; ++e) {
@@ -1771,7 +1775,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             } else {
                 double d = p.y[g] - acc;
                 int rb = p.rb_of_row[g];
-                if (!serial && rb >= 0 && mask_has(hdr.epoch_mask, rb)) p.r[g] = d;
+                if (!serial && rb >= 0 && mask_has(p.masks, rb)) p.r[g] = d;
                 rsq = fma(d, d, rsq);
             }
         }
@@ -1846,12 +1850,20 @@ namespace bct {
 
 std::string cuda_err(cudaError_t e) { return std::string(cudaGetErrorString(e)); }
 
+size_t epoch_static_smem(int dtype)
+{
+    cudaFuncAttributes fa;
+    const void *fn = dtype == 0 ? (const void *)epoch_kernel<double> : (const void *)epoch_kernel<float>;
+    if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return 16 * 1024;
+    return fa.sharedSizeBytes;
+}
+
 int epoch_grid_size(int dtype, int device, size_t smem, int *block)
 {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const void *fn = dtype == 0 ? (const void *)epoch_kernel<double> : (const void *)epoch_kernel<float>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 218 * 1024);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (dtype == 0)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<double>, BLOCK, smem);
     else

@@ -16,8 +16,12 @@
 #include <string>
 #include <vector>
 
-#define BCT_MASKW 4                 // up to 256 row blocks
-#define BCT_MAX_M (64 * BCT_MASKW)
+// Row-block sets are bitsets of mask_words(m) 64-bit words in a per-epoch
+// device array (EpochParams::masks): the epoch's drawn blocks first, then per
+// task its group and its visit's union.  m is bounded by the 12 bits the
+// layout's band keys give the row block (layout.cu band_key_k).
+#define BCT_MAX_M 4096
+__host__ __device__ __forceinline__ int mask_words(int m) { return (m + 63) >> 6; }
 
 // One owned column panel in HBM (see layout.cu for the design).
 struct PanelDev {
@@ -48,7 +52,7 @@ struct PanelDev {
     const int32_t *corder;     // tile order of device columns, tile_cols per tile
     const int32_t *band_ptr;   // [n_tiles+1] ranges of each tile
     const int2 *band_meta;     // per range: (first measurement id, slot << 16 | length)
-    const uint8_t *band_rb;    // row block of each range
+    const uint16_t *band_rb;   // row block of each range
     // rows / voxels
     const int32_t *rbp;        // [m+1]
     const int32_t *l2g;        // [n_rows] global measurement ids
@@ -87,11 +91,9 @@ struct PanelDev {
 struct TaskDev {
     int32_t lp;        // owned panel index
     int32_t j;         // global column block id
-    int32_t flags;     // bit0: last task of its visit; bit1: first task of its visit
+    int32_t flags;     // TASK_* bits
     int32_t visit;
     double beta;
-    uint64_t mask[BCT_MASKW];        // row blocks of the task's group
-    uint64_t visit_mask[BCT_MASKW];  // union over the visit (serial refresh set)
     // epoch-batched parallel path (full-panel tasks): flattened work prefixes
     // and the task's slices of the batch scratch buffers
     int32_t tile_pre, slice_pre, row_pre, vox_pre;   // exclusive prefixes over tasks
@@ -101,7 +103,11 @@ struct TaskDev {
     int64_t ent_pre;   // forward-store entries of the tasks before this one
 };
 
-enum { TASK_LAST_OF_VISIT = 1, TASK_FIRST_OF_VISIT = 2 };
+enum { TASK_LAST_OF_VISIT = 1, TASK_FIRST_OF_VISIT = 2, TASK_FULL = 4 };  // FULL: every row block
+
+// the masks of task k in EpochParams::masks (after the epoch mask)
+__host__ __device__ __forceinline__ int64_t task_mask_off(int64_t k, int mw) { return (1 + 2 * k) * mw; }
+__host__ __device__ __forceinline__ int64_t visit_mask_off(int64_t k, int mw) { return (2 + 2 * k) * mw; }
 
 struct EpochHeader {
     int32_t n_tasks;
@@ -109,9 +115,8 @@ struct EpochHeader {
     int32_t flags;
     int32_t batched;   // 1: parallel epoch of full-panel tasks, phase-by-phase over all tasks
     int32_t n_tiles_total, n_slices_total, n_rows_total, n_vox_total;
-    uint64_t epoch_mask[BCT_MASKW];  // union of all drawn blocks (parallel refresh)
     int64_t n_ent_total;             // forward-store entries of the batched tasks
-    int32_t host_prep;               // 1: EpochParams::prep holds every task's TaskPrep
+    int32_t host_prep;               // 1: EpochParams::prep holds every task's record
     int32_t pad_;
 };
 
@@ -124,39 +129,48 @@ struct EpochOut {
 
 // ---- per-task path set-up (epoch.cu per-task loop; built by api.cu when the
 // masks are host-known) ----
-constexpr int MAX_RUNS = BCT_MAX_M / 2 + 1;
-constexpr int MAX_ST = 64;
-
-// Contiguous runs of set bits of a task's row-block mask, with their local row
-// ranges and the task's SELL slices per super tile.
-struct Runs {
-    int n;
-    int i0[MAX_RUNS];
-    int i1[MAX_RUNS];
-    int rows0[MAX_RUNS];       // first local row of the run
-    int pre[MAX_RUNS + 1];     // prefix of run row counts
-    int nst;
-    int st_pre[MAX_ST + 1];    // prefix over super tiles of the task's slice counts
-    bool full;                 // the task covers every row block
-};
-
-// The drawn row blocks of a visit with their row prefixes (serial refresh).
-struct VisitRows {
-    int nvb;
-    int vb[BCT_MAX_M];
-    int vpre[BCT_MAX_M + 1];
-};
-
 // Everything a task of the per-task path needs before phase 1: its TaskDev,
-// its panel, the runs of its row-block mask and its visit's drawn rows.  On
-// the device one thread builds it, a chain of dependent loads (~6 us); when
-// the host knows the masks (bct_run_epoch) it builds every task's with the
-// plan and each CTA copies it into shared memory in one pass.
-struct alignas(16) TaskPrep {
+// its panel, the contiguous runs of its row-block mask (with their local row
+// ranges and the task's SELL slices per super tile) and its visit's drawn
+// row blocks (serial refresh).  Fixed header + int arrays sized by the
+// context (PrepDims); each CTA copies a task's record into dynamic shared
+// memory.  On the device one thread builds it (sampled epochs: a chain of
+// dependent loads); when the host knows the masks (bct_run_epoch) it builds
+// every task's with the plan.
+struct alignas(16) PrepHdr {
     TaskDev T;
     PanelDev P;
-    Runs R;
-    VisitRows V;
+    int32_t n_runs;    // contiguous runs of set bits of the task's mask
+    int32_t nst;       // super tiles of the panel
+    int32_t full;      // the task covers every row block
+    int32_t nvb;       // drawn row blocks of the visit
+};
+// int arrays after the header: i0, i1, rows0 [rc], pre [rc+1], st_pre [sc+1],
+// vb [m], vpre [m+1] (rc = max runs = m/2+1, sc = max super tiles per panel)
+struct PrepDims {
+    int32_t rc, sc, m, pad_;
+    __host__ __device__ int words() const { return 4 * rc + 1 + sc + 1 + 2 * m + 1; }
+    __host__ __device__ int64_t bytes() const   // record stride, 16-byte multiple
+    {
+        return ((int64_t)sizeof(PrepHdr) + 4 * (int64_t)words() + 15) & ~15ll;
+    }
+};
+// views of a record's arrays
+struct PrepView {
+    PrepHdr *h;
+    int *i0, *i1, *rows0, *pre, *st_pre, *vb, *vpre;
+    __host__ __device__ PrepView(void *rec, const PrepDims &d)
+    {
+        h = static_cast<PrepHdr *>(rec);
+        int *a = reinterpret_cast<int *>(static_cast<char *>(rec) + sizeof(PrepHdr));
+        i0 = a; a += d.rc;
+        i1 = a; a += d.rc;
+        rows0 = a; a += d.rc;
+        pre = a; a += d.rc + 1;
+        st_pre = a; a += d.sc + 1;
+        vb = a; a += d.m;
+        vpre = a;
+    }
 };
 
 struct EpochParams {
@@ -186,6 +200,10 @@ struct EpochParams {
     // plan
     const EpochHeader *hdr;
     const TaskDev *tasks;
+    const uint64_t *masks;     // [mw] epoch's drawn blocks, then per task [mw] group, [mw] visit
+    int32_t mw;                // mask words per set
+    int32_t prep_smem_off;     // byte offset of the task record in dynamic shared memory
+    PrepDims prep_dims;
     // scratch
     double *gx;                // 2 buffers x (2*max_cols) : (g, x_J) interleaved, device order
     int64_t gx_stride;
@@ -205,7 +223,7 @@ struct EpochParams {
     unsigned int *bar;         // grid barrier word
     unsigned int *ticket;      // last-block counter
     long long *timeline;       // optional phase timestamps (BCT_TIMELINE=1)
-    const struct TaskPrep *prep;  // per-task path: host-built set-up of every task (hdr.host_prep)
+    const char *prep;          // per-task path: host-built records (hdr.host_prep), prep_dims.bytes() apart
 };
 
 struct bct_ctx_s;
@@ -287,8 +305,9 @@ struct SamplerParams {
     const double *exp;       // exponential variates, visit order
     int32_t strategy, group_size;
     double theta, b;
-    TaskDev *tasks;          // the epoch's device task array (masks, betas written)
-    EpochHeader *hdr;        // epoch_mask ORed
+    TaskDev *tasks;          // the epoch's device task array (betas written)
+    uint64_t *masks;         // EpochParams::masks layout: epoch mask ORed, task masks written
+    int32_t mw;
     int32_t *plan_ids;       // drawn ids, visit order, draw order
 };
 void launch_sampler(const SamplerParams &p, int n_visits, cudaStream_t s, cudaError_t *err);
@@ -299,6 +318,7 @@ std::string cuda_err(cudaError_t e);
 void launch_epoch(const EpochParams &p, int dtype, int grid, int block, size_t smem,
                   cudaStream_t s, cudaError_t *err);
 int epoch_grid_size(int dtype, int device, size_t smem, int *block);
+size_t epoch_static_smem(int dtype);   // the epoch kernel's static shared arrays
 int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nnz,
                     const double *vals64, const int32_t *cols_c, const int32_t *indptr_c,
                     const int32_t *l2g, const int32_t *rbp, const std::vector<int32_t> &c2d_h,

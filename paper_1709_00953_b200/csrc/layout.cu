@@ -392,7 +392,7 @@ __global__ void colcount_k(const int32_t *sorted_d, int64_t nnz, int32_t n_cols,
     }
 }
 
-// band keys: tile << 40 | row block << 32 | global row, per CSC entry in sorted
+// band keys: tile << 44 | row block << 32 | global row, per CSC entry in sorted
 // order (ranges never cross a row block, so a partial task can zero the rest)
 __global__ void band_key_k(const int32_t *perm, const int32_t *rowid, const int32_t *l2g,
                            const int32_t *rbp, int m, const int32_t *sorted_d,
@@ -403,7 +403,8 @@ __global__ void band_key_k(const int32_t *perm, const int32_t *rowid, const int3
     const int32_t lr = rowid[perm[q]];
     const int32_t g = l2g[lr];
     const int blk = (int)lb_i32(rbp, 0, m + 1, lr + 1) - 1;
-    bkey[q] = ((uint64_t)(uint32_t)tile_of_d[sorted_d[q]] << 40) | ((uint64_t)blk << 32) |
+    // tile (20 bits) | row block (12 bits, BCT_MAX_M) | measurement id (32 bits)
+    bkey[q] = ((uint64_t)(uint32_t)tile_of_d[sorted_d[q]] << 44) | ((uint64_t)blk << 32) |
               (uint32_t)g;
 }
 
@@ -435,7 +436,7 @@ __global__ void tile_bounds_k(const uint64_t *u, int64_t nu, const int32_t *rfla
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t > n_tiles) return;
-    int64_t q = lb_u64(u, 0, nu, (uint64_t)(uint32_t)t << 40);
+    int64_t q = lb_u64(u, 0, nu, (uint64_t)(uint32_t)t << 44);
     tile_u0[t] = (int32_t)q;
     // ranges before q = number of range starts in [0, q)
     band_ptr[t] = q == 0 ? 0 : rflag_incl[q - 1];
@@ -446,12 +447,12 @@ __global__ void tile_bounds_k(const uint64_t *u, int64_t nu, const int32_t *rfla
 // starts at a band slot that is a multiple of 4 (apre = exclusive prefix of
 // alen): 4 FP32 or 2 FP64 residuals per granule (bct::BAND_ALIGN).
 __global__ void ranges_k(const uint64_t *u, int64_t nu, const int32_t *rflag, const int32_t *rincl,
-                         int32_t *rstart, int32_t *rlen, int32_t *alen, uint8_t *band_rb)
+                         int32_t *rstart, int32_t *rlen, int32_t *alen, uint16_t *band_rb)
 {
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= nu || !rflag[q]) return;
     int k = rincl[q] - 1;
-    band_rb[k] = (uint8_t)(u[q] >> 32);
+    band_rb[k] = (uint16_t)((u[q] >> 32) & 0xfff);
     const int32_t g0 = (int32_t)(uint32_t)u[q];
     // length: up to the next range start
     int64_t e = q + 1;
@@ -469,7 +470,7 @@ __global__ void range_meta_k(const uint64_t *u, const int32_t *rstart, const int
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n_ranges) return;
     const uint64_t key = u[rstart[k]];
-    const int t = (int)(key >> 40);
+    const int t = (int)(key >> 44);
     const int32_t pre = apre[k] - apre[band_ptr[t]];
     band_meta[k] = make_int2((int32_t)(uint32_t)key,
                              (int32_t)(((uint32_t)pre << 16) | (uint32_t)rlen[k]));
@@ -782,6 +783,10 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     const int vs = dtype == 0 ? 8 : 4;
     const int32_t n_st = (int32_t)st_ptr_h.size() - 1;
     const int32_t n_tiles = (int32_t)((corder_h.size() + tile_cols - 1) / tile_cols);
+    if (n_tiles >= (1 << 20) || m > BCT_MAX_M) {   // band key fields (band_key_k)
+        err = "panel exceeds 2^20 tiles or BCT_MAX_M row blocks";
+        return -1;
+    }
 
     // host tables -> device
     std::vector<int32_t> d2st_h(n_cols), tile_of_d_h(n_cols);
@@ -974,7 +979,7 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     if (nnz > 0) {
         band_key_k<<<nb(nnz, 256), 256, 0, s>>>(cperm, rowid, l2g, rbp, m, sd, tile_of_d, nnz,
                                                  bkey);
-        LCK(sort_keys_u64(bkey, bsorted, nnz, 40 + bits_for(n_tiles), tmp, s));
+        LCK(sort_keys_u64(bkey, bsorted, nnz, 44 + bits_for(n_tiles), tmp, s));
         uniq_flag_k<<<nb(nnz, 256), 256, 0, s>>>(bsorted, nnz, flag);
         LCK(scan_i32(flag, incl, nnz, true, tmp, s));
         nu = read1(incl + nnz - 1, s);
@@ -992,7 +997,7 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     }
     int32_t *band_ptr = K.get<int32_t>(n_tiles + 1);
     int2 *band_meta = K.get<int2>(n_ranges + 1);
-    uint8_t *band_rb = K.get<uint8_t>(n_ranges + 1);
+    uint16_t *band_rb = K.get<uint16_t>(n_ranges + 1);
     int32_t *rstart = T.get<int32_t>(n_ranges + 1), *rlen = T.get<int32_t>(n_ranges + 1);
     int32_t *alen = T.get<int32_t>(n_ranges + 1), *apre = T.get<int32_t>(n_ranges + 1);
     LNN(band_ptr); LNN(band_meta); LNN(band_rb); LNN(rstart); LNN(rlen); LNN(alen); LNN(apre);

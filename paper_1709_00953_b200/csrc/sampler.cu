@@ -25,7 +25,7 @@
 
 namespace {
 
-constexpr int SBLOCK = 256;   // >= BCT_MAX_M
+constexpr int SBLOCK = 256;   // threads per visit; row blocks are strided over them
 
 // numpy pairwise_sum (numpy/_core/src/umath/loops_utils.h.src) over
 // values[ids[q]*stride + j], q in [0, n): sequential below 8 terms, eight
@@ -56,37 +56,54 @@ __device__ double np_pairwise(const int *ids, int n, const double *values, int s
                      np_pairwise(ids + n2, n - n2, values, stride, j));
 }
 
+// shared memory per visit CTA: keys, live flags, live positions, drawn ids
+// (m each) and the visit mask
+inline size_t sampler_smem(int m)
+{
+    return (size_t)m * (8 + 4 + 4 + 4) + 8 * (size_t)mask_words(m);
+}
+
 __global__ void __launch_bounds__(SBLOCK) sample_k(bct::SamplerParams p)
 {
-    __shared__ double key_s[SBLOCK];
-    __shared__ int live_s[SBLOCK];
-    __shared__ int ids_s[SBLOCK];
+    extern __shared__ double smem_d[];
+    const int m = p.m, mw = p.mw;
+    double *key_s = smem_d;
+    int *live_s = reinterpret_cast<int *>(key_s + m);
+    int *pos_s = live_s + m;
+    int *ids_s = pos_s + m;
+    unsigned long long *vmask = reinterpret_cast<unsigned long long *>(
+        smem_d + ((size_t)m * 20 + 7) / 8);
     __shared__ double top_s;
-    __shared__ unsigned long long vmask[BCT_MASKW];
     const int v = blockIdx.x;
     const bct::SampleVisit V = p.visits[v];
-    const int i = threadIdx.x;
-    const int m = p.m;
-    const double raw = i < m ? p.values[(int64_t)i * p.n_panels + V.j] : 0.0;
-    const int live = raw > 0.0 ? 1 : 0;
-    live_s[i] = live;
-    if (i == 0) top_s = 0.0;
-    if (i < BCT_MASKW) vmask[i] = 0ull;
+    if (threadIdx.x == 0) top_s = 0.0;
+    for (int w = threadIdx.x; w < mw; w += SBLOCK) vmask[w] = 0ull;
+    for (int i = threadIdx.x; i < m; i += SBLOCK) {
+        const double raw = p.values[(int64_t)i * p.n_panels + V.j];
+        live_s[i] = raw > 0.0 ? 1 : 0;
+    }
     __syncthreads();
     // max over live raw (order-free), positions of live blocks (exclusive count)
-    if (live && p.strategy != 0) {
+    for (int i = threadIdx.x; i < m; i += SBLOCK) {
+        const double raw = p.values[(int64_t)i * p.n_panels + V.j];
         // doubles > 0 order like their bit patterns
-        atomicMax(reinterpret_cast<unsigned long long *>(&top_s), __double_as_longlong(raw));
+        if (live_s[i] && p.strategy != 0)
+            atomicMax(reinterpret_cast<unsigned long long *>(&top_s), __double_as_longlong(raw));
+        int pos = 0;
+        for (int q = 0; q < i; ++q) pos += live_s[q];
+        pos_s[i] = pos;
     }
-    int pos = 0;
-    for (int q = 0; q < i; ++q) pos += live_s[q];
     __syncthreads();
-    double w = raw;
-    if (p.strategy != 0 && live)
-        w = __dadd_rn(raw, __dmul_rn(p.theta, __dsub_rn(top_s, raw)));
-    key_s[i] = live ? p.exp[V.var_off + pos] / w : 0.0;
+    for (int i = threadIdx.x; i < m; i += SBLOCK) {
+        const double raw = p.values[(int64_t)i * p.n_panels + V.j];
+        double w = raw;
+        if (p.strategy != 0 && live_s[i])
+            w = __dadd_rn(raw, __dmul_rn(p.theta, __dsub_rn(top_s, raw)));
+        key_s[i] = live_s[i] ? p.exp[V.var_off + pos_s[i]] / w : 0.0;
+    }
     __syncthreads();
-    if (live) {
+    for (int i = threadIdx.x; i < m; i += SBLOCK) {
+        if (!live_s[i]) continue;
         const double k = key_s[i];
         int rank = 0;
         for (int q = 0; q < m; ++q)
@@ -98,20 +115,20 @@ __global__ void __launch_bounds__(SBLOCK) sample_k(bct::SamplerParams p)
         }
     }
     __syncthreads();
-    if (i < BCT_MASKW && vmask[i])
-        atomicOr(reinterpret_cast<unsigned long long *>(&p.hdr->epoch_mask[i]), vmask[i]);
+    for (int w = threadIdx.x; w < mw; w += SBLOCK)
+        if (vmask[w]) atomicOr(reinterpret_cast<unsigned long long *>(p.masks + w), vmask[w]);
     if (V.task_base < 0) return;   // another rank's column block: record only
     const int n_groups = (V.draws + p.group_size - 1) / p.group_size;
-    for (int t = i; t < n_groups; t += SBLOCK) {
+    for (int t = threadIdx.x; t < n_groups; t += SBLOCK) {
         const int q0 = t * p.group_size;
         const int n = min(p.group_size, V.draws - q0);
-        TaskDev &T = p.tasks[V.task_base + t];
-        unsigned long long mk[BCT_MASKW] = {0ull, 0ull, 0ull, 0ull};
+        const int64_t k = V.task_base + t;
+        TaskDev &T = p.tasks[k];
+        // the host uploaded zeroed masks for this task
+        uint64_t *mk = p.masks + task_mask_off(k, mw);
+        uint64_t *vk = p.masks + visit_mask_off(k, mw);
         for (int q = 0; q < n; ++q) mk[ids_s[q0 + q] >> 6] |= 1ull << (ids_s[q0 + q] & 63);
-        for (int w4 = 0; w4 < BCT_MASKW; ++w4) {
-            T.mask[w4] = mk[w4];
-            T.visit_mask[w4] = vmask[w4];
-        }
+        for (int w = 0; w < mw; ++w) vk[w] = vmask[w];
         const double s = np_pairwise(ids_s + q0, n, p.values, p.n_panels, V.j);
         T.beta = __dmul_rn(p.b, s) / p.totals[V.j];
     }
@@ -123,7 +140,10 @@ namespace bct {
 
 void launch_sampler(const SamplerParams &p, int n_visits, cudaStream_t s, cudaError_t *err)
 {
-    if (n_visits > 0) sample_k<<<n_visits, SBLOCK, 0, s>>>(p);
+    const size_t smem = sampler_smem(p.m);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(sample_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (n_visits > 0) sample_k<<<n_visits, SBLOCK, smem, s>>>(p);
     *err = cudaGetLastError();
 }
 
