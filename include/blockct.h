@@ -58,7 +58,8 @@ enum { BCT_SERIAL_FAITHFUL = 0, BCT_PARALLEL = 1 };         /* executor.py:37 */
 /* whole-system baselines (solvers.py:283-379): sweep kind and scaling rule */
 enum { BCT_ROW_ACTION = 0, BCT_COLUMN_ACTION = 1 };
 enum { BCT_M_IDENTITY = 0, BCT_M_SUM_INVERSE = 1, BCT_M_NORM_INVERSE = 2 };   /* M_RULES */
-enum { BCT_COMMIT = 1, BCT_METRICS = 2, BCT_SHARDED = 4 };  /* bct_run_epoch flags */
+enum { BCT_COMMIT = 1, BCT_METRICS = 2, BCT_SHARDED = 4,   /* bct_run_epoch flags */
+       BCT_GUARD = 8, BCT_GUARD_REF = 16 };                 /* divergence guard    */
 enum { BCT_IMPORTANCE = 0, BCT_RANDOM = 1, BCT_MIXED = 2 }; /* sampling.py:25 */
 
 /* One column panel A_:j in the reference's cached layout (projector.py:474-488). */
@@ -197,6 +198,12 @@ int bct_audit(bct_ctx *ctx, double *drift);
  * _commit_epoch afterwards, BCT_METRICS fills the result norms,
  * BCT_SHARDED writes partial projection sums to the exchange buffer instead
  * of refreshing r (finish with bct_finish_sharded after an all-reduce).
+ * Divergence guard (solvers.py:251-258, for pipelined drivers that submit
+ * epoch e+1 before reading epoch e): BCT_GUARD_REF (with BCT_COMMIT) records
+ * max(|x|, 1e-12) after the epoch as the reference norm; BCT_GUARD makes the
+ * epoch a no-op when the previous epoch left |x| non-finite or above
+ * factor * reference (bct_set_divergence_factor), so the state stays at the
+ * diverged epoch like the reference's when it raises DivergenceError.
  * Invalid plans fail with BCT_ESCHEDULE before any device state changes.
  */
 int bct_run_epoch(bct_ctx *ctx, int32_t mode, int64_t n_tasks, const int32_t *task_j,
@@ -218,6 +225,9 @@ int bct_sample_epoch(bct_ctx *ctx, int32_t mode, int32_t n_visits, const int32_t
                      int32_t group_size, double b, int32_t strategy, double theta,
                      int32_t flags, int64_t *plan_ids_out);
 
+/* Factor of the divergence guard (SolverParams.divergence_factor, 1e6). */
+int bct_set_divergence_factor(bct_ctx *ctx, double factor);
+
 /* Blocks until the last epoch finished; mus/statuses optional [n_tasks]. */
 int bct_wait_epoch(bct_ctx *ctx, bct_epoch_result *out, double *mus, int32_t *statuses);
 
@@ -230,7 +240,8 @@ int bct_debug_timeline(bct_ctx *ctx, long long *out, int64_t n_tasks, int32_t *g
 /* After the all-reduce of the exchange buffer (enqueued on the context's
  * stream): r = y - S on the drawn rows; the last epoch's result (bct_wait_epoch)
  * then holds the global |y - S|^2, |x|^2, |x_t - x|^2.  Asynchronous when
- * resid_sq is NULL, else it synchronises and returns |y - S|^2. */
+ * resid_sq is NULL, else it synchronises and returns |y - S|^2.  flags: the
+ * epoch's BCT_GUARD / BCT_GUARD_REF (the guard acts on the global |x|). */
 int bct_finish_sharded(bct_ctx *ctx, int32_t flags, double *resid_sq);
 
 /*

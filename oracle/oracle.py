@@ -55,6 +55,11 @@ def lib():
     L = ctypes.CDLL(path)
     L.oracle_trace_ray.restype = _i64
     L.oracle_trace_ray.argtypes = [_dp, _dp, _dp, _dp, _i64p, _i64p, _i64p, _dp]
+    L.oracle_forward_rays.restype = _i64
+    L.oracle_forward_rays.argtypes = [_i64, _dp, _dp, _dp, _dp, _i64p, _dp, _dp]
+    L.oracle_trace_rays.restype = _i64
+    L.oracle_trace_rays.argtypes = [_i64, _dp, _dp, _dp, _dp, _i64p, _i64p, _i64, _i64p, _dp,
+                                    _i64p]
     L.oracle_pb_panel_counts.restype = None
     L.oracle_pb_panel_counts.argtypes = [_i64, _i64, _i64, _dp, _dp, _i64, _i64, _i64p]
     L.oracle_pb_panel_fill.restype = None
@@ -214,49 +219,49 @@ class OracleSystem:
     def scan(cls, geometry, partition, values):
         """_assemble (projector.py:563-626) for a general scan: every column
         block's rays traced per row block in order with the C restatement of
-        _trace_ray_kernel; pixel centres as geometry.py:234-240.  Small cases
-        only (one ctypes call per ray)."""
+        _trace_ray_kernel (hit rows only, entries in the tracer's sorted
+        order); pixel centres as geometry.py:227-240."""
         L = lib()
-        g, det = geometry.grid, geometry.detector
+        g = geometry.grid
         origin = _c(g.origin, np.float64)
         vsize = _c(g.voxel_size, np.float64)
-        nu, nv = det.pixel_counts
-        du, dv = det.pixel_spacing
-        u = (np.arange(nu) - (nu - 1) / 2.0) * du
-        v = (np.arange(nv) - (nv - 1) / 2.0) * dv
-        uu, vv = np.meshgrid(u, v)
-        off = np.column_stack([uu.ravel(), vv.ravel()])
-        per = nu * nv
+        per = geometry.detector.pixels_per_view
+        centers = [oracle_pixel_centers(geometry, v) for v in range(geometry.n_views)]
+        sources = np.array([p.source for p in geometry.poses], dtype=np.float64)
         m, nc = partition.n_row_blocks, partition.n_col_blocks
+        ray_src, ray_dst = [], []
+        for meas in partition.rows:
+            meas = np.asarray(meas, dtype=np.int64)
+            ray_src.append(_c(sources[meas // per], np.float64))
+            ray_dst.append(_c(np.array([centers[int(v)][int(q)] for v, q in
+                                        zip(meas // per, meas % per)]).reshape(-1, 3),
+                              np.float64))
         data, cols, indptr, rbp, l2g = [], [], [], [], []
         for j in range(nc):
             lo = _c(partition.vol_lo[j], np.int64)
             hi = _c(partition.vol_hi[j], np.int64)
             cap = int((hi - lo).sum() + 3)
-            idx = np.empty(cap, np.int64)
-            lng = np.empty(cap)
-            d_parts, c_parts, counts, rows = [], [], [], []
+            d_parts, c_parts, counts_all, rows = [], [], [], []
             rb = np.zeros(m + 1, np.int64)
             for i, meas in enumerate(partition.rows):
-                hits = 0
-                for gm in meas:
-                    pose = geometry.poses[int(gm) // per]
-                    o = off[int(gm) % per]
-                    dst = _c(pose.detector_center + o[0] * pose.det_u + o[1] * pose.det_v,
-                             np.float64)
-                    k = L.oracle_trace_ray(_c(pose.source, np.float64), dst, origin, vsize, lo,
-                                           hi, idx, lng)
-                    if k < 0:
-                        raise ValueError("degenerate ray")
-                    if k > 0:
-                        d_parts.append(lng[:k].copy())
-                        c_parts.append(idx[:k].astype(np.int32))
-                        counts.append(k)
-                        rows.append(int(gm))
-                        hits += 1
-                rb[i + 1] = rb[i] + hits
-            ip = np.zeros(len(counts) + 1, np.int64)
-            np.cumsum(counts, out=ip[1:])
+                n = len(meas)
+                idx = np.empty(n * cap, np.int64)
+                lng = np.empty(n * cap)
+                cnt = np.empty(n, np.int64)
+                bad = L.oracle_trace_rays(n, ray_src[i], ray_dst[i], origin, vsize, lo, hi, cap,
+                                          idx, lng, cnt)
+                if bad >= 0:
+                    raise ValueError("degenerate ray")
+                hit = np.flatnonzero(cnt > 0)
+                for q in hit:
+                    k = int(cnt[q])
+                    d_parts.append(lng[q * cap:q * cap + k])
+                    c_parts.append(idx[q * cap:q * cap + k].astype(np.int32))
+                    counts_all.append(k)
+                rows.extend(int(v) for v in np.asarray(meas, np.int64)[hit])
+                rb[i + 1] = rb[i] + hit.size
+            ip = np.zeros(len(counts_all) + 1, np.int64)
+            np.cumsum(counts_all, out=ip[1:])
             data.append(np.concatenate(d_parts) if d_parts else np.empty(0))
             cols.append(np.concatenate(c_parts) if c_parts else np.empty(0, np.int32))
             indptr.append(ip)
@@ -323,6 +328,39 @@ class OracleSystem:
             rows = np.repeat(self.l2g[j], np.diff(self.indptr[j]))
             A[rows, self.vidx[j][self.cols[j]]] = self.data[j]
         return A
+
+
+def oracle_pixel_centers(geometry, view):
+    """ScanGeometry.pixel_centers (geometry.py:227-240): detector centre +
+    u offset * det_u + v offset * det_v, the reference's numpy expression."""
+    det = geometry.detector
+    nu, nv = det.pixel_counts
+    du, dv = det.pixel_spacing
+    u = (np.arange(nu) - (nu - 1) / 2.0) * du
+    v = (np.arange(nv) - (nv - 1) / 2.0) * dv
+    uu, vv = np.meshgrid(u, v)
+    off = np.column_stack([uu.ravel(), vv.ravel()])
+    pose = geometry.poses[view]
+    return (pose.detector_center[None, :] + off[:, 0:1] * pose.det_u[None, :]
+            + off[:, 1:] * pose.det_v[None, :])
+
+
+def oracle_forward_project(geometry, x):
+    """forward_project (projector.py:348-371): y = A x with every ray traced
+    through the whole grid (simulate_projections with noise 'none',
+    phantoms.py:161-170)."""
+    g = geometry.grid
+    per = geometry.detector.pixels_per_view
+    nv = geometry.n_views
+    src = np.repeat(np.array([p.source for p in geometry.poses], dtype=np.float64), per, axis=0)
+    dst = np.concatenate([oracle_pixel_centers(geometry, v) for v in range(nv)])
+    out = np.empty(nv * per)
+    bad = lib().oracle_forward_rays(nv * per, _c(src, np.float64), _c(dst, np.float64),
+                                    _c(g.origin, np.float64), _c(g.voxel_size, np.float64),
+                                    _c(g.dims, np.int64), _c(x, np.float64), out)
+    if bad >= 0:
+        raise ValueError(f"degenerate ray {bad}")
+    return out
 
 
 # ---------------------------------------------------------------------------

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("BCT_LIB") or os.path.join(
 BCT_OK, BCT_EINVAL, BCT_ECUDA, BCT_ENOMEM, BCT_ESCHEDULE = 0, -1, -2, -3, -4
 BCT_F64, BCT_F32 = 0, 1
 MODES = {"serial_faithful": 0, "parallel": 1}
-BCT_COMMIT, BCT_METRICS, BCT_SHARDED = 1, 2, 4
+BCT_COMMIT, BCT_METRICS, BCT_SHARDED, BCT_GUARD, BCT_GUARD_REF = 1, 2, 4, 8, 16
 STRATEGY_CODES = {"importance": 0, "random": 1, "mixed": 2}
 BCT_ROW_ACTION, BCT_COLUMN_ACTION = 0, 1
 M_RULE_CODES = {"identity": 0, "sum_inverse": 1, "norm_inverse": 2}
@@ -95,6 +95,7 @@ _SIGS = {
     "bct_run_epoch": [_p, _i32, _i64, _p, _p, _p, _p, _p, _i32],
     "bct_sample_epoch": [_p, _i32, _i32, _p, _p, _i64, _p, _i32, _dbl, _i32, _dbl, _i32, _p],
     "bct_wait_epoch": [_p, ctypes.POINTER(EpochResult), _p, _p],
+    "bct_set_divergence_factor": [_p, ctypes.c_double],
     "bct_exchange_buffer": [_p, _pp, ctypes.POINTER(_i64)],
     "bct_finish_sharded": [_p, _i32, _p],
     "bct_debug_timeline": [_p, _p, _i64, _p],
@@ -168,4 +169,5 @@ def i32(a):
 
 __all__ = ["load", "ptr", "check", "Panel", "SystemDesc", "PBDesc", "EpochResult", "EXPORTED",
            "MODES", "BCT_F64", "BCT_F32", "BCT_COMMIT", "BCT_METRICS", "BCT_SHARDED",
+           "BCT_GUARD", "BCT_GUARD_REF",
            "STRATEGY_CODES", "ScheduleError"]

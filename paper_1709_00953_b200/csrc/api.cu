@@ -50,8 +50,10 @@ cudaError_t audit(const double *, const double *, const double *, int64_t, unsig
                   cudaStream_t);
 cudaError_t commit(const PanelDev *, int, int32_t *, double *, double *, cudaStream_t);
 cudaError_t sharded_finish(const double *, const double *, int64_t, const int32_t *,
-                           const uint64_t *, double *, double *, int, cudaStream_t);
-cudaError_t sharded_out(const double *, int, const double *, EpochOut *, cudaStream_t);
+                           const uint64_t *, double *, double *, int, const FinishGuard &,
+                           cudaStream_t);
+cudaError_t sharded_out(const double *, int, const double *, EpochOut *, const FinishGuard &,
+                        cudaStream_t);
 }  // namespace bct
 
 namespace {
@@ -122,6 +124,8 @@ struct bct_ctx {
     double *mus = nullptr, *exchange = nullptr, *vec = nullptr;
     int32_t *statuses = nullptr;
     EpochOut *out = nullptr;
+    double *guard_ref = nullptr;     // divergence guard reference norm (device)
+    double guard_factor = 1e6;
     unsigned int *bar = nullptr, *ticket = nullptr;
     char *d_prep = nullptr;          // [task_cap] per-task records (host_prep), pd.bytes() apart
     char *h_prep = nullptr;          // pinned
@@ -565,6 +569,8 @@ int finalize(bct_ctx *c)
     c->grid = bct::epoch_grid_size(c->dtype, c->device, c->smem_total, &c->block);
     DALLOC(c->part, 8 * (int64_t)c->grid + 8);
     DALLOC(c->out, 1);
+    DALLOC(c->guard_ref, 1);
+    CK(cudaMemsetAsync(c->out, 0, sizeof(EpochOut), c->stream));
     DALLOC(c->bar, 1);
     DALLOC(c->ticket, 1);
     DALLOC(c->audit2, 2);
@@ -1550,6 +1556,7 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
     p.part_task = c->part_task;
     p.statuses = c->statuses; p.out = c->out;
     p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
+    p.guard_ref = c->guard_ref;
     p.prep = c->d_prep;
     p.masks = c->d_masks;
     p.mw = c->mw;
@@ -1797,6 +1804,7 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
     c->h_hdr->n_rows_total = (int32_t)tot_rows;
     c->h_hdr->n_vox_total = (int32_t)tot_vox;
     c->h_hdr->n_ent_total = tot_ent;
+    c->h_hdr->guard_factor = c->guard_factor;
     if (nt) memcpy(c->h_tasks, tasks.data(), sizeof(TaskDev) * nt);
     // masks: the epoch's, then per task its group and its visit's union
     std::copy(emask.begin(), emask.end(), c->h_masks);
@@ -1813,6 +1821,13 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
             host_prep(c, tasks[k], tmasks.data() + (size_t)k * mw, vmasks.data() + (size_t)k * mw,
                       c->h_prep + c->pd.bytes() * k);
     return launch_staged(c, nt, n_visits, hook);
+}
+
+int bct_set_divergence_factor(bct_ctx *c, double factor)
+{
+    if (!c || !(factor > 0.0)) return BCT_EINVAL;
+    c->guard_factor = factor;
+    return 0;
 }
 
 int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *statuses)
@@ -1869,15 +1884,17 @@ int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
 {
     if (!c) return BCT_EINVAL;
     DEVICE_GUARD(c);
-    (void)flags;
     // the drawn blocks of the last epoch, as the device saw them (host plan or sampler)
     const uint64_t *dmask = c->d_masks;   // epoch mask first (EpochParams::masks)
     const int nb = 296;
+    // flags: the epoch's BCT_GUARD / BCT_GUARD_REF (a skipped epoch skips its finish)
+    FinishGuard guard{&c->out->x_sq, c->guard_ref, c->guard_factor, (flags & BCT_GUARD) ? 1 : 0,
+                      (flags & BCT_GUARD_REF) ? 1 : 0};
     CK(bct::sharded_finish(c->y, c->exchange, c->n_meas, c->rb_of_row, dmask, c->r, c->part, nb,
-                           c->stream));
+                           guard, c->stream));
     // the epoch's result (slot of the last submitted epoch) now carries the
     // global norms; bct_wait_epoch returns them
-    CK(bct::sharded_out(c->part, nb, c->exchange + c->n_meas, c->out, c->stream));
+    CK(bct::sharded_out(c->part, nb, c->exchange + c->n_meas, c->out, guard, c->stream));
     Slot &S = c->slots[(c->head + RING - 1) % RING];
     if (S.pending) {
         CK(cudaMemcpyAsync(S.h_out, c->out, sizeof(EpochOut), cudaMemcpyDeviceToHost, c->stream));

@@ -664,8 +664,9 @@ __global__ void commit_kernel(const PanelDev *panels, int np, int32_t *counts, d
 // Sharded tail: r = y - S for rows of drawn blocks; residual norm partials.
 __global__ void sharded_finish_kernel(const double *y, const double *S, int64_t n,
                                       const int32_t *rb_of_row, const uint64_t *mask, double *r,
-                                      double *part)
+                                      double *part, FinishGuard guard)
 {
+    if (guard_tripped(guard)) return;   // the epoch was skipped: r stays
     __shared__ double sh[32];
     double acc = 0.0;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
@@ -688,14 +689,17 @@ __global__ void sharded_finish_kernel(const double *y, const double *S, int64_t 
 // Sharded epoch result on the device: |y - S|^2 from the finish partials (block
 // order, like the host sum it replaces), |x|^2 and |x_t - x|^2 from the
 // all-reduced exchange tail.
-__global__ void sharded_out_kernel(const double *part, int nb, const double *tail, EpochOut *out)
+__global__ void sharded_out_kernel(const double *part, int nb, const double *tail, EpochOut *out,
+                                   FinishGuard guard)
 {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (guard_tripped(guard)) return;   // keep the diverged epoch's result
     double s = 0.0;
     for (int b = 0; b < nb; ++b) s += part[b];
     out->resid_sq = s;
     out->x_sq = tail[0];
     out->err_sq = tail[1];
+    if (guard.set_ref) *guard.ref = fmax(sqrt(tail[0]), 1e-12);
 }
 
 inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
@@ -925,16 +929,17 @@ cudaError_t commit(const PanelDev *panels, int np, int32_t *counts, double *x, d
 }
 
 cudaError_t sharded_finish(const double *y, const double *S, int64_t n, const int32_t *rb_of_row,
-                           const uint64_t *mask, double *r, double *part, int nb, cudaStream_t s)
+                           const uint64_t *mask, double *r, double *part, int nb,
+                           const FinishGuard &guard, cudaStream_t s)
 {
-    sharded_finish_kernel<<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, r, part);
+    sharded_finish_kernel<<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, r, part, guard);
     return cudaGetLastError();
 }
 
 cudaError_t sharded_out(const double *part, int nb, const double *tail, EpochOut *out,
-                        cudaStream_t s)
+                        const FinishGuard &guard, cudaStream_t s)
 {
-    sharded_out_kernel<<<1, 32, 0, s>>>(part, nb, tail, out);
+    sharded_out_kernel<<<1, 32, 0, s>>>(part, nb, tail, out, guard);
     return cudaGetLastError();
 }
 

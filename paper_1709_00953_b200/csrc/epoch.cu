@@ -28,6 +28,7 @@
 // phase-2 code per task, three grid barriers per task, and in serial mode the
 // refresh of the visit's drawn rows after its last task (executor.py:215-223).
 #include <cstdio>
+#include <mutex>
 #include <cuda_runtime.h>
 #include <type_traits>
 
@@ -1462,6 +1463,13 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     const int nthreads = gridDim.x * BLOCK;
     const int m = p.m;
     const EpochHeader hdr = *p.hdr;
+    if (hdr.flags & 8) {
+        // divergence guard: the previous epoch's |x| (its result is still in
+        // p.out; every block reads it before any block can pass a grid
+        // barrier, and only the last block of this launch rewrites it)
+        const double nx = sqrt(__ldcg(&p.out->x_sq));
+        if (!isfinite(nx) || nx > hdr.guard_factor * __ldcg(p.guard_ref)) return;
+    }
     const int n_tasks = hdr.n_tasks;
     const bool serial = hdr.mode == 0;
     const bool sharded = (hdr.flags & 4) != 0;
@@ -1839,6 +1847,8 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             }
             if (do_commit)
                 for (int lp = 0; lp < p.n_panels_owned; ++lp) p.counts[lp] = 0;
+            // reference |x| (sharded: the finish writes it from the global norm)
+            if ((hdr.flags & 16) && !sharded) *p.guard_ref = fmax(sqrt(a1), 1e-12);
             *p.ticket = 0;
         }
     }
@@ -1849,6 +1859,24 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
 namespace bct {
 
 std::string cuda_err(cudaError_t e) { return std::string(cudaGetErrorString(e)); }
+
+// The dynamic shared-memory limit is a per-function, per-device attribute
+// shared by every context of the process: raise it (never lower it) to a
+// context's need before that context sizes or launches its grid.
+static void ensure_smem_attr(int dtype, size_t smem)
+{
+    static std::mutex mu;
+    static size_t set_for[64][2] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    size_t &cur = set_for[dev & 63][dtype != 0];
+    if (smem <= cur) return;
+    cudaFuncSetAttribute(dtype == 0 ? (const void *)epoch_kernel<double>
+                                    : (const void *)epoch_kernel<float>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cur = smem;
+}
 
 size_t epoch_static_smem(int dtype)
 {
@@ -1862,8 +1890,7 @@ int epoch_grid_size(int dtype, int device, size_t smem, int *block)
 {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const void *fn = dtype == 0 ? (const void *)epoch_kernel<double> : (const void *)epoch_kernel<float>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem_attr(dtype, smem);
     if (dtype == 0)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, epoch_kernel<double>, BLOCK, smem);
     else
@@ -1879,15 +1906,7 @@ void launch_epoch(const EpochParams &p, int dtype, int grid, int block, size_t s
 {
     EpochParams local = p;
     void *args[] = {&local};
-    // the dynamic shared-memory limit is per function, shared by every context
-    // of the process: set it to this context's need before each launch
-    static size_t set_for[2] = {0, 0};
-    if (set_for[dtype != 0] != smem) {
-        cudaFuncSetAttribute(dtype == 0 ? (const void *)epoch_kernel<double>
-                                        : (const void *)epoch_kernel<float>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        set_for[dtype != 0] = smem;
-    }
+    ensure_smem_attr(dtype, smem);
     if (dtype == 0)
         *err = cudaLaunchCooperativeKernel((const void *)epoch_kernel<double>, grid, block, args,
                                            smem, s);

@@ -118,6 +118,12 @@ struct EpochHeader {
     int64_t n_ent_total;             // forward-store entries of the batched tasks
     int32_t host_prep;               // 1: EpochParams::prep holds every task's record
     int32_t pad_;
+    // divergence guard (solvers.py:251-258): BCT_GUARD_REF records the
+    // reference norm max(|x|, 1e-12) after this epoch; BCT_GUARD skips the
+    // whole epoch when the previous one left |x| non-finite or above
+    // guard_factor * reference, so a pipelined run stops at the diverged
+    // epoch's state like the reference
+    double guard_factor;
 };
 
 // Device-side per-epoch outputs.
@@ -220,6 +226,7 @@ struct EpochParams {
     int32_t *statuses;
     EpochOut *out;
     double *exchange;          // sharded: n_meas partial sums + 2
+    double *guard_ref;         // divergence guard: reference |x| (device scalar)
     unsigned int *bar;         // grid barrier word
     unsigned int *ticket;      // last-block counter
     long long *timeline;       // optional phase timestamps (BCT_TIMELINE=1)
@@ -227,6 +234,22 @@ struct EpochParams {
 };
 
 struct bct_ctx_s;
+
+// divergence guard of the sharded finish (see EpochHeader::guard_factor): the
+// previous epoch's global |x|^2 is still in EpochOut when the finish of a
+// guarded epoch runs; a diverged predecessor makes the finish a no-op too
+struct FinishGuard {
+    const double *x_sq_prev;   // EpochOut::x_sq
+    double *ref;               // reference |x| (written with set_ref)
+    double factor;
+    int32_t check, set_ref;
+};
+__device__ __forceinline__ bool guard_tripped(const FinishGuard &g)
+{
+    if (!g.check) return false;
+    const double nx = sqrt(*(volatile const double *)g.x_sq_prev);
+    return !isfinite(nx) || nx > g.factor * *(volatile const double *)g.ref;
+}
 
 // builder / launch helpers implemented in the .cu files
 // Position of super-tile voxel q in the staged (g, x) array: the low four bits

@@ -141,14 +141,26 @@ def sharded_forward(system, x, allreduce=None):
 
 
 def run_gcsgd_sharded(system, y, params, x_true=None, schedule=None, plan_record=None,
-                      runner=None):
+                      runner=None, allreduce=None, callback=None):
     """run_gcsgd with the column blocks sharded over the process group
-    (parallel execution).  Returns the full x on every rank and the trace."""
+    (parallel execution).  Returns the full x on every rank and the trace.
+
+    Pipelined like run_gcsgd: epoch e+1 is planned, packed and enqueued
+    (partial epoch, all-reduce, finish -- all on the context's stream) before
+    the host reads epoch e's norms; the device divergence guard makes an epoch
+    submitted after a diverged one a no-op on every rank (the guard reads the
+    all-reduced |x|), so the state on DivergenceError is the diverged epoch's.
+    ``allreduce`` (default torch.distributed.all_reduce) sums a device tensor
+    in place across ranks.  A callback disables the pipelining, as in
+    run_gcsgd.  Audits are rank-local and not offered here."""
     import torch
     import torch.distributed as dist
     if params.execution_mode != "parallel":
         raise ConfigurationError("sharded execution requires execution_mode='parallel'")
-    runner = runner or ShardedRunner(system)
+    if params.audit_interval:
+        raise ConfigurationError("audit_interval is not supported by sharded runs")
+    allreduce = allreduce or dist.all_reduce
+    runner = runner or ShardedRunner(system, allreduce=allreduce)
     if schedule is not None:
         scheduler = ScriptedScheduler(schedule, group_size=params.group_size)
     else:
@@ -163,18 +175,44 @@ def run_gcsgd_sharded(system, y, params, x_true=None, schedule=None, plan_record
         system.set_x_true(x_true)
     else:
         system.set_x_true(None)
+    N.check(N.load().bct_set_divergence_factor(system.ctx, float(params.divergence_factor)),
+            system.ctx)
     flags = N.BCT_COMMIT | N.BCT_METRICS
     trace = ConvergenceTrace()
     started = time.perf_counter()
     ref_norm = None
-    for epoch in range(1, params.epochs + 1):
+    pipelined = callback is None
+
+    def prepare(epoch):
         theta_now = scheduler.theta
-        plan = scheduler.epoch_plan(epoch, rng)
+        try:
+            plan = scheduler.epoch_plan(epoch, rng)
+            packed = pack_loops(_loops(plan, system.table, params.b), system)
+        except Exception as exc:  # surfaced when the loop reaches this epoch
+            return exc, None, theta_now
         if plan_record is not None:
             plan_record[epoch] = plan
-        packed = pack_loops(_loops(plan, system.table, params.b), system)
-        res = runner.epoch(packed, flags)
         scheduler.advance_epoch()
+        return packed, plan, theta_now
+
+    def launch(prep, epoch):
+        if not isinstance(prep[0], Exception):
+            runner.submit(prep[0], flags | (N.BCT_GUARD_REF if epoch == 1 else N.BCT_GUARD))
+
+    pending = None
+    if params.epochs >= 1:
+        pending = prepare(1)
+        launch(pending, 1)
+    for epoch in range(1, params.epochs + 1):
+        packed, _, theta_now = pending
+        if isinstance(packed, Exception):
+            raise packed
+        nxt = None
+        if pipelined and epoch < params.epochs:
+            nxt = prepare(epoch + 1)
+            launch(nxt, epoch + 1)
+        res = runner.collect()
+        state.epoch = epoch
         snr = snr_from_sq(xt_norm, res.err_sq) if x_true is not None else math.nan
         gap = snr_from_sq(y_norm, res.resid_sq) if y_norm > 0 else math.nan
         row = TraceRow(epoch, epoch * params.sampling.alpha, snr, gap,
@@ -185,8 +223,18 @@ def run_gcsgd_sharded(system, y, params, x_true=None, schedule=None, plan_record
         if ref_norm is None:
             ref_norm = max(norm_x, 1e-12)
         if not math.isfinite(norm_x) or norm_x > params.divergence_factor * ref_norm:
+            if nxt is not None and not isinstance(nxt[0], Exception):
+                runner.collect()          # the guarded no-op epoch
+                if plan_record is not None:
+                    plan_record.pop(epoch + 1, None)
             raise DivergenceError(f"image norm {norm_x:.3e} left the stable region at epoch "
                                   f"{epoch}", last_good_epoch=epoch - 1, trace=trace)
+        if callback is not None:
+            callback(epoch, state, row)
+        if not pipelined and epoch < params.epochs:
+            nxt = prepare(epoch + 1)
+            launch(nxt, epoch + 1)
+        pending = nxt
     # assemble the full image: owned entries from every rank
     x_local = system.get_x()
     mine = np.zeros(system.n_voxels)
@@ -194,5 +242,5 @@ def run_gcsgd_sharded(system, y, params, x_true=None, schedule=None, plan_record
         v = system.voxel_indices(j)
         mine[v] = x_local[v]
     t = torch.as_tensor(mine, device=f"cuda:{system.device}")
-    dist.all_reduce(t)
+    allreduce(t)
     return t.cpu().numpy(), trace

@@ -108,6 +108,34 @@ def circular_trajectory(n_views, radius, rotation_center=(0.0, 0.0, 0.0), angula
     return poses
 
 
+def random_sphere_trajectory(n_views, radius, source_detector_distance, seed):
+    """Random sphere scan about the origin (geometry.py:283-312): per view
+    a ~ U[0, pi], b ~ U[0, 2 pi) from ``default_rng(seed)`` (all a's drawn
+    first, then all b's); source at radius * (sin a cos b, sin a sin b, cos a),
+    detector centre ``source_detector_distance`` along the inward axis w,
+    det_u = normalised (h x w) with h = +z unless |w_z| >= 0.9 (then +x),
+    det_v = w x det_u.  Same numpy/math operations, so the poses (and the
+    traced panels) are bit-identical to the reference's."""
+    n_views = check_count("n_views", n_views)
+    radius = check_positive("radius", radius)
+    dist = check_positive("source_detector_distance", source_detector_distance)
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(0.0, math.pi, size=n_views)
+    b = rng.uniform(0.0, 2.0 * math.pi, size=n_views)
+    poses = []
+    for k in range(n_views):
+        sa, ca = math.sin(a[k]), math.cos(a[k])
+        sb, cb = math.sin(b[k]), math.cos(b[k])
+        src = radius * np.array([sa * cb, sa * sb, ca])
+        w = -src / radius
+        det = src + dist * w
+        h = np.array([0.0, 0.0, 1.0]) if abs(w[2]) < 0.9 else np.array([1.0, 0.0, 0.0])
+        u = np.cross(h, w)
+        u /= np.linalg.norm(u)
+        poses.append(ViewPose(src, det, u, np.cross(w, u)))
+    return poses
+
+
 @dataclass(frozen=True)
 class ScanGeometry:
     grid: VolumeGrid

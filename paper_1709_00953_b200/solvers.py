@@ -187,6 +187,11 @@ def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=N
     else:
         system.set_x_true(None)
     flags = N.BCT_COMMIT | N.BCT_METRICS
+    # divergence guard on the device: epoch 1 records the reference norm, and
+    # an epoch submitted before the host saw its predecessor diverge is a
+    # no-op, so the state on raise is the diverged epoch's (solvers.py:251-258)
+    N.check(N.load().bct_set_divergence_factor(system.ctx, float(params.divergence_factor)),
+            system.ctx)
     mode = params.execution_mode
     started = time.perf_counter()
     ref_norm = None
@@ -210,18 +215,19 @@ def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=N
         scheduler.advance_epoch()
         return packed, theta_now
 
-    def launch(prep):
+    def launch(prep, epoch):
         if isinstance(prep[0], Exception):
             return
+        fl = flags | (N.BCT_GUARD_REF if epoch == 1 else N.BCT_GUARD)
         if sampled:
-            submit_sampled(system, mode, prep[0], params.b, params.sampling.strategy, flags)
+            submit_sampled(system, mode, prep[0], params.b, params.sampling.strategy, fl)
         else:
-            submit(system, mode, prep[0], flags)
+            submit(system, mode, prep[0], fl)
 
     pending = None
     if params.epochs >= 1:
         pending = prepare(1)
-        launch(pending)
+        launch(pending, 1)
     for epoch in range(1, params.epochs + 1):
         packed, theta_now = pending
         if isinstance(packed, Exception):
@@ -229,7 +235,7 @@ def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=N
         nxt = None
         if pipelined and epoch < params.epochs:
             nxt = prepare(epoch + 1)
-            launch(nxt)
+            launch(nxt, epoch + 1)
         res, _, _ = wait(system, packed.task_j.size)
         if sampled:
             plan = packed.finalize()
@@ -264,7 +270,7 @@ def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=N
             callback(epoch, state, row)
         if not pipelined and epoch < params.epochs:
             nxt = prepare(epoch + 1)
-            launch(nxt)
+            launch(nxt, epoch + 1)
         pending = nxt
     return system.get_x(), trace
 
