@@ -283,17 +283,26 @@ def run_ours(args):
     warm_params = SolverParams(epochs=args.warmup, b=cfg.b, group_size=cfg.group_size,
                                execution_mode=cfg.mode, seed=cfg.solver_seed + 2,
                                sampling=SamplingConfig(alpha=cfg.alpha, gamma=cfg.gamma))
-    if sharded:
-        D.run_gcsgd_sharded(system, y, warm_params, x_true=x_true)
-        torch.distributed.barrier()
-    else:
-        run_gcsgd(system, y, warm_params, x_true=x_true)
+    # the host inputs live in pinned memory (the contract's "from pinned host
+    # memory"); the library DMAs page-locked buffers directly
+    y_h = torch.empty(y.size, dtype=torch.float64).pin_memory().numpy()
+    xt_h = torch.empty(x_true.size, dtype=torch.float64).pin_memory().numpy()
+    y_h[:] = y
+    xt_h[:] = x_true
+    # two untimed calls: the first pays one-time set-up, the second still
+    # warms host-side caches (measured: config 3 28 -> 12 -> 8 ms per call)
+    for _ in range(2):
+        if sharded:
+            D.run_gcsgd_sharded(system, y_h, warm_params, x_true=xt_h)
+            torch.distributed.barrier()
+        else:
+            run_gcsgd(system, y_h, warm_params, x_true=xt_h)
     torch.cuda.synchronize(device)
     e0.record(stream)
     if sharded:
-        x_out, tr = D.run_gcsgd_sharded(system, y, e2e_params, x_true=x_true)
+        x_out, tr = D.run_gcsgd_sharded(system, y_h, e2e_params, x_true=xt_h)
     else:
-        x_out, tr = run_gcsgd(system, y, e2e_params, x_true=x_true)
+        x_out, tr = run_gcsgd(system, y_h, e2e_params, x_true=xt_h)
     e1.record(stream)
     torch.cuda.synchronize(device)
     e2e_ms = e0.elapsed_time(e1)

@@ -50,8 +50,8 @@ cudaError_t audit(const double *, const double *, const double *, int64_t, unsig
                   cudaStream_t);
 cudaError_t commit(const PanelDev *, int, int32_t *, double *, double *, cudaStream_t);
 cudaError_t sharded_finish(const double *, const double *, int64_t, const int32_t *,
-                           const uint64_t *, double *, double *, int, const FinishGuard &,
-                           cudaStream_t);
+                           const uint64_t *, double *, float *, double *, int,
+                           const FinishGuard &, cudaStream_t);
 cudaError_t sharded_out(const double *, int, const double *, EpochOut *, const FinishGuard &,
                         cudaStream_t);
 }  // namespace bct
@@ -114,6 +114,8 @@ struct bct_ctx {
     int32_t *rb_of_row = nullptr;
     double *y = nullptr, *r = nullptr, *z = nullptr, *x = nullptr, *xhat = nullptr;
     float *r32 = nullptr;   // FP32 mode: band staging copy of r (epoch kernel)
+    bool r32_valid = false; // r32 == (float)r (every device writer of r keeps r32 in step;
+                            // host writes of r clear it)
     double *x_true = nullptr;
     int32_t *counts = nullptr;
     double *gx = nullptr, *t_ax = nullptr, *seg_part = nullptr, *part = nullptr;
@@ -1238,8 +1240,24 @@ static int pin_init(bct_ctx *c)
     return 0;
 }
 
+// Page-locked caller buffers (cudaHostAlloc / cudaHostRegister, e.g. a
+// pinned torch tensor's numpy view) are copied directly at full DMA rate.
+static bool is_pinned(const void *p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 static int h2d_staged(bct_ctx *c, void *dst, const void *src, size_t bytes)
 {
+    if (bytes > 0 && is_pinned(src)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+        return 0;
+    }
     if (int r = pin_init(c)) return r;
     size_t off = 0;
     for (int i = 0; off < bytes; ++i, off += PIN_CHUNK) {
@@ -1256,6 +1274,11 @@ static int h2d_staged(bct_ctx *c, void *dst, const void *src, size_t bytes)
 
 static int d2h_staged(bct_ctx *c, void *dst, const void *src, size_t bytes)
 {
+    if (bytes > 0 && is_pinned(dst)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return 0;
+    }
     if (int r = pin_init(c)) return r;
     const size_t nch = (bytes + PIN_CHUNK - 1) / PIN_CHUNK;
     auto issue = [&](size_t i) -> cudaError_t {
@@ -1366,6 +1389,7 @@ int bct_set_r(bct_ctx *c, const double *r)
     DEVICE_GUARD(c);
     if (int e = h2d_staged(c, c->r, r, 8 * c->n_meas)) return e;
     CK(cudaStreamSynchronize(c->stream));
+    c->r32_valid = false;
     return 0;
 }
 
@@ -1471,6 +1495,7 @@ int bct_reset_residual(bct_ctx *c)
     CK(bct::zsum(c->inv_ptr, c->inv_z, c->n_meas, c->z, c->vec, c->stream));
     CK(bct::sub(c->y, c->vec, c->n_meas, c->r, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    c->r32_valid = false;
     return 0;
 }
 
@@ -1805,6 +1830,9 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
     c->h_hdr->n_vox_total = (int32_t)tot_vox;
     c->h_hdr->n_ent_total = tot_ent;
     c->h_hdr->guard_factor = c->guard_factor;
+    c->h_hdr->r32_valid = c->r32_valid ? 1 : 0;
+    // a batched FP32 epoch refreshes the copy before phase A
+    if (batched && c->dtype == BCT_F32) c->r32_valid = true;
     if (nt) memcpy(c->h_tasks, tasks.data(), sizeof(TaskDev) * nt);
     // masks: the epoch's, then per task its group and its visit's union
     std::copy(emask.begin(), emask.end(), c->h_masks);
@@ -1890,8 +1918,8 @@ int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
     // flags: the epoch's BCT_GUARD / BCT_GUARD_REF (a skipped epoch skips its finish)
     FinishGuard guard{&c->out->x_sq, c->guard_ref, c->guard_factor, (flags & BCT_GUARD) ? 1 : 0,
                       (flags & BCT_GUARD_REF) ? 1 : 0};
-    CK(bct::sharded_finish(c->y, c->exchange, c->n_meas, c->rb_of_row, dmask, c->r, c->part, nb,
-                           guard, c->stream));
+    CK(bct::sharded_finish(c->y, c->exchange, c->n_meas, c->rb_of_row, dmask, c->r, c->r32,
+                           c->part, nb, guard, c->stream));
     // the epoch's result (slot of the last submitted epoch) now carries the
     // global norms; bct_wait_epoch returns them
     CK(bct::sharded_out(c->part, nb, c->exchange + c->n_meas, c->out, guard, c->stream));

@@ -664,7 +664,7 @@ __global__ void commit_kernel(const PanelDev *panels, int np, int32_t *counts, d
 // Sharded tail: r = y - S for rows of drawn blocks; residual norm partials.
 __global__ void sharded_finish_kernel(const double *y, const double *S, int64_t n,
                                       const int32_t *rb_of_row, const uint64_t *mask, double *r,
-                                      double *part, FinishGuard guard)
+                                      float *r32, double *part, FinishGuard guard)
 {
     if (guard_tripped(guard)) return;   // the epoch was skipped: r stays
     __shared__ double sh[32];
@@ -673,7 +673,10 @@ __global__ void sharded_finish_kernel(const double *y, const double *S, int64_t 
          g += (int64_t)gridDim.x * blockDim.x) {
         double d = y[g] - S[g];
         int rb = rb_of_row[g];
-        if (rb >= 0 && ((mask[rb >> 6] >> (rb & 63)) & 1ull)) r[g] = d;
+        if (rb >= 0 && ((mask[rb >> 6] >> (rb & 63)) & 1ull)) {
+            r[g] = d;
+            if (r32) r32[g] = (float)d;   // FP32 mode's band copy stays in step
+        }
         acc = fma(d, d, acc);
     }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -929,10 +932,10 @@ cudaError_t commit(const PanelDev *panels, int np, int32_t *counts, double *x, d
 }
 
 cudaError_t sharded_finish(const double *y, const double *S, int64_t n, const int32_t *rb_of_row,
-                           const uint64_t *mask, double *r, double *part, int nb,
+                           const uint64_t *mask, double *r, float *r32, double *part, int nb,
                            const FinishGuard &guard, cudaStream_t s)
 {
-    sharded_finish_kernel<<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, r, part, guard);
+    sharded_finish_kernel<<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, r, r32, part, guard);
     return cudaGetLastError();
 }
 

@@ -1023,9 +1023,11 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     using TB = typename std::conditional<sizeof(V) == 4, float, double>::type;
     const TB *rband;
     if constexpr (sizeof(V) == 4) {
-        for (int64_t i = (int64_t)b * BLOCK + threadIdx.x; i < p.n_meas; i += (int64_t)G * BLOCK)
-            p.r32[i] = (float)p.r[i];
-        grid_sync(p.bar);
+        if (!hdr.r32_valid) {   // r was written outside an epoch since the last copy
+            for (int64_t i = (int64_t)b * BLOCK + threadIdx.x; i < p.n_meas; i += (int64_t)G * BLOCK)
+                p.r32[i] = (float)p.r[i];
+            grid_sync(p.bar);
+        }
         rband = p.r32;
     } else {
         rband = p.r;
@@ -1739,7 +1741,9 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                     }
                     acc += v;
                 }
-                p.r[g] = p.y[g] - acc;
+                const double rv = p.y[g] - acc;
+                p.r[g] = rv;
+                if (p.r32) p.r32[g] = (float)rv;
             }
             if (k + 1 < n_tasks) grid_sync(p.bar);
         }
@@ -1783,7 +1787,10 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             } else {
                 double d = p.y[g] - acc;
                 int rb = p.rb_of_row[g];
-                if (!serial && rb >= 0 && mask_has(p.masks, rb)) p.r[g] = d;
+                if (!serial && rb >= 0 && mask_has(p.masks, rb)) {
+                    p.r[g] = d;
+                    if (p.r32) p.r32[g] = (float)d;
+                }
                 rsq = fma(d, d, rsq);
             }
         }

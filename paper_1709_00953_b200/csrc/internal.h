@@ -117,7 +117,8 @@ struct EpochHeader {
     int32_t n_tiles_total, n_slices_total, n_rows_total, n_vox_total;
     int64_t n_ent_total;             // forward-store entries of the batched tasks
     int32_t host_prep;               // 1: EpochParams::prep holds every task's record
-    int32_t pad_;
+    int32_t r32_valid;               // FP32 mode: r32 == (float)r on every row (every
+                                     // writer of r in a launch keeps it so)
     // divergence guard (solvers.py:251-258): BCT_GUARD_REF records the
     // reference norm max(|x|, 1e-12) after this epoch; BCT_GUARD skips the
     // whole epoch when the previous one left |x| non-finite or above

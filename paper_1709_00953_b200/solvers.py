@@ -67,7 +67,9 @@ class SolverState:
 
     @classmethod
     def initialize(cls, system, y, x0=None):
-        y = as_vector("y", y, length=system.n_measurements).copy()
+        # float64 and contiguous (no copy when it already is: the device holds
+        # the solver's copy, the host keeps it for the trace's |y| only)
+        y = as_vector("y", y, length=system.n_measurements)
         system.set_y(y)
         system.reset_accumulators()
         if x0 is None:
@@ -177,11 +179,9 @@ def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=N
     state = SolverState.initialize(system, y, x0=x0)
     rng = np.random.default_rng(params.seed)
     trace = ConvergenceTrace()
-    y_norm = float(np.linalg.norm(state.y))
     if x_true is not None:
         x_true = as_vector("x_true", x_true, length=system.n_voxels)
-        xt_norm = float(np.linalg.norm(x_true))
-        if xt_norm == 0.0:
+        if not np.any(x_true):
             raise ConfigurationError("reference signal is identically zero")
         system.set_x_true(x_true)
     else:
@@ -228,6 +228,9 @@ def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=N
     if params.epochs >= 1:
         pending = prepare(1)
         launch(pending, 1)
+    # host-side norms for the trace while the device runs epoch 1
+    y_norm = float(np.linalg.norm(state.y))
+    xt_norm = float(np.linalg.norm(x_true)) if x_true is not None else math.nan
     for epoch in range(1, params.epochs + 1):
         packed, theta_now = pending
         if isinstance(packed, Exception):

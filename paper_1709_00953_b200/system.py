@@ -77,7 +77,6 @@ class DeviceBlockSystem:
                                             None), self._ctx, "bct_panel_info")
             self._n_rows[j] = nr.value
             self._nnz[j] = nz.value
-        self._y_norm = None
 
     # -- construction -------------------------------------------------------
 
@@ -307,7 +306,6 @@ class DeviceBlockSystem:
     def set_y(self, y):
         y = N.f64(y)
         N.check(N.load().bct_set_y(self._ctx, N.ptr(y)), self._ctx)
-        self._y_norm = float(np.linalg.norm(y))
 
     def set_r(self, r):
         r = N.f64(r)
