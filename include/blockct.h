@@ -152,6 +152,9 @@ int bct_destroy(bct_ctx *ctx);
 int bct_info(const bct_ctx *ctx, int64_t *out8);
 int bct_panel_info(const bct_ctx *ctx, int32_t j, int64_t *n_rows, int64_t *nnz,
                    int64_t *n_cols);
+/* The panel in the reference's cached layout (projector.py:474-488); any
+ * output may be NULL; with data, cols and indptr all NULL only the row maps
+ * (rbp, l2g) are produced, without merging the stored entries. */
 int bct_get_panel(bct_ctx *ctx, int32_t j, double *data, int32_t *cols, int64_t *indptr,
                   int64_t *rbp, int64_t *l2g);
 int bct_get_table(bct_ctx *ctx, double *values, double *totals);

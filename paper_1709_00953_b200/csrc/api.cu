@@ -1135,6 +1135,14 @@ int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *i
     int lp = j - c->pb;
     const PanelDev &P = c->h_panels[lp];
     CK(cudaStreamSynchronize(c->stream));
+    if (rbp)
+        for (int i = 0; i <= c->m; ++i) rbp[i] = c->h_rbp[lp][i];
+    if (l2g && P.n_rows > 0) {
+        std::vector<int32_t> lg(P.n_rows);
+        CK(cudaMemcpy(lg.data(), P.l2g, 4 * P.n_rows, cudaMemcpyDeviceToHost));
+        for (int32_t q = 0; q < P.n_rows; ++q) l2g[q] = lg[q];
+    }
+    if (!data && !cols && !indptr) return 0;   // row maps only
     const int64_t cap = std::max<int64_t>(P.fwd_cap, 1);
     std::vector<double> fv(cap);
     std::vector<uint16_t> fi(cap);
@@ -1183,10 +1191,6 @@ int bct_get_panel(bct_ctx *c, int32_t j, double *data, int32_t *cols, int64_t *i
         }
     }
     if (indptr) indptr[P.n_rows] = o;
-    if (rbp)
-        for (int i = 0; i <= c->m; ++i) rbp[i] = c->h_rbp[lp][i];
-    if (l2g)
-        for (int32_t q = 0; q < P.n_rows; ++q) l2g[q] = lg[q];
     return 0;
 }
 

@@ -233,6 +233,14 @@ class DeviceBlockSystem:
     def owns(self, j):
         return self.panel_begin <= j < self.panel_end
 
+    def panel_l2g(self, j):
+        """Global measurement id of each local row of panel j (no entry merge)."""
+        L = N.load()
+        lg = np.empty(self._n_rows[j], dtype=np.int64)
+        N.check(L.bct_get_panel(self._ctx, j, None, None, None, None, N.ptr(lg)), self._ctx,
+                "bct_get_panel")
+        return lg
+
     def panel(self, j):
         """The panel's forward CSR as stored (f32 values are widened)."""
         nr = ctypes.c_int64()

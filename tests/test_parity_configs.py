@@ -334,3 +334,56 @@ def test_cfg4_teacher_forced(cfg4, dtype):
               f"FP32 arithmetic alone x {ax:.3e} r {ar:.3e} z {az:.3e}")
         assert max(ax, ar, az) <= FP32_TF_TOL["r"]
         sysm.close()
+
+
+# ---------------------------------------------------------------------------
+# config 5 (2048^2, 7.69e9 nnz: 64-bit entry counts, 123 GB of A on one B200)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.slow
+def test_cfg5_full_size_two_panel_epoch():
+    """BASELINE configs[4] built on one GPU (FP32 store): a batched epoch of
+    two full-panel visits from the device's own epoch-1 state, checked
+    against the oracle on the reference tracer's FP64 panels of those two
+    column blocks: x and z of the visited blocks within FP32_TF_TOL, and r
+    against y - sum_j z^j (projector.py:742-754's fold) over every row."""
+    cfg = CONFIGS[5]
+    s = cfg.spec
+    dev = DeviceBlockSystem.parallel_beam(s, dtype="f32")
+    assert dev.nnz == 7690094897
+    xt = random_ellipses(s.n, cfg.n_ellipses, cfg.phantom_seed)
+    y, _ = add_noise(dev.forward(xt), cfg.noise_frac, cfg.noise_seed)
+    run_gcsgd(dev, y, cfg_params(cfg, 1), x_true=xt)
+    assert dev.audit_drift() <= 1e-8
+    x0, r0, z0 = dev.get_x(), dev.get_r(), dev.get_z()
+    js = (5, 40)
+    ora = OracleSystem.parallel_beam(s.n, s.views, s.bins, s.m, s.nc, panels=set(js))
+    for j in js:   # same hit rows and structure as the device's store
+        np.testing.assert_array_equal(ora.l2g[j], dev.panel_l2g(j))
+    rng = np.random.default_rng(3)
+    loops = []
+    for j in js:
+        ids = rng.permutation(s.m).astype(np.int64)
+        loops.append((j, [(ids, oracle_group_beta(ora.table, cfg.b, j, ids))]))
+    st = OracleState.initialize(ora, y)
+    st.x, st.r = x0.copy(), r0.copy()
+    st.z = [z0[j].copy() if j in js else np.zeros(0) for j in range(s.nc)]
+    oracle_run_epoch(ora, st, loops, "parallel", workers=WORKERS)
+    oracle_commit_epoch(st, ora)
+    sst = SolverState.initialize(dev, y)
+    sst.load(x0, r0, z0)
+    EpochExecutor("parallel").run_epoch(2, loops, sst, dev)
+    dev.commit_epoch()
+    vox = np.concatenate([dev.voxel_indices(j) for j in js])
+    xd, zd, rd = dev.get_x(), dev.get_z(), dev.get_r()
+    ex = rel(xd[vox], st.x[vox])
+    ez = max(rel(zd[j], st.z[j]) for j in js)
+    acc = np.zeros(s.n_measurements)
+    for j in range(s.nc):
+        np.add.at(acc, dev.panel_l2g(j), st.z[j] if j in js else z0[j])
+    er = rel(rd, y - acc)
+    print(f"cfg5 f32 two-panel epoch rel err x {ex:.3e} z {ez:.3e} r {er:.3e}")
+    assert ex <= FP32_TF_TOL["x"] and ez <= FP32_TF_TOL["z"] and er <= FP32_TF_TOL["r"]
+    assert np.array_equal(xd[np.setdiff1d(np.arange(s.n_voxels), vox)],
+                          x0[np.setdiff1d(np.arange(s.n_voxels), vox)])
+    dev.close()
