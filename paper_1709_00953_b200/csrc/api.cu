@@ -61,14 +61,16 @@ namespace {
 constexpr int RING = 4;
 // voxels per super tile: its (g, x) pairs are staged in shared memory for
 // phase 2 -- 16384 x 8 B (float2, 128 KB) in FP32 mode: fewer (row, super
-// tile) segments per row for the batched epochs; 4096 x 16 B in FP64 mode,
-// whose serial per-task epochs would stage a large tile per CTA for little work
-// (the matrix-free phase B needs segments that are whole walk runs: <= 255
-// entries, so it keeps 4096-voxel super tiles)
+// tile) segments per row for the batched epochs; 8192 x 16 B (128 KB) in
+// FP64 mode (the matrix-free phase B needs segments that are whole walk
+// runs: <= 255 entries, so it keeps 4096-voxel super tiles)
 inline int st_voxels(int dtype)
 {
     if (getenv("BCT_ST_SMALL") || getenv("BCT_REPLAY")) return 4096;
-    return dtype == 0 ? 4096 : 16384;   // FP64 configs run per-task (small) epochs
+    // FP64 configs run per-task (small) epochs: a strip panel of up to 8192
+    // voxels is one super tile, so its rows are single segments (epoch.cu
+    // phase 2a then finishes rows without a grid barrier)
+    return dtype == 0 ? 8192 : 16384;
 }
 constexpr size_t SMEM_BUDGET = 218 * 1024;  // dynamic shared memory per CTA (one CTA per SM;
                                             // 227 KB less the kernel's static arrays)

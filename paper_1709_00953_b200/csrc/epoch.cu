@@ -834,6 +834,29 @@ __device__ __forceinline__ void tile_vr(const PanelDev &P, int m, int t, int sl0
     }
 }
 
+// A super tile's (g, x) pairs into shared memory, swizzled (swz_idx), as
+// GS (float2 in FP32 mode): each thread issues its loads of a round before
+// its stores (a load-store chain per element costs one L2 round trip each).
+// L2-coherent loads: the pairs were written earlier in this launch.
+template <typename GS>
+__device__ __forceinline__ void stage_gx(GS *gs, const double2 *src, int n, int shift)
+{
+    constexpr int U = 4;
+    for (int q0 = threadIdx.x; q0 < n; q0 += U * BLOCK) {
+        double2 a[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = q0 + u * BLOCK;
+            a[u] = q < n ? __ldcg(src + q) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = q0 + u * BLOCK;
+            if (q < n) gs[swz_idx(q, shift)] = GS{(decltype(GS::x))a[u].x, (decltype(GS::x))a[u].y};
+        }
+    }
+}
+
 __device__ __forceinline__ double z_value(double t, double ax, double mu, int status)
 {
     return status == 0 ? fma(mu, t, ax) : ax;
@@ -1177,10 +1200,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const double2 *gx = gxb + T.gx_off;
             ++dbg_segs;
             const long long tst0 = p.timeline ? gtimer() : 0;
-            for (int q = threadIdx.x; q < v1 - v0; q += BLOCK) {
-                const double2 a = gx[v0 + q];
-                gs[swz_idx(q, P.swz_shift)] = GS{(decltype(GS::x))a.x, (decltype(GS::x))a.y};
-            }
+            stage_gx(gs, gx + v0, v1 - v0, P.swz_shift);
             __syncthreads();
             if (p.timeline) dbg_stage += gtimer() - tst0;   // profiling: super-tile staging
             const V *fv = static_cast<const V *>(P.fvals);
@@ -1534,6 +1554,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             for (int it = 0; it < n_items; ++it) {
                 cp_async_wait_all();
                 __syncthreads();
+                if (it == 0) TL_MARK(k, 7);   // profiling: the first band is staged
                 const int t = item_tile(it);
                 int c0 = 0, c1 = NSL;
                 if (it >= full) {
@@ -1574,15 +1595,22 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         // SELL-32 slices, one segment per lane; (g, x) of the slice's super
         // tile staged in shared memory.  A full-panel task splits the slices
         // among CTAs by stored entries, any other task by slice count.
+        // A panel whose rows are single segments (one super tile, uncut
+        // runs: every strip panel of an FP64 context up to 8192 voxels) has
+        // its rows complete in this CTA's slices: the CTA sums their parts
+        // itself, and the grid barrier + row pass of phase 2b go away.
+        const bool fused = P.n_st == 1 && P.n_seg == P.n_rows;
+        const bool rfull = R.h->full != 0;
+        int ub, ue;
         {
             const V *fv = static_cast<const V *>(P.fvals);
             double2 *spart = reinterpret_cast<double2 *>(p.seg_part);
             const int ns = R.st_pre[R.h->nst];
-            const bool rfull = R.h->full != 0;
-            int ub, ue;
             if (rfull) {
                 __shared__ int s_lim[2];
                 if (threadIdx.x < 2) {
+                    // equal shares of stored entries (a per-slice cost as in the
+                    // batched phase B measured slower here: 13.1 -> 14.0 us)
                     const int64_t F = __ldg(P.slice_start + P.n_slices);
                     const int32_t key = (int32_t)(F * (blockIdx.x + threadIdx.x) / gridDim.x);
                     int lo = 0, hi = P.n_slices;
@@ -1605,10 +1633,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 while (fu >= R.st_pre[st + 1]) ++st;
                 const int ge = min(ue, R.st_pre[st + 1]);
                 const int v0 = __ldg(P.st_ptr + st), v1 = __ldg(P.st_ptr + st + 1);
-                for (int q = threadIdx.x; q < v1 - v0; q += BLOCK) {
-                    const double2 a = gx[v0 + q];
-                    gs[swz_idx(q, P.swz_shift)] = GS{(decltype(GS::x))a.x, (decltype(GS::x))a.y};
-                }
+                stage_gx(gs, gx + v0, v1 - v0, P.swz_shift);
                 __syncthreads();
                 // work unit = (slice, part): part q of a slice takes its
                 // vectors kv = q (mod TASK_SPLIT), so a single task (a few
@@ -1641,11 +1666,35 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             }
         }
         TL_MARK(k, 3);
+        const int n_task_rows = R.pre[R.h->n_runs];
+        wsum = 0.0;
+        if (fused) {
+            // rows of this CTA's slices (written by this CTA above: the
+            // __syncthreads that closed the loop orders them): t, ax = the
+            // lane's TASK_SPLIT parts in order; denominators per CTA
+            const double2 *spart = reinterpret_cast<const double2 *>(p.seg_part);
+            double2 *tax = reinterpret_cast<double2 *>(p.t_ax);
+            for (int q = ub * 32 + (int)threadIdx.x; q < ue * 32; q += BLOCK) {
+                const int f = q >> 5, ln = q & 31;
+                const int sl = rfull ? f : task_slice(R, P, m, f, 0);
+                const int seg = __ldg(P.sl_seg + (int64_t)sl * 32 + ln);
+                if (seg < 0) continue;
+                const int lr = __ldg(P.seg_key + seg);   // one super tile: key = local row
+                const double2 *pp = spart + ((int64_t)sl * TASK_SPLIT) * 32 + ln;
+                double t = 0.0, ax = 0.0;
+#pragma unroll
+                for (int part = 0; part < TASK_SPLIT; ++part) {
+                    const double2 a = pp[part * 32];
+                    t += a.x;
+                    ax += a.y;
+                }
+                tax[lr] = make_double2(t, ax);
+                wsum = fma(t, t, wsum);
+            }
+        } else {
         grid_sync(p.bar);
 
         // ---- phase 2b: rows = sum of their segments in tile order ----------
-        const int n_task_rows = R.pre[R.h->n_runs];
-        wsum = 0.0;
         {
             const double2 *spart = reinterpret_cast<const double2 *>(p.seg_part);
             double2 *tax = reinterpret_cast<double2 *>(p.t_ax);
@@ -1669,6 +1718,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 tax[lr] = make_double2(t, ax);
                 wsum = fma(t, t, wsum);
             }
+        }
         }
         TL_MARK(k, 4);
         bsum = block_sum_all(wsum, sh);

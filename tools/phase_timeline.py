@@ -87,6 +87,11 @@ def main():
         if k < 3 or k == nt - 1:
             print(f"{k:4d} " + " ".join(f"{v:6.1f}" for v in row) + f" {t[6].max() - start:7.1f}")
     print("mean " + " ".join(f"{v / nt:6.1f}" for v in tot))
+    d7 = (tl[:, 7, :] - tl[:, 0, :]).ravel()
+    d7 = d7[(d7 > 0) & (d7 < 1e4)]
+    if d7.size:
+        q = np.percentile(d7, [0, 50, 100])
+        print(f"p1 first band staged after (us): min {q[0]:.1f} med {q[1]:.1f} max {q[2]:.1f}")
     d1 = (tl[:, 1, :] - tl[:, 0, :]).ravel()
     d2 = (tl[:, 3, :] - tl[:, 2, :]).ravel()
     for name, d in (("p1 per block", d1), ("p2a per block", d2)):
