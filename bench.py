@@ -297,15 +297,22 @@ def run_ours(args):
             torch.distributed.barrier()
         else:
             run_gcsgd(system, y_h, warm_params, x_true=xt_h)
-    torch.cuda.synchronize(device)
-    e0.record(stream)
-    if sharded:
-        x_out, tr = D.run_gcsgd_sharded(system, y_h, e2e_params, x_true=xt_h)
-    else:
-        x_out, tr = run_gcsgd(system, y_h, e2e_params, x_true=xt_h)
-    e1.record(stream)
-    torch.cuda.synchronize(device)
-    e2e_ms = e0.elapsed_time(e1)
+    # three timed calls, the median reported (all three in the JSON): a
+    # single call of a few ms is exposed to one-off host hiccups
+    e2e_runs = []
+    for _ in range(3):
+        torch.cuda.synchronize(device)
+        if sharded:
+            torch.distributed.barrier()
+        e0.record(stream)
+        if sharded:
+            x_out, tr = D.run_gcsgd_sharded(system, y_h, e2e_params, x_true=xt_h)
+        else:
+            x_out, tr = run_gcsgd(system, y_h, e2e_params, x_true=xt_h)
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+        e2e_runs.append(e0.elapsed_time(e1))
+    e2e_ms = float(np.median(e2e_runs))
     if sharded:
         t = torch.tensor([e2e_ms], device=f"cuda:{device}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -358,6 +365,7 @@ def run_ours(args):
                     "unit": "block-updates/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "api": "run_gcsgd(system, y_host, params, x_true=host) -> x_host",
+                    "runs_ms": [round(v, 3) for v in e2e_runs], "reported": "median of 3 calls",
                     "final_snr_db": tr.rows[-1].snr_db if tr.rows else None},
             "gpu_launches": args.steps,
             "clocks": clk.summary(),

@@ -78,9 +78,7 @@ constexpr size_t SMEM_BUDGET = 218 * 1024;  // dynamic shared memory per CTA (on
 struct Slot {
     cudaEvent_t done = nullptr;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
-    EpochOut *h_out = nullptr;      // pinned
-    double *h_mus = nullptr;        // pinned [task_cap]
-    int32_t *h_status = nullptr;    // pinned [task_cap]
+    char *h_res = nullptr;          // pinned copy of the result block [out | mus | statuses]
     int64_t n_tasks = 0, n_visits = 0;
     bool pending = false;
     int32_t *h_plan = nullptr;      // pinned: device-sampled ids of the epoch
@@ -131,21 +129,24 @@ struct bct_ctx {
     double *guard_ref = nullptr;     // divergence guard reference norm (device)
     double guard_factor = 1e6;
     unsigned int *bar = nullptr, *ticket = nullptr;
-    char *d_prep = nullptr;          // [task_cap] per-task records (host_prep), pd.bytes() apart
-    char *h_prep = nullptr;          // pinned
+    // one upload per epoch: [EpochHeader | TaskDev x nt | masks | records]
+    // (UpLayout), staged in pinned memory; one download of the result block
+    // [EpochOut | mus x nt | statuses x nt]: each small copy costs the
+    // stream a few microseconds
+    char *d_up = nullptr, *h_up = nullptr;
+    size_t up_cap = 0;
+    char *d_res = nullptr;
+    uint64_t *cur_masks = nullptr;   // device masks / tasks of the last submitted epoch
+    TaskDev *cur_tasks = nullptr;
     PrepDims pd{};                   // record dimensions (finalize)
     int32_t prep_off = 0;            // byte offset of the record in dynamic shared memory
     int32_t sc_bound = 1;            // bound on super tiles per panel (record size at layout)
     int mw = 1;                      // 64-bit words per row-block set
-    uint64_t *d_masks = nullptr;     // [(1 + 2 task_cap) mw] epoch mask, task / visit masks
-    uint64_t *h_masks = nullptr;     // pinned
     unsigned long long *audit2 = nullptr;
-    EpochHeader *d_hdr = nullptr;
-    TaskDev *d_tasks = nullptr;
+
     int64_t task_cap = 0;
     // staging
-    EpochHeader *h_hdr = nullptr;
-    TaskDev *h_tasks = nullptr;
+
     cudaEvent_t staged = nullptr;
     Slot slots[RING];
     int head = 0, tail = 0;           // ring: tail = oldest pending
@@ -446,6 +447,8 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     return 0;
 }
 
+int ensure_task_cap(bct_ctx *c, int64_t n);
+
 // Common tail of context creation: offsets, row-block tables, inverse map, state.
 int finalize(bct_ctx *c)
 {
@@ -572,13 +575,10 @@ int finalize(bct_ctx *c)
     }
     c->grid = bct::epoch_grid_size(c->dtype, c->device, c->smem_total, &c->block);
     DALLOC(c->part, 8 * (int64_t)c->grid + 8);
-    DALLOC(c->out, 1);
     DALLOC(c->guard_ref, 1);
-    CK(cudaMemsetAsync(c->out, 0, sizeof(EpochOut), c->stream));
     DALLOC(c->bar, 1);
     DALLOC(c->ticket, 1);
     DALLOC(c->audit2, 2);
-    DALLOC(c->d_hdr, 1);
     CK(cudaMemsetAsync(c->y, 0, 8 * c->n_meas, c->stream));
     CK(cudaMemsetAsync(c->r, 0, 8 * (c->n_meas + 2), c->stream));
     CK(cudaMemsetAsync(c->z, 0, 8 * std::max<int64_t>(c->z_len, 1), c->stream));
@@ -587,17 +587,32 @@ int finalize(bct_ctx *c)
     CK(cudaMemsetAsync(c->counts, 0, 4 * std::max(c->np, 1), c->stream));
     CK(cudaMemsetAsync(c->bar, 0, 4, c->stream));
     CK(cudaMemsetAsync(c->ticket, 0, 4, c->stream));
-    CK(cudaHostAlloc((void **)&c->h_hdr, sizeof(EpochHeader), cudaHostAllocDefault));
     CK(cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming));
     for (int s = 0; s < RING; ++s) {
         CK(cudaEventCreateWithFlags(&c->slots[s].done, cudaEventDisableTiming));
         CK(cudaEventCreate(&c->slots[s].t0));
         CK(cudaEventCreate(&c->slots[s].t1));
-        CK(cudaHostAlloc((void **)&c->slots[s].h_out, sizeof(EpochOut), cudaHostAllocDefault));
     }
     CK(cudaStreamSynchronize(c->stream));
-    return 0;
+    return ensure_task_cap(c, 1);
 }
+
+// Byte layout of an epoch's upload block for nt tasks (16-byte aligned parts).
+struct UpLayout {
+    size_t tasks, masks, prep, total;
+};
+static size_t a16(size_t v) { return (v + 15) & ~(size_t)15; }
+static UpLayout up_layout(const bct_ctx *c, int64_t nt, bool with_prep)
+{
+    UpLayout L;
+    L.tasks = a16(sizeof(EpochHeader));
+    L.masks = a16(L.tasks + sizeof(TaskDev) * (size_t)nt);
+    L.prep = a16(L.masks + 8 * (size_t)c->mw * (1 + 2 * (size_t)nt));
+    L.total = L.prep + (with_prep ? (size_t)c->pd.bytes() * (size_t)nt : 0);
+    return L;
+}
+constexpr size_t RES_HEAD = 64;   // EpochOut at the start of the result block
+static_assert(sizeof(EpochOut) <= RES_HEAD, "result block head");
 
 int ensure_task_cap(bct_ctx *c, int64_t n)
 {
@@ -605,28 +620,27 @@ int ensure_task_cap(bct_ctx *c, int64_t n)
     int64_t cap = std::max<int64_t>(n, 2 * c->task_cap);
     // drain pending epochs before reallocating buffers they use
     CK(cudaStreamSynchronize(c->stream));
-    if (c->d_tasks) cudaFree(c->d_tasks);
-    if (c->mus) cudaFree(c->mus);
-    if (c->statuses) cudaFree(c->statuses);
-    if (c->h_tasks) cudaFreeHost(c->h_tasks);
-    if (c->d_prep) cudaFree(c->d_prep);
-    if (c->h_prep) cudaFreeHost(c->h_prep);
-    if (c->d_masks) cudaFree(c->d_masks);
-    if (c->h_masks) cudaFreeHost(c->h_masks);
-    CK(cudaMalloc((void **)&c->d_tasks, sizeof(TaskDev) * cap));
-    CK(cudaMalloc((void **)&c->d_prep, c->pd.bytes() * cap));
-    CK(cudaHostAlloc((void **)&c->h_prep, c->pd.bytes() * cap, cudaHostAllocDefault));
-    CK(cudaMalloc((void **)&c->d_masks, 8 * (size_t)c->mw * (1 + 2 * cap)));
-    CK(cudaHostAlloc((void **)&c->h_masks, 8 * (size_t)c->mw * (1 + 2 * cap),
-                     cudaHostAllocDefault));
-    CK(cudaMalloc((void **)&c->mus, 8 * cap));
-    CK(cudaMalloc((void **)&c->statuses, 4 * cap));
-    CK(cudaHostAlloc((void **)&c->h_tasks, sizeof(TaskDev) * cap, cudaHostAllocDefault));
+    const size_t up = up_layout(c, cap, true).total;
+    if (c->d_up) cudaFree(c->d_up);
+    if (c->h_up) cudaFreeHost(c->h_up);
+    CK(cudaMalloc((void **)&c->d_up, up));
+    CK(cudaHostAlloc((void **)&c->h_up, up, cudaHostAllocDefault));
+    c->up_cap = up;
+    // the result block; the last epoch's EpochOut carries over (the
+    // divergence guard of the next epoch reads it)
+    char *res = nullptr;
+    const size_t rb = RES_HEAD + 12 * (size_t)cap;
+    CK(cudaMalloc((void **)&res, rb));
+    CK(cudaMemset(res, 0, rb));
+    if (c->d_res) {
+        CK(cudaMemcpy(res, c->d_res, sizeof(EpochOut), cudaMemcpyDeviceToDevice));
+        cudaFree(c->d_res);
+    }
+    c->d_res = res;
+    c->out = reinterpret_cast<EpochOut *>(res);
     for (int s = 0; s < RING; ++s) {
-        if (c->slots[s].h_mus) cudaFreeHost(c->slots[s].h_mus);
-        if (c->slots[s].h_status) cudaFreeHost(c->slots[s].h_status);
-        CK(cudaHostAlloc((void **)&c->slots[s].h_mus, 8 * cap, cudaHostAllocDefault));
-        CK(cudaHostAlloc((void **)&c->slots[s].h_status, 4 * cap, cudaHostAllocDefault));
+        if (c->slots[s].h_res) cudaFreeHost(c->slots[s].h_res);
+        CK(cudaHostAlloc((void **)&c->slots[s].h_res, rb, cudaHostAllocDefault));
     }
     c->task_cap = cap;
     return 0;
@@ -652,26 +666,18 @@ void destroy(bct_ctx *c)
         if (c->h_pin[i]) cudaFreeHost(c->h_pin[i]);
         if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
     }
-    if (c->d_tasks) cudaFree(c->d_tasks);
-    if (c->mus) cudaFree(c->mus);
-    if (c->statuses) cudaFree(c->statuses);
+    if (c->d_res) cudaFree(c->d_res);
     if (c->timeline) cudaFree(c->timeline);
     for (double *q : {c->gx_batch, c->seg_batch, c->tax_batch, c->part_task})
         if (q) cudaFree(q);
-    if (c->h_tasks) cudaFreeHost(c->h_tasks);
-    if (c->d_prep) cudaFree(c->d_prep);
-    if (c->h_prep) cudaFreeHost(c->h_prep);
-    if (c->d_masks) cudaFree(c->d_masks);
-    if (c->h_masks) cudaFreeHost(c->h_masks);
-    if (c->h_hdr) cudaFreeHost(c->h_hdr);
+    if (c->d_up) cudaFree(c->d_up);
+    if (c->h_up) cudaFreeHost(c->h_up);
     for (int s = 0; s < RING; ++s) {
         Slot &S = c->slots[s];
         if (S.done) cudaEventDestroy(S.done);
         if (S.t0) cudaEventDestroy(S.t0);
         if (S.t1) cudaEventDestroy(S.t1);
-        if (S.h_out) cudaFreeHost(S.h_out);
-        if (S.h_mus) cudaFreeHost(S.h_mus);
-        if (S.h_status) cudaFreeHost(S.h_status);
+        if (S.h_res) cudaFreeHost(S.h_res);
     }
     if (c->staged) cudaEventDestroy(c->staged);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -1544,7 +1550,7 @@ int bct_audit(bct_ctx *c, double *drift)
 
 // ---- epochs ---------------------------------------------------------------
 
-static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
+static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, const UpLayout &L,
                          const std::function<int(Slot &)> &before_epoch = nullptr)
 {
     int s = c->head;
@@ -1555,16 +1561,12 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
         S.pending = false;
         c->tail = (c->tail + 1) % RING;
     }
-    CK(cudaMemcpyAsync(c->d_hdr, c->h_hdr, sizeof(EpochHeader), cudaMemcpyHostToDevice, c->stream));
-    if (n_tasks > 0)
-        CK(cudaMemcpyAsync(c->d_tasks, c->h_tasks, sizeof(TaskDev) * n_tasks,
-                           cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->d_masks, c->h_masks, 8 * (size_t)c->mw * (1 + 2 * n_tasks),
-                       cudaMemcpyHostToDevice, c->stream));
-    if (n_tasks > 0 && c->h_hdr->host_prep)
-        CK(cudaMemcpyAsync(c->d_prep, c->h_prep, c->pd.bytes() * n_tasks,
-                           cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_up, c->h_up, L.total, cudaMemcpyHostToDevice, c->stream));
     CK(cudaEventRecord(c->staged, c->stream));
+    c->cur_masks = reinterpret_cast<uint64_t *>(c->d_up + L.masks);
+    c->cur_tasks = reinterpret_cast<TaskDev *>(c->d_up + L.tasks);
+    c->mus = reinterpret_cast<double *>(c->d_res + RES_HEAD);
+    c->statuses = reinterpret_cast<int32_t *>(c->d_res + RES_HEAD + 8 * (size_t)n_tasks);
     S.plan_user = nullptr;
     S.n_plan = 0;
     if (before_epoch) {
@@ -1580,7 +1582,9 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
     p.rb_rows = c->d_rb_rows; p.rb_of_row = c->rb_of_row; p.y = c->y; p.r = c->r; p.r32 = c->r32; p.z = c->z;
     p.x = c->x; p.xhat = c->xhat; p.counts = c->counts;
     p.x_true = c->has_x_true ? c->x_true : nullptr;
-    p.hdr = c->d_hdr; p.tasks = c->d_tasks; p.gx = c->gx; p.gx_stride = 2 * c->max_cols;
+    p.hdr = reinterpret_cast<const EpochHeader *>(c->d_up);
+    p.tasks = reinterpret_cast<const TaskDev *>(c->d_up + L.tasks);
+    p.gx = c->gx; p.gx_stride = 2 * c->max_cols;
     p.t_ax = c->t_ax; p.seg_part = c->seg_part; p.part = c->part; p.mus = c->mus;
     p.band_cap = c->band_cap; p.band_dbuf = c->band_dbuf;
     p.gx_batch = c->gx_batch; p.seg_batch = c->seg_batch; p.tax_batch = c->tax_batch;
@@ -1588,8 +1592,8 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
     p.statuses = c->statuses; p.out = c->out;
     p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
     p.guard_ref = c->guard_ref;
-    p.prep = c->d_prep;
-    p.masks = c->d_masks;
+    p.prep = c->d_up + L.prep;
+    p.masks = c->cur_masks;
     p.mw = c->mw;
     p.prep_smem_off = c->prep_off;
     p.prep_dims = c->pd;
@@ -1607,12 +1611,8 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits,
     bct::launch_epoch(p, c->dtype, c->grid, c->block, c->smem_total, c->stream, &e);
     if (e != cudaSuccess) return fail(c, BCT_ECUDA, "epoch launch: %s", cudaGetErrorString(e));
     CK(cudaEventRecord(S.t1, c->stream));
-    CK(cudaMemcpyAsync(S.h_out, c->out, sizeof(EpochOut), cudaMemcpyDeviceToHost, c->stream));
-    if (n_tasks > 0) {
-        CK(cudaMemcpyAsync(S.h_mus, c->mus, 8 * n_tasks, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(S.h_status, c->statuses, 4 * n_tasks, cudaMemcpyDeviceToHost,
-                           c->stream));
-    }
+    CK(cudaMemcpyAsync(S.h_res, c->d_res, RES_HEAD + 12 * (size_t)n_tasks,
+                       cudaMemcpyDeviceToHost, c->stream));
     CK(cudaEventRecord(S.done, c->stream));
     S.n_tasks = n_tasks;
     S.n_visits = n_visits;
@@ -1823,38 +1823,42 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
         if ((r = grow(&c->tax_batch, &c->tax_batch_n, 2 * txo))) return r;
         if ((r = grow(&c->part_task, &c->part_task_n, 33 * nt * (int64_t)c->grid + nt))) return r;
     }
-    // the staging buffers of the previous epoch must have been consumed
+    // the staging block of the previous epoch must have been consumed
     CK(cudaEventSynchronize(c->staged));
-    memset(c->h_hdr, 0, sizeof(EpochHeader));
-    c->h_hdr->n_tasks = (int32_t)nt;
-    c->h_hdr->mode = mode;
-    c->h_hdr->flags = flags;
-    c->h_hdr->batched = batched ? 1 : 0;
-    c->h_hdr->n_tiles_total = (int32_t)tot_tiles;
-    c->h_hdr->n_slices_total = (int32_t)tot_slices;
-    c->h_hdr->n_rows_total = (int32_t)tot_rows;
-    c->h_hdr->n_vox_total = (int32_t)tot_vox;
-    c->h_hdr->n_ent_total = tot_ent;
-    c->h_hdr->guard_factor = c->guard_factor;
-    c->h_hdr->r32_valid = c->r32_valid ? 1 : 0;
+    const bool host_prep_on = !batched && host_masks && nt > 0;
+    const UpLayout L = up_layout(c, nt, host_prep_on);
+    EpochHeader *hh = reinterpret_cast<EpochHeader *>(c->h_up);
+    memset(hh, 0, sizeof(EpochHeader));
+    hh->n_tasks = (int32_t)nt;
+    hh->mode = mode;
+    hh->flags = flags;
+    hh->batched = batched ? 1 : 0;
+    hh->n_tiles_total = (int32_t)tot_tiles;
+    hh->n_slices_total = (int32_t)tot_slices;
+    hh->n_rows_total = (int32_t)tot_rows;
+    hh->n_vox_total = (int32_t)tot_vox;
+    hh->n_ent_total = tot_ent;
+    hh->guard_factor = c->guard_factor;
+    hh->r32_valid = c->r32_valid ? 1 : 0;
     // a batched FP32 epoch refreshes the copy before phase A
     if (batched && c->dtype == BCT_F32) c->r32_valid = true;
-    if (nt) memcpy(c->h_tasks, tasks.data(), sizeof(TaskDev) * nt);
+    if (nt) memcpy(c->h_up + L.tasks, tasks.data(), sizeof(TaskDev) * nt);
     // masks: the epoch's, then per task its group and its visit's union
-    std::copy(emask.begin(), emask.end(), c->h_masks);
+    uint64_t *hm = reinterpret_cast<uint64_t *>(c->h_up + L.masks);
+    std::copy(emask.begin(), emask.end(), hm);
     for (int64_t k = 0; k < nt; ++k) {
         std::copy(tmasks.begin() + (size_t)k * mw, tmasks.begin() + (size_t)(k + 1) * mw,
-                  c->h_masks + task_mask_off(k, mw));
+                  hm + task_mask_off(k, mw));
         std::copy(vmasks.begin() + (size_t)k * mw, vmasks.begin() + (size_t)(k + 1) * mw,
-                  c->h_masks + visit_mask_off(k, mw));
+                  hm + visit_mask_off(k, mw));
     }
     // per-task path with host-known masks: every task's set-up built here
-    c->h_hdr->host_prep = (!batched && host_masks && nt > 0) ? 1 : 0;
-    if (c->h_hdr->host_prep)
+    hh->host_prep = host_prep_on ? 1 : 0;
+    if (host_prep_on)
         for (int64_t k = 0; k < nt; ++k)
             host_prep(c, tasks[k], tmasks.data() + (size_t)k * mw, vmasks.data() + (size_t)k * mw,
-                      c->h_prep + c->pd.bytes() * k);
-    return launch_staged(c, nt, n_visits, hook);
+                      c->h_up + L.prep + c->pd.bytes() * k);
+    return launch_staged(c, nt, n_visits, L, hook);
 }
 
 int bct_set_divergence_factor(bct_ctx *c, double factor)
@@ -1873,17 +1877,18 @@ int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *status
     CK(cudaEventSynchronize(S.done));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(c, BCT_ECUDA, "epoch: %s", cudaGetErrorString(e));
+    const EpochOut *ho = reinterpret_cast<const EpochOut *>(S.h_res);
     o->n_tasks = S.n_tasks;
     o->n_visits = S.n_visits;
-    o->n_degenerate = S.h_out->n_degenerate;
-    o->resid_sq = S.h_out->resid_sq;
-    o->x_sq = S.h_out->x_sq;
-    o->err_sq = S.h_out->err_sq;
+    o->n_degenerate = ho->n_degenerate;
+    o->resid_sq = ho->resid_sq;
+    o->x_sq = ho->x_sq;
+    o->err_sq = ho->err_sq;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, S.t0, S.t1);
     o->kernel_ms = ms;
-    if (mus) memcpy(mus, S.h_mus, 8 * S.n_tasks);
-    if (statuses) memcpy(statuses, S.h_status, 4 * S.n_tasks);
+    if (mus) memcpy(mus, S.h_res + RES_HEAD, 8 * S.n_tasks);
+    if (statuses) memcpy(statuses, S.h_res + RES_HEAD + 8 * S.n_tasks, 4 * S.n_tasks);
     if (S.plan_user)
         for (int64_t q = 0; q < S.n_plan; ++q) S.plan_user[q] = S.h_plan[q];
     S.plan_user = nullptr;
@@ -1919,7 +1924,8 @@ int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
     if (!c) return BCT_EINVAL;
     DEVICE_GUARD(c);
     // the drawn blocks of the last epoch, as the device saw them (host plan or sampler)
-    const uint64_t *dmask = c->d_masks;   // epoch mask first (EpochParams::masks)
+    const uint64_t *dmask = c->cur_masks;   // epoch mask first (EpochParams::masks)
+    if (!dmask) return fail(c, BCT_EINVAL, "no sharded epoch submitted");
     const int nb = 296;
     // flags: the epoch's BCT_GUARD / BCT_GUARD_REF (a skipped epoch skips its finish)
     FinishGuard guard{&c->out->x_sq, c->guard_ref, c->guard_factor, (flags & BCT_GUARD) ? 1 : 0,
@@ -1931,7 +1937,7 @@ int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
     CK(bct::sharded_out(c->part, nb, c->exchange + c->n_meas, c->out, guard, c->stream));
     Slot &S = c->slots[(c->head + RING - 1) % RING];
     if (S.pending) {
-        CK(cudaMemcpyAsync(S.h_out, c->out, sizeof(EpochOut), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(S.h_res, c->out, sizeof(EpochOut), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaEventRecord(S.done, c->stream));
     }
     if (resid_sq) {   // synchronous form
@@ -2049,8 +2055,8 @@ int bct_sample_epoch(bct_ctx *c, int32_t mode, int32_t n_visits, const int32_t *
         sp.theta = theta;
         sp.group_size = group_size;
         sp.b = b;
-        sp.tasks = c->d_tasks;
-        sp.masks = c->d_masks;
+        sp.tasks = c->cur_tasks;   // this epoch's upload block (launch_staged)
+        sp.masks = c->cur_masks;
         sp.mw = c->mw;
         sp.plan_ids = c->d_plan;
         cudaError_t e;
