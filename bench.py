@@ -424,33 +424,68 @@ def cpu_sample(cfg_key, threads, budget_s=10.0, plans=None):
             "trace_s": trace_s, "run_once": run_once, "reps": reps}
 
 
+def cpu_model():
+    """The host CPU (the reference arm's hardware), from /proc/cpuinfo."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
+    """The reference's algorithm on the host cores, full epochs of the same
+    workload: oracle_run_gcsgd (the C restatement of _run_tasks / commits /
+    refresh under the numpy restatement of run_gcsgd, solvers.py:188-269)
+    in parallel mode with one visit per thread (executor.py:182-198), the
+    reference's FP64 values, refresh, _commit_epoch and per-epoch metrics
+    (projection_sum's np.add.at included, projector.py:767-777).  The panels
+    are traced with the reference tracer's C restatement (set-up, untimed)."""
     world, rank, _ = dist_env()
     if world > 1 and rank != 0:
         return None
-    from paper_1709_00953_b200 import CONFIGS
+    from oracle.oracle import OracleSystem, oracle_run_gcsgd
+    from paper_1709_00953_b200 import CONFIGS, add_noise, random_ellipses
     cfg = CONFIGS[args.config]
+    spec = cfg.spec
     cores = os.cpu_count() or 1
-    s = cpu_sample(args.config, cores, budget_s=1.0)
-    times = []
-    for _ in range(max(args.warmup, 0)):
-        s["run_once"]()
-    for _ in range(args.steps):
-        t = time.perf_counter()
-        s["run_once"]()
-        times.append(time.perf_counter() - t)
-    sec = float(np.mean(times)) if times else s["seconds"]
-    val = s["block_updates"] / sec
-    sample = (f"{s['tasks']} full-panel tasks of {cfg.name} epoch 1 (one per thread), "
-              f"f64 values, C restatement of _run_tasks")
+    t0 = time.perf_counter()
+    ora = OracleSystem.parallel_beam(spec.n, spec.views, spec.bins, spec.m, spec.nc)
+    x_true = random_ellipses(spec.n, cfg.n_ellipses, cfg.phantom_seed)
+    y, _ = add_noise(ora.forward(x_true), cfg.noise_frac, cfg.noise_seed)
+    setup_s = time.perf_counter() - t0
+    stamps = []
+    n_ep = max(args.warmup, 0) + args.steps
+    t_start = time.perf_counter()
+    oracle_run_gcsgd(ora, y, n_ep, cfg.b, alpha=cfg.alpha, gamma=cfg.gamma,
+                     group_size=cfg.group_size, mode=cfg.mode, seed=cfg.solver_seed,
+                     x_true=x_true, workers=cores,
+                     callback=lambda e, st, row: stamps.append(time.perf_counter()))
+    marks = [t_start] + stamps
+    times = np.diff(marks)[max(args.warmup, 0):]
+    sec = float(np.mean(times))
+    # blocks per epoch (sampling.py:140-152): ceil(gamma n) visits of
+    # min(s ceil(ceil(alpha m) / s), m) drawn blocks each
+    import math
+    draws = min(cfg.group_size * math.ceil(math.ceil(cfg.alpha * spec.m) / cfg.group_size),
+                spec.m)
+    visits = math.ceil(cfg.gamma * spec.nc)
+    blocks = draws * visits
+    val = blocks / sec
+    sample = (f"full epochs of {cfg.name} ({visits} visits x {draws} blocks), "
+              f"{cfg.mode} mode, {cores} threads, FP64, with refresh, commit and metrics")
     return {"metric": "block updates/s", "value": val, "unit": "block-updates/s",
             "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "sample": sample},
-            "nnz_per_s": s["nnz"] / sec,
-            "cpu_baseline": {"value": val, "unit": "block-updates/s", "cores": s["tasks"],
-                             "kind": "port", "sample": sample},
+            "config": {"workload": cfg.name, "sample": sample, "same_config": True,
+                       "setup_s": setup_s},
+            "nnz_per_s": ora.nnz / sec,
+            "cpu_baseline": {"value": val, "unit": "block-updates/s", "cores": cores,
+                             "kind": "port", "sample": sample, "cpu": cpu_model()},
             "e2e": {"value": val, "unit": "block-updates/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
@@ -480,7 +515,7 @@ def main():
                 "cores": s["tasks"], "kind": "port",
                 "sample": f"{s['tasks']} full-panel {cfg.name} tasks, one per thread, f64 "
                           f"(C restatement of _run_tasks), {s['seconds']:.3f} s per pass, "
-                          f"{s['reps']} passes"}
+                          f"{s['reps']} passes", "cpu": cpu_model()}
         print(json.dumps(out))
     import torch
     if torch.distributed.is_available() and torch.distributed.is_initialized():
