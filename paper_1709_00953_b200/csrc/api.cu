@@ -1874,6 +1874,13 @@ int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *status
     DEVICE_GUARD(c);
     Slot &S = c->slots[c->tail];
     if (!S.pending) return fail(c, BCT_EINVAL, "no pending epoch");
+    // poll (the epoch is usually a fraction of a millisecond away): a
+    // blocking wait parks the thread and pays the OS wake-up on every epoch
+    for (int spin = 0; spin < (1 << 22); ++spin) {
+        const cudaError_t q = cudaEventQuery(S.done);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) return fail(c, BCT_ECUDA, "epoch: %s", cudaGetErrorString(q));
+    }
     CK(cudaEventSynchronize(S.done));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(c, BCT_ECUDA, "epoch: %s", cudaGetErrorString(e));

@@ -58,7 +58,7 @@ def main():
     import pstats
     for rep in range(4):
         marks.clear()
-        prof = cProfile.Profile() if rep == 0 else None
+        prof = cProfile.Profile() if rep == 0 and os.environ.get("PROFILE") else None
         t0 = time.perf_counter()
         if prof:
             prof.enable()
