@@ -117,7 +117,7 @@ def _ncu_traffic(cfg_key):
     """dram__bytes_read.sum + dram__bytes_write.sum of the epoch kernel from the
     committed ncu --set full capture of this config (profiles/), else None."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                        f"r01_epoch_kernel_cfg{cfg_key}.json")
+                        f"r02_epoch_kernel_cfg{cfg_key}.json")
     try:
         with open(path) as fh:
             return float(json.load(fh)["traffic_bytes_per_launch"])
