@@ -52,7 +52,18 @@ namespace {
 #define BCT_NO_REPLAY_K 0   // 1: phase B streams the stored values even when replay records exist
 #endif
 constexpr int P1U = BCT_P1_UNROLL;
-constexpr int TASK_SPLIT = 4;       // per-task phase 2a: parts per SELL slice
+// per-task phase 2a: a SELL slice of nvec lane-vectors is split into
+// parts_of(nvec) work units (one per ~PART_VECS vectors, at most TS_MAX), so
+// a CTA's longest slice is not one warp's long latency chain; the partials of
+// a lane sit at spart[(slice * TS_MAX + part) * 32 + lane]
+constexpr int TS_MAX = 16;
+constexpr int PART_VECS = 4;
+constexpr int UCAP = 256;           // slices per prefix round (shared memory)
+constexpr int TS_PARTIAL = 4;       // partial tasks (a few short slices): fixed parts
+__host__ __device__ __forceinline__ int parts_of(int nvec, bool full)
+{
+    return full ? min(TS_MAX, max(1, (nvec + PART_VECS - 1) / PART_VECS)) : TS_PARTIAL;
+}
 constexpr int P2U = BCT_P2_UNROLL;
 constexpr int BLOCK = 1024;         // one CTA per SM
 constexpr int WARPS = BLOCK / 32;
@@ -1478,6 +1489,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     // the current task's record (PrepHdr + arrays) after the phase buffers
     PrepView R(reinterpret_cast<char *>(dyn_smem) + p.prep_smem_off, p.prep_dims);
     __shared__ int2 vr_s[8];
+    __shared__ int s_upre[UCAP + 1];   // per-task phase 2a unit prefix
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -1506,18 +1518,26 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     __shared__ RingSlot ring[RING];
     __shared__ int s_tpre[bct::MAX_BATCH_TASKS + 1], s_lp[bct::MAX_BATCH_TASKS];
     if (hdr.batched) batched_epoch<V>(p, hdr, rs, sh, ring, s_tpre, s_lp);
-    for (int k = 0; k < (hdr.batched ? 0 : n_tasks); ++k) {
-        __syncthreads();  // the previous task's record may still be in use
+    // a task's set-up record into shared memory: built on the host with the
+    // plan (api.cu host_prep, one copy) or by one thread (sampled epochs)
+    auto load_record = [&](int kk) {
         if (!hdr.host_prep) {
-            if (threadIdx.x == 0) prep_task(p, k, R);
+            if (threadIdx.x == 0) prep_task(p, kk, R);
         } else {
-            // built on the host with the plan (api.cu host_prep): one copy
             const int64_t rb = p.prep_dims.bytes();
-            const float4 *src = reinterpret_cast<const float4 *>(p.prep + rb * k);
+            const float4 *src = reinterpret_cast<const float4 *>(p.prep + rb * kk);
             float4 *dst = reinterpret_cast<float4 *>(R.h);
             for (int q = threadIdx.x; q < (int)(rb / 16); q += BLOCK) dst[q] = __ldcg(src + q);
         }
-        __syncthreads();
+    };
+    bool have_rec = false;   // loaded ahead, before the previous task's last barrier
+    for (int k = 0; k < (hdr.batched ? 0 : n_tasks); ++k) {
+        if (!have_rec) {
+            __syncthreads();  // the previous task's record may still be in use
+            load_record(k);
+            __syncthreads();
+        }
+        have_rec = false;
         const TaskDev &T = R.h->T;
         const PanelDev &P = R.h->P;
         const uint64_t *tmask = p.masks + task_mask_off(k, p.mw);
@@ -1634,34 +1654,93 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 const int ge = min(ue, R.st_pre[st + 1]);
                 const int v0 = __ldg(P.st_ptr + st), v1 = __ldg(P.st_ptr + st + 1);
                 stage_gx(gs, gx + v0, v1 - v0, P.swz_shift);
-                __syncthreads();
-                // work unit = (slice, part): part q of a slice takes its
-                // vectors kv = q (mod TASK_SPLIT), so a single task (a few
-                // slices per CTA) still keeps every warp streaming; the
-                // TASK_SPLIT partials of a lane are summed in phase 2b
-                for (int u = fu * TASK_SPLIT + warp; u < ge * TASK_SPLIT; u += WARPS) {
-                    const int f = u / TASK_SPLIT, part = u - f * TASK_SPLIT;
-                    const int sl = rfull ? f : task_slice(R, P, m, f, st);
-                    const int base = __ldg(P.slice_start + sl);
-                    const int nvec = (__ldg(P.slice_start + sl + 1) - base) >> 7;
-                    double t = 0.0, ax = 0.0;
+                // work unit = (slice, part): part q of a slice with np parts
+                // takes its vectors kv = q (mod np); the units of up to UCAP
+                // slices are numbered through a prefix of their part counts
+                // (partial tasks: TS_PARTIAL parts per slice, no prefix)
+                if (!rfull) {
+                    __syncthreads();
+                    for (int u = fu * TS_PARTIAL + warp; u < ge * TS_PARTIAL; u += WARPS) {
+                        const int f = u / TS_PARTIAL, part = u - f * TS_PARTIAL;
+                        const int sl = task_slice(R, P, m, f, st);
+                        const int base = __ldg(P.slice_start + sl);
+                        const int nvec = (__ldg(P.slice_start + sl + 1) - base) >> 7;
+                        double t = 0.0, ax = 0.0;
 #pragma unroll P2U
-                    for (int kv = part; kv < nvec; kv += TASK_SPLIT) {
-                        const int i = base + ((kv * 32 + lane) << 2);
-                        int cc[4];
-                        double v[4];
-                        ld4u16(P.fidx + i, cc);
-                        ld4v(fv + i, v);
+                        for (int kv = part; kv < nvec; kv += TS_PARTIAL) {
+                            const int i = base + ((kv * 32 + lane) << 2);
+                            int cc[4];
+                            double v[4];
+                            ld4u16(P.fidx + i, cc);
+                            ld4v(fv + i, v);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const GS a = gs[cc[q]];
-                            t = fma(v[q], (double)a.x, t);
-                            ax = fma(v[q], (double)a.y, ax);
+                            for (int q = 0; q < 4; ++q) {
+                                const GS a = gs[cc[q]];
+                                t = fma(v[q], (double)a.x, t);
+                                ax = fma(v[q], (double)a.y, ax);
+                            }
                         }
+                        spart[((int64_t)sl * TS_MAX + part) * 32 + lane] = make_double2(t, ax);
                     }
-                    spart[((int64_t)sl * TASK_SPLIT + part) * 32 + lane] = make_double2(t, ax);
+                    __syncthreads();
+                    fu = ge;
+                    continue;
                 }
-                __syncthreads();
+                for (int c0 = fu; c0 < ge; c0 += UCAP) {
+                    const int nc = min(ge - c0, UCAP);
+                    for (int i = threadIdx.x; i < nc; i += BLOCK) {
+                        const int sl = rfull ? c0 + i : task_slice(R, P, m, c0 + i, st);
+                        s_upre[i] = parts_of((__ldg(P.slice_start + sl + 1) -
+                                              __ldg(P.slice_start + sl)) >> 7, true);
+                    }
+                    __syncthreads();
+                    if (warp == 0) {   // exclusive prefix, 32 slices per step
+                        int carry = 0;
+                        for (int b0 = 0; b0 < nc; b0 += 32) {
+                            const int v = b0 + lane < nc ? s_upre[b0 + lane] : 0;
+                            int incl = v;
+#pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                                if (lane >= o) incl += y;
+                            }
+                            if (b0 + lane < nc) s_upre[b0 + lane] = carry + incl - v;
+                            carry += __shfl_sync(0xffffffffu, incl, 31);
+                        }
+                        if (lane == 0) s_upre[nc] = carry;
+                    }
+                    __syncthreads();
+                    const int total = s_upre[nc];
+                    for (int u = warp; u < total; u += WARPS) {
+                        int lo = 0, hi = nc - 1;   // last slice whose units start <= u
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if (s_upre[mid] <= u) lo = mid; else hi = mid - 1;
+                        }
+                        const int part = u - s_upre[lo], np = s_upre[lo + 1] - s_upre[lo];
+                        const int f = c0 + lo;
+                        const int sl = rfull ? f : task_slice(R, P, m, f, st);
+                        const int base = __ldg(P.slice_start + sl);
+                        const int nvec = (__ldg(P.slice_start + sl + 1) - base) >> 7;
+                        double t = 0.0, ax = 0.0;
+#pragma unroll P2U
+                        for (int kv = part; kv < nvec; kv += np) {
+                            const int i = base + ((kv * 32 + lane) << 2);
+                            int cc[4];
+                            double v[4];
+                            ld4u16(P.fidx + i, cc);
+                            ld4v(fv + i, v);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const GS a = gs[cc[q]];
+                                t = fma(v[q], (double)a.x, t);
+                                ax = fma(v[q], (double)a.y, ax);
+                            }
+                        }
+                        spart[((int64_t)sl * TS_MAX + part) * 32 + lane] = make_double2(t, ax);
+                    }
+                    __syncthreads();
+                }
                 fu = ge;
             }
         }
@@ -1671,7 +1750,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         if (fused) {
             // rows of this CTA's slices (written by this CTA above: the
             // __syncthreads that closed the loop orders them): t, ax = the
-            // lane's TASK_SPLIT parts in order; denominators per CTA
+            // lane's parts in order; denominators per CTA
             const double2 *spart = reinterpret_cast<const double2 *>(p.seg_part);
             double2 *tax = reinterpret_cast<double2 *>(p.t_ax);
             for (int q = ub * 32 + (int)threadIdx.x; q < ue * 32; q += BLOCK) {
@@ -1680,10 +1759,11 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 const int seg = __ldg(P.sl_seg + (int64_t)sl * 32 + ln);
                 if (seg < 0) continue;
                 const int lr = __ldg(P.seg_key + seg);   // one super tile: key = local row
-                const double2 *pp = spart + ((int64_t)sl * TASK_SPLIT) * 32 + ln;
+                const double2 *pp = spart + ((int64_t)sl * TS_MAX) * 32 + ln;
+                const int np = parts_of((__ldg(P.slice_start + sl + 1) -
+                                         __ldg(P.slice_start + sl)) >> 7, rfull);
                 double t = 0.0, ax = 0.0;
-#pragma unroll
-                for (int part = 0; part < TASK_SPLIT; ++part) {
+                for (int part = 0; part < np; ++part) {
                     const double2 a = pp[part * 32];
                     t += a.x;
                     ax += a.y;
@@ -1704,10 +1784,12 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 const int q1 = __ldg(P.rseg_ptr + lr + 1);
                 for (int q = __ldg(P.rseg_ptr + lr); q < q1; ++q) {
                     const int rp = __ldg(P.rpos + q);   // SELL position: slice*32 + lane
-                    const double2 *pp = spart + ((int64_t)(rp >> 5) * TASK_SPLIT) * 32 + (rp & 31);
+                    const int sq = rp >> 5;
+                    const double2 *pp = spart + ((int64_t)sq * TS_MAX) * 32 + (rp & 31);
+                    const int np = parts_of((__ldg(P.slice_start + sq + 1) -
+                                             __ldg(P.slice_start + sq)) >> 7, R.h->full != 0);
                     double st_ = 0.0, sa_ = 0.0;
-#pragma unroll
-                    for (int part = 0; part < TASK_SPLIT; ++part) {
+                    for (int part = 0; part < np; ++part) {
                         const double2 a = pp[part * 32];
                         st_ += a.x;
                         sa_ += a.y;
@@ -1795,7 +1877,15 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 p.r[g] = rv;
                 if (p.r32) p.r32[g] = (float)rv;
             }
-            if (k + 1 < n_tasks) grid_sync(p.bar);
+            if (k + 1 < n_tasks) {
+                // this task's record is no longer read: load the next task's
+                // while the other CTAs finish their refresh (it depends on
+                // the plan only, not on r)
+                __syncthreads();
+                load_record(k + 1);
+                have_rec = true;
+                grid_sync(p.bar);
+            }
         }
         TL_MARK(k, 6);
     }
