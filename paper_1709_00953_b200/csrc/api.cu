@@ -50,10 +50,8 @@ cudaError_t audit(const double *, const double *, const double *, int64_t, unsig
                   cudaStream_t);
 cudaError_t commit(const PanelDev *, int, int32_t *, double *, double *, cudaStream_t);
 cudaError_t sharded_finish(const double *, const double *, int64_t, const int32_t *,
-                           const uint64_t *, double *, float *, double *, int,
-                           const FinishGuard &, cudaStream_t);
-cudaError_t sharded_out(const double *, int, const double *, EpochOut *, const FinishGuard &,
-                        cudaStream_t);
+                           const uint64_t *, double *, float *, double *, int, const double *,
+                           EpochOut *, unsigned int *, const FinishGuard &, cudaStream_t);
 }  // namespace bct
 
 namespace {
@@ -138,6 +136,7 @@ struct bct_ctx {
     char *d_res = nullptr;
     uint64_t *cur_masks = nullptr;   // device masks / tasks of the last submitted epoch
     TaskDev *cur_tasks = nullptr;
+    int32_t cur_flags = 0;           // flags of the last submitted epoch
     PrepDims pd{};                   // record dimensions (finalize)
     int32_t prep_off = 0;            // byte offset of the record in dynamic shared memory
     int32_t sc_bound = 1;            // bound on super tiles per panel (record size at layout)
@@ -1611,8 +1610,11 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, const Up
     bct::launch_epoch(p, c->dtype, c->grid, c->block, c->smem_total, c->stream, &e);
     if (e != cudaSuccess) return fail(c, BCT_ECUDA, "epoch launch: %s", cudaGetErrorString(e));
     CK(cudaEventRecord(S.t1, c->stream));
-    CK(cudaMemcpyAsync(S.h_res, c->d_res, RES_HEAD + 12 * (size_t)n_tasks,
-                       cudaMemcpyDeviceToHost, c->stream));
+    // a sharded epoch's result is copied by bct_finish_sharded (after the
+    // all-reduce); every other epoch's here
+    if (!(c->cur_flags & BCT_SHARDED))
+        CK(cudaMemcpyAsync(S.h_res, c->d_res, RES_HEAD + 12 * (size_t)n_tasks,
+                           cudaMemcpyDeviceToHost, c->stream));
     CK(cudaEventRecord(S.done, c->stream));
     S.n_tasks = n_tasks;
     S.n_visits = n_visits;
@@ -1832,6 +1834,7 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
     hh->n_tasks = (int32_t)nt;
     hh->mode = mode;
     hh->flags = flags;
+    c->cur_flags = flags;
     hh->batched = batched ? 1 : 0;
     hh->n_tiles_total = (int32_t)tot_tiles;
     hh->n_slices_total = (int32_t)tot_slices;
@@ -1938,13 +1941,14 @@ int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
     FinishGuard guard{&c->out->x_sq, c->guard_ref, c->guard_factor, (flags & BCT_GUARD) ? 1 : 0,
                       (flags & BCT_GUARD_REF) ? 1 : 0};
     CK(bct::sharded_finish(c->y, c->exchange, c->n_meas, c->rb_of_row, dmask, c->r, c->r32,
-                           c->part, nb, guard, c->stream));
-    // the epoch's result (slot of the last submitted epoch) now carries the
-    // global norms; bct_wait_epoch returns them
-    CK(bct::sharded_out(c->part, nb, c->exchange + c->n_meas, c->out, guard, c->stream));
+                           c->part, nb, c->exchange + c->n_meas, c->out, c->ticket, guard,
+                           c->stream));
+    // the epoch's result block (slot of the last submitted epoch) now carries
+    // the global norms; one copy (the epoch launch skipped its own when sharded)
     Slot &S = c->slots[(c->head + RING - 1) % RING];
     if (S.pending) {
-        CK(cudaMemcpyAsync(S.h_res, c->out, sizeof(EpochOut), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(S.h_res, c->d_res, RES_HEAD + 12 * (size_t)S.n_tasks,
+                           cudaMemcpyDeviceToHost, c->stream));
         CK(cudaEventRecord(S.done, c->stream));
     }
     if (resid_sq) {   // synchronous form

@@ -662,12 +662,18 @@ __global__ void commit_kernel(const PanelDev *panels, int np, int32_t *counts, d
 }
 
 // Sharded tail: r = y - S for rows of drawn blocks; residual norm partials.
+// One launch: r = y - S on the drawn rows (+ r32), |y - S|^2 partials per
+// block, and the last block to finish (ticket) writes the epoch's global
+// result: |y - S|^2 (block order, like the host sum it replaces), |x|^2 and
+// |x_t - x|^2 from the all-reduced exchange tail.
 __global__ void sharded_finish_kernel(const double *y, const double *S, int64_t n,
                                       const int32_t *rb_of_row, const uint64_t *mask, double *r,
-                                      float *r32, double *part, FinishGuard guard)
+                                      float *r32, double *part, const double *tail,
+                                      EpochOut *out, unsigned int *ticket, FinishGuard guard)
 {
-    if (guard_tripped(guard)) return;   // the epoch was skipped: r stays
+    if (guard_tripped(guard)) return;   // the epoch was skipped: r and the result stay
     __shared__ double sh[32];
+    __shared__ bool is_last;
     double acc = 0.0;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
          g += (int64_t)gridDim.x * blockDim.x) {
@@ -686,23 +692,19 @@ __global__ void sharded_finish_kernel(const double *y, const double *S, int64_t 
         double s = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
         part[blockIdx.x] = s;
+        __threadfence();
+        is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
-}
-
-// Sharded epoch result on the device: |y - S|^2 from the finish partials (block
-// order, like the host sum it replaces), |x|^2 and |x_t - x|^2 from the
-// all-reduced exchange tail.
-__global__ void sharded_out_kernel(const double *part, int nb, const double *tail, EpochOut *out,
-                                   FinishGuard guard)
-{
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (guard_tripped(guard)) return;   // keep the diverged epoch's result
+    __syncthreads();
+    if (!is_last || threadIdx.x != 0) return;
+    __threadfence();
     double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += part[b];
+    for (unsigned b = 0; b < gridDim.x; ++b) s += ((volatile double *)part)[b];
     out->resid_sq = s;
     out->x_sq = tail[0];
     out->err_sq = tail[1];
     if (guard.set_ref) *guard.ref = fmax(sqrt(tail[0]), 1e-12);
+    *ticket = 0;
 }
 
 inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
@@ -933,16 +935,11 @@ cudaError_t commit(const PanelDev *panels, int np, int32_t *counts, double *x, d
 
 cudaError_t sharded_finish(const double *y, const double *S, int64_t n, const int32_t *rb_of_row,
                            const uint64_t *mask, double *r, float *r32, double *part, int nb,
+                           const double *tail, EpochOut *out, unsigned int *ticket,
                            const FinishGuard &guard, cudaStream_t s)
 {
-    sharded_finish_kernel<<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, r, r32, part, guard);
-    return cudaGetLastError();
-}
-
-cudaError_t sharded_out(const double *part, int nb, const double *tail, EpochOut *out,
-                        const FinishGuard &guard, cudaStream_t s)
-{
-    sharded_out_kernel<<<1, 32, 0, s>>>(part, nb, tail, out, guard);
+    sharded_finish_kernel<<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, r, r32, part, tail, out,
+                                             ticket, guard);
     return cudaGetLastError();
 }
 
