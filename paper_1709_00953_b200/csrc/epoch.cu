@@ -21,9 +21,13 @@
 //   D  mu, status per task; xhat += x_new per visit; z = ax + mu t
 //   tail: r = y - sum_j z^j on the drawn rows (ascending j, interleaved
 //      inverse map), commit, norms
-// FP32 mode computes the streamed inner products (phase A lane sums, phase B
-// segment partials) in FP32; every reduction across lanes, warps, segments
-// and tasks, and all state, is FP64.  FP64 mode is FP64 throughout.
+// FP32 mode computes the streamed inner products in FP32: phase A's lane sums
+// over an FP32 copy of r, phase B's segment partials over (g, x) staged as
+// float2, and the batched path stores segment partials and row (t, ax) as
+// FP32 pairs (so z = ax + mu t and the denominator use FP32-rounded t, ax).
+// Every sum across lanes, warps, segments and tasks, mu, x, xhat, z, r and the
+// norms are FP64.  FP64 mode is FP64 throughout.  (Measured cost against the
+// FP64 reference: tests/test_parity_configs.py.)
 // Per-task path (serial_faithful and partial groups): the same phase-1 and
 // phase-2 code per task, three grid barriers per task, and in serial mode the
 // refresh of the visit's drawn rows after its last task (executor.py:215-223).

@@ -126,7 +126,8 @@ def cfg1_system_f32():
 
 @pytest.mark.parametrize("name", list(VARIANTS))
 def test_fp32_residual_curve_matches_reference(cfg1_system_f32, cfg1_runs, name):
-    """FP32 value storage (f64 arithmetic): the residual-versus-iteration
+    """FP32 value storage (FP32 streamed inner products over FP32-staged
+    (g, x), FP64 reductions and state; csrc/epoch.cu header): the residual-versus-iteration
     curve of the reference (f64) run within 1e-4 relative (north_star), with
     the identical selection stream."""
     g = cfg1_runs
