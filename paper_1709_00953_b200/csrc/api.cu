@@ -65,6 +65,7 @@ constexpr int RING = 4;
 inline int st_voxels(int dtype)
 {
     if (getenv("BCT_ST_SMALL") || getenv("BCT_REPLAY")) return 4096;
+    if (dtype == 1 && getenv("BCT_F32_ACC64")) return 8192;   // measurement variant (epoch.cu)
     // FP64 configs run per-task (small) epochs: a strip panel of up to 8192
     // voxels is one super tile, so its rows are single segments (epoch.cu
     // phase 2a then finishes rows without a grid barrier)
@@ -442,7 +443,8 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     c->max_seg = std::max<int64_t>(c->max_seg, (int64_t)P.n_slices * 32);   // partial slots
     c->band_cap = std::max(c->band_cap, (P.band_max + 3) & ~3);   // 16-byte aligned FP32 buffers
     // staged super tile: (g, x) as float2 in FP32 mode, double2 in FP64 mode (swizzled)
-    c->smem = std::max<size_t>(c->smem, (size_t)((P.st_max + 15) & ~15) * (c->dtype == 0 ? 16 : 8));
+    c->smem = std::max<size_t>(c->smem, (size_t)((P.st_max + 15) & ~15) *
+                                            (c->dtype == 0 || getenv("BCT_F32_ACC64") ? 16 : 8));
     return 0;
 }
 

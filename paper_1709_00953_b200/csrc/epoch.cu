@@ -40,6 +40,16 @@
 
 namespace {
 
+// Measurement variant: FP32 values with FP64 inner
+// products -- FP64 bands and (g, x) staging, FP64 lane and segment partials
+// (build with -DBCT_F32_ACC64=1 and run with BCT_F32_ACC64=1 set, which gives
+// FP32 contexts 8192-voxel super tiles so the double2 staging fits)
+#ifndef BCT_F32_ACC64
+#define BCT_F32_ACC64 0
+#endif
+// narrow (FP32) streamed arithmetic for value type V
+template <typename V>
+__host__ __device__ constexpr bool narrow_math() { return sizeof(V) == 4 && !BCT_F32_ACC64; }
 #ifndef BCT_EXP
 #define BCT_EXP 0   // profiling variants (5: no band copies, 6: no phase-1 stream, 7: no gathers)
 #endif
@@ -477,7 +487,7 @@ __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv,
                                                  int nvec, int lane, int wst, const GS *gs,
                                                  int hdr)
 {
-    using A = V;
+    using A = typename std::conditional<narrow_math<V>(), float, double>::type;
     const int sy = (hdr >> 16) & 1 ? -1 : 1;
     const int shift = P.swz_shift;
     int q = hdr & 0xffff;
@@ -501,8 +511,8 @@ __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv,
                 const int code = (word[j >> 2] >> (8 * (j & 3) + 2 * e)) & 3;
                 q += ((code & 1) ? sy : 0) + (code >> 1) * wst;
                 const GS a = gs[swz_idx(q, shift)];
-                t = fma(v[j][e], (A)a.x, t);
-                ax = fma(v[j][e], (A)a.y, ax);
+                t = fma((A)v[j][e], (A)a.x, t);
+                ax = fma((A)v[j][e], (A)a.y, ax);
             }
     }
 #if BCT_FC_TAIL_GROUP
@@ -533,8 +543,8 @@ __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv,
                 const int code = (word[j >> 2] >> (8 * (j & 3) + 2 * e)) & 3;
                 q += ((code & 1) ? sy : 0) + (code >> 1) * wst;
                 const GS a = gs[swz_idx(q, shift)];
-                t = fma(v[j][e], (A)a.x, t);
-                ax = fma(v[j][e], (A)a.y, ax);
+                t = fma((A)v[j][e], (A)a.x, t);
+                ax = fma((A)v[j][e], (A)a.y, ax);
             }
         }
     }
@@ -549,8 +559,8 @@ __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv,
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const GS a = gs[cc[e]];
-            t = fma(v[e], (A)a.x, t);
-            ax = fma(v[e], (A)a.y, ax);
+            t = fma((A)v[e], (A)a.x, t);
+            ax = fma((A)v[e], (A)a.y, ax);
         }
     }
 #endif
@@ -1045,7 +1055,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     double2 *gxb = reinterpret_cast<double2 *>(p.gx_batch);
     // segment partials and row (t, ax) pairs: FP32 in FP32 mode (the lane
     // partials are FP32 sums already), FP64 in FP64 mode
-    using PT = typename std::conditional<sizeof(V) == 4, float2, double2>::type;
+    using PT = typename std::conditional<narrow_math<V>(), float2, double2>::type;
     PT *segb = reinterpret_cast<PT *>(p.seg_batch);
     PT *taxb = reinterpret_cast<PT *>(p.tax_batch);
     double *pgg = p.part_task;                       // [k][G][WARPS]
@@ -1058,9 +1068,9 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     // double-buffered by tile parity.  gg partials per (task, CTA, warp).
     // FP32 mode: the bands are staged from an FP32 copy of the epoch-start r
     // (half the staging bytes and single-wavefront gathers)
-    using TB = typename std::conditional<sizeof(V) == 4, float, double>::type;
+    using TB = typename std::conditional<narrow_math<V>(), float, double>::type;
     const TB *rband;
-    if constexpr (sizeof(V) == 4) {
+    if constexpr (narrow_math<V>()) {
         if (!hdr.r32_valid) {   // r was written outside an epoch since the last copy
             for (int64_t i = (int64_t)b * BLOCK + threadIdx.x; i < p.n_meas; i += (int64_t)G * BLOCK)
                 p.r32[i] = (float)p.r[i];
@@ -1158,7 +1168,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
 
     // ---- phase B: segment partials of every task (contiguous slice ranges) --
     {
-        using GS = typename std::conditional<sizeof(V) == 4, float2, double2>::type;
+        using GS = typename std::conditional<narrow_math<V>(), float2, double2>::type;
         GS *gs = reinterpret_cast<GS *>(rs);
         // this CTA: the slices whose first entry lies in an equal share of the
         // epoch's stored entries (slices differ in length)
@@ -1285,7 +1295,9 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                     const double2 cp = coded_segment<V, GS>(P, fv, sl, base, nvec, lane, wst, gs, hdr);
                     if (dst >= 0) spart[dst] = PT{(decltype(PT::x))cp.x, (decltype(PT::x))cp.y};
                 } else {
-                    V t = V(0), ax = V(0);   // FP32 mode: FP32 lane partials (see coded_segment)
+                    // FP32 mode: FP32 lane partials (see coded_segment)
+                    using A = typename std::conditional<narrow_math<V>(), float, double>::type;
+                    A t = A(0), ax = A(0);
 #pragma unroll P2U
                     for (int kv = 0; kv < nvec; ++kv) {
                         const int i = base + ((kv * 32 + lane) << 2);
@@ -1296,8 +1308,8 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             const GS a = gs[cc[q]];
-                            t = fma(v[q], (V)a.x, t);
-                            ax = fma(v[q], (V)a.y, ax);
+                            t = fma((A)v[q], (A)a.x, t);
+                            ax = fma((A)v[q], (A)a.y, ax);
                         }
                     }
                     if (dst >= 0) spart[dst] = PT{(decltype(PT::x))t, (decltype(PT::x))ax};
@@ -1516,7 +1528,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     double *part_m = p.part + 2 * gridDim.x;
     double *rs = reinterpret_cast<double *>(dyn_smem);   // phase 1 band
     // phase 2 super tile: (g, x) pairs, float2 when values are float (FP32 mode)
-    using GS = typename std::conditional<sizeof(V) == 4, float2, double2>::type;
+    using GS = typename std::conditional<narrow_math<V>(), float2, double2>::type;
     GS *gs = reinterpret_cast<GS *>(dyn_smem);
 
     __shared__ RingSlot ring[RING];
