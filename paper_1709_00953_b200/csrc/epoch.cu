@@ -139,19 +139,32 @@ __device__ __forceinline__ bool mask_has(const uint64_t *mask, int i)
     return (mask[i >> 6] >> (i & 63)) & 1ull;
 }
 
-// Sum of part[0..n) in a fixed order, identical in every block.
-__device__ double fixed_sum(const double *part, int n, double *sh)
+// Sums of pa[0..n) and pb[0..n) in a fixed order, identical in every block.
+__device__ void fixed_sum2(const double *pa, const double *pb, int n, double *sh, double &a,
+                           double &b)
 {
-    double v = 0.0;
-    for (int k = threadIdx.x; k < n; k += BLOCK) v += part[k];
-    v = warp_sum(v);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __shared__ double sh2[WARPS];
+    double va = 0.0, vb = 0.0;
+    for (int k = threadIdx.x; k < n; k += BLOCK) {
+        va += pa[k];
+        vb += pb[k];
+    }
+    va = warp_sum(va);
+    vb = warp_sum(vb);
+    if ((threadIdx.x & 31) == 0) {
+        sh[threadIdx.x >> 5] = va;
+        sh2[threadIdx.x >> 5] = vb;
+    }
     __syncthreads();
-    double s = 0.0;
+    double sa = 0.0, sb = 0.0;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) s += sh[w];
+    for (int w = 0; w < WARPS; ++w) {
+        sa += sh[w];
+        sb += sh2[w];
+    }
     __syncthreads();
-    return s;
+    a = sa;
+    b = sb;
 }
 
 // Per-block sum of a per-thread value, fixed order.
@@ -1621,10 +1634,15 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             }
         }
         TL_MARK(k, 1);
+        // gg is first needed for mu, after the next barrier: reduced there,
+        // together with the denominators (one read of the partials off the
+        // critical path here).  Partials alternate between two buffers by
+        // task: without a barrier between tasks (parallel mode) a fast CTA
+        // writes the next task's while a slow one may still read these.
+        double *pgg = part_gg + ((k & 1) ? 5 * gridDim.x : 0);
         double bsum = block_sum_all(wsum, sh);
-        if (threadIdx.x == 0) part_gg[blockIdx.x] = bsum;
+        if (threadIdx.x == 0) pgg[blockIdx.x] = bsum;
         grid_sync(p.bar);
-        const double gg = fixed_sum(part_gg, gridDim.x, sh);
         TL_MARK(k, 2);
 
         // ---- phase 2a: segment partials of t = A_I g, ax = A_I x_J -------
@@ -1822,7 +1840,8 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         bsum = block_sum_all(wsum, sh);
         if (threadIdx.x == 0) part_den[blockIdx.x] = bsum;
         grid_sync(p.bar);
-        const double denom = fixed_sum(part_den, gridDim.x, sh);
+        double gg, denom;
+        fixed_sum2(pgg, part_den, gridDim.x, sh, gg, denom);
         TL_MARK(k, 5);
 
         // ---- phase 3: step, x accumulation, z store, serial refresh -----
