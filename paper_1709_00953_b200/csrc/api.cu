@@ -29,11 +29,6 @@ cudaError_t exclusive_scan_i32(const int32_t *, int32_t *, int64_t, void *, size
 cudaError_t pb_fill(int64_t, int64_t, int64_t, const double *, const double *, int64_t, int64_t,
                     const int32_t *, const int32_t *, int64_t, double *, int32_t *, cudaStream_t);
 cudaError_t pb_rbp(const int32_t *, int64_t, const int64_t *, int, int32_t *, cudaStream_t);
-cudaError_t pb_replay(int64_t, int64_t, const double *, const double *, int64_t, int64_t,
-                      const int32_t *, const int32_t *, int64_t, const int32_t *, const int32_t *,
-                      const int32_t *, const int32_t *, double *, double *, double *, int2 *,
-                      cudaStream_t);
-unsigned long long pb_replay_check(int, const PanelDev &, int64_t, int64_t, cudaStream_t);
 cudaError_t inv_count(const int32_t *, int32_t, int32_t *, cudaStream_t);
 cudaError_t invt_len(const int32_t *, int64_t, int32_t *, cudaStream_t);
 cudaError_t invt_fill(const int32_t *, const int32_t *, int64_t, const int32_t *, int32_t *,
@@ -60,11 +55,10 @@ constexpr int RING = 4;
 // voxels per super tile: its (g, x) pairs are staged in shared memory for
 // phase 2 -- 16384 x 8 B (float2, 128 KB) in FP32 mode: fewer (row, super
 // tile) segments per row for the batched epochs; 8192 x 16 B (128 KB) in
-// FP64 mode (the matrix-free phase B needs segments that are whole walk
-// runs: <= 255 entries, so it keeps 4096-voxel super tiles)
+// FP64 mode
 inline int st_voxels(int dtype)
 {
-    if (getenv("BCT_ST_SMALL") || getenv("BCT_REPLAY")) return 4096;
+    if (getenv("BCT_ST_SMALL")) return 4096;
     if (dtype == 1 && getenv("BCT_F32_ACC64")) return 8192;   // measurement variant (epoch.cu)
     // FP64 configs run per-task (small) epochs: a strip panel of up to 8192
     // voxels is one super tile, so its rows are single segments (epoch.cu
@@ -313,17 +307,9 @@ Placement place_voxels(int64_t n_cols, int64_t h, int64_t w, int th, int tw, int
 
 // Lays out panel lp from its compact forward CSR on the device
 // (vals64/cols/indptr temporaries; l2g persistent), rbp on the host.
-// Parallel-beam geometry of a strip panel (enables the matrix-free phase B).
-struct ReplayGeom {
-    int64_t n, bins;
-    const double *cosv, *sinv;
-    int64_t x0, x1;
-};
-
 int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *vals64,
                 const int32_t *cols, const int32_t *indptr, int32_t *l2g,
-                const std::vector<int32_t> &rbp, int64_t h, int64_t w,
-                const ReplayGeom *geo = nullptr)
+                const std::vector<int32_t> &rbp, int64_t h, int64_t w)
 {
     PanelDev &P = c->h_panels[lp];
     const int j = c->pb + lp;
@@ -352,11 +338,6 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     c->sc_bound = std::max<int32_t>(c->sc_bound, (int32_t)((4ll * n_cols) / st_voxels(c->dtype) + 2));
     const size_t budget = smem_budget(c, c->sc_bound);
     Placement pl;
-    // matrix-free phase B is opt-in (BCT_REPLAY=1): regenerating the values
-    // costs more FP64 issue than streaming them saves
-    const bool replay = geo != nullptr && getenv("BCT_REPLAY") && nnz > 0;
-    int32_t *seg_of = nullptr;
-    if (replay) DALLOC(seg_of, nnz);
     for (size_t si = 0; si < shapes.size(); ++si) {
         const int th = shapes[si].th, tw = shapes[si].tw;
         pl = place_voxels(n_cols, h, w, th, tw, c->dtype);
@@ -364,16 +345,13 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
         std::vector<void *> kept;
         PanelDev Q = P;
         Q.swz_shift = pl.swz_shift;
-        // replayed segments must be contiguous runs of the ray's walk: whole
-        // (row, super tile) runs, so no cap inside a strip (a run is at most
-        // strip height + super tile width entries; K is stored in 8 bits)
-        // (step-coded phase B: no cap at all, so no run is cut and every
-        // segment codes; the replay records store K in 8 bits)
-        Q.seg_cap = pl.st_w > 0 ? (replay ? 255 : 1 << 20) : 0;
+        // strip panels: no cap on a (row, super tile) run, so no run is cut
+        // and every segment step-codes (phase B); generic panels cap at 64
+        Q.seg_cap = pl.st_w > 0 ? 1 << 20 : 0;
         Q.st_h = pl.st_w > 0 ? (int32_t)h : 0;   // strip placement: step-coded phase B
         if (bct::layout_panel_v2(c->dtype, c->m, n_rows, n_cols, nnz, vals64, cols, indptr, l2g,
                                  d_rbp, pl.c2d, pl.st_ptr, pl.corder, th * tw, Q, kept, err,
-                                 c->stream, seg_of))
+                                 c->stream))
             return fail(c, BCT_ENOMEM, "panel %d layout: %s", j, err.c_str());
         if ((size_t)shapes[si].nbuf * Q.band_max * 8 + bct::PHASE1_RED_BYTES <= budget ||
             si + 1 == shapes.size()) {
@@ -392,39 +370,6 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
         return fail(c, BCT_EINVAL, "panel %d: %d super tiles exceed the record bound %d", j,
                     P.n_st, c->sc_bound);
     CK(cudaMemcpy(d_d2c, pl.d2c.data(), 4 * n_cols, cudaMemcpyHostToDevice));
-    if (replay && pl.st_w > 0) {
-        // walk states of the forward segments: phase B regenerates the values
-        const int64_t slots = std::max<int64_t>((int64_t)P.n_slices * 32, 1);
-        double *rt = nullptr, *r0 = nullptr, *r1 = nullptr;
-        int2 *rm = nullptr;
-        DALLOC(rt, slots);
-        DALLOC(r0, slots);
-        DALLOC(r1, slots);
-        DALLOC(rm, slots);
-        CK(cudaMemsetAsync(rm, 0, sizeof(int2) * slots, c->stream));
-        CK(bct::pb_replay(geo->n, geo->bins, geo->cosv, geo->sinv, geo->x0, geo->x1, l2g, indptr,
-                          n_rows, seg_of, P.seg_slice, P.seg_lane, P.seg_len, rt, r0, r1, rm,
-                          c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        P.rp_t = rt;
-        P.rp_tm0 = r0;
-        P.rp_tm1 = r1;
-        P.rp_meta = rm;
-        P.pb_cos = geo->cosv;
-        P.pb_sin = geo->sinv;
-        P.pb_n = geo->n;
-        P.pb_bins = geo->bins;
-        P.pb_x0 = (int32_t)geo->x0;
-        P.pb_x1 = (int32_t)geo->x1;
-        P.st_w = pl.st_w;
-        if (getenv("BCT_CHECK_REPLAY")) {
-            P.l2g = l2g;
-            fprintf(stderr, "panel %d: replay check, %llu mismatching segments of %lld\n", j,
-                    bct::pb_replay_check(c->dtype, P, geo->x0, geo->x1, c->stream),
-                    (long long)P.n_seg);
-        }
-    }
-    if (seg_of) free_tmp(c, seg_of);
     P.rbp = d_rbp;
     P.l2g = l2g;
     P.d2c = d_d2c;
@@ -923,9 +868,8 @@ int bct_create_parallel_beam(const bct_pb_desc *d, bct_ctx **out)
         std::vector<int32_t> rb(c->m + 1);
         CK(cudaMemcpyAsync(rb.data(), rbp_tmp, 4 * (c->m + 1), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        ReplayGeom geo{n, bins, d_cos, d_sin, xedge[j], xedge[j + 1]};
         if ((r = build_panel(c, lp, (int32_t)rows[lp], nnzs[lp], vals64, cols, p_ip[lp], p_l2g[lp],
-                             rb, xedge[j + 1] - xedge[j], n, &geo)))
+                             rb, xedge[j + 1] - xedge[j], n)))
             return bail(r);
         free_tmp(c, p_ip[lp]);
     }

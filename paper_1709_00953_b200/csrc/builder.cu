@@ -316,135 +316,6 @@ __global__ void gather_i32_kernel(const int32_t *src, const int32_t *idx, int64_
     if (q < n) dst[q] = src[idx[q]];
 }
 
-// Replay records of the forward segments (matrix-free phase B, epoch.cu): the
-// traversal state at the first entry (in walk order) of every (row, super
-// tile) segment -- t, tmax[0..1], the voxel -- so the epoch kernel re-walks
-// the ray for the segment's K entries and regenerates the exact intersection
-// lengths instead of streaming stored values and indices.  A segment is a
-// contiguous run of the walk (a lexicographic column range of one straight
-// ray inside one strip), so one state per segment suffices.  The entry ->
-// segment map is the layout's (seg_of_entry, CSR order); CSR slots follow
-// pb_fill_kernel's placement.
-__global__ void pb_replay_kernel(int64_t n, int64_t bins, const double *cosv, const double *sinv,
-                                 int64_t x0, int64_t x1, const int32_t *l2g, const int32_t *indptr,
-                                 int64_t n_hit, const int32_t *seg_of_entry,
-                                 const int32_t *seg_slice, const int32_t *seg_lane,
-                                 const int32_t *seg_len, double *rp_t, double *rp_tm0,
-                                 double *rp_tm1, int2 *rp_meta)
-{
-    int64_t lr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (lr >= n_hit) return;
-    double src[3], dst[3], dv[3];
-    int64_t r = l2g[lr], a = r / bins, k = r % bins;
-    pb_endpoints(n, bins, cosv[a], sinv[a], k, src, dst);
-    double origin[3] = {-0.5 * (double)n, -0.5 * (double)n, -0.5};
-    int64_t lo[3] = {x0, 0, 0}, hi[3] = {x1, n, 1};
-    int colcnt[MAX_STRIP];
-    const int w = (int)(x1 - x0);
-    for (int q = 0; q < w; ++q) colcnt[q] = 0;
-    RayTrace T;
-    if (!trace_init(src, dst, origin, lo, hi, T, dv)) return;
-    RayTrace T2 = T;
-    trace_walk(T, [&](int64_t ix, int64_t, double) { ++colcnt[ix - x0]; });
-    int acc = 0;
-    for (int q = 0; q < w; ++q) {
-        int c = colcnt[q];
-        colcnt[q] = acc;
-        acc += c;
-    }
-    const bool ydown = T2.step[1] < 0;
-    const int base = indptr[lr];
-    int64_t cur_ix = -1;
-    int run_pos = 0, run_len = 0, cur_seg = -1;
-    trace_walk(T2, [&](int64_t ix, int64_t iy, double) {
-        if (ix != cur_ix) {
-            cur_ix = ix;
-            run_pos = 0;
-            int q = (int)(ix - x0);
-            int next = (q + 1 < w) ? colcnt[q + 1] : acc;
-            run_len = next - colcnt[q];
-        }
-        int q = (int)(ix - x0);
-        int slot = colcnt[q] + (ydown ? (run_len - 1 - run_pos) : run_pos);
-        ++run_pos;
-        const int sgi = seg_of_entry[base + slot];
-        if (sgi != cur_seg) {   // first entry of a segment in walk order: record the state
-            cur_seg = sgi;
-            const int64_t at = (int64_t)seg_slice[sgi] * 32 + seg_lane[sgi];
-            rp_t[at] = T2.t;
-            rp_tm0[at] = T2.tmax[0];
-            rp_tm1[at] = T2.tmax[1];
-            rp_meta[at] = make_int2((int32_t)lr, (int32_t)(((uint32_t)(ix - x0) << 24) |
-                                                           ((uint32_t)seg_len[sgi] << 16) |
-                                                           (uint32_t)iy));
-        }
-    });
-}
-
-// Set-up check (BCT_CHECK_REPLAY=1): replay every recorded segment with the
-// tracer's own walk and compare with the stored forward entries of its slot
-// (same value multiset in the same voxels): counts mismatching slots.
-template <typename V>
-__global__ void pb_replay_check_kernel(int64_t n, int64_t bins, const double *cosv,
-                                       const double *sinv, int64_t x0, int64_t x1,
-                                       const int32_t *l2g, const double *rp_t, const double *rp_tm0,
-                                       const double *rp_tm1, const int2 *rp_meta,
-                                       const int32_t *slice_start, const V *fvals,
-                                       const uint16_t *fidx, int64_t n_slots, int32_t st_w,
-                                       int swz_shift, const int32_t *stbs_unused,
-                                       unsigned long long *bad)
-{
-    int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (slot >= n_slots) return;
-    const int2 meta = rp_meta[slot];
-    const int K = (meta.y >> 16) & 0xff;
-    if (K == 0) return;
-    const int64_t sl = slot / 32, lane = slot % 32;
-    double src[3], dst[3], dv[3];
-    int64_t r = l2g[meta.x], a = r / bins, k = r % bins;
-    pb_endpoints(n, bins, cosv[a], sinv[a], k, src, dst);
-    double origin[3] = {-0.5 * (double)n, -0.5 * (double)n, -0.5};
-    int64_t lo[3] = {x0, 0, 0}, hi[3] = {x1, n, 1};
-    RayTrace T;
-    if (!trace_init(src, dst, origin, lo, hi, T, dv)) { atomicAdd(bad, 1ull); return; }
-    T.t = rp_t[slot];
-    T.tmax[0] = rp_tm0[slot];
-    T.tmax[1] = rp_tm1[slot];
-    T.iv[0] = x0 + ((unsigned)meta.y >> 24);
-    T.iv[1] = meta.y & 0xffff;
-    // stored entries of this lane: value sum and voxel-index sum as a signature
-    const int base = slice_start[sl];
-    double vs = 0.0;
-    long long is = 0;
-    for (int e = 0; e < K; ++e) {
-        int64_t pos = base + ((int64_t)(e >> 2) * 32 + lane) * 4 + (e & 3);
-        vs += (double)fvals[pos];
-        is += fidx[pos];
-    }
-    double rvs = 0.0;
-    long long ris = 0;
-    int got = 0;
-    const int64_t stv = (int64_t)st_w;
-    for (int it = 0; it < 4 * K + 8 && got < K; ++it) {
-        int ax = 0;
-        double tm = T.tmax[0];
-        if (T.tmax[1] < tm) { ax = 1; tm = T.tmax[1]; }
-        double tn = tm < T.t1 ? tm : T.t1;
-        double seg = (tn - T.t) * T.length;
-        if (seg > 0.0) {
-            ++got;
-            rvs += (double)(V)seg;
-            int64_t y0 = (T.iv[1] / stv) * stv;
-            int64_t wid = min(stv, n - y0);
-            ris += swz_idx((int)((T.iv[0] - x0) * wid + (T.iv[1] - y0)), swz_shift);
-        }
-        if (tm >= T.t1) break;
-        T.iv[ax] += T.step[ax];
-        T.tmax[ax] += T.tdel[ax];
-        T.t = tn;
-    }
-    if (got != K || ris != is || fabs(rvs - vs) > 1e-9 * fabs(vs)) atomicAdd(bad, 1ull);
-}
 
 __global__ void flag_hits_kernel(const int32_t *counts, int64_t n, int32_t *flags)
 {
@@ -802,45 +673,6 @@ cudaError_t gather_i32(const int32_t *src, const int32_t *idx, int64_t n, int32_
     return cudaGetLastError();
 }
 
-cudaError_t pb_replay(int64_t n, int64_t bins, const double *d_cos, const double *d_sin,
-                      int64_t x0, int64_t x1, const int32_t *d_l2g, const int32_t *d_indptr,
-                      int64_t n_hit, const int32_t *seg_of_entry, const int32_t *seg_slice,
-                      const int32_t *seg_lane, const int32_t *seg_len, double *rp_t,
-                      double *rp_tm0, double *rp_tm1, int2 *rp_meta, cudaStream_t s)
-{
-    if (x1 - x0 > MAX_STRIP) return cudaErrorInvalidValue;
-    if (n_hit == 0) return cudaSuccess;
-    pb_replay_kernel<<<nblk(n_hit, 64), 64, 0, s>>>(n, bins, d_cos, d_sin, x0, x1, d_l2g,
-                                                    d_indptr, n_hit, seg_of_entry, seg_slice,
-                                                    seg_lane, seg_len, rp_t, rp_tm0, rp_tm1,
-                                                    rp_meta);
-    return cudaGetLastError();
-}
-
-unsigned long long pb_replay_check(int dtype, const PanelDev &P, int64_t x0, int64_t x1,
-                                   cudaStream_t s)
-{
-    unsigned long long *d = nullptr, h = ~0ull;
-    if (cudaMalloc(&d, 8) != cudaSuccess) return h;
-    cudaMemsetAsync(d, 0, 8, s);
-    const int64_t slots = (int64_t)P.n_slices * 32;
-    if (slots > 0) {
-        if (dtype == 0)
-            pb_replay_check_kernel<double><<<nblk(slots, 128), 128, 0, s>>>(
-                P.pb_n, P.pb_bins, P.pb_cos, P.pb_sin, x0, x1, P.l2g, P.rp_t, P.rp_tm0, P.rp_tm1,
-                P.rp_meta, P.slice_start, (const double *)P.fvals, P.fidx, slots, P.st_w,
-                P.swz_shift, P.stbs, d);
-        else
-            pb_replay_check_kernel<float><<<nblk(slots, 128), 128, 0, s>>>(
-                P.pb_n, P.pb_bins, P.pb_cos, P.pb_sin, x0, x1, P.l2g, P.rp_t, P.rp_tm0, P.rp_tm1,
-                P.rp_meta, P.slice_start, (const float *)P.fvals, P.fidx, slots, P.st_w,
-                P.swz_shift, P.stbs, d);
-    }
-    cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    cudaFree(d);
-    return h;
-}
 
 cudaError_t pb_rbp(const int32_t *d_l2g, int64_t n_hit, const int64_t *d_edges, int m,
                    int32_t *d_rbp, cudaStream_t s)

@@ -62,9 +62,6 @@ __host__ __device__ constexpr bool narrow_math() { return sizeof(V) == 4 && !BCT
 #ifndef BCT_FENCED_BARRIER
 #define BCT_FENCED_BARRIER 0
 #endif
-#ifndef BCT_NO_REPLAY_K
-#define BCT_NO_REPLAY_K 0   // 1: phase B streams the stored values even when replay records exist
-#endif
 constexpr int P1U = BCT_P1_UNROLL;
 // per-task phase 2a: a SELL slice of nvec lane-vectors is split into
 // parts_of(nvec) work units (one per ~PART_VECS vectors, at most TS_MAX), so
@@ -934,100 +931,6 @@ __device__ __forceinline__ int lower_bound_warp(At at, int n, K key)
     }
 }
 
-// ---- matrix-free phase B (parallel-beam strips) ----------------------------
-// The forward store's values are the reference tracer's segment lengths
-// (projector.py:51-198, builder.cu).  Instead of streaming them (value + index,
-// 6-10 B per entry) phase B re-walks each segment's ray from a 32-byte state
-// recorded at set-up (pb_replay_kernel) and regenerates the same doubles: the
-// ray constants and every step use the tracer's operations in the tracer's
-// order with explicit round-to-nearest intrinsics (no contraction), so the
-// values are bit-identical to the stored ones (FP32 mode rounds them to float
-// exactly as the store did).
-struct RayC {
-    double len, t1, tdel0, tdel1;
-    int step0, step1;
-};
-
-__device__ __forceinline__ RayC ray_consts(const PanelDev &P, int64_t g)
-{
-    const int64_t a = g / P.pb_bins, k = g - a * P.pb_bins;
-    const double c = __ldg(P.pb_cos + a), s = __ldg(P.pb_sin + a);
-    const double n = (double)P.pb_n;
-    // pb_endpoints
-    const double u = __dsub_rn((double)k, __ddiv_rn((double)(P.pb_bins - 1), 2.0));
-    const double L = __dmul_rn(4.0, n);
-    const double cx = __dmul_rn(u, -s), cy = __dmul_rn(u, c);
-    const double lc = __dmul_rn(L, c), ls = __dmul_rn(L, s);
-    const double s0 = __dsub_rn(cx, lc), s1 = __dsub_rn(cy, ls);
-    const double dv0 = __dsub_rn(__dadd_rn(cx, lc), s0);
-    const double dv1 = __dsub_rn(__dadd_rn(cy, ls), s1);
-    // trace_init: length, clip to the strip, steps
-    RayC R;
-    R.len = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dv0, dv0), __dmul_rn(dv1, dv1)), 0.0));
-    const double scale = fmax(fabs(dv0), fabs(dv1));
-    const double eps_d = __dmul_rn(1e-12, scale);
-    const double origin = __dmul_rn(-0.5, n);
-    double t1 = 1.0;
-    R.tdel0 = R.tdel1 = INFINITY;
-    R.step0 = R.step1 = 0;
-    if (fabs(dv0) > eps_d) {
-        double ta = __ddiv_rn(__dsub_rn(__dadd_rn(origin, (double)P.pb_x0), s0), dv0);
-        double tb = __ddiv_rn(__dsub_rn(__dadd_rn(origin, (double)P.pb_x1), s0), dv0);
-        if (ta > tb) tb = ta;
-        if (tb < t1) t1 = tb;
-        R.step0 = dv0 > 0.0 ? 1 : -1;
-        R.tdel0 = __ddiv_rn(1.0, fabs(dv0));
-    }
-    if (fabs(dv1) > eps_d) {
-        double ta = __ddiv_rn(__dsub_rn(__dadd_rn(origin, 0.0), s1), dv1);
-        double tb = __ddiv_rn(__dsub_rn(__dadd_rn(origin, n), s1), dv1);
-        if (ta > tb) tb = ta;
-        if (tb < t1) t1 = tb;
-        R.step1 = dv1 > 0.0 ? 1 : -1;
-        R.tdel1 = __ddiv_rn(1.0, fabs(dv1));
-    }
-    R.t1 = t1;
-    return R;
-}
-
-// (t, ax) partial of the forward segment in SELL slot `slot` of panel P,
-// gathered from the staged super tile gs (voxel columns y0.., rows of `wid`).
-template <typename V, typename GS>
-__device__ __forceinline__ double2 replay_segment(const PanelDev &P, int64_t slot, const GS *gs,
-                                                  int y0, int wid)
-{
-    const int2 meta = __ldg(P.rp_meta + slot);
-    const int K = (meta.y >> 16) & 0xff;
-    double t_acc = 0.0, ax = 0.0;
-    if (K == 0) return make_double2(0.0, 0.0);
-    const RayC R = ray_consts(P, __ldg(P.l2g + meta.x));
-    double t = __ldg(P.rp_t + slot), tm0 = __ldg(P.rp_tm0 + slot), tm1 = __ldg(P.rp_tm1 + slot);
-    int ix = (int)((unsigned)meta.y >> 24), iy = meta.y & 0xffff;   // ix relative to the strip
-    for (int done = 0, steps = 0; done < K && steps < 4 * K + 8; ++steps) {
-        const bool a1 = tm1 < tm0;
-        const double tm = a1 ? tm1 : tm0;
-        const double tn = tm < R.t1 ? tm : R.t1;
-        const double seg = __dmul_rn(__dsub_rn(tn, t), R.len);
-        if (seg > 0.0) {
-            const double v = (double)(V)seg;
-            const GS gv = gs[swz_idx(ix * wid + (iy - y0), P.swz_shift)];
-            t_acc = fma(v, (double)gv.x, t_acc);
-            ax = fma(v, (double)gv.y, ax);
-            ++done;
-        }
-        if (tm >= R.t1) break;   // the ray left the strip (never before K entries)
-        if (a1) {
-            iy += R.step1;
-            tm1 = __dadd_rn(tm1, R.tdel1);
-        } else {
-            ix += R.step0;
-            tm0 = __dadd_rn(tm0, R.tdel0);
-        }
-        t = tn;
-    }
-    return make_double2(t_acc, ax);
-}
-
 __device__ __forceinline__ int task_of(const TaskDev *tasks, int n_tasks, int which, int f)
 {
     // last task whose prefix (field `which`) is <= f
@@ -1243,9 +1146,6 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             if (p.timeline) dbg_stage += gtimer() - tst0;   // profiling: super-tile staging
             const V *fv = static_cast<const V *>(P.fvals);
             PT *spart = segb + T.seg_off;
-            const bool replay = P.rp_meta != nullptr && !BCT_NO_REPLAY_K;
-            const int y0 = st * P.st_w;
-            const int wid = P.pb_x1 > P.pb_x0 ? (v1 - v0) / (P.pb_x1 - P.pb_x0) : 1;
             const int wst = P.st_h > 0 ? (v1 - v0) / P.st_h : 1;   // step-coded row length
             // slices are taken one at a time from a shared counter: their
             // lengths vary (up to seg_cap/4 vectors), so a static round robin
@@ -1299,10 +1199,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
 #endif
                 }
                 const int nvec = (bend - base) >> 7;
-                if (replay) {
-                    const double2 rp = replay_segment<V, GS>(P, (int64_t)sl * 32 + lane, gs, y0, wid);
-                    if (dst >= 0) spart[dst] = PT{(decltype(PT::x))rp.x, (decltype(PT::x))rp.y};
-                } else if (coded && !__any_sync(0xffffffffu, (hdr >> 17) & 1)) {
+                if (coded && !__any_sync(0xffffffffu, (hdr >> 17) & 1)) {
                     // step-coded slice (a lane flagged in fq0 bit 17 keeps its
                     // 16-bit indices: the indexed loop below)
                     const double2 cp = coded_segment<V, GS>(P, fv, sl, base, nvec, lane, wst, gs, hdr);

@@ -67,14 +67,6 @@ struct PanelDev {
     int32_t tile_cols;         // columns per phase-1 tile (multiple of 32)
     int32_t n_cslices;
     int32_t swz_shift;         // phase-2 super tile swizzle (see swz_idx)
-    // matrix-free phase B (parallel-beam strips): per SELL slot the walk state at
-    // the segment's first entry (builder.cu pb_replay_kernel); null: stored values
-    const double *rp_t, *rp_tm0, *rp_tm1;
-    const int2 *rp_meta;       // (local row, ix-x0 << 24 | K << 16 | iy)
-    const double *pb_cos, *pb_sin;
-    int64_t pb_n, pb_bins;
-    int32_t pb_x0, pb_x1;      // strip rows [x0, x1)
-    int32_t st_w;              // super tile row length (voxels per strip row)
     int32_t seg_cap;           // set-up input: max entries per forward segment (0: 64)
     // step-coded voxel indices of the forward store (strip panels; phase B):
     // a segment's entries are stored in walk order, so each entry is its
@@ -348,5 +340,5 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
                     const int32_t *l2g, const int32_t *rbp, const std::vector<int32_t> &c2d_h,
                     const std::vector<int32_t> &st_ptr_h, const std::vector<int32_t> &corder_h,
                     int tile_cols, PanelDev &P, std::vector<void *> &keep, std::string &err,
-                    cudaStream_t s, int32_t *seg_of_entry = nullptr);
+                    cudaStream_t s);
 }

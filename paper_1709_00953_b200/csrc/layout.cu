@@ -341,13 +341,6 @@ __global__ void rkey_k(const int32_t *seg_key, int32_t n_seg, int32_t n_rows, in
     rkey[s] = (seg_key[s] % n_rows) * n_st + seg_key[s] / n_rows;
 }
 
-__global__ void seg_of_entry_k(const int32_t *perm, const int32_t *incl, int64_t nnz,
-                               int32_t *out)
-{
-    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (q < nnz) out[perm[q]] = incl[q] - 1;
-}
-
 __global__ void rq_k(const int32_t *rpos, int32_t n_seg, int32_t *rq)
 {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -844,7 +837,7 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
                     const int32_t *l2g, const int32_t *rbp, const std::vector<int32_t> &c2d_h,
                     const std::vector<int32_t> &st_ptr_h, const std::vector<int32_t> &corder_h,
                     int tile_cols, PanelDev &P, std::vector<void *> &keep, std::string &err,
-                    cudaStream_t s, int32_t *seg_of_entry)
+                    cudaStream_t s)
 {
     std::vector<void *> tmp;
     Alloc K{&keep, &err}, T{&tmp, &err};
@@ -901,8 +894,6 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
     int32_t n_slices = 0;
     if (n_seg > 0) {
         seg_first_k<<<nb(nnz, 256), 256, 0, s>>>(flag, incl, skey, nnz, seg_first, seg_key);
-        if (seg_of_entry)   // CSR entry -> its forward segment (replay records, builder.cu)
-            seg_of_entry_k<<<nb(nnz, 256), 256, 0, s>>>(perm, incl, nnz, seg_of_entry);
         seg_len_k<<<nb(n_seg, 256), 256, 0, s>>>(seg_first, n_seg, nnz, seg_len, nvec);
         sell_key_k<<<nb(n_seg, 256), 256, 0, s>>>(seg_key, nvec, n_seg, n_rows, rbp, m, skey0);
         iota_k<<<nb(n_seg, 256), 256, 0, s>>>(sid0, n_seg);
