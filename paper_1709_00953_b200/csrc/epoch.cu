@@ -50,6 +50,19 @@ namespace {
 // narrow (FP32) streamed arithmetic for value type V
 template <typename V>
 __host__ __device__ constexpr bool narrow_math() { return sizeof(V) == 4 && !BCT_F32_ACC64; }
+// Checked build (-DBCT_CHECK=1, tools/checked_build.sh): bounds of every
+// gather and scattered store of the epoch kernel, trapping on a violation
+// (compute-sanitizer is not available on the GPU pool).
+#ifndef BCT_CHECK
+#define BCT_CHECK 0
+#endif
+#define BCT_ASSERT(cond)                                                              \
+    do {                                                                              \
+        if (BCT_CHECK && !(cond)) {                                                   \
+            printf("bct check failed %s:%d: %s\n", __FILE__, __LINE__, #cond);       \
+            __trap();                                                                 \
+        }                                                                             \
+    } while (0)
 #ifndef BCT_EXP
 #define BCT_EXP 0   // profiling variants (5: no band copies, 6: no phase-1 stream, 7: no gathers)
 #endif
@@ -520,6 +533,7 @@ __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv,
             for (int e = 0; e < 4; ++e) {
                 const int code = (word[j >> 2] >> (8 * (j & 3) + 2 * e)) & 3;
                 q += ((code & 1) ? sy : 0) + (code >> 1) * wst;
+                BCT_ASSERT(q >= 0 && swz_idx(q, shift) < P.st_max);
                 const GS a = gs[swz_idx(q, shift)];
                 t = fma((A)v[j][e], (A)a.x, t);
                 ax = fma((A)v[j][e], (A)a.y, ax);
@@ -552,6 +566,7 @@ __device__ __forceinline__ double2 coded_segment(const PanelDev &P, const V *fv,
             for (int e = 0; e < 4; ++e) {
                 const int code = (word[j >> 2] >> (8 * (j & 3) + 2 * e)) & 3;
                 q += ((code & 1) ? sy : 0) + (code >> 1) * wst;
+                BCT_ASSERT(q >= 0 && swz_idx(q, shift) < P.st_max);
                 const GS a = gs[swz_idx(q, shift)];
                 t = fma((A)v[j][e], (A)a.x, t);
                 ax = fma((A)v[j][e], (A)a.y, ax);
@@ -773,6 +788,12 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
                         const float vf[8] = {a[r][0].x, a[r][0].y, a[r][0].z, a[r][0].w,
                                              a[r][1].x, a[r][1].y, a[r][1].z, a[r][1].w};
                         const uint32_t bb = bts + 4u * (uint32_t)b0[r];
+                        BCT_ASSERT(b0[r] >= 0 &&
+                                   b0[r] + (int)max(max(max(o[r].x & 0xff, (o[r].x >> 8) & 0xff),
+                                                        max((o[r].x >> 16) & 0xff, o[r].x >> 24)),
+                                                    max(max(o[r].y & 0xff, (o[r].y >> 8) & 0xff),
+                                                        max((o[r].y >> 16) & 0xff, o[r].y >> 24))) <
+                                   ((P.band_max + 3) & ~3));
 #pragma unroll
                         for (int e = 0; e < 4; ++e)
                             acc32 = fmaf(vf[e], lds_f32(bb + 4u * ((o[r].x >> (8 * e)) & 0xff)), acc32);
@@ -806,8 +827,10 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
                 double v[8];
                 ld8v(tv + i, v);
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
+                for (int e = 0; e < 4; ++e) {
+                    BCT_ASSERT(b0 + ((o.x >> (8 * e)) & 0xff) < ((P.band_max + 3) & ~3));
                     acc = fma(v[e], lds_band<TB>(bts, b0 + ((o.x >> (8 * e)) & 0xff)), acc);
+                }
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
                     acc = fma(v[4 + e], lds_band<TB>(bts, b0 + ((o.y >> (8 * e)) & 0xff)), acc);
@@ -823,8 +846,10 @@ __device__ __forceinline__ double tile_g(const PanelDev &P, int t, int sl0, int 
                 ld8u16(tloc + i, loc);
                 ld8v(tv + i, v);
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
+                for (int e = 0; e < 8; ++e) {
+                    BCT_ASSERT(loc[e] < ((P.band_max + 3) & ~3));
                     acc = fma(v[e], BCT_EXP == 7 ? (double)loc[e] : lds_band<TB>(bts, loc[e]), acc);
+                }
             }
         }
         red[sub * (ns * 32) + si * 32 + lane] = acc;
@@ -1203,6 +1228,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                     // step-coded slice (a lane flagged in fq0 bit 17 keeps its
                     // 16-bit indices: the indexed loop below)
                     const double2 cp = coded_segment<V, GS>(P, fv, sl, base, nvec, lane, wst, gs, hdr);
+                    BCT_ASSERT(dst < P.n_slices * 32);
                     if (dst >= 0) spart[dst] = PT{(decltype(PT::x))cp.x, (decltype(PT::x))cp.y};
                 } else {
                     // FP32 mode: FP32 lane partials (see coded_segment)
@@ -1217,6 +1243,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                         ld4raw(fv + i, v);
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
+                            BCT_ASSERT(cc[q] < P.st_max);
                             const GS a = gs[cc[q]];
                             t = fma((A)v[q], (A)a.x, t);
                             ax = fma((A)v[q], (A)a.y, ax);
@@ -1606,7 +1633,8 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                             ld4v(fv + i, v);
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                const GS a = gs[cc[q]];
+                                BCT_ASSERT(cc[q] < P.st_max);
+                            const GS a = gs[cc[q]];
                                 t = fma(v[q], (double)a.x, t);
                                 ax = fma(v[q], (double)a.y, ax);
                             }
@@ -1663,7 +1691,8 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                             ld4v(fv + i, v);
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                const GS a = gs[cc[q]];
+                                BCT_ASSERT(cc[q] < P.st_max);
+                            const GS a = gs[cc[q]];
                                 t = fma(v[q], (double)a.x, t);
                                 ax = fma(v[q], (double)a.y, ax);
                             }
@@ -1699,6 +1728,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                     t += a.x;
                     ax += a.y;
                 }
+                BCT_ASSERT(lr >= 0 && lr < P.n_rows);
                 tax[lr] = make_double2(t, ax);
                 wsum = fma(t, t, wsum);
             }
@@ -1728,6 +1758,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                     t += st_;
                     ax += sa_;
                 }
+                BCT_ASSERT(lr >= 0 && lr < P.n_rows);
                 tax[lr] = make_double2(t, ax);
                 wsum = fma(t, t, wsum);
             }
@@ -1795,6 +1826,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 double acc = 0.0;
                 for (int e = p.inv_ptr[g]; e < p.inv_ptr[g + 1]; ++e) {
                     const int off = p.inv_z[e];
+                    BCT_ASSERT(off >= 0 && off < p.z_len);
                     double v;
                     if (cur && off >= zlo && off < zhi) {
                         const double2 qq = tax[off - zlo];
