@@ -115,6 +115,13 @@ struct bct_ctx {
     // epoch-batched parallel path scratch (grow-only)
     double *gx_batch = nullptr, *seg_batch = nullptr, *tax_batch = nullptr, *part_task = nullptr;
     int64_t gx_batch_n = 0, seg_batch_n = 0, tax_batch_n = 0, part_task_n = 0;
+    // z in (t, ax) form after fused batched epochs (epoch.cu; EpochParams::zt):
+    // per-row pairs (allocated at the first such epoch) and per-panel form;
+    // z_lazy: some panel may be in that form (materialize_z before z is used)
+    void *zt = nullptr;
+    int32_t *zl_on = nullptr, *zl_st = nullptr;
+    double *zl_mu = nullptr;
+    bool z_lazy = false;
     std::vector<std::vector<int32_t>> h_stbs;  // per panel (n_st*(m+1)) first slice table
     double *mus = nullptr, *exchange = nullptr, *vec = nullptr;
     int32_t *statuses = nullptr;
@@ -490,6 +497,10 @@ int finalize(bct_ctx *c)
     DALLOC(c->vec, c->n_meas + 2);
     DALLOC(c->exchange, c->n_meas + 2);
     DALLOC(c->z, c->z_len);
+    DALLOC(c->zl_on, std::max(c->np, 1));
+    DALLOC(c->zl_st, std::max(c->np, 1));
+    DALLOC(c->zl_mu, std::max(c->np, 1));
+    CK(cudaMemsetAsync(c->zl_on, 0, 4 * std::max(c->np, 1), c->stream));
     DALLOC(c->x, c->x_len);
     DALLOC(c->xhat, c->x_len);
     DALLOC(c->x_true, c->x_len);
@@ -616,6 +627,7 @@ void destroy(bct_ctx *c)
     if (c->timeline) cudaFree(c->timeline);
     for (double *q : {c->gx_batch, c->seg_batch, c->tax_batch, c->part_task})
         if (q) cudaFree(q);
+    if (c->zt) cudaFree(c->zt);
     if (c->d_up) cudaFree(c->d_up);
     if (c->h_up) cudaFreeHost(c->h_up);
     for (int s = 0; s < RING; ++s) {
@@ -1359,10 +1371,22 @@ int bct_get_r(bct_ctx *c, double *r)
     return 0;
 }
 
+// Panels whose z is in (t, ax) form get it written out (enqueued on the
+// context's stream) before anything but a fused batched epoch uses z.
+static int materialize_z(bct_ctx *c)
+{
+    if (!c->z_lazy) return 0;
+    CK(bct::z_materialize(c->dtype, c->d_panels, c->np, c->zt, c->zl_mu, c->zl_st, c->zl_on,
+                          c->z, c->stream));
+    c->z_lazy = false;
+    return 0;
+}
+
 int bct_set_z(bct_ctx *c, int32_t j, const double *zj)
 {
     if (!c || !zj) return BCT_EINVAL;
     DEVICE_GUARD(c);
+    if (int r = materialize_z(c)) return r;
     if (j < c->pb || j >= c->pe) return fail(c, BCT_EINVAL, "panel %d not owned", j);
     const PanelDev &P = c->h_panels[j - c->pb];
     CK(cudaMemcpyAsync(c->z + P.row_off, zj, 8 * P.n_rows, cudaMemcpyHostToDevice, c->stream));
@@ -1374,6 +1398,7 @@ int bct_get_z(bct_ctx *c, int32_t j, double *zj)
 {
     if (!c || !zj) return BCT_EINVAL;
     DEVICE_GUARD(c);
+    if (int r = materialize_z(c)) return r;
     if (j < c->pb || j >= c->pe) return fail(c, BCT_EINVAL, "panel %d not owned", j);
     const PanelDev &P = c->h_panels[j - c->pb];
     CK(cudaMemcpyAsync(zj, c->z + P.row_off, 8 * P.n_rows, cudaMemcpyDeviceToHost, c->stream));
@@ -1395,6 +1420,7 @@ int bct_clear_state(bct_ctx *c)
 {
     if (!c) return BCT_EINVAL;
     DEVICE_GUARD(c);
+    if (int r = materialize_z(c)) return r;
     CK(cudaMemsetAsync(c->x, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
     CK(cudaMemsetAsync(c->z, 0, 8 * std::max<int64_t>(c->z_len, 1), c->stream));
     CK(cudaMemsetAsync(c->xhat, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
@@ -1429,6 +1455,7 @@ int bct_fill_z_from_image(bct_ctx *c)
 {
     if (!c) return BCT_EINVAL;
     DEVICE_GUARD(c);
+    if (int r = materialize_z(c)) return r;
     CK(bct::fill_z(c->dtype, c->d_panels, c->np, c->z_len, c->x, c->z, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return 0;
@@ -1438,6 +1465,7 @@ int bct_projection_sum(bct_ctx *c, double *out)
 {
     if (!c || !out) return BCT_EINVAL;
     DEVICE_GUARD(c);
+    if (int r = materialize_z(c)) return r;
     CK(bct::zsum(c->inv_ptr, c->inv_z, c->n_meas, c->z, c->vec, c->stream));
     CK(cudaMemcpyAsync(out, c->vec, 8 * c->n_meas, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1449,6 +1477,7 @@ int bct_reset_residual(bct_ctx *c)
 {
     if (!c) return BCT_EINVAL;
     DEVICE_GUARD(c);
+    if (int r = materialize_z(c)) return r;
     CK(bct::zsum(c->inv_ptr, c->inv_z, c->n_meas, c->z, c->vec, c->stream));
     CK(bct::sub(c->y, c->vec, c->n_meas, c->r, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1479,6 +1508,7 @@ int bct_audit(bct_ctx *c, double *drift)
 {
     if (!c || !drift) return BCT_EINVAL;
     DEVICE_GUARD(c);
+    if (int r = materialize_z(c)) return r;
     CK(bct::zsum(c->inv_ptr, c->inv_z, c->n_meas, c->z, c->vec, c->stream));
     CK(cudaMemsetAsync(c->audit2, 0, 16, c->stream));
     CK(bct::audit(c->y, c->r, c->vec, c->n_meas, c->audit2, c->stream));
@@ -1533,6 +1563,7 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, const Up
     p.t_ax = c->t_ax; p.seg_part = c->seg_part; p.part = c->part; p.mus = c->mus;
     p.band_cap = c->band_cap; p.band_dbuf = c->band_dbuf;
     p.gx_batch = c->gx_batch; p.seg_batch = c->seg_batch; p.tax_batch = c->tax_batch;
+    p.zt = c->zt; p.zl_on = c->zl_on; p.zl_st = c->zl_st; p.zl_mu = c->zl_mu;
     p.part_task = c->part_task;
     p.statuses = c->statuses; p.out = c->out;
     p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
@@ -1756,6 +1787,10 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
             tot_tiles >= (1ll << 31) || tot_vox >= (1ll << 31))
             batched = false;
     }
+    // phase D folded into the tail: per owned panel its z / x offsets, its
+    // task, z form and (g, x) offset in shared memory (epoch.cu tail)
+    const bool fuse = batched && !getenv("BCT_NO_FUSE_TAIL") &&
+                      (size_t)(c->np + 1) * bct::FT_PANEL_BYTES + (size_t)nt * 16 + 64 <= c->smem;
     if (batched) {
         // the device may still read the old scratch: drain before growing it
         auto grow = [&](double **ptr, int64_t *have, int64_t need) -> int {
@@ -1768,7 +1803,7 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
         };
         if ((r = grow(&c->gx_batch, &c->gx_batch_n, 2 * gxo))) return r;
         if ((r = grow(&c->seg_batch, &c->seg_batch_n, 2 * sgo))) return r;
-        if ((r = grow(&c->tax_batch, &c->tax_batch_n, 2 * txo))) return r;
+        if (!fuse && (r = grow(&c->tax_batch, &c->tax_batch_n, 2 * txo))) return r;
         if ((r = grow(&c->part_task, &c->part_task_n, 33 * nt * (int64_t)c->grid + nt))) return r;
     }
     // the staging block of the previous epoch must have been consumed
@@ -1789,6 +1824,15 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
     hh->n_ent_total = tot_ent;
     hh->guard_factor = c->guard_factor;
     hh->r32_valid = c->r32_valid ? 1 : 0;
+    hh->fuse_tail = fuse ? 1 : 0;
+    if (hh->fuse_tail && !c->zt) {
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaMalloc(&c->zt, bct::zt_pair_bytes(c->dtype) * std::max<int64_t>(c->z_len, 1)));
+    }
+    // any other epoch reads the stored z
+    if (!hh->fuse_tail) {
+        if ((r = materialize_z(c))) return r;
+    }
     // a batched FP32 epoch refreshes the copy before phase A
     if (batched && c->dtype == BCT_F32) c->r32_valid = true;
     if (nt) memcpy(c->h_up + L.tasks, tasks.data(), sizeof(TaskDev) * nt);
@@ -1807,7 +1851,9 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
         for (int64_t k = 0; k < nt; ++k)
             host_prep(c, tasks[k], tmasks.data() + (size_t)k * mw, vmasks.data() + (size_t)k * mw,
                       c->h_up + L.prep + c->pd.bytes() * k);
-    return launch_staged(c, nt, n_visits, L, hook);
+    r = launch_staged(c, nt, n_visits, L, hook);
+    if (r == 0 && hh->fuse_tail) c->z_lazy = true;
+    return r;
 }
 
 int bct_set_divergence_factor(bct_ctx *c, double factor)

@@ -56,6 +56,7 @@ __host__ __device__ constexpr bool narrow_math() { return sizeof(V) == 4 && !BCT
 #ifndef BCT_CHECK
 #define BCT_CHECK 0
 #endif
+
 #define BCT_ASSERT(cond)                                                              \
     do {                                                                              \
         if (BCT_CHECK && !(cond)) {                                                   \
@@ -982,6 +983,36 @@ struct RingSlot {
 constexpr int RING = 4;
 static_assert(sizeof(RingSlot) % 8 == 0, "ring slots are copied in 8-byte words");
 
+// fused batched tail (EpochHeader::fuse_tail): tables in the phase buffers
+// after the per-task mu / status, per owned panel lp: z and x offsets (one
+// past the last panel: z_len, x_len), its task this epoch (-1: none), the
+// offset of that task's (g, x) pairs relative to x, and the form of its z:
+// st >= 0: z = ax + mu t from the persistent (t, ax) pairs (EpochParams::zt)
+// with this mu / status, st = -1: the stored z
+struct FuseTables {
+    double *mu_t;   // per task (phase D's mu)
+    int *st_t;
+    int64_t *xoff, *gxo;
+    double *mu;
+    int32_t *roff, *task, *st;
+};
+
+__device__ __forceinline__ FuseTables fuse_tables(double *rs, int n_tasks, int np)
+{
+    FuseTables t;
+    t.mu_t = rs;
+    t.st_t = reinterpret_cast<int *>(rs + n_tasks);
+    int64_t *q = reinterpret_cast<int64_t *>(rs + n_tasks + (n_tasks + 1) / 2);
+    t.xoff = q;
+    t.gxo = q + np + 1;
+    t.mu = reinterpret_cast<double *>(q + 2 * np + 1);
+    int32_t *w = reinterpret_cast<int32_t *>(t.mu + np);
+    t.roff = w;
+    t.task = w + np + 1;
+    t.st = w + 2 * np + 1;
+    return t;
+}
+
 template <typename V>
 __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, double *rs, double *sh,
                               RingSlot *ring, int *s_tpre, int *s_lp)
@@ -1297,7 +1328,10 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const PanelDev &P = p.panels[T.lp];
             const int f1 = min(rb1, T.row_pre + P.n_rows);
             const PT *spart = segb + T.seg_off;
-            PT *tax = taxb + T.tax_off;
+            // fused tail: (t, ax) kept per panel row (the z of the panel from
+            // now on), else per-epoch scratch for phase D
+            PT *tax = hdr.fuse_tail ? reinterpret_cast<PT *>(p.zt) + P.row_off
+                                    : taxb + T.tax_off;
             double wsum = 0.0;
             // CR rows per thread at a time, their (pointer, position, partial)
             // loads issued level by level: CR-fold memory parallelism for a
@@ -1373,6 +1407,36 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
         }
     }
     __syncthreads();
+    if (hdr.fuse_tail) {
+        // phase D is done by the epoch tail (z from (t, ax) where the refresh
+        // reads it, x-hat in the commit pass; counts by the last block):
+        // per owned panel its offsets and task, after mu / status
+        const FuseTables ft = fuse_tables(rs, n_tasks, p.n_panels_owned);
+        for (int lp = threadIdx.x; lp <= p.n_panels_owned; lp += BLOCK) {
+            const bool in = lp < p.n_panels_owned;
+            ft.roff[lp] = in ? (int32_t)p.panels[lp].row_off : (int32_t)p.z_len;
+            ft.xoff[lp] = in ? p.panels[lp].x_off : p.x_len;
+            if (in) {
+                // z form left by earlier epochs (rewritten by the last block)
+                const bool lazy = p.zl_on[lp] != 0;
+                ft.task[lp] = -1;
+                ft.st[lp] = lazy ? p.zl_st[lp] : -1;
+                ft.mu[lp] = lazy ? p.zl_mu[lp] : 0.0;
+            }
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < n_tasks; k += BLOCK) {
+            const TaskDev &T = p.tasks[k];
+            const PanelDev &P = p.panels[T.lp];
+            ft.task[T.lp] = k;   // one task per panel on this path (api.cu)
+            ft.st[T.lp] = st_s[k];
+            ft.mu[T.lp] = mu_s[k];
+            ft.gxo[T.lp] = T.gx_off - P.x_off;
+        }
+        __syncthreads();
+        if (!BCT_NO_TL_BATCH) TL_MARK(0, 6);
+        return;
+    }
     if (b == 0 && threadIdx.x == 0)
         for (int k = 0; k < n_tasks; ++k) p.counts[p.tasks[k].lp] += 1;
     {
@@ -1855,10 +1919,46 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     }
 
     // ---- epoch tail ------------------------------------------------------
-    grid_sync(p.bar);
+    // fused batched tail: phase D's work is done here, after phase C's barrier
+    const bool fuse = hdr.batched && hdr.fuse_tail;
+    if (!fuse) grid_sync(p.bar);
     const bool do_metrics = (hdr.flags & 2) != 0;
     const bool do_commit = (hdr.flags & 1) != 0;
     double rsq = 0.0, xsq = 0.0, esq = 0.0;
+    using PT = typename std::conditional<narrow_math<V>(), float2, double2>::type;
+    const PT *zt = reinterpret_cast<const PT *>(p.zt);
+    const FuseTables ft = fuse_tables(rs, n_tasks, p.n_panels_owned);
+    int lpc = 0;   // panel of the thread's last z offset (offsets ascend within a row)
+    // z values at offsets o[0..N) (-1: none): the stored z, or on the fused
+    // path z = ax + mu t from the panel's persistent (t, ax) pairs
+    auto zvals = [&](auto &o, auto &v) {
+        constexpr int N = sizeof(o) / sizeof(o[0]);
+        if (!fuse) {
+#pragma unroll
+            for (int u = 0; u < N; ++u) v[u] = o[u] >= 0 ? __ldcg(p.z + o[u]) : 0.0;
+            return;
+        }
+        int lq[N];
+#pragma unroll
+        for (int u = 0; u < N; ++u) {
+            lq[u] = -1;
+            if (o[u] < 0) continue;
+            while (o[u] < ft.roff[lpc]) --lpc;
+            while (o[u] >= ft.roff[lpc + 1]) ++lpc;
+            lq[u] = lpc;
+        }
+        PT q[N];
+#pragma unroll
+        for (int u = 0; u < N; ++u) {
+            // (t, ax) written in phase C of this launch: L2-coherent loads
+            if (lq[u] >= 0 && ft.st[lq[u]] >= 0) q[u] = __ldcg(zt + o[u]);
+            else v[u] = o[u] >= 0 ? __ldcg(p.z + o[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < N; ++u)
+            if (lq[u] >= 0 && ft.st[lq[u]] >= 0)
+                v[u] = z_value((double)q[u].x, (double)q[u].y, ft.mu[lq[u]], ft.st[lq[u]]);
+    };
     if (!serial || do_metrics || sharded) {
         // warps cover 32 consecutive measurements (gtid and nthreads are
         // multiples of 32): the interleaved inverse map is read coalesced
@@ -1875,15 +1975,16 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 double v[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) o[u] = __ldg(p.invt + e + 32 * u);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = o[u] >= 0 ? __ldcg(p.z + o[u]) : 0.0;
+                zvals(o, v);
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
                     if (o[u] >= 0) acc += v[u];
             }
             for (; e < e1; e += 32) {
-                const int o = __ldg(p.invt + e);
-                if (o >= 0) acc += __ldcg(p.z + o);
+                int o[1] = {__ldg(p.invt + e)};
+                double v[1];
+                zvals(o, v);
+                if (o[0] >= 0) acc += v[0];
             }
             if (g >= p.n_meas) continue;
             if (sharded) {
@@ -1903,15 +2004,31 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     // contiguous in x / xhat / x_true); the panel of a voxel by binary search
     {
         const int npo = p.n_panels_owned;
+        const double2 *gxb = reinterpret_cast<const double2 *>(p.gx_batch);
         for (int64_t v = gtid; v < p.x_len; v += nthreads) {
             int lo = 0, hi = npo - 1;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
-                if (p.panels[mid].x_off <= v) lo = mid; else hi = mid - 1;
+                if ((fuse ? ft.xoff[mid] : p.panels[mid].x_off) <= v) lo = mid; else hi = mid - 1;
             }
-            const int cnt = p.counts[lo];
+            int cnt = p.counts[lo];
             double xv = p.x[v];
-            if (do_commit && cnt > 0) {
+            const int kf = fuse ? ft.task[lo] : -1;
+            if (kf >= 0) {
+                // phase D's x-hat update of the visit (one task), then commit
+                const double2 a = __ldcg(gxb + ft.gxo[lo] + v);
+                const double xs =
+                    0.0 + (ft.st[lo] == 0 ? __dadd_rn(xv, __dmul_rn(ft.mu[lo], a.x)) : xv);
+                const double xh = p.xhat[v] + xs;
+                ++cnt;
+                if (do_commit) {
+                    xv = xh / (double)cnt;
+                    p.x[v] = xv;
+                    p.xhat[v] = 0.0;
+                } else {
+                    p.xhat[v] = xh;
+                }
+            } else if (do_commit && cnt > 0) {
                 xv = p.xhat[v] / (double)cnt;
                 p.x[v] = xv;
                 p.xhat[v] = 0.0;
@@ -1958,6 +2075,14 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             }
             if (do_commit)
                 for (int lp = 0; lp < p.n_panels_owned; ++lp) p.counts[lp] = 0;
+            if (fuse)   // phase D's updates (every block has read the old values)
+                for (int k = 0; k < n_tasks; ++k) {
+                    const int lp = p.tasks[k].lp;
+                    if (!do_commit) p.counts[lp] += 1;
+                    p.zl_on[lp] = 1;
+                    p.zl_mu[lp] = p.mus[k];
+                    p.zl_st[lp] = p.statuses[k];
+                }
             // reference |x| (sharded: the finish writes it from the global norm)
             if ((hdr.flags & 16) && !sharded) *p.guard_ref = fmax(sqrt(a1), 1e-12);
             *p.ticket = 0;
@@ -1965,9 +2090,51 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     }
 }
 
+// z of every owned panel in (t, ax) form written out (z = ax + mu t, the
+// fused tail's value bit for bit) and the panel returned to the stored form;
+// blockIdx.y = panel
+template <typename V>
+__global__ void z_materialize_kernel(const PanelDev *panels, const void *zt_, const double *mu,
+                                     const int32_t *st, const int32_t *on, double *z)
+{
+    using PT = typename std::conditional<narrow_math<V>(), float2, double2>::type;
+    const int lp = blockIdx.y;
+    if (!on[lp]) return;
+    const PT *zt = reinterpret_cast<const PT *>(zt_) + panels[lp].row_off;
+    double *zr = z + panels[lp].row_off;
+    const double m = mu[lp];
+    const int s = st[lp];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < panels[lp].n_rows;
+         i += gridDim.x * blockDim.x) {
+        const PT q = zt[i];
+        zr[i] = z_value((double)q.x, (double)q.y, m, s);
+    }
+}
+
 }  // namespace
 
 namespace bct {
+
+size_t zt_pair_bytes(int dtype)
+{
+    return dtype == 0 ? sizeof(double2)
+                      : (narrow_math<float>() ? sizeof(float2) : sizeof(double2));
+}
+
+cudaError_t z_materialize(int dtype, const PanelDev *panels, int np, const void *zt,
+                          const double *mu, const int32_t *st, int32_t *on, double *z,
+                          cudaStream_t s)
+{
+    if (np < 1) return cudaSuccess;
+    const dim3 grid(64, np);
+    if (dtype == 0)
+        z_materialize_kernel<double><<<grid, 256, 0, s>>>(panels, zt, mu, st, on, z);
+    else
+        z_materialize_kernel<float><<<grid, 256, 0, s>>>(panels, zt, mu, st, on, z);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaMemsetAsync(on, 0, sizeof(int32_t) * np, s);
+}
 
 std::string cuda_err(cudaError_t e) { return std::string(cudaGetErrorString(e)); }
 

@@ -111,6 +111,12 @@ struct EpochHeader {
     int32_t host_prep;               // 1: EpochParams::prep holds every task's record
     int32_t r32_valid;               // FP32 mode: r32 == (float)r on every row (every
                                      // writer of r in a launch keeps it so)
+    int32_t fuse_tail;               // batched: no phase D; phase C keeps (t, ax) per
+                                     // panel row (z in (t, ax) form, EpochParams::zt),
+                                     // the tail forms z = ax + mu t where it sums z and
+                                     // updates x-hat; the per-panel tables fit in
+                                     // dynamic shared memory
+    int32_t pad_;
     // divergence guard (solvers.py:251-258): BCT_GUARD_REF records the
     // reference norm max(|x|, 1e-12) after this epoch; BCT_GUARD skips the
     // whole epoch when the previous one left |x| non-finite or above
@@ -212,6 +218,11 @@ struct EpochParams {
     double *seg_batch;
     double *tax_batch;
     double *part_task;         // [n_tasks][2][grid] gg / denom partials (batched)
+    // z in (t, ax) form (fused batched tail): panel lp's z is ax + mu t from
+    // zt[row_off..) with zl_mu / zl_st[lp] while zl_on[lp] (api.cu materialize_z)
+    void *zt;
+    int32_t *zl_on, *zl_st;
+    double *zl_mu;
     int32_t band_cap;          // shared-memory slots per band buffer
     int32_t band_dbuf;         // 1: two band buffers (copy next tile while computing)
     double *part;              // per-block partials: [4][grid]
@@ -304,6 +315,9 @@ constexpr int BAND_ALIGN = 4;
 
 // epoch-batched path: at most this many tasks (task tables live in shared memory)
 constexpr int MAX_BATCH_TASKS = 256;
+// fused batched tail: shared-memory bytes per owned panel (z / x offsets,
+// task, (g, x) offset, z form: mu / status)
+constexpr int FT_PANEL_BYTES = 36;
 
 // device sampler (sampler.cu)
 struct SampleVisit {
@@ -335,6 +349,12 @@ void launch_epoch(const EpochParams &p, int dtype, int grid, int block, size_t s
                   cudaStream_t s, cudaError_t *err);
 int epoch_grid_size(int dtype, int device, size_t smem, int *block);
 size_t epoch_static_smem(int dtype);   // the epoch kernel's static shared arrays
+// z in (t, ax) form (EpochParams::zt): bytes per pair, and the pass that
+// writes such panels' z out and returns them to the stored form
+size_t zt_pair_bytes(int dtype);
+cudaError_t z_materialize(int dtype, const PanelDev *panels, int np, const void *zt,
+                          const double *mu, const int32_t *st, int32_t *on, double *z,
+                          cudaStream_t s);
 int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nnz,
                     const double *vals64, const int32_t *cols_c, const int32_t *indptr_c,
                     const int32_t *l2g, const int32_t *rbp, const std::vector<int32_t> &c2d_h,
