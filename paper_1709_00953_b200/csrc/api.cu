@@ -133,7 +133,14 @@ struct bct_ctx {
     // (UpLayout), staged in pinned memory; one download of the result block
     // [EpochOut | mus x nt | statuses x nt]: each small copy costs the
     // stream a few microseconds
+    // Double-buffered: epoch e uploads into buffer e & 1 on the copy stream
+    // while epoch e-1 still runs; d_up / h_up point at the current buffer.
     char *d_up = nullptr, *h_up = nullptr;
+    char *d_upb[2] = {nullptr, nullptr}, *h_upb[2] = {nullptr, nullptr};
+    int up_i = 0;
+    cudaStream_t cstream = nullptr;          // upload copies
+    cudaEvent_t staged_b[2] = {nullptr, nullptr};   // upload of buffer b done (copy stream)
+    cudaEvent_t free_b[2] = {nullptr, nullptr};     // main-stream work that read buffer b done
     size_t up_cap = 0;
     char *d_res = nullptr;
     uint64_t *cur_masks = nullptr;   // device masks / tasks of the last submitted epoch
@@ -148,7 +155,6 @@ struct bct_ctx {
     int64_t task_cap = 0;
     // staging
 
-    cudaEvent_t staged = nullptr;
     Slot slots[RING];
     int head = 0, tail = 0;           // ring: tail = oldest pending
     int grid = 0, block = 0;
@@ -544,7 +550,6 @@ int finalize(bct_ctx *c)
     CK(cudaMemsetAsync(c->counts, 0, 4 * std::max(c->np, 1), c->stream));
     CK(cudaMemsetAsync(c->bar, 0, 4, c->stream));
     CK(cudaMemsetAsync(c->ticket, 0, 4, c->stream));
-    CK(cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming));
     for (int s = 0; s < RING; ++s) {
         CK(cudaEventCreateWithFlags(&c->slots[s].done, cudaEventDisableTiming));
         CK(cudaEventCreate(&c->slots[s].t0));
@@ -577,11 +582,16 @@ int ensure_task_cap(bct_ctx *c, int64_t n)
     int64_t cap = std::max<int64_t>(n, 2 * c->task_cap);
     // drain pending epochs before reallocating buffers they use
     CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(c->cstream));
     const size_t up = up_layout(c, cap, true).total;
-    if (c->d_up) cudaFree(c->d_up);
-    if (c->h_up) cudaFreeHost(c->h_up);
-    CK(cudaMalloc((void **)&c->d_up, up));
-    CK(cudaHostAlloc((void **)&c->h_up, up, cudaHostAllocDefault));
+    for (int b = 0; b < 2; ++b) {
+        if (c->d_upb[b]) cudaFree(c->d_upb[b]);
+        if (c->h_upb[b]) cudaFreeHost(c->h_upb[b]);
+        CK(cudaMalloc((void **)&c->d_upb[b], up));
+        CK(cudaHostAlloc((void **)&c->h_upb[b], up, cudaHostAllocDefault));
+    }
+    c->d_up = c->d_upb[c->up_i];
+    c->h_up = c->h_upb[c->up_i];
     c->up_cap = up;
     // the result block; the last epoch's EpochOut carries over (the
     // divergence guard of the next epoch reads it)
@@ -628,8 +638,13 @@ void destroy(bct_ctx *c)
     for (double *q : {c->gx_batch, c->seg_batch, c->tax_batch, c->part_task})
         if (q) cudaFree(q);
     if (c->zt) cudaFree(c->zt);
-    if (c->d_up) cudaFree(c->d_up);
-    if (c->h_up) cudaFreeHost(c->h_up);
+    if (c->cstream) cudaStreamSynchronize(c->cstream);
+    for (int b = 0; b < 2; ++b) {
+        if (c->d_upb[b]) cudaFree(c->d_upb[b]);
+        if (c->h_upb[b]) cudaFreeHost(c->h_upb[b]);
+        if (c->staged_b[b]) cudaEventDestroy(c->staged_b[b]);
+        if (c->free_b[b]) cudaEventDestroy(c->free_b[b]);
+    }
     for (int s = 0; s < RING; ++s) {
         Slot &S = c->slots[s];
         if (S.done) cudaEventDestroy(S.done);
@@ -637,7 +652,7 @@ void destroy(bct_ctx *c)
         if (S.t1) cudaEventDestroy(S.t1);
         if (S.h_res) cudaFreeHost(S.h_res);
     }
-    if (c->staged) cudaEventDestroy(c->staged);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -647,6 +662,11 @@ int init_ctx(bct_ctx *c, int device, int np)
     c->device = device;
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaEventCreateWithFlags(&c->staged_b[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->free_b[b], cudaEventDisableTiming));
+    }
     int coop = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
     if (!coop) return fail(c, BCT_ECUDA, "device %d lacks cooperative launch", device);
@@ -1536,8 +1556,19 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, const Up
         S.pending = false;
         c->tail = (c->tail + 1) % RING;
     }
-    CK(cudaMemcpyAsync(c->d_up, c->h_up, L.total, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaEventRecord(c->staged, c->stream));
+    {
+        // upload on the copy stream (it overlaps the previous epoch); buffer
+        // b was last read by the epoch before the previous one (free_b[b],
+        // recorded when the previous epoch was launched)
+        const int b = c->up_i;
+        CK(cudaStreamWaitEvent(c->cstream, c->free_b[b], 0));
+        CK(cudaMemcpyAsync(c->d_up, c->h_up, L.total, cudaMemcpyHostToDevice, c->cstream));
+        CK(cudaEventRecord(c->staged_b[b], c->cstream));
+        // all work queued so far (the previous epoch and its all-reduce /
+        // finish) is the last reader of the other buffer
+        CK(cudaEventRecord(c->free_b[b ^ 1], c->stream));
+        CK(cudaStreamWaitEvent(c->stream, c->staged_b[b], 0));
+    }
     c->cur_masks = reinterpret_cast<uint64_t *>(c->d_up + L.masks);
     c->cur_tasks = reinterpret_cast<TaskDev *>(c->d_up + L.tasks);
     c->mus = reinterpret_cast<double *>(c->d_res + RES_HEAD);
@@ -1806,8 +1837,11 @@ static int plan_and_launch(bct_ctx *c, int32_t mode, int32_t flags, std::vector<
         if (!fuse && (r = grow(&c->tax_batch, &c->tax_batch_n, 2 * txo))) return r;
         if ((r = grow(&c->part_task, &c->part_task_n, 33 * nt * (int64_t)c->grid + nt))) return r;
     }
-    // the staging block of the previous epoch must have been consumed
-    CK(cudaEventSynchronize(c->staged));
+    // switch upload buffers; this one's copy (two epochs ago) must be done
+    c->up_i ^= 1;
+    c->d_up = c->d_upb[c->up_i];
+    c->h_up = c->h_upb[c->up_i];
+    CK(cudaEventSynchronize(c->staged_b[c->up_i]));
     const bool host_prep_on = !batched && host_masks && nt > 0;
     const UpLayout L = up_layout(c, nt, host_prep_on);
     EpochHeader *hh = reinterpret_cast<EpochHeader *>(c->h_up);
@@ -1928,7 +1962,7 @@ int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
     // the drawn blocks of the last epoch, as the device saw them (host plan or sampler)
     const uint64_t *dmask = c->cur_masks;   // epoch mask first (EpochParams::masks)
     if (!dmask) return fail(c, BCT_EINVAL, "no sharded epoch submitted");
-    const int nb = 296;
+    const int nb = 8 * c->grid;   // c->part holds 8 * grid + 8 partials
     // flags: the epoch's BCT_GUARD / BCT_GUARD_REF (a skipped epoch skips its finish)
     FinishGuard guard{&c->out->x_sq, c->guard_ref, c->guard_factor, (flags & BCT_GUARD) ? 1 : 0,
                       (flags & BCT_GUARD_REF) ? 1 : 0};

@@ -12,6 +12,7 @@
 //   inverse row map and the bitwise forward / z-fill / projection-sum
 //   kernels used for state set-up (projector.py:220-244, 756-777); the panel
 //   layout itself is built in layout.cu.
+#include <algorithm>
 #include <climits>
 #include <cstdint>
 #include <cub/cub.cuh>
@@ -537,6 +538,7 @@ __global__ void commit_kernel(const PanelDev *panels, int np, int32_t *counts, d
 // block, and the last block to finish (ticket) writes the epoch's global
 // result: |y - S|^2 (block order, like the host sum it replaces), |x|^2 and
 // |x_t - x|^2 from the all-reduced exchange tail.
+constexpr int FIN_U = 4;
 __global__ void sharded_finish_kernel(const double *y, const double *S, int64_t n,
                                       const int32_t *rb_of_row, const uint64_t *mask, double *r,
                                       float *r32, double *part, const double *tail,
@@ -546,31 +548,53 @@ __global__ void sharded_finish_kernel(const double *y, const double *S, int64_t 
     __shared__ double sh[32];
     __shared__ bool is_last;
     double acc = 0.0;
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
-         g += (int64_t)gridDim.x * blockDim.x) {
-        double d = y[g] - S[g];
-        int rb = rb_of_row[g];
-        if (rb >= 0 && ((mask[rb >> 6] >> (rb & 63)) & 1ull)) {
-            r[g] = d;
-            if (r32) r32[g] = (float)d;   // FP32 mode's band copy stays in step
+    // FIN_U rows per thread in flight (their loads issued before the stores)
+    const int64_t step = (int64_t)gridDim.x * blockDim.x * FIN_U;
+    for (int64_t g0 = (int64_t)blockIdx.x * blockDim.x * FIN_U + threadIdx.x; g0 < n; g0 += step) {
+        double d[FIN_U];
+        int rb[FIN_U];
+#pragma unroll
+        for (int u = 0; u < FIN_U; ++u) {
+            const int64_t g = g0 + (int64_t)u * blockDim.x;
+            d[u] = g < n ? __ldg(y + g) - __ldcg(S + g) : 0.0;
+            rb[u] = g < n ? __ldg(rb_of_row + g) : -1;
         }
-        acc = fma(d, d, acc);
+#pragma unroll
+        for (int u = 0; u < FIN_U; ++u) {
+            const int64_t g = g0 + (int64_t)u * blockDim.x;
+            if (rb[u] >= 0 && ((__ldg(mask + (rb[u] >> 6)) >> (rb[u] & 63)) & 1ull)) {
+                r[g] = d[u];
+                if (r32) r32[g] = (float)d[u];   // FP32 mode's band copy stays in step
+            }
+            acc = fma(d[u], d[u], acc);
+        }
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    // fixed-order block sum
+    auto block_sum = [&](double v) {
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+        __syncthreads();
         double s = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
-        part[blockIdx.x] = s;
+        if (threadIdx.x == 0)
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+        return s;
+    };
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = acc;
         __threadfence();
         is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!is_last || threadIdx.x != 0) return;
+    if (!is_last) return;
+    // the last block: every thread sums blocks t, t + blockDim, ... (L2
+    // loads), then the fixed-order block sum
     __threadfence();
     double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += ((volatile double *)part)[b];
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) s += __ldcg(part + b);
+    s = block_sum(s);
+    if (threadIdx.x != 0) return;
     out->resid_sq = s;
     out->x_sq = tail[0];
     out->err_sq = tail[1];
@@ -770,6 +794,8 @@ cudaError_t sharded_finish(const double *y, const double *S, int64_t n, const in
                            const double *tail, EpochOut *out, unsigned int *ticket,
                            const FinishGuard &guard, cudaStream_t s)
 {
+    // FIN_U rows per thread, at most nb blocks (the partials array's size)
+    nb = (int)std::min<int64_t>(nb, std::max<int64_t>(1, (n + 256 * FIN_U - 1) / (256 * FIN_U)));
     sharded_finish_kernel<<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, r, r32, part, tail, out,
                                              ticket, guard);
     return cudaGetLastError();

@@ -2055,37 +2055,49 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     }
     __syncthreads();
     if (is_last) {
+        // the whole last block: the blocks' partials summed by thread
+        // (blocks t, t + BLOCK, ...), then the fixed-order block sum; the
+        // per-task and per-panel updates one per thread (a one-thread loop of
+        // dependent L2 round trips here cost ~20 us per epoch)
         __threadfence();
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (unsigned int b = threadIdx.x; b < gridDim.x; b += BLOCK) {
+            a0 += __ldcg(part_m + 3 * b + 0);
+            a1 += __ldcg(part_m + 3 * b + 1);
+            a2 += __ldcg(part_m + 3 * b + 2);
+        }
+        double nd = 0.0;
+        for (int k = threadIdx.x; k < n_tasks; k += BLOCK) nd += __ldcg(p.statuses + k) != 0;
+        a0 = block_sum_all(a0, sh);
+        a1 = block_sum_all(a1, sh);
+        a2 = block_sum_all(a2, sh);
+        nd = block_sum_all(nd, sh);
         if (threadIdx.x == 0) {
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-            for (unsigned int b = 0; b < gridDim.x; ++b) {
-                a0 += ((volatile double *)part_m)[3 * b + 0];
-                a1 += ((volatile double *)part_m)[3 * b + 1];
-                a2 += ((volatile double *)part_m)[3 * b + 2];
-            }
-            int ndeg = 0;
-            for (int k = 0; k < n_tasks; ++k) ndeg += p.statuses[k] != 0;
             p.out->resid_sq = a0;
             p.out->x_sq = a1;
             p.out->err_sq = p.x_true ? a2 : __longlong_as_double(0x7ff8000000000000ll);
-            p.out->n_degenerate = ndeg;
+            p.out->n_degenerate = (int)nd;
             if (sharded) {
                 p.exchange[p.n_meas] = a1;
                 p.exchange[p.n_meas + 1] = a2;
             }
-            if (do_commit)
-                for (int lp = 0; lp < p.n_panels_owned; ++lp) p.counts[lp] = 0;
-            if (fuse)   // phase D's updates (every block has read the old values)
-                for (int k = 0; k < n_tasks; ++k) {
-                    const int lp = p.tasks[k].lp;
-                    if (!do_commit) p.counts[lp] += 1;
-                    p.zl_on[lp] = 1;
-                    p.zl_mu[lp] = p.mus[k];
-                    p.zl_st[lp] = p.statuses[k];
-                }
             // reference |x| (sharded: the finish writes it from the global norm)
             if ((hdr.flags & 16) && !sharded) *p.guard_ref = fmax(sqrt(a1), 1e-12);
             *p.ticket = 0;
+        }
+        if (do_commit)
+            for (int lp = threadIdx.x; lp < p.n_panels_owned; lp += BLOCK) p.counts[lp] = 0;
+        if (fuse) {
+            // phase D's updates (every block has read the old values); one
+            // task per panel on this path
+            __syncthreads();
+            for (int k = threadIdx.x; k < n_tasks; k += BLOCK) {
+                const int lp = p.tasks[k].lp;
+                if (!do_commit) p.counts[lp] += 1;
+                p.zl_on[lp] = 1;
+                p.zl_mu[lp] = __ldcg(p.mus + k);
+                p.zl_st[lp] = __ldcg(p.statuses + k);
+            }
         }
     }
 }
