@@ -548,27 +548,42 @@ __global__ void sharded_finish_kernel(const double *y, const double *S, int64_t 
     __shared__ double sh[32];
     __shared__ bool is_last;
     double acc = 0.0;
-    // FIN_U rows per thread in flight (their loads issued before the stores)
+    // one wave of blocks; each thread takes FIN_U pairs of consecutive rows
+    // per round (16-byte loads of y and S, all issued before the stores)
+    auto row = [&](int64_t g, double d, int rb) {
+        if (rb >= 0 && ((__ldg(mask + (rb >> 6)) >> (rb & 63)) & 1ull)) {
+            r[g] = d;
+            if (r32) r32[g] = (float)d;   // FP32 mode's band copy stays in step
+        }
+        acc = fma(d, d, acc);
+    };
+    const int64_t npair = n >> 1;
     const int64_t step = (int64_t)gridDim.x * blockDim.x * FIN_U;
-    for (int64_t g0 = (int64_t)blockIdx.x * blockDim.x * FIN_U + threadIdx.x; g0 < n; g0 += step) {
-        double d[FIN_U];
-        int rb[FIN_U];
+    for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x * FIN_U + threadIdx.x; q0 < npair; q0 += step) {
+        double2 d[FIN_U];
+        int2 rb[FIN_U];
 #pragma unroll
         for (int u = 0; u < FIN_U; ++u) {
-            const int64_t g = g0 + (int64_t)u * blockDim.x;
-            d[u] = g < n ? __ldg(y + g) - __ldcg(S + g) : 0.0;
-            rb[u] = g < n ? __ldg(rb_of_row + g) : -1;
+            const int64_t q = q0 + (int64_t)u * blockDim.x;
+            if (q < npair) {
+                const double2 yy = __ldg(reinterpret_cast<const double2 *>(y) + q);
+                const double2 ss = __ldcg(reinterpret_cast<const double2 *>(S) + q);
+                d[u] = make_double2(yy.x - ss.x, yy.y - ss.y);
+                rb[u] = __ldg(reinterpret_cast<const int2 *>(rb_of_row) + q);
+            } else {
+                d[u] = make_double2(0.0, 0.0);
+                rb[u] = make_int2(-1, -1);
+            }
         }
 #pragma unroll
         for (int u = 0; u < FIN_U; ++u) {
-            const int64_t g = g0 + (int64_t)u * blockDim.x;
-            if (rb[u] >= 0 && ((__ldg(mask + (rb[u] >> 6)) >> (rb[u] & 63)) & 1ull)) {
-                r[g] = d[u];
-                if (r32) r32[g] = (float)d[u];   // FP32 mode's band copy stays in step
-            }
-            acc = fma(d[u], d[u], acc);
+            const int64_t q = q0 + (int64_t)u * blockDim.x;
+            row(2 * q, d[u].x, rb[u].x);
+            row(2 * q + 1, d[u].y, rb[u].y);
         }
     }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)   // odd last row
+        row(n - 1, __ldg(y + n - 1) - __ldcg(S + n - 1), __ldg(rb_of_row + n - 1));
     // fixed-order block sum
     auto block_sum = [&](double v) {
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -794,8 +809,18 @@ cudaError_t sharded_finish(const double *y, const double *S, int64_t n, const in
                            const double *tail, EpochOut *out, unsigned int *ticket,
                            const FinishGuard &guard, cudaStream_t s)
 {
-    // FIN_U rows per thread, at most nb blocks (the partials array's size)
-    nb = (int)std::min<int64_t>(nb, std::max<int64_t>(1, (n + 256 * FIN_U - 1) / (256 * FIN_U)));
+    // FIN_U row pairs per thread and round, one wave of resident blocks, at
+    // most nb blocks (the partials array's size)
+    static int wave = 0;
+    if (wave == 0) {
+        int dev = 0, sms = 148, per = 4;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sharded_finish_kernel, 256, 0);
+        wave = std::max(1, sms * std::max(per, 1));
+    }
+    nb = (int)std::min<int64_t>(std::min(nb, wave),
+                                std::max<int64_t>(1, (n / 2 + 256 * FIN_U - 1) / (256 * FIN_U)));
     sharded_finish_kernel<<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, r, r32, part, tail, out,
                                              ticket, guard);
     return cudaGetLastError();

@@ -270,6 +270,9 @@ __device__ __forceinline__ int task_slice(const PrepView &R, const PanelDev &P, 
 #ifndef BCT_B_HINT
 #define BCT_B_HINT 1
 #endif
+#ifndef BCT_A_DEPHASE
+#define BCT_A_DEPHASE 1          // phase A: CTAs' tile boundaries offset by (b % 8)/8 tile
+#endif
 #ifndef BCT_B_PREFETCH
 #define BCT_B_PREFETCH 8         // phase B prefetches the values of slice f+8 into L2 (0: off)
 #endif
@@ -977,8 +980,7 @@ struct RingSlot {
     PanelDev P;
     int64_t gx_off;
     int k, t;
-    int part, nparts;   // slice part of a split last-round tile (nparts 1: whole tile)
-    int pad_;
+    int q0, q1, qd;     // slices [nsl*q0/qd, nsl*q1/qd) of the tile (0, 1, 1: whole tile)
 };
 constexpr int RING = 4;
 static_assert(sizeof(RingSlot) % 8 == 0, "ring slots are copied in 8-byte words");
@@ -1062,17 +1064,42 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     __syncthreads();
     {
         // whole tiles in rounds of G; the tiles of the last partial round are
-        // cut into up to 8 slice parts so every CTA gets the same share
+        // cut into up to 8 slice parts so every CTA gets the same share.
+        // The CTAs' tile boundaries are de-phased: CTA b starts with the last
+        // (8 - f)/8 of its first tile (f = b % 8) and does its first f/8 after
+        // its other whole tiles.  In lock step every CTA waits for its next
+        // band and restarts its streams at the same moment, leaving HBM idle
+        // at each tile start (measured: the first tiles of an epoch ran
+        // 36 -> 28 us until the CTAs drifted apart).
         const int bb = b;
         const int full = hdr.n_tiles_total / G, rem = hdr.n_tiles_total - full * G;
         const int nsplit = rem > 0 ? max(1, min(8, G / rem)) : 1;
-        const int n_items = full + (bb < rem * nsplit ? 1 : 0);
+        const int fph = BCT_A_DEPHASE ? bb % 8 : 0;
+        const bool wrap = full >= 2 && fph > 0;
+        const int n_whole = full + (wrap ? 1 : 0);   // items before the remainder part
+        const int n_items = n_whole + (bb < rem * nsplit ? 1 : 0);
         // FP32 bands: two buffers fit in one FP64 band's space
         const bool dbuf = sizeof(TB) == 4 || p.band_dbuf != 0;
         TB *buf[2] = {reinterpret_cast<TB *>(rs), reinterpret_cast<TB *>(rs) + (dbuf ? p.band_cap : 0)};
         double *red = rs + (int64_t)p.band_cap * (sizeof(TB) == 4 ? 1 : (dbuf ? 2 : 1));
         auto ring_issue = [&](int it) {   // warp 0
-            const int item = it < full ? bb + it * G : full * G + bb / nsplit;
+            int item, q0 = 0, q1 = 1, qd = 1;
+            if (it >= n_whole) {   // the remainder tile's part
+                item = full * G + bb / nsplit;
+                q0 = bb % nsplit;
+                q1 = q0 + 1;
+                qd = nsplit;
+            } else if (wrap && it == 0) {   // the first tile's last (8 - fph)/8
+                item = bb;
+                q0 = fph;
+                q1 = qd = 8;
+            } else if (wrap && it == full) {   // ... and its first fph/8
+                item = bb;
+                q1 = fph;
+                qd = 8;
+            } else {
+                item = bb + it * G;
+            }
             int lo = 0, hi = n_tasks - 1;  // last task with tile_pre <= item
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
@@ -1086,8 +1113,9 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                 cp_async8(&S.gx_off, &p.tasks[lo].gx_off);
                 S.k = lo;
                 S.t = item - s_tpre[lo];
-                S.part = it < full ? 0 : bb % nsplit;
-                S.nparts = it < full ? 1 : nsplit;
+                S.q0 = q0;
+                S.q1 = q1;
+                S.qd = qd;
             }
             cp_async_commit();
         };
@@ -1110,22 +1138,28 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                 cp_async_wait_all();
                 __syncthreads();
             }
+            if (it == 0 && p.timeline && threadIdx.x == 0 && n_tasks > 1)   // profiling: first band
+                p.timeline[((int64_t)1 * 8 + 5) * gridDim.x + blockIdx.x] = gtimer();
+            if (it == 1 && p.timeline && threadIdx.x == 0 && n_tasks > 1)   // profiling: first tile done
+                p.timeline[((int64_t)1 * 8 + 6) * gridDim.x + blockIdx.x] = gtimer();
+            if (it < 8 && p.timeline && threadIdx.x == 0 && n_tasks > 2)    // profiling: tile starts
+                p.timeline[((int64_t)2 * 8 + it) * gridDim.x + blockIdx.x] = gtimer();
             const RingSlot &S = ring[it % RING];
             // the other buffer was last read by tile it-1 (before its barrier)
             if (dbuf && it + 1 < n_items)
                 band_issue(ring[(it + 1) % RING].P, bm, rband, buf[cb ^ 1], nullptr);
             if (warp == 0 && it + 2 < n_items) ring_issue(it + 2);
             const int nsl = S.P.tile_cols >> 5;
-            const double wsum = tile_g<V, TB>(S.P, S.t, S.part * nsl / S.nparts,
-                                          (S.part + 1) * nsl / S.nparts, buf[cb],
+            const double wsum = tile_g<V, TB>(S.P, S.t, S.q0 * nsl / S.qd, S.q1 * nsl / S.qd, buf[cb],
                                           p.x + S.P.x_off, gxb + S.gx_off,
                                           red + (it & 1) * RED_DOUBLES, nullptr);
             wacc += wsum;
             // flush this warp's gg partial when the next item is another task
+            // (added: the de-phased first tile's task comes back later)
             const int k = S.k;
             if (it + 1 == n_items || ring[(it + 1) % RING].k != k) {
                 const double ws = warp_sum(wacc);
-                if (lane == 0) pgg[((int64_t)k * G + b) * WARPS + warp] = ws;
+                if (lane == 0) pgg[((int64_t)k * G + b) * WARPS + warp] += ws;
                 wacc = 0.0;
             }
             if (!dbuf && it + 1 < n_items)
@@ -1298,6 +1332,13 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
         }
     }
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 3);
+    if (p.timeline && n_tasks > 1) {   // profiling: every warp of the block done with B
+        __syncthreads();
+        if (threadIdx.x == 0) p.timeline[((int64_t)1 * 8 + 4) * gridDim.x + blockIdx.x] = gtimer();
+        if (threadIdx.x == 0) __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) p.timeline[((int64_t)1 * 8 + 7) * gridDim.x + blockIdx.x] = gtimer();
+    }
     if (p.timeline && threadIdx.x == 0 && n_tasks > 1) {   // profiling: phase-B shares
         p.timeline[((int64_t)1 * 8 + 0) * gridDim.x + blockIdx.x] = s_range_dbg[0];
         p.timeline[((int64_t)1 * 8 + 1) * gridDim.x + blockIdx.x] = s_range_dbg[1];

@@ -63,6 +63,23 @@ def main():
                         ("C per block", t[5] - t[4])):
             q = np.percentile(d, [0, 10, 50, 90, 100])
             print(f"{name:12s} min {q[0]:6.1f} p10 {q[1]:6.1f} med {q[2]:6.1f} p90 {q[3]:6.1f} max {q[4]:6.1f}")
+        if tl.shape[0] > 1:
+            t1 = tl[1]
+            allB = t1[4] - t[2]
+            fb = t1[5] - t[0]
+            ft = t1[6] - t[0]
+            for name, d in (("B all warps", allB), ("A first band", fb), ("A first tile", ft),
+                            ("B fence", t1[7] - t1[4])):
+                q = np.percentile(d, [0, 10, 50, 90, 100])
+                print(f"{name:12s} min {q[0]:6.1f} p10 {q[1]:6.1f} med {q[2]:6.1f} p90 {q[3]:6.1f} "
+                      f"max {q[4]:6.1f}")
+            if tl.shape[0] > 2:
+                ts = tl[2]
+                dd = [np.median(ts[i + 1] - ts[i]) for i in range(7) if (ts[i + 1] > 0).all()]
+                print("A tile durations (median over blocks, us):", " ".join(f"{v:.1f}" for v in dd))
+            print("B: last warp done %.1f us after the first block started B; fenced %.1f; "
+                  "barrier release %.1f" % (t1[4].max() - t[2].min(), t1[7].max() - t[2].min(),
+                                            t[4].max() - t[2].min()))
         if os.environ.get("DUMP_BLOCKS") and tl.shape[0] > 1:
             ub, ue, nst, stg = (buf[(1 * 8 + q) * G:(1 * 8 + q + 1) * G] for q in range(4))
             print("B super-tile staging per block (us):",
