@@ -71,7 +71,8 @@ constexpr size_t SMEM_BUDGET = 218 * 1024;  // dynamic shared memory per CTA (on
 struct Slot {
     cudaEvent_t done = nullptr;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
-    char *h_res = nullptr;          // pinned copy of the result block [out | mus | statuses]
+    char *h_res = nullptr;          // mapped pinned result block [out | mus | statuses],
+    char *d_hres = nullptr;         // written by the epoch's last block (device view d_hres)
     int64_t n_tasks = 0, n_visits = 0;
     bool pending = false;
     int32_t *h_plan = nullptr;      // pinned: device-sampled ids of the epoch
@@ -573,7 +574,7 @@ static UpLayout up_layout(const bct_ctx *c, int64_t nt, bool with_prep)
     L.total = L.prep + (with_prep ? (size_t)c->pd.bytes() * (size_t)nt : 0);
     return L;
 }
-constexpr size_t RES_HEAD = 64;   // EpochOut at the start of the result block
+constexpr size_t RES_HEAD = bct::RES_HEAD_BYTES;   // EpochOut at the start of the result block
 static_assert(sizeof(EpochOut) <= RES_HEAD, "result block head");
 
 int ensure_task_cap(bct_ctx *c, int64_t n)
@@ -607,7 +608,8 @@ int ensure_task_cap(bct_ctx *c, int64_t n)
     c->out = reinterpret_cast<EpochOut *>(res);
     for (int s = 0; s < RING; ++s) {
         if (c->slots[s].h_res) cudaFreeHost(c->slots[s].h_res);
-        CK(cudaHostAlloc((void **)&c->slots[s].h_res, rb, cudaHostAllocDefault));
+        CK(cudaHostAlloc((void **)&c->slots[s].h_res, rb, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer((void **)&c->slots[s].d_hres, c->slots[s].h_res, 0));
     }
     c->task_cap = cap;
     return 0;
@@ -1596,7 +1598,7 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, const Up
     p.gx_batch = c->gx_batch; p.seg_batch = c->seg_batch; p.tax_batch = c->tax_batch;
     p.zt = c->zt; p.zl_on = c->zl_on; p.zl_st = c->zl_st; p.zl_mu = c->zl_mu;
     p.part_task = c->part_task;
-    p.statuses = c->statuses; p.out = c->out;
+    p.statuses = c->statuses; p.out = c->out; p.res_host = S.d_hres;
     p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
     p.guard_ref = c->guard_ref;
     p.prep = c->d_up + L.prep;
@@ -1618,11 +1620,8 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, const Up
     bct::launch_epoch(p, c->dtype, c->grid, c->block, c->smem_total, c->stream, &e);
     if (e != cudaSuccess) return fail(c, BCT_ECUDA, "epoch launch: %s", cudaGetErrorString(e));
     CK(cudaEventRecord(S.t1, c->stream));
-    // a sharded epoch's result is copied by bct_finish_sharded (after the
-    // all-reduce); every other epoch's here
-    if (!(c->cur_flags & BCT_SHARDED))
-        CK(cudaMemcpyAsync(S.h_res, c->d_res, RES_HEAD + 12 * (size_t)n_tasks,
-                           cudaMemcpyDeviceToHost, c->stream));
+    // the last block wrote the result into the slot's mapped block (no copy
+    // on the stream); a sharded epoch's norms follow from bct_finish_sharded
     CK(cudaEventRecord(S.done, c->stream));
     S.n_tasks = n_tasks;
     S.n_visits = n_visits;
@@ -1964,19 +1963,16 @@ int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
     if (!dmask) return fail(c, BCT_EINVAL, "no sharded epoch submitted");
     const int nb = 8 * c->grid;   // c->part holds 8 * grid + 8 partials
     // flags: the epoch's BCT_GUARD / BCT_GUARD_REF (a skipped epoch skips its finish)
+    Slot &S = c->slots[(c->head + RING - 1) % RING];
     FinishGuard guard{&c->out->x_sq, c->guard_ref, c->guard_factor, (flags & BCT_GUARD) ? 1 : 0,
-                      (flags & BCT_GUARD_REF) ? 1 : 0};
+                      (flags & BCT_GUARD_REF) ? 1 : 0,
+                      S.pending ? reinterpret_cast<EpochOut *>(S.d_hres) : nullptr};
     CK(bct::sharded_finish(c->y, c->exchange, c->n_meas, c->rb_of_row, dmask, c->r, c->r32,
                            c->part, nb, c->exchange + c->n_meas, c->out, c->ticket, guard,
                            c->stream));
-    // the epoch's result block (slot of the last submitted epoch) now carries
-    // the global norms; one copy (the epoch launch skipped its own when sharded)
-    Slot &S = c->slots[(c->head + RING - 1) % RING];
-    if (S.pending) {
-        CK(cudaMemcpyAsync(S.h_res, c->d_res, RES_HEAD + 12 * (size_t)S.n_tasks,
-                           cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaEventRecord(S.done, c->stream));
-    }
+    // the epoch's mapped result block (slot of the last submitted epoch) now
+    // carries the global norms (written by the finish's last block)
+    if (S.pending) CK(cudaEventRecord(S.done, c->stream));
     if (resid_sq) {   // synchronous form
         double s = 0.0;
         CK(cudaMemcpyAsync(&s, &c->out->resid_sq, 8, cudaMemcpyDeviceToHost, c->stream));

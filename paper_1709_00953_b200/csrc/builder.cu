@@ -613,6 +613,11 @@ __global__ void sharded_finish_kernel(const double *y, const double *S, int64_t 
     out->resid_sq = s;
     out->x_sq = tail[0];
     out->err_sq = tail[1];
+    if (guard.host_out) {
+        guard.host_out->resid_sq = s;
+        guard.host_out->x_sq = tail[0];
+        guard.host_out->err_sq = tail[1];
+    }
     if (guard.set_ref) *guard.ref = fmax(sqrt(tail[0]), 1e-12);
     *ticket = 0;
 }

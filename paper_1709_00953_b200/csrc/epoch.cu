@@ -1560,7 +1560,15 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         // p.out; every block reads it before any block can pass a grid
         // barrier, and only the last block of this launch rewrites it)
         const double nx = sqrt(__ldcg(&p.out->x_sq));
-        if (!isfinite(nx) || nx > hdr.guard_factor * __ldcg(p.guard_ref)) return;
+        if (!isfinite(nx) || nx > hdr.guard_factor * __ldcg(p.guard_ref)) {
+            // skipped: the result block repeats the previous epoch's (as the
+            // device block still holds it)
+            if (blockIdx.x == 0 && p.res_host)
+                for (int q = threadIdx.x; q < (int)(sizeof(EpochOut) / 8); q += BLOCK)
+                    reinterpret_cast<double *>(p.res_host)[q] =
+                        __ldcg(reinterpret_cast<const double *>(p.out) + q);
+            return;
+        }
     }
     const int n_tasks = hdr.n_tasks;
     const bool serial = hdr.mode == 0;
@@ -2125,6 +2133,21 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             // reference |x| (sharded: the finish writes it from the global norm)
             if ((hdr.flags & 16) && !sharded) *p.guard_ref = fmax(sqrt(a1), 1e-12);
             *p.ticket = 0;
+            if (p.res_host) {   // the host's copy (mapped pinned memory)
+                EpochOut *ho = reinterpret_cast<EpochOut *>(p.res_host);
+                ho->resid_sq = p.out->resid_sq;
+                ho->x_sq = a1;
+                ho->err_sq = p.out->err_sq;
+                ho->n_degenerate = (int)nd;
+            }
+        }
+        if (p.res_host) {   // mu and status per task (written earlier in this launch)
+            double *hm = reinterpret_cast<double *>(p.res_host + bct::RES_HEAD_BYTES);
+            int32_t *hs = reinterpret_cast<int32_t *>(p.res_host + bct::RES_HEAD_BYTES + 8 * (int64_t)n_tasks);
+            for (int k = threadIdx.x; k < n_tasks; k += BLOCK) {
+                hm[k] = __ldcg(p.mus + k);
+                hs[k] = __ldcg(p.statuses + k);
+            }
         }
         if (do_commit)
             for (int lp = threadIdx.x; lp < p.n_panels_owned; lp += BLOCK) p.counts[lp] = 0;

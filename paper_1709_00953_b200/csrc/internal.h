@@ -229,6 +229,8 @@ struct EpochParams {
     double *mus;
     int32_t *statuses;
     EpochOut *out;
+    char *res_host;            // the epoch's result block in mapped pinned host memory
+                               // [EpochOut | mus | statuses], written by the last block
     double *exchange;          // sharded: n_meas partial sums + 2
     double *guard_ref;         // divergence guard: reference |x| (device scalar)
     unsigned int *bar;         // grid barrier word
@@ -247,6 +249,7 @@ struct FinishGuard {
     double *ref;               // reference |x| (written with set_ref)
     double factor;
     int32_t check, set_ref;
+    EpochOut *host_out;        // mapped result block of the epoch (norms written there too)
 };
 __device__ __forceinline__ bool guard_tripped(const FinishGuard &g)
 {
@@ -278,6 +281,7 @@ struct Box {
 };
 
 namespace bct {
+constexpr int RES_HEAD_BYTES = 64;   // EpochOut at the start of an epoch's result block
 
 // whole-system baselines (baseline.cu): A as a device CSR and CSC, global
 // measurement rows x global voxel columns, in BlockSystem.to_scipy's order
