@@ -106,6 +106,7 @@ struct bct_ctx {
     int32_t *inv_ptr = nullptr, *inv_z = nullptr, *d_rb_ptr = nullptr, *d_rb_rows = nullptr;
     int32_t *invt = nullptr, *invt_off = nullptr;   // interleaved inverse map (epoch tail)
     int32_t *rb_of_row = nullptr;
+    int32_t *cta_split = nullptr;   // per panel [grid+1]: per-task path phase-2 slice split
     double *y = nullptr, *r = nullptr, *z = nullptr, *x = nullptr, *xhat = nullptr;
     float *r32 = nullptr;   // FP32 mode: band staging copy of r (epoch kernel)
     bool r32_valid = false; // r32 == (float)r (every device writer of r keeps r32 in step;
@@ -539,6 +540,29 @@ int finalize(bct_ctx *c)
     }
     c->grid = bct::epoch_grid_size(c->dtype, c->device, c->smem_total, &c->block);
     DALLOC(c->part, 8 * (int64_t)c->grid + 8);
+    {
+        // per-task path, full-panel tasks: CTA b streams the slices whose first
+        // entry lies in [F*b/G, F*(b+1)/G) of the panel's F stored entries (a
+        // static split, tabled here instead of searched per task)
+        const int G = c->grid;
+        std::vector<int32_t> split((size_t)std::max(c->np, 1) * (G + 1), 0);
+        std::vector<int32_t> ss;
+        for (int lp = 0; lp < c->np; ++lp) {
+            const PanelDev &P = c->h_panels[lp];
+            ss.resize((size_t)P.n_slices + 1);
+            CK(cudaMemcpy(ss.data(), P.slice_start, 4 * ss.size(), cudaMemcpyDeviceToHost));
+            const int64_t F = ss[P.n_slices];
+            for (int b = 0; b <= G; ++b) {
+                const int32_t key = (int32_t)(F * b / G);
+                split[(size_t)lp * (G + 1) + b] =
+                    b == G ? P.n_slices
+                           : (int32_t)(std::lower_bound(ss.begin(), ss.begin() + P.n_slices, key) -
+                                       ss.begin());
+            }
+        }
+        DALLOC(c->cta_split, split.size());
+        CK(cudaMemcpy(c->cta_split, split.data(), 4 * split.size(), cudaMemcpyHostToDevice));
+    }
     DALLOC(c->guard_ref, 1);
     DALLOC(c->bar, 1);
     DALLOC(c->ticket, 1);
@@ -1600,6 +1624,7 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, const Up
     p.part_task = c->part_task;
     p.statuses = c->statuses; p.out = c->out; p.res_host = S.d_hres;
     p.exchange = c->exchange; p.bar = c->bar; p.ticket = c->ticket;
+    p.cta_split = c->cta_split;
     p.guard_ref = c->guard_ref;
     p.prep = c->d_up + L.prep;
     p.masks = c->cur_masks;

@@ -306,6 +306,12 @@ __device__ __forceinline__ int task_slice(const PrepView &R, const PanelDev &P, 
 #ifndef BCT_NO_FCODE_K
 #define BCT_NO_FCODE_K 0         // 1: phase B ignores the step codes (profiling)
 #endif
+#ifndef BCT_P1_PF
+#define BCT_P1_PF 0              // per-task phase 1: L2 prefetch of the CTA's streams behind the first band
+#endif
+#ifndef BCT_REFRESH_RF
+#define BCT_REFRESH_RF 4         // per-task serial refresh: z slots of a row loaded in groups of 4 (1: 2% slower, 8: 0.1%)
+#endif
 #ifndef BCT_STREAM_HINT_F64
 #define BCT_STREAM_HINT_F64 1    // f64 values (serial configs): the hint helps
 #endif
@@ -1022,6 +1028,11 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     __shared__ long long s_range_dbg[3];
     __shared__ long long s_stage_dbg;
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 0);
+    if (p.timeline && threadIdx.x == 0 && hdr.n_tasks > 3) {   // profiling: the block's SM
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.timeline[((int64_t)3 * 8 + 0) * gridDim.x + blockIdx.x] = smid;
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int G = gridDim.x, b = blockIdx.x;
     const int n_tasks = hdr.n_tasks;
@@ -1539,6 +1550,47 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
     if (!BCT_NO_TL_BATCH) TL_MARK(0, 6);
 }
 
+// Per-task phase 2a: exclusive prefix of the work units (parts_of) of slices
+// [c0, c0 + nc) of super tile st into s_upre[0..nc] (whole CTA; complete after
+// the caller's next __syncthreads)
+__device__ __forceinline__ void unit_prefix(const PanelDev &P, const PrepView &R, int m, int c0,
+                                            int nc, int st, bool rfull, int *s_upre)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < nc; i += BLOCK) {
+        const int sl = rfull ? c0 + i : task_slice(R, P, m, c0 + i, st);
+        s_upre[i] = parts_of((__ldg(P.slice_start + sl + 1) - __ldg(P.slice_start + sl)) >> 7, true);
+    }
+    __syncthreads();
+    if (warp == 0) {   // exclusive prefix, 32 slices per step
+        int carry = 0;
+        for (int b0 = 0; b0 < nc; b0 += 32) {
+            const int v = b0 + lane < nc ? s_upre[b0 + lane] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (b0 + lane < nc) s_upre[b0 + lane] = carry + incl - v;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) s_upre[nc] = carry;
+    }
+}
+
+// L2 prefetch of a byte range by one warp (bulk requests of <= 16 KB; the
+// range is widened to 16-byte granules)
+__device__ __forceinline__ void prefetch_range(const void *ptr, int64_t bytes, int lane)
+{
+    if (bytes <= 0) return;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(ptr) & ~(uintptr_t)15;
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(ptr) + bytes + 15) & ~(uintptr_t)15;
+    constexpr uintptr_t CH = 16384;
+    for (uintptr_t a = a0 + lane * CH; a < a1; a += 32 * CH)
+        prefetch_l2(reinterpret_cast<const void *>(a), (uint32_t)min((uintptr_t)CH, a1 - a));
+}
+
 template <typename V>
 __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
 {
@@ -1597,6 +1649,25 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         }
     };
     bool have_rec = false;   // loaded ahead, before the previous task's last barrier
+    // phase-1 work items: whole tiles in rounds of gridDim.x; the tiles left
+    // for the last round are split into column parts so every CTA gets the
+    // same share
+    struct Items {
+        int full, S, n;
+        __device__ Items(const PanelDev &P)
+        {
+            const int NSL = P.tile_cols >> 5, G = gridDim.x;
+            full = P.n_tiles / G;
+            const int rem = P.n_tiles - full * G;
+            S = rem > 0 ? max(1, min(NSL, G / rem)) : 1;
+            n = full + ((int)blockIdx.x < rem * S ? 1 : 0);
+        }
+        __device__ int tile(int it) const
+        {
+            return it < full ? (int)blockIdx.x + it * (int)gridDim.x
+                             : full * (int)gridDim.x + (int)blockIdx.x / S;
+        }
+    };
     for (int k = 0; k < (hdr.batched ? 0 : n_tasks); ++k) {
         if (!have_rec) {
             __syncthreads();  // the previous task's record may still be in use
@@ -1610,7 +1681,26 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         TL_MARK(k, 0);
         double2 *gx = reinterpret_cast<double2 *>(p.gx + (k & 1) * p.gx_stride);
         const double *xj = p.x + P.x_off;
+        const bool rfull = R.h->full != 0;
+        const Items items(P);
 
+        // This CTA's phase-2a slices: a full-panel task splits them by stored
+        // entries (table built at set-up, api.cu finalize: no per-task search),
+        // any other task by slice count.
+        // (CTA-uniform values kept in shared memory: registers are scarce)
+        __shared__ int s_ub, s_ue, s_pre_nc;
+        int ub, ue;
+        {
+            const int ns = R.st_pre[R.h->nst];
+            if (rfull) {
+                const int32_t *cs = p.cta_split + (int64_t)T.lp * (gridDim.x + 1) + blockIdx.x;
+                ub = __ldg(cs);
+                ue = __ldg(cs + 1);
+            } else {
+                ub = (int)((int64_t)ns * blockIdx.x / gridDim.x);
+                ue = (int)((int64_t)ns * (blockIdx.x + 1) / gridDim.x);
+            }
+        }
         // ---- phase 1: g = A_I^T r_I, tile bands in shared memory ----------
         // Work items are whole tiles in rounds of gridDim.x; the tiles left for
         // the last round are split into column parts so every CTA gets the
@@ -1619,13 +1709,8 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         double wsum = 0.0;
         {
             const int NSL = P.tile_cols >> 5;
-            const int G = gridDim.x;
-            const int full = P.n_tiles / G, rem = P.n_tiles - full * G;
-            const int S = rem > 0 ? max(1, min(NSL, G / rem)) : 1;
-            const int n_items = full + ((int)blockIdx.x < rem * S ? 1 : 0);
-            auto item_tile = [&](int it) {
-                return it < full ? (int)blockIdx.x + it * G : full * G + (int)blockIdx.x / S;
-            };
+            const int full = items.full, S = items.S, n_items = items.n;
+            auto item_tile = [&](int it) { return items.tile(it); };
             const bool dbuf = p.band_dbuf != 0;
             double *buf0 = rs, *buf1 = rs + (dbuf ? p.band_cap : 0);
             double *red = rs + (int64_t)p.band_cap * (dbuf ? 2 : 1);
@@ -1636,6 +1721,51 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 band_issue(P, bm, p.r, buf0, bmask);
                 if (n_items > 1) band_meta_load(P, item_tile(1), bm, bmask);
             }
+#if BCT_P1_PF
+            // L2 prefetch of this CTA's phase-1 streams, behind the first band
+            if (threadIdx.x < 32) {
+                for (int it = 0; it < n_items; ++it) {
+                    const int t = item_tile(it);
+                    int c0 = 0, c1 = NSL;
+                    if (it >= full) {
+                        const int part = (int)blockIdx.x % S;
+                        c0 = part * NSL / S;
+                        c1 = (part + 1) * NSL / S;
+                    }
+                    const int sb = t * NSL + c0, se = min(t * NSL + c1, P.n_cslices);
+                    if (se <= sb) continue;
+                    const int64_t e0 = __ldg(P.csl_start + sb), e1 = __ldg(P.csl_start + se);
+                    prefetch_range(static_cast<const V *>(P.tvals) + e0, (e1 - e0) * (int64_t)sizeof(V), lane);
+                    if (P.toff != nullptr) {
+                        prefetch_range(P.toff + e0, e1 - e0, lane);
+                        prefetch_range(P.tbase + (e0 >> 3), (e1 - e0) >> 2, lane);
+                    } else {
+                        prefetch_range(P.tloc + e0, (e1 - e0) * 2, lane);
+                    }
+                }
+            }
+#endif
+            // while the first band is in flight: the unit prefix of this
+            // CTA's first phase-2a chunk (plan-only).  (L2 prefetches of the
+            // CTA's phase-1 or phase-2a streams here or at the task start, and
+            // loading the next task's first band metadata before the refresh
+            // barrier, measured slower: config 2 2.1-6% per epoch)
+            // unit prefix of the first phase-2a chunk (full tasks; chunk [ub, ub + s_pre_nc))
+            {
+                int pre_nc = 0;
+                if (rfull && ue > ub) {
+                    int st = 0;
+                    while (ub >= R.st_pre[st + 1]) ++st;
+                    pre_nc = min(min(ue, R.st_pre[st + 1]) - ub, UCAP);
+                    unit_prefix(P, R, m, ub, pre_nc, st, true, s_upre);
+                }
+                if (threadIdx.x == 0) {
+                    s_ub = ub;
+                    s_ue = ue;
+                    s_pre_nc = pre_nc;
+                }
+            }
+
             int cur = 0;
             for (int it = 0; it < n_items; ++it) {
                 cp_async_wait_all();
@@ -1691,33 +1821,12 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
         // its rows complete in this CTA's slices: the CTA sums their parts
         // itself, and the grid barrier + row pass of phase 2b go away.
         const bool fused = P.n_st == 1 && P.n_seg == P.n_rows;
-        const bool rfull = R.h->full != 0;
-        int ub, ue;
         {
             const V *fv = static_cast<const V *>(P.fvals);
             double2 *spart = reinterpret_cast<double2 *>(p.seg_part);
-            const int ns = R.st_pre[R.h->nst];
-            if (rfull) {
-                __shared__ int s_lim[2];
-                if (threadIdx.x < 2) {
-                    // equal shares of stored entries (a per-slice cost as in the
-                    // batched phase B measured slower here: 13.1 -> 14.0 us)
-                    const int64_t F = __ldg(P.slice_start + P.n_slices);
-                    const int32_t key = (int32_t)(F * (blockIdx.x + threadIdx.x) / gridDim.x);
-                    int lo = 0, hi = P.n_slices;
-                    while (lo < hi) {
-                        int mid = (lo + hi) / 2;
-                        if (__ldg(P.slice_start + mid) < key) lo = mid + 1; else hi = mid;
-                    }
-                    s_lim[threadIdx.x] = (blockIdx.x + threadIdx.x == gridDim.x) ? P.n_slices : lo;
-                }
-                __syncthreads();
-                ub = s_lim[0];
-                ue = s_lim[1];
-            } else {
-                ub = (int)((int64_t)ns * blockIdx.x / gridDim.x);
-                ue = (int)((int64_t)ns * (blockIdx.x + 1) / gridDim.x);
-            }
+            ub = s_ub;
+            ue = s_ue;
+            const int pre_c0 = ub, pre_nc = s_pre_nc;
             int fu = ub;
             while (fu < ue) {
                 int st = 0;
@@ -1760,28 +1869,8 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 }
                 for (int c0 = fu; c0 < ge; c0 += UCAP) {
                     const int nc = min(ge - c0, UCAP);
-                    for (int i = threadIdx.x; i < nc; i += BLOCK) {
-                        const int sl = rfull ? c0 + i : task_slice(R, P, m, c0 + i, st);
-                        s_upre[i] = parts_of((__ldg(P.slice_start + sl + 1) -
-                                              __ldg(P.slice_start + sl)) >> 7, true);
-                    }
-                    __syncthreads();
-                    if (warp == 0) {   // exclusive prefix, 32 slices per step
-                        int carry = 0;
-                        for (int b0 = 0; b0 < nc; b0 += 32) {
-                            const int v = b0 + lane < nc ? s_upre[b0 + lane] : 0;
-                            int incl = v;
-#pragma unroll
-                            for (int o = 1; o < 32; o <<= 1) {
-                                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                                if (lane >= o) incl += y;
-                            }
-                            if (b0 + lane < nc) s_upre[b0 + lane] = carry + incl - v;
-                            carry += __shfl_sync(0xffffffffu, incl, 31);
-                        }
-                        if (lane == 0) s_upre[nc] = carry;
-                    }
-                    __syncthreads();
+                    if (c0 != pre_c0 || nc != pre_nc) unit_prefix(P, R, m, c0, nc, st, rfull, s_upre);
+                    __syncthreads();   // (the staged (g, x) too)
                     const int total = s_upre[nc];
                     for (int u = warp; u < total; u += WARPS) {
                         int lo = 0, hi = nc - 1;   // last slice whose units start <= u
@@ -1935,22 +2024,36 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 }
                 const int i = s_vb[lo];
                 const bool cur = mask_has(tmask, i);
-                const int g = p.rb_rows[p.rb_ptr[i] + (f - s_vpre[lo])];
+                const int g = __ldg(p.rb_rows + __ldg(p.rb_ptr + i) + (f - s_vpre[lo]));
+                const int e1 = __ldg(p.inv_ptr + g + 1);
+                const double yg = __ldg(p.y + g);
                 double acc = 0.0;
-                for (int e = p.inv_ptr[g]; e < p.inv_ptr[g + 1]; ++e) {
-                    const int off = p.inv_z[e];
-                    BCT_ASSERT(off >= 0 && off < p.z_len);
-                    double v;
-                    if (cur && off >= zlo && off < zhi) {
-                        const double2 qq = tax[off - zlo];
-                        v = z_value(qq.x, qq.y, mu, status);
-                        p.z[off] = v;
-                    } else {
-                        v = p.z[off];
+                // the row's z slots (ascending j) in groups of RF: their
+                // offsets, then their values, in flight together
+                constexpr int RF = BCT_REFRESH_RF;
+                for (int e = __ldg(p.inv_ptr + g); e < e1; e += RF) {
+                    int off[RF];
+                    double v[RF];
+#pragma unroll
+                    for (int u = 0; u < RF; ++u) off[u] = e + u < e1 ? __ldg(p.inv_z + e + u) : -1;
+#pragma unroll
+                    for (int u = 0; u < RF; ++u) {
+                        BCT_ASSERT(off[u] < p.z_len);
+                        if (off[u] < 0) {
+                            v[u] = 0.0;
+                        } else if (cur && off[u] >= zlo && off[u] < zhi) {
+                            const double2 qq = tax[off[u] - zlo];
+                            v[u] = z_value(qq.x, qq.y, mu, status);
+                            p.z[off[u]] = v[u];
+                        } else {
+                            v[u] = __ldcg(p.z + off[u]);
+                        }
                     }
-                    acc += v;
+#pragma unroll
+                    for (int u = 0; u < RF; ++u)
+                        if (off[u] >= 0) acc += v[u];
                 }
-                const double rv = p.y[g] - acc;
+                const double rv = yg - acc;
                 p.r[g] = rv;
                 if (p.r32) p.r32[g] = (float)rv;
             }
