@@ -238,7 +238,8 @@ int bct_wait_epoch(bct_ctx *ctx, bct_epoch_result *out, double *mus, int32_t *st
  * n_meas partial projection sums followed by x_sq and err_sq. */
 int bct_exchange_buffer(bct_ctx *ctx, double **dev_ptr, int64_t *len);
 /* Profiling only: per-block phase timestamps of the last epoch when the
- * environment sets BCT_TIMELINE=1 ([task][6][grid] globaltimer ns). */
+ * environment sets BCT_TIMELINE=1 ([2][task][8][grid] globaltimer ns: phase
+ * marks, then per-task sub-phase marks; out holds 16 * n_tasks * grid). */
 int bct_debug_timeline(bct_ctx *ctx, long long *out, int64_t n_tasks, int32_t *grid);
 /* After the all-reduce of the exchange buffer (enqueued on the context's
  * stream): r = y - S on the drawn rows; the last epoch's result (bct_wait_epoch)

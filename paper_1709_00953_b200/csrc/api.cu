@@ -177,7 +177,7 @@ struct bct_ctx {
     int32_t *d_plan = nullptr;
     int64_t d_plan_n = 0;
     std::vector<void *> allocs;
-    long long *timeline = nullptr;    // BCT_TIMELINE=1: [task][8][grid] globaltimer stamps
+    long long *timeline = nullptr;    // BCT_TIMELINE=1: [2][task][8][grid] globaltimer stamps
     int64_t timeline_tasks = 0;
 };
 
@@ -1635,10 +1635,11 @@ static int launch_staged(bct_ctx *c, int64_t n_tasks, int64_t n_visits, const Up
     if (getenv("BCT_TIMELINE") && n_tasks > 0) {
         if (c->timeline_tasks < n_tasks) {
             if (c->timeline) cudaFree(c->timeline);
-            CK(cudaMalloc((void **)&c->timeline, 8 * 8 * (size_t)n_tasks * c->grid));
+            CK(cudaMalloc((void **)&c->timeline, 8 * 16 * (size_t)n_tasks * c->grid));
             c->timeline_tasks = n_tasks;
         }
         p.timeline = c->timeline;
+        p.tl_tasks = c->timeline_tasks;
     }
     CK(cudaEventRecord(S.t0, c->stream));
     cudaError_t e;
@@ -1957,7 +1958,8 @@ int bct_wait_epoch(bct_ctx *c, bct_epoch_result *o, double *mus, int32_t *status
     return 0;
 }
 
-// Profiling: phase timestamps of the last epoch (BCT_TIMELINE=1), [task][8][grid].
+// Profiling: phase timestamps of the last epoch (BCT_TIMELINE=1), [2][task][8][grid]
+// (the second half: per-task sub-phase marks); out holds 16 * n_tasks * grid.
 int bct_debug_timeline(bct_ctx *c, long long *out, int64_t n_tasks, int32_t *grid)
 {
     if (!c || !grid) return BCT_EINVAL;
@@ -1965,7 +1967,9 @@ int bct_debug_timeline(bct_ctx *c, long long *out, int64_t n_tasks, int32_t *gri
     *grid = c->grid;
     if (!c->timeline || !out) return 0;
     CK(cudaStreamSynchronize(c->stream));
-    CK(cudaMemcpy(out, c->timeline, 8 * 8 * (size_t)std::min(n_tasks, c->timeline_tasks) * c->grid,
+    const size_t nt = (size_t)std::min(n_tasks, c->timeline_tasks), half = 8 * nt * c->grid;
+    CK(cudaMemcpy(out, c->timeline, 8 * half, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out + half, c->timeline + 8 * (size_t)c->timeline_tasks * c->grid, 8 * half,
                   cudaMemcpyDeviceToHost));
     return 0;
 }

@@ -110,6 +110,15 @@ __device__ __forceinline__ long long gtimer()
             p.timeline[((int64_t)(k) * 8 + (ph)) * gridDim.x + blockIdx.x] = gtimer(); \
     } while (0)
 
+// per-task sub-phase marks: second half of the timeline, [task][8][block]
+// (p.tl_tasks = tasks the buffer holds)
+#define TL_MARK2(k, ph)                                                               \
+    do {                                                                              \
+        if (p.timeline && threadIdx.x == 0)                                           \
+            p.timeline[(((int64_t)p.tl_tasks + (k)) * 8 + (ph)) * gridDim.x + blockIdx.x] = \
+                gtimer();                                                             \
+    } while (0)
+
 __device__ __forceinline__ void grid_sync(unsigned int *bar)
 {
     __syncthreads();
@@ -1790,6 +1799,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                     __syncthreads();
                 }
                 wsum += tile_g<V>(P, t, c0, c1, bt, xj, gx, red, bmask != nullptr ? vr_s : nullptr);
+                if (it == 0) TL_MARK2(k, 0);   // profiling: first item computed
 
                 __syncthreads();
                 if (dbuf) {
@@ -1871,6 +1881,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                     const int nc = min(ge - c0, UCAP);
                     if (c0 != pre_c0 || nc != pre_nc) unit_prefix(P, R, m, c0, nc, st, rfull, s_upre);
                     __syncthreads();   // (the staged (g, x) too)
+                    if (c0 == ub) TL_MARK2(k, 1);   // profiling: super tile staged
                     const int total = s_upre[nc];
                     for (int u = warp; u < total; u += WARPS) {
                         int lo = 0, hi = nc - 1;   // last slice whose units start <= u
@@ -1907,6 +1918,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             }
         }
         TL_MARK(k, 3);
+        TL_MARK2(k, 2);
         const int n_task_rows = R.pre[R.h->n_runs];
         wsum = 0.0;
         if (fused) {
@@ -1997,6 +2009,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 xh[d] += xn;
             }
         }
+        TL_MARK2(k, 3);   // profiling: mu, xhat done
         const bool last_of_visit = (T.flags & TASK_LAST_OF_VISIT) != 0;
         const bool refresh = serial && last_of_visit;
         if (!refresh) {   // (the refresh below stores this task's z itself)
@@ -2057,6 +2070,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 p.r[g] = rv;
                 if (p.r32) p.r32[g] = (float)rv;
             }
+            TL_MARK2(k, 4);   // profiling: refresh done (this block)
             if (k + 1 < n_tasks) {
                 // this task's record is no longer read: load the next task's
                 // while the other CTAs finish their refresh (it depends on
@@ -2064,6 +2078,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 __syncthreads();
                 load_record(k + 1);
                 have_rec = true;
+                TL_MARK2(k, 5);
                 grid_sync(p.bar);
             }
         }

@@ -236,6 +236,7 @@ struct EpochParams {
     unsigned int *bar;         // grid barrier word
     unsigned int *ticket;      // last-block counter
     long long *timeline;       // optional phase timestamps (BCT_TIMELINE=1)
+    int64_t tl_tasks;          // tasks per half of the timeline buffer
     const int32_t *cta_split;  // per owned panel [grid+1]: phase-2a slice split (full tasks)
     const char *prep;          // per-task path: host-built records (hdr.host_prep), prep_dims.bytes() apart
 };

@@ -46,7 +46,7 @@ def main():
         res = wait(s, packed.task_j.size)[0]
     nt = packed.task_j.size
     grid = ctypes.c_int32()
-    buf = np.zeros(8 * nt * 4096, dtype=np.int64)
+    buf = np.zeros(16 * nt * 4096, dtype=np.int64)
     N.check(N.load().bct_debug_timeline(s.ctx, N.ptr(buf), nt, ctypes.byref(grid)), s.ctx)
     G = grid.value
     tl = buf[:nt * 8 * G].reshape(nt, 8, G).astype(np.float64) / 1e3  # us
@@ -114,6 +114,21 @@ def main():
     for name, d in (("p1 per block", d1), ("p2a per block", d2)):
         q = np.percentile(d, [0, 10, 50, 90, 100])
         print(f"{name:14s} min {q[0]:6.1f} p10 {q[1]:6.1f} med {q[2]:6.1f} p90 {q[3]:6.1f} max {q[4]:6.1f}")
+    # sub-phases per block (second half of the buffer): median / max over blocks and tasks
+    x = buf[nt * 8 * G:2 * nt * 8 * G].reshape(nt, 8, G).astype(np.float64) / 1e3
+    parts = [("band staged", tl[:, 7] - tl[:, 0]), ("first item", x[:, 0] - tl[:, 7]),
+             ("p1 rest+sum", tl[:, 1] - x[:, 0]), ("bar1 wait", tl[:, 2] - tl[:, 1]),
+             ("2a stage", x[:, 1] - tl[:, 2]), ("2a units", tl[:, 3] - x[:, 1]),
+             ("rows", tl[:, 4] - tl[:, 3]), ("bar2+sums", tl[:, 5] - tl[:, 4]),
+             ("mu, xhat", x[:, 3] - tl[:, 5]), ("refresh", x[:, 4] - x[:, 3]),
+             ("record", x[:, 5] - x[:, 4]), ("bar3 wait", tl[1:, 0] - x[:-1, 5])]
+    print("sub-phase (us per block, tasks pooled)   p10    med    p90    max")
+    for name, d in parts:
+        d = d.ravel()
+        d = d[(d > -1) & (d < 1e4)]
+        if d.size:
+            q = np.percentile(d, [10, 50, 90, 100])
+            print(f"  {name:14s} " + " ".join(f"{v:6.2f}" for v in q))
     k = 0
     d2k = tl[k, 3, :] - tl[k, 2, :]
     print("task 0 p2a by block (every 8th):", " ".join(f"{v:.0f}" for v in d2k[::8]))
