@@ -45,7 +45,7 @@ cudaError_t audit(const double *, const double *, const double *, int64_t, unsig
                   cudaStream_t);
 cudaError_t commit(const PanelDev *, int, int32_t *, double *, double *, cudaStream_t);
 cudaError_t sharded_finish(const double *, const double *, int64_t, const int32_t *,
-                           const uint64_t *, double *, float *, double *, int, const double *,
+                           const uint64_t *, int, double *, float *, double *, int, const double *,
                            EpochOut *, unsigned int *, const FinishGuard &, cudaStream_t);
 }  // namespace bct
 
@@ -1996,7 +1996,7 @@ int bct_finish_sharded(bct_ctx *c, int32_t flags, double *resid_sq)
     FinishGuard guard{&c->out->x_sq, c->guard_ref, c->guard_factor, (flags & BCT_GUARD) ? 1 : 0,
                       (flags & BCT_GUARD_REF) ? 1 : 0,
                       S.pending ? reinterpret_cast<EpochOut *>(S.d_hres) : nullptr};
-    CK(bct::sharded_finish(c->y, c->exchange, c->n_meas, c->rb_of_row, dmask, c->r, c->r32,
+    CK(bct::sharded_finish(c->y, c->exchange, c->n_meas, c->rb_of_row, dmask, c->m, c->r, c->r32,
                            c->part, nb, c->exchange + c->n_meas, c->out, c->ticket, guard,
                            c->stream));
     // the epoch's mapped result block (slot of the last submitted epoch) now

@@ -539,47 +539,69 @@ __global__ void commit_kernel(const PanelDev *panels, int np, int32_t *counts, d
 // result: |y - S|^2 (block order, like the host sum it replaces), |x|^2 and
 // |x_t - x|^2 from the all-reduced exchange tail.
 constexpr int FIN_U = 4;
-__global__ void sharded_finish_kernel(const double *y, const double *S, int64_t n,
-                                      const int32_t *rb_of_row, const uint64_t *mask, double *r,
-                                      float *r32, double *part, const double *tail,
+template <int U>
+__global__ void __launch_bounds__(256, 4) sharded_finish_kernel(const double *y, const double *S, int64_t n,
+                                      const int32_t *rb_of_row, const uint64_t *mask, int m,
+                                      double *r, float *r32, double *part, const double *tail,
                                       EpochOut *out, unsigned int *ticket, FinishGuard guard)
 {
     if (guard_tripped(guard)) return;   // the epoch was skipped: r and the result stay
     __shared__ double sh[32];
     __shared__ bool is_last;
+    __shared__ int s_partial;
+    // every row block drawn (full-panel plans): no per-row block lookup
+    if (threadIdx.x == 0) s_partial = 0;
+    __syncthreads();
+    for (int w = threadIdx.x; w < (m + 63) / 64; w += blockDim.x) {
+        const int nbits = min(64, m - 64 * w);
+        const uint64_t want = nbits == 64 ? ~0ull : ((1ull << nbits) - 1);
+        if ((__ldg(mask + w) & want) != want) s_partial = 1;
+    }
+    __syncthreads();
+    const bool partial = s_partial != 0;
     double acc = 0.0;
-    // one wave of blocks; each thread takes FIN_U pairs of consecutive rows
-    // per round (16-byte loads of y and S, all issued before the stores)
+    // one wave of blocks; each thread takes U pairs of consecutive rows per
+    // round (16-byte loads of y and S, all issued before the stores)
     auto row = [&](int64_t g, double d, int rb) {
-        if (rb >= 0 && ((__ldg(mask + (rb >> 6)) >> (rb & 63)) & 1ull)) {
+        if (!partial || (rb >= 0 && ((__ldg(mask + (rb >> 6)) >> (rb & 63)) & 1ull))) {
             r[g] = d;
             if (r32) r32[g] = (float)d;   // FP32 mode's band copy stays in step
         }
         acc = fma(d, d, acc);
     };
     const int64_t npair = n >> 1;
-    const int64_t step = (int64_t)gridDim.x * blockDim.x * FIN_U;
-    for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x * FIN_U + threadIdx.x; q0 < npair; q0 += step) {
-        double2 d[FIN_U];
-        int2 rb[FIN_U];
+    const int64_t step = (int64_t)gridDim.x * blockDim.x * U;
+    for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; q0 < npair; q0 += step) {
+        double2 d[U];
+        int2 rb[U];
 #pragma unroll
-        for (int u = 0; u < FIN_U; ++u) {
+        for (int u = 0; u < U; ++u) {
             const int64_t q = q0 + (int64_t)u * blockDim.x;
             if (q < npair) {
                 const double2 yy = __ldg(reinterpret_cast<const double2 *>(y) + q);
                 const double2 ss = __ldcg(reinterpret_cast<const double2 *>(S) + q);
                 d[u] = make_double2(yy.x - ss.x, yy.y - ss.y);
-                rb[u] = __ldg(reinterpret_cast<const int2 *>(rb_of_row) + q);
+                rb[u] = partial ? __ldg(reinterpret_cast<const int2 *>(rb_of_row) + q) : make_int2(0, 0);
             } else {
                 d[u] = make_double2(0.0, 0.0);
                 rb[u] = make_int2(-1, -1);
             }
         }
 #pragma unroll
-        for (int u = 0; u < FIN_U; ++u) {
+        for (int u = 0; u < U; ++u) {
             const int64_t q = q0 + (int64_t)u * blockDim.x;
-            row(2 * q, d[u].x, rb[u].x);
-            row(2 * q + 1, d[u].y, rb[u].y);
+            if (q >= npair) continue;
+            if (r32 && (!partial || (rb[u].x >= 0 && rb[u].x == rb[u].y &&
+                                     ((__ldg(mask + (rb[u].x >> 6)) >> (rb[u].x & 63)) & 1ull)))) {
+                // both rows stored: one 16-byte r and one 8-byte r32 store
+                reinterpret_cast<double2 *>(r)[q] = d[u];
+                reinterpret_cast<float2 *>(r32)[q] = make_float2((float)d[u].x, (float)d[u].y);
+                acc = fma(d[u].x, d[u].x, acc);
+                acc = fma(d[u].y, d[u].y, acc);
+            } else {
+                row(2 * q, d[u].x, rb[u].x);
+                row(2 * q + 1, d[u].y, rb[u].y);
+            }
         }
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)   // odd last row
@@ -810,24 +832,32 @@ cudaError_t commit(const PanelDev *panels, int np, int32_t *counts, double *x, d
 }
 
 cudaError_t sharded_finish(const double *y, const double *S, int64_t n, const int32_t *rb_of_row,
-                           const uint64_t *mask, double *r, float *r32, double *part, int nb,
+                           const uint64_t *mask, int m, double *r, float *r32, double *part, int nb,
                            const double *tail, EpochOut *out, unsigned int *ticket,
                            const FinishGuard &guard, cudaStream_t s)
 {
-    // FIN_U row pairs per thread and round, one wave of resident blocks, at
-    // most nb blocks (the partials array's size)
-    static int wave = 0;
+    // U row pairs per thread and round, one wave of resident blocks, at most
+    // nb blocks (the partials array's size)
+    static int wave = 0, U = FIN_U;
     if (wave == 0) {
         int dev = 0, sms = 148, per = 4;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sharded_finish_kernel, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sharded_finish_kernel<FIN_U>, 256, 0);
         wave = std::max(1, sms * std::max(per, 1));
+        if (const char *e = getenv("BCT_FIN_U")) U = atoi(e) == 1 ? 1 : atoi(e) == 2 ? 2 : 4;
     }
     nb = (int)std::min<int64_t>(std::min(nb, wave),
-                                std::max<int64_t>(1, (n / 2 + 256 * FIN_U - 1) / (256 * FIN_U)));
-    sharded_finish_kernel<<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, r, r32, part, tail, out,
-                                             ticket, guard);
+                                std::max<int64_t>(1, (n / 2 + 256 * U - 1) / (256 * U)));
+    if (U == 1)
+        sharded_finish_kernel<1><<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, m, r, r32, part, tail,
+                                                    out, ticket, guard);
+    else if (U == 2)
+        sharded_finish_kernel<2><<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, m, r, r32, part, tail,
+                                                    out, ticket, guard);
+    else
+        sharded_finish_kernel<4><<<nb, 256, 0, s>>>(y, S, n, rb_of_row, mask, m, r, r32, part, tail,
+                                                    out, ticket, guard);
     return cudaGetLastError();
 }
 
