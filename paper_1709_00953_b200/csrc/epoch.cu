@@ -321,6 +321,9 @@ __device__ __forceinline__ int task_slice(const PrepView &R, const PanelDev &P, 
 #ifndef BCT_REFRESH_RF
 #define BCT_REFRESH_RF 4         // per-task serial refresh: z slots of a row loaded in groups of 4 (1: 2% slower, 8: 0.1%)
 #endif
+#ifndef BCT_B_ROT
+#define BCT_B_ROT 1              // batched phase B: a share's last (partial) row-block group visited first
+#endif
 #ifndef BCT_STREAM_HINT_F64
 #define BCT_STREAM_HINT_F64 1    // f64 values (serial configs): the hint helps
 #endif
@@ -1235,7 +1238,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                 const int k = task_of(p.tasks, n_tasks, 1, fu);
                 ring[0].k = k;
                 ring[0].P = p.panels[p.tasks[k].lp];
-                s_next = fu;
+                s_next = 0;
             }
             __syncthreads();
             const PanelDev &P = ring[0].P;
@@ -1251,9 +1254,30 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             const double2 *gx = gxb + T.gx_off;
             ++dbg_segs;
             const long long tst0 = p.timeline ? gtimer() : 0;
+            // Visit order of [fu, ge): the part from the start of its last
+            // (super tile, row block) group first, then the rest.  Groups are
+            // stored longest slice first, so a share that ends inside a group
+            // would otherwise take that group's longest slices last, and the
+            // warp holding the last one would finish long after the others.
+            __shared__ int s_cut;
+            if (threadIdx.x == 0) {
+                int cut = fu;
+                if (BCT_B_ROT) {
+                    const int32_t *g = P.stbs + st * (m + 1);
+                    int lo = 0, hi = m;   // last group start < ge
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (T.slice_pre + __ldg(g + mid) < ge) lo = mid; else hi = mid - 1;
+                    }
+                    cut = max(fu, T.slice_pre + __ldg(g + lo));
+                }
+                s_cut = cut;
+            }
             stage_gx(gs, gx + v0, v1 - v0, P.swz_shift);
             __syncthreads();
             if (p.timeline) dbg_stage += gtimer() - tst0;   // profiling: super-tile staging
+            const int n_hi = ge - s_cut, cut = s_cut;
+            auto pos = [&](int gq) { return gq < n_hi ? cut + gq : fu + (gq - n_hi); };
             const V *fv = static_cast<const V *>(P.fvals);
             PT *spart = segb + T.seg_off;
             const int wst = P.st_h > 0 ? (v1 - v0) / P.st_h : 1;   // step-coded row length
@@ -1264,10 +1288,11 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             // current one is processed: short slices (rays across the strip)
             // would otherwise pay the counter, slice_start and fq0 round trips
             // back to back before their first stream load.
-            auto grab = [&]() {
+            auto grab = [&]() {   // next visit position (ge: done)
                 int g = 0;
                 if (lane == 0) g = atomicAdd(&s_next, 1);
-                return __shfl_sync(0xffffffffu, g, 0);
+                g = __shfl_sync(0xffffffffu, g, 0);
+                return g < ge - fu ? pos(g) : ge;
             };
             const bool coded = P.fcode != nullptr && !BCT_NO_FCODE_K;
             int f = grab();
@@ -1295,7 +1320,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
                     if (coded) nhdr = __ldg(P.fq0 + (int64_t)sn * 32 + lane);
                     ndst = dst_of(sn);
                 }
-                if (BCT_B_PREFETCH > 0 && lane == 0 && f + BCT_B_PREFETCH < ge) {
+                if (BCT_B_PREFETCH > 0 && lane == 0 && f + BCT_B_PREFETCH < (f >= cut ? ge : cut)) {
                     // the slice another warp takes next round: into L2 now
                     const int sp = sl + BCT_B_PREFETCH;
                     const int e0 = __ldg(P.slice_start + sp), e1 = __ldg(P.slice_start + sp + 1);
