@@ -315,14 +315,14 @@ __device__ __forceinline__ int task_slice(const PrepView &R, const PanelDev &P, 
 #ifndef BCT_NO_FCODE_K
 #define BCT_NO_FCODE_K 0         // 1: phase B ignores the step codes (profiling)
 #endif
-#ifndef BCT_P1_PF
-#define BCT_P1_PF 0              // per-task phase 1: L2 prefetch of the CTA's streams behind the first band
-#endif
 #ifndef BCT_REFRESH_RF
 #define BCT_REFRESH_RF 4         // per-task serial refresh: z slots of a row loaded in groups of 4 (1: 2% slower, 8: 0.1%)
 #endif
 #ifndef BCT_B_ROT
 #define BCT_B_ROT 1              // batched phase B: a share's last (partial) row-block group visited first
+#endif
+#ifndef BCT_REFRESH_ALL
+#define BCT_REFRESH_ALL 1        // per-task serial refresh of every row: interleaved inverse map
 #endif
 #ifndef BCT_STREAM_HINT_F64
 #define BCT_STREAM_HINT_F64 1    // f64 values (serial configs): the hint helps
@@ -1613,18 +1613,6 @@ __device__ __forceinline__ void unit_prefix(const PanelDev &P, const PrepView &R
     }
 }
 
-// L2 prefetch of a byte range by one warp (bulk requests of <= 16 KB; the
-// range is widened to 16-byte granules)
-__device__ __forceinline__ void prefetch_range(const void *ptr, int64_t bytes, int lane)
-{
-    if (bytes <= 0) return;
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(ptr) & ~(uintptr_t)15;
-    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(ptr) + bytes + 15) & ~(uintptr_t)15;
-    constexpr uintptr_t CH = 16384;
-    for (uintptr_t a = a0 + lane * CH; a < a1; a += 32 * CH)
-        prefetch_l2(reinterpret_cast<const void *>(a), (uint32_t)min((uintptr_t)CH, a1 - a));
-}
-
 template <typename V>
 __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
 {
@@ -1755,30 +1743,6 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
                 band_issue(P, bm, p.r, buf0, bmask);
                 if (n_items > 1) band_meta_load(P, item_tile(1), bm, bmask);
             }
-#if BCT_P1_PF
-            // L2 prefetch of this CTA's phase-1 streams, behind the first band
-            if (threadIdx.x < 32) {
-                for (int it = 0; it < n_items; ++it) {
-                    const int t = item_tile(it);
-                    int c0 = 0, c1 = NSL;
-                    if (it >= full) {
-                        const int part = (int)blockIdx.x % S;
-                        c0 = part * NSL / S;
-                        c1 = (part + 1) * NSL / S;
-                    }
-                    const int sb = t * NSL + c0, se = min(t * NSL + c1, P.n_cslices);
-                    if (se <= sb) continue;
-                    const int64_t e0 = __ldg(P.csl_start + sb), e1 = __ldg(P.csl_start + se);
-                    prefetch_range(static_cast<const V *>(P.tvals) + e0, (e1 - e0) * (int64_t)sizeof(V), lane);
-                    if (P.toff != nullptr) {
-                        prefetch_range(P.toff + e0, e1 - e0, lane);
-                        prefetch_range(P.tbase + (e0 >> 3), (e1 - e0) >> 2, lane);
-                    } else {
-                        prefetch_range(P.tloc + e0, (e1 - e0) * 2, lane);
-                    }
-                }
-            }
-#endif
             // while the first band is in flight: the unit prefix of this
             // CTA's first phase-2a chunk (plan-only).  (L2 prefetches of the
             // CTA's phase-1 or phase-2a streams here or at the task start, and
@@ -2054,7 +2018,49 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             const int nvb = R.h->nvb, tot = s_vpre[nvb];
             const double2 *tax = reinterpret_cast<const double2 *>(p.t_ax);
             const int64_t zlo = P.row_off, zhi = P.row_off + P.n_rows;
-            for (int f = gtid; f < tot; f += nthreads) {
+            // every row block drawn and in the task's group (full-panel serial
+            // visits): every measurement is refreshed, so walk them in order
+            // through the interleaved inverse map (coalesced slot lists, the
+            // same ascending-j fold) instead of block -> row -> list lookups
+            const bool all_rows = BCT_REFRESH_ALL && R.h->full && nvb == m && tot == p.n_meas;
+            if (all_rows) {
+                const int64_t n_pad = (p.n_meas + 31) & ~31ll;
+                for (int64_t g = gtid; g < n_pad; g += nthreads) {
+                    const int64_t G = g >> 5;
+                    const int e0 = __ldg(p.invt_off + G), e1 = __ldg(p.invt_off + G + 1);
+                    const double yg = g < p.n_meas ? __ldg(p.y + g) : 0.0;
+                    double acc = 0.0;
+                    constexpr int RF = BCT_REFRESH_RF;
+                    for (int e = e0 + (int)(g & 31); e < e1; e += 32 * RF) {
+                        int off[RF];
+                        double v[RF];
+#pragma unroll
+                        for (int u = 0; u < RF; ++u)
+                            off[u] = e + 32 * u < e1 ? __ldg(p.invt + e + 32 * u) : -1;
+#pragma unroll
+                        for (int u = 0; u < RF; ++u) {
+                            BCT_ASSERT(off[u] < p.z_len);
+                            if (off[u] < 0) {
+                                v[u] = 0.0;
+                            } else if (off[u] >= zlo && off[u] < zhi) {
+                                const double2 qq = tax[off[u] - zlo];
+                                v[u] = z_value(qq.x, qq.y, mu, status);
+                                p.z[off[u]] = v[u];
+                            } else {
+                                v[u] = __ldcg(p.z + off[u]);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < RF; ++u)
+                            if (off[u] >= 0) acc += v[u];
+                    }
+                    if (g >= p.n_meas) continue;
+                    const double rv = yg - acc;
+                    p.r[g] = rv;
+                    if (p.r32) p.r32[g] = (float)rv;
+                }
+            }
+            for (int f = all_rows ? tot : gtid; f < tot; f += nthreads) {
                 int lo = 0, hi = nvb - 1;   // last drawn block with prefix <= f
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
