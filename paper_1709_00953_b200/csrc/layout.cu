@@ -921,6 +921,10 @@ int layout_panel_v2(int dtype, int m, int32_t n_rows, int32_t n_cols, int64_t nn
         LCK(cudaMemsetAsync(slice_len + n_slices, 0, 4, s));
         LCK(scan_i32(slice_len, slice_start, n_slices + 1, false, tmp, s));
         fwd_cap = read1(slice_start + n_slices, s);
+        if (getenv("BCT_VERBOSE"))
+            fprintf(stderr, "forward store: %lld entries in %d slices for %lld stored (%.2f%% padding)\n",
+                    (long long)fwd_cap, n_slices, (long long)nnz,
+                    nnz > 0 ? 100.0 * ((double)fwd_cap / (double)nnz - 1.0) : 0.0);
     } else {
         LCK(cudaMemsetAsync(slice_start, 0, 4, s));
     }
