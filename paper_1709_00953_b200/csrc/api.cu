@@ -2190,17 +2190,35 @@ int bct_baseline_epoch(bct_ctx *c, double omega, double *norms4)
     DEVICE_GUARD(c);
     if (c->bl_kind < 0) return fail(c, BCT_EINVAL, "bct_baseline_init first");
     if (!(omega > 0.0) || !std::isfinite(omega)) return fail(c, BCT_EINVAL, "omega %g", omega);
+    // a block whose ids form one range [lo, hi) is passed as that range (the
+    // kernels then find its entries by binary search), else lo = -1
+    auto id_range = [](const int64_t *ids, int64_t n, int32_t &lo, int32_t &hi) {
+        lo = -1;
+        hi = -1;
+        if (n <= 0) return;
+        const int64_t a = *std::min_element(ids, ids + n), b = *std::max_element(ids, ids + n);
+        if (b - a + 1 == n && b < INT32_MAX) {   // ids are distinct
+            lo = (int32_t)a;
+            hi = (int32_t)(b + 1);
+        }
+    };
     if (c->bl_kind == BCT_ROW_ACTION) {
-        for (int i = 0; i < c->m; ++i)   // row blocks in partition order
+        for (int i = 0; i < c->m; ++i) {   // row blocks in partition order
+            int32_t lo, hi;
+            id_range(c->rb_rows.data() + c->rb_ptr[i], c->rb_ptr[i + 1] - c->rb_ptr[i], lo, hi);
             CK(bct::baseline_row_block(c->bm, c->d_rb_rows + c->rb_ptr[i],
-                                       c->rb_ptr[i + 1] - c->rb_ptr[i], i, c->rb_of_row, omega,
-                                       c->y, c->bl_diag, c->bl_tmp, c->bl_x, c->stream));
+                                       c->rb_ptr[i + 1] - c->rb_ptr[i], i, lo, hi, c->rb_of_row,
+                                       omega, c->y, c->bl_diag, c->bl_tmp, c->bl_x, c->stream));
+        }
     } else {
-        for (int j = 0; j < c->n_panels; ++j)   // volume blocks in partition order
+        for (int j = 0; j < c->n_panels; ++j) {   // volume blocks in partition order
+            int32_t lo, hi;
+            id_range(c->col_vox.data() + c->col_ptr[j], c->col_ptr[j + 1] - c->col_ptr[j], lo, hi);
             CK(bct::baseline_col_block(c->bm, c->bl_col_vox + c->col_ptr[j],
-                                       c->col_ptr[j + 1] - c->col_ptr[j], j, c->bl_cb_of_vox,
-                                       omega, c->bl_diag, c->bl_tmp, c->bl_x, c->bl_r,
-                                       c->stream));
+                                       c->col_ptr[j + 1] - c->col_ptr[j], j, lo, hi,
+                                       c->bl_cb_of_vox, omega, c->bl_diag, c->bl_tmp, c->bl_x,
+                                       c->bl_r, c->stream));
+        }
     }
     CK(bct::baseline_norms(c->bm, c->y, c->bl_r, c->bl_x, c->has_x_true ? c->x_true : nullptr,
                            c->d_gvox, c->x_len, c->bl_kind == BCT_COLUMN_ACTION, c->bl_part,

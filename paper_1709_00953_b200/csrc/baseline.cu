@@ -134,16 +134,35 @@ __global__ void ra_res_k(const int64_t *row_ptr, const int32_t *col, const doubl
 
 // row action, step 2: x[c] += w * sum over the block's rows (ascending) of
 // A[g, c] res[g]  (csc_matvec of A_I^T: rows of A_I in order, from 0.0)
+// First entry in [a, b) of a sorted index list with idx >= key.
+__device__ __forceinline__ int64_t lb_idx(const int32_t *idx, int64_t a, int64_t b, int32_t key)
+{
+    while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (idx[mid] < key) a = mid + 1; else b = mid;
+    }
+    return a;
+}
+
+// (g_lo >= 0: the block's rows are the id range [g_lo, g_hi), so a column's
+// entries of the block are one run of its row-sorted list, found by binary
+// search -- O(entries of the block) per pass instead of the whole matrix)
 __global__ void ra_upd_k(const int64_t *col_ptr, const int32_t *row, const double *val,
-                         const int32_t *rb_of_row, int blk, int64_t n_vox, double omega,
-                         const double *res, double *x)
+                         const int32_t *rb_of_row, int blk, int32_t g_lo, int32_t g_hi,
+                         int64_t n_vox, double omega, const double *res, double *x)
 {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= n_vox) return;
     double s = 0.0;
-    for (int64_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) {
-        const int g = row[e];
-        if (rb_of_row[g] == blk) s = __dadd_rn(s, __dmul_rn(val[e], res[g]));
+    if (g_lo >= 0) {
+        const int64_t e1 = col_ptr[c + 1];
+        for (int64_t e = lb_idx(row, col_ptr[c], e1, g_lo); e < e1 && row[e] < g_hi; ++e)
+            s = __dadd_rn(s, __dmul_rn(val[e], res[row[e]]));
+    } else {
+        for (int64_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) {
+            const int g = row[e];
+            if (rb_of_row[g] == blk) s = __dadd_rn(s, __dmul_rn(val[e], res[g]));
+        }
     }
     x[c] = __dadd_rn(x[c], __dmul_rn(omega, s));
 }
@@ -166,16 +185,24 @@ __global__ void ca_dx_k(const int64_t *col_ptr, const int32_t *row, const double
 
 // column action, step 2: r[g] -= sum over the row's entries in block J
 // (column order, from 0.0) of A[g, c] dx[c]  (csc_matvec of A_J)
+// (v_lo >= 0: the block's voxels are the id range [v_lo, v_hi): one run of
+// each row's column-sorted list, by binary search)
 __global__ void ca_res_k(const int64_t *row_ptr, const int32_t *col, const double *val,
-                         const int32_t *cb_of_vox, int blk, int64_t n_meas, const double *dx,
-                         double *r)
+                         const int32_t *cb_of_vox, int blk, int32_t v_lo, int32_t v_hi,
+                         int64_t n_meas, const double *dx, double *r)
 {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_meas) return;
     double s = 0.0;
-    for (int64_t e = row_ptr[g]; e < row_ptr[g + 1]; ++e) {
-        const int c = col[e];
-        if (cb_of_vox[c] == blk) s = __dadd_rn(s, __dmul_rn(val[e], dx[c]));
+    if (v_lo >= 0) {
+        const int64_t e1 = row_ptr[g + 1];
+        for (int64_t e = lb_idx(col, row_ptr[g], e1, v_lo); e < e1 && col[e] < v_hi; ++e)
+            s = __dadd_rn(s, __dmul_rn(val[e], dx[col[e]]));
+    } else {
+        for (int64_t e = row_ptr[g]; e < row_ptr[g + 1]; ++e) {
+            const int c = col[e];
+            if (cb_of_vox[c] == blk) s = __dadd_rn(s, __dmul_rn(val[e], dx[c]));
+        }
     }
     r[g] = __dsub_rn(r[g], s);
 }
@@ -328,19 +355,21 @@ cudaError_t baseline_scale(const BaselineMat &M, int kind, int rule, double *dia
 }
 
 cudaError_t baseline_row_block(const BaselineMat &M, const int32_t *rows, int64_t n_rows, int blk,
-                               const int32_t *rb_of_row, double omega, const double *y,
-                               const double *mdiag, double *res, double *x, cudaStream_t s)
+                               int32_t g_lo, int32_t g_hi, const int32_t *rb_of_row, double omega,
+                               const double *y, const double *mdiag, double *res, double *x,
+                               cudaStream_t s)
 {
     if (n_rows > 0)
         ra_res_k<<<nblk(n_rows, 128), 128, 0, s>>>(M.row_ptr, M.csr_col, M.csr_val, rows, n_rows,
                                                    y, x, mdiag, res);
     ra_upd_k<<<nblk(M.n_vox, 128), 128, 0, s>>>(M.col_ptr, M.csc_row, M.csc_val, rb_of_row, blk,
-                                                M.n_vox, omega, res, x);
+                                                g_lo, g_hi, M.n_vox, omega, res, x);
     return cudaGetLastError();
 }
 
 cudaError_t baseline_col_block(const BaselineMat &M, const int64_t *vox, int64_t n_vox_blk,
-                               int blk, const int32_t *cb_of_vox, double omega,
+                               int blk, int32_t v_lo, int32_t v_hi, const int32_t *cb_of_vox,
+                               double omega,
                                const double *ddiag, double *dx, double *x, double *r,
                                cudaStream_t s)
 {
@@ -348,7 +377,7 @@ cudaError_t baseline_col_block(const BaselineMat &M, const int64_t *vox, int64_t
         ca_dx_k<<<nblk(n_vox_blk, 128), 128, 0, s>>>(M.col_ptr, M.csc_row, M.csc_val, vox,
                                                      n_vox_blk, omega, ddiag, r, x, dx);
     ca_res_k<<<nblk(M.n_meas, 128), 128, 0, s>>>(M.row_ptr, M.csr_col, M.csr_val, cb_of_vox, blk,
-                                                 M.n_meas, dx, r);
+                                                 v_lo, v_hi, M.n_meas, dx, r);
     return cudaGetLastError();
 }
 

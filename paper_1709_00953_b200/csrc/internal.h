@@ -297,13 +297,15 @@ cudaError_t baseline_build(int dtype, const PanelDev *h_panels, int np, const in
                            int64_t n_meas, int64_t n_vox, BaselineMat &M, cudaStream_t s);
 void baseline_free(BaselineMat &M);
 cudaError_t baseline_scale(const BaselineMat &M, int kind, int rule, double *diag, cudaStream_t s);
+// (lo, hi): the block's ids as one range [lo, hi) when they form one, else -1
 cudaError_t baseline_row_block(const BaselineMat &M, const int32_t *rows, int64_t n_rows, int blk,
-                               const int32_t *rb_of_row, double omega, const double *y,
-                               const double *mdiag, double *res, double *x, cudaStream_t s);
-cudaError_t baseline_col_block(const BaselineMat &M, const int64_t *vox, int64_t n_vox_blk,
-                               int blk, const int32_t *cb_of_vox, double omega,
-                               const double *ddiag, double *dx, double *x, double *r,
+                               int32_t g_lo, int32_t g_hi, const int32_t *rb_of_row, double omega,
+                               const double *y, const double *mdiag, double *res, double *x,
                                cudaStream_t s);
+cudaError_t baseline_col_block(const BaselineMat &M, const int64_t *vox, int64_t n_vox_blk,
+                               int blk, int32_t v_lo, int32_t v_hi, const int32_t *cb_of_vox,
+                               double omega, const double *ddiag, double *dx, double *x,
+                               double *r, cudaStream_t s);
 cudaError_t baseline_norms(const BaselineMat &M, const double *y, const double *r, const double *x,
                            const double *x_true, const int32_t *gvox, int64_t x_len, int use_r,
                            double *part, double *out4, cudaStream_t s);
