@@ -181,6 +181,13 @@ int bct_get_counts(bct_ctx *ctx, int64_t *counts);            /* [n_panels] */
 int bct_commit_epoch(bct_ctx *ctx);
 /* r = y - sum_j z^j over all measurements (SolverState.initialize). */
 int bct_reset_residual(bct_ctx *ctx);
+/* Solver start with x0 = 0 (SolverState.initialize + set_x_true of
+ * src/solvers.py:188-230 in one call): y uploaded, x = z = xhat = 0,
+ * counts = 0, r = y, x_true uploaded (NULL: none).  Enqueued on the
+ * context's stream with no host wait when y and x_true are page-locked: the
+ * caller keeps them unchanged until its next synchronising call (an epoch
+ * result, a state read). */
+int bct_begin_solve(bct_ctx *ctx, const double *y, const double *x_true);
 
 /* z^j = A_:j x_J for owned panels (projector.py:756-765, bitwise order). */
 int bct_fill_z_from_image(bct_ctx *ctx);

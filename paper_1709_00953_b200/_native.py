@@ -88,6 +88,7 @@ _SIGS = {
     "bct_get_counts": [_p, _p],
     "bct_commit_epoch": [_p],
     "bct_reset_residual": [_p],
+    "bct_begin_solve": [_p, _p, _p],
     "bct_fill_z_from_image": [_p],
     "bct_projection_sum": [_p, _p],
     "bct_forward": [_p, _p, _p],

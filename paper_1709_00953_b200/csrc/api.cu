@@ -1236,6 +1236,16 @@ __global__ void vox_scatter_k(const double *src, const int32_t *gvox, int64_t n,
     if (i < n) stage[gvox[i]] = src[i];
 }
 
+// r = y (the residual of x = 0, z = 0: y - 0.0 is y exactly) and its FP32 copy
+__global__ void init_r_k(const double *y, int64_t n, double *r, float *r32)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v = y[i];
+    r[i] = v;
+    if (r32) r32[i] = (float)v;
+}
+
 // Image transfers in global voxel order; the permutation runs on the device.
 // A context owning every panel moves the whole image in one copy; a shard
 // moves only its own voxels on the host side (global order untouched elsewhere).
@@ -1519,6 +1529,41 @@ int bct_projection_sum(bct_ctx *c, double *out)
 }
 
 // r = y - sum_j z^j over every measurement (SolverState.initialize warm start)
+int bct_begin_solve(bct_ctx *c, const double *y, const double *x_true)
+{
+    if (!c || !y) return BCT_EINVAL;
+    DEVICE_GUARD(c);
+    // z is zeroed: a (t, ax) form left by earlier batched epochs is dropped
+    CK(cudaMemsetAsync(c->zl_on, 0, 4 * std::max(c->np, 1), c->stream));
+    c->z_lazy = false;
+    if (int r = h2d_staged(c, c->y, y, 8 * c->n_meas)) return r;
+    CK(cudaMemsetAsync(c->x, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
+    CK(cudaMemsetAsync(c->z, 0, 8 * std::max<int64_t>(c->z_len, 1), c->stream));
+    CK(cudaMemsetAsync(c->xhat, 0, 8 * std::max<int64_t>(c->x_len, 1), c->stream));
+    CK(cudaMemsetAsync(c->counts, 0, 4 * std::max(c->np, 1), c->stream));
+    if (c->n_meas > 0)
+        init_r_k<<<(unsigned)((c->n_meas + 255) / 256), 256, 0, c->stream>>>(c->y, c->n_meas, c->r,
+                                                                           c->r32);
+    CK(cudaGetLastError());
+    c->r32_valid = c->r32 != nullptr;
+    if (!x_true) {
+        c->has_x_true = false;
+        return 0;
+    }
+    if (c->np == c->n_panels) {   // one copy + the device permutation, no host wait
+        if (int r = h2d_staged(c, c->d_xstage, x_true, 8 * c->n_vox)) return r;
+        if (c->x_len > 0)
+            vox_gather_k<<<(unsigned)((c->x_len + 255) / 256), 256, 0, c->stream>>>(
+                c->d_xstage, c->d_gvox, c->x_len, c->x_true);
+        CK(cudaGetLastError());
+        c->has_x_true = true;
+        return 0;
+    }
+    int r = xvec_to_dev(c, x_true, c->x_true);
+    if (!r) c->has_x_true = true;
+    return r;
+}
+
 int bct_reset_residual(bct_ctx *c)
 {
     if (!c) return BCT_EINVAL;

@@ -35,7 +35,6 @@ from .executor import pack_loops, submit, wait
 from .metrics import ConvergenceTrace, TraceRow, snr_from_sq
 from .sampling import BlockScheduler, ScriptedScheduler
 from .solvers import SolverState, _loops
-from .validation import as_vector
 
 
 def owned_range(n_panels, world, rank):
@@ -165,16 +164,10 @@ def run_gcsgd_sharded(system, y, params, x_true=None, schedule=None, plan_record
         scheduler = ScriptedScheduler(schedule, group_size=params.group_size)
     else:
         scheduler = BlockScheduler(system.table, params.sampling, group_size=params.group_size)
-    state = SolverState.initialize(system, y)
+    # cold start and x_true in one asynchronous call (uploads overlap planning
+    # epoch 1); the host norms for the trace are taken while epoch 1 runs
+    state, x_true = SolverState.begin(system, y, x_true)
     rng = np.random.default_rng(params.seed)
-    y_norm = float(np.linalg.norm(state.y))
-    xt_norm = None
-    if x_true is not None:
-        x_true = as_vector("x_true", x_true, length=system.n_voxels)
-        xt_norm = float(np.linalg.norm(x_true))
-        system.set_x_true(x_true)
-    else:
-        system.set_x_true(None)
     N.check(N.load().bct_set_divergence_factor(system.ctx, float(params.divergence_factor)),
             system.ctx)
     flags = N.BCT_COMMIT | N.BCT_METRICS
@@ -203,6 +196,8 @@ def run_gcsgd_sharded(system, y, params, x_true=None, schedule=None, plan_record
     if params.epochs >= 1:
         pending = prepare(1)
         launch(pending, 1)
+    y_norm = float(np.linalg.norm(state.y))
+    xt_norm = float(np.linalg.norm(x_true)) if x_true is not None else None
     for epoch in range(1, params.epochs + 1):
         packed, _, theta_now = pending
         if isinstance(packed, Exception):

@@ -66,6 +66,18 @@ class SolverState:
         self.epoch = 0
 
     @classmethod
+    def begin(cls, system, y, x_true=None):
+        """Cold start (x0 = 0) and the reference image in one asynchronous
+        device call (bct_begin_solve): y and x_true are uploaded and r = y
+        without a host wait when they are page-locked; the caller keeps both
+        arrays alive and unchanged until its next synchronising call."""
+        y = as_vector("y", y, length=system.n_measurements)
+        xt = None if x_true is None else as_vector("x_true", x_true, length=system.n_voxels)
+        N.check(N.load().bct_begin_solve(system.ctx, N.ptr(y),
+                                         None if xt is None else N.ptr(xt)), system.ctx)
+        return cls(system, y), xt
+
+    @classmethod
     def initialize(cls, system, y, x0=None):
         # float64 and contiguous (no copy when it already is: the device holds
         # the solver's copy, the host keeps it for the trace's |y| only)
@@ -176,16 +188,18 @@ def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=N
         scheduler = ScriptedScheduler(schedule, group_size=params.group_size)
     else:
         scheduler = BlockScheduler(system.table, params.sampling, group_size=params.group_size)
-    state = SolverState.initialize(system, y, x0=x0)
+    if x0 is None:
+        # one asynchronous call: the uploads overlap planning epoch 1
+        state, x_true = SolverState.begin(system, y, x_true)
+    else:
+        state = SolverState.initialize(system, y, x0=x0)
+        if x_true is not None:
+            x_true = as_vector("x_true", x_true, length=system.n_voxels)
+            system.set_x_true(x_true)
+        else:
+            system.set_x_true(None)
     rng = np.random.default_rng(params.seed)
     trace = ConvergenceTrace()
-    if x_true is not None:
-        x_true = as_vector("x_true", x_true, length=system.n_voxels)
-        if not np.any(x_true):
-            raise ConfigurationError("reference signal is identically zero")
-        system.set_x_true(x_true)
-    else:
-        system.set_x_true(None)
     flags = N.BCT_COMMIT | N.BCT_METRICS
     # divergence guard on the device: epoch 1 records the reference norm, and
     # an epoch submitted before the host saw its predecessor diverge is a
@@ -245,6 +259,12 @@ def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=N
             if plan_record is not None:
                 plan_record[epoch] = plan
         state.epoch = epoch
+        if x_true is not None and xt_norm == 0.0:
+            # the reference's snr_db raises at the first epoch's metrics
+            # (metrics.py:25-27, solvers.py:239)
+            if nxt is not None and not isinstance(nxt[0], Exception):
+                wait(system, nxt[0].task_j.size)
+            raise ConfigurationError("reference signal is identically zero")
         snr = snr_from_sq(xt_norm, res.err_sq) if x_true is not None else math.nan
         gap = snr_from_sq(y_norm, res.resid_sq) if y_norm > 0.0 else math.nan
         row = TraceRow(epoch=epoch, effective_epoch=epoch * params.sampling.alpha, snr_db=snr,
