@@ -109,3 +109,39 @@ def test_schedule_replay_reproduces_recorded_run(cfg1, tmp_path, mode, gs):
     for e in rec:
         assert [(j, [g.tolist() for g in gs_]) for j, gs_ in rec[e]] == \
                [(j, [g.tolist() for g in gs_]) for j, gs_ in rec2[e]]
+
+
+def test_solver_start_inputs_pinned_or_pageable_and_state(cfg1):
+    """bct_begin_solve (run_gcsgd's x0 = 0 start): the same run from
+    page-locked inputs (asynchronous uploads) and from ordinary numpy arrays
+    (staged uploads) is bit for bit the same, and equals the classic start
+    (SolverState.initialize + set_x_true, the x0 path with x0 = 0)."""
+    import torch
+
+    dev, y, xt = cfg1
+    params = p1(epochs=6)
+    x_np, tr_np = run_gcsgd(dev, y.copy(), params, x_true=xt.copy())
+    y_pin = torch.empty(y.size, dtype=torch.float64).pin_memory().numpy()
+    xt_pin = torch.empty(xt.size, dtype=torch.float64).pin_memory().numpy()
+    y_pin[:] = y
+    xt_pin[:] = xt
+    x_pin, tr_pin = run_gcsgd(dev, y_pin, params, x_true=xt_pin)
+    assert np.array_equal(x_np, x_pin)
+    assert [r.snr_db for r in tr_np.rows] == [r.snr_db for r in tr_pin.rows]
+    r_pin = dev.get_r()
+    x_cl, tr_cl = run_gcsgd(dev, y, params, x_true=xt, x0=np.zeros(dev.n_voxels))
+    assert np.array_equal(x_np, x_cl)
+    assert np.array_equal(r_pin, dev.get_r())
+    assert [r.snr_db for r in tr_np.rows] == [r.snr_db for r in tr_cl.rows]
+
+
+def test_zero_reference_raises_at_first_metrics(cfg1):
+    """The reference's snr_db raises 'reference signal is identically zero'
+    at the first epoch's metrics (src/metrics.py:25-27, src/solvers.py:239):
+    a zero x_true raises with epochs >= 1 and not with epochs = 0."""
+    from paper_1709_00953_b200 import ConfigurationError
+    dev, y, xt = cfg1
+    with pytest.raises(ConfigurationError, match="identically zero"):
+        run_gcsgd(dev, y, p1(epochs=3), x_true=np.zeros_like(xt))
+    x0, tr = run_gcsgd(dev, y, p1(epochs=0), x_true=np.zeros_like(xt))
+    assert len(tr.rows) == 0 and not np.any(x0)
