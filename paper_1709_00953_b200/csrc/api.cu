@@ -515,7 +515,7 @@ int finalize(bct_ctx *c)
     DALLOC(c->counts, c->np);
     DALLOC(c->gx, 4 * c->max_cols);
     DALLOC(c->t_ax, 2 * c->max_rows);
-    DALLOC(c->seg_part, 2 * 16 * c->max_seg + 2);   // TS_MAX (epoch.cu) partials per lane
+    DALLOC(c->seg_part, 2 * bct::TASK_PARTS_MAX * c->max_seg + 2);   // partials per lane (epoch.cu)
     // two band buffers when they fit, else one (staging then serializes)
     // phase-1 bands (double-buffered when they fit) + the tile reduction area
     // per-task records: runs of a mask, super tiles, the visit's row blocks

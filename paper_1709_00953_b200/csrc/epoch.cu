@@ -81,8 +81,11 @@ constexpr int P1U = BCT_P1_UNROLL;
 // parts_of(nvec) work units (one per ~PART_VECS vectors, at most TS_MAX), so
 // a CTA's longest slice is not one warp's long latency chain; the partials of
 // a lane sit at spart[(slice * TS_MAX + part) * 32 + lane]
-constexpr int TS_MAX = 16;
-constexpr int PART_VECS = 4;
+constexpr int TS_MAX = bct::TASK_PARTS_MAX;
+#ifndef BCT_PART_VECS
+#define BCT_PART_VECS 4
+#endif
+constexpr int PART_VECS = BCT_PART_VECS;
 constexpr int UCAP = 256;           // slices per prefix round (shared memory)
 constexpr int TS_PARTIAL = 4;       // partial tasks (a few short slices): fixed parts
 __host__ __device__ __forceinline__ int parts_of(int nvec, bool full)

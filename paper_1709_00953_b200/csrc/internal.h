@@ -351,6 +351,12 @@ struct SamplerParams {
 void launch_sampler(const SamplerParams &p, int n_visits, cudaStream_t s, cudaError_t *err);
 
 // phase-1 tile reduction areas in dynamic shared memory (2 x epoch.cu RED_DOUBLES)
+// per-task phase 2a: at most this many work units (parts) per SELL slice; the
+// segment-partial scratch holds that many partials per slot
+#ifndef BCT_TASK_PARTS_MAX
+#define BCT_TASK_PARTS_MAX 16
+#endif
+constexpr int TASK_PARTS_MAX = BCT_TASK_PARTS_MAX;
 constexpr size_t PHASE1_RED_BYTES = 2 * 32 * 256 / 8 * 8;
 std::string cuda_err(cudaError_t e);
 void launch_epoch(const EpochParams &p, int dtype, int grid, int block, size_t smem,

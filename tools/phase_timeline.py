@@ -129,6 +129,16 @@ def main():
         if d.size:
             q = np.percentile(d, [10, 50, 90, 100])
             print(f"  {name:14s} " + " ".join(f"{v:6.2f}" for v in q))
+    if os.environ.get("DUMP_BLOCKS"):
+        # phase-2a units (super-tile staged -> units done) per block, by task
+        u = (tl[:, 3] - x[:, 1])
+        for k in range(min(nt, 4)):
+            print(f"task {k} 2a units by block:", " ".join(f"{v:.1f}" for v in u[k]))
+        if nt > 2:
+            print("2a units: corr task0-task1 %.2f, task1-task2 %.2f" %
+                  (np.corrcoef(u[0], u[1])[0, 1], np.corrcoef(u[1], u[2])[0, 1]))
+            slow = np.argsort(u.mean(axis=0))[-8:]
+            print("slowest blocks (mean over tasks):", slow, u.mean(axis=0)[slow].round(2))
     k = 0
     d2k = tl[k, 3, :] - tl[k, 2, :]
     print("task 0 p2a by block (every 8th):", " ".join(f"{v:.0f}" for v in d2k[::8]))
