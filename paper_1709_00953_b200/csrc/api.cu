@@ -545,19 +545,26 @@ int finalize(bct_ctx *c)
         // entry lies in [F*b/G, F*(b+1)/G) of the panel's F stored entries (a
         // static split, tabled here instead of searched per task)
         const int G = c->grid;
+        // (config 2: 256 entries per slice 0.265 -> 0.2625 ms per epoch kernel; 128 and 384
+        // no better than 0 -- the gain is partly where the cuts fall)
+        const int64_t SC = getenv("BCT_TASK_SLICE_COST") ? atoll(getenv("BCT_TASK_SLICE_COST")) : 256;
         std::vector<int32_t> split((size_t)std::max(c->np, 1) * (G + 1), 0);
         std::vector<int32_t> ss;
         for (int lp = 0; lp < c->np; ++lp) {
             const PanelDev &P = c->h_panels[lp];
             ss.resize((size_t)P.n_slices + 1);
             CK(cudaMemcpy(ss.data(), P.slice_start, 4 * ss.size(), cudaMemcpyDeviceToHost));
-            const int64_t F = ss[P.n_slices];
+            // cost of a slice prefix: its stored entries + SC per slice (a
+            // slice's fixed latency: metadata, its first load round trip)
+            std::vector<int64_t> cost(ss.size());
+            for (size_t q = 0; q < ss.size(); ++q) cost[q] = (int64_t)ss[q] + SC * (int64_t)q;
+            const int64_t F = cost[P.n_slices];
             for (int b = 0; b <= G; ++b) {
-                const int32_t key = (int32_t)(F * b / G);
+                const int64_t key = F * b / G;
                 split[(size_t)lp * (G + 1) + b] =
                     b == G ? P.n_slices
-                           : (int32_t)(std::lower_bound(ss.begin(), ss.begin() + P.n_slices, key) -
-                                       ss.begin());
+                           : (int32_t)(std::lower_bound(cost.begin(), cost.begin() + P.n_slices, key) -
+                                       cost.begin());
             }
         }
         DALLOC(c->cta_split, split.size());
