@@ -327,6 +327,9 @@ __device__ __forceinline__ int task_slice(const PrepView &R, const PanelDev &P, 
 #ifndef BCT_REFRESH_ALL
 #define BCT_REFRESH_ALL 1        // per-task serial refresh of every row: interleaved inverse map
 #endif
+#ifndef BCT_TAIL_U
+#define BCT_TAIL_U 6             // epoch tail: z slots of a measurement loaded in predicated groups of 6 (4, 8: slower; 12 spills)
+#endif
 #ifndef BCT_STREAM_HINT_F64
 #define BCT_STREAM_HINT_F64 1    // f64 values (serial configs): the hint helps
 #endif
@@ -2163,36 +2166,38 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
     if (!serial || do_metrics || sharded) {
         // warps cover 32 consecutive measurements (gtid and nthreads are
         // multiples of 32): the interleaved inverse map is read coalesced
+        // (contiguous CTA shares balanced by z slots measured slower: 1.736 ->
+        // 1.746 ms at config 4, the strided deal spreads long and short lists)
         const int64_t n_pad = (p.n_meas + 31) & ~31ll;
         for (int64_t g = gtid; g < n_pad; g += nthreads) {
             double acc = 0.0;
             const int64_t G = g >> 5;
             const int e0 = __ldg(p.invt_off + G), e1 = __ldg(p.invt_off + G + 1);
+            // the row's y and block, loaded ahead of its slot chain
+            const bool live = g < p.n_meas && !sharded;
+            const double yg = live ? __ldg(p.y + g) : 0.0;
+            const int rbg = live ? __ldg(p.rb_of_row + g) : -1;
             // ascending j (the reference's fold); z was written earlier in this
-            // launch: L2-coherent loads, four in flight; -1 pads a list
-            int e = e0 + (int)(g & 31);
-            for (; e + 96 < e1; e += 128) {
-                int o[4];
-                double v[4];
+            // launch: L2-coherent loads, TU in flight (predicated groups: a
+            // list's last few slots do not pay one round trip each); -1 pads
+            // a list
+            constexpr int TU = BCT_TAIL_U;
+            for (int e = e0 + (int)(g & 31); e < e1; e += 32 * TU) {
+                int o[TU];
+                double v[TU];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) o[u] = __ldg(p.invt + e + 32 * u);
+                for (int u = 0; u < TU; ++u) o[u] = e + 32 * u < e1 ? __ldg(p.invt + e + 32 * u) : -1;
                 zvals(o, v);
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                for (int u = 0; u < TU; ++u)
                     if (o[u] >= 0) acc += v[u];
-            }
-            for (; e < e1; e += 32) {
-                int o[1] = {__ldg(p.invt + e)};
-                double v[1];
-                zvals(o, v);
-                if (o[0] >= 0) acc += v[0];
             }
             if (g >= p.n_meas) continue;
             if (sharded) {
                 p.exchange[g] = acc;
             } else {
-                double d = p.y[g] - acc;
-                int rb = p.rb_of_row[g];
+                double d = yg - acc;
+                int rb = rbg;
                 if (!serial && rb >= 0 && mask_has(p.masks, rb)) {
                     p.r[g] = d;
                     if (p.r32) p.r32[g] = (float)d;
@@ -2201,6 +2206,7 @@ __global__ void __launch_bounds__(BLOCK, 1) epoch_kernel(EpochParams p)
             }
         }
     }
+    if (hdr.batched) TL_MARK2(0, 0);   // profiling: the tail's measurement pass done
     // commit and image norms over all owned voxels at once (panels are
     // contiguous in x / xhat / x_true); the panel of a voxel by binary search
     {

@@ -63,6 +63,11 @@ def main():
                         ("C per block", t[5] - t[4])):
             q = np.percentile(d, [0, 10, 50, 90, 100])
             print(f"{name:12s} min {q[0]:6.1f} p10 {q[1]:6.1f} med {q[2]:6.1f} p90 {q[3]:6.1f} max {q[4]:6.1f}")
+        x2 = buf[nt * 8 * G:2 * nt * 8 * G].reshape(nt, 8, G).astype(np.float64) / 1e3
+        if (x2[0, 0] > 0).all():
+            print("tail: measurement pass per block med %.1f max %.1f us; voxel pass med %.1f max %.1f us"
+                  % (np.median(x2[0, 0] - t[6]), (x2[0, 0] - t[6]).max(),
+                     np.median(t[7] - x2[0, 0]), (t[7] - x2[0, 0]).max()))
         if tl.shape[0] > 1:
             t1 = tl[1]
             allB = t1[4] - t[2]
