@@ -75,14 +75,16 @@ def test_mixed_weights_and_column_draws():
 @pytest.mark.parametrize("alpha,gamma,gs", [(1.0, 1.0, 1), (0.5, 0.67, 3), (0.25, 1.0, 64)])
 def test_variate_bundle_replays_plan(strategy, theta0, step, alpha, gamma, gs):
     """The device sampler's input (one choice + one bulk exponential call per
-    epoch) reproduces epoch_plan exactly, epoch after epoch."""
+    epoch), raced for all visits at once (epoch_plan), reproduces the
+    reference's visit-by-visit draws (epoch_plan_per_visit) exactly, epoch
+    after epoch."""
     tab = _table(seed=2, m=12, n=5)
     cfg = SamplingConfig(strategy=strategy, alpha=alpha, gamma=gamma, theta0=theta0,
                          theta_step=step)
     a, b = BlockScheduler(tab, cfg, gs), BlockScheduler(tab, cfg, gs)
     ra, rb = np.random.default_rng(9), np.random.default_rng(9)
     for ep in range(1, 6):
-        pa = a.epoch_plan(ep, ra)
+        pa = a.epoch_plan_per_visit(ep, ra)
         v = b.epoch_variates(ep, rb)
         pb = b.plan_from_variates(v)
         assert [j for j, _ in pa] == [j for j, _ in pb]
@@ -257,3 +259,40 @@ def test_numpy_sum_is_the_pairwise_order_of_the_device_sampler():
         for _ in range(5):
             a = rng.random(n) * 10.0 ** rng.integers(-6, 6, n)
             assert _np_pairwise(a) == float(np.sum(a))
+
+
+def test_vectorised_plan_matches_per_visit_draws_on_random_tables():
+    """epoch_plan (one variate stream, a stable sort by (visit, E/w)) equals
+    the per-visit loop on random tables with empty columns, zero blocks and
+    tied weights, for every strategy and group size; the RNG ends in the same
+    state."""
+    rs = np.random.default_rng(0)
+    checked = 0
+    for trial in range(120):
+        m, n = int(rs.integers(1, 60)), int(rs.integers(1, 30))
+        vals = rs.random((m, n)) * (rs.random((m, n)) > rs.random() * 0.6)
+        if rs.random() < 0.3:
+            vals[:, rs.integers(0, n)] = 0.0
+        vals[rs.random((m, n)) < 0.05] = 0.5
+        tab = ProbabilityTable(vals, vals.sum(0))
+        if tab.active_cols.size == 0:
+            continue
+        strategy = ["importance", "random", "mixed"][trial % 3]
+        cfg = SamplingConfig(alpha=float(rs.choice([0.1, 0.25, 0.5, 1.0])),
+                             gamma=float(rs.choice([0.5, 1.0])), strategy=strategy,
+                             theta0=0.2, theta_step=0.3)
+        gs = int(rs.integers(1, 9))
+        a, b = BlockScheduler(tab, cfg, gs), BlockScheduler(tab, cfg, gs)
+        ra, rb = np.random.default_rng(trial), np.random.default_rng(trial)
+        for ep in range(1, 5):
+            pa, pb = a.epoch_plan(ep, ra), b.epoch_plan_per_visit(ep, rb)
+            assert [j for j, _ in pa] == [j for j, _ in pb]
+            for (_, ga), (_, gb) in zip(pa, pb):
+                assert len(ga) == len(gb)
+                for x, y in zip(ga, gb):
+                    np.testing.assert_array_equal(x, y)
+            a.advance_epoch()
+            b.advance_epoch()
+        assert ra.random() == rb.random()
+        checked += 1
+    assert checked > 100
