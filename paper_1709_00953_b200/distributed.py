@@ -34,7 +34,7 @@ from .errors import ConfigurationError, DivergenceError
 from .executor import pack_loops, submit, wait
 from .metrics import ConvergenceTrace, TraceRow, snr_from_sq
 from .sampling import BlockScheduler, ScriptedScheduler
-from .solvers import SolverState, _loops
+from .solvers import SolverState, _loops, _without_gc_pauses
 
 
 def owned_range(n_panels, world, rank):
@@ -139,6 +139,7 @@ def sharded_forward(system, x, allreduce=None):
     return t.cpu().numpy()
 
 
+@_without_gc_pauses
 def run_gcsgd_sharded(system, y, params, x_true=None, schedule=None, plan_record=None,
                       runner=None, allreduce=None, callback=None):
     """run_gcsgd with the column blocks sharded over the process group

@@ -11,6 +11,8 @@ Without a callback the host draws epoch e+1 while the device runs epoch e.
 
 from __future__ import annotations
 
+import functools
+import gc
 import logging
 import math
 import time
@@ -174,6 +176,23 @@ def _loops(plan, table, b):
     return [(j, [(ids, group_beta(table, b, j, ids)) for ids in groups]) for j, groups in plan]
 
 
+def _without_gc_pauses(fn):
+    """Run fn with Python's cyclic garbage collector paused (restored after):
+    the pipelined epoch loop submits epoch e+1 before it waits on epoch e, and
+    a collection pause in between leaves the device idle."""
+    @functools.wraps(fn)
+    def run(*args, **kwargs):
+        was = gc.isenabled()
+        gc.disable()
+        try:
+            return fn(*args, **kwargs)
+        finally:
+            if was:
+                gc.enable()
+    return run
+
+
+@_without_gc_pauses
 def run_gcsgd(system, y, params, x_true=None, x0=None, callback=None, schedule=None,
               plan_record=None, device_sampling=False):
     """Grouped solver for ``params.epochs`` epochs (solvers.py:188-269).
