@@ -56,13 +56,13 @@ def main():
     S.submit = sub
     import cProfile
     import pstats
-    for rep in range(4):
+    for rep in range(int(os.environ.get('REPS', '4'))):
         marks.clear()
         prof = cProfile.Profile() if rep == 0 and os.environ.get("PROFILE") else None
         t0 = time.perf_counter()
         if prof:
             prof.enable()
-        run_gcsgd(s, y_h, p, x_true=xt_h)
+        _, tr = run_gcsgd(s, y_h, p, x_true=xt_h)
         if prof:
             prof.disable()
             pstats.Stats(prof).sort_stats("cumulative").print_stats(18)
@@ -71,6 +71,13 @@ def main():
                 for i in range(len(marks) - 1)]
         print(f"run {rep}: {1e3 * (t1 - t0):.2f} ms; first submit {1e3 * (marks[0][1] - t0):.2f} "
               f"ms; {' '.join(gaps[:10])} ...")
+        waits = [m[1] for m in marks if m[0] == "wait"]
+        iv = [1e3 * (b - a) for a, b in zip(waits, waits[1:])]
+        kms = [r.kernel_ms for r in tr.rows]
+        print(f"   kernel sum {sum(kms):.2f} ms (min {min(kms):.3f} max {max(kms):.3f}); "
+              f"wait-to-wait max {max(iv):.2f} ms; last wait -> return {1e3 * (t1 - waits[-1]):.2f} ms")
+        print("   wait-to-wait " + " ".join(f"{v:.2f}" for v in iv))
+        print("   kernel_ms " + " ".join(f"{v:.3f}" for v in kms))
 
 
 if __name__ == "__main__":
