@@ -342,6 +342,11 @@ int build_panel(bct_ctx *c, int lp, int32_t n_rows, int64_t nnz, const double *v
     // forces a shape (profiling).
     struct Shape { int th, tw, nbuf; };
     std::vector<Shape> shapes = {{16, 16, 1}, {8, 8, 2}, {4, 8, 2}, {4, 8, 1}};
+    // FP32 contexts: the batched path stages FP32 bands, two of which fit in
+    // one FP64 band's space, so a shape only has to hold one FP64 band (the
+    // per-task path then runs single-buffered).  Config 5 (1440 views) gets
+    // 8x8 tiles instead of 4x8: phase A 11.8 -> 8.9 ms per epoch.
+    if (c->dtype != 0) shapes = {{16, 16, 1}, {8, 8, 1}, {4, 8, 1}};
     if (const char *e = getenv("BCT_TILE")) {
         int a = 0, b2 = 0;
         if (sscanf(e, "%dx%d", &a, &b2) == 2 && a > 0 && b2 > 0 && (a * b2) % 32 == 0 &&

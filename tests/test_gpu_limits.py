@@ -172,3 +172,38 @@ def test_revisited_blocks_match_oracle(small, name, mode):
     assert rel(st.x, st_o.x) <= 1e-12
     assert rel(st.r, st_o.r) <= 1e-12
     assert rel(np.concatenate(st.z), np.concatenate(st_o.z)) <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# single-buffered phase-1 bands (a shape whose two FP64 bands exceed shared
+# memory: FP32 contexts at config 5's 1440 views take 8x8 tiles this way)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("mode,gs", [("serial_faithful", 2), ("parallel", 3), ("parallel", 6)])
+def test_single_buffered_bands_match_double_buffered(monkeypatch, dtype, mode, gs):
+    """The same 8x8-tile layout with one band buffer (BCT_TILE_NBUF1) and with
+    two gives bitwise the same run on the per-task and batched paths, and the
+    FP64 run matches the oracle."""
+    n, views, bins, m, nc = 32, 48, 46, 6, 4
+    spec = ParallelBeamSpec(n, views, bins, m, nc)
+    xt = random_ellipses(n, 4, 5)
+    ora = OracleSystem.parallel_beam(n, views, bins, m, nc)
+    y, _ = add_noise(ora.forward(xt), 0.01, 6)
+    p = SolverParams(epochs=4, b=0.3, group_size=gs, seed=9, execution_mode=mode,
+                     sampling=SamplingConfig(alpha=0.6))
+    xs = []
+    for nbuf1 in (False, True):
+        monkeypatch.setenv("BCT_TILE", "8x8")
+        if nbuf1:
+            monkeypatch.setenv("BCT_TILE_NBUF1", "1")
+        else:
+            monkeypatch.delenv("BCT_TILE_NBUF1", raising=False)
+        dev = DeviceBlockSystem.parallel_beam(spec, dtype=dtype)
+        x, _ = run_gcsgd(dev, y, p, x_true=xt)
+        xs.append(np.array(x))
+        dev.close()
+    assert np.array_equal(xs[0], xs[1])
+    if dtype == "f64":
+        x_ref, _ = oracle_run_gcsgd(ora, y, 4, 0.3, alpha=0.6, group_size=gs, mode=mode, seed=9)
+        assert rel(xs[1], x_ref) <= 1e-10
