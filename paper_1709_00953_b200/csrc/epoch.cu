@@ -1014,7 +1014,11 @@ struct RingSlot {
     int k, t;
     int q0, q1, qd;     // slices [nsl*q0/qd, nsl*q1/qd) of the tile (0, 1, 1: whole tile)
 };
-constexpr int RING = 4;
+#ifndef BCT_A_META_EARLY
+#define BCT_A_META_EARLY 0       // batched phase A: tile it+2's band metadata loaded before tile it's
+                                 // streams (ring one slot deeper) instead of after them
+#endif
+constexpr int RING = BCT_A_META_EARLY ? 5 : 4;
 static_assert(sizeof(RingSlot) % 8 == 0, "ring slots are copied in 8-byte words");
 
 // fused batched tail (EpochHeader::fuse_tail): tables in the phase buffers
@@ -1160,6 +1164,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
         if (warp == 0) {
             if (n_items > 0) ring_issue(0);
             if (n_items > 1) ring_issue(1);
+            if (BCT_A_META_EARLY && n_items > 2) ring_issue(2);
             cp_async_wait_all();
         }
         __syncthreads();
@@ -1185,7 +1190,15 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             // the other buffer was last read by tile it-1 (before its barrier)
             if (dbuf && it + 1 < n_items)
                 band_issue(ring[(it + 1) % RING].P, bm, rband, buf[cb ^ 1], nullptr);
-            if (warp == 0 && it + 2 < n_items) ring_issue(it + 2);
+            if (BCT_A_META_EARLY) {
+                // slot it+3 was last read in iteration it-2 (a barrier ago); slot
+                // it+2 completed at the end of the last tile
+                if (warp == 0 && it + 3 < n_items) ring_issue(it + 3);
+                if (dbuf && it + 2 < n_items)
+                    band_meta_load(ring[(it + 2) % RING].P, ring[(it + 2) % RING].t, bm, nullptr);
+            } else if (warp == 0 && it + 2 < n_items) {
+                ring_issue(it + 2);
+            }
             const int nsl = S.P.tile_cols >> 5;
             const double wsum = tile_g<V, TB>(S.P, S.t, S.q0 * nsl / S.qd, S.q1 * nsl / S.qd, buf[cb],
                                           p.x + S.P.x_off, gxb + S.gx_off,
@@ -1201,7 +1214,7 @@ __device__ void batched_epoch(const EpochParams &p, const EpochHeader &hdr, doub
             }
             if (!dbuf && it + 1 < n_items)
                 band_issue(ring[(it + 1) % RING].P, bm, rband, buf[0], nullptr);
-            if (it + 2 < n_items)
+            if (it + 2 < n_items && !(BCT_A_META_EARLY && dbuf))
                 band_meta_load(ring[(it + 2) % RING].P, ring[(it + 2) % RING].t, bm, nullptr);
         }
     }
