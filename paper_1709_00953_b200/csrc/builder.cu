@@ -23,7 +23,6 @@
 namespace {
 
 constexpr double REL_EPS = 1e-12;
-constexpr int MAX_STRIP = 128;   // strip height (ix extent) supported by the fill kernel
 
 struct RayTrace {
     double length, t0, t1, t;
@@ -150,7 +149,53 @@ __global__ void pb_count_kernel(int64_t n, int64_t views, int64_t bins, const do
     counts[r] = cnt;
 }
 
+// trace_walk one positive segment at a time (the same arithmetic in the same
+// order); false when the traversal has ended.
+struct TraceIter {
+    int64_t it = 0;
+    bool done = false;
+};
+
+__device__ __forceinline__ bool trace_next(RayTrace &T, TraceIter &I, int64_t &ix, int64_t &iy,
+                                           double &seg_out)
+{
+    while (!I.done && I.it < T.max_steps) {
+        ++I.it;
+        int a = 0;
+        double tm = T.tmax[0];
+        if (T.tmax[1] < tm) { a = 1; tm = T.tmax[1]; }
+        if (T.tmax[2] < tm) { a = 2; tm = T.tmax[2]; }
+        double tn = tm < T.t1 ? tm : T.t1;
+        double seg = (tn - T.t) * T.length;
+        const int64_t cx = T.iv[0], cy = T.iv[1];
+        if (tm >= T.t1) {
+            I.done = true;
+        } else {
+            T.iv[a] += T.step[a];
+            if (T.iv[a] < T.lo[a] || T.iv[a] >= T.hi[a]) {
+                I.done = true;
+            } else {
+                T.tmax[a] += T.tdel[a];
+                T.t = tn;
+            }
+        }
+        if (seg > 0.0) {
+            ix = cx;
+            iy = cy;
+            seg_out = seg;
+            return true;
+        }
+    }
+    return false;
+}
+
 // Writes the sorted row of every hit ray: entries ordered by ix, then iy.
+// Along a ray ix and iy are each monotone, so the sorted slot of an entry
+// follows from its position in the walk: the walk order itself (ix and iy
+// both ascending), its mirror image (both descending), or, when the two run
+// in opposite directions, the walk's ix runs (in order or mirrored) with each
+// run reversed -- a second walker runs one ix run ahead to give the run's
+// length.  No per-column table: any strip width.
 __global__ void pb_fill_kernel(int64_t n, int64_t views, int64_t bins, const double *cosv,
                                const double *sinv, int64_t x0, int64_t x1, const int32_t *l2g,
                                const int32_t *indptr, int64_t n_hit, double *data,
@@ -163,39 +208,41 @@ __global__ void pb_fill_kernel(int64_t n, int64_t views, int64_t bins, const dou
     pb_endpoints(n, bins, cosv[a], sinv[a], k, src, dst);
     double origin[3] = {-0.5 * (double)n, -0.5 * (double)n, -0.5};
     int64_t lo[3] = {x0, 0, 0}, hi[3] = {x1, n, 1};
-    int colcnt[MAX_STRIP];
-    const int w = (int)(x1 - x0);
-    for (int q = 0; q < w; ++q) colcnt[q] = 0;
     RayTrace T;
     if (!trace_init(src, dst, origin, lo, hi, T, dv)) return;
-    RayTrace T2 = T;
-    trace_walk(T, [&](int64_t ix, int64_t, double) { ++colcnt[ix - x0]; });
-    // exclusive prefix -> first slot of every ix column
-    int acc = 0;
-    for (int q = 0; q < w; ++q) {
-        int c = colcnt[q];
-        colcnt[q] = acc;
-        acc += c;
+    const bool xdown = T.step[0] < 0, ydown = T.step[1] < 0;
+    const int base = indptr[lr], len = indptr[lr + 1] - base;
+    int p = 0;
+    if (xdown == ydown) {
+        trace_walk(T, [&](int64_t ix, int64_t iy, double seg) {
+            const int slot = xdown ? len - 1 - p : p;
+            data[base + slot] = seg;
+            cols[base + slot] = (int32_t)((ix - x0) * n + iy);
+            ++p;
+        });
+        return;
     }
-    const bool ydown = T2.step[1] < 0;
-    const int base = indptr[lr];
-    int64_t cur_ix = -1;
-    int run_pos = 0, run_len = 0;
-    // within an ix column the traversal is monotone in iy: place ascending
-    trace_walk(T2, [&](int64_t ix, int64_t iy, double seg) {
-        if (ix != cur_ix) {
-            cur_ix = ix;
-            run_pos = 0;
-            int q = (int)(ix - x0);
-            int next = (q + 1 < w) ? colcnt[q + 1] : acc;
-            run_len = next - colcnt[q];
+    RayTrace S = T;   // scout: one ix run ahead
+    TraceIter si, wi;
+    int64_t six = 0, siy = 0, ix = 0, iy = 0;
+    double sseg = 0.0, seg = 0.0;
+    bool have = trace_next(S, si, six, siy, sseg);
+    while (have) {
+        const int64_t gx = six;
+        int run_len = 0;
+        while (have && six == gx) {
+            ++run_len;
+            have = trace_next(S, si, six, siy, sseg);
         }
-        int q = (int)(ix - x0);
-        int slot = colcnt[q] + (ydown ? (run_len - 1 - run_pos) : run_pos);
-        data[base + slot] = seg;
-        cols[base + slot] = (int32_t)((ix - x0) * n + iy);
-        ++run_pos;
-    });
+        for (int q = 0; q < run_len; ++q) {
+            if (!trace_next(T, wi, ix, iy, seg)) return;
+            const int w = p + (run_len - 1 - q);
+            const int slot = xdown ? len - 1 - w : w;
+            data[base + slot] = seg;
+            cols[base + slot] = (int32_t)((ix - x0) * n + iy);
+        }
+        p += run_len;
+    }
 }
 
 // ---- general scan geometry (fan / cone beam, geometry.py + projector.py) ----
@@ -708,7 +755,6 @@ cudaError_t pb_fill(int64_t n, int64_t views, int64_t bins, const double *d_cos,
                     const int32_t *d_indptr, int64_t n_hit, double *d_data, int32_t *d_cols,
                     cudaStream_t s)
 {
-    if (x1 - x0 > MAX_STRIP) return cudaErrorInvalidValue;
     if (n_hit == 0) return cudaSuccess;
     pb_fill_kernel<<<nblk(n_hit, 64), 64, 0, s>>>(n, views, bins, d_cos, d_sin, x0, x1, d_l2g,
                                                   d_indptr, n_hit, d_data, d_cols);

@@ -207,3 +207,29 @@ def test_single_buffered_bands_match_double_buffered(monkeypatch, dtype, mode, g
     if dtype == "f64":
         x_ref, _ = oracle_run_gcsgd(ora, y, 4, 0.3, alpha=0.6, group_size=gs, mode=mode, seed=9)
         assert rel(xs[1], x_ref) <= 1e-10
+
+
+# ---------------------------------------------------------------------------
+# column blocks wider than 128 pixel columns (the device tracer's fill kernel
+# orders a ray's entries from the walk's directions, without a per-column table)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,views,bins,m,nc", [(160, 24, 230, 3, 1), (300, 16, 430, 2, 2)])
+def test_wide_strip_panels_match_oracle(n, views, bins, m, nc):
+    ora = OracleSystem.parallel_beam(n, views, bins, m, nc)
+    dev = DeviceBlockSystem.parallel_beam(ParallelBeamSpec(n, views, bins, m, nc), dtype="f64")
+    for j in range(nc):
+        p = dev.panel(j)
+        np.testing.assert_array_equal(p.data, ora.data[j])
+        np.testing.assert_array_equal(p.cols, ora.cols[j])
+        np.testing.assert_array_equal(p.indptr, ora.indptr[j])
+        np.testing.assert_array_equal(p.rbp, ora.rbp[j])
+        np.testing.assert_array_equal(p.l2g, ora.l2g[j])
+    xt = random_ellipses(n, 4, 7)
+    y = ora.forward(xt)
+    np.testing.assert_array_equal(dev.forward(xt), y)
+    p = SolverParams(epochs=3, b=0.4, group_size=m, seed=2, execution_mode="parallel")
+    x, _ = run_gcsgd(dev, y, p, x_true=xt)
+    x_ref, _ = oracle_run_gcsgd(ora, y, 3, 0.4, group_size=m, mode="parallel", seed=2)
+    assert rel(x, x_ref) <= 1e-10
+    dev.close()
