@@ -303,6 +303,32 @@ def test_cfg4_free_running_fp64(cfg4):
                                [r["obs_gap_db"] for r in rows], rtol=1e-9)
 
 
+def test_cfg4_fp32_residual_curve(cfg4):
+    """The bench path itself: FP32 storage, batched epochs, the 20 epochs
+    bench.py's end-to-end run makes.  ||y - sum z|| per epoch within 1e-4
+    relative of the FP64 oracle's (north_star), same plans, and the final SNR."""
+    cfg, ora, _, xt, y = cfg4
+    dev32 = DeviceBlockSystem.parallel_beam(cfg.spec, dtype="f32")
+    E = 20
+    rec = {}
+    _, tr = run_gcsgd(dev32, y, cfg_params(cfg, E), x_true=xt, plan_record=rec)
+    rec_o = {}
+    _, rows = oracle_run_gcsgd(ora, y, E, cfg.b, alpha=cfg.alpha, gamma=cfg.gamma,
+                               group_size=cfg.group_size, mode=cfg.mode, seed=1234,
+                               x_true=xt, plan_record=rec_o, workers=WORKERS)
+    for e in rec_o:
+        assert [j for j, _ in rec[e]] == [j for j, _ in rec_o[e]]
+    ynorm = np.linalg.norm(y)
+    r_dev = ynorm / 10.0 ** (np.array([r.obs_gap_db for r in tr.rows]) / 20.0)
+    r_ref = ynorm / 10.0 ** (np.array([r["obs_gap_db"] for r in rows]) / 20.0)
+    dev = np.max(np.abs(r_dev - r_ref) / r_ref)
+    dsnr = abs(tr.rows[-1].snr_db - rows[-1]["snr_db"])
+    print(f"cfg4 fp32 residual-curve max rel dev {dev:.3e}; final SNR differs by {dsnr:.2e} dB")
+    assert dev <= 1e-4
+    assert dsnr <= 1e-4
+    dev32.close()
+
+
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_cfg4_teacher_forced(cfg4, dtype):
     """One config-4 epoch from a shared state (the device FP64 run's epoch-3
