@@ -54,9 +54,9 @@ class ThreadAllReduce:
         self.barrier.wait()
 
 
-def run_shards(spec, y, p, xt, ranges):
+def run_shards(spec, y, p, xt, ranges, dtype="f64"):
     ar = ThreadAllReduce(len(ranges))
-    systems = [DeviceBlockSystem.parallel_beam(spec, dtype="f64", panel_range=pr)
+    systems = [DeviceBlockSystem.parallel_beam(spec, dtype=dtype, panel_range=pr)
                for pr in ranges]
     out = [None] * len(ranges)
 
@@ -133,3 +133,41 @@ def test_sharded_divergence_guard(cfg1):
             v = s.voxel_indices(j)
             x[v] = xl[v]
     assert rel(x, x_full) <= 1e-9
+
+
+@pytest.mark.parametrize("dtype,world,tol", [("f64", 2, 1e-12), ("f32", 2, 1e-6), ("f32", 4, 1e-6)])
+def test_sharded_batched_epochs_at_config3(dtype, world, tol):
+    """The path a multi-GPU bench run takes: config 3's parallel full-panel
+    epochs (the batched epoch kernel with BCT_SHARDED, exchange, finish) over
+    2 and 4 shards against the one-context run of the same dtype.  FP64 folds
+    the shards' projection sums in a different order (1e-12); the FP32 store's
+    (t, ax) pairs are FP32, so a different fold of S moves r at the 1e-7 level."""
+    cfg = CONFIGS[3]
+    spec = cfg.spec
+    from paper_1709_00953_b200 import add_noise, random_ellipses
+    full = DeviceBlockSystem.parallel_beam(spec, dtype=dtype)
+    xt = random_ellipses(spec.n, cfg.n_ellipses, cfg.phantom_seed)
+    y, _ = add_noise(full.forward(xt), cfg.noise_frac, cfg.noise_seed)
+    p = SolverParams(epochs=6, b=cfg.b, group_size=cfg.group_size, seed=1234,
+                     execution_mode=cfg.mode,
+                     sampling=SamplingConfig(alpha=cfg.alpha, gamma=cfg.gamma))
+    x_ref, tr_ref = run_gcsgd(full, y, p, x_true=xt)
+    r_ref = full.get_r()
+    full.close()
+    nc = spec.nc
+    ranges = [(q * nc // world, (q + 1) * nc // world) for q in range(world)]
+    out, systems = run_shards(spec, y, p, xt, ranges, dtype=dtype)
+    for r in out:
+        assert not isinstance(r, Exception), r
+    for x_sh, tr_sh in out:
+        assert rel(x_sh, x_ref) <= tol
+        np.testing.assert_allclose([r.obs_gap_db for r in tr_sh.rows],
+                                   [r.obs_gap_db for r in tr_ref.rows], rtol=max(tol, 1e-11))
+        np.testing.assert_allclose([r.snr_db for r in tr_sh.rows],
+                                   [r.snr_db for r in tr_ref.rows], rtol=max(tol, 1e-11))
+    r0 = systems[0].get_r()
+    for s in systems[1:]:
+        assert np.array_equal(s.get_r(), r0)
+    assert rel(r0, r_ref) <= 10 * tol
+    for s in systems:
+        s.close()
