@@ -248,7 +248,7 @@ def run_ours(args):
     blocks_per_step = sum(int(p.task_gptr[-1]) for p in plans[args.warmup:]) / args.steps
     nnz_total = system.nnz
     if sharded:
-        t = torch.tensor([float(nnz_total)], device=f"cuda:{device}")
+        t = torch.tensor([int(nnz_total)], dtype=torch.int64, device=f"cuda:{device}")
         torch.distributed.all_reduce(t)
         nnz_total = int(t.item())
     # every task is a full panel when alpha=1, gamma=1: nnz per epoch = nnz(A)
