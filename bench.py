@@ -163,6 +163,11 @@ def run_ours(args):
     sharded = world > 1 or os.environ.get("BCT_BENCH_SHARDED") == "1"
     if sharded:
         torch.cuda.set_device(local)
+        if world == 1:   # plain `python bench.py` with BCT_BENCH_SHARDED=1: no launcher env
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.distributed.init_process_group("nccl")
     device = local if world > 1 else 0
     torch.cuda.set_device(device)
